@@ -1,0 +1,239 @@
+"""Generate golden vectors by running the REFERENCE implementation itself.
+
+Run in the build container (the only place /root/reference exists):
+
+    python tests/golden/make_golden.py
+
+It imports the read-only reference package from /root/reference/pkg/src,
+feeds it seeded inputs from `paper_1812_01307_b200.problems` (plus the
+reference's own fan-beam/Morton generator), and writes small compressed
+fixtures next to this script.  The fixtures pin the CPU oracle
+(tests/test_oracle_golden.py, bit-exact) and the CUDA path
+(tests/test_gpu_*.py, within the north-star tolerances).  Nothing at test
+time reads /root/reference.
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import sys
+
+import numpy as np
+from scipy import sparse
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, REPO)
+sys.path.insert(0, "/root/reference/pkg/src")
+
+from bsgdtv import blockops, metrics, sim, solvers, spectral, tv  # noqa: E402
+
+from paper_1812_01307_b200 import problems  # noqa: E402
+
+
+def save(name, **arrays):
+    path = os.path.join(HERE, name + ".npz")
+    np.savez_compressed(path, **arrays)
+    print("wrote", path, os.path.getsize(path), "bytes")
+
+
+def csr_arrays(a):
+    a = sparse.csr_array(a)
+    return {"indptr": a.indptr.astype(np.int64), "indices": a.indices.astype(np.int32),
+            "data": a.data, "shape": np.array(a.shape, dtype=np.int64)}
+
+
+def trace_arrays(trace):
+    return {"samples": np.array([tuple(s) for s in trace.samples], dtype=np.float64).reshape(-1, 4),
+            "flags": np.array([-1 if f is None else int(f) for f in trace.decrease_flags], dtype=np.int64),
+            "csv": np.frombuffer(trace.to_csv_string().encode(), dtype=np.uint8)}
+
+
+# --- partitions -------------------------------------------------------------
+
+def gen_partitions():
+    cases = [(4, 4, 1, 1), (10, 8, 4, 4), (32940, 16384, 4, 4), (2000000, 500000, 8, 8),
+             (523440, 262144, 8, 8), (1050, 576, 4, 5), (7, 7, 7, 7), (13, 5, 3, 2)]
+    out = {}
+    for k, (r, c, m, n) in enumerate(cases):
+        p = blockops.make_partition(r, c, m, n)
+        out[f"case{k}"] = np.array([r, c, m, n], dtype=np.int64)
+        out[f"rows{k}"] = np.array([b for b, _ in p.row_bounds] + [p.rows], dtype=np.int64)
+        out[f"cols{k}"] = np.array([b for b, _ in p.col_bounds] + [p.cols], dtype=np.int64)
+    errors = [(4, 4, 5, 1), (4, 4, 1, 5), (4, 4, 0, 1), (0, 4, 1, 1)]
+    for k, (r, c, m, n) in enumerate(errors):
+        try:
+            blockops.make_partition(r, c, m, n)
+            raise AssertionError("expected ValueError")
+        except ValueError:
+            pass
+        out[f"err{k}"] = np.array([r, c, m, n], dtype=np.int64)
+    save("partitions", **out)
+
+
+# --- TV prox ------------------------------------------------------------------
+
+def gen_prox():
+    rng = np.random.default_rng(123)
+    images = {
+        "rand16": rng.random((16, 16)),
+        "rag7x13": rng.standard_normal((7, 13)),
+        "row1x9": rng.random((1, 9)),
+        "col9x1": rng.random((9, 1)),
+        "const6": np.full((6, 6), 5.0),
+    }
+    pc = np.zeros((8, 8))
+    pc[:, 4:] = 1.0
+    images["pc8"] = pc + 0.1 * rng.standard_normal((8, 8))
+    images["rand32"] = rng.random((32, 32)) * 3.0
+    weights = [0.0, 1e-4, 1e-2, 0.3, 1.0]
+    settings = [(100, 1e-5), (20, 1e-12), (7, 1e-3)]
+    out = {}
+    k = 0
+    for name, img in images.items():
+        for w in weights:
+            for (mi, tol) in settings:
+                grid = tv.ImageGrid.from_matrix(img)
+                res, info = tv.tv_prox(grid, w, tv.ProxSettings(mi, tol), return_info=True)
+                out[f"in{k}"] = img
+                out[f"out{k}"] = res.as_matrix()
+                out[f"par{k}"] = np.array([w, mi, tol])
+                out[f"info{k}"] = np.array([info.iterations, int(info.converged), info.restarts,
+                                            int(info.fell_back)], dtype=np.int64)
+                out[f"dual{k}"] = np.array(info.dual_objectives)
+                out[f"tv{k}"] = np.array([tv.tv_value(grid), tv.tv_value(res)])
+                k += 1
+    # the identity fallback (`tv.py:250-253`) is rare: seeded search for a case
+    srng = np.random.default_rng(5)
+    for _ in range(40000):
+        h, wd = srng.integers(1, 5, 2)
+        img = srng.standard_normal((h, wd)) * 10 ** srng.uniform(-2, 2)
+        w = 10 ** srng.uniform(-3, 3)
+        mi = int(srng.integers(1, 4))
+        res, info = tv.tv_prox(tv.ImageGrid.from_matrix(img), w, tv.ProxSettings(mi, 1e-5),
+                               return_info=True)
+        if info.fell_back:
+            out[f"in{k}"] = img
+            out[f"out{k}"] = res.as_matrix()
+            out[f"par{k}"] = np.array([w, mi, 1e-5])
+            out[f"info{k}"] = np.array([info.iterations, int(info.converged), info.restarts,
+                                        int(info.fell_back)], dtype=np.int64)
+            out[f"dual{k}"] = np.array(info.dual_objectives)
+            out[f"tv{k}"] = np.array([tv.tv_value(tv.ImageGrid.from_matrix(img)), tv.tv_value(res)])
+            k += 1
+            break
+    out["count"] = np.array(k)
+    # hand values (SPEC.md tv examples)
+    out["tv_2x2"] = np.array(tv.tv_value(tv.ImageGrid.from_matrix(np.array([[0.0, 1.0], [1.0, 1.0]]))))
+    out["tv_1x2"] = np.array(tv.tv_value(tv.ImageGrid.from_matrix(np.array([[0.0, 3.0]]))))
+    u = rng.standard_normal((5, 7))
+    pv, ph = rng.standard_normal((5, 7)), rng.standard_normal((5, 7))
+    gv, gh = tv.discrete_gradient(tv.ImageGrid.from_matrix(u))
+    dvg = tv.discrete_divergence(pv, ph).as_matrix()
+    out["adj_u"], out["adj_pv"], out["adj_ph"] = u, pv, ph
+    out["adj_gv"], out["adj_gh"], out["adj_div"] = gv, gh, dvg
+    save("prox", **out)
+
+
+# --- solver runs ----------------------------------------------------------------
+
+def solver_case(name, a, y, x_true, layout, m, n, cfg, sample_every=1, epochs_state=3,
+                rng_seed=7):
+    op = blockops.BlockOperator(a, blockops.make_partition(a.shape[0], a.shape[1], m, n))
+    pr = solvers.Problem(op=op, y=y, x_true=x_true, layout=layout)
+    out = dict(csr_arrays(a))
+    out.update(y=np.asarray(y, dtype=np.float64), x_true=np.asarray(x_true, dtype=np.float64),
+               mn=np.array([m, n], dtype=np.int64))
+    if layout is not None:
+        out.update(perm=layout.perm.astype(np.int64), hw=np.array([layout.height, layout.width]))
+    out["cfg"] = np.frombuffer(json.dumps({
+        "mu": cfg.mu, "lam": cfg.lam, "alpha": cfg.alpha, "gamma": cfg.gamma, "epochs": cfg.epochs,
+        "seed": cfg.seed, "max_inner_iters": cfg.prox.max_inner_iters, "tol": cfg.prox.tol,
+        "monitor_decrease": cfg.monitor_decrease, "enforce_decrease": cfg.enforce_decrease,
+        "max_halvings": cfg.max_halvings, "divergence_limit": cfg.divergence_limit,
+        "sample_every": sample_every}).encode(), dtype=np.uint8)
+    # per-block products on seeded vectors
+    rng = np.random.default_rng(rng_seed)
+    xv = rng.standard_normal(a.shape[1])
+    rv = rng.standard_normal(a.shape[0])
+    out["probe_x"], out["probe_r"] = xv, rv
+    part = op.partition
+    for i in range(m):
+        for j in range(n):
+            out[f"z_{i}_{j}"] = op.block_matvec(i, j, xv[part.col_slice(j)])
+            out[f"gh_{i}_{j}"] = op.block_matvec_transpose(i, j, rv[part.row_slice(i)])
+            out[f"nnz_{i}_{j}"] = np.array(op.block_nnz(i, j))
+    out["matvec"] = op.matvec(xv)
+    out["rmatvec"] = op.rmatvec(rv)
+    # single epochs through bsgd_tv_iteration
+    state = solvers.init_bsgd_state(op, y, cfg)
+    for e in range(epochs_state):
+        solvers.bsgd_tv_iteration(state, op, y, cfg, layout=layout)
+        out[f"ep{e}_x"] = state.x.copy()
+        out[f"ep{e}_r"] = state.r_vec.copy()
+        out[f"ep{e}_g"] = state.g.copy()
+        out[f"ep{e}_scalars"] = np.array([state.f_curr, state.mu_eff, state.epoch,
+                                          -1 if state.last_decrease_ok is None else int(state.last_decrease_ok)])
+    # full run through run_solver (the operator carries the charges made above)
+    out["applied0"] = np.array(op._nnz_applied, dtype=np.int64)
+    try:
+        trace = solvers.run_solver("bsgd", pr, cfg, sample_every=sample_every)
+        out.update(trace_arrays(trace))
+        out["final_x"] = trace.final_x
+        out["diverged"] = np.array(0)
+    except solvers.DivergenceError as exc:
+        out.update(trace_arrays(exc.trace))
+        out["diverged"] = np.array(1)
+        out["message"] = np.frombuffer(str(exc).encode(), dtype=np.uint8)
+    save(name, **out)
+
+
+def gen_solvers():
+    # P1: parallel-beam CT, ragged 4x5 blocking, prox weight large enough to matter
+    d = problems.ct_problem("P1", 24, 30, 35, 6, 0.01, 4, 5.0, 20, 15, np.float64)
+    a = d.matrix
+    op = blockops.BlockOperator(a, blockops.make_partition(a.shape[0], a.shape[1], 4, 5))
+    pw = spectral.largest_eigenvalue(op, max_iters=50)
+    mu = 0.9 / (2.0 * pw.value)
+    layout = tv.PixelLayout.row_major(24, 24)
+    cfg = solvers.SolverConfig(mu=mu, lam=5.0, epochs=15, prox=tv.ProxSettings(20, 1e-5))
+    solver_case("p1_ct", a, d.y, d.x_true, layout, 4, 5, cfg)
+    save("p1_eig", value=np.array(pw.value), converged=np.array(int(pw.converged)),
+         iterations=np.array(pw.iterations))
+
+    # P1 stochastic alpha = gamma = 0.5 (z_cache staleness path)
+    cfg_s = solvers.SolverConfig(mu=mu, lam=5.0, alpha=0.5, gamma=0.5, epochs=6,
+                                 prox=tv.ProxSettings(20, 1e-5))
+    solver_case("p1_stoch", a, d.y, d.x_true, layout, 4, 4, cfg_s)
+
+    # P2: the reference's own fan-beam problem with a Morton layout and enforced decrease
+    sp = sim.make_ct_problem(16, num_angles=12, num_row_blocks=4, num_col_blocks=4)
+    a2 = sp.problem.op.tocsr()
+    op2 = blockops.BlockOperator(a2, blockops.make_partition(a2.shape[0], a2.shape[1], 4, 4))
+    pw2 = spectral.largest_eigenvalue(op2, max_iters=50)
+    cfg2 = solvers.SolverConfig(mu=1.6 / (2.0 * pw2.value), lam=0.1, epochs=8,
+                                prox=tv.ProxSettings(30, 1e-6), enforce_decrease=True)
+    solver_case("p2_morton", a2, sp.problem.y, sp.problem.x_true, sp.problem.layout, 4, 4, cfg2)
+
+    # P3: random least squares (float32 values), ragged 8x8 blocking, monitor on
+    d3 = problems.ls_problem("P3", 2000, 500, 32, 8, 30)
+    a3 = d3.matrix
+    op3 = blockops.BlockOperator(a3, blockops.make_partition(2000, 500, 8, 8))
+    pw3 = spectral.largest_eigenvalue(op3, max_iters=50)
+    mu3 = 0.9 / (2.0 * pw3.value)
+    cfg3 = solvers.SolverConfig(mu=mu3, lam=0.0, epochs=30)
+    solver_case("p3_ls", a3, d3.y, d3.x_true, None, 8, 8, cfg3, sample_every=3)
+    save("p3_eig", value=np.array(pw3.value), converged=np.array(int(pw3.converged)),
+         iterations=np.array(pw3.iterations))
+
+    # P4: divergence (mu beyond the Theorem-1 bound)
+    cfg4 = solvers.SolverConfig(mu=1.3 / (2.0 * pw3.value), lam=0.0, epochs=400,
+                                monitor_decrease=False)
+    solver_case("p4_div", a3, d3.y, d3.x_true, None, 2, 3, cfg4, sample_every=25)
+
+
+if __name__ == "__main__":
+    gen_partitions()
+    gen_prox()
+    gen_solvers()

@@ -1,0 +1,142 @@
+"""Pin the CPU oracle against golden vectors produced by the reference itself.
+
+Every comparison here is bit-exact (np.array_equal): the oracle restates the
+reference's arithmetic order (see oracle/oracle.py and oracle/bsgd_oracle.c).
+"""
+
+import numpy as np
+import pytest
+
+from conftest import golden_cfg, golden_csr, load_golden
+from oracle import oracle as orc
+
+SOLVER_CASES = ["p1_ct", "p2_morton", "p3_ls", "p4_div", "p1_stoch"]
+
+
+def test_partitions_match_reference():
+    z = load_golden("partitions")
+    k = 0
+    while f"case{k}" in z:
+        r, c, m, n = (int(v) for v in z[f"case{k}"])
+        rb, cb = orc.partition_bounds(r, c, m, n)
+        assert np.array_equal(rb, z[f"rows{k}"])
+        assert np.array_equal(cb, z[f"cols{k}"])
+        k += 1
+    k = 0
+    while f"err{k}" in z:
+        with pytest.raises(ValueError):
+            orc.partition_bounds(*(int(v) for v in z[f"err{k}"]))
+        k += 1
+
+
+def test_prox_bit_exact():
+    z = load_golden("prox")
+    for k in range(int(z["count"])):
+        w, mi, tol = z[f"par{k}"]
+        out, rep = orc.tv_prox(z[f"in{k}"], float(w), int(mi), float(tol))
+        assert np.array_equal(out, z[f"out{k}"]), k
+        info = [rep.iterations, int(rep.converged), rep.restarts, int(rep.fell_back)]
+        assert info == list(z[f"info{k}"]), k
+        assert np.array_equal(np.array(rep.dual_objectives), z[f"dual{k}"]), k
+        assert orc.tv_value(z[f"in{k}"]) == z[f"tv{k}"][0]
+        assert orc.tv_value(out) == z[f"tv{k}"][1]
+
+
+def test_tv_hand_values_and_adjointness():
+    z = load_golden("prox")
+    # SPEC.md:131 quotes 2+sqrt(2) for ((0,1),(1,1)); the reference itself returns 2
+    # (that hand value belongs to ((0,1),(1,0))).  We pin the reference.
+    assert float(z["tv_2x2"]) == 2.0 == orc.tv_value(np.array([[0.0, 1.0], [1.0, 1.0]]))
+    assert abs(orc.tv_value(np.array([[0.0, 1.0], [1.0, 0.0]])) - (2 + np.sqrt(2))) < 1e-12
+    assert float(z["tv_1x2"]) == 3.0
+    gv, gh = orc.forward_diff(z["adj_u"])
+    assert np.array_equal(gv, z["adj_gv"]) and np.array_equal(gh, z["adj_gh"])
+    dv = orc.divergence(z["adj_pv"], z["adj_ph"])
+    assert np.array_equal(dv, z["adj_div"])
+    lhs = np.sum(gv * z["adj_pv"]) + np.sum(gh * z["adj_ph"])
+    rhs = -np.sum(z["adj_u"] * dv)
+    assert abs(lhs - rhs) < 1e-12
+
+
+def _operator(z):
+    m, n = (int(v) for v in z["mn"])
+    return orc.OracleOperator(golden_csr(z), m, n, threads=4)
+
+
+@pytest.mark.parametrize("case", SOLVER_CASES)
+def test_block_products_bit_exact(case):
+    z = load_golden(case)
+    op = _operator(z)
+    xv, rv = z["probe_x"], z["probe_r"]
+    for i in range(op.M):
+        for j in range(op.N):
+            r0, r1 = op.row_bounds[i], op.row_bounds[i + 1]
+            c0, c1 = op.col_bounds[j], op.col_bounds[j + 1]
+            assert np.array_equal(op.block_matvec(i, j, xv[c0:c1]), z[f"z_{i}_{j}"])
+            assert np.array_equal(op.block_matvec_transpose(i, j, rv[r0:r1]), z[f"gh_{i}_{j}"])
+            assert op.block_nnz(i, j) == int(z[f"nnz_{i}_{j}"])
+    assert np.array_equal(op.matvec(xv), z["matvec"])
+    assert np.array_equal(op.rmatvec(rv), z["rmatvec"])
+    # every block charged twice (forward + transposed) plus two full products
+    assert op.applied == 4 * op.nnz
+
+
+def _params(cfg):
+    return orc.Params(mu=cfg["mu"], lam=cfg["lam"], alpha=cfg["alpha"], gamma=cfg["gamma"],
+                      epochs=cfg["epochs"], seed=cfg["seed"], max_inner_iters=cfg["max_inner_iters"],
+                      tol=cfg["tol"], monitor_decrease=cfg["monitor_decrease"],
+                      enforce_decrease=cfg["enforce_decrease"], max_halvings=cfg["max_halvings"],
+                      divergence_limit=cfg["divergence_limit"])
+
+
+def _layout(z):
+    if "perm" in z:
+        return z["perm"], tuple(int(v) for v in z["hw"])
+    return None, None
+
+
+@pytest.mark.parametrize("case", SOLVER_CASES)
+def test_epochs_bit_exact(case):
+    z = load_golden(case)
+    op = _operator(z)
+    prm = _params(golden_cfg(z))
+    perm, hw = _layout(z)
+    st = orc.init_state(op, z["y"], prm)
+    for e in range(3):
+        orc.epoch(st, op, z["y"], prm, perm, hw)
+        assert np.array_equal(st.x, z[f"ep{e}_x"]), (case, e)
+        assert np.array_equal(st.r_vec, z[f"ep{e}_r"]), (case, e)
+        assert np.array_equal(st.g, z[f"ep{e}_g"]), (case, e)
+        f, mu, ep, ok = z[f"ep{e}_scalars"]
+        assert st.f_curr == f and st.mu_eff == mu and st.epoch == ep
+        assert (-1 if st.last_decrease_ok is None else int(st.last_decrease_ok)) == ok
+
+
+@pytest.mark.parametrize("case", SOLVER_CASES)
+def test_run_bsgd_bit_exact(case):
+    z = load_golden(case)
+    op = _operator(z)
+    cfg = golden_cfg(z)
+    perm, hw = _layout(z)
+    op.applied = int(z["applied0"])  # the reference ran on an operator with prior charges
+    res = orc.run_bsgd(op, z["y"], _params(cfg), x_true=z["x_true"], perm=perm, hw=hw,
+                       sample_every=cfg["sample_every"])
+    samples = np.array(res.samples, dtype=np.float64).reshape(-1, 4)
+    assert np.array_equal(samples, z["samples"]), case
+    flags = [int(f) for f in res.decrease_flags]
+    assert flags == list(z["flags"])
+    assert res.diverged == bool(int(z["diverged"]))
+    if res.diverged:
+        assert res.message == bytes(z["message"]).decode().split(": ", 1)[-1] or \
+            res.message in bytes(z["message"]).decode()
+    else:
+        assert np.array_equal(res.final_x, z["final_x"])
+
+
+@pytest.mark.parametrize("case,eig", [("p1_ct", "p1_eig"), ("p3_ls", "p3_eig")])
+def test_largest_eigenvalue_bit_exact(case, eig):
+    z = load_golden(case)
+    e = load_golden(eig)
+    op = orc.OracleOperator(golden_csr(z), 4 if case == "p1_ct" else 8, 5 if case == "p1_ct" else 8)
+    val, conv, its = orc.largest_eigenvalue(op, max_iters=50)
+    assert val == float(e["value"]) and int(conv) == int(e["converged"]) and its == int(e["iterations"])
