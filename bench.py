@@ -1,0 +1,353 @@
+#!/usr/bin/env python
+"""BSGD-TV epoch throughput on B200 (BASELINE.json metric, configs[1] workload).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+A step is one BSGD-TV epoch (Algorithm 1, `bsgd_tv_iteration`, alpha = gamma
+= 1, monitor off) over the configs[1] system: A 2,000,000 x 500,000 with 32
+distinct uniform columns per row, float32 values N(0,1)/sqrt(32), M = N = 8
+blocks, lambda = 0, mu = 0.9 / (2 u_max) from 50 power iterations.  Inputs are
+seeded synthetic data of exactly that shape.  A (0.5 GB) and A^T (0.5 GB)
+exceed the 126 MB L2, so every epoch streams from HBM without an explicit
+flush.
+
+Arms:
+  ours       value: K epochs with the state resident in HBM (CUDA-graph replay),
+             device time from CUDA events, max over ranks.
+             e2e: K epochs through the drop-in `bsgd_tv_iteration` with HOST
+             numpy state (x, r uploaded before and downloaded after every epoch).
+             roofline: the dominant SpMV kernel timed alone with CUDA events.
+             cpu_baseline: the CPU oracle port (C + OpenMP, all host threads) on
+             a bounded sample of epochs of the same workload.
+  reference  the CPU oracle port alone (rank 0), printed as the reference arm.
+Multi-GPU (torchrun, N > 1): row-slab ownership, see paper_1812_01307_b200/parallel.py.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "BSGD-TV epochs/s + achieved HBM GB/s (SpMV, TV-prox) at 1/2/4/8 B200"
+WORKLOAD = ("configs[1]: pure BSGD least squares (lambda=0), A 2,000,000 x 500,000, 32 nnz/row, "
+            "float32 values, M=N=8, mu=0.9/(2 u_max)")
+ROWS, COLS, NNZ_ROW, BLOCKS = 2_000_000, 500_000, 32, 8
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def peaks():
+    path = os.path.join(REPO, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def config_dict(extra=None):
+    d = {"workload": WORKLOAD, "rows": ROWS, "cols": COLS, "nnz_per_row": NNZ_ROW, "nnz": ROWS * NNZ_ROW,
+         "blocks": f"{BLOCKS}x{BLOCKS}", "lam": 0.0, "monitor_decrease": False,
+         "matrix_dtype": "f32 values, int32 indices, int64 row pointers", "vector_dtype": "f64",
+         "l2": "no flush needed: A and A^T (1.0 GB) exceed the 126 MB L2 every epoch",
+         "seeds": {"matrix": 2, "x_true": 0, "solver": 0, "power_iteration": 0}}
+    if extra:
+        d.update(extra)
+    return d
+
+
+def make_problem():
+    from paper_1812_01307_b200 import problems
+    t0 = time.time()
+    d = problems.config(1)
+    log(f"[bench] generated configs[1] in {time.time() - t0:.1f}s: {d.matrix.shape}, nnz={d.matrix.nnz}")
+    return d
+
+
+# --- CPU (oracle port) ---------------------------------------------------------
+
+def cpu_epochs(d, steps, warmup, mu=None, budget_s=None):
+    """Time oracle epochs (C restatement + numpy, all host threads). Returns (epochs/s, info)."""
+    from oracle import oracle as orc
+    threads = orc.default_threads()
+    oop = orc.OracleOperator(d.matrix, BLOCKS, BLOCKS, threads=threads)
+    if mu is None:
+        t0 = time.time()
+        u, _, _ = orc.largest_eigenvalue(oop, max_iters=50)
+        mu = 0.9 / (2.0 * u)
+        log(f"[bench] oracle power iteration: u_max={u:.6f} in {time.time() - t0:.1f}s")
+    prm = orc.Params(mu=mu, lam=0.0, epochs=10 ** 9, monitor_decrease=False)
+    st = orc.init_state(oop, d.y, prm)
+    for _ in range(warmup):
+        orc.epoch(st, oop, d.y, prm)
+    times = []
+    t_start = time.perf_counter()
+    for k in range(steps):
+        t0 = time.perf_counter()
+        orc.epoch(st, oop, d.y, prm)
+        times.append(time.perf_counter() - t0)
+        if budget_s is not None and time.perf_counter() - t_start > budget_s:
+            break
+    total = sum(times)
+    return len(times) / total, {"cores": threads, "epochs_timed": len(times), "seconds": total, "mu": mu}
+
+
+# --- clocks ------------------------------------------------------------------------
+
+class Clocks:
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.QUERY}",
+                                          "--format=csv,noheader,nounits", "-lms", "100", "-f", self.path],
+                                         stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if self.proc is None or not self.path or not os.path.exists(self.path):
+            return None
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        with open(self.path) as fh:
+            for line in fh:
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) < 9:
+                    continue
+                try:
+                    sm.append(float(parts[1]))
+                    mx.append(float(parts[2]))
+                except ValueError:
+                    continue
+                for n, v in zip(names, parts[5:9]):
+                    if v.lower() == "active":
+                        reasons.add(n)
+        os.unlink(self.path)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# --- GPU arm ---------------------------------------------------------------------------
+
+def dist_info():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def bytes_model():
+    """Algorithmic bytes per launch of the two SpMV kernels (DESIGN.md §Byte model)."""
+    nnz = ROWS * NNZ_ROW
+    k1 = nnz * (4 + 4) + (ROWS + 1) * 8 + COLS * 8 + 2 * ROWS * 8          # A, rowptr, x once, y in, r out
+    k2 = nnz * (4 + 4) + (COLS + 1) * 8 + ROWS * 8 + 3 * COLS * 8          # A^T, ptr, r once, x in, g + x out
+    return k1, k2
+
+
+def run_ours(args):
+    import torch
+    from paper_1812_01307_b200 import _native as nat
+    from paper_1812_01307_b200 import blockops, solvers, spectral
+
+    world, rank, local = dist_info()
+    if world > 1:
+        from paper_1812_01307_b200 import parallel
+        return parallel.bench_main(args)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    d = make_problem()
+    t0 = time.time()
+    op = blockops.BlockOperator(d.matrix, blockops.make_partition(ROWS, COLS, BLOCKS, BLOCKS))
+    torch.cuda.synchronize()
+    log(f"[bench] plan (upload + device transpose) {time.time() - t0:.2f}s")
+    pw = spectral.largest_eigenvalue(op, max_iters=50)
+    mu = 0.9 / (2.0 * pw.value)
+    log(f"[bench] GPU power iteration u_max={pw.value:.6f} converged={pw.converged}")
+    cfg = solvers.SolverConfig(mu=mu, lam=0.0, epochs=10 ** 9, monitor_decrease=False)
+
+    # ---- value: resident state, graph replay ----
+    st = solvers.init_bsgd_state(op, d.y, cfg)
+    st._ensure_history(args.steps + args.warmup + 16)
+    for _ in range(max(1, args.warmup)):
+        solvers.bsgd_tv_iteration(st, op, d.y, cfg)
+    runner = solvers._GraphRunner(st, cfg, None, st._y, 2)
+    assert runner.capture(False), "CUDA graph capture failed"
+    pairs_needed = args.steps // 2
+    runner.replay()  # warm the graph itself
+    torch.cuda.synchronize()
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        torch.cuda.synchronize()
+        start.record()
+        for _ in range(pairs_needed):
+            runner.replay()
+        if args.steps % 2:
+            solvers.bsgd_tv_iteration(st, op, st._y, cfg)
+        stop.record()
+        torch.cuda.synchronize()
+    ms = start.elapsed_time(stop)
+    ms_per_step = ms / args.steps
+    value = 1000.0 / ms_per_step
+    clocks = clk.summary()
+    log(f"[bench] resident: {ms_per_step:.4f} ms/epoch -> {value:.1f} epochs/s")
+
+    # ---- roofline: the two SpMV kernels timed alone on the same inputs ----
+    rows, cols = op.shape
+    x = st.x_device.clone()
+    r = st.r_device.clone()
+    y = st._y
+    rout = torch.empty_like(r)
+    g = torch.empty_like(x)
+    scratch = torch.empty(nat.SCRATCH_BYTES // 8, dtype=torch.float64, device=dev)
+    s_dev = torch.empty(1, dtype=torch.float64, device=dev)
+    reps = 20
+
+    def time_kernel(fn):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps
+
+    sp = nat.stream_ptr(dev)
+    t_k1 = time_kernel(lambda: nat.call("bsgd_residual", op.plan, nat.ptr(x), nat.ptr(y), nat.ptr(rout), None, None, sp))
+    t_k2 = time_kernel(lambda: nat.call("bsgd_grad", op.plan, nat.ptr(r), nat.ptr(g), sp))
+    b1, b2 = bytes_model()
+    peak, peak_src = peaks()
+    k1_gbs, k2_gbs = b1 / (t_k1 * 1e6), b2 / (t_k2 * 1e6)
+    dominant = ("K1 forward CSR SpMV + residual epilogue", b1, t_k1, k1_gbs) if t_k1 >= t_k2 else \
+               ("K2 transposed CSR SpMV + step epilogue", b2, t_k2, k2_gbs)
+    traffic = None
+    prof = os.path.join(REPO, "profiles", "roofline_traffic.json")
+    if os.path.exists(prof):
+        with open(prof) as fh:
+            traffic = json.load(fh).get("dram_bytes_per_launch")
+    roofline = {"bound": "hbm", "kernel": dominant[0], "achieved": round(dominant[3], 1), "peak": peak,
+                "unit": "GB/s", "frac": round(dominant[3] / peak, 4), "traffic": traffic,
+                "algorithmic_bytes": dominant[1], "launch_ms": round(dominant[2], 5), "peak_source": peak_src,
+                "kernels": {"k1_forward": {"ms": round(t_k1, 5), "bytes": b1, "gbs": round(k1_gbs, 1)},
+                            "k2_transposed": {"ms": round(t_k2, 5), "bytes": b2, "gbs": round(k2_gbs, 1)}},
+                "epoch_gbs": round((b1 + b2) / (ms_per_step * 1e6), 1)}
+    log(f"[bench] K1 {t_k1:.4f} ms {k1_gbs:.0f} GB/s | K2 {t_k2:.4f} ms {k2_gbs:.0f} GB/s (peak {peak})")
+
+    # ---- e2e: host numpy state through the drop-in API ----
+    st2 = solvers.init_bsgd_state(op, d.y, cfg)
+    hx = np.zeros(cols)
+    hr = np.asarray(d.y, dtype=np.float64).copy()
+    e2e_steps = max(2, min(args.steps, 20))
+    for _ in range(2):
+        st2.x, st2.r_vec = hx, hr
+        solvers.bsgd_tv_iteration(st2, op, d.y, cfg)
+        hx, hr = st2.x, st2.r_vec
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        st2.x, st2.r_vec = hx, hr
+        solvers.bsgd_tv_iteration(st2, op, d.y, cfg)
+        hx, hr = st2.x, st2.r_vec
+    torch.cuda.synchronize()
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    e2e = {"value": round(1.0 / e2e_s, 2), "unit": "epochs/s", "h2d_bytes_per_step": (rows + cols) * 8,
+           "d2h_bytes_per_step": (rows + cols) * 8,
+           "how": "bsgd_tv_iteration with numpy x, r_vec set before and read after every epoch"}
+    log(f"[bench] e2e host-state: {e2e_s * 1e3:.3f} ms/epoch")
+
+    # ---- CPU baseline (oracle port) on a bounded sample ----
+    cpu = None
+    if not args.no_cpu:
+        v, info = cpu_epochs(d, steps=max(3, args.cpu_epochs), warmup=1, mu=mu, budget_s=args.cpu_budget)
+        cpu = {"value": round(v, 3), "unit": "epochs/s", "cores": info["cores"], "kind": "port",
+               "sample": f"{info['epochs_timed']} epochs of the same configs[1] system (same A, y, mu), "
+                         f"oracle/ C restatement of scipy csr/csc_matvec + numpy epilogue, OpenMP over block pairs"}
+        log(f"[bench] cpu oracle: {v:.3f} epochs/s on {info['cores']} threads")
+
+    out = {"metric": METRIC, "value": round(value, 2), "unit": "epochs/s", "n_gpus": 1, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": round(ms_per_step, 5), "higher_is_better": True,
+           "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, configs[1] shapes)",
+           "config": config_dict({"parallelism": "single GPU", "mu": mu, "u_max": pw.value}),
+           "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+           "gpu_launches": 3 * args.steps, "clocks": clocks}
+    print(json.dumps(out), flush=True)
+
+
+def run_reference(args):
+    world, rank, _ = dist_info()
+    if rank != 0:
+        return
+    d = make_problem()
+    v, info = cpu_epochs(d, steps=args.steps, warmup=args.warmup, mu=None, budget_s=args.cpu_budget * 4)
+    cpu = {"value": round(v, 3), "unit": "epochs/s", "cores": info["cores"], "kind": "port",
+           "sample": f"{info['epochs_timed']} full epochs of configs[1] (each step one epoch)"}
+    out = {"impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": "epochs/s", "n_gpus": world,
+           "steps": info["epochs_timed"], "warmup": args.warmup, "ms_per_step": round(1000.0 / v, 3),
+           "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic (seeded, configs[1] shapes)",
+           "config": config_dict({"parallelism": f"{info['cores']} host threads", "mu": info["mu"]}),
+           "cpu_baseline": cpu,
+           "e2e": {"value": round(v, 3), "unit": "epochs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-epochs", type=int, default=40)
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        log("[bench] warmup raised to 3 (timing rules)")
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,195 @@
+/*
+ * bsgd_b200 -- C ABI of the B200-native BSGD-TV epoch path.
+ *
+ * Plain C types only (no torch, no C++ in the signatures).  All vector
+ * pointers are DEVICE pointers to float64 arrays owned by the caller unless a
+ * parameter says "host".  Every compute call is asynchronous on `stream` (a
+ * cudaStream_t passed as void*, NULL = legacy default stream) and is safe to
+ * capture into a CUDA graph; none of them synchronises the device.
+ *
+ * Status codes: BSGD_OK, BSGD_EINVAL (the reference raises ValueError),
+ * BSGD_ECUDA / BSGD_ENOMEM (RuntimeError).  bsgd_last_error() returns the
+ * calling thread's last message.  No C++ exception crosses this boundary.
+ *
+ * Each entry point names the reference interface it replaces
+ * (paths relative to /root/reference/pkg/src/bsgdtv/).
+ */
+#ifndef BSGD_B200_H
+#define BSGD_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BSGD_OK 0
+#define BSGD_EINVAL 1
+#define BSGD_ECUDA 2
+#define BSGD_ENOMEM 3
+
+/* value dtype codes = element size in bytes */
+#define BSGD_F32 4
+#define BSGD_F64 8
+
+/* epoch flags */
+#define BSGD_EP_R_NEXT 1u     /* compute r_next = y - A x_k (lookahead r invalid) */
+#define BSGD_EP_LOOKAHEAD 2u  /* compute r_ahead = y - A x_next and f_next = ||r_ahead||^2 */
+#define BSGD_EP_MONITOR 4u    /* Eq. 9 test + f_curr update (solvers.py:316-334) */
+#define BSGD_EP_SKIP_GRAD 8u  /* reuse g already in args->g (step re-try, solvers.py:327-332) */
+#define BSGD_EP_NO_TAIL 16u   /* caller runs bsgd_epoch_tail itself (multi-GPU) */
+
+/* history row layout (doubles), one row per epoch */
+#define BSGD_H_FNEXT 0      /* ||y - A x_next||^2 (NaN if not computed) */
+#define BSGD_H_HOLDS 1      /* 1 / 0, or -1 when the monitor is off */
+#define BSGD_H_XX 2         /* ||x_next||^2 */
+#define BSGD_H_XE 3         /* ||x_next - x_true||^2 (0 without x_true) */
+#define BSGD_H_TV 4         /* TV(image of x_next) when lam > 0, else 0 */
+#define BSGD_H_PITER 5      /* prox iterations */
+#define BSGD_H_PRESTART 6   /* prox restarts */
+#define BSGD_H_PCONV 7      /* prox converged */
+#define BSGD_H_PFELL 8      /* prox fell back to the identity */
+#define BSGD_H_DG 9         /* (x_next - x_k) . g */
+#define BSGD_H_DD 10        /* ||x_next - x_k||^2 */
+#define BSGD_H_FCURR 11     /* f_curr used by the test */
+#define BSGD_HIST_COLS 12
+
+/* device scratch needed by the reducing helpers (residual, dot, sqdist, tv_value) */
+#define BSGD_SCRATCH_BYTES 65536
+
+typedef struct bsgd_plan bsgd_plan;
+
+/* ProxInfo (tv.py:155-163) as written by the device */
+typedef struct bsgd_prox_info {
+    int32_t iterations;
+    int32_t converged;
+    int32_t restarts;
+    int32_t fell_back;
+} bsgd_prox_info;
+
+/* One BSGD-TV epoch (bsgd_tv_iteration, solvers.py:259-341) on a resident plan. */
+typedef struct bsgd_epoch_args {
+    const double *x_k;        /* [cols]  snapshot x_k (solvers.py:276) */
+    const double *r_k;        /* [rows]  snapshot r_k = y - A x_{k-1} (solvers.py:277) */
+    const double *y;          /* [rows] */
+    double *g;                /* [cols]  out: 2 A^T r_k (solvers.py:299-303); in with SKIP_GRAD */
+    double *x_next;           /* [cols]  out: prox(x_k + mu g) (solvers.py:307-314) */
+    double *r_next;           /* [rows]  out with R_NEXT: y - A x_k (solvers.py:297) */
+    double *r_ahead;          /* [rows]  out with LOOKAHEAD: y - A x_next (solvers.py:319-320) */
+    const double *x_true;     /* [cols]  or NULL */
+    const int64_t *perm;      /* [cols]  vector position -> row-major pixel, NULL = identity */
+    double mu;                /* state.mu_eff */
+    double lam;               /* cfg.lam; prox weight = mu * lam */
+    int64_t height, width;    /* image grid, height * width == cols when lam > 0 */
+    int32_t max_inner_iters;  /* ProxSettings.max_inner_iters */
+    double tol;               /* ProxSettings.tol */
+    double *f_curr;           /* device scalar, in/out with MONITOR */
+    double *history;          /* device [history_capacity x BSGD_HIST_COLS] */
+    int64_t *epoch_counter;   /* device scalar: history row index, incremented per epoch */
+    int64_t history_capacity;
+    double *dual_objectives;  /* device [max_inner_iters + 1] or NULL */
+    void *workspace;          /* device, bsgd_epoch_workspace_bytes(), zero-filled once */
+    size_t workspace_bytes;
+    uint32_t flags;
+} bsgd_epoch_args;
+
+/* --- library ----------------------------------------------------------- */
+const char *bsgd_last_error(void);
+int bsgd_version(void);
+int bsgd_device_count(int *out);
+
+/* --- BlockOperator (blockops.py:112-261) ------------------------------ */
+/* __init__ (blockops.py:123-152): canonical CSR (sorted, summed; host
+ * arrays) + partition bounds.  Uploads A and builds A^T on the device. */
+int bsgd_plan_create(bsgd_plan **out, int device, int64_t rows, int64_t cols, int64_t nnz,
+                     const int64_t *indptr, const int32_t *indices, const void *values,
+                     int value_dtype, int64_t num_row_blocks, int64_t num_col_blocks,
+                     const int64_t *row_bounds, const int64_t *col_bounds, void *stream);
+int bsgd_plan_destroy(bsgd_plan *plan);
+/* shape / nnz / dtype / device bytes (blockops.py:156-162) */
+int bsgd_plan_info(const bsgd_plan *plan, int64_t *rows, int64_t *cols, int64_t *nnz,
+                   int *value_dtype, int64_t *device_bytes);
+/* block_nnz (blockops.py:179-180), host out */
+int bsgd_plan_block_nnz(const bsgd_plan *plan, int64_t i, int64_t j, int64_t *out);
+/* block (blockops.py:176-177): block-local CSR copied to HOST buffers sized
+ * (|I_i| + 1, block_nnz, block_nnz); values in the plan dtype. Synchronous. */
+int bsgd_plan_block_copy(const bsgd_plan *plan, int64_t i, int64_t j, int64_t *indptr_out,
+                         int32_t *indices_out, void *values_out, void *stream);
+/* transposed pattern check: A^T rows (= A columns) [c0,c1) copied to HOST */
+int bsgd_plan_transpose_copy(const bsgd_plan *plan, int64_t *indptr_out, int32_t *indices_out,
+                             void *values_out, void *stream);
+
+/* block_matvec (blockops.py:207-214): out[|I_i|] = A_ij x_j[|J_j|] */
+int bsgd_block_matvec(const bsgd_plan *plan, int64_t i, int64_t j, const double *x_j, double *out,
+                      void *stream);
+/* block_matvec_transpose (blockops.py:216-223): out[|J_j|] = A_ij^T r_i[|I_i|] */
+int bsgd_block_matvec_transpose(const bsgd_plan *plan, int64_t i, int64_t j, const double *r_i,
+                                double *out, void *stream);
+/* matvec / rmatvec (blockops.py:225-261) */
+int bsgd_matvec(const bsgd_plan *plan, const double *x, double *out, void *stream);
+int bsgd_rmatvec(const bsgd_plan *plan, const double *w, double *out, void *stream);
+/* y - A x and ||y - A x||^2 (metrics.py:32-33, solvers.py:319-320); sumsq_out device scalar */
+int bsgd_residual(const bsgd_plan *plan, const double *x, const double *y, double *r_out,
+                  double *sumsq_out, void *scratch, void *stream);
+
+/* assemble_residual (blockops.py:264-278): out = y - z[0] - ... - z[N-1] */
+int bsgd_assemble_residual(int64_t rows, int64_t num_col_blocks, const double *y,
+                           const double *z_cache, double *out, void *stream);
+
+/* --- stochastic pair path (solvers.py:274-303 with alpha/gamma < 1) ---- */
+/* z_cache[j, I_i] = A_ij x_k[J_j] for the selected pairs; g[J_j] = 2 sum_i A_ij^T r_k[I_i]
+ * over selected i (zero for unselected column blocks); r_next = y - sum_j z_cache[j].
+ * row_sel / col_sel: host arrays of selected block indices. */
+int bsgd_pair_products(const bsgd_plan *plan, int64_t n_rows_sel, const int64_t *row_sel,
+                       int64_t n_cols_sel, const int64_t *col_sel, const double *x_k,
+                       const double *r_k, const double *y, double *z_cache, double *g,
+                       double *r_next, void *stream);
+
+/* --- total variation (tv.py) ------------------------------------------- */
+size_t bsgd_tv_prox_workspace_bytes(int64_t height, int64_t width);
+/* tv_prox (tv.py:172-255): out = argmin ||t - img||^2 + 2 w TV(t).  info_out
+ * (device) and dual_objectives (device [max_inner_iters + 1]) may be NULL. */
+int bsgd_tv_prox(int64_t height, int64_t width, const double *img, double *out, double weight,
+                 int32_t max_inner_iters, double tol, void *workspace, size_t workspace_bytes,
+                 bsgd_prox_info *info_out, double *dual_objectives, void *stream);
+/* tv_value (tv.py:149-152): device scalar out */
+int bsgd_tv_value(int64_t height, int64_t width, const double *img, double *out, void *scratch,
+                  void *stream);
+/* discrete_gradient / discrete_divergence (tv.py:115-146) */
+int bsgd_discrete_gradient(int64_t height, int64_t width, const double *img, double *dv, double *dh,
+                           void *stream);
+int bsgd_discrete_divergence(int64_t height, int64_t width, const double *pv, const double *ph,
+                             double *out, void *stream);
+
+/* --- reductions (metrics.py, solvers.py:198-215, :517-518) ------------ */
+/* out = sum_k a[k] * b[k]  (deterministic order); device scalar */
+int bsgd_dot(int64_t n, const double *a, const double *b, double *out, void *scratch, void *stream);
+/* out = sum_k (a[k] - b[k])^2; device scalar */
+int bsgd_sqdist(int64_t n, const double *a, const double *b, double *out, void *scratch, void *stream);
+
+/* --- the fused epoch ----------------------------------------------------- */
+size_t bsgd_epoch_workspace_bytes(const bsgd_plan *plan, int64_t height, int64_t width);
+/* bsgd_tv_iteration (solvers.py:259-341), alpha = gamma = 1 */
+int bsgd_epoch(const bsgd_plan *plan, const bsgd_epoch_args *args, void *stream);
+/* multi-GPU pieces of the same epoch (row-slab ownership):
+ *   bsgd_grad:  g = 2 A_local^T r_local  (partial over this rank's rows)
+ *   bsgd_step:  x_next = prox(x_k + mu g) with fused statistics (replicated)
+ *   bsgd_epoch_forward: r_ahead/r_next over local rows + partial ||r||^2
+ *   bsgd_epoch_tail: history row from the (all-reduced) scalars */
+int bsgd_grad(const bsgd_plan *plan, const double *r, double *g, void *stream);
+int bsgd_step(int64_t cols, const bsgd_epoch_args *args, void *stream);
+int bsgd_epoch_forward(const bsgd_plan *plan, const double *x, const double *y, double *r_out,
+                       const bsgd_epoch_args *args, void *stream);
+/* scalars_out (device, 2 doubles): [0] = sum of the forward partials, [1] unused */
+int bsgd_epoch_reduce_forward(const bsgd_plan *plan, const bsgd_epoch_args *args,
+                              double *scalars_out, void *stream);
+/* finish: f_next from fnext_dev (device scalar, may be NULL when no lookahead) */
+int bsgd_epoch_tail(const bsgd_plan *plan, const bsgd_epoch_args *args, const double *fnext_dev,
+                    void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BSGD_B200_H */

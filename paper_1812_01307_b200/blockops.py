@@ -1,0 +1,371 @@
+"""Block-partitioned sparse operator resident on a B200 (drop-in for `bsgdtv.blockops`).
+
+Same public surface as the reference (`pkg/src/bsgdtv/blockops.py:22-278`):
+`BlockPartition`, `make_partition`, `BlockOperator` and `assemble_residual`,
+with the same validation and error types.  The difference is where the
+arithmetic runs: construction uploads the canonical CSR once and builds the
+transposed CSR on the device (`bsgd_plan_create`), and every product is an
+sm_100a kernel.  Products accept numpy arrays (returned as numpy, like the
+reference) or CUDA torch tensors (returned as CUDA tensors, no host copy).
+
+The matvec-unit tally is kept exactly as the reference does: an integer
+nonzero count under a lock, divided on read (`blockops.py:150-152,195-203`).
+"""
+
+from __future__ import annotations
+
+import threading
+from dataclasses import dataclass
+
+import numpy as np
+from scipy import sparse
+
+from . import _native as nat
+
+
+@dataclass(frozen=True)
+class BlockPartition:
+    """Contiguous half-open row / column ranges (`blockops.py:22-81`)."""
+
+    row_bounds: tuple
+    col_bounds: tuple
+
+    def __post_init__(self) -> None:
+        object.__setattr__(self, "row_bounds", tuple((int(a), int(b)) for a, b in self.row_bounds))
+        object.__setattr__(self, "col_bounds", tuple((int(a), int(b)) for a, b in self.col_bounds))
+        for name, bounds in (("row", self.row_bounds), ("col", self.col_bounds)):
+            if len(bounds) == 0:
+                raise ValueError(f"empty {name} partition")
+            if bounds[0][0] != 0:
+                raise ValueError(f"{name} ranges must start at 0")
+            for (_, b), (c, _) in zip(bounds, bounds[1:]):
+                if b != c:
+                    raise ValueError(f"{name} ranges must be contiguous")
+            for a, b in bounds:
+                if b <= a:
+                    raise ValueError(f"{name} ranges must be nonempty")
+
+    @property
+    def num_row_blocks(self) -> int:
+        return len(self.row_bounds)
+
+    @property
+    def num_col_blocks(self) -> int:
+        return len(self.col_bounds)
+
+    @property
+    def rows(self) -> int:
+        return self.row_bounds[-1][1]
+
+    @property
+    def cols(self) -> int:
+        return self.col_bounds[-1][1]
+
+    def row_range(self, i: int):
+        return self.row_bounds[i]
+
+    def col_range(self, j: int):
+        return self.col_bounds[j]
+
+    def row_slice(self, i: int) -> slice:
+        a, b = self.row_bounds[i]
+        return slice(a, b)
+
+    def col_slice(self, j: int) -> slice:
+        a, b = self.col_bounds[j]
+        return slice(a, b)
+
+    def row_sizes(self):
+        return tuple(b - a for a, b in self.row_bounds)
+
+    def col_sizes(self):
+        return tuple(b - a for a, b in self.col_bounds)
+
+    def row_edges(self) -> np.ndarray:
+        return np.array([a for a, _ in self.row_bounds] + [self.rows], dtype=np.int64)
+
+    def col_edges(self) -> np.ndarray:
+        return np.array([a for a, _ in self.col_bounds] + [self.cols], dtype=np.int64)
+
+
+def _split_even(total: int, parts: int):
+    """Near-equal contiguous ranges; the first `total % parts` ranges get one extra."""
+    base, extra = divmod(total, parts)
+    out, start = [], 0
+    for k in range(parts):
+        stop = start + base + (1 if k < extra else 0)
+        out.append((start, stop))
+        start = stop
+    return tuple(out)
+
+
+def make_partition(rows: int, cols: int, num_row_blocks: int, num_col_blocks: int) -> BlockPartition:
+    """M x N near-equal blocking (`blockops.py:96-109`), ValueError on M > r or N > c."""
+    if rows < 1 or cols < 1:
+        raise ValueError("matrix dimensions must be positive")
+    if not 1 <= num_row_blocks <= rows:
+        raise ValueError(f"row block count {num_row_blocks} not in [1, {rows}]")
+    if not 1 <= num_col_blocks <= cols:
+        raise ValueError(f"col block count {num_col_blocks} not in [1, {cols}]")
+    return BlockPartition(_split_even(rows, num_row_blocks), _split_even(cols, num_col_blocks))
+
+
+def _canonical_csr(matrix, dtype=None) -> sparse.csr_array:
+    """float CSR with summed duplicates and sorted indices (`blockops.py:124-126`).
+
+    float32 input stays float32 (exactly representable in the reference's
+    float64); anything else becomes float64 unless ``dtype`` says otherwise.
+    """
+    csr = sparse.csr_array(matrix)
+    want = np.dtype(dtype) if dtype is not None else (
+        np.dtype(np.float32) if csr.dtype == np.float32 else np.dtype(np.float64))
+    if want not in (np.float32, np.float64):
+        raise ValueError("BlockOperator values must be float32 or float64")
+    if csr.dtype != want:
+        csr = csr.astype(want)
+    csr.sum_duplicates()
+    csr.sort_indices()
+    return csr
+
+
+class _Scratch:
+    """Per-device reduction scratch (BSGD_SCRATCH_BYTES) and device scalars."""
+
+    def __init__(self, device):
+        t = nat.torch()
+        self.buf = t.zeros(nat.SCRATCH_BYTES // 8, dtype=t.float64, device=device)
+        self.scalars = t.zeros(8, dtype=t.float64, device=device)
+
+
+class BlockOperator:
+    """Sparse matrix with a block partition, resident on one CUDA device.
+
+    ``device`` selects the GPU (default: the current torch device).  The host
+    canonical CSR is kept (as the reference keeps its copy) for `tocsr`,
+    `to_dense` and `repartition`.
+    """
+
+    def __init__(self, matrix, partition: BlockPartition | None = None, *, device=None, dtype=None):
+        csr = _canonical_csr(matrix, dtype)
+        if csr.nnz == 0:
+            raise ValueError("matrix has no nonzeros")
+        rows, cols = csr.shape
+        if partition is None:
+            partition = make_partition(rows, cols, 1, 1)
+        if partition.rows != rows or partition.cols != cols:
+            raise ValueError(
+                f"partition covers {partition.rows}x{partition.cols}, matrix is {rows}x{cols}")
+        self._csr = csr
+        self._partition = partition
+        self._device = nat.require_cuda(device)
+        self._nnz_total = int(csr.nnz)
+        self._nnz_applied = 0
+        self._lock = threading.Lock()
+        self._scratch = None
+        indptr = np.ascontiguousarray(csr.indptr, dtype=np.int64)
+        indices = np.ascontiguousarray(csr.indices, dtype=np.int32)
+        values = np.ascontiguousarray(csr.data)
+        rb = partition.row_edges()
+        cb = partition.col_edges()
+        handle = nat.c_p()
+        t = nat.torch()
+        with t.cuda.device(self._device):
+            nat.call("bsgd_plan_create", nat.ctypes.byref(handle), self._device.index, rows, cols, csr.nnz,
+                     indptr.ctypes.data, indices.ctypes.data, values.ctypes.data, values.dtype.itemsize,
+                     partition.num_row_blocks, partition.num_col_blocks, rb.ctypes.data, cb.ctypes.data,
+                     nat.stream_ptr(self._device))
+        self._plan = handle
+        nb = partition.num_row_blocks * partition.num_col_blocks
+        counts = np.zeros(nb, dtype=np.int64)
+        for i in range(partition.num_row_blocks):
+            for j in range(partition.num_col_blocks):
+                out = nat.c_i64()
+                nat.call("bsgd_plan_block_nnz", self._plan, i, j, nat.ctypes.byref(out))
+                counts[i * partition.num_col_blocks + j] = out.value
+        if int(counts.sum()) != self._nnz_total:
+            raise AssertionError("blocks must partition the nonzeros")
+        self._block_nnz = counts.reshape(partition.num_row_blocks, partition.num_col_blocks)
+
+    def __del__(self):
+        plan = getattr(self, "_plan", None)
+        if plan is not None and nat._lib is not None:
+            try:
+                nat.load().bsgd_plan_destroy(plan)
+            except Exception:
+                pass
+            self._plan = None
+
+    # --- static structure ------------------------------------------------
+
+    @property
+    def shape(self):
+        return self._csr.shape
+
+    @property
+    def nnz(self) -> int:
+        return self._nnz_total
+
+    @property
+    def partition(self) -> BlockPartition:
+        return self._partition
+
+    @property
+    def num_row_blocks(self) -> int:
+        return self._partition.num_row_blocks
+
+    @property
+    def num_col_blocks(self) -> int:
+        return self._partition.num_col_blocks
+
+    @property
+    def device(self):
+        return self._device
+
+    @property
+    def value_dtype(self):
+        return self._csr.dtype
+
+    @property
+    def plan(self):
+        """Opaque `bsgd_plan*` handle for the C ABI."""
+        return self._plan
+
+    def block(self, i: int, j: int) -> sparse.csr_array:
+        """Block (i, j) with block-local indices, read back from the device copy."""
+        if not (0 <= i < self.num_row_blocks and 0 <= j < self.num_col_blocks):
+            raise IndexError(f"block ({i}, {j}) outside the grid")
+        r0, r1 = self._partition.row_range(i)
+        c0, c1 = self._partition.col_range(j)
+        nz = int(self._block_nnz[i, j])
+        indptr = np.zeros(r1 - r0 + 1, dtype=np.int64)
+        indices = np.zeros(max(nz, 1), dtype=np.int32)
+        values = np.zeros(max(nz, 1), dtype=self._csr.dtype)
+        nat.call("bsgd_plan_block_copy", self._plan, i, j, indptr.ctypes.data, indices.ctypes.data,
+                 values.ctypes.data, nat.stream_ptr(self._device))
+        return sparse.csr_array((values[:nz], indices[:nz], indptr), shape=(r1 - r0, c1 - c0))
+
+    def transpose_pattern(self):
+        """(indptr, indices, values) of the device-built A^T CSR (pattern checks)."""
+        rows, cols = self.shape
+        indptr = np.zeros(cols + 1, dtype=np.int64)
+        indices = np.zeros(self.nnz, dtype=np.int32)
+        values = np.zeros(self.nnz, dtype=self._csr.dtype)
+        nat.call("bsgd_plan_transpose_copy", self._plan, indptr.ctypes.data, indices.ctypes.data,
+                 values.ctypes.data, nat.stream_ptr(self._device))
+        return indptr, indices, values
+
+    def block_nnz(self, i: int, j: int) -> int:
+        return int(self._block_nnz[i, j])
+
+    def to_dense(self) -> np.ndarray:
+        return self._csr.astype(np.float64).toarray()
+
+    def tocsr(self) -> sparse.csr_array:
+        return self._csr
+
+    def repartition(self, num_row_blocks: int, num_col_blocks: int) -> "BlockOperator":
+        rows, cols = self.shape
+        return BlockOperator(self._csr, make_partition(rows, cols, num_row_blocks, num_col_blocks),
+                             device=self._device)
+
+    # --- counter ---------------------------------------------------------
+
+    @property
+    def matvec_units(self) -> float:
+        with self._lock:
+            applied = self._nnz_applied
+        return applied / self._nnz_total
+
+    def _charge(self, nnz: int) -> None:
+        with self._lock:
+            self._nnz_applied += int(nnz)
+
+    # --- device helpers ------------------------------------------------------
+
+    def _scr(self) -> _Scratch:
+        if self._scratch is None:
+            self._scratch = _Scratch(self._device)
+        return self._scratch
+
+    def _vec(self, v, length):
+        return nat.as_f64(v, self._device, length)
+
+    def _out(self, t, like):
+        return t if isinstance(like, nat.torch().Tensor) else t.cpu().numpy()
+
+    # --- products ----------------------------------------------------------
+
+    def block_matvec(self, i: int, j: int, x_j):
+        """A_{I_i}^{J_j} @ x_j (`blockops.py:207-214`); charges nnz(block)."""
+        r0, r1 = self._partition.row_range(i)
+        c0, c1 = self._partition.col_range(j)
+        xv = self._vec(x_j, c1 - c0)
+        out = nat.torch().empty(r1 - r0, dtype=nat.torch().float64, device=self._device)
+        self._charge(self._block_nnz[i, j])
+        nat.call("bsgd_block_matvec", self._plan, i, j, nat.ptr(xv), nat.ptr(out), nat.stream_ptr(self._device))
+        return self._out(out, x_j)
+
+    def block_matvec_transpose(self, i: int, j: int, r_i):
+        """(A_{I_i}^{J_j})^T @ r_i, no factor 2 (`blockops.py:216-223`)."""
+        r0, r1 = self._partition.row_range(i)
+        c0, c1 = self._partition.col_range(j)
+        rv = self._vec(r_i, r1 - r0)
+        out = nat.torch().empty(c1 - c0, dtype=nat.torch().float64, device=self._device)
+        self._charge(self._block_nnz[i, j])
+        nat.call("bsgd_block_matvec_transpose", self._plan, i, j, nat.ptr(rv), nat.ptr(out),
+                 nat.stream_ptr(self._device))
+        return self._out(out, r_i)
+
+    def matvec(self, x, charge: bool = True):
+        """A @ x (`blockops.py:225-244`); charges one unit unless ``charge`` is False."""
+        rows, cols = self.shape
+        xv = self._vec(x, cols)
+        if charge:
+            self._charge(self._nnz_total)
+        out = nat.torch().empty(rows, dtype=nat.torch().float64, device=self._device)
+        nat.call("bsgd_matvec", self._plan, nat.ptr(xv), nat.ptr(out), nat.stream_ptr(self._device))
+        return self._out(out, x)
+
+    def rmatvec(self, w, charge: bool = True):
+        """A^T @ w (`blockops.py:246-261`)."""
+        rows, cols = self.shape
+        wv = self._vec(w, rows)
+        if charge:
+            self._charge(self._nnz_total)
+        out = nat.torch().empty(cols, dtype=nat.torch().float64, device=self._device)
+        nat.call("bsgd_rmatvec", self._plan, nat.ptr(wv), nat.ptr(out), nat.stream_ptr(self._device))
+        return self._out(out, w)
+
+    def residual_sumsq(self, x, y, charge: bool = False):
+        """(y - A x, ||y - A x||^2) on the device; the squared norm stays a device scalar."""
+        rows, cols = self.shape
+        xv = self._vec(x, cols)
+        yv = self._vec(y, rows)
+        if charge:
+            self._charge(self._nnz_total)
+        t = nat.torch()
+        r = t.empty(rows, dtype=t.float64, device=self._device)
+        s = t.empty(1, dtype=t.float64, device=self._device)
+        nat.call("bsgd_residual", self._plan, nat.ptr(xv), nat.ptr(yv), nat.ptr(r), nat.ptr(s),
+                 nat.ptr(self._scr().buf), nat.stream_ptr(self._device))
+        return r, s
+
+
+def assemble_residual(y, z_cache):
+    """r = y - z^0 - z^1 - ... (ascending j, `blockops.py:264-278`) on the device."""
+    t = nat.torch()
+    is_t = isinstance(y, t.Tensor)
+    dev = y.device if is_t and y.is_cuda else nat.require_cuda()
+    yv = nat.as_f64(y, dev)
+    if yv.ndim != 1:
+        raise ValueError("y must be a vector")
+    if isinstance(z_cache, t.Tensor):
+        zc = z_cache.to(device=dev, dtype=t.float64).contiguous()
+    else:
+        zc = t.from_numpy(np.ascontiguousarray(np.asarray(z_cache, dtype=np.float64))).to(dev)
+    if zc.ndim != 2 or zc.shape[1] != yv.shape[0]:
+        raise ValueError(f"z cache shape {tuple(zc.shape)} does not match y of length {yv.shape[0]}")
+    out = t.empty_like(yv)
+    nat.call("bsgd_assemble_residual", yv.shape[0], zc.shape[0], nat.ptr(yv), nat.ptr(zc), nat.ptr(out),
+             nat.stream_ptr(dev))
+    return out if is_t else out.cpu().numpy()

@@ -1,0 +1,1034 @@
+// C ABI of the B200-native BSGD-TV epoch path (declared in include/bsgd_b200.h).
+//
+// Owns the resident matrix (A as CSR and A^T as CSR, built on the device at
+// plan creation), launches the SpMV / TV-prox kernels, and keeps every
+// compute entry point stream-ordered and graph-capturable.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <type_traits>
+#include <unordered_map>
+#include <vector>
+
+#include <cub/device/device_radix_sort.cuh>
+
+#include "../../include/bsgd_b200.h"
+#include "common.cuh"
+#include "fgp.cuh"
+#include "spmv.cuh"
+
+using namespace bsgd;
+
+#define BSGD_VERSION 100
+
+// ---------------------------------------------------------------------------
+// errors
+// ---------------------------------------------------------------------------
+static thread_local std::string g_err;
+
+static int fail(int code, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+#define CU(call)                                                                           \
+    do {                                                                                   \
+        cudaError_t e_ = (call);                                                           \
+        if (e_ != cudaSuccess)                                                             \
+            return fail(e_ == cudaErrorMemoryAllocation ? BSGD_ENOMEM : BSGD_ECUDA,        \
+                        "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, \
+                        __LINE__);                                                         \
+    } while (0)
+
+#define LAUNCHED()                                                                          \
+    do {                                                                                    \
+        cudaError_t e_ = cudaGetLastError();                                                \
+        if (e_ != cudaSuccess)                                                              \
+            return fail(BSGD_ECUDA, "kernel launch failed: %s (%s:%d)", cudaGetErrorString(e_), \
+                        __FILE__, __LINE__);                                                \
+    } while (0)
+
+// ---------------------------------------------------------------------------
+// device facts and occupancy (cached; queried outside graph capture first)
+// ---------------------------------------------------------------------------
+static std::mutex g_mu;
+static std::unordered_map<const void *, int> g_occ;
+static int g_sms[64];
+
+static int num_sms() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) dev = 0;
+    if (g_sms[dev] == 0) {
+        int n = 0;
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        g_sms[dev] = n > 0 ? n : kNumSMs;
+    }
+    return g_sms[dev];
+}
+
+template <typename K>
+static int occupancy(K kernel) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto it = g_occ.find((const void *)kernel);
+    if (it != g_occ.end()) return it->second;
+    int nb = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kernel, kThreads, 0);
+    if (nb < 1) nb = 1;
+    g_occ[(const void *)kernel] = nb;
+    return nb;
+}
+
+static inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// ---------------------------------------------------------------------------
+// plan
+// ---------------------------------------------------------------------------
+struct bsgd_plan {
+    int device = 0;
+    int64_t rows = 0, cols = 0, nnz = 0;
+    int vdt = 8;
+    int64_t M = 1, N = 1;
+    std::vector<int64_t> row_bounds, col_bounds, block_nnz;
+    int64_t *f_ptr = nullptr;
+    int32_t *f_idx = nullptr;
+    void *f_val = nullptr;
+    int64_t *t_ptr = nullptr;
+    int32_t *t_idx = nullptr;
+    void *t_val = nullptr;
+    int64_t *d_row_bounds = nullptr, *d_col_bounds = nullptr;
+    int g_fwd = 32, g_tr = 32;
+    size_t device_bytes = 0;
+};
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+__global__ void check_csr_kernel(int64_t rows, int64_t cols, const int64_t *ptr, const int32_t *idx, int *bad) {
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = ptr[r], e = ptr[r + 1];
+        if (e < b) { atomicOr(bad, 1); continue; }
+        int64_t prevc = -1;
+        for (int64_t k = b; k < e; ++k) {
+            const int64_t c = idx[k];
+            if (c < 0 || c >= cols) { atomicOr(bad, 2); break; }
+            if (c <= prevc) { atomicOr(bad, 4); break; }
+            prevc = c;
+        }
+    }
+}
+
+__global__ void expand_rows_kernel(int64_t rows, const int64_t *ptr, int32_t *rowid) {
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x)
+        for (int64_t k = ptr[r]; k < ptr[r + 1]; ++k) rowid[k] = (int32_t)r;
+}
+
+__global__ void iota_kernel(int64_t n, uint32_t *out) {
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
+        out[k] = (uint32_t)k;
+}
+
+template <typename V>
+__global__ void gather_transpose_kernel(int64_t nnz, const uint32_t *pos, const int32_t *rowid, const V *val,
+                                        int32_t *t_idx, V *t_val) {
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nnz; k += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t p = pos[k];
+        t_idx[k] = rowid[p];
+        t_val[k] = val[p];
+    }
+}
+
+// t_ptr[c] = first position of key >= c in the sorted column keys
+__global__ void col_ptr_kernel(int64_t cols, int64_t nnz, const uint32_t *keys, int64_t *t_ptr) {
+    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c <= cols; c += (int64_t)gridDim.x * blockDim.x) {
+        int64_t lo = 0, hi = nnz;
+        while (lo < hi) {
+            const int64_t mid = lo + ((hi - lo) >> 1);
+            if ((int64_t)keys[mid] < c) lo = mid + 1; else hi = mid;
+        }
+        t_ptr[c] = lo;
+    }
+}
+
+__global__ void block_nnz_kernel(int64_t rows, const int64_t *ptr, const int32_t *idx, int64_t M,
+                                 const int64_t *rb, int64_t N, const int64_t *cb, unsigned long long *cnt) {
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
+        int64_t i = 0;
+        while (i + 1 < M && rb[i + 1] <= r) ++i;
+        int64_t lo = ptr[r];
+        for (int64_t j = 0; j < N; ++j) {
+            const int64_t hi = lower_bound_i32(idx, lo, ptr[r + 1], cb[j + 1]);
+            if (hi > lo) atomicAdd(cnt + i * N + j, (unsigned long long)(hi - lo));
+            lo = hi;
+        }
+    }
+}
+
+static void plan_free(bsgd_plan *p) {
+    if (!p) return;
+    DeviceGuard g(p->device);
+    cudaFree(p->f_ptr); cudaFree(p->f_idx); cudaFree(p->f_val);
+    cudaFree(p->t_ptr); cudaFree(p->t_idx); cudaFree(p->t_val);
+    cudaFree(p->d_row_bounds); cudaFree(p->d_col_bounds);
+    delete p;
+}
+
+static int grid_1d(int64_t n, int per_cta_items = kThreads) {
+    return (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, per_cta_items), (int64_t)num_sms() * 16));
+}
+
+template <typename V>
+static int build_transpose(bsgd_plan *p, cudaStream_t st) {
+    const int64_t nnz = p->nnz;
+    int32_t *rowid = nullptr;
+    uint32_t *keys_out = nullptr, *pos_in = nullptr, *pos_out = nullptr;
+    void *temp = nullptr;
+    size_t temp_bytes = 0;
+    int rc = BSGD_OK;
+    int end_bit = 1;
+    while (end_bit < 32 && ((int64_t)1 << end_bit) <= p->cols) ++end_bit;
+    auto cleanup = [&]() { cudaFree(rowid); cudaFree(keys_out); cudaFree(pos_in); cudaFree(pos_out); cudaFree(temp); };
+#define TRY(call)                                                                        \
+    do {                                                                                 \
+        cudaError_t e_ = (call);                                                         \
+        if (e_ != cudaSuccess) {                                                         \
+            rc = fail(e_ == cudaErrorMemoryAllocation ? BSGD_ENOMEM : BSGD_ECUDA,        \
+                      "%s failed: %s", #call, cudaGetErrorString(e_));                   \
+            cleanup();                                                                   \
+            return rc;                                                                   \
+        }                                                                                \
+    } while (0)
+    TRY(cudaMalloc(&rowid, sizeof(int32_t) * nnz));
+    TRY(cudaMalloc(&keys_out, sizeof(uint32_t) * nnz));
+    TRY(cudaMalloc(&pos_in, sizeof(uint32_t) * nnz));
+    TRY(cudaMalloc(&pos_out, sizeof(uint32_t) * nnz));
+    expand_rows_kernel<<<grid_1d(p->rows), kThreads, 0, st>>>(p->rows, p->f_ptr, rowid);
+    iota_kernel<<<grid_1d(nnz), kThreads, 0, st>>>(nnz, pos_in);
+    TRY(cudaGetLastError());
+    const uint32_t *keys_in = reinterpret_cast<const uint32_t *>(p->f_idx);
+    TRY(cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, keys_in, keys_out, pos_in, pos_out, nnz, 0,
+                                        end_bit, st));
+    TRY(cudaMalloc(&temp, temp_bytes));
+    TRY(cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys_in, keys_out, pos_in, pos_out, nnz, 0,
+                                        end_bit, st));
+    gather_transpose_kernel<V><<<grid_1d(nnz), kThreads, 0, st>>>(nnz, pos_out, rowid, (const V *)p->f_val,
+                                                                  p->t_idx, (V *)p->t_val);
+    col_ptr_kernel<<<grid_1d(p->cols + 1), kThreads, 0, st>>>(p->cols, nnz, keys_out, p->t_ptr);
+    TRY(cudaGetLastError());
+    TRY(cudaStreamSynchronize(st));
+#undef TRY
+    cleanup();
+    return BSGD_OK;
+}
+
+// ---------------------------------------------------------------------------
+// SpMV launchers
+// ---------------------------------------------------------------------------
+template <typename V>
+static Csr<V> fwd_csr(const bsgd_plan *p, const double *vec) {
+    return Csr<V>{p->rows, p->f_ptr, p->f_idx, (const V *)p->f_val, vec};
+}
+template <typename V>
+static Csr<V> tr_csr(const bsgd_plan *p, const double *vec) {
+    return Csr<V>{p->cols, p->t_ptr, p->t_idx, (const V *)p->t_val, vec};
+}
+
+static int ctas_for(int64_t nrows, int G, int cap) {
+    const int64_t warps = cdiv(nrows, 32 / G);
+    return (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(warps, kThreads / 32), cap));
+}
+
+template <typename V, int GA, int GB, class EA, class EB>
+static int launch_dual(const Csr<V> &A, const EA &ea, double *partA, int64_t *cntA, int64_t nnzA,
+                       const Csr<V> &B, const EB &eb, double *partB, int64_t *cntB, int64_t nnzB,
+                       cudaStream_t st) {
+    auto kern = dual_csr_kernel<V, GA, GB, EA, EB>;
+    const int cap = std::min(occupancy(kern) * num_sms(), kMaxPartials);
+    const bool hasB = !std::is_same<EB, EpiNone>::value && B.nrows > 0;
+    int nA = 0, nB = 0;
+    if (hasB) {
+        const double fa = (double)(nnzA + A.nrows) / (double)(nnzA + A.nrows + nnzB + B.nrows);
+        const int capA = std::max(1, (int)std::lround(cap * fa));
+        const int capB = std::max(1, cap - capA);
+        nA = A.nrows > 0 ? ctas_for(A.nrows, GA, capA) : 0;
+        nB = ctas_for(B.nrows, GB, capB);
+    } else {
+        nA = A.nrows > 0 ? ctas_for(A.nrows, GA, cap) : 0;
+    }
+    if (nA + nB == 0) return BSGD_OK;
+    kern<<<nA + nB, kThreads, 0, st>>>(A, ea, partA, nA, cntA, B, eb, partB, cntB);
+    LAUNCHED();
+    return BSGD_OK;
+}
+
+// single product of one operand with lanes-per-row G chosen from the plan
+template <typename V, class E>
+static int launch_one(const Csr<V> &A, int G, const E &e, double *part, int64_t *cnt, int64_t nnz,
+                      cudaStream_t st) {
+    const Csr<V> none{0, nullptr, nullptr, nullptr, nullptr};
+    if (G == 8) return launch_dual<V, 8, 8, E, EpiNone>(A, e, part, cnt, nnz, none, EpiNone{}, nullptr, nullptr, 0, st);
+    return launch_dual<V, 32, 8, E, EpiNone>(A, e, part, cnt, nnz, none, EpiNone{}, nullptr, nullptr, 0, st);
+}
+
+template <typename V, class EA, class EB>
+static int launch_two(const Csr<V> &A, int GA, const EA &ea, double *partA, int64_t *cntA, int64_t nnzA,
+                      const Csr<V> &B, int GB, const EB &eb, double *partB, int64_t *cntB, int64_t nnzB,
+                      cudaStream_t st) {
+    if (GA == 8 && GB == 8)
+        return launch_dual<V, 8, 8, EA, EB>(A, ea, partA, cntA, nnzA, B, eb, partB, cntB, nnzB, st);
+    if (GA == 8)
+        return launch_dual<V, 8, 32, EA, EB>(A, ea, partA, cntA, nnzA, B, eb, partB, cntB, nnzB, st);
+    if (GB == 8)
+        return launch_dual<V, 32, 8, EA, EB>(A, ea, partA, cntA, nnzA, B, eb, partB, cntB, nnzB, st);
+    return launch_dual<V, 32, 32, EA, EB>(A, ea, partA, cntA, nnzA, B, eb, partB, cntB, nnzB, st);
+}
+
+#define DISPATCH_V(p, ...)                                          \
+    ((p)->vdt == BSGD_F32 ? [&]() { using V = float; return __VA_ARGS__; }() \
+                          : [&]() { using V = double; return __VA_ARGS__; }())
+
+// ---------------------------------------------------------------------------
+// workspace layout (shared by the epoch pieces and the standalone prox)
+// ---------------------------------------------------------------------------
+struct Ws {
+    int64_t *ctl;    // [0] nx  [1] nr  [2] scratch count
+    double *scal;    // prox scalars + reduction results
+    double *xpart;   // [kMaxPartials * 4]
+    double *rpart;   // [kMaxPartials]
+    double *red;     // [2 * kMaxPartials * 4]
+    double *uimg;    // [cols]
+    double *fields;  // [6 * hw]
+};
+
+static size_t a256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+static size_t ws_layout(void *base, int64_t cols, int64_t hw, Ws *ws) {
+    size_t off = 0;
+    auto take = [&](size_t bytes) { size_t o = off; off += a256(bytes); return (char *)base + o; };
+    char *ctl = take(sizeof(int64_t) * 16);
+    char *scal = take(sizeof(double) * 32);
+    char *xpart = take(sizeof(double) * kMaxPartials * 4);
+    char *rpart = take(sizeof(double) * kMaxPartials);
+    char *red = take(sizeof(double) * 2 * kMaxPartials * 4);
+    char *uimg = take(sizeof(double) * (size_t)std::max<int64_t>(cols, 1));
+    char *fields = take(sizeof(double) * 6 * (size_t)std::max<int64_t>(hw, 0));
+    if (ws) {
+        ws->ctl = (int64_t *)ctl; ws->scal = (double *)scal; ws->xpart = (double *)xpart;
+        ws->rpart = (double *)rpart; ws->red = (double *)red; ws->uimg = (double *)uimg;
+        ws->fields = (double *)fields;
+    }
+    return off;
+}
+
+// ---------------------------------------------------------------------------
+// small reduction kernels
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads) dot_part_kernel(int64_t n, const double *a, const double *b, int mode,
+                                                            double *part) {
+    __shared__ double sm[kThreads / 32];
+    double v[1] = {0.0};
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+        if (mode == 0) v[0] += a[k] * b[k];
+        else { const double d = a[k] - b[k]; v[0] += d * d; }
+    }
+    block_sum<1>(v, sm);
+    if (threadIdx.x == 0) part[blockIdx.x] = v[0];
+}
+
+__global__ void sum_parts_kernel(const double *part, int n, double *out) {
+    double v[1];
+    warp_sum_partials<1>(part, n, v);
+    if (threadIdx.x == 0) out[0] = v[0];
+}
+
+__global__ void sum_counted_kernel(const double *part, const int64_t *cnt, double *out) {
+    double v[1];
+    warp_sum_partials<1>(part, (int)cnt[0], v);
+    if (threadIdx.x == 0) out[0] = v[0];
+}
+
+__global__ void assemble_kernel(int64_t rows, int64_t N, const double *y, const double *z, double *out) {
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
+        double acc = y[r];
+        for (int64_t j = 0; j < N; ++j) acc = rn_sub(acc, z[j * rows + r]);
+        out[r] = acc;
+    }
+}
+
+__global__ void set_info_kernel(int32_t *info, int32_t a, int32_t b, int32_t c, int32_t d) {
+    info[0] = a; info[1] = b; info[2] = c; info[3] = d;
+}
+
+struct TailArgs {
+    const int64_t *ctl;
+    const double *xpart;
+    const double *rpart;
+    const double *scal;
+    const double *fnext_dev;
+    int fnext_mode;  // 0 none, 1 from rpart, 2 from fnext_dev
+    int monitor;
+    int has_prox;
+    double mu;
+    double *f_curr;
+    double *history;
+    int64_t *counter;
+    int64_t cap;
+};
+
+__global__ void tail_kernel(TailArgs t) {
+    double xs[4];
+    warp_sum_partials<4>(t.xpart, (int)t.ctl[0], xs);
+    double fn = __longlong_as_double(0x7ff8000000000000LL);
+    if (t.fnext_mode == 1) {
+        double r[1];
+        warp_sum_partials<1>(t.rpart, (int)t.ctl[1], r);
+        fn = r[0];
+    } else if (t.fnext_mode == 2) {
+        fn = t.fnext_dev[0];
+    }
+    if (threadIdx.x == 0) {
+        const int64_t row = t.counter[0];
+        const double fc = t.f_curr != nullptr ? t.f_curr[0] : 0.0;
+        double holds = -1.0;
+        if (t.monitor) {
+            // sufficient_decrease_holds (solvers.py:198-215): f_next < f_curr + d.(-g) + |d|^2/(2 mu)
+            double bound = rn_add(fc, -xs[2]);
+            bound = rn_add(bound, xs[3] / (2.0 * t.mu));
+            holds = (fn < bound) ? 1.0 : 0.0;
+            t.f_curr[0] = fn;
+        }
+        if (row >= 0 && row < t.cap) {
+            double *h = t.history + row * BSGD_HIST_COLS;
+            h[BSGD_H_FNEXT] = fn;
+            h[BSGD_H_HOLDS] = holds;
+            h[BSGD_H_XX] = xs[0];
+            h[BSGD_H_XE] = xs[1];
+            h[BSGD_H_TV] = t.has_prox ? t.scal[0] : 0.0;
+            h[BSGD_H_PITER] = t.has_prox ? t.scal[1] : 0.0;
+            h[BSGD_H_PRESTART] = t.has_prox ? t.scal[2] : 0.0;
+            h[BSGD_H_PCONV] = t.has_prox ? t.scal[3] : 0.0;
+            h[BSGD_H_PFELL] = t.has_prox ? t.scal[4] : 0.0;
+            h[BSGD_H_DG] = xs[2];
+            h[BSGD_H_DD] = xs[3];
+            h[BSGD_H_FCURR] = fc;
+        }
+        t.counter[0] = row + 1;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// prox launch
+// ---------------------------------------------------------------------------
+static int launch_prox(ProxArgs &a, cudaStream_t st) {
+    const int occ = occupancy(fgp_kernel);
+    int grid = (int)std::min<int64_t>(cdiv(a.N, kThreads), (int64_t)occ * num_sms());
+    grid = std::max(1, std::min(grid, kMaxPartials));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CU(cudaLaunchKernelEx(&cfg, fgp_kernel, a));
+    return BSGD_OK;
+}
+
+static void prox_fields(ProxArgs &a, const Ws &ws, int64_t hw) {
+    for (int k = 0; k < 6; ++k) a.f[k] = ws.fields + (size_t)k * hw;
+    a.red = ws.red;
+}
+
+// ---------------------------------------------------------------------------
+// C ABI
+// ---------------------------------------------------------------------------
+extern "C" {
+
+const char *bsgd_last_error(void) { return g_err.c_str(); }
+
+int bsgd_version(void) { return BSGD_VERSION; }
+
+int bsgd_device_count(int *out) {
+    if (!out) return fail(BSGD_EINVAL, "out is NULL");
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess) { cudaGetLastError(); n = 0; }
+    *out = n;
+    return BSGD_OK;
+}
+
+int bsgd_plan_create(bsgd_plan **out, int device, int64_t rows, int64_t cols, int64_t nnz,
+                     const int64_t *indptr, const int32_t *indices, const void *values, int value_dtype,
+                     int64_t num_row_blocks, int64_t num_col_blocks, const int64_t *row_bounds,
+                     const int64_t *col_bounds, void *stream) {
+    if (!out) return fail(BSGD_EINVAL, "out is NULL");
+    *out = nullptr;
+    if (rows < 1 || cols < 1) return fail(BSGD_EINVAL, "matrix dimensions must be positive");
+    if (cols >= ((int64_t)1 << 31) || rows >= ((int64_t)1 << 31))
+        return fail(BSGD_EINVAL, "dimensions must be < 2^31 (int32 indices)");
+    if (nnz == 0) return fail(BSGD_EINVAL, "matrix has no nonzeros");
+    if (nnz < 0 || nnz >= ((int64_t)1 << 32)) return fail(BSGD_EINVAL, "nnz %lld out of range", (long long)nnz);
+    if (value_dtype != BSGD_F32 && value_dtype != BSGD_F64) return fail(BSGD_EINVAL, "value dtype must be 4 or 8");
+    if (!indptr || !indices || !values || !row_bounds || !col_bounds) return fail(BSGD_EINVAL, "NULL array");
+    if (indptr[0] != 0 || indptr[rows] != nnz) return fail(BSGD_EINVAL, "indptr must run from 0 to nnz");
+    if (num_row_blocks < 1 || num_row_blocks > rows) return fail(BSGD_EINVAL, "row block count not in [1, rows]");
+    if (num_col_blocks < 1 || num_col_blocks > cols) return fail(BSGD_EINVAL, "col block count not in [1, cols]");
+    for (int64_t i = 0; i < num_row_blocks; ++i)
+        if (row_bounds[i + 1] <= row_bounds[i]) return fail(BSGD_EINVAL, "row ranges must be nonempty and ascending");
+    for (int64_t j = 0; j < num_col_blocks; ++j)
+        if (col_bounds[j + 1] <= col_bounds[j]) return fail(BSGD_EINVAL, "col ranges must be nonempty and ascending");
+    if (row_bounds[0] != 0 || col_bounds[0] != 0) return fail(BSGD_EINVAL, "ranges must start at 0");
+    if (row_bounds[num_row_blocks] != rows || col_bounds[num_col_blocks] != cols)
+        return fail(BSGD_EINVAL, "partition covers %lldx%lld, matrix is %lldx%lld",
+                    (long long)row_bounds[num_row_blocks], (long long)col_bounds[num_col_blocks],
+                    (long long)rows, (long long)cols);
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return fail(BSGD_ECUDA, "no CUDA device available");
+    }
+    if (device < 0 || device >= ndev) return fail(BSGD_EINVAL, "device %d out of range", device);
+    DeviceGuard guard(device);
+    cudaStream_t st = (cudaStream_t)stream;
+    bsgd_plan *p = new bsgd_plan();
+    p->device = device;
+    p->rows = rows; p->cols = cols; p->nnz = nnz; p->vdt = value_dtype;
+    p->M = num_row_blocks; p->N = num_col_blocks;
+    p->row_bounds.assign(row_bounds, row_bounds + num_row_blocks + 1);
+    p->col_bounds.assign(col_bounds, col_bounds + num_col_blocks + 1);
+    const double mean_r = (double)nnz / rows, mean_c = (double)nnz / cols;
+    p->g_fwd = mean_r < 64.0 ? 8 : 32;
+    p->g_tr = mean_c < 64.0 ? 8 : 32;
+    int rc = BSGD_OK;
+#define PTRY(call)                                                                         \
+    do {                                                                                   \
+        cudaError_t e_ = (call);                                                           \
+        if (e_ != cudaSuccess) {                                                           \
+            rc = fail(e_ == cudaErrorMemoryAllocation ? BSGD_ENOMEM : BSGD_ECUDA,          \
+                      "%s failed: %s", #call, cudaGetErrorString(e_));                     \
+            plan_free(p);                                                                  \
+            return rc;                                                                     \
+        }                                                                                  \
+    } while (0)
+    const size_t vb = (size_t)value_dtype;
+    PTRY(cudaMalloc(&p->f_ptr, sizeof(int64_t) * (rows + 1)));
+    PTRY(cudaMalloc(&p->f_idx, sizeof(int32_t) * nnz));
+    PTRY(cudaMalloc(&p->f_val, vb * nnz));
+    PTRY(cudaMalloc(&p->t_ptr, sizeof(int64_t) * (cols + 1)));
+    PTRY(cudaMalloc(&p->t_idx, sizeof(int32_t) * nnz));
+    PTRY(cudaMalloc(&p->t_val, vb * nnz));
+    PTRY(cudaMalloc(&p->d_row_bounds, sizeof(int64_t) * (num_row_blocks + 1)));
+    PTRY(cudaMalloc(&p->d_col_bounds, sizeof(int64_t) * (num_col_blocks + 1)));
+    p->device_bytes = sizeof(int64_t) * (rows + cols + 2) + 2 * (sizeof(int32_t) + vb) * nnz;
+    PTRY(cudaMemcpyAsync(p->f_ptr, indptr, sizeof(int64_t) * (rows + 1), cudaMemcpyHostToDevice, st));
+    PTRY(cudaMemcpyAsync(p->f_idx, indices, sizeof(int32_t) * nnz, cudaMemcpyHostToDevice, st));
+    PTRY(cudaMemcpyAsync(p->f_val, values, vb * nnz, cudaMemcpyHostToDevice, st));
+    PTRY(cudaMemcpyAsync(p->d_row_bounds, row_bounds, sizeof(int64_t) * (num_row_blocks + 1), cudaMemcpyHostToDevice, st));
+    PTRY(cudaMemcpyAsync(p->d_col_bounds, col_bounds, sizeof(int64_t) * (num_col_blocks + 1), cudaMemcpyHostToDevice, st));
+    // structural check (canonical form: sorted unique in-range indices per row)
+    int *d_bad = nullptr;
+    PTRY(cudaMalloc(&d_bad, sizeof(int)));
+    PTRY(cudaMemsetAsync(d_bad, 0, sizeof(int), st));
+    check_csr_kernel<<<grid_1d(rows), kThreads, 0, st>>>(rows, cols, p->f_ptr, p->f_idx, d_bad);
+    int bad = 0;
+    PTRY(cudaMemcpyAsync(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+    PTRY(cudaStreamSynchronize(st));
+    cudaFree(d_bad);
+    if (bad) {
+        plan_free(p);
+        return fail(BSGD_EINVAL, "CSR is not canonical (code %d: 1=indptr, 2=index range, 4=unsorted/duplicate)", bad);
+    }
+    rc = (value_dtype == BSGD_F32) ? build_transpose<float>(p, st) : build_transpose<double>(p, st);
+    if (rc != BSGD_OK) { plan_free(p); return rc; }
+    // block nnz table (blockops.py:179-180)
+    unsigned long long *d_cnt = nullptr;
+    const int64_t nb = num_row_blocks * num_col_blocks;
+    PTRY(cudaMalloc(&d_cnt, sizeof(unsigned long long) * nb));
+    PTRY(cudaMemsetAsync(d_cnt, 0, sizeof(unsigned long long) * nb, st));
+    block_nnz_kernel<<<grid_1d(rows), kThreads, 0, st>>>(rows, p->f_ptr, p->f_idx, num_row_blocks, p->d_row_bounds,
+                                                         num_col_blocks, p->d_col_bounds, d_cnt);
+    std::vector<unsigned long long> cnt(nb);
+    PTRY(cudaMemcpyAsync(cnt.data(), d_cnt, sizeof(unsigned long long) * nb, cudaMemcpyDeviceToHost, st));
+    PTRY(cudaStreamSynchronize(st));
+    cudaFree(d_cnt);
+    p->block_nnz.assign(cnt.begin(), cnt.end());
+#undef PTRY
+    // warm occupancy caches outside any graph capture
+    (void)occupancy(fgp_kernel);
+    *out = p;
+    return BSGD_OK;
+}
+
+int bsgd_plan_destroy(bsgd_plan *plan) {
+    plan_free(plan);
+    return BSGD_OK;
+}
+
+int bsgd_plan_info(const bsgd_plan *p, int64_t *rows, int64_t *cols, int64_t *nnz, int *value_dtype,
+                   int64_t *device_bytes) {
+    if (!p) return fail(BSGD_EINVAL, "plan is NULL");
+    if (rows) *rows = p->rows;
+    if (cols) *cols = p->cols;
+    if (nnz) *nnz = p->nnz;
+    if (value_dtype) *value_dtype = p->vdt;
+    if (device_bytes) *device_bytes = (int64_t)p->device_bytes;
+    return BSGD_OK;
+}
+
+static int check_block(const bsgd_plan *p, int64_t i, int64_t j) {
+    if (!p) return fail(BSGD_EINVAL, "plan is NULL");
+    if (i < 0 || i >= p->M || j < 0 || j >= p->N)
+        return fail(BSGD_EINVAL, "block (%lld, %lld) outside the %lldx%lld grid", (long long)i, (long long)j,
+                    (long long)p->M, (long long)p->N);
+    return BSGD_OK;
+}
+
+int bsgd_plan_block_nnz(const bsgd_plan *p, int64_t i, int64_t j, int64_t *out) {
+    int rc = check_block(p, i, j);
+    if (rc) return rc;
+    if (!out) return fail(BSGD_EINVAL, "out is NULL");
+    *out = p->block_nnz[i * p->N + j];
+    return BSGD_OK;
+}
+
+int bsgd_plan_block_copy(const bsgd_plan *p, int64_t i, int64_t j, int64_t *indptr_out, int32_t *indices_out,
+                         void *values_out, void *stream) {
+    int rc = check_block(p, i, j);
+    if (rc) return rc;
+    if (!indptr_out || !indices_out || !values_out) return fail(BSGD_EINVAL, "NULL output");
+    DeviceGuard guard(p->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t r0 = p->row_bounds[i], r1 = p->row_bounds[i + 1];
+    const int64_t c0 = p->col_bounds[j], c1 = p->col_bounds[j + 1];
+    std::vector<int64_t> ptr(r1 - r0 + 1);
+    CU(cudaMemcpyAsync(ptr.data(), p->f_ptr + r0, sizeof(int64_t) * (r1 - r0 + 1), cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    const int64_t base = ptr[0], len = ptr[r1 - r0] - base;
+    std::vector<int32_t> idx(len);
+    std::vector<char> val((size_t)len * p->vdt);
+    if (len > 0) {
+        CU(cudaMemcpyAsync(idx.data(), p->f_idx + base, sizeof(int32_t) * len, cudaMemcpyDeviceToHost, st));
+        CU(cudaMemcpyAsync(val.data(), (const char *)p->f_val + (size_t)base * p->vdt, (size_t)len * p->vdt,
+                           cudaMemcpyDeviceToHost, st));
+        CU(cudaStreamSynchronize(st));
+    }
+    int64_t w = 0;
+    indptr_out[0] = 0;
+    for (int64_t r = 0; r < r1 - r0; ++r) {
+        const int32_t *b = idx.data() + (ptr[r] - base), *e = idx.data() + (ptr[r + 1] - base);
+        const int32_t *lo = std::lower_bound(b, e, (int32_t)c0);
+        const int32_t *hi = std::lower_bound(lo, e, (int32_t)c1);
+        for (const int32_t *q = lo; q < hi; ++q, ++w) {
+            indices_out[w] = *q - (int32_t)c0;
+            memcpy((char *)values_out + (size_t)w * p->vdt, val.data() + (size_t)(q - idx.data()) * p->vdt, p->vdt);
+        }
+        indptr_out[r + 1] = w;
+    }
+    return BSGD_OK;
+}
+
+int bsgd_plan_transpose_copy(const bsgd_plan *p, int64_t *indptr_out, int32_t *indices_out, void *values_out,
+                             void *stream) {
+    if (!p) return fail(BSGD_EINVAL, "plan is NULL");
+    if (!indptr_out || !indices_out || !values_out) return fail(BSGD_EINVAL, "NULL output");
+    DeviceGuard guard(p->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    CU(cudaMemcpyAsync(indptr_out, p->t_ptr, sizeof(int64_t) * (p->cols + 1), cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(indices_out, p->t_idx, sizeof(int32_t) * p->nnz, cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(values_out, p->t_val, (size_t)p->vdt * p->nnz, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    return BSGD_OK;
+}
+
+int bsgd_block_matvec(const bsgd_plan *p, int64_t i, int64_t j, const double *x_j, double *out, void *stream) {
+    int rc = check_block(p, i, j);
+    if (rc) return rc;
+    if (!x_j || !out) return fail(BSGD_EINVAL, "NULL vector");
+    DeviceGuard guard(p->device);
+    const int64_t r0 = p->row_bounds[i], r1 = p->row_bounds[i + 1];
+    const int64_t c0 = p->col_bounds[j], c1 = p->col_bounds[j + 1];
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(r1 - r0, kThreads / 32), num_sms() * 8));
+    if (p->vdt == BSGD_F32)
+        block_seg_kernel<float><<<grid, kThreads, 0, (cudaStream_t)stream>>>(p->f_ptr, p->f_idx, (const float *)p->f_val,
+                                                                            r0, r1, c0, c1, x_j, out);
+    else
+        block_seg_kernel<double><<<grid, kThreads, 0, (cudaStream_t)stream>>>(p->f_ptr, p->f_idx, (const double *)p->f_val,
+                                                                             r0, r1, c0, c1, x_j, out);
+    LAUNCHED();
+    return BSGD_OK;
+}
+
+int bsgd_block_matvec_transpose(const bsgd_plan *p, int64_t i, int64_t j, const double *r_i, double *out,
+                                void *stream) {
+    int rc = check_block(p, i, j);
+    if (rc) return rc;
+    if (!r_i || !out) return fail(BSGD_EINVAL, "NULL vector");
+    DeviceGuard guard(p->device);
+    const int64_t r0 = p->row_bounds[i], r1 = p->row_bounds[i + 1];
+    const int64_t c0 = p->col_bounds[j], c1 = p->col_bounds[j + 1];
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(c1 - c0, kThreads / 32), num_sms() * 8));
+    // A^T rows [c0, c1), entries with A-row index in [r0, r1)
+    if (p->vdt == BSGD_F32)
+        block_seg_kernel<float><<<grid, kThreads, 0, (cudaStream_t)stream>>>(p->t_ptr, p->t_idx, (const float *)p->t_val,
+                                                                            c0, c1, r0, r1, r_i, out);
+    else
+        block_seg_kernel<double><<<grid, kThreads, 0, (cudaStream_t)stream>>>(p->t_ptr, p->t_idx, (const double *)p->t_val,
+                                                                             c0, c1, r0, r1, r_i, out);
+    LAUNCHED();
+    return BSGD_OK;
+}
+
+int bsgd_matvec(const bsgd_plan *p, const double *x, double *out, void *stream) {
+    if (!p || !x || !out) return fail(BSGD_EINVAL, "NULL argument");
+    DeviceGuard guard(p->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    return DISPATCH_V(p, launch_one<V>(fwd_csr<V>(p, x), p->g_fwd, EpiStore{out, 1.0}, nullptr, nullptr, p->nnz, st));
+}
+
+int bsgd_rmatvec(const bsgd_plan *p, const double *w, double *out, void *stream) {
+    if (!p || !w || !out) return fail(BSGD_EINVAL, "NULL argument");
+    DeviceGuard guard(p->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    return DISPATCH_V(p, launch_one<V>(tr_csr<V>(p, w), p->g_tr, EpiStore{out, 1.0}, nullptr, nullptr, p->nnz, st));
+}
+
+int bsgd_grad(const bsgd_plan *p, const double *r, double *g, void *stream) {
+    if (!p || !r || !g) return fail(BSGD_EINVAL, "NULL argument");
+    DeviceGuard guard(p->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    return DISPATCH_V(p, launch_one<V>(tr_csr<V>(p, r), p->g_tr, EpiStore{g, 2.0}, nullptr, nullptr, p->nnz, st));
+}
+
+int bsgd_residual(const bsgd_plan *p, const double *x, const double *y, double *r_out, double *sumsq_out,
+                  void *scratch, void *stream) {
+    if (!p || !x || !y || !r_out) return fail(BSGD_EINVAL, "NULL argument");
+    if (sumsq_out && !scratch) return fail(BSGD_EINVAL, "scratch required for sumsq_out");
+    DeviceGuard guard(p->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    double *part = sumsq_out ? (double *)scratch : nullptr;
+    int64_t *cnt = sumsq_out ? (int64_t *)((char *)scratch + sizeof(double) * kMaxPartials) : nullptr;
+    EpiResid e{y, r_out};
+    int rc = DISPATCH_V(p, launch_one<V>(fwd_csr<V>(p, x), p->g_fwd, e, part, cnt, p->nnz, st));
+    if (rc) return rc;
+    if (sumsq_out) {
+        sum_counted_kernel<<<1, 32, 0, st>>>(part, cnt, sumsq_out);
+        LAUNCHED();
+    }
+    return BSGD_OK;
+}
+
+int bsgd_assemble_residual(int64_t rows, int64_t num_col_blocks, const double *y, const double *z_cache,
+                           double *out, void *stream) {
+    if (rows < 1 || num_col_blocks < 0 || !y || !out || (num_col_blocks > 0 && !z_cache))
+        return fail(BSGD_EINVAL, "bad assemble_residual arguments");
+    assemble_kernel<<<grid_1d(rows), kThreads, 0, (cudaStream_t)stream>>>(rows, num_col_blocks, y, z_cache, out);
+    LAUNCHED();
+    return BSGD_OK;
+}
+
+int bsgd_pair_products(const bsgd_plan *p, int64_t n_rows_sel, const int64_t *row_sel, int64_t n_cols_sel,
+                       const int64_t *col_sel, const double *x_k, const double *r_k, const double *y,
+                       double *z_cache, double *g, double *r_next, void *stream) {
+    if (!p || !x_k || !r_k || !y || !z_cache || !g || !r_next) return fail(BSGD_EINVAL, "NULL argument");
+    if (p->M > 256 || p->N > 256) return fail(BSGD_EINVAL, "pair path supports at most 256 blocks per side");
+    if (n_rows_sel < 1 || n_cols_sel < 1 || !row_sel || !col_sel)
+        return fail(BSGD_EINVAL, "alpha/gamma select no blocks");
+    BlockMask rs{{0, 0, 0, 0}}, cs{{0, 0, 0, 0}};
+    for (int64_t k = 0; k < n_rows_sel; ++k) {
+        if (row_sel[k] < 0 || row_sel[k] >= p->M) return fail(BSGD_EINVAL, "row block index out of range");
+        rs.w[row_sel[k] >> 6] |= 1ull << (row_sel[k] & 63);
+    }
+    for (int64_t k = 0; k < n_cols_sel; ++k) {
+        if (col_sel[k] < 0 || col_sel[k] >= p->N) return fail(BSGD_EINVAL, "col block index out of range");
+        cs.w[col_sel[k] >> 6] |= 1ull << (col_sel[k] & 63);
+    }
+    DeviceGuard guard(p->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    const int gr = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(p->rows, kThreads / 32), num_sms() * 8));
+    const int gc = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(p->cols, kThreads / 32), num_sms() * 8));
+    if (p->vdt == BSGD_F32) {
+        pair_grad_kernel<float><<<gc, kThreads, 0, st>>>(p->t_ptr, p->t_idx, (const float *)p->t_val, p->cols,
+                                                         p->d_row_bounds, p->M, p->d_col_bounds, p->N, rs, cs, r_k, g);
+        pair_forward_kernel<float><<<gr, kThreads, 0, st>>>(p->f_ptr, p->f_idx, (const float *)p->f_val, p->rows,
+                                                            p->d_row_bounds, p->M, p->d_col_bounds, p->N, rs, cs,
+                                                            x_k, y, z_cache, r_next);
+    } else {
+        pair_grad_kernel<double><<<gc, kThreads, 0, st>>>(p->t_ptr, p->t_idx, (const double *)p->t_val, p->cols,
+                                                          p->d_row_bounds, p->M, p->d_col_bounds, p->N, rs, cs, r_k, g);
+        pair_forward_kernel<double><<<gr, kThreads, 0, st>>>(p->f_ptr, p->f_idx, (const double *)p->f_val, p->rows,
+                                                             p->d_row_bounds, p->M, p->d_col_bounds, p->N, rs, cs,
+                                                             x_k, y, z_cache, r_next);
+    }
+    LAUNCHED();
+    return BSGD_OK;
+}
+
+// ---- TV ----
+size_t bsgd_tv_prox_workspace_bytes(int64_t height, int64_t width) {
+    if (height < 1 || width < 1) return 0;
+    return ws_layout(nullptr, 1, height * width, nullptr);
+}
+
+int bsgd_tv_prox(int64_t height, int64_t width, const double *img, double *out, double weight,
+                 int32_t max_inner_iters, double tol, void *workspace, size_t workspace_bytes,
+                 bsgd_prox_info *info_out, double *dual_objectives, void *stream) {
+    if (height < 1 || width < 1) return fail(BSGD_EINVAL, "image dimensions must be positive");
+    if (!img || !out) return fail(BSGD_EINVAL, "NULL image");
+    if (!(weight >= 0.0)) return fail(BSGD_EINVAL, "prox weight must be nonnegative");
+    if (max_inner_iters < 1) return fail(BSGD_EINVAL, "max_inner_iters must be >= 1");
+    if (!(tol > 0.0)) return fail(BSGD_EINVAL, "tol must be positive");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t hw = height * width;
+    if (weight == 0.0) {  // tv.py:190-193: identity, converged
+        CU(cudaMemcpyAsync(out, img, sizeof(double) * hw, cudaMemcpyDeviceToDevice, st));
+        if (info_out) {
+            const bsgd_prox_info zero = {0, 1, 0, 0};
+            static_assert(sizeof(bsgd_prox_info) == 16, "layout");
+            set_info_kernel<<<1, 1, 0, st>>>((int32_t *)info_out, zero.iterations, zero.converged, zero.restarts,
+                                             zero.fell_back);
+            LAUNCHED();
+        }
+        return BSGD_OK;
+    }
+    Ws ws;
+    const size_t need = ws_layout(workspace, 1, hw, &ws);
+    if (!workspace || workspace_bytes < need) return fail(BSGD_EINVAL, "workspace too small (%zu < %zu)", workspace_bytes, need);
+    ProxArgs a = {};
+    a.H = height; a.W = width; a.N = hw;
+    a.b = img;
+    prox_fields(a, ws, hw);
+    a.w = weight;
+    a.step = 1.0 / (8.0 * weight);
+    a.tol = tol;
+    a.max_iters = max_inner_iters;
+    a.out_img = out;
+    a.scal = ws.scal;
+    a.info = (int32_t *)info_out;
+    a.dual = dual_objectives;
+    return launch_prox(a, st);
+}
+
+static int reduce_launch(int64_t n, const double *a, const double *b, int mode, double *out, void *scratch,
+                         cudaStream_t st) {
+    if (n < 0 || !out || !scratch || (n > 0 && (!a || !b))) return fail(BSGD_EINVAL, "bad reduction arguments");
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, kThreads), std::min(num_sms() * 8, kMaxPartials)));
+    double *part = (double *)scratch;
+    dot_part_kernel<<<grid, kThreads, 0, st>>>(n, a, b, mode, part);
+    sum_parts_kernel<<<1, 32, 0, st>>>(part, grid, out);
+    LAUNCHED();
+    return BSGD_OK;
+}
+
+int bsgd_dot(int64_t n, const double *a, const double *b, double *out, void *scratch, void *stream) {
+    return reduce_launch(n, a, b, 0, out, scratch, (cudaStream_t)stream);
+}
+
+int bsgd_sqdist(int64_t n, const double *a, const double *b, double *out, void *scratch, void *stream) {
+    return reduce_launch(n, a, b, 1, out, scratch, (cudaStream_t)stream);
+}
+
+int bsgd_tv_value(int64_t height, int64_t width, const double *img, double *out, void *scratch, void *stream) {
+    if (height < 1 || width < 1 || !img || !out || !scratch) return fail(BSGD_EINVAL, "bad tv_value arguments");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t hw = height * width;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(hw, kThreads), std::min(num_sms() * 8, kMaxPartials)));
+    tv_value_kernel<<<grid, kThreads, 0, st>>>(height, width, img, (double *)scratch);
+    sum_parts_kernel<<<1, 32, 0, st>>>((double *)scratch, grid, out);
+    LAUNCHED();
+    return BSGD_OK;
+}
+
+int bsgd_discrete_gradient(int64_t height, int64_t width, const double *img, double *dv, double *dh, void *stream) {
+    if (height < 1 || width < 1 || !img || !dv || !dh) return fail(BSGD_EINVAL, "bad gradient arguments");
+    gradient_kernel<<<grid_1d(height * width), kThreads, 0, (cudaStream_t)stream>>>(height, width, img, dv, dh);
+    LAUNCHED();
+    return BSGD_OK;
+}
+
+int bsgd_discrete_divergence(int64_t height, int64_t width, const double *pv, const double *ph, double *out,
+                             void *stream) {
+    if (height < 1 || width < 1 || !pv || !ph || !out) return fail(BSGD_EINVAL, "bad divergence arguments");
+    divergence_kernel<<<grid_1d(height * width), kThreads, 0, (cudaStream_t)stream>>>(height, width, pv, ph, out);
+    LAUNCHED();
+    return BSGD_OK;
+}
+
+// ---- epoch ----
+size_t bsgd_epoch_workspace_bytes(const bsgd_plan *p, int64_t height, int64_t width) {
+    if (!p) return 0;
+    const int64_t hw = (height > 0 && width > 0) ? height * width : 0;
+    return ws_layout(nullptr, p->cols, hw, nullptr);
+}
+
+static int check_epoch_args(int64_t cols, const bsgd_epoch_args *a, Ws *ws) {
+    if (!a) return fail(BSGD_EINVAL, "args is NULL");
+    if (!(a->mu > 0.0)) return fail(BSGD_EINVAL, "mu must be positive");
+    if (a->lam < 0.0) return fail(BSGD_EINVAL, "lam must be nonnegative");
+    const bool prox = a->lam > 0.0;
+    if (prox) {
+        if (a->height < 1 || a->width < 1 || a->height * a->width != cols)
+            return fail(BSGD_EINVAL, "layout required when lam > 0 (height*width must equal cols)");
+        if (a->max_inner_iters < 1) return fail(BSGD_EINVAL, "max_inner_iters must be >= 1");
+        if (!(a->tol > 0.0)) return fail(BSGD_EINVAL, "tol must be positive");
+    }
+    if (!a->x_k || !a->g || !a->x_next) return fail(BSGD_EINVAL, "x_k, g and x_next are required");
+    if (!a->workspace) return fail(BSGD_EINVAL, "workspace is NULL");
+    const int64_t hw = prox ? a->height * a->width : 0;
+    const size_t need = ws_layout(a->workspace, cols, hw, ws);
+    if (a->workspace_bytes < need) return fail(BSGD_EINVAL, "workspace too small (%zu < %zu)", a->workspace_bytes, need);
+    if (!(a->flags & BSGD_EP_NO_TAIL) && (!a->history || !a->epoch_counter))
+        return fail(BSGD_EINVAL, "history and epoch_counter are required");
+    if ((a->flags & BSGD_EP_MONITOR) && !a->f_curr) return fail(BSGD_EINVAL, "f_curr required with MONITOR");
+    return BSGD_OK;
+}
+
+// x_next = prox(x_k + mu g) from a g already in memory (solvers.py:305-314)
+static int run_step(int64_t cols, const bsgd_epoch_args *a, const Ws &ws, cudaStream_t st) {
+    const bool prox = a->lam > 0.0;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(cols, kThreads), std::min(num_sms() * 8, kMaxPartials)));
+    step_kernel<<<grid, kThreads, 0, st>>>(cols, a->x_k, a->g, a->mu, a->x_next, prox ? ws.uimg : nullptr, a->perm,
+                                          a->x_true, ws.xpart, ws.ctl);
+    LAUNCHED();
+    return BSGD_OK;
+}
+
+static int run_prox(const bsgd_epoch_args *a, const Ws &ws, cudaStream_t st) {
+    const int64_t hw = a->height * a->width;
+    ProxArgs pa = {};
+    pa.H = a->height; pa.W = a->width; pa.N = hw;
+    pa.b = ws.uimg;
+    prox_fields(pa, ws, hw);
+    pa.w = a->mu * a->lam;  // tv.py weight = mu_try * cfg.lam (solvers.py:310)
+    pa.step = 1.0 / (8.0 * pa.w);
+    pa.tol = a->tol;
+    pa.max_iters = a->max_inner_iters;
+    pa.out_img = nullptr;
+    pa.x_next = a->x_next; pa.perm = a->perm; pa.x_k = a->x_k; pa.g = a->g; pa.x_true = a->x_true;
+    pa.xpart = ws.xpart; pa.nx = ws.ctl; pa.scal = ws.scal;
+    pa.info = nullptr;
+    pa.dual = a->dual_objectives;
+    return launch_prox(pa, st);
+}
+
+static int run_tail(const bsgd_epoch_args *a, const Ws &ws, int fnext_mode, const double *fnext_dev, cudaStream_t st) {
+    TailArgs t = {};
+    t.ctl = ws.ctl; t.xpart = ws.xpart; t.rpart = ws.rpart; t.scal = ws.scal;
+    t.fnext_dev = fnext_dev;
+    t.fnext_mode = fnext_mode;
+    t.monitor = (a->flags & BSGD_EP_MONITOR) ? 1 : 0;
+    t.has_prox = a->lam > 0.0 ? 1 : 0;
+    t.mu = a->mu;
+    t.f_curr = a->f_curr;
+    t.history = a->history;
+    t.counter = a->epoch_counter;
+    t.cap = a->history_capacity;
+    tail_kernel<<<1, 32, 0, st>>>(t);
+    LAUNCHED();
+    return BSGD_OK;
+}
+
+int bsgd_epoch(const bsgd_plan *p, const bsgd_epoch_args *a, void *stream) {
+    if (!p) return fail(BSGD_EINVAL, "plan is NULL");
+    Ws ws;
+    int rc = check_epoch_args(p->cols, a, &ws);
+    if (rc) return rc;
+    const uint32_t fl = a->flags;
+    if (!(fl & BSGD_EP_SKIP_GRAD) && !a->r_k) return fail(BSGD_EINVAL, "r_k is required");
+    if ((fl & (BSGD_EP_R_NEXT | BSGD_EP_LOOKAHEAD)) && !a->y) return fail(BSGD_EINVAL, "y is required");
+    if ((fl & BSGD_EP_R_NEXT) && !a->r_next) return fail(BSGD_EINVAL, "r_next is required");
+    if ((fl & BSGD_EP_LOOKAHEAD) && !a->r_ahead) return fail(BSGD_EINVAL, "r_ahead is required");
+    DeviceGuard guard(p->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    const bool prox = a->lam > 0.0;
+    EpiStep es{a->g, a->x_k, a->mu, a->x_next, prox ? ws.uimg : nullptr, a->perm, a->x_true};
+    if (fl & BSGD_EP_SKIP_GRAD) {
+        rc = run_step(p->cols, a, ws, st);
+        if (!rc && (fl & BSGD_EP_R_NEXT))
+            rc = DISPATCH_V(p, launch_one<V>(fwd_csr<V>(p, a->x_k), p->g_fwd, EpiResid{a->y, a->r_next}, ws.rpart,
+                                              ws.ctl + 2, p->nnz, st));
+    } else if (fl & BSGD_EP_R_NEXT) {
+        // K1(x_k) and K2(r_k) read the same snapshot: one grid (solvers.py:281-290)
+        rc = DISPATCH_V(p, launch_two<V>(fwd_csr<V>(p, a->x_k), p->g_fwd, EpiResid{a->y, a->r_next}, ws.rpart, ws.ctl + 2,
+                                          p->nnz, tr_csr<V>(p, a->r_k), p->g_tr, es, ws.xpart, ws.ctl, p->nnz, st));
+    } else {
+        rc = DISPATCH_V(p, launch_one<V>(tr_csr<V>(p, a->r_k), p->g_tr, es, ws.xpart, ws.ctl, p->nnz, st));
+    }
+    if (rc) return rc;
+    if (prox) {
+        rc = run_prox(a, ws, st);
+        if (rc) return rc;
+    }
+    if (fl & BSGD_EP_LOOKAHEAD) {
+        // K1(x_next): the next epoch's residual and the Eq. 9 monitor's f_next (solvers.py:319-320)
+        rc = DISPATCH_V(p, launch_one<V>(fwd_csr<V>(p, a->x_next), p->g_fwd, EpiResid{a->y, a->r_ahead}, ws.rpart,
+                                          ws.ctl + 1, p->nnz, st));
+        if (rc) return rc;
+    }
+    if (!(fl & BSGD_EP_NO_TAIL)) return run_tail(a, ws, (fl & BSGD_EP_LOOKAHEAD) ? 1 : 0, nullptr, st);
+    return BSGD_OK;
+}
+
+int bsgd_step(int64_t cols, const bsgd_epoch_args *a, void *stream) {
+    Ws ws;
+    int rc = check_epoch_args(cols, a, &ws);
+    if (rc) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    rc = run_step(cols, a, ws, st);
+    if (rc) return rc;
+    if (a->lam > 0.0) rc = run_prox(a, ws, st);
+    return rc;
+}
+
+int bsgd_epoch_forward(const bsgd_plan *p, const double *x, const double *y, double *r_out,
+                       const bsgd_epoch_args *a, void *stream) {
+    if (!p || !x || !y || !r_out || !a || !a->workspace) return fail(BSGD_EINVAL, "NULL argument");
+    Ws ws;
+    ws_layout(a->workspace, p->cols, a->lam > 0.0 ? a->height * a->width : 0, &ws);
+    DeviceGuard guard(p->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    return DISPATCH_V(p, launch_one<V>(fwd_csr<V>(p, x), p->g_fwd, EpiResid{y, r_out}, ws.rpart, ws.ctl + 1, p->nnz, st));
+}
+
+int bsgd_epoch_reduce_forward(const bsgd_plan *p, const bsgd_epoch_args *a, double *scalars_out, void *stream) {
+    if (!p || !a || !a->workspace || !scalars_out) return fail(BSGD_EINVAL, "NULL argument");
+    Ws ws;
+    ws_layout(a->workspace, p->cols, a->lam > 0.0 ? a->height * a->width : 0, &ws);
+    sum_counted_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(ws.rpart, ws.ctl + 1, scalars_out);
+    LAUNCHED();
+    return BSGD_OK;
+}
+
+int bsgd_epoch_tail(const bsgd_plan *p, const bsgd_epoch_args *a, const double *fnext_dev, void *stream) {
+    if (!p) return fail(BSGD_EINVAL, "plan is NULL");
+    Ws ws;
+    int rc = check_epoch_args(p->cols, a, &ws);
+    if (rc) return rc;
+    if (!a->history || !a->epoch_counter) return fail(BSGD_EINVAL, "history and epoch_counter are required");
+    return run_tail(a, ws, fnext_dev ? 2 : 0, fnext_dev, (cudaStream_t)stream);
+}
+
+}  // extern "C"

@@ -1,0 +1,316 @@
+// TV proximal step: restarted dual fast gradient projection (tv.py:172-255)
+// as ONE persistent cooperative kernel per prox call.
+//
+// The FGP control flow is global: every inner iteration needs the dual value
+// phi over the whole image before it may commit (restart test, tv.py:217),
+// and the stop test needs ||c - p|| and ||c|| (tv.py:239-248).  Instead of
+// ~4 launches per iteration plus host round trips, one co-resident grid
+// loops over the iterations and meets at grid barriers:
+//
+//   A  c = proj(q + step * grad(b + w div q))          (stencil, writes c)
+//   B  phi = sum (b + w div c)^2                         (stencil, grid sum)
+//      phi > phi_prev -> A', B' from p (restart)         (uniform decision)
+//   C  q = c + beta (c - p); ||c - p||^2, ||c||^2        (grid sum); p <- c by
+//      swapping the p / c buffer pair (no copy)
+//
+// All decisions are taken redundantly by every CTA from the same fixed-order
+// sums, so they agree without another barrier.  Fields that are rewritten
+// inside the kernel are read with ld.global.cg (L2) because L1 is not
+// coherent across SMs.  Elementwise arithmetic uses explicit round-to-nearest
+// intrinsics (no FMA contraction) in the reference's operation order, so the
+// only deviation from numpy is the order of the three global sums.
+#pragma once
+
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+
+namespace bsgd {
+
+namespace cg = cooperative_groups;
+
+struct ProxArgs {
+    int64_t H, W, N;
+    const double *b;       // input image (row-major)
+    double *f[6];          // pv, ph, qv, qh, cv, ch (workspace)
+    double *red;           // [2][kMaxPartials * 4] reduction partials
+    double w, step, tol;
+    int32_t max_iters;
+    // outputs -- standalone (tv_prox) mode
+    double *out_img;       // NULL in epoch mode
+    // outputs -- epoch mode (vector order, fused statistics)
+    double *x_next;
+    const int64_t *perm;
+    const double *x_k;
+    const double *g;
+    const double *x_true;
+    double *xpart;         // [gridDim.x * 4] per-CTA statistics
+    int64_t *nx;           // number of xpart rows written
+    double *scal;          // [0] TV(final) [1] iterations [2] restarts [3] converged [4] fell_back
+    int32_t *info;         // bsgd_prox_info or NULL
+    double *dual;          // dual objectives or NULL
+};
+
+__device__ __forceinline__ double ldcg(const double *p) { return __ldcg(p); }
+
+// div p at (s, t): ((pv[s+1] - pv[s]) + ph[t+1]) - ph[t], zero outside (tv.py:124-132)
+__device__ __forceinline__ double div_at(const double *pv, const double *ph, int64_t s, int64_t t,
+                                         int64_t H, int64_t W) {
+    const int64_t o = s * W + t;
+    const double a = (s + 1 < H) ? ldcg(pv + o + W) : 0.0;
+    const double b = (s > 0) ? ldcg(pv + o) : 0.0;
+    const double c = (t + 1 < W) ? ldcg(ph + o + 1) : 0.0;
+    const double d = (t > 0) ? ldcg(ph + o) : 0.0;
+    return rn_sub(rn_add(rn_sub(a, b), c), d);
+}
+
+// u = b + w div q at (s, t)
+__device__ __forceinline__ double u_at(const ProxArgs &a, const double *qv, const double *qh, int64_t s,
+                                       int64_t t) {
+    return rn_add(__ldg(a.b + s * a.W + t), rn_mul(a.w, div_at(qv, qh, s, t, a.H, a.W)));
+}
+
+// projected gradient candidate from (qv, qh) at pixel p (tv.py:207-214)
+__device__ __forceinline__ void candidate(const ProxArgs &a, const double *qv, const double *qh, int64_t p,
+                                          double &cv, double &ch) {
+    const int64_t s = p / a.W, t = p - s * a.W;
+    const double uc = u_at(a, qv, qh, s, t);
+    const double gv = (s > 0) ? rn_sub(uc, u_at(a, qv, qh, s - 1, t)) : 0.0;
+    const double gh = (t > 0) ? rn_sub(uc, u_at(a, qv, qh, s, t - 1)) : 0.0;
+    cv = rn_add(ldcg(qv + p), rn_mul(a.step, gv));
+    ch = rn_add(ldcg(qh + p), rn_mul(a.step, gh));
+    double mag = sqrt(rn_add(rn_mul(cv, cv), rn_mul(ch, ch)));
+    mag = (mag < 1.0) ? 1.0 : mag;  // np.maximum(mag, 1): NaN propagates
+    cv = cv / mag;
+    ch = ch / mag;
+}
+
+// isotropic TV term at pixel p of image u (tv.py:149-152)
+__device__ __forceinline__ double tv_term(const double *u, int64_t p, int64_t W, bool cg_load) {
+    const int64_t s = p / W, t = p - s * W;
+    const double uc = cg_load ? ldcg(u + p) : __ldg(u + p);
+    double dv = 0.0, dh = 0.0;
+    if (s > 0) dv = rn_sub(uc, cg_load ? ldcg(u + p - W) : __ldg(u + p - W));
+    if (t > 0) dh = rn_sub(uc, cg_load ? ldcg(u + p - 1) : __ldg(u + p - 1));
+    return sqrt(rn_add(rn_mul(dv, dv), rn_mul(dh, dh)));
+}
+
+// grid-wide fixed-order sum of K values; all threads of all CTAs get the totals
+template <int K>
+__device__ __forceinline__ void grid_sum(cg::grid_group &grid, double (&v)[K], double *red, int &round,
+                                         double *sm) {
+    block_sum<K>(v, sm);
+    double *buf = red + (size_t)(round & 1) * kMaxPartials * 4;
+    if (threadIdx.x == 0)
+        for (int k = 0; k < K; ++k) buf[(size_t)blockIdx.x * K + k] = v[k];
+    grid.sync();
+    if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            double s = 0.0;
+            for (int b = lane; b < (int)gridDim.x; b += 32) s += ldcg(buf + (size_t)b * K + k);
+            s = warp_sum(s);
+            if (lane == 0) sm[k] = s;
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < K; ++k) v[k] = sm[k];
+    __syncthreads();
+    ++round;
+}
+
+__global__ void __launch_bounds__(kThreads) fgp_kernel(ProxArgs a) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ double sm[4 * (kThreads / 32)];
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
+    const int64_t N = a.N;
+    int round = 0;
+    double *pv = a.f[0], *ph = a.f[1], *qv = a.f[2], *qh = a.f[3], *cv = a.f[4], *ch = a.f[5];
+
+    // --- setup: p = q = 0, phi_prev = sum b^2 (tv.py:195-204), TV(b) for the fallback
+    double v2[2] = {0.0, 0.0};
+    for (int64_t p = tid; p < N; p += nthr) {
+        pv[p] = 0.0; ph[p] = 0.0; qv[p] = 0.0; qh[p] = 0.0;
+        const double bb = __ldg(a.b + p);
+        v2[0] += bb * bb;
+        v2[1] += tv_term(a.b, p, a.W, false);
+    }
+    grid_sum<2>(grid, v2, a.red, round, sm);
+    double phi_prev = v2[0];
+    const double tv_b = v2[1];
+    double t_mom = 1.0;
+    int iters = 0, restarts = 0, converged = 0;
+    if (tid == 0 && a.dual != nullptr) a.dual[0] = phi_prev;
+
+    for (int it = 0; it < a.max_iters; ++it) {
+        // A: candidate from q
+        for (int64_t p = tid; p < N; p += nthr) {
+            double x, y;
+            candidate(a, qv, qh, p, x, y);
+            cv[p] = x; ch[p] = y;
+        }
+        grid.sync();
+        // B: dual value of the candidate
+        double v1[1] = {0.0};
+        for (int64_t p = tid; p < N; p += nthr) {
+            const int64_t s = p / a.W, t = p - s * a.W;
+            const double r = rn_add(__ldg(a.b + p), rn_mul(a.w, div_at(cv, ch, s, t, a.H, a.W)));
+            v1[0] += r * r;
+        }
+        grid_sum<1>(grid, v1, a.red, round, sm);
+        double phi = v1[0];
+        if (phi > phi_prev) {  // restart from the last accepted point (tv.py:217-231)
+            ++restarts;
+            t_mom = 1.0;
+            for (int64_t p = tid; p < N; p += nthr) {
+                double x, y;
+                candidate(a, pv, ph, p, x, y);
+                cv[p] = x; ch[p] = y;
+            }
+            grid.sync();
+            v1[0] = 0.0;
+            for (int64_t p = tid; p < N; p += nthr) {
+                const int64_t s = p / a.W, t = p - s * a.W;
+                const double r = rn_add(__ldg(a.b + p), rn_mul(a.w, div_at(cv, ch, s, t, a.H, a.W)));
+                v1[0] += r * r;
+            }
+            grid_sum<1>(grid, v1, a.red, round, sm);
+            phi = v1[0];
+        }
+        // C: momentum commit (tv.py:233-245)
+        const double t_next = 0.5 * (1.0 + sqrt(rn_add(1.0, rn_mul(rn_mul(4.0, t_mom), t_mom))));
+        const double beta = (t_mom - 1.0) / t_next;
+        double v3[2] = {0.0, 0.0};
+        for (int64_t p = tid; p < N; p += nthr) {
+            const double c0 = ldcg(cv + p), c1 = ldcg(ch + p);
+            const double s0 = rn_sub(c0, ldcg(pv + p)), s1 = rn_sub(c1, ldcg(ph + p));
+            qv[p] = rn_add(c0, rn_mul(beta, s0));
+            qh[p] = rn_add(c1, rn_mul(beta, s1));
+            v3[0] += s0 * s0 + s1 * s1;
+            v3[1] += c0 * c0 + c1 * c1;
+        }
+        grid_sum<2>(grid, v3, a.red, round, sm);
+        double *tv_ = pv; pv = cv; cv = tv_;   // p <- c
+        double *th_ = ph; ph = ch; ch = th_;
+        phi_prev = (phi_prev < phi) ? phi_prev : phi;  // Python min(phi, phi_prev)
+        t_mom = t_next;
+        iters = it + 1;
+        if (tid == 0 && a.dual != nullptr) a.dual[it + 1] = phi_prev;
+        const double change = sqrt(v3[0]), scale = sqrt(v3[1]);
+        const double floor_scale = (1e-30 > scale) ? 1e-30 : scale;  // Python max(scale, 1e-30)
+        if (change <= a.tol * floor_scale) { converged = 1; break; }
+    }
+
+    // --- finalize: out = b + w div p, fallback to b if the primal objective is worse
+    double *tmp = cv;  // scratch pair after the swap
+    for (int64_t p = tid; p < N; p += nthr) {
+        const int64_t s = p / a.W, t = p - s * a.W;
+        tmp[p] = rn_add(__ldg(a.b + p), rn_mul(a.w, div_at(pv, ph, s, t, a.H, a.W)));
+    }
+    grid.sync();
+    double e2[2] = {0.0, 0.0};
+    for (int64_t p = tid; p < N; p += nthr) {
+        const double d = rn_sub(ldcg(tmp + p), __ldg(a.b + p));
+        e2[0] += d * d;
+        e2[1] += tv_term(tmp, p, a.W, true);
+    }
+    grid_sum<2>(grid, e2, a.red, round, sm);
+    const double two_w = 2.0 * a.w;
+    const double obj_out = rn_add(e2[0], rn_mul(two_w, e2[1]));
+    const double obj_b = rn_add(0.0, rn_mul(two_w, tv_b));
+    const int fell = obj_out > obj_b ? 1 : 0;
+
+    if (a.out_img != nullptr) {
+        for (int64_t p = tid; p < N; p += nthr) a.out_img[p] = fell ? __ldg(a.b + p) : ldcg(tmp + p);
+    } else {
+        double st[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int64_t k = tid; k < N; k += nthr) {
+            const int64_t p = (a.perm != nullptr) ? a.perm[k] : k;
+            const double xv = fell ? __ldg(a.b + p) : ldcg(tmp + p);
+            a.x_next[k] = xv;
+            const double d = rn_sub(xv, a.x_k[k]);
+            st[0] += xv * xv;
+            if (a.x_true != nullptr) {
+                const double e = xv - a.x_true[k];
+                st[1] += e * e;
+            }
+            st[2] += d * a.g[k];
+            st[3] += d * d;
+        }
+        block_sum<4>(st, sm);
+        if (threadIdx.x == 0)
+            for (int k = 0; k < 4; ++k) a.xpart[(size_t)blockIdx.x * 4 + k] = st[k];
+    }
+    if (tid == 0) {
+        if (a.scal != nullptr) {
+            a.scal[0] = fell ? tv_b : e2[1];
+            a.scal[1] = iters; a.scal[2] = restarts; a.scal[3] = converged; a.scal[4] = fell;
+        }
+        if (a.nx != nullptr) a.nx[0] = gridDim.x;
+        if (a.info != nullptr) {
+            a.info[0] = iters; a.info[1] = converged; a.info[2] = restarts; a.info[3] = fell;
+        }
+    }
+}
+
+// elementwise step for the retry path (solvers.py:307-314 with the stored g):
+// x = x_k + mu g, scattered to image order for the prox or stored with stats.
+__global__ void __launch_bounds__(kThreads) step_kernel(int64_t n, const double *xk, const double *g, double mu,
+                                                        double *xn, double *uimg, const int64_t *perm,
+                                                        const double *xtrue, double *xpart, int64_t *nx) {
+    __shared__ double sm[4 * (kThreads / 32)];
+    double st[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+        const double gg = g[k];
+        const double xo = xk[k];
+        const double xv = rn_add(xo, rn_mul(mu, gg));
+        if (uimg != nullptr) {
+            uimg[perm != nullptr ? perm[k] : k] = xv;
+        } else {
+            xn[k] = xv;
+            const double d = rn_sub(xv, xo);
+            st[0] += xv * xv;
+            if (xtrue != nullptr) { const double e = xv - xtrue[k]; st[1] += e * e; }
+            st[2] += d * gg;
+            st[3] += d * d;
+        }
+    }
+    if (uimg == nullptr) {
+        block_sum<4>(st, sm);
+        if (threadIdx.x == 0)
+            for (int k = 0; k < 4; ++k) xpart[(size_t)blockIdx.x * 4 + k] = st[k];
+        if (blockIdx.x == 0 && threadIdx.x == 0) nx[0] = gridDim.x;
+    }
+}
+
+// ---- small image kernels (tv.py:115-152) ----
+__global__ void __launch_bounds__(kThreads) tv_value_kernel(int64_t H, int64_t W, const double *u, double *part) {
+    __shared__ double sm[kThreads / 32];
+    double v[1] = {0.0};
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < H * W; p += (int64_t)gridDim.x * blockDim.x)
+        v[0] += tv_term(u, p, W, false);
+    block_sum<1>(v, sm);
+    if (threadIdx.x == 0) part[blockIdx.x] = v[0];
+}
+
+__global__ void __launch_bounds__(kThreads) gradient_kernel(int64_t H, int64_t W, const double *u, double *dv,
+                                                            double *dh) {
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < H * W; p += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t s = p / W, t = p - s * W;
+        dv[p] = s > 0 ? rn_sub(u[p], u[p - W]) : 0.0;
+        dh[p] = t > 0 ? rn_sub(u[p], u[p - 1]) : 0.0;
+    }
+}
+
+__global__ void __launch_bounds__(kThreads) divergence_kernel(int64_t H, int64_t W, const double *pv,
+                                                              const double *ph, double *out) {
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < H * W; p += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t s = p / W, t = p - s * W;
+        out[p] = div_at(pv, ph, s, t, H, W);
+    }
+}
+
+}  // namespace bsgd

@@ -1,0 +1,304 @@
+// CSR row-product kernels for the two SpMV directions of a BSGD-TV epoch.
+//
+// K1 (forward)    : r[row] = y[row] - sum_k A[row, k] x[k]       on A   (CSR)
+// K2 (transposed) : g[col] = 2 sum_k A[k, col] r[k]  (+ step)     on A^T (CSR)
+// Both are the same row-product over a CSR stream with a fused epilogue.
+//
+// Mapping: a warp owns 32/G consecutive rows per pass, G lanes per row
+// (G = 8 for short rows such as the 32-nnz random system, 32 for CT rows of
+// ~100-900 nnz).  Each lane streams a strided slice of its row's (index,
+// value) pairs with L1-bypassing evict-first loads, gathers the vector
+// through the read-only path (the vector stays L2-resident), and accumulates
+// in float64.  The in-row reduction is a fixed shuffle tree, so results are
+// deterministic run to run.
+#pragma once
+
+#include "common.cuh"
+
+namespace bsgd {
+
+// ---------------------------------------------------------------------------
+// epilogues: called once per row by the row's lane 0 with the float64 sum
+// ---------------------------------------------------------------------------
+
+struct EpiStore {  // out[row] = scale * s  (matvec / rmatvec: 1; partial gradient: 2, exact)
+    double *out;
+    double scale;
+    static constexpr int K = 0;
+    __device__ __forceinline__ void operator()(int64_t row, double s) { out[row] = scale * s; }
+    __device__ __forceinline__ void flush(double *) {}
+};
+
+struct EpiResid {  // r[row] = y[row] - s, accumulate ||r||^2  (assemble_residual, blockops.py:264-278)
+    const double *y;
+    double *r;
+    double acc = 0.0;
+    static constexpr int K = 1;
+    __device__ __forceinline__ void operator()(int64_t row, double s) {
+        const double v = rn_sub(y[row], s);
+        r[row] = v;
+        acc += v * v;
+    }
+    __device__ __forceinline__ void flush(double *v) { v[0] = acc; }
+};
+
+// g = 2 * s (solvers.py:299-303), x_new = x_k + mu * g (solvers.py:308).
+// With a prox the step is scattered into image order (tv.py:87-93) for the
+// FGP kernel; without one it is the iterate, and its epoch statistics
+// (||x||^2, ||x - x_true||^2, (x_new - x_k).g, ||x_new - x_k||^2) are fused.
+struct EpiStep {
+    double *g;
+    const double *xk;
+    double mu;
+    double *xn;            // lam == 0: iterate out
+    double *uimg;          // lam > 0: image-order step out
+    const int64_t *perm;   // NULL = identity
+    const double *xtrue;   // NULL = no relative error
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    static constexpr int K = 4;
+    __device__ __forceinline__ void operator()(int64_t col, double s) {
+        const double gg = 2.0 * s;
+        g[col] = gg;
+        const double xo = xk[col];
+        const double xv = rn_add(xo, rn_mul(mu, gg));
+        if (uimg != nullptr) {
+            uimg[perm != nullptr ? perm[col] : col] = xv;
+        } else {
+            xn[col] = xv;
+            const double d = rn_sub(xv, xo);
+            acc[0] += xv * xv;
+            if (xtrue != nullptr) {
+                const double e = xv - xtrue[col];
+                acc[1] += e * e;
+            }
+            acc[2] += d * gg;
+            acc[3] += d * d;
+        }
+    }
+    __device__ __forceinline__ void flush(double *v) {
+        v[0] = acc[0]; v[1] = acc[1]; v[2] = acc[2]; v[3] = acc[3];
+    }
+};
+
+struct EpiNone {
+    static constexpr int K = 0;
+    __device__ __forceinline__ void operator()(int64_t, double) {}
+    __device__ __forceinline__ void flush(double *) {}
+};
+
+// ---------------------------------------------------------------------------
+// one CSR operand (matrix + gathered vector)
+// ---------------------------------------------------------------------------
+template <typename V>
+struct Csr {
+    int64_t nrows;
+    const int64_t *ptr;
+    const int32_t *idx;
+    const V *val;
+    const double *vec;
+};
+
+template <typename V, int G, class Epi>
+__device__ __forceinline__ void csr_rows(const Csr<V> &A, int64_t warp_id, int64_t nwarps, Epi &epi) {
+    constexpr int RPW = 32 / G;
+    const int lane = threadIdx.x & 31;
+    const int sub = lane / G;
+    const int gl = lane % G;
+    const uint64_t pol = policy_evict_first();
+    const int32_t *__restrict__ idx = A.idx;
+    const V *__restrict__ val = A.val;
+    const double *__restrict__ vec = A.vec;
+    for (int64_t base = warp_id * RPW; base < A.nrows; base += nwarps * RPW) {
+        const int64_t row = base + sub;
+        double s = 0.0;
+        if (row < A.nrows) {
+            const int64_t beg = A.ptr[row];
+            const int64_t end = A.ptr[row + 1];
+            int64_t k = beg + gl;
+            for (; k + 3 * G < end; k += 4 * G) {
+                const int32_t c0 = ld_stream(idx + k, pol);
+                const int32_t c1 = ld_stream(idx + k + G, pol);
+                const int32_t c2 = ld_stream(idx + k + 2 * G, pol);
+                const int32_t c3 = ld_stream(idx + k + 3 * G, pol);
+                const V v0 = ld_stream(val + k, pol);
+                const V v1 = ld_stream(val + k + G, pol);
+                const V v2 = ld_stream(val + k + 2 * G, pol);
+                const V v3 = ld_stream(val + k + 3 * G, pol);
+                const double x0 = __ldg(vec + c0);
+                const double x1 = __ldg(vec + c1);
+                const double x2 = __ldg(vec + c2);
+                const double x3 = __ldg(vec + c3);
+                s = fma((double)v0, x0, s);
+                s = fma((double)v1, x1, s);
+                s = fma((double)v2, x2, s);
+                s = fma((double)v3, x3, s);
+            }
+            for (; k < end; k += G) {
+                const int32_t c0 = ld_stream(idx + k, pol);
+                const V v0 = ld_stream(val + k, pol);
+                s = fma((double)v0, __ldg(vec + c0), s);
+            }
+        }
+#pragma unroll
+        for (int off = G / 2; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+        if (gl == 0 && row < A.nrows) epi(row, s);
+    }
+}
+
+// Two independent CSR products in one grid: CTAs [0, nblkA) run part A, the
+// rest run part B (used to overlap K1(x_k) and K2(r_k), which read the same
+// snapshot, solvers.py:276-290).  Each part writes one partial per CTA.
+template <typename V, int GA, int GB, class EA, class EB>
+__global__ void __launch_bounds__(kThreads) dual_csr_kernel(Csr<V> A, EA ea, double *partA, int nblkA,
+                                                            int64_t *cntA, Csr<V> B, EB eb,
+                                                            double *partB, int64_t *cntB) {
+    __shared__ double sm[8 * (kThreads / 32)];
+    const int wpb = kThreads / 32;
+    if ((int)blockIdx.x < nblkA) {
+        const int64_t warp = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5);
+        csr_rows<V, GA>(A, warp, (int64_t)nblkA * wpb, ea);
+        if constexpr (EA::K > 0) {
+            double v[EA::K];
+            ea.flush(v);
+            block_sum<EA::K>(v, sm);
+            if (threadIdx.x == 0)
+                for (int k = 0; k < EA::K; ++k) partA[(size_t)blockIdx.x * EA::K + k] = v[k];
+        }
+        if (blockIdx.x == 0 && threadIdx.x == 0 && cntA != nullptr) cntA[0] = nblkA;
+    } else {
+        const int nblkB = gridDim.x - nblkA;
+        const int bb = blockIdx.x - nblkA;
+        const int64_t warp = (int64_t)bb * wpb + (threadIdx.x >> 5);
+        csr_rows<V, GB>(B, warp, (int64_t)nblkB * wpb, eb);
+        if constexpr (EB::K > 0) {
+            double v[EB::K];
+            eb.flush(v);
+            block_sum<EB::K>(v, sm);
+            if (threadIdx.x == 0)
+                for (int k = 0; k < EB::K; ++k) partB[(size_t)bb * EB::K + k] = v[k];
+        }
+        if (bb == 0 && threadIdx.x == 0 && cntB != nullptr) cntB[0] = nblkB;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// block-restricted products (blockops.py:207-223): rows [r0, r1) of a CSR,
+// entries with column in [c0, c1) (a contiguous run: indices are sorted).
+// out[row - r0] = sum A[row, c] vec[c - c0].  One warp per row.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int64_t lower_bound_i32(const int32_t *a, int64_t lo, int64_t hi, int64_t key) {
+    while (lo < hi) {
+        const int64_t mid = lo + ((hi - lo) >> 1);
+        if ((int64_t)a[mid] < key) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+template <typename V>
+__global__ void __launch_bounds__(kThreads) block_seg_kernel(const int64_t *ptr, const int32_t *idx,
+                                                             const V *val, int64_t r0, int64_t r1,
+                                                             int64_t c0, int64_t c1,
+                                                             const double *vec, double *out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = (int64_t)gridDim.x * (kThreads / 32);
+    for (int64_t row = r0 + (int64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5); row < r1; row += nw) {
+        int64_t lo = 0, hi = 0;
+        if (lane == 0) {
+            lo = lower_bound_i32(idx, ptr[row], ptr[row + 1], c0);
+            hi = lower_bound_i32(idx, lo, ptr[row + 1], c1);
+        }
+        lo = __shfl_sync(0xffffffffu, lo, 0);
+        hi = __shfl_sync(0xffffffffu, hi, 0);
+        double s = 0.0;
+        for (int64_t k = lo + lane; k < hi; k += 32) s = fma((double)val[k], vec[idx[k] - c0], s);
+        s = warp_sum(s);
+        if (lane == 0) out[row - r0] = s;
+    }
+}
+
+// block-selection bitmask passed by value (up to 256 blocks per side)
+struct BlockMask {
+    uint64_t w[4];
+    __host__ __device__ bool has(int64_t b) const { return (w[b >> 6] >> (b & 63)) & 1ull; }
+};
+
+__device__ __forceinline__ int64_t block_of(const int64_t *bounds, int64_t nb, int64_t x) {
+    int64_t lo = 0, hi = nb;  // largest b with bounds[b] <= x
+    while (hi - lo > 1) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (bounds[mid] <= x) lo = mid; else hi = mid;
+    }
+    return lo;
+}
+
+// Stochastic pairs (solvers.py:274-303, alpha/gamma < 1): for rows of the
+// selected row blocks, z_cache[j, row] = segment sum over column block j for
+// every selected j; then every row's r_next = y - z_cache[0] - ... (ascending j).
+template <typename V>
+__global__ void __launch_bounds__(kThreads) pair_forward_kernel(const int64_t *ptr, const int32_t *idx,
+                                                                const V *val, int64_t rows,
+                                                                const int64_t *row_bounds, int64_t M,
+                                                                const int64_t *col_bounds, int64_t N,
+                                                                BlockMask rsel, BlockMask csel,
+                                                                const double *x, const double *y,
+                                                                double *z_cache, double *r_next) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = (int64_t)gridDim.x * (kThreads / 32);
+    for (int64_t row = (int64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5); row < rows; row += nw) {
+        if (rsel.has(block_of(row_bounds, M, row))) {
+            int64_t lo = ptr[row];
+            for (int64_t j = 0; j < N; ++j) {
+                int64_t hi = 0;
+                if (lane == 0) hi = lower_bound_i32(idx, lo, ptr[row + 1], col_bounds[j + 1]);
+                hi = __shfl_sync(0xffffffffu, hi, 0);
+                if (csel.has(j)) {
+                    double s = 0.0;
+                    for (int64_t k = lo + lane; k < hi; k += 32) s = fma((double)val[k], x[idx[k]], s);
+                    s = warp_sum(s);
+                    if (lane == 0) z_cache[j * rows + row] = s;
+                }
+                lo = hi;
+            }
+        }
+        __syncwarp();
+        if (lane == 0) {
+            double acc = y[row];
+            for (int64_t j = 0; j < N; ++j) acc = rn_sub(acc, z_cache[j * rows + row]);
+            r_next[row] = acc;
+        }
+    }
+}
+
+// g[col] = 2 * sum over selected row blocks (ascending) of the A^T segment sums,
+// zero for columns of unselected column blocks (solvers.py:299-303).
+template <typename V>
+__global__ void __launch_bounds__(kThreads) pair_grad_kernel(const int64_t *tptr, const int32_t *tidx,
+                                                             const V *tval, int64_t cols,
+                                                             const int64_t *row_bounds, int64_t M,
+                                                             const int64_t *col_bounds, int64_t N,
+                                                             BlockMask rsel, BlockMask csel,
+                                                             const double *r, double *g) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = (int64_t)gridDim.x * (kThreads / 32);
+    for (int64_t col = (int64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5); col < cols; col += nw) {
+        double acc = 0.0;
+        if (csel.has(block_of(col_bounds, N, col))) {
+            int64_t lo = tptr[col];
+            for (int64_t i = 0; i < M; ++i) {
+                int64_t hi = 0;
+                if (lane == 0) hi = lower_bound_i32(tidx, lo, tptr[col + 1], row_bounds[i + 1]);
+                hi = __shfl_sync(0xffffffffu, hi, 0);
+                if (rsel.has(i)) {
+                    double s = 0.0;
+                    for (int64_t k = lo + lane; k < hi; k += 32) s = fma((double)tval[k], r[tidx[k]], s);
+                    s = warp_sum(s);
+                    acc = rn_add(acc, s);
+                }
+                lo = hi;
+            }
+        }
+        if (lane == 0) g[col] = 2.0 * acc;
+    }
+}
+
+}  // namespace bsgd

@@ -81,7 +81,10 @@ def _trace_angle(n: int, theta: float, offsets: np.ndarray):
     ct, st = math.cos(theta), math.sin(theta)
     px = offsets * ct
     py = offsets * st
-    dx, dy = -st, ct
+    # directions within 1e-12 of an axis are snapped to it, so rays that run
+    # along a grid line (cos(pi/2) = 6e-17) are traced like the exact axis case
+    dx = 0.0 if abs(st) < 1e-12 else -st
+    dy = 0.0 if abs(ct) < 1e-12 else ct
     nb = offsets.shape[0]
     t_lo = np.full(nb, -np.inf)
     t_hi = np.full(nb, np.inf)

@@ -1,0 +1,257 @@
+"""CUDA kernel parity: SpMV (K1/K2), block products, patterns, TV prox, reductions.
+
+Checked against the reference's own golden vectors (tests/golden) and the CPU
+oracle (oracle/) on the same seeded inputs.  Floating-point tolerances: the
+kernels differ from scipy only in the summation order inside a row (parallel
+float64 reduction, FMA), so products agree to ~1e-15 relative; we assert
+1e-12.  The TV prox mirrors the reference's elementwise rounding exactly and
+differs only in the order of its three global sums: outputs 1e-10, ProxInfo
+counts exact.
+"""
+
+import numpy as np
+import pytest
+from scipy import sparse
+
+from conftest import golden_csr, load_golden
+from oracle import oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+SOLVER_CASES = ["p1_ct", "p2_morton", "p3_ls", "p4_div", "p1_stoch"]
+
+
+def rel(a, b):
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    d = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / (d if d > 0 else 1.0)
+
+
+@pytest.fixture(scope="module")
+def B(cuda_ok):
+    from paper_1812_01307_b200 import blockops, metrics, spectral, tv
+    return blockops, tv, metrics, spectral
+
+
+def _op(B, z, dtype=None):
+    blockops = B[0]
+    a = golden_csr(z)
+    m, n = (int(v) for v in z["mn"])
+    return blockops.BlockOperator(a, blockops.make_partition(a.shape[0], a.shape[1], m, n), dtype=dtype)
+
+
+@pytest.mark.parametrize("case", SOLVER_CASES)
+def test_block_products_vs_reference(B, case):
+    z = load_golden(case)
+    op = _op(B, z)
+    part = op.partition
+    xv, rv = z["probe_x"], z["probe_r"]
+    for i in range(op.num_row_blocks):
+        for j in range(op.num_col_blocks):
+            zz = op.block_matvec(i, j, xv[part.col_slice(j)])
+            gg = op.block_matvec_transpose(i, j, rv[part.row_slice(i)])
+            assert rel(zz, z[f"z_{i}_{j}"]) < 1e-12
+            assert rel(gg, z[f"gh_{i}_{j}"]) < 1e-12
+            assert op.block_nnz(i, j) == int(z[f"nnz_{i}_{j}"])
+    assert rel(op.matvec(xv), z["matvec"]) < 1e-12
+    assert rel(op.rmatvec(rv), z["rmatvec"]) < 1e-12
+    assert op.matvec_units == pytest.approx(4.0, abs=0)
+
+
+@pytest.mark.parametrize("case", ["p1_ct", "p3_ls", "p2_morton"])
+def test_block_patterns_bit_exact(B, case):
+    z = load_golden(case)
+    op = _op(B, z)
+    oop = orc.OracleOperator(golden_csr(z), *(int(v) for v in z["mn"]))
+    for i in range(op.num_row_blocks):
+        for j in range(op.num_col_blocks):
+            got, ref = op.block(i, j), oop.block_csr(i, j)
+            assert got.shape == ref.shape
+            assert np.array_equal(got.indptr, ref.indptr)
+            assert np.array_equal(got.indices, ref.indices)
+            assert np.array_equal(got.data, ref.data)
+    indptr, indices, values = op.transpose_pattern()
+    at = sparse.csr_array(golden_csr(z).T)
+    at.sort_indices()
+    assert np.array_equal(indptr, at.indptr) and np.array_equal(indices, at.indices)
+    assert np.array_equal(values, at.data)
+
+
+def test_float32_values_match_float64_products(B):
+    z = load_golden("p3_ls")  # values are float32-representable
+    op32 = _op(B, z, dtype=np.float32)
+    op64 = _op(B, z, dtype=np.float64)
+    assert op32.value_dtype == np.float32
+    x = z["probe_x"]
+    assert rel(op32.matvec(x), op64.matvec(x)) < 1e-14
+    assert rel(op32.rmatvec(z["probe_r"]), z["rmatvec"]) < 1e-12
+
+
+def test_device_tensors_in_and_out(B):
+    import torch
+    z = load_golden("p1_ct")
+    op = _op(B, z)
+    xt = torch.tensor(z["probe_x"], device="cuda")
+    out = op.matvec(xt)
+    assert isinstance(out, torch.Tensor) and out.is_cuda
+    assert rel(out.cpu().numpy(), z["matvec"]) < 1e-12
+
+
+def test_product_validation_errors(B):
+    z = load_golden("p1_ct")
+    op = _op(B, z)
+    with pytest.raises(ValueError):
+        op.block_matvec(0, 0, np.zeros(3))
+    with pytest.raises(ValueError):
+        op.matvec(np.zeros(5))
+    with pytest.raises(ValueError):
+        B[0].BlockOperator(sparse.csr_array((3, 3)))
+    with pytest.raises(ValueError, match="partition covers"):
+        B[0].BlockOperator(golden_csr(z), B[0].make_partition(5, 5, 1, 1))
+
+
+def test_assemble_residual(B):
+    blockops = B[0]
+    rng = np.random.default_rng(0)
+    y = rng.standard_normal(37)
+    zc = rng.standard_normal((5, 37))
+    assert np.array_equal(blockops.assemble_residual(y, zc), orc.assemble_residual(y, zc))
+    assert np.array_equal(blockops.assemble_residual(y, np.zeros((3, 37))), y)
+    assert np.array_equal(blockops.assemble_residual(y, y[None, :]), np.zeros(37))
+    with pytest.raises(ValueError):
+        blockops.assemble_residual(y, np.zeros((2, 36)))
+
+
+def test_empty_rows_and_empty_blocks(B):
+    blockops = B[0]
+    # block-diagonal with empty rows: off-diagonal blocks have nnz 0
+    d = sparse.block_diag([sparse.random(30, 20, 0.2, random_state=1), sparse.random(30, 20, 0.2, random_state=2)])
+    a = sparse.csr_array(d)
+    a = sparse.csr_array(a.multiply(np.arange(60)[:, None] % 7 != 0))  # force empty rows
+    op = blockops.BlockOperator(a, blockops.make_partition(60, 40, 2, 2))
+    oop = orc.OracleOperator(a, 2, 2)
+    assert op.block_nnz(0, 1) == 0 and op.block_nnz(1, 0) == 0
+    x = np.random.default_rng(1).standard_normal(40)
+    w = np.random.default_rng(2).standard_normal(60)
+    assert rel(op.matvec(x), oop.matvec(x)) < 1e-12
+    assert rel(op.rmatvec(w), oop.rmatvec(w)) < 1e-12
+    assert np.array_equal(op.block_matvec(0, 1, x[20:]), np.zeros(30))
+    assert op.block(0, 1).nnz == 0
+
+
+@pytest.mark.parametrize("scale", [0.05, 1.0])
+def test_c1_geometry_products_vs_oracle(B, scale):
+    from paper_1812_01307_b200 import problems
+    d = problems.config(0, scale=scale)
+    blockops = B[0]
+    op = blockops.BlockOperator(d.matrix, blockops.make_partition(*d.shape, 4, 4))
+    oop = orc.OracleOperator(d.matrix, 4, 4)
+    x = d.x_true
+    w = np.random.default_rng(5).standard_normal(d.shape[0])
+    assert rel(op.matvec(x), oop.matvec(x)) < 1e-12
+    assert rel(op.rmatvec(w), oop.rmatvec(w)) < 1e-12
+    for (i, j) in [(0, 0), (1, 3), (3, 2)]:
+        r0, r1 = op.partition.row_range(i)
+        c0, c1 = op.partition.col_range(j)
+        assert rel(op.block_matvec(i, j, x[c0:c1]), oop.block_matvec(i, j, x[c0:c1])) < 1e-12
+        assert rel(op.block_matvec_transpose(i, j, w[r0:r1]), oop.block_matvec_transpose(i, j, w[r0:r1])) < 1e-12
+
+
+def test_c2_full_size_adjoint_and_linearity(B):
+    """Full configs[1] size (2e6 x 5e5, 6.4e7 nnz): size-independent properties."""
+    from paper_1812_01307_b200 import problems
+    blockops = B[0]
+    a = problems.random_sparse_system(2_000_000, 500_000, 32, 2)
+    op = blockops.BlockOperator(a, blockops.make_partition(*a.shape, 8, 8))
+    rng = np.random.default_rng(9)
+    x, x2 = rng.standard_normal(500_000), rng.standard_normal(500_000)
+    w = rng.standard_normal(2_000_000)
+    ax, atw = op.matvec(x), op.rmatvec(w)
+    assert abs(ax @ w - x @ atw) <= 1e-12 * np.linalg.norm(ax) * np.linalg.norm(w)
+    lin = op.matvec(2.5 * x - x2)
+    assert rel(lin, 2.5 * ax - op.matvec(x2)) < 1e-13
+    # spot-check sampled blocks against the oracle restatement
+    oop = orc.OracleOperator(a, 8, 8, threads=8)
+    for (i, j) in [(0, 0), (7, 3)]:
+        c0, c1 = op.partition.col_range(j)
+        assert rel(op.block_matvec(i, j, x[c0:c1]), oop.block_matvec(i, j, x[c0:c1])) < 1e-12
+
+
+# --- TV -------------------------------------------------------------------------
+
+def test_tv_prox_vs_reference_golden(B):
+    tv = B[1]
+    z = load_golden("prox")
+    for k in range(int(z["count"])):
+        w, mi, tol = z[f"par{k}"]
+        out, info = tv.tv_prox(tv.ImageGrid.from_matrix(z[f"in{k}"]), float(w),
+                               tv.ProxSettings(int(mi), float(tol)), return_info=True)
+        ref = z[f"out{k}"]
+        assert rel(out.as_matrix(), ref) < 1e-10, k
+        assert [info.iterations, int(info.converged), info.restarts, int(info.fell_back)] == list(z[f"info{k}"]), k
+        if float(w) > 0:
+            assert np.allclose(info.dual_objectives, z[f"dual{k}"], rtol=1e-11, atol=0), k
+        assert tv.tv_value(out) == pytest.approx(float(z[f"tv{k}"][1]), rel=1e-12, abs=1e-12)
+
+
+@pytest.mark.parametrize("shape,w", [((64, 64), 1e-3), ((64, 64), 0.05), ((37, 101), 0.2), ((200, 3), 1.0),
+                                     ((256, 256), 0.01)])
+def test_tv_prox_vs_oracle_random(B, shape, w):
+    tv = B[1]
+    img = np.random.default_rng(sum(shape)).random(shape) * 2.0
+    out, info = tv.tv_prox(tv.ImageGrid.from_matrix(img), w, tv.ProxSettings(20, 1e-12), return_info=True)
+    ref, rep = orc.tv_prox(img, w, 20, 1e-12)
+    assert rel(out.as_matrix(), ref) < 1e-9
+    assert (info.iterations, info.restarts, info.fell_back) == (rep.iterations, rep.restarts, rep.fell_back)
+
+
+def test_tv_prox_edge_cases(B):
+    tv = B[1]
+    img = tv.ImageGrid.from_matrix(np.random.default_rng(0).random((5, 6)))
+    same, info = tv.tv_prox(img, 0.0, return_info=True)
+    assert np.array_equal(same.data, img.data) and info.converged and info.iterations == 0
+    const = tv.ImageGrid.from_matrix(np.full((7, 7), 5.0))
+    assert np.array_equal(tv.tv_prox(const, 0.7).data, const.data)
+    with pytest.raises(ValueError):
+        tv.tv_prox(img, -1.0)
+    one = tv.ImageGrid.from_matrix(np.array([[3.0]]))
+    assert np.array_equal(tv.tv_prox(one, 1.0).data, one.data)
+
+
+def test_tv_value_and_difference_operators(B):
+    tv = B[1]
+    z = load_golden("prox")
+    assert tv.tv_value(tv.ImageGrid.from_matrix(np.array([[0.0, 1.0], [1.0, 1.0]]))) == float(z["tv_2x2"])
+    assert tv.tv_value(tv.ImageGrid.from_matrix(np.array([[0.0, 3.0]]))) == 3.0
+    assert tv.tv_value(tv.ImageGrid.from_matrix(np.full((4, 5), 2.0))) == 0.0
+    gv, gh = tv.discrete_gradient(tv.ImageGrid.from_matrix(z["adj_u"]))
+    assert np.array_equal(gv, z["adj_gv"]) and np.array_equal(gh, z["adj_gh"])
+    dv = tv.discrete_divergence(z["adj_pv"], z["adj_ph"]).as_matrix()
+    assert np.array_equal(dv, z["adj_div"])
+    u = np.random.default_rng(4).random((9, 11))
+    a = 3.7
+    assert tv.tv_value(tv.ImageGrid.from_matrix(a * u)) == pytest.approx(a * tv.tv_value(tv.ImageGrid.from_matrix(u)),
+                                                                         rel=1e-12)
+
+
+def test_metrics_and_spectral(B):
+    blockops, tv, metrics, spectral = B
+    z = load_golden("p1_ct")
+    op = _op(B, z)
+    e = load_golden("p1_eig")
+    res = spectral.largest_eigenvalue(op, max_iters=50)
+    assert res.iterations == int(e["iterations"]) and res.converged == bool(int(e["converged"]))
+    assert res.value == pytest.approx(float(e["value"]), rel=1e-10)
+    x = z["final_x"]
+    oop = orc.OracleOperator(golden_csr(z), 4, 5)
+    assert metrics.relative_error(x, z["x_true"]) == pytest.approx(orc.relative_error(x, z["x_true"]), rel=1e-12)
+    lay = tv.PixelLayout.row_major(24, 24)
+    got = metrics.objective_value(x, op, z["y"], 5.0, lay)
+    assert got == pytest.approx(orc.objective_value(x, oop, z["y"], 5.0, lay.perm, (24, 24)), rel=1e-12)
+    with pytest.raises(ValueError):
+        metrics.relative_error(x, np.zeros_like(x))
+    sb = spectral.step_bound(9.0)
+    assert sb.mu_sup == 1.0 / 18 and sb.admits(0.05) and not sb.admits(1 / 18)
+    v1, v2 = spectral.iteration_eigenvalues(1.0, 0.5)
+    assert abs(abs(v1) - 1.0) < 1e-12 and abs(abs(v2) - 1.0) < 1e-12

@@ -1,0 +1,197 @@
+"""Epoch- and run-level parity of the CUDA path with the reference (golden) and the oracle.
+
+North-star tolerances: x within relative L2 1e-4 of the reference after the
+stated epoch count and objective within 1e-5 relative.  With float64 vectors
+the CUDA path is far tighter; the fp64 golden cases assert 1e-9 so a
+regression shows long before the north-star bar is at risk.
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+from conftest import golden_cfg, golden_csr, load_golden
+from oracle import oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+X_TOL = 1e-4      # north star: relative L2 of x
+OBJ_TOL = 1e-5    # north star: relative objective
+
+
+def rel(a, b):
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    d = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / (d if d > 0 else 1.0)
+
+
+@pytest.fixture(scope="module")
+def S(cuda_ok):
+    from paper_1812_01307_b200 import blockops, solvers, tv
+    return blockops, solvers, tv
+
+
+def _setup(S, z):
+    blockops, solvers, tv = S
+    a = golden_csr(z)
+    m, n = (int(v) for v in z["mn"])
+    op = blockops.BlockOperator(a, blockops.make_partition(a.shape[0], a.shape[1], m, n))
+    c = golden_cfg(z)
+    cfg = solvers.SolverConfig(mu=c["mu"], lam=c["lam"], alpha=c["alpha"], gamma=c["gamma"], epochs=c["epochs"],
+                               seed=c["seed"], prox=tv.ProxSettings(c["max_inner_iters"], c["tol"]),
+                               monitor_decrease=c["monitor_decrease"], enforce_decrease=c["enforce_decrease"],
+                               max_halvings=c["max_halvings"], divergence_limit=c["divergence_limit"])
+    layout = None
+    if "perm" in z:
+        h, w = (int(v) for v in z["hw"])
+        layout = tv.PixelLayout(h, w, z["perm"])
+    return op, cfg, layout, c
+
+
+@pytest.mark.parametrize("case", ["p1_ct", "p2_morton", "p3_ls", "p4_div", "p1_stoch"])
+def test_epochs_vs_reference(S, case):
+    _, solvers, _ = S
+    z = load_golden(case)
+    op, cfg, layout, _ = _setup(S, z)
+    st = solvers.init_bsgd_state(op, z["y"], cfg)
+    for e in range(3):
+        solvers.bsgd_tv_iteration(st, op, z["y"], cfg, layout=layout)
+        assert rel(st.x, z[f"ep{e}_x"]) < 1e-9, (case, e)
+        assert rel(st.r_vec, z[f"ep{e}_r"]) < 1e-9, (case, e)
+        assert rel(st.g, z[f"ep{e}_g"]) < 1e-9, (case, e)
+        f, mu, ep, ok = z[f"ep{e}_scalars"]
+        assert st.f_curr == pytest.approx(f, rel=1e-10)
+        assert st.mu_eff == mu and st.epoch == ep
+        assert (-1 if st.last_decrease_ok is None else int(st.last_decrease_ok)) == int(ok)
+
+
+@pytest.mark.parametrize("case", ["p1_ct", "p2_morton", "p3_ls", "p1_stoch"])
+@pytest.mark.parametrize("graphs", [True, False])
+def test_run_solver_vs_reference(S, case, graphs):
+    _, solvers, _ = S
+    z = load_golden(case)
+    op, cfg, layout, c = _setup(S, z)
+    op._nnz_applied = int(z["applied0"])
+    prob = solvers.Problem(op=op, y=z["y"], x_true=z["x_true"], layout=layout)
+    tr = solvers.run_solver("bsgd", prob, cfg, sample_every=c["sample_every"], use_graphs=graphs)
+    got = np.array([tuple(s) for s in tr.samples])
+    ref = z["samples"]
+    assert got.shape == ref.shape
+    assert np.array_equal(got[:, 0], ref[:, 0])                  # epochs
+    assert np.array_equal(got[:, 3], ref[:, 3])                  # matvec units, exact bookkeeping
+    assert np.allclose(got[:, 1], ref[:, 1], rtol=1e-9, atol=0)  # relative error
+    assert np.allclose(got[:, 2], ref[:, 2], rtol=1e-9, atol=0)  # objective
+    assert [int(f) for f in tr.decrease_flags] == list(z["flags"])
+    assert rel(tr.final_x, z["final_x"]) < 1e-9
+
+
+def test_divergence_vs_reference(S):
+    _, solvers, _ = S
+    z = load_golden("p4_div")
+    op, cfg, layout, c = _setup(S, z)
+    op._nnz_applied = int(z["applied0"])
+    prob = solvers.Problem(op=op, y=z["y"], x_true=z["x_true"], layout=layout)
+    with pytest.raises(solvers.DivergenceError) as ei:
+        solvers.run_solver("bsgd", prob, cfg, sample_every=c["sample_every"])
+    msg = bytes(z["message"]).decode()
+    assert str(ei.value).split(" left")[1] == msg.split(" left")[1]   # same epoch
+    got = np.array([tuple(s) for s in ei.value.trace.samples])
+    assert got.shape == z["samples"].shape
+    assert np.allclose(got, z["samples"], rtol=1e-9)
+    assert ei.value.trace.final_x is None
+
+
+def test_run_solver_argument_errors(S):
+    blockops, solvers, tv = S
+    z = load_golden("p3_ls")
+    op, cfg, layout, _ = _setup(S, z)
+    prob = solvers.Problem(op=op, y=z["y"])
+    with pytest.raises(ValueError):
+        solvers.run_solver("nope", prob, cfg)
+    with pytest.raises(ValueError):
+        solvers.run_solver("bsgd", prob, cfg, sample_every=0)
+    with pytest.raises(ValueError):
+        solvers.run_solver("bsgd", prob, cfg, workers=0)
+    with pytest.raises(ValueError, match="layout"):
+        solvers.run_solver("bsgd", prob, solvers.SolverConfig(mu=cfg.mu, lam=0.1))
+    tr = solvers.run_solver("bsgd", prob, solvers.SolverConfig(mu=cfg.mu, epochs=0))
+    assert len(tr.samples) == 1 and tr.samples[0].epoch == 0.0 and math.isnan(tr.samples[0].relative_error)
+
+
+def test_host_state_roundtrip_matches_device_state(S):
+    """The e2e usage (numpy state in and out every epoch) equals the resident path."""
+    _, solvers, _ = S
+    z = load_golden("p1_ct")
+    op, cfg, layout, _ = _setup(S, z)
+    a = solvers.init_bsgd_state(op, z["y"], cfg)
+    b = solvers.init_bsgd_state(op, z["y"], cfg)
+    for _ in range(4):
+        solvers.bsgd_tv_iteration(a, op, z["y"], cfg, layout=layout)
+        x, r = b.x, b.r_vec
+        b.x, b.r_vec = x, r
+        solvers.bsgd_tv_iteration(b, op, z["y"], cfg, layout=layout)
+    assert rel(a.x, b.x) < 1e-13 and rel(a.r_vec, b.r_vec) < 1e-13
+    # z cache of a full sweep = block products of the previous iterate
+    zc = a.z_cache
+    assert zc.shape == (op.num_col_blocks, op.shape[0])
+    assert rel(zc.sum(axis=0), z["y"] - a.r_vec) < 1e-12
+
+
+def _oracle_run(d, m, n, lam, epochs, mu, max_inner=20, monitor=True):
+    oop = orc.OracleOperator(d.matrix, m, n)
+    prm = orc.Params(mu=mu, lam=lam, epochs=epochs, max_inner_iters=max_inner, tol=1e-5,
+                     monitor_decrease=monitor)
+    perm = np.arange(d.height * d.width) if lam > 0 else None
+    return orc.run_bsgd(oop, d.y, prm, x_true=d.x_true, perm=perm, hw=(d.height, d.width), sample_every=10)
+
+
+@pytest.mark.parametrize("cfg_index,scale,epochs", [(0, 1.0, 100), (1, 0.02, 200), (2, 0.25, 30)])
+def test_config_runs_vs_oracle(S, cfg_index, scale, epochs):
+    """configs[0] at full size, configs[1]/[2] scaled: the north-star bar on the stated epochs."""
+    blockops, solvers, tv = S
+    from paper_1812_01307_b200 import problems, spectral
+    d = problems.config(cfg_index, scale=scale)
+    m = d.num_row_blocks
+    op = blockops.BlockOperator(d.matrix, blockops.make_partition(*d.shape, m, m))
+    u = spectral.largest_eigenvalue(op, max_iters=50).value
+    mu = 0.9 / (2.0 * u)
+    lam = d.lam
+    layout = tv.PixelLayout.row_major(d.height, d.width) if lam > 0 else None
+    cfg = solvers.SolverConfig(mu=mu, lam=lam, epochs=epochs, prox=tv.ProxSettings(d.max_inner_iters, 1e-5))
+    tr = solvers.run_solver("bsgd", solvers.Problem(op, d.y, d.x_true, layout), cfg, sample_every=10)
+    ref = _oracle_run(d, m, m, lam, epochs, mu, d.max_inner_iters)
+    assert rel(tr.final_x, ref.final_x) < X_TOL
+    got = np.array([tuple(s) for s in tr.samples])
+    want = np.array(ref.samples)
+    assert np.allclose(got[:, 2], want[:, 2], rtol=OBJ_TOL)
+    assert np.array_equal(got[:, 3], want[:, 3])
+
+
+def test_deterministic_bitwise(S):
+    blockops, solvers, tv = S
+    z = load_golden("p1_ct")
+    outs = []
+    for _ in range(2):
+        op, cfg, layout, c = _setup(S, z)
+        tr = solvers.run_solver("bsgd", solvers.Problem(op, z["y"], z["x_true"], layout), cfg)
+        outs.append((tr.final_x, tr.to_csv_string()))
+    assert np.array_equal(outs[0][0], outs[1][0]) and outs[0][1] == outs[1][1]
+
+
+def test_c2_full_size_convergence(S):
+    """configs[1] at full size: 200 epochs drive x to x_true (noise-free, consistent system)."""
+    blockops, solvers, tv = S
+    from paper_1812_01307_b200 import problems, spectral
+    d = problems.config(1)
+    op = blockops.BlockOperator(d.matrix, blockops.make_partition(*d.shape, 8, 8))
+    u = spectral.largest_eigenvalue(op, max_iters=50).value
+    assert 8.5 < u < 10.0
+    cfg = solvers.SolverConfig(mu=0.9 / (2 * u), epochs=200)
+    tr = solvers.run_solver("bsgd", solvers.Problem(op, d.y, d.x_true), cfg, sample_every=50)
+    errs = tr.relative_errors()
+    assert errs[0] == 1.0 and np.all(np.diff(errs) < 0)
+    assert errs[-1] < 1e-3
+    # 2 charged units per epoch + 1 per earlier sample (0, 50, 100, 150)
+    assert tr.matvec_units()[-1] == 2 * 200 + 4
