@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(kThreads) dual_csr_kernel(Csr<V> A, EA ea, dou
             double v[EA::K];
             ea.flush(v);
             block_sum<EA::K>(v, sm);
-            if (threadIdx.x == 0)
+            if (threadIdx.x == 0 && partA != nullptr)
                 for (int k = 0; k < EA::K; ++k) partA[(size_t)blockIdx.x * EA::K + k] = v[k];
         }
         if (blockIdx.x == 0 && threadIdx.x == 0 && cntA != nullptr) cntA[0] = nblkA;
@@ -174,7 +174,7 @@ __global__ void __launch_bounds__(kThreads) dual_csr_kernel(Csr<V> A, EA ea, dou
             double v[EB::K];
             eb.flush(v);
             block_sum<EB::K>(v, sm);
-            if (threadIdx.x == 0)
+            if (threadIdx.x == 0 && partB != nullptr)
                 for (int k = 0; k < EB::K; ++k) partB[(size_t)bb * EB::K + k] = v[k];
         }
         if (bb == 0 && threadIdx.x == 0 && cntB != nullptr) cntB[0] = nblkB;
