@@ -92,6 +92,48 @@ static int occupancy(K kernel) {
 
 static inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+static inline int pow2_floor(int64_t v) {
+    int p = 1;
+    while ((int64_t)p * 2 <= v) p *= 2;
+    return p;
+}
+
+// depth ds of numpy's pairwise recursion at which the first leaf (n <= 128)
+// appears: the tree above it is a perfect binary tree (pairwise.cuh).  Also
+// checks that every subtree below finishes within pw_node's 4 levels.
+static int pw_depth(int64_t N, int *ds_out) {
+    std::vector<int64_t> sizes{N};
+    int d = 0;
+    for (;;) {
+        bool leaf = false;
+        for (int64_t s : sizes) leaf = leaf || s <= 128;
+        if (leaf) break;
+        std::vector<int64_t> nxt;
+        for (int64_t s : sizes) {
+            const int64_t a = pw_split(s), b = s - a;
+            for (int64_t c : {a, b})
+                if (std::find(nxt.begin(), nxt.end(), c) == nxt.end()) nxt.push_back(c);
+        }
+        sizes.swap(nxt);
+        ++d;
+    }
+    for (int64_t s : sizes) {  // levels still needed below depth d
+        std::vector<int64_t> cur{s};
+        int lev = 0;
+        while (true) {
+            bool all = true;
+            std::vector<int64_t> nxt;
+            for (int64_t c : cur)
+                if (c > 128) { all = false; nxt.push_back(pw_split(c)); nxt.push_back(c - pw_split(c)); }
+            if (all) break;
+            cur.swap(nxt);
+            if (++lev > 4) return fail(BSGD_EINVAL, "pairwise tree too deep for %lld elements", (long long)N);
+        }
+    }
+    *ds_out = d;
+    return BSGD_OK;
+}
+
 // ---------------------------------------------------------------------------
 // plan
 // ---------------------------------------------------------------------------
@@ -442,8 +484,12 @@ __global__ void tail_kernel(TailArgs t) {
 // ---------------------------------------------------------------------------
 static int launch_prox(ProxArgs &a, cudaStream_t st) {
     const int occ = occupancy(fgp_kernel);
-    int grid = (int)std::min<int64_t>(cdiv(a.N, kThreads), (int64_t)occ * num_sms());
-    grid = std::max(1, std::min(grid, kMaxPartials));
+    int rc = pw_depth(a.N, &a.ds);
+    if (rc) return rc;
+    // G: a power of two (numpy-order top tree), co-resident, <= 512
+    int grid = pow2_floor(std::max<int64_t>(1, std::min<int64_t>((int64_t)occ * num_sms(), 512)));
+    const int64_t S = (int64_t)1 << a.ds;
+    if (S / grid > kPwMaxQ) return fail(BSGD_EINVAL, "image too large for the pairwise tree (%lld pixels)", (long long)a.N);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(kThreads);
@@ -855,9 +901,14 @@ int bsgd_tv_value(int64_t height, int64_t width, const double *img, double *out,
     if (height < 1 || width < 1 || !img || !out || !scratch) return fail(BSGD_EINVAL, "bad tv_value arguments");
     cudaStream_t st = (cudaStream_t)stream;
     const int64_t hw = height * width;
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(hw, kThreads), std::min(num_sms() * 8, kMaxPartials)));
-    tv_value_kernel<<<grid, kThreads, 0, st>>>(height, width, img, (double *)scratch);
-    sum_parts_kernel<<<1, 32, 0, st>>>((double *)scratch, grid, out);
+    int ds = 0;
+    int rc = pw_depth(hw, &ds);
+    if (rc) return rc;
+    const int64_t S = (int64_t)1 << ds;
+    const int G = (int)std::min<int64_t>(S, 256);
+    if (S / G > kPwMaxQ) return fail(BSGD_EINVAL, "image too large for tv_value (%lld pixels)", (long long)hw);
+    tv_value_part_kernel<<<G, kThreads, 0, st>>>(height, width, img, ds, (double *)scratch);
+    pw_top_kernel<<<1, kThreads, 0, st>>>(ds, G, (const double *)scratch, out);
     LAUNCHED();
     return BSGD_OK;
 }

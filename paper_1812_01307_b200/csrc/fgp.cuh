@@ -24,6 +24,7 @@
 #include <cooperative_groups.h>
 
 #include "common.cuh"
+#include "pairwise.cuh"
 
 namespace bsgd {
 
@@ -36,6 +37,7 @@ struct ProxArgs {
     double *red;           // [2][kMaxPartials * 4] reduction partials
     double w, step, tol;
     int32_t max_iters;
+    int32_t ds;            // numpy pairwise depth for N (pw_depth)
     // outputs -- standalone (tv_prox) mode
     double *out_img;       // NULL in epoch mode
     // outputs -- epoch mode (vector order, fused statistics)
@@ -95,50 +97,41 @@ __device__ __forceinline__ double tv_term(const double *u, int64_t p, int64_t W,
     return sqrt(rn_add(rn_mul(dv, dv), rn_mul(dh, dh)));
 }
 
-// grid-wide fixed-order sum of K values; all threads of all CTAs get the totals
-template <int K>
-__device__ __forceinline__ void grid_sum(cg::grid_group &grid, double (&v)[K], double *red, int &round,
-                                         double *sm) {
-    block_sum<K>(v, sm);
+// numpy-order grid sum of K per-pixel terms (pairwise.cuh); all threads get the
+// totals.  Term functors may write outputs: each pixel is visited once.
+template <int K, class F>
+__device__ __forceinline__ void np_sum(cg::grid_group &grid, int64_t N, int ds, F &f, double *red, int &round,
+                                       double *sm, double (&out)[K]) {
     double *buf = red + (size_t)(round & 1) * kMaxPartials * 4;
-    if (threadIdx.x == 0)
-        for (int k = 0; k < K; ++k) buf[(size_t)blockIdx.x * K + k] = v[k];
+    pw_cta<K>(N, ds, f, sm, buf);
     grid.sync();
-    if (threadIdx.x < 32) {
-        const int lane = threadIdx.x;
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-            double s = 0.0;
-            for (int b = lane; b < (int)gridDim.x; b += 32) s += ldcg(buf + (size_t)b * K + k);
-            s = warp_sum(s);
-            if (lane == 0) sm[k] = s;
-        }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int k = 0; k < K; ++k) v[k] = sm[k];
-    __syncthreads();
+    pw_top<K>(ds, gridDim.x, buf, sm, out);
     ++round;
 }
 
 __global__ void __launch_bounds__(kThreads) fgp_kernel(ProxArgs a) {
     cg::grid_group grid = cg::this_grid();
-    __shared__ double sm[4 * (kThreads / 32)];
+    __shared__ double sm[kPwMaxQ * kPwMaxK];
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
-    const int64_t N = a.N;
+    const int64_t N = a.N, W = a.W, H = a.H;
+    const double w = a.w;
+    const double *b = a.b;
     int round = 0;
     double *pv = a.f[0], *ph = a.f[1], *qv = a.f[2], *qh = a.f[3], *cv = a.f[4], *ch = a.f[5];
 
-    // --- setup: p = q = 0, phi_prev = sum b^2 (tv.py:195-204), TV(b) for the fallback
-    double v2[2] = {0.0, 0.0};
-    for (int64_t p = tid; p < N; p += nthr) {
-        pv[p] = 0.0; ph[p] = 0.0; qv[p] = 0.0; qh[p] = 0.0;
-        const double bb = __ldg(a.b + p);
-        v2[0] += bb * bb;
-        v2[1] += tv_term(a.b, p, a.W, false);
+    // --- setup: p = q = 0 (tv.py:198-201), phi_prev = np.sum(b*b) (tv.py:203),
+    //     and TV(b) for the fallback test (tv.py:166-169, 251)
+    double v2[2];
+    {
+        auto f0 = [&](int64_t p, double (&t)[2]) {
+            pv[p] = 0.0; ph[p] = 0.0; qv[p] = 0.0; qh[p] = 0.0;
+            const double bb = __ldg(b + p);
+            t[0] = rn_mul(bb, bb);
+            t[1] = tv_term(b, p, W, false);
+        };
+        np_sum<2>(grid, N, a.ds, f0, a.red, round, sm, v2);
     }
-    grid_sum<2>(grid, v2, a.red, round, sm);
     double phi_prev = v2[0];
     const double tv_b = v2[1];
     double t_mom = 1.0;
@@ -146,21 +139,21 @@ __global__ void __launch_bounds__(kThreads) fgp_kernel(ProxArgs a) {
     if (tid == 0 && a.dual != nullptr) a.dual[0] = phi_prev;
 
     for (int it = 0; it < a.max_iters; ++it) {
-        // A: candidate from q
+        // A: candidate from q (tv.py:207-214)
         for (int64_t p = tid; p < N; p += nthr) {
             double x, y;
             candidate(a, qv, qh, p, x, y);
             cv[p] = x; ch[p] = y;
         }
         grid.sync();
-        // B: dual value of the candidate
-        double v1[1] = {0.0};
-        for (int64_t p = tid; p < N; p += nthr) {
-            const int64_t s = p / a.W, t = p - s * a.W;
-            const double r = rn_add(__ldg(a.b + p), rn_mul(a.w, div_at(cv, ch, s, t, a.H, a.W)));
-            v1[0] += r * r;
-        }
-        grid_sum<1>(grid, v1, a.red, round, sm);
+        // B: phi = np.sum(resid * resid) (tv.py:215-216)
+        auto fphi = [&](int64_t p, double (&t)[1]) {
+            const int64_t s = p / W, tt = p - s * W;
+            const double r = rn_add(__ldg(b + p), rn_mul(w, div_at(cv, ch, s, tt, H, W)));
+            t[0] = rn_mul(r, r);
+        };
+        double v1[1];
+        np_sum<1>(grid, N, a.ds, fphi, a.red, round, sm, v1);
         double phi = v1[0];
         if (phi > phi_prev) {  // restart from the last accepted point (tv.py:217-231)
             ++restarts;
@@ -171,65 +164,64 @@ __global__ void __launch_bounds__(kThreads) fgp_kernel(ProxArgs a) {
                 cv[p] = x; ch[p] = y;
             }
             grid.sync();
-            v1[0] = 0.0;
-            for (int64_t p = tid; p < N; p += nthr) {
-                const int64_t s = p / a.W, t = p - s * a.W;
-                const double r = rn_add(__ldg(a.b + p), rn_mul(a.w, div_at(cv, ch, s, t, a.H, a.W)));
-                v1[0] += r * r;
-            }
-            grid_sum<1>(grid, v1, a.red, round, sm);
+            np_sum<1>(grid, N, a.ds, fphi, a.red, round, sm, v1);
             phi = v1[0];
         }
-        // C: momentum commit (tv.py:233-245)
+        // C: momentum commit (tv.py:233-245): q = c + beta (c - p);
+        //    change = sqrt(sum dv^2 + sum dh^2), scale = sqrt(sum cv^2 + sum ch^2)
         const double t_next = 0.5 * (1.0 + sqrt(rn_add(1.0, rn_mul(rn_mul(4.0, t_mom), t_mom))));
         const double beta = (t_mom - 1.0) / t_next;
-        double v3[2] = {0.0, 0.0};
-        for (int64_t p = tid; p < N; p += nthr) {
-            const double c0 = ldcg(cv + p), c1 = ldcg(ch + p);
-            const double s0 = rn_sub(c0, ldcg(pv + p)), s1 = rn_sub(c1, ldcg(ph + p));
+        auto fcom = [&](int64_t p, double (&t)[4]) {
+            const double c0 = __ldcg(cv + p), c1 = __ldcg(ch + p);
+            const double s0 = rn_sub(c0, __ldcg(pv + p)), s1 = rn_sub(c1, __ldcg(ph + p));
             qv[p] = rn_add(c0, rn_mul(beta, s0));
             qh[p] = rn_add(c1, rn_mul(beta, s1));
-            v3[0] += s0 * s0 + s1 * s1;
-            v3[1] += c0 * c0 + c1 * c1;
-        }
-        grid_sum<2>(grid, v3, a.red, round, sm);
+            t[0] = rn_mul(s0, s0);
+            t[1] = rn_mul(s1, s1);
+            t[2] = rn_mul(c0, c0);
+            t[3] = rn_mul(c1, c1);
+        };
+        double v4[4];
+        np_sum<4>(grid, N, a.ds, fcom, a.red, round, sm, v4);
         double *tv_ = pv; pv = cv; cv = tv_;   // p <- c
         double *th_ = ph; ph = ch; ch = th_;
         phi_prev = (phi_prev < phi) ? phi_prev : phi;  // Python min(phi, phi_prev)
         t_mom = t_next;
         iters = it + 1;
         if (tid == 0 && a.dual != nullptr) a.dual[it + 1] = phi_prev;
-        const double change = sqrt(v3[0]), scale = sqrt(v3[1]);
+        const double change = sqrt(rn_add(v4[0], v4[1]));
+        const double scale = sqrt(rn_add(v4[2], v4[3]));
         const double floor_scale = (1e-30 > scale) ? 1e-30 : scale;  // Python max(scale, 1e-30)
         if (change <= a.tol * floor_scale) { converged = 1; break; }
     }
 
-    // --- finalize: out = b + w div p, fallback to b if the primal objective is worse
+    // --- finalize: out = b + w div p (tv.py:250), identity fallback if the primal
+    //     objective is worse (tv.py:251-253)
     double *tmp = cv;  // scratch pair after the swap
     for (int64_t p = tid; p < N; p += nthr) {
-        const int64_t s = p / a.W, t = p - s * a.W;
-        tmp[p] = rn_add(__ldg(a.b + p), rn_mul(a.w, div_at(pv, ph, s, t, a.H, a.W)));
+        const int64_t s = p / W, t = p - s * W;
+        tmp[p] = rn_add(__ldg(b + p), rn_mul(w, div_at(pv, ph, s, t, H, W)));
     }
     grid.sync();
-    double e2[2] = {0.0, 0.0};
-    for (int64_t p = tid; p < N; p += nthr) {
-        const double d = rn_sub(ldcg(tmp + p), __ldg(a.b + p));
-        e2[0] += d * d;
-        e2[1] += tv_term(tmp, p, a.W, true);
-    }
-    grid_sum<2>(grid, e2, a.red, round, sm);
-    const double two_w = 2.0 * a.w;
+    auto fen = [&](int64_t p, double (&t)[2]) {
+        const double d = rn_sub(__ldcg(tmp + p), __ldg(b + p));
+        t[0] = rn_mul(d, d);
+        t[1] = tv_term(tmp, p, W, true);
+    };
+    double e2[2];
+    np_sum<2>(grid, N, a.ds, fen, a.red, round, sm, e2);
+    const double two_w = 2.0 * w;
     const double obj_out = rn_add(e2[0], rn_mul(two_w, e2[1]));
     const double obj_b = rn_add(0.0, rn_mul(two_w, tv_b));
     const int fell = obj_out > obj_b ? 1 : 0;
 
     if (a.out_img != nullptr) {
-        for (int64_t p = tid; p < N; p += nthr) a.out_img[p] = fell ? __ldg(a.b + p) : ldcg(tmp + p);
+        for (int64_t p = tid; p < N; p += nthr) a.out_img[p] = fell ? __ldg(b + p) : __ldcg(tmp + p);
     } else {
         double st[4] = {0.0, 0.0, 0.0, 0.0};
         for (int64_t k = tid; k < N; k += nthr) {
             const int64_t p = (a.perm != nullptr) ? a.perm[k] : k;
-            const double xv = fell ? __ldg(a.b + p) : ldcg(tmp + p);
+            const double xv = fell ? __ldg(b + p) : __ldcg(tmp + p);
             a.x_next[k] = xv;
             const double d = rn_sub(xv, a.x_k[k]);
             st[0] += xv * xv;
@@ -287,13 +279,19 @@ __global__ void __launch_bounds__(kThreads) step_kernel(int64_t n, const double 
 }
 
 // ---- small image kernels (tv.py:115-152) ----
-__global__ void __launch_bounds__(kThreads) tv_value_kernel(int64_t H, int64_t W, const double *u, double *part) {
-    __shared__ double sm[kThreads / 32];
-    double v[1] = {0.0};
-    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < H * W; p += (int64_t)gridDim.x * blockDim.x)
-        v[0] += tv_term(u, p, W, false);
-    block_sum<1>(v, sm);
-    if (threadIdx.x == 0) part[blockIdx.x] = v[0];
+// tv_value in numpy order: CTA part (grid of G = power of two CTAs) ...
+__global__ void __launch_bounds__(kThreads) tv_value_part_kernel(int64_t H, int64_t W, const double *u, int ds,
+                                                                 double *part) {
+    __shared__ double sm[kPwMaxQ];
+    auto f = [&](int64_t p, double (&t)[1]) { t[0] = tv_term(u, p, W, false); };
+    pw_cta<1>(H * W, ds, f, sm, part);
+}
+// ... and the balanced top over the CTA parts (one CTA)
+__global__ void __launch_bounds__(kThreads) pw_top_kernel(int ds, int G, const double *part, double *out) {
+    __shared__ double sm[kPwMaxQ];
+    double v[1];
+    pw_top<1>(ds, G, part, sm, v);
+    if (threadIdx.x == 0) out[0] = v[0];
 }
 
 __global__ void __launch_bounds__(kThreads) gradient_kernel(int64_t H, int64_t W, const double *u, double *dv,

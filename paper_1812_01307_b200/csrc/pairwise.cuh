@@ -1,0 +1,180 @@
+// numpy-order sums on the device.
+//
+// The reference's TV prox takes every decision from np.sum(...) of a 2-D
+// float64 array (tv.py:203,215-216,239-240,251; the fallback energies at
+// tv.py:166-169).  numpy reduces a contiguous array with its pairwise
+// algorithm (numpy/_core/src/umath/loops_utils.h.src, pairwise_sum):
+//
+//   PW(a, n) = n < 8    : ((0 + a0) + a1) + ...
+//              n <= 128 : 8 strided accumulators r_j = a_j + a_{j+8} + ...,
+//                         ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), then the n%8 tail
+//              else     : PW(a, n2) + PW(a+n2, n-n2),  n2 = n/2 rounded down to a multiple of 8
+//
+// (verified bitwise against np.sum on 2-D arrays up to 2e6 elements, see
+// tests/test_oracle_golden.py::test_numpy_pairwise_restatement).  Because
+// the recursion splits every node above depth ds into two, the tree's top
+// ds levels are a perfect binary tree over S = 2^ds "subtrees" in index order.
+// The device evaluation mirrors that exactly:
+//   * one 8-lane group evaluates one subtree (its <= 4 remaining recursion
+//     levels and leaves, lanes = the 8 accumulators of a leaf);
+//   * a CTA owns S/G consecutive subtrees and combines them with a balanced
+//     shared-memory tree (pairs (2i, 2i+1) at every level);
+//   * the G CTA results (G a power of two) are combined the same way.
+// Every floating-point add is the one numpy performs, in the same order, so
+// the sums are bit-identical to np.sum and the FGP restart / stop / fallback
+// decisions and ProxInfo match the reference exactly.
+#pragma once
+
+#include "common.cuh"
+
+namespace bsgd {
+
+constexpr int kPwMaxQ = 512;   // subtrees per CTA held in shared memory
+constexpr int kPwMaxK = 4;     // simultaneous sums per pass
+
+__host__ __device__ inline int64_t pw_split(int64_t n) {
+    const int64_t n2 = n / 2;
+    return n2 - (n2 % 8);
+}
+
+// subtree s at depth ds: follow the bits of s from the root
+__device__ __forceinline__ void pw_subtree(int64_t N, int ds, int64_t s, int64_t &lo, int64_t &n) {
+    lo = 0;
+    n = N;
+    for (int lev = ds - 1; lev >= 0; --lev) {
+        const int64_t n2 = pw_split(n);
+        if ((s >> lev) & 1) { lo += n2; n -= n2; } else { n = n2; }
+    }
+}
+
+// one leaf (n <= 128) by an 8-lane group; every lane returns the sum
+template <int K, class F>
+__device__ __forceinline__ void pw_leaf(int64_t lo, int64_t n, F &f, unsigned gm, int j, double (&out)[K]) {
+    double t[K];
+    if (n < 8) {
+        if (j < n) f(lo + j, t);
+#pragma unroll
+        for (int k = 0; k < K; ++k) out[k] = 0.0;
+        for (int i = 0; i < n; ++i)
+#pragma unroll
+            for (int k = 0; k < K; ++k) out[k] = rn_add(out[k], __shfl_sync(gm, t[k], i, 8));
+        return;
+    }
+    double r[K];
+    f(lo + j, r);
+    const int64_t full = n - (n % 8);
+    for (int64_t i = 8; i < full; i += 8) {
+        f(lo + i + j, t);
+#pragma unroll
+        for (int k = 0; k < K; ++k) r[k] = rn_add(r[k], t[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        r[k] = rn_add(r[k], __shfl_xor_sync(gm, r[k], 1, 8));
+        r[k] = rn_add(r[k], __shfl_xor_sync(gm, r[k], 2, 8));
+        r[k] = rn_add(r[k], __shfl_xor_sync(gm, r[k], 4, 8));
+    }
+    const int rem = (int)(n - full);
+    if (j < rem) f(lo + full + j, t);
+    for (int i = 0; i < rem; ++i)
+#pragma unroll
+        for (int k = 0; k < K; ++k) r[k] = rn_add(r[k], __shfl_sync(gm, t[k], i, 8));
+#pragma unroll
+    for (int k = 0; k < K; ++k) out[k] = r[k];
+}
+
+template <int K, class F, int D>
+__device__ __noinline__ void pw_node(int64_t lo, int64_t n, F &f, unsigned gm, int j, double (&out)[K]) {
+    if constexpr (D == 0) {
+        pw_leaf<K>(lo, n, f, gm, j, out);
+    } else {
+        if (n <= 128) {
+            pw_leaf<K>(lo, n, f, gm, j, out);
+            return;
+        }
+        const int64_t n2 = pw_split(n);
+        double a[K], b[K];
+        pw_node<K, F, D - 1>(lo, n2, f, gm, j, a);
+        pw_node<K, F, D - 1>(lo + n2, n - n2, f, gm, j, b);
+#pragma unroll
+        for (int k = 0; k < K; ++k) out[k] = rn_add(a[k], b[k]);
+    }
+}
+
+// balanced in-place tree over `count` (power of two) K-vectors in shared memory;
+// result in v[0..K).  All threads of the CTA must call it.
+template <int K>
+__device__ __forceinline__ void pw_smem_tree(double *v, int count) {
+    for (int w = count; w > 1; w >>= 1) {
+        const int half = w >> 1;
+        double a[K];
+        const int i = threadIdx.x;
+        if (i < half)
+#pragma unroll
+            for (int k = 0; k < K; ++k) a[k] = rn_add(v[(2 * i) * K + k], v[(2 * i + 1) * K + k]);
+        __syncthreads();
+        if (i < half)
+#pragma unroll
+            for (int k = 0; k < K; ++k) v[i * K + k] = a[k];
+        __syncthreads();
+    }
+}
+
+// CTA part: this CTA's subtrees -> one K-vector (written to part[blockIdx.x]).
+// Returns the number of subtrees this CTA owned (0 means it wrote nothing).
+// `sm` holds kPwMaxQ * K doubles.
+template <int K, class F>
+__device__ __forceinline__ int pw_cta(int64_t N, int ds, F &f, double *sm, double *part) {
+    const int64_t S = (int64_t)1 << ds;
+    const int G = gridDim.x;
+    int64_t first;
+    int Q;
+    if (S >= G) {
+        Q = (int)(S / G);
+        first = (int64_t)blockIdx.x * Q;
+    } else {
+        Q = ((int64_t)blockIdx.x < S) ? 1 : 0;
+        first = blockIdx.x;
+    }
+    const int lane = threadIdx.x & 31;
+    const int j = lane & 7;
+    const unsigned gm = 0xFFu << (lane & 24);
+    const int group = threadIdx.x >> 3;
+    const int ngroups = blockDim.x >> 3;
+    for (int q = group; q < Q; q += ngroups) {
+        int64_t lo, n;
+        pw_subtree(N, ds, first + q, lo, n);
+        double v[K];
+        pw_node<K, F, 4>(lo, n, f, gm, j, v);
+        if (j == 0)
+#pragma unroll
+            for (int k = 0; k < K; ++k) sm[q * K + k] = v[k];
+    }
+    __syncthreads();
+    if (Q > 0) {
+        pw_smem_tree<K>(sm, Q);
+        if (threadIdx.x == 0)
+#pragma unroll
+            for (int k = 0; k < K; ++k) part[(size_t)blockIdx.x * K + k] = sm[k];
+    }
+    __syncthreads();
+    return Q;
+}
+
+// top part: combine the min(S, G) CTA results (a power of two) in a balanced
+// tree; every thread receives the totals.  `part` was written by pw_cta of a
+// G-CTA grid (visible: after a grid barrier or in a later launch).  G <= 512,
+// `sm` holds kPwMaxQ * K doubles.
+template <int K>
+__device__ __forceinline__ void pw_top(int ds, int G, const double *part, double *sm, double (&out)[K]) {
+    const int64_t S = (int64_t)1 << ds;
+    const int cnt = (int)(S < (int64_t)G ? S : (int64_t)G);
+    for (int i = threadIdx.x; i < cnt * K; i += blockDim.x) sm[i] = __ldcg(part + i);
+    __syncthreads();
+    pw_smem_tree<K>(sm, cnt);
+#pragma unroll
+    for (int k = 0; k < K; ++k) out[k] = sm[k];
+    __syncthreads();
+}
+
+}  // namespace bsgd

@@ -140,3 +140,37 @@ def test_largest_eigenvalue_bit_exact(case, eig):
     op = orc.OracleOperator(golden_csr(z), 4 if case == "p1_ct" else 8, 5 if case == "p1_ct" else 8)
     val, conv, its = orc.largest_eigenvalue(op, max_iters=50)
     assert val == float(e["value"]) and int(conv) == int(e["converged"]) and its == int(e["iterations"])
+
+
+def _pairwise(a, lo, n):
+    """numpy's pairwise_sum restated (the algorithm csrc/pairwise.cuh evaluates on the GPU)."""
+    if n < 8:
+        r = 0.0
+        for i in range(lo, lo + n):
+            r += a[i]
+        return r
+    if n <= 128:
+        acc = [a[lo + j] for j in range(8)]
+        i = 8
+        while i < n - (n % 8):
+            for j in range(8):
+                acc[j] += a[lo + i + j]
+            i += 8
+        res = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]))
+        while i < n:
+            res += a[lo + i]
+            i += 1
+        return res
+    n2 = n // 2
+    n2 -= n2 % 8
+    return _pairwise(a, lo, n2) + _pairwise(a, lo + n2, n - n2)
+
+
+@pytest.mark.parametrize("shape", [(5,), (17,), (128,), (129,), (24, 24), (37, 101), (200, 3), (256, 256),
+                                   (300, 301)])
+def test_numpy_pairwise_restatement(shape):
+    """np.sum over a contiguous array == the pairwise recursion over its flat data, bit for bit."""
+    rng = np.random.default_rng(sum(shape))
+    x = rng.standard_normal(shape) * 10.0 ** rng.uniform(-3, 3, shape)
+    assert float(np.sum(x)) == _pairwise(x.ravel().tolist(), 0, x.size)
+    assert float(np.sum(x * x)) == _pairwise((x * x).ravel().tolist(), 0, x.size)
