@@ -17,11 +17,14 @@
 #include <vector>
 
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+#include <cstdlib>
 
 #include "../../include/bsgd_b200.h"
 #include "common.cuh"
 #include "fgp.cuh"
 #include "spmv.cuh"
+#include "tiled.cuh"
 
 using namespace bsgd;
 
@@ -152,6 +155,20 @@ struct bsgd_plan {
     int64_t *d_row_bounds = nullptr, *d_col_bounds = nullptr;
     int g_fwd = 32, g_tr = 32;
     size_t device_bytes = 0;
+    // panel-tiled copies of A and A^T (tiled.cuh); used when built and enabled
+    struct TiledStore {
+        bool ok = false;
+        int R = 0, P = 0, NG = 0, NP = 0;
+        int64_t nrows = 0, ncols = 0;
+        uint32_t *keys = nullptr;
+        void *vals = nullptr;
+        uint64_t *unit_start = nullptr;
+        uint32_t *unit_len = nullptr, *unit_rc = nullptr, *tile_unit = nullptr;
+        uint16_t *rc_off = nullptr;
+        size_t bytes = 0;
+        int clusters = 0;  // co-resident clusters of kTileCL CTAs
+    } tf, tt;
+    bool use_tiled = true;
 };
 
 struct DeviceGuard {
@@ -227,9 +244,17 @@ __global__ void block_nnz_kernel(int64_t rows, const int64_t *ptr, const int32_t
     }
 }
 
+static void tiled_free(bsgd_plan::TiledStore &t) {
+    cudaFree(t.keys); cudaFree(t.vals); cudaFree(t.unit_start); cudaFree(t.unit_len);
+    cudaFree(t.unit_rc); cudaFree(t.tile_unit); cudaFree(t.rc_off);
+    t = bsgd_plan::TiledStore();
+}
+
 static void plan_free(bsgd_plan *p) {
     if (!p) return;
     DeviceGuard g(p->device);
+    tiled_free(p->tf);
+    tiled_free(p->tt);
     cudaFree(p->f_ptr); cudaFree(p->f_idx); cudaFree(p->f_val);
     cudaFree(p->t_ptr); cudaFree(p->t_idx); cudaFree(p->t_val);
     cudaFree(p->d_row_bounds); cudaFree(p->d_col_bounds);
@@ -282,6 +307,177 @@ static int build_transpose(bsgd_plan *p, cudaStream_t st) {
 #undef TRY
     cleanup();
     return BSGD_OK;
+}
+
+
+// ---------------------------------------------------------------------------
+// panel-tiled format (tiled.cuh)
+// ---------------------------------------------------------------------------
+static void choose_tiling(int64_t nrows, int64_t ncols, int &R, int &P) {
+    P = (int)std::min<int64_t>(8192, (ncols + 1) & ~(int64_t)1);
+    if (P < 2) P = 2;
+    const int64_t ctas = (int64_t)(num_sms() / kTileCL) * kTileCL;
+    R = 256;
+    for (int r : {4096, 2048, 1024, 512, 256}) {
+        if (cdiv(nrows, r) >= (ctas * 4) / 5) { R = r; break; }
+    }
+}
+
+template <typename V>
+static int build_tiled(bsgd_plan::TiledStore &T, int64_t nrows, int64_t ncols, int64_t nnz, const int64_t *ptr,
+                       const int32_t *idx, const V *val, cudaStream_t st) {
+    constexpr int CH = TileCfg<V>::CH;
+    choose_tiling(nrows, ncols, T.R, T.P);
+    T.nrows = nrows; T.ncols = ncols;
+    T.NG = (int)cdiv(nrows, T.R);
+    T.NP = (int)cdiv(ncols, T.P);
+    const int64_t ntiles = (int64_t)T.NG * T.NP;
+    if (ntiles >= ((int64_t)1 << 32) || nnz >= ((int64_t)1 << 32)) return BSGD_OK;  // not eligible
+    int32_t *rowid = nullptr;
+    uint32_t *tkey = nullptr, *packed = nullptr, *pos = nullptr, *skey = nullptr, *perm = nullptr;
+    uint32_t *n_rc = nullptr, *n_unit = nullptr, *rc_base = nullptr, *unit_base = nullptr;
+    uint64_t *tile_ptr = nullptr;
+    int *d_bad = nullptr;
+    void *temp = nullptr;
+    size_t temp_bytes = 0;
+    int rc = BSGD_OK;
+    auto cleanup = [&]() {
+        cudaFree(rowid); cudaFree(tkey); cudaFree(packed); cudaFree(pos); cudaFree(skey); cudaFree(perm);
+        cudaFree(n_rc); cudaFree(n_unit); cudaFree(rc_base); cudaFree(unit_base); cudaFree(tile_ptr);
+        cudaFree(d_bad); cudaFree(temp);
+    };
+#define TTRY(call)                                                                          \
+    do {                                                                                    \
+        cudaError_t e_ = (call);                                                            \
+        if (e_ != cudaSuccess) {                                                            \
+            rc = fail(e_ == cudaErrorMemoryAllocation ? BSGD_ENOMEM : BSGD_ECUDA,           \
+                      "tiled build: %s failed: %s", #call, cudaGetErrorString(e_));         \
+            cleanup();                                                                      \
+            tiled_free(T);                                                                  \
+            return rc;                                                                      \
+        }                                                                                   \
+    } while (0)
+    TTRY(cudaMalloc(&rowid, sizeof(int32_t) * nnz));
+    TTRY(cudaMalloc(&tkey, sizeof(uint32_t) * nnz));
+    TTRY(cudaMalloc(&packed, sizeof(uint32_t) * nnz));
+    TTRY(cudaMalloc(&pos, sizeof(uint32_t) * nnz));
+    TTRY(cudaMalloc(&skey, sizeof(uint32_t) * nnz));
+    TTRY(cudaMalloc(&perm, sizeof(uint32_t) * nnz));
+    TTRY(cudaMalloc(&T.keys, sizeof(uint32_t) * (nnz + 8)));
+    TTRY(cudaMalloc(&T.vals, sizeof(V) * (nnz + 8)));
+    TTRY(cudaMemsetAsync(T.keys, 0, sizeof(uint32_t) * (nnz + 8), st));
+    TTRY(cudaMemsetAsync(T.vals, 0, sizeof(V) * (nnz + 8), st));
+    expand_rows_kernel<<<grid_1d(nrows), kThreads, 0, st>>>(nrows, ptr, rowid);
+    tile_keys_kernel<<<grid_1d(nnz), kThreads, 0, st>>>(nnz, rowid, idx, T.R, T.P, T.NP, tkey, packed, pos);
+    TTRY(cudaGetLastError());
+    int end_bit = 1;
+    while (end_bit < 32 && ((int64_t)1 << end_bit) <= ntiles) ++end_bit;
+    TTRY(cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, tkey, skey, pos, perm, nnz, 0, end_bit, st));
+    TTRY(cudaMalloc(&temp, temp_bytes));
+    TTRY(cub::DeviceRadixSort::SortPairs(temp, temp_bytes, tkey, skey, pos, perm, nnz, 0, end_bit, st));
+    tile_gather_kernel<V><<<grid_1d(nnz), kThreads, 0, st>>>(nnz, perm, packed, val, T.keys, (V *)T.vals);
+    TTRY(cudaMalloc(&tile_ptr, sizeof(uint64_t) * (ntiles + 1)));
+    tile_ptr_kernel<<<grid_1d(ntiles + 1), kThreads, 0, st>>>(ntiles, nnz, skey, tile_ptr);
+    TTRY(cudaGetLastError());
+    TTRY(cudaMalloc(&n_rc, sizeof(uint32_t) * ntiles));
+    TTRY(cudaMalloc(&n_unit, sizeof(uint32_t) * ntiles));
+    TTRY(cudaMalloc(&rc_base, sizeof(uint32_t) * ntiles));
+    TTRY(cudaMalloc(&unit_base, sizeof(uint32_t) * ntiles));
+    TTRY(cudaMalloc(&d_bad, sizeof(int)));
+    TTRY(cudaMemsetAsync(d_bad, 0, sizeof(int), st));
+    tile_segment_kernel<CH><<<grid_1d(ntiles, 64), 64, 0, st>>>(ntiles, tile_ptr, T.keys, 0, n_rc, n_unit, nullptr,
+                                                                 nullptr, nullptr, nullptr, nullptr, nullptr, d_bad);
+    TTRY(cudaGetLastError());
+    size_t scan_bytes = 0;
+    TTRY(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, n_rc, rc_base, ntiles, st));
+    if (scan_bytes > temp_bytes) {
+        TTRY(cudaFree(temp));
+        temp = nullptr;
+        TTRY(cudaMalloc(&temp, scan_bytes));
+        temp_bytes = scan_bytes;
+    }
+    TTRY(cub::DeviceScan::ExclusiveSum(temp, temp_bytes, n_rc, rc_base, ntiles, st));
+    TTRY(cub::DeviceScan::ExclusiveSum(temp, temp_bytes, n_unit, unit_base, ntiles, st));
+    uint32_t last[4] = {0, 0, 0, 0};
+    int bad = 0;
+    TTRY(cudaMemcpyAsync(&last[0], rc_base + ntiles - 1, 4, cudaMemcpyDeviceToHost, st));
+    TTRY(cudaMemcpyAsync(&last[1], n_rc + ntiles - 1, 4, cudaMemcpyDeviceToHost, st));
+    TTRY(cudaMemcpyAsync(&last[2], unit_base + ntiles - 1, 4, cudaMemcpyDeviceToHost, st));
+    TTRY(cudaMemcpyAsync(&last[3], n_unit + ntiles - 1, 4, cudaMemcpyDeviceToHost, st));
+    TTRY(cudaMemcpyAsync(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+    TTRY(cudaStreamSynchronize(st));
+    if (bad) {  // a row has more than CH entries in one tile: keep the CSR kernels
+        cleanup();
+        tiled_free(T);
+        return BSGD_OK;
+    }
+    const uint32_t total_rc = last[0] + last[1], total_units = last[2] + last[3];
+    TTRY(cudaMalloc(&T.unit_start, sizeof(uint64_t) * (total_units + 1)));
+    TTRY(cudaMalloc(&T.unit_len, sizeof(uint32_t) * (total_units + 1)));
+    TTRY(cudaMalloc(&T.unit_rc, sizeof(uint32_t) * (total_units + 1)));
+    TTRY(cudaMalloc(&T.rc_off, sizeof(uint16_t) * (total_rc + 1)));
+    TTRY(cudaMalloc(&T.tile_unit, sizeof(uint32_t) * (ntiles + 1)));
+    tile_segment_kernel<CH><<<grid_1d(ntiles, 64), 64, 0, st>>>(ntiles, tile_ptr, T.keys, 1, n_rc, n_unit, rc_base,
+                                                                 unit_base, T.unit_start, T.unit_len, T.unit_rc,
+                                                                 T.rc_off, d_bad);
+    tile_finish_kernel<<<grid_1d(ntiles + 1), kThreads, 0, st>>>(ntiles, n_unit, unit_base, total_units, total_rc,
+                                                                 T.tile_unit, T.unit_rc);
+    TTRY(cudaGetLastError());
+    TTRY(cudaStreamSynchronize(st));
+#undef TTRY
+    cleanup();
+    T.bytes = (sizeof(uint32_t) + sizeof(V)) * (nnz + 8) + 16 * (size_t)(total_units + 1) +
+              2 * (size_t)(total_rc + 1) + 4 * (size_t)(ntiles + 1);
+    // launch configuration: 1 CTA per SM, clusters of kTileCL
+    auto kern = tile_spmv_kernel<V, EpiStore>;
+    const size_t smem = TileSmem<V>::bytes(T.R, T.P);
+    cudaFuncSetAttribute(tile_spmv_kernel<V, EpiStore>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(tile_spmv_kernel<V, EpiResid>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(tile_spmv_kernel<V, EpiStep>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(kTileCL * (num_sms() / kTileCL));
+    cfg.blockDim = dim3(kTileThreads);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = kTileCL; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int nclusters = 0;
+    cudaError_t e = cudaOccupancyMaxActiveClusters(&nclusters, kern, &cfg);
+    if (e != cudaSuccess || nclusters < 1) {
+        cudaGetLastError();
+        tiled_free(T);
+        return BSGD_OK;
+    }
+    T.clusters = std::min(nclusters, num_sms() / kTileCL);
+    T.ok = true;
+    return BSGD_OK;
+}
+
+template <typename V, class E>
+static int launch_tiled(const bsgd_plan::TiledStore &S, const double *vec, const E &e, double *part, int64_t *cnt,
+                        cudaStream_t st) {
+    Tiled<V> T;
+    T.nrows = S.nrows; T.ncols = S.ncols; T.R = S.R; T.P = S.P; T.NG = S.NG; T.NP = S.NP;
+    T.keys = S.keys; T.vals = (const V *)S.vals; T.unit_start = S.unit_start; T.unit_len = S.unit_len;
+    T.unit_rc = S.unit_rc; T.rc_off = S.rc_off; T.tile_unit = S.tile_unit; T.vec = vec;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(kTileCL * S.clusters);
+    cfg.blockDim = dim3(kTileThreads);
+    cfg.dynamicSmemBytes = TileSmem<V>::bytes(S.R, S.P);
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = kTileCL; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    CU(cudaLaunchKernelEx(&cfg, tile_spmv_kernel<V, E>, T, e, part, cnt));
+    return BSGD_OK;
+}
+
+static bool tiled_usable(const bsgd_plan *p, const bsgd_plan::TiledStore &S, const double *vec) {
+    return p->use_tiled && S.ok && (((uintptr_t)vec) & 15) == 0;
 }
 
 // ---------------------------------------------------------------------------
@@ -344,6 +540,18 @@ static int launch_two(const Csr<V> &A, int GA, const EA &ea, double *partA, int6
     if (GB == 8)
         return launch_dual<V, 32, 8, EA, EB>(A, ea, partA, cntA, nnzA, B, eb, partB, cntB, nnzB, st);
     return launch_dual<V, 32, 32, EA, EB>(A, ea, partA, cntA, nnzA, B, eb, partB, cntB, nnzB, st);
+}
+
+template <typename V, class E>
+static int launch_fwd(const bsgd_plan *p, const double *vec, const E &e, double *part, int64_t *cnt, cudaStream_t st) {
+    if (tiled_usable(p, p->tf, vec)) return launch_tiled<V>(p->tf, vec, e, part, cnt, st);
+    return launch_one<V>(fwd_csr<V>(p, vec), p->g_fwd, e, part, cnt, p->nnz, st);
+}
+
+template <typename V, class E>
+static int launch_tr(const bsgd_plan *p, const double *vec, const E &e, double *part, int64_t *cnt, cudaStream_t st) {
+    if (tiled_usable(p, p->tt, vec)) return launch_tiled<V>(p->tt, vec, e, part, cnt, st);
+    return launch_one<V>(tr_csr<V>(p, vec), p->g_tr, e, part, cnt, p->nnz, st);
 }
 
 #define DISPATCH_V(p, ...)                                          \
@@ -610,6 +818,21 @@ int bsgd_plan_create(bsgd_plan **out, int device, int64_t rows, int64_t cols, in
     }
     rc = (value_dtype == BSGD_F32) ? build_transpose<float>(p, st) : build_transpose<double>(p, st);
     if (rc != BSGD_OK) { plan_free(p); return rc; }
+    {
+        const char *env = getenv("BSGD_TILED");
+        p->use_tiled = !(env && env[0] == '0');
+    }
+    if (p->use_tiled) {
+        if (value_dtype == BSGD_F32) {
+            rc = build_tiled<float>(p->tf, rows, cols, nnz, p->f_ptr, p->f_idx, (const float *)p->f_val, st);
+            if (!rc) rc = build_tiled<float>(p->tt, cols, rows, nnz, p->t_ptr, p->t_idx, (const float *)p->t_val, st);
+        } else {
+            rc = build_tiled<double>(p->tf, rows, cols, nnz, p->f_ptr, p->f_idx, (const double *)p->f_val, st);
+            if (!rc) rc = build_tiled<double>(p->tt, cols, rows, nnz, p->t_ptr, p->t_idx, (const double *)p->t_val, st);
+        }
+        if (rc != BSGD_OK) { plan_free(p); return rc; }
+        p->device_bytes += p->tf.bytes + p->tt.bytes;
+    }
     // block nnz table (blockops.py:179-180)
     unsigned long long *d_cnt = nullptr;
     const int64_t nb = num_row_blocks * num_col_blocks;
@@ -752,21 +975,21 @@ int bsgd_matvec(const bsgd_plan *p, const double *x, double *out, void *stream) 
     if (!p || !x || !out) return fail(BSGD_EINVAL, "NULL argument");
     DeviceGuard guard(p->device);
     cudaStream_t st = (cudaStream_t)stream;
-    return DISPATCH_V(p, launch_one<V>(fwd_csr<V>(p, x), p->g_fwd, EpiStore{out, 1.0}, nullptr, nullptr, p->nnz, st));
+    return DISPATCH_V(p, launch_fwd<V>(p, x, EpiStore{out, 1.0}, nullptr, nullptr, st));
 }
 
 int bsgd_rmatvec(const bsgd_plan *p, const double *w, double *out, void *stream) {
     if (!p || !w || !out) return fail(BSGD_EINVAL, "NULL argument");
     DeviceGuard guard(p->device);
     cudaStream_t st = (cudaStream_t)stream;
-    return DISPATCH_V(p, launch_one<V>(tr_csr<V>(p, w), p->g_tr, EpiStore{out, 1.0}, nullptr, nullptr, p->nnz, st));
+    return DISPATCH_V(p, launch_tr<V>(p, w, EpiStore{out, 1.0}, nullptr, nullptr, st));
 }
 
 int bsgd_grad(const bsgd_plan *p, const double *r, double *g, void *stream) {
     if (!p || !r || !g) return fail(BSGD_EINVAL, "NULL argument");
     DeviceGuard guard(p->device);
     cudaStream_t st = (cudaStream_t)stream;
-    return DISPATCH_V(p, launch_one<V>(tr_csr<V>(p, r), p->g_tr, EpiStore{g, 2.0}, nullptr, nullptr, p->nnz, st));
+    return DISPATCH_V(p, launch_tr<V>(p, r, EpiStore{g, 2.0}, nullptr, nullptr, st));
 }
 
 int bsgd_residual(const bsgd_plan *p, const double *x, const double *y, double *r_out, double *sumsq_out,
@@ -778,7 +1001,7 @@ int bsgd_residual(const bsgd_plan *p, const double *x, const double *y, double *
     double *part = sumsq_out ? (double *)scratch : nullptr;
     int64_t *cnt = sumsq_out ? (int64_t *)((char *)scratch + sizeof(double) * kMaxPartials) : nullptr;
     EpiResid e{y, r_out};
-    int rc = DISPATCH_V(p, launch_one<V>(fwd_csr<V>(p, x), p->g_fwd, e, part, cnt, p->nnz, st));
+    int rc = DISPATCH_V(p, launch_fwd<V>(p, x, e, part, cnt, st));
     if (rc) return rc;
     if (sumsq_out) {
         sum_counted_kernel<<<1, 32, 0, st>>>(part, cnt, sumsq_out);
@@ -1016,17 +1239,20 @@ int bsgd_epoch(const bsgd_plan *p, const bsgd_epoch_args *a, void *stream) {
     cudaStream_t st = (cudaStream_t)stream;
     const bool prox = a->lam > 0.0;
     EpiStep es{a->g, a->x_k, a->mu, a->x_next, prox ? ws.uimg : nullptr, a->perm, a->x_true};
+    const bool tiled = tiled_usable(p, p->tf, a->x_k) && tiled_usable(p, p->tt, a->r_k);
     if (fl & BSGD_EP_SKIP_GRAD) {
         rc = run_step(p->cols, a, ws, st);
         if (!rc && (fl & BSGD_EP_R_NEXT))
-            rc = DISPATCH_V(p, launch_one<V>(fwd_csr<V>(p, a->x_k), p->g_fwd, EpiResid{a->y, a->r_next}, ws.rpart,
-                                              ws.ctl + 2, p->nnz, st));
+            rc = DISPATCH_V(p, launch_fwd<V>(p, a->x_k, EpiResid{a->y, a->r_next}, ws.rpart, ws.ctl + 2, st));
+    } else if ((fl & BSGD_EP_R_NEXT) && tiled) {
+        rc = DISPATCH_V(p, launch_fwd<V>(p, a->x_k, EpiResid{a->y, a->r_next}, ws.rpart, ws.ctl + 2, st));
+        if (!rc) rc = DISPATCH_V(p, launch_tr<V>(p, a->r_k, es, ws.xpart, ws.ctl, st));
     } else if (fl & BSGD_EP_R_NEXT) {
         // K1(x_k) and K2(r_k) read the same snapshot: one grid (solvers.py:281-290)
         rc = DISPATCH_V(p, launch_two<V>(fwd_csr<V>(p, a->x_k), p->g_fwd, EpiResid{a->y, a->r_next}, ws.rpart, ws.ctl + 2,
                                           p->nnz, tr_csr<V>(p, a->r_k), p->g_tr, es, ws.xpart, ws.ctl, p->nnz, st));
     } else {
-        rc = DISPATCH_V(p, launch_one<V>(tr_csr<V>(p, a->r_k), p->g_tr, es, ws.xpart, ws.ctl, p->nnz, st));
+        rc = DISPATCH_V(p, launch_tr<V>(p, a->r_k, es, ws.xpart, ws.ctl, st));
     }
     if (rc) return rc;
     if (prox) {
@@ -1035,8 +1261,7 @@ int bsgd_epoch(const bsgd_plan *p, const bsgd_epoch_args *a, void *stream) {
     }
     if (fl & BSGD_EP_LOOKAHEAD) {
         // K1(x_next): the next epoch's residual and the Eq. 9 monitor's f_next (solvers.py:319-320)
-        rc = DISPATCH_V(p, launch_one<V>(fwd_csr<V>(p, a->x_next), p->g_fwd, EpiResid{a->y, a->r_ahead}, ws.rpart,
-                                          ws.ctl + 1, p->nnz, st));
+        rc = DISPATCH_V(p, launch_fwd<V>(p, a->x_next, EpiResid{a->y, a->r_ahead}, ws.rpart, ws.ctl + 1, st));
         if (rc) return rc;
     }
     if (!(fl & BSGD_EP_NO_TAIL)) return run_tail(a, ws, (fl & BSGD_EP_LOOKAHEAD) ? 1 : 0, nullptr, st);
@@ -1061,7 +1286,7 @@ int bsgd_epoch_forward(const bsgd_plan *p, const double *x, const double *y, dou
     ws_layout(a->workspace, p->cols, a->lam > 0.0 ? a->height * a->width : 0, &ws);
     DeviceGuard guard(p->device);
     cudaStream_t st = (cudaStream_t)stream;
-    return DISPATCH_V(p, launch_one<V>(fwd_csr<V>(p, x), p->g_fwd, EpiResid{y, r_out}, ws.rpart, ws.ctl + 1, p->nnz, st));
+    return DISPATCH_V(p, launch_fwd<V>(p, x, EpiResid{y, r_out}, ws.rpart, ws.ctl + 1, st));
 }
 
 int bsgd_epoch_reduce_forward(const bsgd_plan *p, const bsgd_epoch_args *a, double *scalars_out, void *stream) {
