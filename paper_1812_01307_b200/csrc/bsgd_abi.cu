@@ -332,7 +332,8 @@ static int build_tiled(bsgd_plan::TiledStore &T, int64_t nrows, int64_t ncols, i
     T.NG = (int)cdiv(nrows, T.R);
     T.NP = (int)cdiv(ncols, T.P);
     const int64_t ntiles = (int64_t)T.NG * T.NP;
-    if (ntiles >= ((int64_t)1 << 32) || nnz >= ((int64_t)1 << 32)) return BSGD_OK;  // not eligible
+    if (ntiles >= ((int64_t)1 << 32) || nnz >= ((int64_t)1 << 32) || T.NP > kTileMaxNP || T.R > 32768)
+        return BSGD_OK;  // not eligible: keep the CSR kernels
     int32_t *rowid = nullptr;
     uint32_t *tkey = nullptr, *packed = nullptr, *pos = nullptr, *skey = nullptr, *perm = nullptr;
     uint32_t *n_rc = nullptr, *n_unit = nullptr, *rc_base = nullptr, *unit_base = nullptr;
@@ -415,7 +416,8 @@ static int build_tiled(bsgd_plan::TiledStore &T, int64_t nrows, int64_t ncols, i
     TTRY(cudaMalloc(&T.unit_start, sizeof(uint64_t) * (total_units + 1)));
     TTRY(cudaMalloc(&T.unit_len, sizeof(uint32_t) * (total_units + 1)));
     TTRY(cudaMalloc(&T.unit_rc, sizeof(uint32_t) * (total_units + 1)));
-    TTRY(cudaMalloc(&T.rc_off, sizeof(uint16_t) * (total_rc + 1)));
+    TTRY(cudaMalloc(&T.rc_off, sizeof(uint16_t) * (total_rc + 16)));
+    TTRY(cudaMemsetAsync(T.rc_off, 0, sizeof(uint16_t) * (total_rc + 16), st));
     TTRY(cudaMalloc(&T.tile_unit, sizeof(uint32_t) * (ntiles + 1)));
     tile_segment_kernel<CH><<<grid_1d(ntiles, 64), 64, 0, st>>>(ntiles, tile_ptr, T.keys, 1, n_rc, n_unit, rc_base,
                                                                  unit_base, T.unit_start, T.unit_len, T.unit_rc,
@@ -431,9 +433,11 @@ static int build_tiled(bsgd_plan::TiledStore &T, int64_t nrows, int64_t ncols, i
     // launch configuration: 1 CTA per SM, clusters of kTileCL
     auto kern = tile_spmv_kernel<V, EpiStore>;
     const size_t smem = TileSmem<V>::bytes(T.R, T.P);
-    cudaFuncSetAttribute(tile_spmv_kernel<V, EpiStore>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(tile_spmv_kernel<V, EpiResid>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(tile_spmv_kernel<V, EpiStep>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    // the attribute is per function, shared by every plan: set the largest layout once
+    const int smem_max = (int)TileSmem<V>::bytes(4096, 8192);
+    cudaFuncSetAttribute(tile_spmv_kernel<V, EpiStore>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max);
+    cudaFuncSetAttribute(tile_spmv_kernel<V, EpiResid>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max);
+    cudaFuncSetAttribute(tile_spmv_kernel<V, EpiStep>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(kTileCL * (num_sms() / kTileCL));
     cfg.blockDim = dim3(kTileThreads);

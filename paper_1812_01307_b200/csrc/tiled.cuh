@@ -30,10 +30,11 @@
 
 namespace bsgd {
 
-constexpr int kTileConsumerWarps = 8;
+constexpr int kTileConsumerWarps = 16;
 constexpr int kTileThreads = 32 * (2 + kTileConsumerWarps);
 constexpr int kTileCL = 8;     // cluster size (portable)
 constexpr int kTileNS = 3;     // ring slots
+constexpr int kTileMaxNP = 1023;
 
 template <typename V>
 struct TileCfg {
@@ -49,21 +50,33 @@ struct Tiled {
     const uint64_t *unit_start;   // [NU]   absolute entry index
     const uint32_t *unit_len;     // [NU]
     const uint32_t *unit_rc;      // [NU+1] row-chunk index range
-    const uint16_t *rc_off;       // [NRC]  chunk start within its unit
+    const uint16_t *rc_off;       // [NRC+8] chunk start within its unit
     const uint32_t *tile_unit;    // [NG*NP+1] unit range of each tile
     const double *vec;            // gathered vector, ncols
+};
+
+// per-slot unit descriptor written by the ring producer into shared memory
+struct UnitMeta {
+    uint32_t len;      // entries in the unit
+    uint32_t kdelta;   // first entry's offset inside the slot (copy starts 16-byte aligned)
+    uint32_t nrc;      // row chunks
+    uint32_t rdelta;   // first chunk offset's index inside the slot's rc area
 };
 
 template <typename V>
 struct TileSmem {
     static constexpr int CH = TileCfg<V>::CH;
-    static constexpr int SLOT = CH + 8;  // + alignment slack (units are copied from a 4-entry boundary)
+    static constexpr int SLOT = CH + 8;       // + alignment slack (copies start at a 4-entry boundary)
+    static constexpr int RCSLOT = CH + 16;    // u16 chunk offsets + 8-entry alignment slack
     static size_t bytes(int R, int P) {
         size_t b = 0;
         b += (size_t)2 * P * sizeof(double);                 // vector panels
         b += (size_t)kTileNS * SLOT * sizeof(uint32_t);      // ring keys
         b += (size_t)kTileNS * SLOT * sizeof(V);             // ring values
+        b += (size_t)kTileNS * RCSLOT * sizeof(uint16_t);    // ring chunk offsets
+        b += (size_t)kTileNS * sizeof(UnitMeta);             // ring unit descriptors
         b += (size_t)R * sizeof(double);                     // row accumulators
+        b += (size_t)(kTileMaxNP + 1) * sizeof(uint32_t);    // tile -> unit range of the group
         b += 16 * sizeof(uint64_t);                          // barriers
         return b;
     }
@@ -173,14 +186,17 @@ __global__ void tile_finish_kernel(int64_t ntiles, const uint32_t *n_unit, const
 // ---------------------------------------------------------------------------
 template <typename V, class Epi>
 __global__ void __launch_bounds__(kTileThreads, 1) tile_spmv_kernel(Tiled<V> T, Epi epi, double *part, int64_t *cnt) {
-    constexpr int CH = TileCfg<V>::CH;
     constexpr int SLOT = TileSmem<V>::SLOT;
+    constexpr int RCSLOT = TileSmem<V>::RCSLOT;
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    double *xbuf = reinterpret_cast<double *>(smem_raw);                          // [2][P]
-    uint32_t *rkeys = reinterpret_cast<uint32_t *>(xbuf + 2 * (size_t)T.P);       // [NS][SLOT]
-    V *rvals = reinterpret_cast<V *>(rkeys + (size_t)kTileNS * SLOT);             // [NS][SLOT]
-    double *acc = reinterpret_cast<double *>(rvals + (size_t)kTileNS * SLOT);     // [R]
-    uint64_t *bars = reinterpret_cast<uint64_t *>(acc + T.R);
+    double *xbuf = reinterpret_cast<double *>(smem_raw);                              // [2][P]
+    uint32_t *rkeys = reinterpret_cast<uint32_t *>(xbuf + 2 * (size_t)T.P);           // [NS][SLOT]
+    V *rvals = reinterpret_cast<V *>(rkeys + (size_t)kTileNS * SLOT);                 // [NS][SLOT]
+    uint16_t *rrc = reinterpret_cast<uint16_t *>(rvals + (size_t)kTileNS * SLOT);     // [NS][RCSLOT]
+    UnitMeta *rmeta = reinterpret_cast<UnitMeta *>(rrc + (size_t)kTileNS * RCSLOT);   // [NS]
+    double *acc = reinterpret_cast<double *>(rmeta + kTileNS);                        // [R]
+    uint32_t *tu = reinterpret_cast<uint32_t *>(acc + T.R);                           // [NP+1]
+    uint64_t *bars = reinterpret_cast<uint64_t *>(tu + kTileMaxNP + 1);
     uint64_t *ring_full = bars;            // [NS]
     uint64_t *ring_empty = bars + 4;       // [NS]
     uint64_t *x_full = bars + 8;           // [2]
@@ -205,23 +221,41 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_spmv_kernel(Tiled<V> T, 
     cluster_sync_all();
 
     if (warp == 0) {
-        // ---------------- ring producer ----------------
-        if (lane == 0) {
-            uint32_t k = 0;
-            for (int rd = 0; rd < rounds; ++rd) {
-                const int64_t g = my + (int64_t)rd * ctas;
-                if (g >= T.NG) continue;
-                const uint32_t u0 = T.tile_unit[g * NP], u1 = T.tile_unit[(g + 1) * NP];
-                for (uint32_t u = u0; u < u1; ++u, ++k) {
-                    const int s = k % kTileNS;
-                    if (k >= (uint32_t)kTileNS) mbar_wait(ring_empty + s, ((k / kTileNS) - 1) & 1);
-                    const uint64_t st = T.unit_start[u];
-                    const uint64_t a0 = st & ~(uint64_t)3;
-                    const uint64_t a1 = (st + T.unit_len[u] + 3) & ~(uint64_t)3;
-                    const uint32_t n4 = (uint32_t)(a1 - a0);
-                    mbar_arrive_expect_tx(ring_full + s, n4 * (uint32_t)(sizeof(uint32_t) + sizeof(V)));
-                    bulk_g2s(rkeys + (size_t)s * SLOT, T.keys + a0, n4 * sizeof(uint32_t), ring_full + s);
-                    bulk_g2s(rvals + (size_t)s * SLOT, T.vals + a0, n4 * (uint32_t)sizeof(V), ring_full + s);
+        // ---------------- ring producer (whole warp: metadata is fetched 32 units at a time) ----------------
+        uint32_t k = 0;
+        for (int rd = 0; rd < rounds; ++rd) {
+            const int64_t g = my + (int64_t)rd * ctas;
+            if (g >= T.NG) continue;
+            const uint32_t u0 = T.tile_unit[g * NP], u1 = T.tile_unit[(g + 1) * NP];
+            for (uint32_t ub = u0; ub < u1; ub += 32) {
+                const uint32_t u = ub + lane;
+                uint64_t m_st = 0;
+                uint32_t m_len = 0, m_r0 = 0, m_r1 = 0;
+                if (u < u1) { m_st = T.unit_start[u]; m_len = T.unit_len[u]; m_r0 = T.unit_rc[u]; m_r1 = T.unit_rc[u + 1]; }
+                const uint32_t nb = (u1 - ub < 32u) ? (u1 - ub) : 32u;
+                for (uint32_t j = 0; j < nb; ++j, ++k) {
+                    const uint64_t st = __shfl_sync(0xffffffffu, m_st, j);
+                    const uint32_t len = __shfl_sync(0xffffffffu, m_len, j);
+                    const uint32_t r0 = __shfl_sync(0xffffffffu, m_r0, j);
+                    const uint32_t r1 = __shfl_sync(0xffffffffu, m_r1, j);
+                    if (lane == 0) {
+                        const int s = k % kTileNS;
+                        if (k >= (uint32_t)kTileNS) mbar_wait(ring_empty + s, ((k / kTileNS) - 1) & 1);
+                        const uint64_t a0 = st & ~(uint64_t)3;
+                        const uint64_t a1 = (st + len + 3) & ~(uint64_t)3;
+                        const uint32_t n4 = (uint32_t)(a1 - a0);
+                        const uint32_t c0 = r0 & ~7u, c1 = (r1 + 7u) & ~7u;
+                        const uint32_t nrc8 = c1 - c0;
+                        UnitMeta m;
+                        m.len = len; m.kdelta = (uint32_t)(st - a0); m.nrc = r1 - r0; m.rdelta = r0 - c0;
+                        rmeta[s] = m;
+                        mbar_arrive_expect_tx(ring_full + s,
+                                              n4 * (uint32_t)(sizeof(uint32_t) + sizeof(V)) + nrc8 * 2u);
+                        bulk_g2s(rkeys + (size_t)s * SLOT, T.keys + a0, n4 * sizeof(uint32_t), ring_full + s);
+                        bulk_g2s(rvals + (size_t)s * SLOT, T.vals + a0, n4 * (uint32_t)sizeof(V), ring_full + s);
+                        bulk_g2s(rrc + (size_t)s * RCSLOT, T.rc_off + c0, nrc8 * 2u, ring_full + s);
+                    }
+                    __syncwarp();
                 }
             }
         }
@@ -246,6 +280,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_spmv_kernel(Tiled<V> T, 
                 }
             }
         }
+        __syncwarp();
     } else {
         // ---------------- consumers ----------------
         const int cw = warp - 2;
@@ -257,6 +292,8 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_spmv_kernel(Tiled<V> T, 
             const int64_t g = my + (int64_t)rd * ctas;
             const bool live = g < T.NG;
             for (int i = ctid; i < T.R; i += NCT) acc[i] = 0.0;
+            if (live)
+                for (int i = ctid; i <= NP; i += NCT) tu[i] = T.tile_unit[g * NP + i];
             named_bar_sync(1, NCT);
             for (int p = 0; p < NP; ++p, ++q) {
                 const int s = q & 1;
@@ -272,33 +309,50 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_spmv_kernel(Tiled<V> T, 
                     named_bar_sync(1, NCT);
                 }
                 if (live) {
-                    const uint32_t u0 = T.tile_unit[g * NP + p], u1 = T.tile_unit[g * NP + p + 1];
+                    const uint32_t u0 = tu[p], u1 = tu[p + 1];
                     for (uint32_t u = u0; u < u1; ++u, ++k) {
                         const int rs = k % kTileNS;
                         mbar_wait(ring_full + rs, (k / kTileNS) & 1);
-                        const uint64_t st = T.unit_start[u];
-                        const uint32_t delta = (uint32_t)(st & 3);
-                        const uint32_t len = T.unit_len[u];
-                        const uint32_t *kk = rkeys + (size_t)rs * SLOT + delta;
-                        const V *vv = rvals + (size_t)rs * SLOT + delta;
-                        const uint32_t r0 = T.unit_rc[u], r1 = T.unit_rc[u + 1];
-                        for (uint32_t rc = r0 + cw; rc < r1; rc += kTileConsumerWarps) {
-                            const uint32_t e0 = T.rc_off[rc];
-                            const uint32_t e1 = (rc + 1 < r1) ? T.rc_off[rc + 1] : len;
+                        const UnitMeta m = rmeta[rs];
+                        const uint32_t *kk = rkeys + (size_t)rs * SLOT + m.kdelta;
+                        const V *vv = rvals + (size_t)rs * SLOT + m.kdelta;
+                        const uint16_t *ro = rrc + (size_t)rs * RCSLOT + m.rdelta;
+                        for (uint32_t rc = cw; rc < m.nrc; rc += kTileConsumerWarps) {
+                            const uint32_t e0 = ro[rc];
+                            const uint32_t e1 = (rc + 1 < m.nrc) ? ro[rc + 1] : m.len;
                             const uint32_t nn = e1 - e0;
                             if (nn <= 32) {
                                 const bool valid = lane < (int)nn;
                                 const uint32_t key = valid ? kk[e0 + lane] : 0u;
-                                int row = valid ? (int)(key >> 16) : -1 - lane;
-                                double v = valid ? (double)vv[e0 + lane] * xs[key & 0xFFFFu] : 0.0;
+                                const int row = valid ? (int)(key >> 16) : -1 - lane;
+                                const int rp = __shfl_up_sync(0xffffffffu, row, 1);
+                                const bool head = valid && (lane == 0 || rp != row);
+                                const uint32_t heads = __ballot_sync(0xffffffffu, head);
+                                const int nseg = __popc(heads);
+                                if (nseg > 4) {
+                                    // one lane per row: sequential left-to-right sum of its entries
+                                    if (lane < nseg) {
+                                        const int b = __fns(heads, 0, lane + 1);
+                                        const int e = (lane + 1 < nseg) ? __fns(heads, 0, lane + 2) : (int)nn;
+                                        const uint32_t k0 = kk[e0 + b];
+                                        double v = (double)vv[e0 + b] * xs[k0 & 0xFFFFu];
+                                        for (int t = b + 1; t < e; ++t) {
+                                            const uint32_t kt = kk[e0 + t];
+                                            v = fma((double)vv[e0 + t], xs[kt & 0xFFFFu], v);
+                                        }
+                                        acc[k0 >> 16] += v;
+                                    }
+                                } else {
+                                    double v = valid ? (double)vv[e0 + lane] * xs[key & 0xFFFFu] : 0.0;
 #pragma unroll
-                                for (int off = 1; off < 32; off <<= 1) {
-                                    const double vo = __shfl_up_sync(0xffffffffu, v, off);
-                                    const int ro = __shfl_up_sync(0xffffffffu, row, off);
-                                    if (lane >= off && ro == row) v += vo;
+                                    for (int off = 1; off < 32; off <<= 1) {
+                                        const double vo = __shfl_up_sync(0xffffffffu, v, off);
+                                        const int rw = __shfl_up_sync(0xffffffffu, row, off);
+                                        if (lane >= off && rw == row) v += vo;
+                                    }
+                                    const int rn = __shfl_down_sync(0xffffffffu, row, 1);
+                                    if (valid && (lane == (int)nn - 1 || rn != row)) acc[row] += v;
                                 }
-                                const int rn = __shfl_down_sync(0xffffffffu, row, 1);
-                                if (valid && (lane == (int)nn - 1 || rn != row)) acc[row] += v;
                             } else {  // one long row
                                 const uint32_t row = kk[e0] >> 16;
                                 double v = 0.0;
@@ -324,7 +378,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_spmv_kernel(Tiled<V> T, 
         }
     }
     __syncwarp();
-    // statistics of the epilogue (consumers only carry nonzero values)
+    // statistics of the epilogue (only consumers carry nonzero values)
     if constexpr (Epi::K > 0) {
         __shared__ double red_sm[Epi::K * (kTileThreads / 32)];
         double v[Epi::K];

@@ -20,6 +20,7 @@ def main():
     ap.add_argument("--scale", type=float, default=0.05)
     ap.add_argument("--config", type=int, default=1)
     ap.add_argument("--time", action="store_true")
+    ap.add_argument("--profile", action="store_true", help="3 tiled launches of each kernel only")
     a = ap.parse_args()
     d = problems.config(a.config, scale=a.scale)
     m = d.num_row_blocks
@@ -28,6 +29,15 @@ def main():
     op_t = blockops.BlockOperator(d.matrix, blockops.make_partition(*d.shape, m, m))
     torch.cuda.synchronize()
     print(f"tiled plan {time.time() - t0:.2f}s", flush=True)
+    if a.profile:
+        x = torch.randn(d.shape[1], dtype=torch.float64, device="cuda")
+        w = torch.randn(d.shape[0], dtype=torch.float64, device="cuda")
+        for _ in range(3):
+            op_t.matvec(x)
+            op_t.rmatvec(w)
+        torch.cuda.synchronize()
+        print("profiled")
+        return
     os.environ["BSGD_TILED"] = "0"
     op_c = blockops.BlockOperator(d.matrix, blockops.make_partition(*d.shape, m, m))
     rng = np.random.default_rng(0)
