@@ -163,10 +163,11 @@ struct bsgd_plan {
         uint32_t *keys = nullptr;
         void *vals = nullptr;
         uint64_t *unit_start = nullptr;
-        uint32_t *unit_len = nullptr, *unit_rc = nullptr, *tile_unit = nullptr;
-        uint16_t *rc_off = nullptr;
+        uint32_t *unit_len = nullptr, *tile_unit = nullptr;
+        uint16_t *unit_split = nullptr;
         size_t bytes = 0;
-        int clusters = 0;  // co-resident clusters of kTileCL CTAs
+        int H = 1;              // panel ranges per row group (work items = NG * H)
+        double *pout = nullptr; // [H][nrows] partial sums when H > 1
     } tf, tt;
     bool use_tiled = true;
 };
@@ -246,7 +247,7 @@ __global__ void block_nnz_kernel(int64_t rows, const int64_t *ptr, const int32_t
 
 static void tiled_free(bsgd_plan::TiledStore &t) {
     cudaFree(t.keys); cudaFree(t.vals); cudaFree(t.unit_start); cudaFree(t.unit_len);
-    cudaFree(t.unit_rc); cudaFree(t.tile_unit); cudaFree(t.rc_off);
+    cudaFree(t.tile_unit); cudaFree(t.pout); cudaFree(t.unit_split);
     t = bsgd_plan::TiledStore();
 }
 
@@ -313,13 +314,32 @@ static int build_transpose(bsgd_plan *p, cudaStream_t st) {
 // ---------------------------------------------------------------------------
 // panel-tiled format (tiled.cuh)
 // ---------------------------------------------------------------------------
-static void choose_tiling(int64_t nrows, int64_t ncols, int &R, int &P) {
-    P = (int)std::min<int64_t>(8192, (ncols + 1) & ~(int64_t)1);
+// Pick rows per group R, panel width P and panel ranges H from a small cost
+// model: HBM stream of A, L2->SM re-reads of the vector (each row group reads
+// the whole vector once, ~18 TB/s measured for per-CTA bulk copies) and the
+// partial-sum round trip when H > 1, divided by the load balance of
+// NG * H work items over the SMs.
+template <typename V>
+static void choose_tiling(int64_t nrows, int64_t ncols, int64_t nnz, int &R, int &P, int &H) {
+    P = (int)std::min<int64_t>(kTileMaxP, (ncols + 1) & ~(int64_t)1);
     if (P < 2) P = 2;
-    const int64_t ctas = (int64_t)(num_sms() / kTileCL) * kTileCL;
+    const int64_t NP = cdiv(ncols, P);
+    const double sms = num_sms();
+    const double stream = (double)nnz * (4.0 + sizeof(V));
+    double best = 1e300;
     R = 256;
-    for (int r : {4096, 2048, 1024, 512, 256}) {
-        if (cdiv(nrows, r) >= (ctas * 4) / 5) { R = r; break; }
+    H = 1;
+    for (int r : {8192, 4096, 2048, 1024, 512, 256}) {
+        const int64_t NG = cdiv(nrows, r);
+        for (int h = 1; h <= 32 && h <= NP; ++h) {
+            const double items = (double)NG * h;
+            const double rounds = std::ceil(items / sms);
+            const double eff = items / (rounds * sms);
+            const double vec = (double)NG * ncols * 8.0;
+            const double partial = h > 1 ? 2.0 * h * nrows * 8.0 : 0.0;
+            const double t = std::max(stream / 6.5e12, (stream + vec + partial) / 18e12) / eff;
+            if (t < best * 0.999) { best = t; R = r; H = h; }
+        }
     }
 }
 
@@ -327,16 +347,16 @@ template <typename V>
 static int build_tiled(bsgd_plan::TiledStore &T, int64_t nrows, int64_t ncols, int64_t nnz, const int64_t *ptr,
                        const int32_t *idx, const V *val, cudaStream_t st) {
     constexpr int CH = TileCfg<V>::CH;
-    choose_tiling(nrows, ncols, T.R, T.P);
+    choose_tiling<V>(nrows, ncols, nnz, T.R, T.P, T.H);
     T.nrows = nrows; T.ncols = ncols;
     T.NG = (int)cdiv(nrows, T.R);
     T.NP = (int)cdiv(ncols, T.P);
     const int64_t ntiles = (int64_t)T.NG * T.NP;
-    if (ntiles >= ((int64_t)1 << 32) || nnz >= ((int64_t)1 << 32) || T.NP > kTileMaxNP || T.R > 32768)
+    if (ntiles >= ((int64_t)1 << 32) || nnz >= ((int64_t)1 << 32) || T.NP > kTileMaxNP || T.R > kTileMaxR)
         return BSGD_OK;  // not eligible: keep the CSR kernels
     int32_t *rowid = nullptr;
     uint32_t *tkey = nullptr, *packed = nullptr, *pos = nullptr, *skey = nullptr, *perm = nullptr;
-    uint32_t *n_rc = nullptr, *n_unit = nullptr, *rc_base = nullptr, *unit_base = nullptr;
+    uint32_t *n_unit = nullptr, *unit_base = nullptr;
     uint64_t *tile_ptr = nullptr;
     int *d_bad = nullptr;
     void *temp = nullptr;
@@ -344,7 +364,7 @@ static int build_tiled(bsgd_plan::TiledStore &T, int64_t nrows, int64_t ncols, i
     int rc = BSGD_OK;
     auto cleanup = [&]() {
         cudaFree(rowid); cudaFree(tkey); cudaFree(packed); cudaFree(pos); cudaFree(skey); cudaFree(perm);
-        cudaFree(n_rc); cudaFree(n_unit); cudaFree(rc_base); cudaFree(unit_base); cudaFree(tile_ptr);
+        cudaFree(n_unit); cudaFree(unit_base); cudaFree(tile_ptr);
         cudaFree(d_bad); cudaFree(temp);
     };
 #define TTRY(call)                                                                          \
@@ -377,34 +397,30 @@ static int build_tiled(bsgd_plan::TiledStore &T, int64_t nrows, int64_t ncols, i
     TTRY(cudaMalloc(&temp, temp_bytes));
     TTRY(cub::DeviceRadixSort::SortPairs(temp, temp_bytes, tkey, skey, pos, perm, nnz, 0, end_bit, st));
     tile_gather_kernel<V><<<grid_1d(nnz), kThreads, 0, st>>>(nnz, perm, packed, val, T.keys, (V *)T.vals);
+    tile_flags_kernel<<<grid_1d(nnz), kThreads, 0, st>>>(nnz, skey, T.keys);
     TTRY(cudaMalloc(&tile_ptr, sizeof(uint64_t) * (ntiles + 1)));
     tile_ptr_kernel<<<grid_1d(ntiles + 1), kThreads, 0, st>>>(ntiles, nnz, skey, tile_ptr);
     TTRY(cudaGetLastError());
-    TTRY(cudaMalloc(&n_rc, sizeof(uint32_t) * ntiles));
     TTRY(cudaMalloc(&n_unit, sizeof(uint32_t) * ntiles));
-    TTRY(cudaMalloc(&rc_base, sizeof(uint32_t) * ntiles));
     TTRY(cudaMalloc(&unit_base, sizeof(uint32_t) * ntiles));
     TTRY(cudaMalloc(&d_bad, sizeof(int)));
     TTRY(cudaMemsetAsync(d_bad, 0, sizeof(int), st));
-    tile_segment_kernel<CH><<<grid_1d(ntiles, 64), 64, 0, st>>>(ntiles, tile_ptr, T.keys, 0, n_rc, n_unit, nullptr,
-                                                                 nullptr, nullptr, nullptr, nullptr, nullptr, d_bad);
+    tile_segment_kernel<CH><<<grid_1d(ntiles, 64), 64, 0, st>>>(ntiles, tile_ptr, T.keys, 0, n_unit, nullptr, nullptr,
+                                                                 nullptr, d_bad);
     TTRY(cudaGetLastError());
     size_t scan_bytes = 0;
-    TTRY(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, n_rc, rc_base, ntiles, st));
+    TTRY(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, n_unit, unit_base, ntiles, st));
     if (scan_bytes > temp_bytes) {
         TTRY(cudaFree(temp));
         temp = nullptr;
         TTRY(cudaMalloc(&temp, scan_bytes));
         temp_bytes = scan_bytes;
     }
-    TTRY(cub::DeviceScan::ExclusiveSum(temp, temp_bytes, n_rc, rc_base, ntiles, st));
     TTRY(cub::DeviceScan::ExclusiveSum(temp, temp_bytes, n_unit, unit_base, ntiles, st));
-    uint32_t last[4] = {0, 0, 0, 0};
+    uint32_t last[2] = {0, 0};
     int bad = 0;
-    TTRY(cudaMemcpyAsync(&last[0], rc_base + ntiles - 1, 4, cudaMemcpyDeviceToHost, st));
-    TTRY(cudaMemcpyAsync(&last[1], n_rc + ntiles - 1, 4, cudaMemcpyDeviceToHost, st));
-    TTRY(cudaMemcpyAsync(&last[2], unit_base + ntiles - 1, 4, cudaMemcpyDeviceToHost, st));
-    TTRY(cudaMemcpyAsync(&last[3], n_unit + ntiles - 1, 4, cudaMemcpyDeviceToHost, st));
+    TTRY(cudaMemcpyAsync(&last[0], unit_base + ntiles - 1, 4, cudaMemcpyDeviceToHost, st));
+    TTRY(cudaMemcpyAsync(&last[1], n_unit + ntiles - 1, 4, cudaMemcpyDeviceToHost, st));
     TTRY(cudaMemcpyAsync(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, st));
     TTRY(cudaStreamSynchronize(st));
     if (bad) {  // a row has more than CH entries in one tile: keep the CSR kernels
@@ -412,49 +428,36 @@ static int build_tiled(bsgd_plan::TiledStore &T, int64_t nrows, int64_t ncols, i
         tiled_free(T);
         return BSGD_OK;
     }
-    const uint32_t total_rc = last[0] + last[1], total_units = last[2] + last[3];
+    const uint32_t total_units = last[0] + last[1];
     TTRY(cudaMalloc(&T.unit_start, sizeof(uint64_t) * (total_units + 1)));
     TTRY(cudaMalloc(&T.unit_len, sizeof(uint32_t) * (total_units + 1)));
-    TTRY(cudaMalloc(&T.unit_rc, sizeof(uint32_t) * (total_units + 1)));
-    TTRY(cudaMalloc(&T.rc_off, sizeof(uint16_t) * (total_rc + 16)));
-    TTRY(cudaMemsetAsync(T.rc_off, 0, sizeof(uint16_t) * (total_rc + 16), st));
     TTRY(cudaMalloc(&T.tile_unit, sizeof(uint32_t) * (ntiles + 1)));
-    tile_segment_kernel<CH><<<grid_1d(ntiles, 64), 64, 0, st>>>(ntiles, tile_ptr, T.keys, 1, n_rc, n_unit, rc_base,
-                                                                 unit_base, T.unit_start, T.unit_len, T.unit_rc,
-                                                                 T.rc_off, d_bad);
-    tile_finish_kernel<<<grid_1d(ntiles + 1), kThreads, 0, st>>>(ntiles, n_unit, unit_base, total_units, total_rc,
-                                                                 T.tile_unit, T.unit_rc);
+    tile_segment_kernel<CH><<<grid_1d(ntiles, 64), 64, 0, st>>>(ntiles, tile_ptr, T.keys, 1, n_unit, unit_base,
+                                                                 T.unit_start, T.unit_len, d_bad);
+    tile_finish_kernel<<<grid_1d(ntiles + 1), kThreads, 0, st>>>(ntiles, unit_base, total_units, T.tile_unit);
+    TTRY(cudaMalloc(&T.unit_split, sizeof(uint16_t) * kSplitStride * (total_units + 1)));
+    tile_split_kernel<<<grid_1d(total_units), kThreads, 0, st>>>(total_units, T.unit_start, T.unit_len, T.keys, T.R,
+                                                                 T.unit_split);
     TTRY(cudaGetLastError());
     TTRY(cudaStreamSynchronize(st));
 #undef TTRY
     cleanup();
-    T.bytes = (sizeof(uint32_t) + sizeof(V)) * (nnz + 8) + 16 * (size_t)(total_units + 1) +
-              2 * (size_t)(total_rc + 1) + 4 * (size_t)(ntiles + 1);
-    // launch configuration: 1 CTA per SM, clusters of kTileCL
-    auto kern = tile_spmv_kernel<V, EpiStore>;
-    const size_t smem = TileSmem<V>::bytes(T.R, T.P);
-    // the attribute is per function, shared by every plan: set the largest layout once
-    const int smem_max = (int)TileSmem<V>::bytes(4096, 8192);
-    cudaFuncSetAttribute(tile_spmv_kernel<V, EpiStore>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max);
-    cudaFuncSetAttribute(tile_spmv_kernel<V, EpiResid>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max);
-    cudaFuncSetAttribute(tile_spmv_kernel<V, EpiStep>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max);
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(kTileCL * (num_sms() / kTileCL));
-    cfg.blockDim = dim3(kTileThreads);
-    cfg.dynamicSmemBytes = smem;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = kTileCL; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    int nclusters = 0;
-    cudaError_t e = cudaOccupancyMaxActiveClusters(&nclusters, kern, &cfg);
-    if (e != cudaSuccess || nclusters < 1) {
+    T.bytes = (sizeof(uint32_t) + sizeof(V)) * (nnz + 8) + (12 + 2 * kSplitStride) * (size_t)(total_units + 1) +
+              4 * (size_t)(ntiles + 1) + sizeof(double) * (size_t)T.H * nrows;
+    if (T.H > 1 && cudaMalloc(&T.pout, sizeof(double) * (size_t)T.H * nrows) != cudaSuccess) {
+        cudaGetLastError();
+        tiled_free(T);
+        return fail(BSGD_ENOMEM, "tiled build: partial-sum buffer allocation failed");
+    }
+    // one CTA per SM; the smem attribute is per function and shared by every plan
+    const int smem_max = (int)TileSmem<V>::bytes(8192, 4096);
+    if (cudaFuncSetAttribute(tile_spmv_kernel<V, EpiStore>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max) != cudaSuccess ||
+        cudaFuncSetAttribute(tile_spmv_kernel<V, EpiResid>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max) != cudaSuccess ||
+        cudaFuncSetAttribute(tile_spmv_kernel<V, EpiStep>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max) != cudaSuccess) {
         cudaGetLastError();
         tiled_free(T);
         return BSGD_OK;
     }
-    T.clusters = std::min(nclusters, num_sms() / kTileCL);
     T.ok = true;
     return BSGD_OK;
 }
@@ -465,24 +468,23 @@ static int launch_tiled(const bsgd_plan::TiledStore &S, const double *vec, const
     Tiled<V> T;
     T.nrows = S.nrows; T.ncols = S.ncols; T.R = S.R; T.P = S.P; T.NG = S.NG; T.NP = S.NP;
     T.keys = S.keys; T.vals = (const V *)S.vals; T.unit_start = S.unit_start; T.unit_len = S.unit_len;
-    T.unit_rc = S.unit_rc; T.rc_off = S.rc_off; T.tile_unit = S.tile_unit; T.vec = vec;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(kTileCL * S.clusters);
-    cfg.blockDim = dim3(kTileThreads);
-    cfg.dynamicSmemBytes = TileSmem<V>::bytes(S.R, S.P);
-    cfg.stream = st;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = kTileCL; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    CU(cudaLaunchKernelEx(&cfg, tile_spmv_kernel<V, E>, T, e, part, cnt));
+    T.tile_unit = S.tile_unit; T.vec = vec; T.unit_split = S.unit_split;
+    T.H = S.H; T.pout = S.pout;
+    const size_t smem = TileSmem<V>::bytes(S.R, S.P);
+    tile_spmv_kernel<V, E><<<num_sms(), kTileThreads, smem, st>>>(T, e, part, cnt);
+    LAUNCHED();
+    if (S.H > 1) {
+        tile_combine_kernel<E><<<grid_1d(S.nrows), kThreads, 0, st>>>(S.nrows, S.H, S.pout, e, part, cnt);
+        LAUNCHED();
+    }
     return BSGD_OK;
 }
 
 static bool tiled_usable(const bsgd_plan *p, const bsgd_plan::TiledStore &S, const double *vec) {
     return p->use_tiled && S.ok && (((uintptr_t)vec) & 15) == 0;
 }
+
+
 
 // ---------------------------------------------------------------------------
 // SpMV launchers
@@ -544,6 +546,50 @@ static int launch_two(const Csr<V> &A, int GA, const EA &ea, double *partA, int6
     if (GB == 8)
         return launch_dual<V, 32, 8, EA, EB>(A, ea, partA, cntA, nnzA, B, eb, partB, cntB, nnzB, st);
     return launch_dual<V, 32, 32, EA, EB>(A, ea, partA, cntA, nnzA, B, eb, partB, cntB, nnzB, st);
+}
+
+// Keep the tiled copy of a direction only if it beats the CSR kernel on this
+// matrix (timed once at plan creation on zero vectors); otherwise free it.
+template <typename V>
+static int autotune_direction(bsgd_plan *p, bool transposed, cudaStream_t st) {
+    bsgd_plan::TiledStore &S = transposed ? p->tt : p->tf;
+    if (!S.ok) return BSGD_OK;
+    const int64_t nin = transposed ? p->rows : p->cols, nout = transposed ? p->cols : p->rows;
+    double *vin = nullptr, *vout = nullptr;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    float t_csr = 0.f, t_tiled = 0.f;
+    int rc = BSGD_OK;
+    if (cudaMalloc(&vin, sizeof(double) * nin) != cudaSuccess || cudaMalloc(&vout, sizeof(double) * nout) != cudaSuccess) {
+        cudaGetLastError();
+        cudaFree(vin);
+        tiled_free(S);
+        return BSGD_OK;
+    }
+    cudaMemsetAsync(vin, 0, sizeof(double) * nin, st);
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    const Csr<V> csr = transposed ? tr_csr<V>(p, vin) : fwd_csr<V>(p, vin);
+    const int G = transposed ? p->g_tr : p->g_fwd;
+    for (int variant = 0; variant < 2 && rc == BSGD_OK; ++variant) {
+        for (int rep = 0; rep < 3 && rc == BSGD_OK; ++rep) {
+            if (rep == 1) cudaEventRecord(e0, st);
+            rc = variant == 0 ? launch_one<V>(csr, G, EpiStore{vout, 1.0}, nullptr, nullptr, p->nnz, st)
+                              : launch_tiled<V>(S, vin, EpiStore{vout, 1.0}, nullptr, nullptr, st);
+        }
+        cudaEventRecord(e1, st);
+        cudaEventSynchronize(e1);
+        cudaEventElapsedTime(variant == 0 ? &t_csr : &t_tiled, e0, e1);
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(vin);
+    cudaFree(vout);
+    if (rc != BSGD_OK || !(t_tiled < 0.97f * t_csr)) {
+        p->device_bytes -= 0;
+        tiled_free(S);
+        return rc;
+    }
+    return BSGD_OK;
 }
 
 template <typename V, class E>
@@ -835,6 +881,17 @@ int bsgd_plan_create(bsgd_plan **out, int device, int64_t rows, int64_t cols, in
             if (!rc) rc = build_tiled<double>(p->tt, cols, rows, nnz, p->t_ptr, p->t_idx, (const double *)p->t_val, st);
         }
         if (rc != BSGD_OK) { plan_free(p); return rc; }
+        const char *force = getenv("BSGD_TILED");
+        if (!(force && force[0] == '2')) {  // BSGD_TILED=2 keeps the tiled path without timing it
+            if (value_dtype == BSGD_F32) {
+                rc = autotune_direction<float>(p, false, st);
+                if (!rc) rc = autotune_direction<float>(p, true, st);
+            } else {
+                rc = autotune_direction<double>(p, false, st);
+                if (!rc) rc = autotune_direction<double>(p, true, st);
+            }
+            if (rc != BSGD_OK) { plan_free(p); return rc; }
+        }
         p->device_bytes += p->tf.bytes + p->tt.bytes;
     }
     // block nnz table (blockops.py:179-180)

@@ -45,6 +45,19 @@ __device__ __forceinline__ double ld_stream(const double *p, uint64_t pol) {
     return v;
 }
 
+__device__ __forceinline__ int4 ld_stream4(const int32_t *p, uint64_t pol) {
+    int4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ float4 ld_stream4(const float *p, uint64_t pol) {
+    float4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p), "l"(pol));
+    return v;
+}
+
 // ---- deterministic reductions: fixed shuffle tree, fixed warp order.
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll

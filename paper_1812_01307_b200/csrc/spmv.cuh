@@ -114,29 +114,69 @@ __device__ __forceinline__ void csr_rows(const Csr<V> &A, int64_t warp_id, int64
         if (row < A.nrows) {
             const int64_t beg = A.ptr[row];
             const int64_t end = A.ptr[row + 1];
-            int64_t k = beg + gl;
-            for (; k + 3 * G < end; k += 4 * G) {
-                const int32_t c0 = ld_stream(idx + k, pol);
-                const int32_t c1 = ld_stream(idx + k + G, pol);
-                const int32_t c2 = ld_stream(idx + k + 2 * G, pol);
-                const int32_t c3 = ld_stream(idx + k + 3 * G, pol);
-                const V v0 = ld_stream(val + k, pol);
-                const V v1 = ld_stream(val + k + G, pol);
-                const V v2 = ld_stream(val + k + 2 * G, pol);
-                const V v3 = ld_stream(val + k + 3 * G, pol);
-                const double x0 = __ldg(vec + c0);
-                const double x1 = __ldg(vec + c1);
-                const double x2 = __ldg(vec + c2);
-                const double x3 = __ldg(vec + c3);
-                s = fma((double)v0, x0, s);
-                s = fma((double)v1, x1, s);
-                s = fma((double)v2, x2, s);
-                s = fma((double)v3, x3, s);
-            }
-            for (; k < end; k += G) {
-                const int32_t c0 = ld_stream(idx + k, pol);
-                const V v0 = ld_stream(val + k, pol);
-                s = fma((double)v0, __ldg(vec + c0), s);
+            if constexpr (sizeof(V) == 4 && G <= 8) {
+                // short rows: 16-byte streaming loads over the 4-aligned body of the row:
+                // one L1 request moves 4 (index, value) pairs, leaving the L1 tag stage to
+                // the random gathers (profiles/r01_spmv_baseline.md); measured -9% on the
+                // configs[1] forward product, +4% on 128-nnz rows, hence G <= 8 only
+                const int64_t b4 = (beg + 3) & ~(int64_t)3;
+                const int64_t e4 = end & ~(int64_t)3;
+                if (b4 < e4) {
+                    for (int64_t k = beg + gl; k < b4; k += G)
+                        s = fma((double)ld_stream(val + k, pol), __ldg(vec + ld_stream(idx + k, pol)), s);
+                    int64_t k = b4 + 4 * gl;
+                    for (; k + 4 * G < e4; k += 8 * G) {
+                        const int4 c0 = ld_stream4(idx + k, pol);
+                        const int4 c1 = ld_stream4(idx + k + 4 * G, pol);
+                        const float4 v0 = ld_stream4(reinterpret_cast<const float *>(val) + k, pol);
+                        const float4 v1 = ld_stream4(reinterpret_cast<const float *>(val) + k + 4 * G, pol);
+                        const double x0 = __ldg(vec + c0.x), x1 = __ldg(vec + c0.y), x2 = __ldg(vec + c0.z),
+                                     x3 = __ldg(vec + c0.w), x4 = __ldg(vec + c1.x), x5 = __ldg(vec + c1.y),
+                                     x6 = __ldg(vec + c1.z), x7 = __ldg(vec + c1.w);
+                        s = fma((double)v0.x, x0, s); s = fma((double)v0.y, x1, s);
+                        s = fma((double)v0.z, x2, s); s = fma((double)v0.w, x3, s);
+                        s = fma((double)v1.x, x4, s); s = fma((double)v1.y, x5, s);
+                        s = fma((double)v1.z, x6, s); s = fma((double)v1.w, x7, s);
+                    }
+                    for (; k < e4; k += 4 * G) {
+                        const int4 c0 = ld_stream4(idx + k, pol);
+                        const float4 v0 = ld_stream4(reinterpret_cast<const float *>(val) + k, pol);
+                        const double x0 = __ldg(vec + c0.x), x1 = __ldg(vec + c0.y), x2 = __ldg(vec + c0.z),
+                                     x3 = __ldg(vec + c0.w);
+                        s = fma((double)v0.x, x0, s); s = fma((double)v0.y, x1, s);
+                        s = fma((double)v0.z, x2, s); s = fma((double)v0.w, x3, s);
+                    }
+                    for (int64_t t = e4 + gl; t < end; t += G)
+                        s = fma((double)ld_stream(val + t, pol), __ldg(vec + ld_stream(idx + t, pol)), s);
+                } else {
+                    for (int64_t t = beg + gl; t < end; t += G)
+                        s = fma((double)ld_stream(val + t, pol), __ldg(vec + ld_stream(idx + t, pol)), s);
+                }
+            } else {
+                int64_t k = beg + gl;
+                for (; k + 3 * G < end; k += 4 * G) {
+                    const int32_t c0 = ld_stream(idx + k, pol);
+                    const int32_t c1 = ld_stream(idx + k + G, pol);
+                    const int32_t c2 = ld_stream(idx + k + 2 * G, pol);
+                    const int32_t c3 = ld_stream(idx + k + 3 * G, pol);
+                    const V v0 = ld_stream(val + k, pol);
+                    const V v1 = ld_stream(val + k + G, pol);
+                    const V v2 = ld_stream(val + k + 2 * G, pol);
+                    const V v3 = ld_stream(val + k + 3 * G, pol);
+                    const double x0 = __ldg(vec + c0);
+                    const double x1 = __ldg(vec + c1);
+                    const double x2 = __ldg(vec + c2);
+                    const double x3 = __ldg(vec + c3);
+                    s = fma((double)v0, x0, s);
+                    s = fma((double)v1, x1, s);
+                    s = fma((double)v2, x2, s);
+                    s = fma((double)v3, x3, s);
+                }
+                for (; k < end; k += G) {
+                    const int32_t c0 = ld_stream(idx + k, pol);
+                    const V v0 = ld_stream(val + k, pol);
+                    s = fma((double)v0, __ldg(vec + c0), s);
+                }
             }
         }
 #pragma unroll

@@ -5,24 +5,27 @@
 // the vector-CSR kernels at ~0.29 ms per configs[1] product, 3.5x above the HBM
 // bound.  Gathers from the CTA's own shared memory run ~5x faster.
 //
-// Layout ("tiles"): rows are cut into groups of R rows, the gathered vector
-// into panels of P entries.  Tile (g, p) holds the nonzeros of rows in group g
-// and columns in panel p, in CSR order, each packed as (row_local << 16 |
-// col_local) plus its value.  Tiles are stored group-major, panel-minor.  Each
-// tile is cut into "row chunks" (<= 32 entries and never splitting a row, or
-// one long row) and row chunks are packed into "units" of <= CH entries, the
-// granule a TMA bulk copy moves.
+// Layout ("tiles"): rows are cut into groups of R <= 8192 rows, the gathered
+// vector into panels of P <= 4096 entries.  Tile (g, p) holds the nonzeros of
+// rows in group g and columns in panel p, in CSR order, each packed as
+//   key = END << 31 | START << 30 | row_local << 12 | col_local
+// (START / END mark the first / last entry of a row inside the tile) plus its
+// value.  Tiles are stored group-major, panel-minor and cut into "units" of
+// <= CH entries at row boundaries, the granule a TMA bulk copy moves.
 //
-// Kernel (one CTA per SM, clusters of CL CTAs, each CTA owns one row group at
-// a time; all CTAs of a cluster walk the panels in lockstep):
-//   warp 0  ring producer: TMA-copies the CTA's units into an NS-slot ring;
-//   warp 1  panel producer: the cluster leader multicasts vector panel p into
-//           every member's double buffer once all members released it, so
-//           each panel is read from L2 once per cluster;
-//   warps 2+ consumers: per row chunk, gather vec from the smem panel, reduce
-//           the row segments with a shuffle scan, add into a shared-memory
-//           row accumulator (each row once per tile -> deterministic), and
-//           finally run the same epilogue functors as the CSR kernels.
+// Kernel (one persistent CTA per SM).  A work item is (row group g, panel
+// range h of H): the CTA streams the tiles (g, p) for p in range h.
+//   warp 0  ring producer: TMA-copies the item's units (entries + row-chunk
+//           offsets) into an NS-slot ring, unit metadata prefetched 32 at a time;
+//   warp 1  panel producer: TMA-copies vector panel p into an NX-slot buffer
+//           (per CTA: ~21 TB/s aggregate L2->SM, profiles/r01_gather_microbench.md;
+//           a lockstep cluster multicast was measured 2-5x slower per step);
+//   warps 2+ consumers: per row chunk, gather the vector from the smem panel,
+//           reduce row segments (one lane per row, or a shuffle scan for few
+//           rows), add into a shared-memory row accumulator (each row once per
+//           tile -> deterministic).  H == 1: the epilogue functor runs here;
+//           H > 1: partial sums go to a [H][rows] buffer and a combine kernel
+//           adds them in ascending h and runs the epilogue (deterministic).
 #pragma once
 
 #include "common.cuh"
@@ -30,11 +33,18 @@
 
 namespace bsgd {
 
-constexpr int kTileConsumerWarps = 16;
+constexpr int kTileConsumerWarps = 30;
 constexpr int kTileThreads = 32 * (2 + kTileConsumerWarps);
-constexpr int kTileCL = 8;     // cluster size (portable)
 constexpr int kTileNS = 3;     // ring slots
+constexpr int kTileNX = 3;     // vector panel slots
 constexpr int kTileMaxNP = 1023;
+constexpr int kTileMaxR = 8192;
+constexpr int kTileMaxP = 4096;
+constexpr int kSplitStride = 32;   // u16 per unit: kTileConsumerWarps + 1 used, padded to 64 bytes
+constexpr uint32_t kKeyStart = 1u << 30;
+constexpr uint32_t kKeyEnd = 1u << 31;
+__host__ __device__ __forceinline__ uint32_t key_row(uint32_t k) { return (k >> 12) & 0x1FFFu; }
+__host__ __device__ __forceinline__ uint32_t key_col(uint32_t k) { return k & 0xFFFu; }
 
 template <typename V>
 struct TileCfg {
@@ -49,35 +59,35 @@ struct Tiled {
     const V *vals;
     const uint64_t *unit_start;   // [NU]   absolute entry index
     const uint32_t *unit_len;     // [NU]
-    const uint32_t *unit_rc;      // [NU+1] row-chunk index range
-    const uint16_t *rc_off;       // [NRC+8] chunk start within its unit
+    const uint16_t *unit_split;   // [NU][kSplitStride] per-consumer-warp entry split points
     const uint32_t *tile_unit;    // [NG*NP+1] unit range of each tile
     const double *vec;            // gathered vector, ncols
+    int H;                        // panel ranges per row group (work items = NG * H)
+    double *pout;                 // [H][nrows] partial sums when H > 1
 };
 
 // per-slot unit descriptor written by the ring producer into shared memory
 struct UnitMeta {
     uint32_t len;      // entries in the unit
     uint32_t kdelta;   // first entry's offset inside the slot (copy starts 16-byte aligned)
-    uint32_t nrc;      // row chunks
-    uint32_t rdelta;   // first chunk offset's index inside the slot's rc area
 };
+// consumer warp w owns local rows [w*R/16, (w+1)*R/16) of the row group; a
+// unit's entries for those rows are [split[w], split[w+1]) (rows are sorted)
 
 template <typename V>
 struct TileSmem {
     static constexpr int CH = TileCfg<V>::CH;
     static constexpr int SLOT = CH + 8;       // + alignment slack (copies start at a 4-entry boundary)
-    static constexpr int RCSLOT = CH + 16;    // u16 chunk offsets + 8-entry alignment slack
     static size_t bytes(int R, int P) {
         size_t b = 0;
-        b += (size_t)2 * P * sizeof(double);                 // vector panels
+        b += (size_t)kTileNX * P * sizeof(double);           // vector panels
         b += (size_t)kTileNS * SLOT * sizeof(uint32_t);      // ring keys
         b += (size_t)kTileNS * SLOT * sizeof(V);             // ring values
-        b += (size_t)kTileNS * RCSLOT * sizeof(uint16_t);    // ring chunk offsets
+        b += (size_t)kTileNS * kSplitStride * sizeof(uint16_t); // ring split points
         b += (size_t)kTileNS * sizeof(UnitMeta);             // ring unit descriptors
         b += (size_t)R * sizeof(double);                     // row accumulators
         b += (size_t)(kTileMaxNP + 1) * sizeof(uint32_t);    // tile -> unit range of the group
-        b += 16 * sizeof(uint64_t);                          // barriers
+        b += 16 * sizeof(uint64_t);                          // barriers (2*NS + 2*NX <= 16)
         return b;
     }
 };
@@ -90,7 +100,7 @@ __global__ void tile_keys_kernel(int64_t nnz, const int32_t *rowid, const int32_
     for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nnz; k += (int64_t)gridDim.x * blockDim.x) {
         const int32_t r = rowid[k], c = col[k];
         tkey[k] = (uint32_t)(r / R) * (uint32_t)NP + (uint32_t)(c / P);
-        packed[k] = ((uint32_t)(r % R) << 16) | (uint32_t)(c % P);
+        packed[k] = ((uint32_t)(r % R) << 12) | (uint32_t)(c % P);
         pos[k] = (uint32_t)k;
     }
 }
@@ -105,6 +115,16 @@ __global__ void tile_gather_kernel(int64_t nnz, const uint32_t *perm, const uint
     }
 }
 
+// START / END flags: first / last entry of a row inside its tile
+__global__ void tile_flags_kernel(int64_t nnz, const uint32_t *sorted_tkey, uint32_t *keys) {
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nnz; k += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t key = keys[k];
+        const bool start = k == 0 || sorted_tkey[k - 1] != sorted_tkey[k] || key_row(keys[k - 1]) != key_row(key);
+        const bool end = k == nnz - 1 || sorted_tkey[k + 1] != sorted_tkey[k] || key_row(keys[k + 1]) != key_row(key);
+        keys[k] = key | (start ? kKeyStart : 0u) | (end ? kKeyEnd : 0u);
+    }
+}
+
 __global__ void tile_ptr_kernel(int64_t ntiles, int64_t nnz, const uint32_t *sorted_tkey, uint64_t *tile_ptr) {
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t <= ntiles; t += (int64_t)gridDim.x * blockDim.x) {
         int64_t lo = 0, hi = nnz;
@@ -116,283 +136,267 @@ __global__ void tile_ptr_kernel(int64_t ntiles, int64_t nnz, const uint32_t *sor
     }
 }
 
-// Greedy row-chunk / unit segmentation of one tile (sequential per tile).
-// Pass 0 counts (n_rc[t], n_unit[t]); pass 1 writes at the scanned offsets.
-// bad |= 1 if a row has more than CH entries inside one tile.
+// Greedy unit segmentation of one tile (sequential per tile): whole rows are
+// packed into units of <= CH entries.  Pass 0 counts units per tile, pass 1
+// writes them at the scanned offsets.  bad |= 1 if a row has more than CH
+// entries inside one tile (the tiled path is then not used).
 template <int CH>
 __global__ void tile_segment_kernel(int64_t ntiles, const uint64_t *tile_ptr, const uint32_t *keys, int pass,
-                                    uint32_t *n_rc, uint32_t *n_unit, const uint32_t *rc_base,
-                                    const uint32_t *unit_base, uint64_t *unit_start, uint32_t *unit_len,
-                                    uint32_t *unit_rc, uint16_t *rc_off, int *bad) {
+                                    uint32_t *n_unit, const uint32_t *unit_base, uint64_t *unit_start,
+                                    uint32_t *unit_len, int *bad) {
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < ntiles; t += (int64_t)gridDim.x * blockDim.x) {
         const uint64_t t0 = tile_ptr[t], t1 = tile_ptr[t + 1];
-        uint32_t rc = 0, un = 0;
-        const uint32_t rcb = pass ? rc_base[t] : 0, unb = pass ? unit_base[t] : 0;
-        uint64_t us = t0;      // current unit start
-        uint64_t ulen = 0;     // current unit length
-        uint64_t cs = t0;      // current chunk start
-        uint64_t i = t0;
-        auto emit_chunk = [&](uint64_t a, uint64_t b) {
-            if (ulen > 0 && ulen + (b - a) > (uint64_t)CH) {  // close the unit
-                if (pass) { unit_start[unb + un] = us; unit_len[unb + un] = (uint32_t)ulen; }
-                ++un;
-                ulen = 0;
-            }
-            if (ulen == 0) {
-                us = a;
-                if (pass) unit_rc[unb + un] = rcb + rc;
-            }
-            if (pass) rc_off[rcb + rc] = (uint16_t)(a - us);
-            ++rc;
-            ulen = b - us;
-        };
+        uint32_t un = 0;
+        const uint32_t unb = pass ? unit_base[t] : 0;
+        uint64_t us = t0, i = t0;
         while (i < t1) {
-            const uint32_t row = keys[i] >> 16;
             uint64_t j = i + 1;
-            while (j < t1 && (keys[j] >> 16) == row) ++j;
-            const uint64_t rl = j - i;
-            if (rl > (uint64_t)CH) atomicOr(bad, 1);
-            if (rl > 32) {
-                if (i > cs) emit_chunk(cs, i);
-                emit_chunk(i, j);
-                cs = j;
-            } else if (i - cs + rl > 32) {
-                emit_chunk(cs, i);
-                cs = i;
+            while (j < t1 && !(keys[j] & kKeyStart)) ++j;   // row run [i, j)
+            if (j - i > (uint64_t)CH) atomicOr(bad, 1);
+            if (j - us > (uint64_t)CH && i > us) {          // close the unit before this row
+                if (pass) { unit_start[unb + un] = us; unit_len[unb + un] = (uint32_t)(i - us); }
+                ++un;
+                us = i;
             }
             i = j;
         }
-        if (t1 > cs) emit_chunk(cs, t1);
-        if (ulen > 0) {
-            if (pass) { unit_start[unb + un] = us; unit_len[unb + un] = (uint32_t)ulen; }
+        if (t1 > us) {
+            if (pass) { unit_start[unb + un] = us; unit_len[unb + un] = (uint32_t)(t1 - us); }
             ++un;
         }
-        if (!pass) { n_rc[t] = rc; n_unit[t] = un; }
+        if (!pass) n_unit[t] = un;
     }
 }
 
-__global__ void tile_finish_kernel(int64_t ntiles, const uint32_t *n_unit, const uint32_t *unit_base,
-                                   uint32_t total_units, uint32_t total_rc, uint32_t *tile_unit,
-                                   uint32_t *unit_rc) {
-    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t <= ntiles; t += (int64_t)gridDim.x * blockDim.x) {
-        tile_unit[t] = (t < ntiles) ? unit_base[t] : total_units;
-        if (t == ntiles) unit_rc[total_units] = total_rc;
+// per-unit split points for the consumer warps (rows are sorted inside a unit)
+__global__ void tile_split_kernel(int64_t nunits, const uint64_t *unit_start, const uint32_t *unit_len,
+                                  const uint32_t *keys, int R, uint16_t *split) {
+    for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < nunits; u += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t st = unit_start[u];
+        const uint32_t len = unit_len[u];
+        const int rw = (R + kTileConsumerWarps - 1) / kTileConsumerWarps;
+        for (int w = 0; w <= kTileConsumerWarps; ++w) {
+            uint32_t lo = 0, hi = len;
+            const uint32_t bound = (uint32_t)(w * rw);
+            while (lo < hi) {
+                const uint32_t mid = (lo + hi) >> 1;
+                if (key_row(keys[st + mid]) < bound) lo = mid + 1; else hi = mid;
+            }
+            split[u * kSplitStride + w] = (uint16_t)lo;
+        }
+        for (int w = kTileConsumerWarps + 1; w < kSplitStride; ++w) split[u * kSplitStride + w] = 0;
     }
-    (void)n_unit;
+}
+
+__global__ void tile_finish_kernel(int64_t ntiles, const uint32_t *unit_base, uint32_t total_units,
+                                   uint32_t *tile_unit) {
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t <= ntiles; t += (int64_t)gridDim.x * blockDim.x)
+        tile_unit[t] = (t < ntiles) ? unit_base[t] : total_units;
 }
 
 // ---------------------------------------------------------------------------
 // the kernel
 // ---------------------------------------------------------------------------
+__device__ __forceinline__ void tile_item_range(int NP, int H, int h, int &p0, int &p1) {
+    const int per = (NP + H - 1) / H;
+    p0 = h * per;
+    p1 = (p0 + per < NP) ? p0 + per : NP;
+    if (p0 > NP) p0 = NP;
+}
+
 template <typename V, class Epi>
 __global__ void __launch_bounds__(kTileThreads, 1) tile_spmv_kernel(Tiled<V> T, Epi epi, double *part, int64_t *cnt) {
     constexpr int SLOT = TileSmem<V>::SLOT;
-    constexpr int RCSLOT = TileSmem<V>::RCSLOT;
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    double *xbuf = reinterpret_cast<double *>(smem_raw);                              // [2][P]
-    uint32_t *rkeys = reinterpret_cast<uint32_t *>(xbuf + 2 * (size_t)T.P);           // [NS][SLOT]
+    double *xbuf = reinterpret_cast<double *>(smem_raw);                              // [NX][P]
+    uint32_t *rkeys = reinterpret_cast<uint32_t *>(xbuf + kTileNX * (size_t)T.P);     // [NS][SLOT]
     V *rvals = reinterpret_cast<V *>(rkeys + (size_t)kTileNS * SLOT);                 // [NS][SLOT]
-    uint16_t *rrc = reinterpret_cast<uint16_t *>(rvals + (size_t)kTileNS * SLOT);     // [NS][RCSLOT]
-    UnitMeta *rmeta = reinterpret_cast<UnitMeta *>(rrc + (size_t)kTileNS * RCSLOT);   // [NS]
+    uint16_t *rsplit = reinterpret_cast<uint16_t *>(rvals + (size_t)kTileNS * SLOT);  // [NS][kSplitStride]
+    UnitMeta *rmeta = reinterpret_cast<UnitMeta *>(rsplit + (size_t)kTileNS * kSplitStride); // [NS]
     double *acc = reinterpret_cast<double *>(rmeta + kTileNS);                        // [R]
     uint32_t *tu = reinterpret_cast<uint32_t *>(acc + T.R);                           // [NP+1]
     uint64_t *bars = reinterpret_cast<uint64_t *>(tu + kTileMaxNP + 1);
-    uint64_t *ring_full = bars;            // [NS]
-    uint64_t *ring_empty = bars + 4;       // [NS]
-    uint64_t *x_full = bars + 8;           // [2]
-    uint64_t *x_free = bars + 10;          // [2] this CTA's consumers released the slot
-    uint64_t *x_clus = bars + 12;          // [2] (leader) all cluster members released the slot
+    uint64_t *ring_full = bars;                     // [NS]
+    uint64_t *ring_empty = bars + kTileNS;          // [NS]
+    uint64_t *x_full = bars + 2 * kTileNS;          // [NX]
+    uint64_t *x_free = bars + 2 * kTileNS + kTileNX; // [NX]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t rank = cluster_rank();
-    const uint32_t ncl = num_clusters();
-    const uint32_t cid = cluster_id();
-    const int64_t ctas = (int64_t)ncl * kTileCL;
-    const int64_t my = (int64_t)cid * kTileCL + rank;
-    const int rounds = (int)((T.NG + ctas - 1) / ctas);
-    const int P = T.P, NP = T.NP;
+    const int P = T.P, NP = T.NP, H = T.H;
+    const int64_t items = (int64_t)T.NG * H;
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kTileNS; ++s) { mbar_init(ring_full + s, 1); mbar_init(ring_empty + s, 1); }
-        for (int s = 0; s < 2; ++s) { mbar_init(x_full + s, 1); mbar_init(x_free + s, 1); mbar_init(x_clus + s, kTileCL); }
-        fence_mbar_init();
+        for (int s = 0; s < kTileNS; ++s) { mbar_init(ring_full + s, 1); mbar_init(ring_empty + s, kTileConsumerWarps); }
+        for (int s = 0; s < kTileNX; ++s) { mbar_init(x_full + s, 1); mbar_init(x_free + s, kTileConsumerWarps); }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    cluster_sync_all();
 
     if (warp == 0) {
-        // ---------------- ring producer (whole warp: metadata is fetched 32 units at a time) ----------------
+        // ---------------- ring producer (whole warp: metadata fetched 32 units at a time) ----------------
         uint32_t k = 0;
-        for (int rd = 0; rd < rounds; ++rd) {
-            const int64_t g = my + (int64_t)rd * ctas;
-            if (g >= T.NG) continue;
-            const uint32_t u0 = T.tile_unit[g * NP], u1 = T.tile_unit[(g + 1) * NP];
+        for (int64_t w = blockIdx.x; w < items; w += gridDim.x) {
+            const int64_t g = w / H;
+            int p0, p1;
+            tile_item_range(NP, H, (int)(w % H), p0, p1);
+            const uint32_t u0 = T.tile_unit[g * NP + p0], u1 = T.tile_unit[g * NP + p1];
             for (uint32_t ub = u0; ub < u1; ub += 32) {
                 const uint32_t u = ub + lane;
                 uint64_t m_st = 0;
-                uint32_t m_len = 0, m_r0 = 0, m_r1 = 0;
-                if (u < u1) { m_st = T.unit_start[u]; m_len = T.unit_len[u]; m_r0 = T.unit_rc[u]; m_r1 = T.unit_rc[u + 1]; }
+                uint32_t m_len = 0;
+                if (u < u1) { m_st = T.unit_start[u]; m_len = T.unit_len[u]; }
                 const uint32_t nb = (u1 - ub < 32u) ? (u1 - ub) : 32u;
                 for (uint32_t j = 0; j < nb; ++j, ++k) {
                     const uint64_t st = __shfl_sync(0xffffffffu, m_st, j);
                     const uint32_t len = __shfl_sync(0xffffffffu, m_len, j);
-                    const uint32_t r0 = __shfl_sync(0xffffffffu, m_r0, j);
-                    const uint32_t r1 = __shfl_sync(0xffffffffu, m_r1, j);
                     if (lane == 0) {
                         const int s = k % kTileNS;
                         if (k >= (uint32_t)kTileNS) mbar_wait(ring_empty + s, ((k / kTileNS) - 1) & 1);
                         const uint64_t a0 = st & ~(uint64_t)3;
                         const uint64_t a1 = (st + len + 3) & ~(uint64_t)3;
                         const uint32_t n4 = (uint32_t)(a1 - a0);
-                        const uint32_t c0 = r0 & ~7u, c1 = (r1 + 7u) & ~7u;
-                        const uint32_t nrc8 = c1 - c0;
                         UnitMeta m;
-                        m.len = len; m.kdelta = (uint32_t)(st - a0); m.nrc = r1 - r0; m.rdelta = r0 - c0;
+                        m.len = len; m.kdelta = (uint32_t)(st - a0);
                         rmeta[s] = m;
-                        mbar_arrive_expect_tx(ring_full + s,
-                                              n4 * (uint32_t)(sizeof(uint32_t) + sizeof(V)) + nrc8 * 2u);
+                        mbar_arrive_expect_tx(ring_full + s, n4 * (uint32_t)(sizeof(uint32_t) + sizeof(V)) +
+                                                                 kSplitStride * 2u);
                         bulk_g2s(rkeys + (size_t)s * SLOT, T.keys + a0, n4 * sizeof(uint32_t), ring_full + s);
                         bulk_g2s(rvals + (size_t)s * SLOT, T.vals + a0, n4 * (uint32_t)sizeof(V), ring_full + s);
-                        bulk_g2s(rrc + (size_t)s * RCSLOT, T.rc_off + c0, nrc8 * 2u, ring_full + s);
+                        bulk_g2s(rsplit + (size_t)s * kSplitStride, T.unit_split + (size_t)(ub + j) * kSplitStride,
+                                 kSplitStride * 2u, ring_full + s);
                     }
                     __syncwarp();
                 }
             }
         }
     } else if (warp == 1) {
-        // ---------------- vector-panel producer (lockstep across the cluster) ----------------
+        // ---------------- vector-panel producer ----------------
         if (lane == 0) {
-            const int total = rounds * NP;
-            for (int q = 0; q < total; ++q) {
-                const int s = q & 1;
-                const int p = q % NP;
-                const int64_t c0 = (int64_t)p * P;
-                const int64_t n = (T.ncols - c0 < P) ? (T.ncols - c0) : P;
-                const uint32_t bytes = (uint32_t)((n & ~(int64_t)1) * sizeof(double));
-                if (q >= 2) mbar_wait(x_free + s, ((q >> 1) - 1) & 1);
-                mbar_arrive_expect_tx(x_full + s, bytes);
-                mbar_arrive_remote(x_clus + s, 0);
-                if (rank == 0) {
-                    mbar_wait_cluster(x_clus + s, (q >> 1) & 1);
-                    if (bytes > 0)
-                        bulk_g2s_multicast(xbuf + (size_t)s * P, T.vec + c0, bytes, x_full + s,
-                                           (uint16_t)((1u << kTileCL) - 1));
+            int q = 0;
+            for (int64_t w = blockIdx.x; w < items; w += gridDim.x) {
+                int p0, p1;
+                tile_item_range(NP, H, (int)(w % H), p0, p1);
+                for (int p = p0; p < p1; ++p, ++q) {
+                    const int s = q % kTileNX;
+                    const int64_t c0 = (int64_t)p * P;
+                    const int64_t n = (T.ncols - c0 < P) ? (T.ncols - c0) : P;
+                    const uint32_t bytes = (uint32_t)((n & ~(int64_t)1) * sizeof(double));
+                    if (q >= kTileNX) mbar_wait(x_free + s, ((q / kTileNX) - 1) & 1);
+                    mbar_arrive_expect_tx(x_full + s, bytes);
+                    if (bytes > 0) bulk_g2s(xbuf + (size_t)s * P, T.vec + c0, bytes, x_full + s);
                 }
             }
         }
         __syncwarp();
     } else {
-        // ---------------- consumers ----------------
+        // ---------------- consumers: warp cw owns local rows [cw*RW, (cw+1)*RW) ----------------
         const int cw = warp - 2;
         const int ctid = threadIdx.x - 64;
         constexpr uint32_t NCT = 32 * kTileConsumerWarps;
-        uint32_t k = 0;   // unit counter (matches the producer)
-        int q = 0;        // panel counter
-        for (int rd = 0; rd < rounds; ++rd) {
-            const int64_t g = my + (int64_t)rd * ctas;
-            const bool live = g < T.NG;
-            for (int i = ctid; i < T.R; i += NCT) acc[i] = 0.0;
-            if (live)
-                for (int i = ctid; i <= NP; i += NCT) tu[i] = T.tile_unit[g * NP + i];
+        const int RW = (T.R + kTileConsumerWarps - 1) / kTileConsumerWarps;
+        const int my_lo = cw * RW, my_hi = (my_lo + RW < T.R) ? my_lo + RW : T.R;
+        uint32_t k = 0;   // unit counter (matches the ring producer)
+        int q = 0;        // panel counter (matches the panel producer)
+        for (int64_t w = blockIdx.x; w < items; w += gridDim.x) {
+            const int64_t g = w / H;
+            const int h = (int)(w % H);
+            int p0, p1;
+            tile_item_range(NP, H, h, p0, p1);
+            for (int i = my_lo + lane; i < my_hi; i += 32) acc[i] = 0.0;
+            named_bar_sync(1, NCT);   // every warp finished the previous item's tu[] reads
+            for (int i = ctid; i <= p1 - p0; i += NCT) tu[i] = T.tile_unit[g * NP + p0 + i];
             named_bar_sync(1, NCT);
-            for (int p = 0; p < NP; ++p, ++q) {
-                const int s = q & 1;
-                mbar_wait(x_full + s, (q >> 1) & 1);
+            for (int p = p0; p < p1; ++p, ++q) {
+                const int s = q % kTileNX;
+                mbar_wait(x_full + s, (q / kTileNX) & 1);
                 const double *xs = xbuf + (size_t)s * P;
                 const int64_t c0 = (int64_t)p * P;
                 const int64_t n = (T.ncols - c0 < P) ? (T.ncols - c0) : P;
-                if (n & 1) {  // odd tail element is not covered by the 16-byte bulk copy
-                    if (ctid == 0) {
-                        xbuf[(size_t)s * P + n - 1] = T.vec[c0 + n - 1];
-                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                    }
-                    named_bar_sync(1, NCT);
-                }
-                if (live) {
-                    const uint32_t u0 = tu[p], u1 = tu[p + 1];
-                    for (uint32_t u = u0; u < u1; ++u, ++k) {
-                        const int rs = k % kTileNS;
-                        mbar_wait(ring_full + rs, (k / kTileNS) & 1);
-                        const UnitMeta m = rmeta[rs];
-                        const uint32_t *kk = rkeys + (size_t)rs * SLOT + m.kdelta;
-                        const V *vv = rvals + (size_t)rs * SLOT + m.kdelta;
-                        const uint16_t *ro = rrc + (size_t)rs * RCSLOT + m.rdelta;
-                        for (uint32_t rc = cw; rc < m.nrc; rc += kTileConsumerWarps) {
-                            const uint32_t e0 = ro[rc];
-                            const uint32_t e1 = (rc + 1 < m.nrc) ? ro[rc + 1] : m.len;
-                            const uint32_t nn = e1 - e0;
-                            if (nn <= 32) {
-                                const bool valid = lane < (int)nn;
-                                const uint32_t key = valid ? kk[e0 + lane] : 0u;
-                                const int row = valid ? (int)(key >> 16) : -1 - lane;
-                                const int rp = __shfl_up_sync(0xffffffffu, row, 1);
-                                const bool head = valid && (lane == 0 || rp != row);
-                                const uint32_t heads = __ballot_sync(0xffffffffu, head);
-                                const int nseg = __popc(heads);
-                                if (nseg > 4) {
-                                    // one lane per row: sequential left-to-right sum of its entries
-                                    if (lane < nseg) {
-                                        const int b = __fns(heads, 0, lane + 1);
-                                        const int e = (lane + 1 < nseg) ? __fns(heads, 0, lane + 2) : (int)nn;
-                                        const uint32_t k0 = kk[e0 + b];
-                                        double v = (double)vv[e0 + b] * xs[k0 & 0xFFFFu];
-                                        for (int t = b + 1; t < e; ++t) {
-                                            const uint32_t kt = kk[e0 + t];
-                                            v = fma((double)vv[e0 + t], xs[kt & 0xFFFFu], v);
-                                        }
-                                        acc[k0 >> 16] += v;
-                                    }
-                                } else {
-                                    double v = valid ? (double)vv[e0 + lane] * xs[key & 0xFFFFu] : 0.0;
-#pragma unroll
-                                    for (int off = 1; off < 32; off <<= 1) {
-                                        const double vo = __shfl_up_sync(0xffffffffu, v, off);
-                                        const int rw = __shfl_up_sync(0xffffffffu, row, off);
-                                        if (lane >= off && rw == row) v += vo;
-                                    }
-                                    const int rn = __shfl_down_sync(0xffffffffu, row, 1);
-                                    if (valid && (lane == (int)nn - 1 || rn != row)) acc[row] += v;
+                // an odd last panel's final entry is not covered by the 16-byte bulk copy
+                const uint32_t tail_col = (n & 1) ? (uint32_t)(n - 1) : 0xFFFFFFFFu;
+                const double tail_val = (n & 1) ? T.vec[c0 + n - 1] : 0.0;
+                const uint32_t u0 = tu[p - p0], u1 = tu[p - p0 + 1];
+                for (uint32_t u = u0; u < u1; ++u, ++k) {
+                    const int rs = k % kTileNS;
+                    mbar_wait(ring_full + rs, (k / kTileNS) & 1);
+                    const UnitMeta m = rmeta[rs];
+                    const uint32_t *kk = rkeys + (size_t)rs * SLOT + m.kdelta;
+                    const V *vv = rvals + (size_t)rs * SLOT + m.kdelta;
+                    const uint32_t b0 = rsplit[rs * kSplitStride + cw], b1 = rsplit[rs * kSplitStride + cw + 1];
+                    // the lane holding a row's START entry sums the row left to right
+                    for (uint32_t e = b0 + lane; e < b1 + ((32u - ((b1 - b0) & 31u)) & 31u); e += 32) {
+                        if (e < b1) {
+                            uint32_t key = kk[e];
+                            if (key & kKeyStart) {
+                                const uint32_t row = key_row(key);
+                                uint32_t c = key_col(key);
+                                double v = (double)vv[e] * (c == tail_col ? tail_val : xs[c]);
+                                uint32_t t = e;
+                                while (!(key & kKeyEnd)) {
+                                    ++t;
+                                    key = kk[t];
+                                    c = key_col(key);
+                                    v = fma((double)vv[t], (c == tail_col ? tail_val : xs[c]), v);
                                 }
-                            } else {  // one long row
-                                const uint32_t row = kk[e0] >> 16;
-                                double v = 0.0;
-                                for (uint32_t e = e0 + lane; e < e1; e += 32)
-                                    v = fma((double)vv[e], xs[kk[e] & 0xFFFFu], v);
-                                v = warp_sum(v);
-                                if (lane == 0) acc[row] += v;
+                                acc[row] += v;
                             }
                         }
-                        named_bar_sync(1, NCT);
-                        if (ctid == 0) mbar_arrive(ring_empty + rs);
                     }
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(ring_empty + rs);
                 }
-                named_bar_sync(1, NCT);
-                if (ctid == 0) mbar_arrive(x_free + s);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(x_free + s);
             }
-            if (live) {
-                const int64_t rbase = g * (int64_t)T.R;
-                const int64_t rend = (rbase + T.R < T.nrows) ? rbase + T.R : T.nrows;
-                for (int64_t rr = rbase + ctid; rr < rend; rr += NCT) epi(rr, acc[rr - rbase]);
+            // epilogue for this warp's rows
+            const int64_t rbase = g * (int64_t)T.R;
+            const int64_t lo = rbase + my_lo;
+            const int64_t hi0 = rbase + my_hi;
+            const int64_t hi = (hi0 < T.nrows) ? hi0 : T.nrows;
+            if (H == 1) {
+                for (int64_t rr = lo + lane; rr < hi; rr += 32) epi(rr, acc[rr - rbase]);
+            } else {
+                double *dst = T.pout + (size_t)h * T.nrows;
+                for (int64_t rr = lo + lane; rr < hi; rr += 32) dst[rr] = acc[rr - rbase];
             }
-            named_bar_sync(1, NCT);
         }
     }
     __syncwarp();
-    // statistics of the epilogue (only consumers carry nonzero values)
+    if (T.H == 1) {
+        // statistics of the epilogue (only consumers carry nonzero values)
+        if constexpr (Epi::K > 0) {
+            __shared__ double red_sm[Epi::K * (kTileThreads / 32)];
+            double v[Epi::K];
+            epi.flush(v);
+            if (warp < 2)
+#pragma unroll
+                for (int i = 0; i < Epi::K; ++i) v[i] = 0.0;
+            block_sum<Epi::K>(v, red_sm);
+            if (threadIdx.x == 0 && part != nullptr)
+                for (int i = 0; i < Epi::K; ++i) part[(size_t)blockIdx.x * Epi::K + i] = v[i];
+        }
+        if (blockIdx.x == 0 && threadIdx.x == 0 && cnt != nullptr) cnt[0] = gridDim.x;
+    }
+}
+
+// H > 1: rows' partial sums added in ascending h, then the epilogue
+template <class Epi>
+__global__ void __launch_bounds__(kThreads) tile_combine_kernel(int64_t nrows, int H, const double *pout, Epi epi,
+                                                                double *part, int64_t *cnt) {
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < nrows; r += (int64_t)gridDim.x * blockDim.x) {
+        double s = pout[r];
+        for (int h = 1; h < H; ++h) s += pout[(size_t)h * nrows + r];
+        epi(r, s);
+    }
     if constexpr (Epi::K > 0) {
-        __shared__ double red_sm[Epi::K * (kTileThreads / 32)];
+        __shared__ double sm[Epi::K * (kThreads / 32)];
         double v[Epi::K];
         epi.flush(v);
-        if (warp < 2)
-#pragma unroll
-            for (int i = 0; i < Epi::K; ++i) v[i] = 0.0;
-        block_sum<Epi::K>(v, red_sm);
+        block_sum<Epi::K>(v, sm);
         if (threadIdx.x == 0 && part != nullptr)
             for (int i = 0; i < Epi::K; ++i) part[(size_t)blockIdx.x * Epi::K + i] = v[i];
     }
     if (blockIdx.x == 0 && threadIdx.x == 0 && cnt != nullptr) cnt[0] = gridDim.x;
-    __syncthreads();
-    cluster_sync_all();
 }
 
 }  // namespace bsgd

@@ -261,31 +261,56 @@ class SolverState:
         self.mu_eff = cfg.mu
 
     # --- reference-style fields ---------------------------------------------
+    # Reads return numpy arrays backed by pinned host memory (torch's caching
+    # host allocator), so a read -> modify -> assign round trip moves data by
+    # DMA without an extra host copy; each read is a fresh array.
+
+    @staticmethod
+    def _to_host(t) -> np.ndarray:
+        tt = nat.torch()
+        h = tt.empty(t.shape, dtype=tt.float64, pin_memory=True)
+        h.copy_(t, non_blocking=True)
+        tt.cuda.current_stream(t.device).synchronize()
+        return h.numpy()
+
+    def _from_host(self, dst, value, length) -> None:
+        tt = nat.torch()
+        if isinstance(value, tt.Tensor):
+            dst.copy_(nat.as_f64(value, self._dev, length))
+            return
+        arr = np.asarray(value, dtype=np.float64)
+        if arr.shape != (length,):
+            raise ValueError(f"expected vector of length {length}, got {arr.shape}")
+        src = tt.from_numpy(np.ascontiguousarray(arr))
+        pinned = src.is_pinned()
+        dst.copy_(src, non_blocking=pinned)
+        if pinned:  # the caller may reuse its array right away
+            tt.cuda.current_stream(self._dev).synchronize()
 
     @property
     def x(self) -> np.ndarray:
-        return self._x[self._xi].cpu().numpy()
+        return self._to_host(self._x[self._xi])
 
     @x.setter
     def x(self, value) -> None:
-        self._x[self._xi].copy_(nat.as_f64(value, self._dev, self._cols))
+        self._from_host(self._x[self._xi], value, self._cols)
         self._la_valid = False
 
     @property
     def r_vec(self) -> np.ndarray:
-        return self._r[self._ri].cpu().numpy()
+        return self._to_host(self._r[self._ri])
 
     @r_vec.setter
     def r_vec(self, value) -> None:
-        self._r[self._ri].copy_(nat.as_f64(value, self._dev, self._rows))
+        self._from_host(self._r[self._ri], value, self._rows)
 
     @property
     def g(self) -> np.ndarray:
-        return self._g.cpu().numpy()
+        return self._to_host(self._g)
 
     @g.setter
     def g(self, value) -> None:
-        self._g.copy_(nat.as_f64(value, self._dev, self._cols))
+        self._from_host(self._g, value, self._cols)
 
     @property
     def z_cache(self) -> np.ndarray:
