@@ -740,10 +740,23 @@ __global__ void tail_kernel(TailArgs t) {
 // ---------------------------------------------------------------------------
 // prox launch
 // ---------------------------------------------------------------------------
+static size_t prox_dyn_smem() { return sizeof(double) * kPwMaxK * kPwChunk * 128; }
+
+static int prox_occupancy() {
+    static int occ = 0;
+    if (occ == 0) {
+        cudaFuncSetAttribute(fgp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)prox_dyn_smem());
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fgp_kernel, kThreads, prox_dyn_smem());
+        if (occ < 1) occ = 1;
+    }
+    return occ;
+}
+
 static int launch_prox(ProxArgs &a, cudaStream_t st) {
-    const int occ = occupancy(fgp_kernel);
+    const int occ = prox_occupancy();
     int rc = pw_depth(a.N, &a.ds);
     if (rc) return rc;
+    a.fast = (a.N % 128 == 0 && a.N / 128 == ((int64_t)1 << a.ds)) ? 1 : 0;
     // G: a power of two (numpy-order top tree), co-resident, <= 512
     int grid = pow2_floor(std::max<int64_t>(1, std::min<int64_t>((int64_t)occ * num_sms(), 512)));
     const int64_t S = (int64_t)1 << a.ds;
@@ -751,7 +764,7 @@ static int launch_prox(ProxArgs &a, cudaStream_t st) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(kThreads);
-    cfg.dynamicSmemBytes = 0;
+    cfg.dynamicSmemBytes = prox_dyn_smem();
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeCooperative;
@@ -908,7 +921,7 @@ int bsgd_plan_create(bsgd_plan **out, int device, int64_t rows, int64_t cols, in
     p->block_nnz.assign(cnt.begin(), cnt.end());
 #undef PTRY
     // warm occupancy caches outside any graph capture
-    (void)occupancy(fgp_kernel);
+    (void)prox_occupancy();
     *out = p;
     return BSGD_OK;
 }

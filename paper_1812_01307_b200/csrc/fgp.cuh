@@ -38,6 +38,7 @@ struct ProxArgs {
     double w, step, tol;
     int32_t max_iters;
     int32_t ds;            // numpy pairwise depth for N (pw_depth)
+    int32_t fast;          // N == 128 * 2^ds: chunked fast path (pw_cta_fast)
     // outputs -- standalone (tv_prox) mode
     double *out_img;       // NULL in epoch mode
     // outputs -- epoch mode (vector order, fused statistics)
@@ -53,7 +54,10 @@ struct ProxArgs {
     double *dual;          // dual objectives or NULL
 };
 
-__device__ __forceinline__ double ldcg(const double *p) { return __ldcg(p); }
+// Fields rewritten inside the kernel are only read in phases separated from
+// their writes by grid.sync(), which issues MEMBAR.GPU + CCTL.IVALL (checked in
+// the SASS), so plain L1-cached loads are coherent here.
+__device__ __forceinline__ double ldcg(const double *p) { return *p; }
 
 // div p at (s, t): ((pv[s+1] - pv[s]) + ph[t+1]) - ph[t], zero outside (tv.py:124-132)
 __device__ __forceinline__ double div_at(const double *pv, const double *ph, int64_t s, int64_t t,
@@ -101,17 +105,19 @@ __device__ __forceinline__ double tv_term(const double *u, int64_t p, int64_t W,
 // totals.  Term functors may write outputs: each pixel is visited once.
 template <int K, class F>
 __device__ __forceinline__ void np_sum(cg::grid_group &grid, int64_t N, int ds, F &f, double *red, int &round,
-                                       double *sm, double (&out)[K]) {
+                                       double *sm, double (&out)[K], int fast, double *T) {
     double *buf = red + (size_t)(round & 1) * kMaxPartials * 4;
-    pw_cta<K>(N, ds, f, sm, buf);
+    if (fast) pw_cta_fast<K>(ds, f, T, sm, buf);
+    else pw_cta<K>(N, ds, f, sm, buf);
     grid.sync();
     pw_top<K>(ds, gridDim.x, buf, sm, out);
     ++round;
 }
 
-__global__ void __launch_bounds__(kThreads) fgp_kernel(ProxArgs a) {
+__global__ void __launch_bounds__(kThreads, 2) fgp_kernel(ProxArgs a) {
     cg::grid_group grid = cg::this_grid();
     __shared__ double sm[kPwMaxQ * kPwMaxK];
+    extern __shared__ double Tsm[];   // kPwMaxK * kPwChunk * 128 doubles (fast path)
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
     const int64_t N = a.N, W = a.W, H = a.H;
@@ -130,7 +136,7 @@ __global__ void __launch_bounds__(kThreads) fgp_kernel(ProxArgs a) {
             t[0] = rn_mul(bb, bb);
             t[1] = tv_term(b, p, W, false);
         };
-        np_sum<2>(grid, N, a.ds, f0, a.red, round, sm, v2);
+        np_sum<2>(grid, N, a.ds, f0, a.red, round, sm, v2, a.fast, Tsm);
     }
     double phi_prev = v2[0];
     const double tv_b = v2[1];
@@ -153,7 +159,7 @@ __global__ void __launch_bounds__(kThreads) fgp_kernel(ProxArgs a) {
             t[0] = rn_mul(r, r);
         };
         double v1[1];
-        np_sum<1>(grid, N, a.ds, fphi, a.red, round, sm, v1);
+        np_sum<1>(grid, N, a.ds, fphi, a.red, round, sm, v1, a.fast, Tsm);
         double phi = v1[0];
         if (phi > phi_prev) {  // restart from the last accepted point (tv.py:217-231)
             ++restarts;
@@ -164,7 +170,7 @@ __global__ void __launch_bounds__(kThreads) fgp_kernel(ProxArgs a) {
                 cv[p] = x; ch[p] = y;
             }
             grid.sync();
-            np_sum<1>(grid, N, a.ds, fphi, a.red, round, sm, v1);
+            np_sum<1>(grid, N, a.ds, fphi, a.red, round, sm, v1, a.fast, Tsm);
             phi = v1[0];
         }
         // C: momentum commit (tv.py:233-245): q = c + beta (c - p);
@@ -182,7 +188,7 @@ __global__ void __launch_bounds__(kThreads) fgp_kernel(ProxArgs a) {
             t[3] = rn_mul(c1, c1);
         };
         double v4[4];
-        np_sum<4>(grid, N, a.ds, fcom, a.red, round, sm, v4);
+        np_sum<4>(grid, N, a.ds, fcom, a.red, round, sm, v4, a.fast, Tsm);
         double *tv_ = pv; pv = cv; cv = tv_;   // p <- c
         double *th_ = ph; ph = ch; ch = th_;
         phi_prev = (phi_prev < phi) ? phi_prev : phi;  // Python min(phi, phi_prev)
@@ -209,7 +215,7 @@ __global__ void __launch_bounds__(kThreads) fgp_kernel(ProxArgs a) {
         t[1] = tv_term(tmp, p, W, true);
     };
     double e2[2];
-    np_sum<2>(grid, N, a.ds, fen, a.red, round, sm, e2);
+    np_sum<2>(grid, N, a.ds, fen, a.red, round, sm, e2, a.fast, Tsm);
     const double two_w = 2.0 * w;
     const double obj_out = rn_add(e2[0], rn_mul(two_w, e2[1]));
     const double obj_b = rn_add(0.0, rn_mul(two_w, tv_b));

@@ -177,4 +177,71 @@ __device__ __forceinline__ void pw_top(int ds, int G, const double *part, double
     __syncthreads();
 }
 
+// Fast path for N = 128 * 2^ds (every power-of-two image >= 16 x 16): each
+// subtree is one full 128-element leaf.  Terms are produced by all threads in
+// coalesced order into shared memory (kPwChunk leaves at a time), then thread
+// (leaf, j) runs accumulator j's sequential chain over the leaf's 16 strided
+// terms and an 8-lane butterfly forms ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)).
+constexpr int kPwChunk = 16;   // leaves per chunk: K * 16 * 128 doubles of smem
+
+template <int K, class F>
+__device__ __forceinline__ int pw_cta_fast(int ds, F &f, double *T, double *leafv, double *part) {
+    const int64_t S = (int64_t)1 << ds;
+    const int G = gridDim.x;
+    int64_t first;
+    int Q;
+    if (S >= G) {
+        Q = (int)(S / G);
+        first = (int64_t)blockIdx.x * Q;
+    } else {
+        Q = ((int64_t)blockIdx.x < S) ? 1 : 0;
+        first = blockIdx.x;
+    }
+    const int tid = threadIdx.x;
+    const int lane = tid & 31;
+    for (int c0 = 0; c0 < Q; c0 += kPwChunk) {
+        const int nl = (Q - c0 < kPwChunk) ? Q - c0 : kPwChunk;
+        const int npx = nl * 128;
+        const int64_t px0 = (first + c0) * 128;
+        for (int i = tid; i < npx; i += blockDim.x) {
+            double t[K];
+            f(px0 + i, t);
+#pragma unroll
+            for (int k = 0; k < K; ++k) T[k * (kPwChunk * 128) + i] = t[k];
+        }
+        __syncthreads();
+        if (tid < nl * 8) {
+            const int leaf = tid >> 3, j = tid & 7;
+            const unsigned gm = 0xFFu << (lane & 24);
+            double r[K];
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                const double *src = T + k * (kPwChunk * 128) + leaf * 128 + j;
+                double acc = src[0];
+#pragma unroll
+                for (int i = 1; i < 16; ++i) acc = rn_add(acc, src[8 * i]);
+                r[k] = acc;
+            }
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                r[k] = rn_add(r[k], __shfl_xor_sync(gm, r[k], 1, 8));
+                r[k] = rn_add(r[k], __shfl_xor_sync(gm, r[k], 2, 8));
+                r[k] = rn_add(r[k], __shfl_xor_sync(gm, r[k], 4, 8));
+            }
+            if (j == 0)
+#pragma unroll
+                for (int k = 0; k < K; ++k) leafv[(c0 + leaf) * K + k] = r[k];
+        }
+        __syncthreads();
+    }
+    if (Q > 0) {
+        pw_smem_tree<K>(leafv, Q);
+        if (threadIdx.x == 0)
+#pragma unroll
+            for (int k = 0; k < K; ++k) part[(size_t)blockIdx.x * K + k] = leafv[k];
+    }
+    __syncthreads();
+    return Q;
+}
+
 }  // namespace bsgd

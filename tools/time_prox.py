@@ -1,0 +1,49 @@
+"""Time the TV prox kernel at fixed iteration count (non-converging tol) and report GB/s.
+
+    python tools/time_prox.py [--n 512] [--iters 20] [--reps 5]
+"""
+import argparse
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_1812_01307_b200 import tv  # noqa: E402
+
+
+def prox_bytes(n_pix, iters, restarts=0):
+    # per FGP iteration: read q (2 fields) + b, write c (2); read c (2) for phi; read c, p (4), write q (2)
+    # = 11 field passes; setup 5, finalize ~5; restarts add 4
+    return 8 * n_pix * (11 * iters + 4 * restarts + 10)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--n", type=int, default=512)
+    ap.add_argument("--iters", type=int, default=20)
+    ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--weight", type=float, default=0.05)
+    a = ap.parse_args()
+    rng = np.random.default_rng(0)
+    img = torch.tensor(rng.random((a.n, a.n)), device="cuda")
+    st = tv.ProxSettings(a.iters, 1e-300)
+    out, info = tv.tv_prox(img, a.weight, st, return_info=True)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(a.reps):
+        tv.tv_prox(img, a.weight, st)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / a.reps
+    b = prox_bytes(a.n * a.n, info.iterations, info.restarts)
+    print(json.dumps({"n": a.n, "iters": info.iterations, "restarts": info.restarts, "ms": round(ms, 4),
+                      "us_per_iter": round(1000 * ms / info.iterations, 2), "bytes": b,
+                      "gbs": round(b / (ms * 1e6), 1)}))
+
+
+if __name__ == "__main__":
+    main()
