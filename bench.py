@@ -177,7 +177,9 @@ def bytes_model():
     """Algorithmic bytes per launch of the two SpMV kernels (DESIGN.md §Byte model)."""
     nnz = ROWS * NNZ_ROW
     k1 = nnz * (4 + 4) + (ROWS + 1) * 8 + COLS * 8 + 2 * ROWS * 8          # A, rowptr, x once, y in, r out
-    k2 = nnz * (4 + 4) + (COLS + 1) * 8 + ROWS * 8 + 3 * COLS * 8          # A^T, ptr, r once, x in, g + x out
+    # K2 is timed as bsgd_grad (g = 2 A^T r): A^T, ptr, r once, g out; inside the epoch the
+    # step epilogue also reads x_k and writes x_next (+2 * COLS * 8)
+    k2 = nnz * (4 + 4) + (COLS + 1) * 8 + ROWS * 8 + COLS * 8
     return k1, k2
 
 
@@ -303,13 +305,85 @@ def run_ours(args):
                          f"oracle/ C restatement of scipy csr/csc_matvec + numpy epilogue, OpenMP over block pairs"}
         log(f"[bench] cpu oracle: {v:.3f} epochs/s on {info['cores']} threads")
 
+    # The random 8-byte gathers (one per nonzero) are capped by the L1 tag stage at
+    # ~1 distinct sector per SM per cycle (profiles/r01_gather_microbench.md); that
+    # ceiling, not HBM, bounds both products of this random 32-nnz/row system.
+    clk = (clocks or {}).get("sm_mhz") or 1965.0
+    gather_floor_ms = ROWS * NNZ_ROW / (num_sms() * clk * 1e6) * 1e3
+    roofline["gather_ceiling"] = {"gathers_per_launch": ROWS * NNZ_ROW, "loads_per_sm_cycle": 1.0,
+                                  "floor_ms": round(gather_floor_ms, 4),
+                                  "frac_k1": round(gather_floor_ms / t_k1, 3),
+                                  "frac_k2": round(gather_floor_ms / t_k2, 3)}
+    secondary = None
+    if not args.no_ct:
+        secondary = run_ct_secondary(args)
+
     out = {"metric": METRIC, "value": round(value, 2), "unit": "epochs/s", "n_gpus": 1, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": round(ms_per_step, 5), "higher_is_better": True,
            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, configs[1] shapes)",
            "config": config_dict({"parallelism": "single GPU", "mu": mu, "u_max": pw.value}),
            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-           "gpu_launches": 3 * args.steps, "clocks": clocks}
+           "gpu_launches": 3 * args.steps, "clocks": clocks, "secondary": secondary}
     print(json.dumps(out), flush=True)
+
+
+def num_sms():
+    import torch
+    return torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+
+
+def run_ct_secondary(args):
+    """configs[2] (512^2 parallel-beam CT, TV prox on): epochs/s and the prox's GB/s."""
+    import torch
+    from paper_1812_01307_b200 import blockops, problems, solvers, spectral, tv
+    t0 = time.time()
+    d = problems.config(2)
+    log(f"[bench] generated configs[2] in {time.time() - t0:.1f}s: {d.matrix.shape}, nnz={d.matrix.nnz}")
+    op = blockops.BlockOperator(d.matrix, blockops.make_partition(*d.shape, 8, 8))
+    u = spectral.largest_eigenvalue(op, max_iters=50).value
+    mu = 0.9 / (2.0 * u)
+    lay = tv.PixelLayout.row_major(d.height, d.width)
+    cfg = solvers.SolverConfig(mu=mu, lam=d.lam, epochs=10 ** 9, prox=tv.ProxSettings(d.max_inner_iters, 1e-5),
+                               monitor_decrease=False)
+    st = solvers.init_bsgd_state(op, d.y, cfg)
+    steps = max(4, min(args.steps, 20)) // 2 * 2
+    st._ensure_history(steps + 16)
+    for _ in range(3):
+        solvers.bsgd_tv_iteration(st, op, d.y, cfg, layout=lay)
+    runner = solvers._GraphRunner(st, cfg, lay, st._y, 2)
+    assert runner.capture(False)
+    runner.replay()
+    torch.cuda.synchronize()
+    row0 = st._rows_used + 2
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps // 2):
+        runner.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    hist = st._hist[row0:row0 + steps].cpu().numpy()
+    fgp_iters = float(np.mean(hist[:, 5])) if len(hist) else float("nan")
+    # standalone prox at the configured cap (20 iterations, non-converging tol) for GB/s
+    img = torch.rand(d.height, d.width, dtype=torch.float64, device="cuda")
+    pst = tv.ProxSettings(d.max_inner_iters, 1e-300)
+    tv.tv_prox(img, 0.05, pst)
+    torch.cuda.synchronize()
+    p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    p0.record()
+    for _ in range(5):
+        tv.tv_prox(img, 0.05, pst)
+    p1.record()
+    torch.cuda.synchronize()
+    pms = p0.elapsed_time(p1) / 5
+    npx = d.height * d.width
+    pbytes = 8 * npx * (11 * d.max_inner_iters + 10)
+    return {"workload": "configs[2]: 2D parallel-beam CT 512^2, 720x727, lambda=0.01, FGP<=20, M=N=8, float32 values",
+            "nnz": int(d.matrix.nnz), "epochs_per_s": round(1000.0 / ms, 2), "ms_per_epoch": round(ms, 4),
+            "monitor_decrease": False, "mean_fgp_iterations": round(fgp_iters, 2),
+            "tv_prox": {"image": f"{d.height}x{d.width}", "iterations": d.max_inner_iters, "ms": round(pms, 4),
+                        "algorithmic_bytes": pbytes, "gbs": round(pbytes / (pms * 1e6), 1),
+                        "note": "fields are L2-resident; bound by grid barriers / latency, not HBM"}}
 
 
 def run_reference(args):
@@ -337,6 +411,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-ct", action="store_true", help="skip the configs[2] CT secondary measurement")
     ap.add_argument("--cpu-epochs", type=int, default=40)
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     args = ap.parse_args()
