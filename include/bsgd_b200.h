@@ -106,7 +106,17 @@ int bsgd_plan_create(bsgd_plan **out, int device, int64_t rows, int64_t cols, in
                      const int64_t *indptr, const int32_t *indices, const void *values,
                      int value_dtype, int64_t num_row_blocks, int64_t num_col_blocks,
                      const int64_t *row_bounds, const int64_t *col_bounds, void *stream);
+/* same, from a CSR already on the device (e.g. bsgd_siddon_csr output); the
+ * plan ADOPTS the three arrays (they must come from this library's allocator)
+ * and frees them with the plan */
+int bsgd_plan_create_device(bsgd_plan **out, int device, int64_t rows, int64_t cols, int64_t nnz,
+                            int64_t *indptr, int32_t *indices, void *values, int value_dtype,
+                            int64_t num_row_blocks, int64_t num_col_blocks, const int64_t *row_bounds,
+                            const int64_t *col_bounds, void *stream);
 int bsgd_plan_destroy(bsgd_plan *plan);
+/* tocsr (blockops.py:185-186): A's CSR copied to HOST buffers (rows+1, nnz, nnz) */
+int bsgd_plan_csr_copy(const bsgd_plan *plan, int64_t *indptr_out, int32_t *indices_out, void *values_out,
+                       void *stream);
 /* shape / nnz / dtype / device bytes (blockops.py:156-162) */
 int bsgd_plan_info(const bsgd_plan *plan, int64_t *rows, int64_t *cols, int64_t *nnz,
                    int *value_dtype, int64_t *device_bytes);
@@ -145,6 +155,18 @@ int bsgd_pair_products(const bsgd_plan *plan, int64_t n_rows_sel, const int64_t 
                        int64_t n_cols_sel, const int64_t *col_sel, const double *x_k,
                        const double *r_k, const double *y, double *z_cache, double *g,
                        double *r_next, void *stream);
+
+/* --- problem generation on the device ------------------ */
+/* Parallel-beam Siddon intersection-length matrix, (num_angles*num_bins) x n^2,
+ * rows angle-major then bin, bins of unit pitch centred on the axis, columns =
+ * row-major pixels (row 0 at the top) -- the same matrix as
+ * problems.parallel_beam_matrix (bit-identical given the same cos/sin, host).
+ * Allocates device CSR arrays (free with bsgd_device_free or adopt them with
+ * bsgd_plan_create_device). */
+int bsgd_siddon_csr(int device, int64_t n, int64_t num_angles, int64_t num_bins, const double *cos_host,
+                    const double *sin_host, int value_dtype, int64_t **indptr_out, int32_t **indices_out,
+                    void **values_out, int64_t *nnz_out, void *stream);
+int bsgd_device_free(void *ptr);
 
 /* --- total variation (tv.py) ------------------------------------------- */
 size_t bsgd_tv_prox_workspace_bytes(int64_t height, int64_t width);

@@ -52,7 +52,14 @@ _SIGS = {
     "bsgd_device_count": (ctypes.c_int, [ctypes.POINTER(ctypes.c_int)]),
     "bsgd_plan_create": (ctypes.c_int, [ctypes.POINTER(c_p), ctypes.c_int, c_i64, c_i64, c_i64, c_p, c_p, c_p,
                                         ctypes.c_int, c_i64, c_i64, c_p, c_p, c_p]),
+    "bsgd_plan_create_device": (ctypes.c_int, [ctypes.POINTER(c_p), ctypes.c_int, c_i64, c_i64, c_i64, c_p, c_p,
+                                               c_p, ctypes.c_int, c_i64, c_i64, c_p, c_p, c_p]),
     "bsgd_plan_destroy": (ctypes.c_int, [c_p]),
+    "bsgd_plan_csr_copy": (ctypes.c_int, [c_p, c_p, c_p, c_p, c_p]),
+    "bsgd_siddon_csr": (ctypes.c_int, [ctypes.c_int, c_i64, c_i64, c_i64, c_p, c_p, ctypes.c_int,
+                                       ctypes.POINTER(c_p), ctypes.POINTER(c_p), ctypes.POINTER(c_p),
+                                       ctypes.POINTER(c_i64), c_p]),
+    "bsgd_device_free": (ctypes.c_int, [c_p]),
     "bsgd_plan_info": (ctypes.c_int, [c_p, c_p, c_p, c_p, c_p, c_p]),
     "bsgd_plan_block_nnz": (ctypes.c_int, [c_p, c_i64, c_i64, ctypes.POINTER(c_i64)]),
     "bsgd_plan_block_copy": (ctypes.c_int, [c_p, c_i64, c_i64, c_p, c_p, c_p, c_p]),

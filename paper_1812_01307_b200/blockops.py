@@ -156,6 +156,8 @@ class BlockOperator:
             raise ValueError(
                 f"partition covers {partition.rows}x{partition.cols}, matrix is {rows}x{cols}")
         self._csr = csr
+        self._shape = csr.shape
+        self._dtype = csr.dtype
         self._partition = partition
         self._device = nat.require_cuda(device)
         self._nnz_total = int(csr.nnz)
@@ -175,6 +177,60 @@ class BlockOperator:
                      partition.num_row_blocks, partition.num_col_blocks, rb.ctypes.data, cb.ctypes.data,
                      nat.stream_ptr(self._device))
         self._plan = handle
+        self._load_block_table()
+
+    @classmethod
+    def from_parallel_beam(cls, n: int, num_angles: int, num_bins: int, num_row_blocks: int = 1,
+                           num_col_blocks: int = 1, dtype=np.float32, device=None) -> "BlockOperator":
+        """Siddon parallel-beam projector generated on the GPU (`bsgd_siddon_csr`).
+
+        Same matrix as `problems.parallel_beam_matrix` (bit-identical); the host
+        never holds it, so configs[3]-size problems (~2e9 nonzeros) are possible.
+        """
+        import math
+        self = cls.__new__(cls)
+        self._device = nat.require_cuda(device)
+        dt = np.dtype(dtype)
+        ang = [math.pi * a / num_angles for a in range(num_angles)]
+        cs = np.array([math.cos(t) for t in ang], dtype=np.float64)
+        sn = np.array([math.sin(t) for t in ang], dtype=np.float64)
+        rows, cols = num_angles * num_bins, n * n
+        partition = make_partition(rows, cols, num_row_blocks, num_col_blocks)
+        ip, ix, vv = nat.c_p(), nat.c_p(), nat.c_p()
+        nnz = nat.c_i64()
+        t = nat.torch()
+        with t.cuda.device(self._device):
+            st = nat.stream_ptr(self._device)
+            nat.call("bsgd_siddon_csr", self._device.index, n, num_angles, num_bins, cs.ctypes.data, sn.ctypes.data,
+                     dt.itemsize, nat.ctypes.byref(ip), nat.ctypes.byref(ix), nat.ctypes.byref(vv),
+                     nat.ctypes.byref(nnz), st)
+            if nnz.value == 0:
+                for q in (ip, ix, vv):
+                    nat.load().bsgd_device_free(q)
+                raise ValueError("matrix has no nonzeros")
+            rb, cb = partition.row_edges(), partition.col_edges()
+            handle = nat.c_p()
+            rc = nat.load().bsgd_plan_create_device(nat.ctypes.byref(handle), self._device.index, rows, cols,
+                                                    nnz.value, ip, ix, vv, dt.itemsize, partition.num_row_blocks,
+                                                    partition.num_col_blocks, rb.ctypes.data, cb.ctypes.data, st)
+            if rc != nat.OK:
+                for q in (ip, ix, vv):
+                    nat.load().bsgd_device_free(q)
+                nat.check(rc)
+        self._plan = handle
+        self._csr = None
+        self._shape = (rows, cols)
+        self._dtype = dt
+        self._partition = partition
+        self._nnz_total = int(nnz.value)
+        self._nnz_applied = 0
+        self._lock = threading.Lock()
+        self._scratch = None
+        self._load_block_table()
+        return self
+
+    def _load_block_table(self) -> None:
+        partition = self._partition
         nb = partition.num_row_blocks * partition.num_col_blocks
         counts = np.zeros(nb, dtype=np.int64)
         for i in range(partition.num_row_blocks):
@@ -199,7 +255,7 @@ class BlockOperator:
 
     @property
     def shape(self):
-        return self._csr.shape
+        return self._shape
 
     @property
     def nnz(self) -> int:
@@ -223,7 +279,7 @@ class BlockOperator:
 
     @property
     def value_dtype(self):
-        return self._csr.dtype
+        return self._dtype
 
     @property
     def plan(self):
@@ -239,7 +295,7 @@ class BlockOperator:
         nz = int(self._block_nnz[i, j])
         indptr = np.zeros(r1 - r0 + 1, dtype=np.int64)
         indices = np.zeros(max(nz, 1), dtype=np.int32)
-        values = np.zeros(max(nz, 1), dtype=self._csr.dtype)
+        values = np.zeros(max(nz, 1), dtype=self._dtype)
         nat.call("bsgd_plan_block_copy", self._plan, i, j, indptr.ctypes.data, indices.ctypes.data,
                  values.ctypes.data, nat.stream_ptr(self._device))
         return sparse.csr_array((values[:nz], indices[:nz], indptr), shape=(r1 - r0, c1 - c0))
@@ -249,7 +305,7 @@ class BlockOperator:
         rows, cols = self.shape
         indptr = np.zeros(cols + 1, dtype=np.int64)
         indices = np.zeros(self.nnz, dtype=np.int32)
-        values = np.zeros(self.nnz, dtype=self._csr.dtype)
+        values = np.zeros(self.nnz, dtype=self._dtype)
         nat.call("bsgd_plan_transpose_copy", self._plan, indptr.ctypes.data, indices.ctypes.data,
                  values.ctypes.data, nat.stream_ptr(self._device))
         return indptr, indices, values
@@ -258,14 +314,23 @@ class BlockOperator:
         return int(self._block_nnz[i, j])
 
     def to_dense(self) -> np.ndarray:
-        return self._csr.astype(np.float64).toarray()
+        return self.tocsr().astype(np.float64).toarray()
 
     def tocsr(self) -> sparse.csr_array:
+        """Canonical CSR on the host (downloaded once for device-generated operators)."""
+        if self._csr is None:
+            rows, cols = self._shape
+            indptr = np.zeros(rows + 1, dtype=np.int64)
+            indices = np.zeros(self._nnz_total, dtype=np.int32)
+            values = np.zeros(self._nnz_total, dtype=self._dtype)
+            nat.call("bsgd_plan_csr_copy", self._plan, indptr.ctypes.data, indices.ctypes.data, values.ctypes.data,
+                     nat.stream_ptr(self._device))
+            self._csr = sparse.csr_array((values, indices, indptr), shape=self._shape)
         return self._csr
 
     def repartition(self, num_row_blocks: int, num_col_blocks: int) -> "BlockOperator":
         rows, cols = self.shape
-        return BlockOperator(self._csr, make_partition(rows, cols, num_row_blocks, num_col_blocks),
+        return BlockOperator(self.tocsr(), make_partition(rows, cols, num_row_blocks, num_col_blocks),
                              device=self._device)
 
     # --- counter ---------------------------------------------------------

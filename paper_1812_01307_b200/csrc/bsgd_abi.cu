@@ -25,6 +25,7 @@
 #include "fgp.cuh"
 #include "spmv.cuh"
 #include "tiled.cuh"
+#include "siddon.cuh"
 
 using namespace bsgd;
 
@@ -798,74 +799,31 @@ int bsgd_device_count(int *out) {
     return BSGD_OK;
 }
 
-int bsgd_plan_create(bsgd_plan **out, int device, int64_t rows, int64_t cols, int64_t nnz,
-                     const int64_t *indptr, const int32_t *indices, const void *values, int value_dtype,
-                     int64_t num_row_blocks, int64_t num_col_blocks, const int64_t *row_bounds,
-                     const int64_t *col_bounds, void *stream) {
-    if (!out) return fail(BSGD_EINVAL, "out is NULL");
-    *out = nullptr;
-    if (rows < 1 || cols < 1) return fail(BSGD_EINVAL, "matrix dimensions must be positive");
-    if (cols >= ((int64_t)1 << 31) || rows >= ((int64_t)1 << 31))
-        return fail(BSGD_EINVAL, "dimensions must be < 2^31 (int32 indices)");
-    if (nnz == 0) return fail(BSGD_EINVAL, "matrix has no nonzeros");
-    if (nnz < 0 || nnz >= ((int64_t)1 << 32)) return fail(BSGD_EINVAL, "nnz %lld out of range", (long long)nnz);
-    if (value_dtype != BSGD_F32 && value_dtype != BSGD_F64) return fail(BSGD_EINVAL, "value dtype must be 4 or 8");
-    if (!indptr || !indices || !values || !row_bounds || !col_bounds) return fail(BSGD_EINVAL, "NULL array");
-    if (indptr[0] != 0 || indptr[rows] != nnz) return fail(BSGD_EINVAL, "indptr must run from 0 to nnz");
-    if (num_row_blocks < 1 || num_row_blocks > rows) return fail(BSGD_EINVAL, "row block count not in [1, rows]");
-    if (num_col_blocks < 1 || num_col_blocks > cols) return fail(BSGD_EINVAL, "col block count not in [1, cols]");
-    for (int64_t i = 0; i < num_row_blocks; ++i)
-        if (row_bounds[i + 1] <= row_bounds[i]) return fail(BSGD_EINVAL, "row ranges must be nonempty and ascending");
-    for (int64_t j = 0; j < num_col_blocks; ++j)
-        if (col_bounds[j + 1] <= col_bounds[j]) return fail(BSGD_EINVAL, "col ranges must be nonempty and ascending");
-    if (row_bounds[0] != 0 || col_bounds[0] != 0) return fail(BSGD_EINVAL, "ranges must start at 0");
-    if (row_bounds[num_row_blocks] != rows || col_bounds[num_col_blocks] != cols)
-        return fail(BSGD_EINVAL, "partition covers %lldx%lld, matrix is %lldx%lld",
-                    (long long)row_bounds[num_row_blocks], (long long)col_bounds[num_col_blocks],
-                    (long long)rows, (long long)cols);
-    int ndev = 0;
-    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
-        cudaGetLastError();
-        return fail(BSGD_ECUDA, "no CUDA device available");
-    }
-    if (device < 0 || device >= ndev) return fail(BSGD_EINVAL, "device %d out of range", device);
-    DeviceGuard guard(device);
-    cudaStream_t st = (cudaStream_t)stream;
-    bsgd_plan *p = new bsgd_plan();
-    p->device = device;
-    p->rows = rows; p->cols = cols; p->nnz = nnz; p->vdt = value_dtype;
-    p->M = num_row_blocks; p->N = num_col_blocks;
-    p->row_bounds.assign(row_bounds, row_bounds + num_row_blocks + 1);
-    p->col_bounds.assign(col_bounds, col_bounds + num_col_blocks + 1);
-    const double mean_r = (double)nnz / rows, mean_c = (double)nnz / cols;
-    p->g_fwd = mean_r < 64.0 ? 8 : 32;
-    p->g_tr = mean_c < 64.0 ? 8 : 32;
+// everything after A's CSR is on the device: validation, A^T, tiled copies, block table
+static int plan_finish(bsgd_plan *p, cudaStream_t st) {
+    const int64_t rows = p->rows, cols = p->cols, nnz = p->nnz;
+    const int value_dtype = p->vdt;
+    const int64_t num_row_blocks = p->M, num_col_blocks = p->N;
     int rc = BSGD_OK;
 #define PTRY(call)                                                                         \
     do {                                                                                   \
         cudaError_t e_ = (call);                                                           \
         if (e_ != cudaSuccess) {                                                           \
-            rc = fail(e_ == cudaErrorMemoryAllocation ? BSGD_ENOMEM : BSGD_ECUDA,          \
-                      "%s failed: %s", #call, cudaGetErrorString(e_));                     \
-            plan_free(p);                                                                  \
-            return rc;                                                                     \
+            return fail(e_ == cudaErrorMemoryAllocation ? BSGD_ENOMEM : BSGD_ECUDA,        \
+                        "%s failed: %s", #call, cudaGetErrorString(e_));                   \
         }                                                                                  \
     } while (0)
     const size_t vb = (size_t)value_dtype;
-    PTRY(cudaMalloc(&p->f_ptr, sizeof(int64_t) * (rows + 1)));
-    PTRY(cudaMalloc(&p->f_idx, sizeof(int32_t) * nnz));
-    PTRY(cudaMalloc(&p->f_val, vb * nnz));
     PTRY(cudaMalloc(&p->t_ptr, sizeof(int64_t) * (cols + 1)));
     PTRY(cudaMalloc(&p->t_idx, sizeof(int32_t) * nnz));
     PTRY(cudaMalloc(&p->t_val, vb * nnz));
     PTRY(cudaMalloc(&p->d_row_bounds, sizeof(int64_t) * (num_row_blocks + 1)));
     PTRY(cudaMalloc(&p->d_col_bounds, sizeof(int64_t) * (num_col_blocks + 1)));
     p->device_bytes = sizeof(int64_t) * (rows + cols + 2) + 2 * (sizeof(int32_t) + vb) * nnz;
-    PTRY(cudaMemcpyAsync(p->f_ptr, indptr, sizeof(int64_t) * (rows + 1), cudaMemcpyHostToDevice, st));
-    PTRY(cudaMemcpyAsync(p->f_idx, indices, sizeof(int32_t) * nnz, cudaMemcpyHostToDevice, st));
-    PTRY(cudaMemcpyAsync(p->f_val, values, vb * nnz, cudaMemcpyHostToDevice, st));
-    PTRY(cudaMemcpyAsync(p->d_row_bounds, row_bounds, sizeof(int64_t) * (num_row_blocks + 1), cudaMemcpyHostToDevice, st));
-    PTRY(cudaMemcpyAsync(p->d_col_bounds, col_bounds, sizeof(int64_t) * (num_col_blocks + 1), cudaMemcpyHostToDevice, st));
+    PTRY(cudaMemcpyAsync(p->d_row_bounds, p->row_bounds.data(), sizeof(int64_t) * (num_row_blocks + 1),
+                         cudaMemcpyHostToDevice, st));
+    PTRY(cudaMemcpyAsync(p->d_col_bounds, p->col_bounds.data(), sizeof(int64_t) * (num_col_blocks + 1),
+                         cudaMemcpyHostToDevice, st));
     // structural check (canonical form: sorted unique in-range indices per row)
     int *d_bad = nullptr;
     PTRY(cudaMalloc(&d_bad, sizeof(int)));
@@ -876,11 +834,10 @@ int bsgd_plan_create(bsgd_plan **out, int device, int64_t rows, int64_t cols, in
     PTRY(cudaStreamSynchronize(st));
     cudaFree(d_bad);
     if (bad) {
-        plan_free(p);
         return fail(BSGD_EINVAL, "CSR is not canonical (code %d: 1=indptr, 2=index range, 4=unsorted/duplicate)", bad);
     }
     rc = (value_dtype == BSGD_F32) ? build_transpose<float>(p, st) : build_transpose<double>(p, st);
-    if (rc != BSGD_OK) { plan_free(p); return rc; }
+    if (rc != BSGD_OK) return rc;
     {
         const char *env = getenv("BSGD_TILED");
         p->use_tiled = !(env && env[0] == '0');
@@ -893,7 +850,7 @@ int bsgd_plan_create(bsgd_plan **out, int device, int64_t rows, int64_t cols, in
             rc = build_tiled<double>(p->tf, rows, cols, nnz, p->f_ptr, p->f_idx, (const double *)p->f_val, st);
             if (!rc) rc = build_tiled<double>(p->tt, cols, rows, nnz, p->t_ptr, p->t_idx, (const double *)p->t_val, st);
         }
-        if (rc != BSGD_OK) { plan_free(p); return rc; }
+        if (rc != BSGD_OK) return rc;
         const char *force = getenv("BSGD_TILED");
         if (!(force && force[0] == '2')) {  // BSGD_TILED=2 keeps the tiled path without timing it
             if (value_dtype == BSGD_F32) {
@@ -903,7 +860,7 @@ int bsgd_plan_create(bsgd_plan **out, int device, int64_t rows, int64_t cols, in
                 rc = autotune_direction<double>(p, false, st);
                 if (!rc) rc = autotune_direction<double>(p, true, st);
             }
-            if (rc != BSGD_OK) { plan_free(p); return rc; }
+            if (rc != BSGD_OK) return rc;
         }
         p->device_bytes += p->tf.bytes + p->tt.bytes;
     }
@@ -922,7 +879,189 @@ int bsgd_plan_create(bsgd_plan **out, int device, int64_t rows, int64_t cols, in
 #undef PTRY
     // warm occupancy caches outside any graph capture
     (void)prox_occupancy();
+    // warm occupancy caches outside any graph capture
+    (void)prox_occupancy();
+    return BSGD_OK;
+}
+
+static int plan_args_check(int64_t rows, int64_t cols, int64_t nnz, int value_dtype, int64_t num_row_blocks,
+                           int64_t num_col_blocks, const int64_t *row_bounds, const int64_t *col_bounds, int device) {
+    if (rows < 1 || cols < 1) return fail(BSGD_EINVAL, "matrix dimensions must be positive");
+    if (cols >= ((int64_t)1 << 31) || rows >= ((int64_t)1 << 31))
+        return fail(BSGD_EINVAL, "dimensions must be < 2^31 (int32 indices)");
+    if (nnz == 0) return fail(BSGD_EINVAL, "matrix has no nonzeros");
+    if (nnz < 0 || nnz >= ((int64_t)1 << 32)) return fail(BSGD_EINVAL, "nnz %lld out of range", (long long)nnz);
+    if (value_dtype != BSGD_F32 && value_dtype != BSGD_F64) return fail(BSGD_EINVAL, "value dtype must be 4 or 8");
+    if (!row_bounds || !col_bounds) return fail(BSGD_EINVAL, "NULL partition bounds");
+    if (num_row_blocks < 1 || num_row_blocks > rows) return fail(BSGD_EINVAL, "row block count not in [1, rows]");
+    if (num_col_blocks < 1 || num_col_blocks > cols) return fail(BSGD_EINVAL, "col block count not in [1, cols]");
+    for (int64_t i = 0; i < num_row_blocks; ++i)
+        if (row_bounds[i + 1] <= row_bounds[i]) return fail(BSGD_EINVAL, "row ranges must be nonempty and ascending");
+    for (int64_t j = 0; j < num_col_blocks; ++j)
+        if (col_bounds[j + 1] <= col_bounds[j]) return fail(BSGD_EINVAL, "col ranges must be nonempty and ascending");
+    if (row_bounds[0] != 0 || col_bounds[0] != 0) return fail(BSGD_EINVAL, "ranges must start at 0");
+    if (row_bounds[num_row_blocks] != rows || col_bounds[num_col_blocks] != cols)
+        return fail(BSGD_EINVAL, "partition covers %lldx%lld, matrix is %lldx%lld",
+                    (long long)row_bounds[num_row_blocks], (long long)col_bounds[num_col_blocks],
+                    (long long)rows, (long long)cols);
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return fail(BSGD_ECUDA, "no CUDA device available");
+    }
+    if (device < 0 || device >= ndev) return fail(BSGD_EINVAL, "device %d out of range", device);
+    return BSGD_OK;
+}
+
+static bsgd_plan *plan_new(int device, int64_t rows, int64_t cols, int64_t nnz, int value_dtype, int64_t M,
+                           int64_t N, const int64_t *row_bounds, const int64_t *col_bounds) {
+    bsgd_plan *p = new bsgd_plan();
+    p->device = device;
+    p->rows = rows; p->cols = cols; p->nnz = nnz; p->vdt = value_dtype;
+    p->M = M; p->N = N;
+    p->row_bounds.assign(row_bounds, row_bounds + M + 1);
+    p->col_bounds.assign(col_bounds, col_bounds + N + 1);
+    const double mean_r = (double)nnz / rows, mean_c = (double)nnz / cols;
+    p->g_fwd = mean_r < 64.0 ? 8 : 32;
+    p->g_tr = mean_c < 64.0 ? 8 : 32;
+    return p;
+}
+
+int bsgd_plan_create(bsgd_plan **out, int device, int64_t rows, int64_t cols, int64_t nnz,
+                     const int64_t *indptr, const int32_t *indices, const void *values, int value_dtype,
+                     int64_t num_row_blocks, int64_t num_col_blocks, const int64_t *row_bounds,
+                     const int64_t *col_bounds, void *stream) {
+    if (!out) return fail(BSGD_EINVAL, "out is NULL");
+    *out = nullptr;
+    int rc = plan_args_check(rows, cols, nnz, value_dtype, num_row_blocks, num_col_blocks, row_bounds, col_bounds,
+                             device);
+    if (rc) return rc;
+    if (!indptr || !indices || !values) return fail(BSGD_EINVAL, "NULL array");
+    if (indptr[0] != 0 || indptr[rows] != nnz) return fail(BSGD_EINVAL, "indptr must run from 0 to nnz");
+    DeviceGuard guard(device);
+    cudaStream_t st = (cudaStream_t)stream;
+    bsgd_plan *p = plan_new(device, rows, cols, nnz, value_dtype, num_row_blocks, num_col_blocks, row_bounds,
+                            col_bounds);
+    const size_t vb = (size_t)value_dtype;
+    cudaError_t e = cudaSuccess;
+    if (e == cudaSuccess) e = cudaMalloc(&p->f_ptr, sizeof(int64_t) * (rows + 1));
+    if (e == cudaSuccess) e = cudaMalloc(&p->f_idx, sizeof(int32_t) * nnz);
+    if (e == cudaSuccess) e = cudaMalloc(&p->f_val, vb * nnz);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(p->f_ptr, indptr, sizeof(int64_t) * (rows + 1), cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(p->f_idx, indices, sizeof(int32_t) * nnz, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(p->f_val, values, vb * nnz, cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) {
+        plan_free(p);
+        return fail(e == cudaErrorMemoryAllocation ? BSGD_ENOMEM : BSGD_ECUDA, "plan upload failed: %s",
+                    cudaGetErrorString(e));
+    }
+    rc = plan_finish(p, st);
+    if (rc) { plan_free(p); return rc; }
     *out = p;
+    return BSGD_OK;
+}
+
+int bsgd_plan_create_device(bsgd_plan **out, int device, int64_t rows, int64_t cols, int64_t nnz, int64_t *indptr,
+                            int32_t *indices, void *values, int value_dtype, int64_t num_row_blocks,
+                            int64_t num_col_blocks, const int64_t *row_bounds, const int64_t *col_bounds,
+                            void *stream) {
+    if (!out) return fail(BSGD_EINVAL, "out is NULL");
+    *out = nullptr;
+    int rc = plan_args_check(rows, cols, nnz, value_dtype, num_row_blocks, num_col_blocks, row_bounds, col_bounds,
+                             device);
+    if (rc) return rc;
+    if (!indptr || !indices || !values) return fail(BSGD_EINVAL, "NULL array");
+    DeviceGuard guard(device);
+    cudaStream_t st = (cudaStream_t)stream;
+    int64_t ends[2] = {-1, -1};
+    CU(cudaMemcpyAsync(&ends[0], indptr, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(&ends[1], indptr + rows, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    if (ends[0] != 0 || ends[1] != nnz) return fail(BSGD_EINVAL, "indptr must run from 0 to nnz");
+    bsgd_plan *p = plan_new(device, rows, cols, nnz, value_dtype, num_row_blocks, num_col_blocks, row_bounds,
+                            col_bounds);
+    p->f_ptr = indptr;   // adopted: freed with the plan
+    p->f_idx = indices;
+    p->f_val = values;
+    rc = plan_finish(p, st);
+    if (rc) { plan_free(p); return rc; }
+    *out = p;
+    return BSGD_OK;
+}
+
+int bsgd_siddon_csr(int device, int64_t n, int64_t num_angles, int64_t num_bins, const double *cos_host,
+                    const double *sin_host, int value_dtype, int64_t **indptr_out, int32_t **indices_out,
+                    void **values_out, int64_t *nnz_out, void *stream) {
+    if (n < 1 || num_angles < 1 || num_bins < 1 || !cos_host || !sin_host || !indptr_out || !indices_out ||
+        !values_out || !nnz_out)
+        return fail(BSGD_EINVAL, "bad siddon arguments");
+    if (n * n >= ((int64_t)1 << 31)) return fail(BSGD_EINVAL, "image too large for int32 column indices");
+    if (value_dtype != BSGD_F32 && value_dtype != BSGD_F64) return fail(BSGD_EINVAL, "value dtype must be 4 or 8");
+    DeviceGuard guard(device);
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t nrays = num_angles * num_bins;
+    double *ct = nullptr, *sn = nullptr;
+    int64_t *counts = nullptr, *indptr = nullptr;
+    int32_t *idx = nullptr;
+    void *vals = nullptr, *temp = nullptr;
+    size_t temp_bytes = 0;
+    int rc = BSGD_OK;
+    auto cleanup = [&]() { cudaFree(ct); cudaFree(sn); cudaFree(counts); cudaFree(temp); };
+#define STRY(call)                                                                          \
+    do {                                                                                    \
+        cudaError_t e_ = (call);                                                            \
+        if (e_ != cudaSuccess) {                                                            \
+            rc = fail(e_ == cudaErrorMemoryAllocation ? BSGD_ENOMEM : BSGD_ECUDA,           \
+                      "siddon: %s failed: %s", #call, cudaGetErrorString(e_));              \
+            cleanup(); cudaFree(indptr); cudaFree(idx); cudaFree(vals);                     \
+            return rc;                                                                      \
+        }                                                                                   \
+    } while (0)
+    STRY(cudaMalloc(&ct, sizeof(double) * num_angles));
+    STRY(cudaMalloc(&sn, sizeof(double) * num_angles));
+    STRY(cudaMemcpyAsync(ct, cos_host, sizeof(double) * num_angles, cudaMemcpyHostToDevice, st));
+    STRY(cudaMemcpyAsync(sn, sin_host, sizeof(double) * num_angles, cudaMemcpyHostToDevice, st));
+    STRY(cudaMalloc(&counts, sizeof(int64_t) * (nrays + 1)));
+    STRY(cudaMalloc(&indptr, sizeof(int64_t) * (nrays + 1)));
+    RayGeom G{n, num_bins, nrays, ct, sn};
+    siddon_count_kernel<<<grid_1d(nrays, 128), 128, 0, st>>>(G, counts);
+    STRY(cudaMemsetAsync(counts + nrays, 0, sizeof(int64_t), st));
+    STRY(cub::DeviceScan::ExclusiveSum(nullptr, temp_bytes, counts, indptr, nrays + 1, st));
+    STRY(cudaMalloc(&temp, temp_bytes));
+    STRY(cub::DeviceScan::ExclusiveSum(temp, temp_bytes, counts, indptr, nrays + 1, st));
+    int64_t nnz = 0;
+    STRY(cudaMemcpyAsync(&nnz, indptr + nrays, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    STRY(cudaStreamSynchronize(st));
+    STRY(cudaMalloc(&idx, sizeof(int32_t) * std::max<int64_t>(nnz, 1)));
+    STRY(cudaMalloc(&vals, (size_t)value_dtype * std::max<int64_t>(nnz, 1)));
+    if (value_dtype == BSGD_F32)
+        siddon_fill_kernel<float><<<grid_1d(nrays, 128), 128, 0, st>>>(G, indptr, idx, (float *)vals);
+    else
+        siddon_fill_kernel<double><<<grid_1d(nrays, 128), 128, 0, st>>>(G, indptr, idx, (double *)vals);
+    STRY(cudaGetLastError());
+    STRY(cudaStreamSynchronize(st));
+#undef STRY
+    cleanup();
+    *indptr_out = indptr;
+    *indices_out = idx;
+    *values_out = vals;
+    *nnz_out = nnz;
+    return BSGD_OK;
+}
+
+int bsgd_device_free(void *ptr) {
+    if (ptr) CU(cudaFree(ptr));
+    return BSGD_OK;
+}
+
+int bsgd_plan_csr_copy(const bsgd_plan *p, int64_t *indptr_out, int32_t *indices_out, void *values_out, void *stream) {
+    if (!p || !indptr_out || !indices_out || !values_out) return fail(BSGD_EINVAL, "NULL argument");
+    DeviceGuard guard(p->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    CU(cudaMemcpyAsync(indptr_out, p->f_ptr, sizeof(int64_t) * (p->rows + 1), cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(indices_out, p->f_idx, sizeof(int32_t) * p->nnz, cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(values_out, p->f_val, (size_t)p->vdt * p->nnz, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
     return BSGD_OK;
 }
 

@@ -260,3 +260,58 @@ def config(index: int, scale: float = 1.0) -> ProblemData:
         nb = max(9, int(round(1449 * scale)) | 1)
         return ct_problem("C4", n, ang, nb, 60, 0.005, 8, 0.01, 20, 50, np.float32)
     raise ValueError(f"config index {index} has no host generator (3D config needs the device generator)")
+
+
+# --- device-generated instances (configs[3]-size) -------------
+
+
+@dataclass
+class DeviceProblem:
+    """CT instance whose projector lives only on the GPU (no host CSR)."""
+
+    name: str
+    op: object                      # blockops.BlockOperator built by from_parallel_beam
+    y: np.ndarray                   # float64 measurements (host copy, rows doubles)
+    x_true: np.ndarray
+    height: int
+    width: int
+    num_row_blocks: int
+    num_col_blocks: int
+    lam: float
+    max_inner_iters: int
+    epochs: int
+    seeds: dict
+
+
+def ct_problem_device(name: str, n: int, num_angles: int, num_bins: int, num_ellipses: int, noise_frac: float,
+                      num_blocks: int, lam: float, max_inner_iters: int, epochs: int, dtype=np.float32,
+                      phantom_seed: int = 0, noise_seed: int = 1, device=None) -> DeviceProblem:
+    """Same instance definition as `ct_problem`, with A generated and kept on the GPU.
+
+    y = A x_true is formed by the device SpMV (float64 accumulation), so it may
+    differ from the host path's scipy product in the last bits; the noise draw
+    is the same seeded numpy stream.
+    """
+    from .blockops import BlockOperator
+    op = BlockOperator.from_parallel_beam(n, num_angles, num_bins, num_blocks, num_blocks, dtype=dtype,
+                                          device=device)
+    x_true = ellipse_phantom(n, num_ellipses, phantom_seed).ravel()
+    clean = op.matvec(x_true, charge=False)
+    sigma = noise_frac * float(np.max(clean))
+    noise = np.random.default_rng(noise_seed).standard_normal(clean.shape[0]) * sigma
+    return DeviceProblem(name, op, clean + noise, x_true, n, n, num_blocks, num_blocks, lam, max_inner_iters,
+                         epochs, {"phantom": phantom_seed, "noise": noise_seed, "solver": 0})
+
+
+def config_device(index: int, scale: float = 1.0, device=None) -> DeviceProblem:
+    """configs[0], [2] or [3] with the projector generated on the GPU."""
+    table = {0: ("C1", 128, 180, 183, 10, 0.01, 4, 0.02, 20, 100, np.float64),
+             2: ("C3", 512, 720, 727, 30, 0.005, 8, 0.01, 20, 100, np.float32),
+             3: ("C4", 1024, 1440, 1449, 60, 0.005, 8, 0.01, 20, 50, np.float32)}
+    if index not in table:
+        raise ValueError(f"config index {index} is not a 2D CT configuration")
+    name, n, ang, nb, ell, noise, blocks, lam, inner, epochs, dt = table[index]
+    n = max(16, int(round(n * scale)))
+    ang = max(8, int(round(ang * scale)))
+    nb = max(9, int(round(nb * scale)) | 1)
+    return ct_problem_device(name, n, ang, nb, ell, noise, blocks, lam, inner, epochs, dt, device=device)
