@@ -843,12 +843,17 @@ static int plan_finish(bsgd_plan *p, cudaStream_t st) {
         p->use_tiled = !(env && env[0] == '0');
     }
     if (p->use_tiled) {
+        // the tiled kernel sums each tile row with one lane: only short rows can win
+        // (autotune below decides); long-row (CT) directions keep the CSR kernel
+        const bool fwd_short = (double)nnz / rows <= 64.0, tr_short = (double)nnz / cols <= 64.0;
         if (value_dtype == BSGD_F32) {
-            rc = build_tiled<float>(p->tf, rows, cols, nnz, p->f_ptr, p->f_idx, (const float *)p->f_val, st);
-            if (!rc) rc = build_tiled<float>(p->tt, cols, rows, nnz, p->t_ptr, p->t_idx, (const float *)p->t_val, st);
+            if (fwd_short) rc = build_tiled<float>(p->tf, rows, cols, nnz, p->f_ptr, p->f_idx, (const float *)p->f_val, st);
+            if (!rc && tr_short)
+                rc = build_tiled<float>(p->tt, cols, rows, nnz, p->t_ptr, p->t_idx, (const float *)p->t_val, st);
         } else {
-            rc = build_tiled<double>(p->tf, rows, cols, nnz, p->f_ptr, p->f_idx, (const double *)p->f_val, st);
-            if (!rc) rc = build_tiled<double>(p->tt, cols, rows, nnz, p->t_ptr, p->t_idx, (const double *)p->t_val, st);
+            if (fwd_short) rc = build_tiled<double>(p->tf, rows, cols, nnz, p->f_ptr, p->f_idx, (const double *)p->f_val, st);
+            if (!rc && tr_short)
+                rc = build_tiled<double>(p->tt, cols, rows, nnz, p->t_ptr, p->t_idx, (const double *)p->t_val, st);
         }
         if (rc != BSGD_OK) return rc;
         const char *force = getenv("BSGD_TILED");
