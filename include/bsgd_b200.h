@@ -92,6 +92,8 @@ typedef struct bsgd_epoch_args {
     void *workspace;          /* device, bsgd_epoch_workspace_bytes(), zero-filled once */
     size_t workspace_bytes;
     uint32_t flags;
+    int64_t depth;            /* volumes (configs[4]): depth*height*width == cols, 3D TV;
+                                 0 or 1 = image (2D TV, the reference's tv.py) */
 } bsgd_epoch_args;
 
 /* --- library ----------------------------------------------------------- */
@@ -183,6 +185,21 @@ int bsgd_discrete_gradient(int64_t height, int64_t width, const double *img, dou
                            void *stream);
 int bsgd_discrete_divergence(int64_t height, int64_t width, const double *pv, const double *ph,
                              double *out, void *stream);
+
+/* 3D isotropic TV for volumes (z-major, then rows, then columns).  The reference
+ * has 2D TV only (tv.py:28-56); these extend its conventions one axis up:
+ * backward differences along z/rows/columns, div = negative adjoint, dual step
+ * 1/(12 w), the same restart / stop / fallback rules (oracle/oracle.py tv_prox3). */
+size_t bsgd_tv_prox3_workspace_bytes(int64_t depth, int64_t height, int64_t width);
+int bsgd_tv_prox3(int64_t depth, int64_t height, int64_t width, const double *vol, double *out, double weight,
+                  int32_t max_inner_iters, double tol, void *workspace, size_t workspace_bytes,
+                  bsgd_prox_info *info_out, double *dual_objectives, void *stream);
+int bsgd_tv_value3(int64_t depth, int64_t height, int64_t width, const double *vol, double *out, void *scratch,
+                   void *stream);
+int bsgd_discrete_gradient3(int64_t depth, int64_t height, int64_t width, const double *vol, double *dz,
+                            double *dv, double *dh, void *stream);
+int bsgd_discrete_divergence3(int64_t depth, int64_t height, int64_t width, const double *pz, const double *pv,
+                              const double *ph, double *out, void *stream);
 
 /* --- reductions (metrics.py, solvers.py:198-215, :517-518) ------------ */
 /* out = sum_k a[k] * b[k]  (deterministic order); device scalar */

@@ -41,7 +41,7 @@ class EpochArgs(ctypes.Structure):
         ("max_inner_iters", ctypes.c_int32), ("tol", ctypes.c_double), ("f_curr", c_p),
         ("history", c_p), ("epoch_counter", c_p), ("history_capacity", c_i64),
         ("dual_objectives", c_p), ("workspace", c_p), ("workspace_bytes", ctypes.c_size_t),
-        ("flags", ctypes.c_uint32),
+        ("flags", ctypes.c_uint32), ("depth", c_i64),
     ]
 
 
@@ -77,6 +77,12 @@ _SIGS = {
     "bsgd_tv_value": (ctypes.c_int, [c_i64, c_i64, c_p, c_p, c_p, c_p]),
     "bsgd_discrete_gradient": (ctypes.c_int, [c_i64, c_i64, c_p, c_p, c_p, c_p]),
     "bsgd_discrete_divergence": (ctypes.c_int, [c_i64, c_i64, c_p, c_p, c_p, c_p]),
+    "bsgd_tv_prox3_workspace_bytes": (ctypes.c_size_t, [c_i64, c_i64, c_i64]),
+    "bsgd_tv_prox3": (ctypes.c_int, [c_i64, c_i64, c_i64, c_p, c_p, ctypes.c_double, ctypes.c_int32,
+                                     ctypes.c_double, c_p, ctypes.c_size_t, c_p, c_p, c_p]),
+    "bsgd_tv_value3": (ctypes.c_int, [c_i64, c_i64, c_i64, c_p, c_p, c_p, c_p]),
+    "bsgd_discrete_gradient3": (ctypes.c_int, [c_i64, c_i64, c_i64, c_p, c_p, c_p, c_p, c_p]),
+    "bsgd_discrete_divergence3": (ctypes.c_int, [c_i64, c_i64, c_i64, c_p, c_p, c_p, c_p, c_p]),
     "bsgd_dot": (ctypes.c_int, [c_i64, c_p, c_p, c_p, c_p, c_p]),
     "bsgd_sqdist": (ctypes.c_int, [c_i64, c_p, c_p, c_p, c_p, c_p]),
     "bsgd_epoch_workspace_bytes": (ctypes.c_size_t, [c_p, c_i64, c_i64]),

@@ -29,7 +29,7 @@
 
 using namespace bsgd;
 
-#define BSGD_VERSION 100
+#define BSGD_VERSION 110
 
 // ---------------------------------------------------------------------------
 // errors
@@ -619,7 +619,7 @@ struct Ws {
     double *rpart;   // [kMaxPartials]
     double *red;     // [2 * kMaxPartials * 4]
     double *uimg;    // [cols]
-    double *fields;  // [6 * hw]
+    double *fields;  // [9 * n]: p, q, c for up to three axes
 };
 
 static size_t a256(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -633,7 +633,7 @@ static size_t ws_layout(void *base, int64_t cols, int64_t hw, Ws *ws) {
     char *rpart = take(sizeof(double) * kMaxPartials);
     char *red = take(sizeof(double) * 2 * kMaxPartials * 4);
     char *uimg = take(sizeof(double) * (size_t)std::max<int64_t>(cols, 1));
-    char *fields = take(sizeof(double) * 6 * (size_t)std::max<int64_t>(hw, 0));
+    char *fields = take(sizeof(double) * 9 * (size_t)std::max<int64_t>(hw, 0));
     if (ws) {
         ws->ctl = (int64_t *)ctl; ws->scal = (double *)scal; ws->xpart = (double *)xpart;
         ws->rpart = (double *)rpart; ws->red = (double *)red; ws->uimg = (double *)uimg;
@@ -741,20 +741,23 @@ __global__ void tail_kernel(TailArgs t) {
 // ---------------------------------------------------------------------------
 // prox launch
 // ---------------------------------------------------------------------------
-static size_t prox_dyn_smem() { return sizeof(double) * kPwMaxK * kPwChunk * 128; }
+template <int DIM>
+static size_t prox_dyn_smem() { return sizeof(double) * 2 * DIM * kPwChunk * 128; }
 
+template <int DIM>
 static int prox_occupancy() {
     static int occ = 0;
     if (occ == 0) {
-        cudaFuncSetAttribute(fgp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)prox_dyn_smem());
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fgp_kernel, kThreads, prox_dyn_smem());
+        cudaFuncSetAttribute(fgp_kernel<DIM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)prox_dyn_smem<DIM>());
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fgp_kernel<DIM>, kThreads, prox_dyn_smem<DIM>());
         if (occ < 1) occ = 1;
     }
     return occ;
 }
 
-static int launch_prox(ProxArgs &a, cudaStream_t st) {
-    const int occ = prox_occupancy();
+template <int DIM>
+static int launch_prox_dim(ProxArgs &a, cudaStream_t st) {
+    const int occ = prox_occupancy<DIM>();
     int rc = pw_depth(a.N, &a.ds);
     if (rc) return rc;
     a.fast = (a.N % 128 == 0 && a.N / 128 == ((int64_t)1 << a.ds)) ? 1 : 0;
@@ -765,19 +768,25 @@ static int launch_prox(ProxArgs &a, cudaStream_t st) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(kThreads);
-    cfg.dynamicSmemBytes = prox_dyn_smem();
+    cfg.dynamicSmemBytes = prox_dyn_smem<DIM>();
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeCooperative;
     attr[0].val.cooperative = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    CU(cudaLaunchKernelEx(&cfg, fgp_kernel, a));
+    CU(cudaLaunchKernelEx(&cfg, fgp_kernel<DIM>, a));
     return BSGD_OK;
 }
 
-static void prox_fields(ProxArgs &a, const Ws &ws, int64_t hw) {
-    for (int k = 0; k < 6; ++k) a.f[k] = ws.fields + (size_t)k * hw;
+// a.D <= 1: 2D image (tv.py); a.D >= 2: 3D volume (oracle tv_prox3)
+static int launch_prox(ProxArgs &a, cudaStream_t st) {
+    if (a.D <= 1) { a.D = 1; return launch_prox_dim<2>(a, st); }
+    return launch_prox_dim<3>(a, st);
+}
+
+static void prox_fields(ProxArgs &a, const Ws &ws, int64_t n) {
+    for (int k = 0; k < 9; ++k) a.f[k] = ws.fields + (size_t)k * n;
     a.red = ws.red;
 }
 
@@ -883,9 +892,8 @@ static int plan_finish(bsgd_plan *p, cudaStream_t st) {
     p->block_nnz.assign(cnt.begin(), cnt.end());
 #undef PTRY
     // warm occupancy caches outside any graph capture
-    (void)prox_occupancy();
-    // warm occupancy caches outside any graph capture
-    (void)prox_occupancy();
+    (void)prox_occupancy<2>();
+    (void)prox_occupancy<3>();
     return BSGD_OK;
 }
 
@@ -1280,18 +1288,23 @@ size_t bsgd_tv_prox_workspace_bytes(int64_t height, int64_t width) {
     return ws_layout(nullptr, 1, height * width, nullptr);
 }
 
-int bsgd_tv_prox(int64_t height, int64_t width, const double *img, double *out, double weight,
-                 int32_t max_inner_iters, double tol, void *workspace, size_t workspace_bytes,
-                 bsgd_prox_info *info_out, double *dual_objectives, void *stream) {
-    if (height < 1 || width < 1) return fail(BSGD_EINVAL, "image dimensions must be positive");
+size_t bsgd_tv_prox3_workspace_bytes(int64_t depth, int64_t height, int64_t width) {
+    if (depth < 1 || height < 1 || width < 1) return 0;
+    return ws_layout(nullptr, 1, depth * height * width, nullptr);
+}
+
+static int tv_prox_any(int64_t depth, int64_t height, int64_t width, const double *img, double *out, double weight,
+                       int32_t max_inner_iters, double tol, void *workspace, size_t workspace_bytes,
+                       bsgd_prox_info *info_out, double *dual_objectives, void *stream) {
+    if (depth < 1 || height < 1 || width < 1) return fail(BSGD_EINVAL, "image dimensions must be positive");
     if (!img || !out) return fail(BSGD_EINVAL, "NULL image");
     if (!(weight >= 0.0)) return fail(BSGD_EINVAL, "prox weight must be nonnegative");
     if (max_inner_iters < 1) return fail(BSGD_EINVAL, "max_inner_iters must be >= 1");
     if (!(tol > 0.0)) return fail(BSGD_EINVAL, "tol must be positive");
     cudaStream_t st = (cudaStream_t)stream;
-    const int64_t hw = height * width;
+    const int64_t n = depth * height * width;
     if (weight == 0.0) {  // tv.py:190-193: identity, converged
-        CU(cudaMemcpyAsync(out, img, sizeof(double) * hw, cudaMemcpyDeviceToDevice, st));
+        CU(cudaMemcpyAsync(out, img, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
         if (info_out) {
             const bsgd_prox_info zero = {0, 1, 0, 0};
             static_assert(sizeof(bsgd_prox_info) == 16, "layout");
@@ -1302,14 +1315,14 @@ int bsgd_tv_prox(int64_t height, int64_t width, const double *img, double *out, 
         return BSGD_OK;
     }
     Ws ws;
-    const size_t need = ws_layout(workspace, 1, hw, &ws);
+    const size_t need = ws_layout(workspace, 1, n, &ws);
     if (!workspace || workspace_bytes < need) return fail(BSGD_EINVAL, "workspace too small (%zu < %zu)", workspace_bytes, need);
     ProxArgs a = {};
-    a.H = height; a.W = width; a.N = hw;
+    a.D = depth; a.H = height; a.W = width; a.N = n;
     a.b = img;
-    prox_fields(a, ws, hw);
+    prox_fields(a, ws, n);
     a.w = weight;
-    a.step = 1.0 / (8.0 * weight);
+    a.step = 1.0 / ((depth > 1 ? 12.0 : 8.0) * weight);  // 1/(||D||^2 w): 8 in 2D (tv.py:195), 12 in 3D
     a.tol = tol;
     a.max_iters = max_inner_iters;
     a.out_img = out;
@@ -1317,6 +1330,21 @@ int bsgd_tv_prox(int64_t height, int64_t width, const double *img, double *out, 
     a.info = (int32_t *)info_out;
     a.dual = dual_objectives;
     return launch_prox(a, st);
+}
+
+int bsgd_tv_prox(int64_t height, int64_t width, const double *img, double *out, double weight,
+                 int32_t max_inner_iters, double tol, void *workspace, size_t workspace_bytes,
+                 bsgd_prox_info *info_out, double *dual_objectives, void *stream) {
+    return tv_prox_any(1, height, width, img, out, weight, max_inner_iters, tol, workspace, workspace_bytes, info_out,
+                       dual_objectives, stream);
+}
+
+int bsgd_tv_prox3(int64_t depth, int64_t height, int64_t width, const double *vol, double *out, double weight,
+                  int32_t max_inner_iters, double tol, void *workspace, size_t workspace_bytes,
+                  bsgd_prox_info *info_out, double *dual_objectives, void *stream) {
+    if (depth < 2) return fail(BSGD_EINVAL, "bsgd_tv_prox3 needs depth >= 2 (use bsgd_tv_prox for images)");
+    return tv_prox_any(depth, height, width, vol, out, weight, max_inner_iters, tol, workspace, workspace_bytes,
+                       info_out, dual_objectives, stream);
 }
 
 static int reduce_launch(int64_t n, const double *a, const double *b, int mode, double *out, void *scratch,
@@ -1338,20 +1366,31 @@ int bsgd_sqdist(int64_t n, const double *a, const double *b, double *out, void *
     return reduce_launch(n, a, b, 1, out, scratch, (cudaStream_t)stream);
 }
 
-int bsgd_tv_value(int64_t height, int64_t width, const double *img, double *out, void *scratch, void *stream) {
-    if (height < 1 || width < 1 || !img || !out || !scratch) return fail(BSGD_EINVAL, "bad tv_value arguments");
+static int tv_value_any(int64_t depth, int64_t height, int64_t width, const double *img, double *out, void *scratch,
+                        void *stream) {
+    if (depth < 1 || height < 1 || width < 1 || !img || !out || !scratch) return fail(BSGD_EINVAL, "bad tv_value arguments");
     cudaStream_t st = (cudaStream_t)stream;
-    const int64_t hw = height * width;
+    const int64_t n = depth * height * width;
     int ds = 0;
-    int rc = pw_depth(hw, &ds);
+    int rc = pw_depth(n, &ds);
     if (rc) return rc;
     const int64_t S = (int64_t)1 << ds;
     const int G = (int)std::min<int64_t>(S, 256);
-    if (S / G > kPwMaxQ) return fail(BSGD_EINVAL, "image too large for tv_value (%lld pixels)", (long long)hw);
-    tv_value_part_kernel<<<G, kThreads, 0, st>>>(height, width, img, ds, (double *)scratch);
+    if (S / G > kPwMaxQ) return fail(BSGD_EINVAL, "image too large for tv_value (%lld pixels)", (long long)n);
+    if (depth > 1) tv_value_part_kernel<3><<<G, kThreads, 0, st>>>(depth, height, width, img, ds, (double *)scratch);
+    else tv_value_part_kernel<2><<<G, kThreads, 0, st>>>(1, height, width, img, ds, (double *)scratch);
     pw_top_kernel<<<1, kThreads, 0, st>>>(ds, G, (const double *)scratch, out);
     LAUNCHED();
     return BSGD_OK;
+}
+
+int bsgd_tv_value(int64_t height, int64_t width, const double *img, double *out, void *scratch, void *stream) {
+    return tv_value_any(1, height, width, img, out, scratch, stream);
+}
+
+int bsgd_tv_value3(int64_t depth, int64_t height, int64_t width, const double *vol, double *out, void *scratch,
+                   void *stream) {
+    return tv_value_any(depth, height, width, vol, out, scratch, stream);
 }
 
 int bsgd_discrete_gradient(int64_t height, int64_t width, const double *img, double *dv, double *dh, void *stream) {
@@ -1369,11 +1408,33 @@ int bsgd_discrete_divergence(int64_t height, int64_t width, const double *pv, co
     return BSGD_OK;
 }
 
+int bsgd_discrete_gradient3(int64_t depth, int64_t height, int64_t width, const double *vol, double *dz, double *dv,
+                            double *dh, void *stream) {
+    if (depth < 1 || height < 1 || width < 1 || !vol || !dz || !dv || !dh)
+        return fail(BSGD_EINVAL, "bad gradient arguments");
+    gradient3_kernel<<<grid_1d(depth * height * width), kThreads, 0, (cudaStream_t)stream>>>(depth, height, width,
+                                                                                           vol, dz, dv, dh);
+    LAUNCHED();
+    return BSGD_OK;
+}
+
+int bsgd_discrete_divergence3(int64_t depth, int64_t height, int64_t width, const double *pz, const double *pv,
+                              const double *ph, double *out, void *stream) {
+    if (depth < 1 || height < 1 || width < 1 || !pz || !pv || !ph || !out)
+        return fail(BSGD_EINVAL, "bad divergence arguments");
+    divergence3_kernel<<<grid_1d(depth * height * width), kThreads, 0, (cudaStream_t)stream>>>(depth, height, width,
+                                                                                             pz, pv, ph, out);
+    LAUNCHED();
+    return BSGD_OK;
+}
+
 // ---- epoch ----
 size_t bsgd_epoch_workspace_bytes(const bsgd_plan *p, int64_t height, int64_t width) {
     if (!p) return 0;
-    const int64_t hw = (height > 0 && width > 0) ? height * width : 0;
-    return ws_layout(nullptr, p->cols, hw, nullptr);
+    // the prox fields are sized by the plan's columns (height*width, or
+    // depth*height*width for volumes, must equal cols when lam > 0)
+    const int64_t n = (height > 0 && width > 0) ? p->cols : 0;
+    return ws_layout(nullptr, p->cols, n, nullptr);
 }
 
 static int check_epoch_args(int64_t cols, const bsgd_epoch_args *a, Ws *ws) {
@@ -1382,15 +1443,15 @@ static int check_epoch_args(int64_t cols, const bsgd_epoch_args *a, Ws *ws) {
     if (a->lam < 0.0) return fail(BSGD_EINVAL, "lam must be nonnegative");
     const bool prox = a->lam > 0.0;
     if (prox) {
-        if (a->height < 1 || a->width < 1 || a->height * a->width != cols)
-            return fail(BSGD_EINVAL, "layout required when lam > 0 (height*width must equal cols)");
+        const int64_t depth = a->depth > 1 ? a->depth : 1;
+        if (a->height < 1 || a->width < 1 || depth * a->height * a->width != cols)
+            return fail(BSGD_EINVAL, "layout required when lam > 0 (depth*height*width must equal cols)");
         if (a->max_inner_iters < 1) return fail(BSGD_EINVAL, "max_inner_iters must be >= 1");
         if (!(a->tol > 0.0)) return fail(BSGD_EINVAL, "tol must be positive");
     }
     if (!a->x_k || !a->g || !a->x_next) return fail(BSGD_EINVAL, "x_k, g and x_next are required");
     if (!a->workspace) return fail(BSGD_EINVAL, "workspace is NULL");
-    const int64_t hw = prox ? a->height * a->width : 0;
-    const size_t need = ws_layout(a->workspace, cols, hw, ws);
+    const size_t need = ws_layout(a->workspace, cols, prox ? cols : 0, ws);
     if (a->workspace_bytes < need) return fail(BSGD_EINVAL, "workspace too small (%zu < %zu)", a->workspace_bytes, need);
     if (!(a->flags & BSGD_EP_NO_TAIL) && (!a->history || !a->epoch_counter))
         return fail(BSGD_EINVAL, "history and epoch_counter are required");
@@ -1409,13 +1470,14 @@ static int run_step(int64_t cols, const bsgd_epoch_args *a, const Ws &ws, cudaSt
 }
 
 static int run_prox(const bsgd_epoch_args *a, const Ws &ws, cudaStream_t st) {
-    const int64_t hw = a->height * a->width;
+    const int64_t depth = a->depth > 1 ? a->depth : 1;
+    const int64_t n = depth * a->height * a->width;
     ProxArgs pa = {};
-    pa.H = a->height; pa.W = a->width; pa.N = hw;
+    pa.D = depth; pa.H = a->height; pa.W = a->width; pa.N = n;
     pa.b = ws.uimg;
-    prox_fields(pa, ws, hw);
+    prox_fields(pa, ws, n);
     pa.w = a->mu * a->lam;  // tv.py weight = mu_try * cfg.lam (solvers.py:310)
-    pa.step = 1.0 / (8.0 * pa.w);
+    pa.step = 1.0 / ((depth > 1 ? 12.0 : 8.0) * pa.w);
     pa.tol = a->tol;
     pa.max_iters = a->max_inner_iters;
     pa.out_img = nullptr;
@@ -1501,7 +1563,7 @@ int bsgd_epoch_forward(const bsgd_plan *p, const double *x, const double *y, dou
                        const bsgd_epoch_args *a, void *stream) {
     if (!p || !x || !y || !r_out || !a || !a->workspace) return fail(BSGD_EINVAL, "NULL argument");
     Ws ws;
-    ws_layout(a->workspace, p->cols, a->lam > 0.0 ? a->height * a->width : 0, &ws);
+    ws_layout(a->workspace, p->cols, a->lam > 0.0 ? p->cols : 0, &ws);
     DeviceGuard guard(p->device);
     cudaStream_t st = (cudaStream_t)stream;
     return DISPATCH_V(p, launch_fwd<V>(p, x, EpiResid{y, r_out}, ws.rpart, ws.ctl + 1, st));
@@ -1510,7 +1572,7 @@ int bsgd_epoch_forward(const bsgd_plan *p, const double *x, const double *y, dou
 int bsgd_epoch_reduce_forward(const bsgd_plan *p, const bsgd_epoch_args *a, double *scalars_out, void *stream) {
     if (!p || !a || !a->workspace || !scalars_out) return fail(BSGD_EINVAL, "NULL argument");
     Ws ws;
-    ws_layout(a->workspace, p->cols, a->lam > 0.0 ? a->height * a->width : 0, &ws);
+    ws_layout(a->workspace, p->cols, a->lam > 0.0 ? p->cols : 0, &ws);
     sum_counted_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(ws.rpart, ws.ctl + 1, scalars_out);
     LAUNCHED();
     return BSGD_OK;

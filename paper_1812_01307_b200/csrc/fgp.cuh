@@ -31,9 +31,9 @@ namespace bsgd {
 namespace cg = cooperative_groups;
 
 struct ProxArgs {
-    int64_t H, W, N;
+    int64_t D, H, W, N;    // D = 1 for images; 3D volumes are z-major (z, row, column)
     const double *b;       // input image (row-major)
-    double *f[6];          // pv, ph, qv, qh, cv, ch (workspace)
+    double *f[9];          // p[DIM], q[DIM], c[DIM] (workspace); 2D: pv, ph, qv, qh, cv, ch
     double *red;           // [2][kMaxPartials * 4] reduction partials
     double w, step, tol;
     int32_t max_iters;
@@ -59,46 +59,97 @@ struct ProxArgs {
 // the SASS), so plain L1-cached loads are coherent here.
 __device__ __forceinline__ double ldcg(const double *p) { return *p; }
 
-// div p at (s, t): ((pv[s+1] - pv[s]) + ph[t+1]) - ph[t], zero outside (tv.py:124-132)
-__device__ __forceinline__ double div_at(const double *pv, const double *ph, int64_t s, int64_t t,
+// ---- stencils, dimension-generic (DIM = 2: tv.py:115-132; DIM = 3: oracle divergence3) ----
+// fields are passed as DIM pointers ordered (z,) row, column.
+
+// div p at voxel o = ((z*H + s)*W + t):
+//   2D  ((pv[s+1] - pv[s]) + ph[t+1]) - ph[t]
+//   3D  ((((pz[z+1] - pz[z]) + pv[s+1]) - pv[s]) + ph[t+1]) - ph[t]      zero outside
+template <int DIM>
+__device__ __forceinline__ double div_at(const double *const *pf, int64_t z, int64_t s, int64_t t, int64_t D,
                                          int64_t H, int64_t W) {
-    const int64_t o = s * W + t;
+    const int64_t o = (z * H + s) * W + t;
+    const double *pv = pf[DIM - 2], *ph = pf[DIM - 1];
     const double a = (s + 1 < H) ? ldcg(pv + o + W) : 0.0;
     const double b = (s > 0) ? ldcg(pv + o) : 0.0;
     const double c = (t + 1 < W) ? ldcg(ph + o + 1) : 0.0;
     const double d = (t > 0) ? ldcg(ph + o) : 0.0;
-    return rn_sub(rn_add(rn_sub(a, b), c), d);
+    if constexpr (DIM == 2) {
+        return rn_sub(rn_add(rn_sub(a, b), c), d);
+    } else {
+        const double *pz = pf[0];
+        const double az = (z + 1 < D) ? ldcg(pz + o + H * W) : 0.0;
+        const double bz = (z > 0) ? ldcg(pz + o) : 0.0;
+        return rn_sub(rn_add(rn_sub(rn_add(rn_sub(az, bz), a), b), c), d);
+    }
 }
 
-// u = b + w div q at (s, t)
-__device__ __forceinline__ double u_at(const ProxArgs &a, const double *qv, const double *qh, int64_t s,
-                                       int64_t t) {
-    return rn_add(__ldg(a.b + s * a.W + t), rn_mul(a.w, div_at(qv, qh, s, t, a.H, a.W)));
+// voxel index -> (z, row, column); 2D skips the plane division
+template <int DIM>
+__device__ __forceinline__ void split_index(int64_t p, int64_t H, int64_t W, int64_t &z, int64_t &s, int64_t &t) {
+    int64_t r = p;
+    z = 0;
+    if constexpr (DIM == 3) { z = p / (H * W); r = p - z * (H * W); }
+    s = r / W;
+    t = r - s * W;
 }
 
-// projected gradient candidate from (qv, qh) at pixel p (tv.py:207-214)
-__device__ __forceinline__ void candidate(const ProxArgs &a, const double *qv, const double *qh, int64_t p,
-                                          double &cv, double &ch) {
-    const int64_t s = p / a.W, t = p - s * a.W;
-    const double uc = u_at(a, qv, qh, s, t);
-    const double gv = (s > 0) ? rn_sub(uc, u_at(a, qv, qh, s - 1, t)) : 0.0;
-    const double gh = (t > 0) ? rn_sub(uc, u_at(a, qv, qh, s, t - 1)) : 0.0;
-    cv = rn_add(ldcg(qv + p), rn_mul(a.step, gv));
-    ch = rn_add(ldcg(qh + p), rn_mul(a.step, gh));
-    double mag = sqrt(rn_add(rn_mul(cv, cv), rn_mul(ch, ch)));
+// legacy 2D signature (discrete_divergence kernel)
+__device__ __forceinline__ double div_at(const double *pv, const double *ph, int64_t s, int64_t t, int64_t H,
+                                         int64_t W) {
+    const double *pf[2] = {pv, ph};
+    return div_at<2>(pf, 0, s, t, 1, H, W);
+}
+
+// u = b + w div q at voxel (z, s, t)
+template <int DIM>
+__device__ __forceinline__ double u_at(const ProxArgs &a, const double *const *qf, int64_t z, int64_t s, int64_t t) {
+    return rn_add(__ldg(a.b + (z * a.H + s) * a.W + t), rn_mul(a.w, div_at<DIM>(qf, z, s, t, a.D, a.H, a.W)));
+}
+
+// projected gradient candidate from q at voxel p (tv.py:207-214; 3D: same with three fields)
+template <int DIM>
+__device__ __forceinline__ void candidate(const ProxArgs &a, const double *const *qf, int64_t p, double (&c)[DIM]) {
+    int64_t z, s, t;
+    split_index<DIM>(p, a.H, a.W, z, s, t);
+    const double uc = u_at<DIM>(a, qf, z, s, t);
+    double g[DIM];
+    if constexpr (DIM == 3) g[0] = (z > 0) ? rn_sub(uc, u_at<DIM>(a, qf, z - 1, s, t)) : 0.0;
+    g[DIM - 2] = (s > 0) ? rn_sub(uc, u_at<DIM>(a, qf, z, s - 1, t)) : 0.0;
+    g[DIM - 1] = (t > 0) ? rn_sub(uc, u_at<DIM>(a, qf, z, s, t - 1)) : 0.0;
+#pragma unroll
+    for (int k = 0; k < DIM; ++k) c[k] = rn_add(ldcg(qf[k] + p), rn_mul(a.step, g[k]));
+    double m2 = rn_add(rn_mul(c[0], c[0]), rn_mul(c[1], c[1]));
+    if constexpr (DIM == 3) m2 = rn_add(m2, rn_mul(c[2], c[2]));
+    double mag = sqrt(m2);
     mag = (mag < 1.0) ? 1.0 : mag;  // np.maximum(mag, 1): NaN propagates
-    cv = cv / mag;
-    ch = ch / mag;
+#pragma unroll
+    for (int k = 0; k < DIM; ++k) c[k] = c[k] / mag;
 }
 
-// isotropic TV term at pixel p of image u (tv.py:149-152)
-__device__ __forceinline__ double tv_term(const double *u, int64_t p, int64_t W, bool cg_load) {
-    const int64_t s = p / W, t = p - s * W;
+// isotropic TV term at voxel p of u (tv.py:149-152; 3D: sqrt((dz^2 + dv^2) + dh^2))
+template <int DIM>
+__device__ __forceinline__ double tv_term(const double *u, int64_t p, int64_t H, int64_t W, bool cg_load) {
+    const int64_t HW = H * W;
+    int64_t z, s, t;
+    split_index<DIM>(p, H, W, z, s, t);
     const double uc = cg_load ? ldcg(u + p) : __ldg(u + p);
     double dv = 0.0, dh = 0.0;
     if (s > 0) dv = rn_sub(uc, cg_load ? ldcg(u + p - W) : __ldg(u + p - W));
     if (t > 0) dh = rn_sub(uc, cg_load ? ldcg(u + p - 1) : __ldg(u + p - 1));
-    return sqrt(rn_add(rn_mul(dv, dv), rn_mul(dh, dh)));
+    if constexpr (DIM == 2) {
+        return sqrt(rn_add(rn_mul(dv, dv), rn_mul(dh, dh)));
+    } else {
+        double dz = 0.0;
+        if (z > 0) dz = rn_sub(uc, cg_load ? ldcg(u + p - HW) : __ldg(u + p - HW));
+        return sqrt(rn_add(rn_add(rn_mul(dz, dz), rn_mul(dv, dv)), rn_mul(dh, dh)));
+    }
+}
+
+// legacy 2D signature
+__device__ __forceinline__ double tv_term(const double *u, int64_t p, int64_t W, bool cg_load) {
+    const int64_t s = p / W;
+    return tv_term<2>(u, p, s + 1, W, cg_load);
 }
 
 // numpy-order grid sum of K per-pixel terms (pairwise.cuh); all threads get the
@@ -114,27 +165,31 @@ __device__ __forceinline__ void np_sum(cg::grid_group &grid, int64_t N, int ds, 
     ++round;
 }
 
+template <int DIM>
 __global__ void __launch_bounds__(kThreads, 2) fgp_kernel(ProxArgs a) {
     cg::grid_group grid = cg::this_grid();
     __shared__ double sm[kPwMaxQ * kPwMaxK];
-    extern __shared__ double Tsm[];   // kPwMaxK * kPwChunk * 128 doubles (fast path)
+    extern __shared__ double Tsm[];   // 2*DIM * kPwChunk * 128 doubles (fast path)
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
-    const int64_t N = a.N, W = a.W, H = a.H;
+    const int64_t N = a.N, W = a.W, H = a.H, D = a.D;
     const double w = a.w;
     const double *b = a.b;
     int round = 0;
-    double *pv = a.f[0], *ph = a.f[1], *qv = a.f[2], *qh = a.f[3], *cv = a.f[4], *ch = a.f[5];
+    double *P[DIM], *Q[DIM], *C[DIM];
+#pragma unroll
+    for (int k = 0; k < DIM; ++k) { P[k] = a.f[k]; Q[k] = a.f[DIM + k]; C[k] = a.f[2 * DIM + k]; }
 
     // --- setup: p = q = 0 (tv.py:198-201), phi_prev = np.sum(b*b) (tv.py:203),
     //     and TV(b) for the fallback test (tv.py:166-169, 251)
     double v2[2];
     {
         auto f0 = [&](int64_t p, double (&t)[2]) {
-            pv[p] = 0.0; ph[p] = 0.0; qv[p] = 0.0; qh[p] = 0.0;
+#pragma unroll
+            for (int k = 0; k < DIM; ++k) { P[k][p] = 0.0; Q[k][p] = 0.0; }
             const double bb = __ldg(b + p);
             t[0] = rn_mul(bb, bb);
-            t[1] = tv_term(b, p, W, false);
+            t[1] = tv_term<DIM>(b, p, H, W, false);
         };
         np_sum<2>(grid, N, a.ds, f0, a.red, round, sm, v2, a.fast, Tsm);
     }
@@ -144,20 +199,22 @@ __global__ void __launch_bounds__(kThreads, 2) fgp_kernel(ProxArgs a) {
     int iters = 0, restarts = 0, converged = 0;
     if (tid == 0 && a.dual != nullptr) a.dual[0] = phi_prev;
 
+    auto fphi = [&](int64_t p, double (&t)[1]) {
+        int64_t z, s, tt;
+        split_index<DIM>(p, H, W, z, s, tt);
+        const double res = rn_add(__ldg(b + p), rn_mul(w, div_at<DIM>(C, z, s, tt, D, H, W)));
+        t[0] = rn_mul(res, res);
+    };
     for (int it = 0; it < a.max_iters; ++it) {
         // A: candidate from q (tv.py:207-214)
         for (int64_t p = tid; p < N; p += nthr) {
-            double x, y;
-            candidate(a, qv, qh, p, x, y);
-            cv[p] = x; ch[p] = y;
+            double c[DIM];
+            candidate<DIM>(a, Q, p, c);
+#pragma unroll
+            for (int k = 0; k < DIM; ++k) C[k][p] = c[k];
         }
         grid.sync();
         // B: phi = np.sum(resid * resid) (tv.py:215-216)
-        auto fphi = [&](int64_t p, double (&t)[1]) {
-            const int64_t s = p / W, tt = p - s * W;
-            const double r = rn_add(__ldg(b + p), rn_mul(w, div_at(cv, ch, s, tt, H, W)));
-            t[0] = rn_mul(r, r);
-        };
         double v1[1];
         np_sum<1>(grid, N, a.ds, fphi, a.red, round, sm, v1, a.fast, Tsm);
         double phi = v1[0];
@@ -165,54 +222,57 @@ __global__ void __launch_bounds__(kThreads, 2) fgp_kernel(ProxArgs a) {
             ++restarts;
             t_mom = 1.0;
             for (int64_t p = tid; p < N; p += nthr) {
-                double x, y;
-                candidate(a, pv, ph, p, x, y);
-                cv[p] = x; ch[p] = y;
+                double c[DIM];
+                candidate<DIM>(a, P, p, c);
+#pragma unroll
+                for (int k = 0; k < DIM; ++k) C[k][p] = c[k];
             }
             grid.sync();
             np_sum<1>(grid, N, a.ds, fphi, a.red, round, sm, v1, a.fast, Tsm);
             phi = v1[0];
         }
         // C: momentum commit (tv.py:233-245): q = c + beta (c - p);
-        //    change = sqrt(sum dv^2 + sum dh^2), scale = sqrt(sum cv^2 + sum ch^2)
+        //    change = sqrt(sum_k np.sum(s_k^2)), scale = sqrt(sum_k np.sum(c_k^2)), k in order
         const double t_next = 0.5 * (1.0 + sqrt(rn_add(1.0, rn_mul(rn_mul(4.0, t_mom), t_mom))));
         const double beta = (t_mom - 1.0) / t_next;
-        auto fcom = [&](int64_t p, double (&t)[4]) {
-            const double c0 = __ldcg(cv + p), c1 = __ldcg(ch + p);
-            const double s0 = rn_sub(c0, __ldcg(pv + p)), s1 = rn_sub(c1, __ldcg(ph + p));
-            qv[p] = rn_add(c0, rn_mul(beta, s0));
-            qh[p] = rn_add(c1, rn_mul(beta, s1));
-            t[0] = rn_mul(s0, s0);
-            t[1] = rn_mul(s1, s1);
-            t[2] = rn_mul(c0, c0);
-            t[3] = rn_mul(c1, c1);
+        auto fcom = [&](int64_t p, double (&t)[2 * DIM]) {
+#pragma unroll
+            for (int k = 0; k < DIM; ++k) {
+                const double ck = __ldcg(C[k] + p);
+                const double sk = rn_sub(ck, __ldcg(P[k] + p));
+                Q[k][p] = rn_add(ck, rn_mul(beta, sk));
+                t[k] = rn_mul(sk, sk);
+                t[DIM + k] = rn_mul(ck, ck);
+            }
         };
-        double v4[4];
-        np_sum<4>(grid, N, a.ds, fcom, a.red, round, sm, v4, a.fast, Tsm);
-        double *tv_ = pv; pv = cv; cv = tv_;   // p <- c
-        double *th_ = ph; ph = ch; ch = th_;
+        double vc[2 * DIM];
+        np_sum<2 * DIM>(grid, N, a.ds, fcom, a.red, round, sm, vc, a.fast, Tsm);
+#pragma unroll
+        for (int k = 0; k < DIM; ++k) { double *tmp_ = P[k]; P[k] = C[k]; C[k] = tmp_; }  // p <- c
         phi_prev = (phi_prev < phi) ? phi_prev : phi;  // Python min(phi, phi_prev)
         t_mom = t_next;
         iters = it + 1;
         if (tid == 0 && a.dual != nullptr) a.dual[it + 1] = phi_prev;
-        const double change = sqrt(rn_add(v4[0], v4[1]));
-        const double scale = sqrt(rn_add(v4[2], v4[3]));
+        double ch2 = rn_add(vc[0], vc[1]), sc2 = rn_add(vc[DIM], vc[DIM + 1]);
+        if constexpr (DIM == 3) { ch2 = rn_add(ch2, vc[2]); sc2 = rn_add(sc2, vc[5]); }
+        const double change = sqrt(ch2), scale = sqrt(sc2);
         const double floor_scale = (1e-30 > scale) ? 1e-30 : scale;  // Python max(scale, 1e-30)
         if (change <= a.tol * floor_scale) { converged = 1; break; }
     }
 
     // --- finalize: out = b + w div p (tv.py:250), identity fallback if the primal
     //     objective is worse (tv.py:251-253)
-    double *tmp = cv;  // scratch pair after the swap
+    double *tmp = C[0];  // scratch after the swap
     for (int64_t p = tid; p < N; p += nthr) {
-        const int64_t s = p / W, t = p - s * W;
-        tmp[p] = rn_add(__ldg(b + p), rn_mul(w, div_at(pv, ph, s, t, H, W)));
+        int64_t z, s, t;
+        split_index<DIM>(p, H, W, z, s, t);
+        tmp[p] = rn_add(__ldg(b + p), rn_mul(w, div_at<DIM>(P, z, s, t, D, H, W)));
     }
     grid.sync();
     auto fen = [&](int64_t p, double (&t)[2]) {
         const double d = rn_sub(__ldcg(tmp + p), __ldg(b + p));
         t[0] = rn_mul(d, d);
-        t[1] = tv_term(tmp, p, W, true);
+        t[1] = tv_term<DIM>(tmp, p, H, W, true);
     };
     double e2[2];
     np_sum<2>(grid, N, a.ds, fen, a.red, round, sm, e2, a.fast, Tsm);
@@ -286,11 +346,12 @@ __global__ void __launch_bounds__(kThreads) step_kernel(int64_t n, const double 
 
 // ---- small image kernels (tv.py:115-152) ----
 // tv_value in numpy order: CTA part (grid of G = power of two CTAs) ...
-__global__ void __launch_bounds__(kThreads) tv_value_part_kernel(int64_t H, int64_t W, const double *u, int ds,
-                                                                 double *part) {
+template <int DIM>
+__global__ void __launch_bounds__(kThreads) tv_value_part_kernel(int64_t D, int64_t H, int64_t W, const double *u,
+                                                                 int ds, double *part) {
     __shared__ double sm[kPwMaxQ];
-    auto f = [&](int64_t p, double (&t)[1]) { t[0] = tv_term(u, p, W, false); };
-    pw_cta<1>(H * W, ds, f, sm, part);
+    auto f = [&](int64_t p, double (&t)[1]) { t[0] = tv_term<DIM>(u, p, H, W, false); };
+    pw_cta<1>(D * H * W, ds, f, sm, part);
 }
 // ... and the balanced top over the CTA parts (one CTA)
 __global__ void __launch_bounds__(kThreads) pw_top_kernel(int ds, int G, const double *part, double *out) {
@@ -298,6 +359,27 @@ __global__ void __launch_bounds__(kThreads) pw_top_kernel(int ds, int G, const d
     double v[1];
     pw_top<1>(ds, G, part, sm, v);
     if (threadIdx.x == 0) out[0] = v[0];
+}
+
+__global__ void __launch_bounds__(kThreads) gradient3_kernel(int64_t D, int64_t H, int64_t W, const double *u,
+                                                             double *dz, double *dv, double *dh) {
+    const int64_t HW = H * W;
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < D * HW; p += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t z = p / HW, r = p - z * HW, s = r / W, t = r - s * W;
+        dz[p] = z > 0 ? rn_sub(u[p], u[p - HW]) : 0.0;
+        dv[p] = s > 0 ? rn_sub(u[p], u[p - W]) : 0.0;
+        dh[p] = t > 0 ? rn_sub(u[p], u[p - 1]) : 0.0;
+    }
+}
+
+__global__ void __launch_bounds__(kThreads) divergence3_kernel(int64_t D, int64_t H, int64_t W, const double *pz,
+                                                               const double *pv, const double *ph, double *out) {
+    const int64_t HW = H * W;
+    const double *pf[3] = {pz, pv, ph};
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < D * HW; p += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t z = p / HW, r = p - z * HW, s = r / W, t = r - s * W;
+        out[p] = div_at<3>(pf, z, s, t, D, H, W);
+    }
 }
 
 __global__ void __launch_bounds__(kThreads) gradient_kernel(int64_t H, int64_t W, const double *u, double *dv,

@@ -30,7 +30,7 @@
 namespace bsgd {
 
 constexpr int kPwMaxQ = 512;   // subtrees per CTA held in shared memory
-constexpr int kPwMaxK = 4;     // simultaneous sums per pass
+constexpr int kPwMaxK = 6;     // simultaneous sums per pass (3D commit phase)
 
 __host__ __device__ inline int64_t pw_split(int64_t n) {
     const int64_t n2 = n / 2;

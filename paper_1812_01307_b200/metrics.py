@@ -6,7 +6,7 @@ import numpy as np
 
 from . import _native as nat
 from .blockops import BlockOperator
-from .tv import PixelLayout, tv_value
+from .tv import PixelLayout, layout_shape, tv_value
 
 
 def _dev_of(*vals):
@@ -51,5 +51,5 @@ def objective_value(x, op: BlockOperator, y, lam: float, layout: PixelLayout | N
         xv = nat.as_f64(x, op.device, layout.size)
         perm = layout.device_perm(op.device)
         img = xv if perm is None else t.empty_like(xv).index_copy_(0, perm, xv)
-        value += 2.0 * lam * tv_value(img.reshape(layout.height, layout.width))
+        value += 2.0 * lam * tv_value(img.reshape(layout_shape(layout) if hasattr(layout, "depth") else (layout.height, layout.width)))
     return value

@@ -109,6 +109,7 @@ class CudaShard:
         a.perm = nat.ptr(perm) if perm is not None else None
         a.mu, a.lam = mu, cfg.lam
         a.height, a.width = self.hw
+        a.depth = getattr(self.layout, "depth", 1) if self.hw[0] else 0
         a.max_inner_iters, a.tol = cfg.prox.max_inner_iters, cfg.prox.tol
         a.f_curr, a.history, a.epoch_counter = nat.ptr(f_curr), nat.ptr(hist), nat.ptr(counter)
         a.history_capacity = hist.shape[0]

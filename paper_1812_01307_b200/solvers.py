@@ -438,6 +438,7 @@ def _epoch_args(state: SolverState, cfg: SolverConfig, layout, y_dev, xi: int, r
     a.lam = lam
     a.height = layout.height if (lam > 0 and layout is not None) else 0
     a.width = layout.width if (lam > 0 and layout is not None) else 0
+    a.depth = getattr(layout, "depth", 1) if (lam > 0 and layout is not None) else 0
     a.max_inner_iters = cfg.prox.max_inner_iters
     a.tol = cfg.prox.tol
     a.f_curr = nat.ptr(state._f_curr)

@@ -167,10 +167,54 @@ def _pairwise(a, lo, n):
 
 
 @pytest.mark.parametrize("shape", [(5,), (17,), (128,), (129,), (24, 24), (37, 101), (200, 3), (256, 256),
-                                   (300, 301)])
+                                   (300, 301), (4, 3, 5), (16, 16, 16), (5, 40, 7), (32, 32, 32)])
 def test_numpy_pairwise_restatement(shape):
     """np.sum over a contiguous array == the pairwise recursion over its flat data, bit for bit."""
     rng = np.random.default_rng(sum(shape))
     x = rng.standard_normal(shape) * 10.0 ** rng.uniform(-3, 3, shape)
     assert float(np.sum(x)) == _pairwise(x.ravel().tolist(), 0, x.size)
     assert float(np.sum(x * x)) == _pairwise((x * x).ravel().tolist(), 0, x.size)
+
+
+# --- 3-D extension (configs[4]); PARITY UNPINNED: no reference implementation ----
+
+def test_oracle_3d_operators_are_adjoint():
+    rng = np.random.default_rng(7)
+    u = rng.standard_normal((5, 6, 7))
+    p = [rng.standard_normal(u.shape) for _ in range(3)]
+    g = orc.forward_diff3(u)
+    lhs = sum(float(np.sum(a * b)) for a, b in zip(g, p))
+    assert lhs == pytest.approx(-float(np.sum(u * orc.divergence3(*p))), rel=1e-12)
+    # a volume constant along z has 3-D TV = sum over slices of the 2-D TV
+    img = rng.random((9, 11))
+    vol = np.repeat(img[None], 4, axis=0)
+    assert orc.tv_value3(vol) == pytest.approx(4 * orc.tv_value(img), rel=1e-12)
+
+
+def test_oracle_3d_prox_decreases_energy():
+    rng = np.random.default_rng(8)
+    b = rng.random((6, 8, 10))
+    for w in (0.01, 0.1, 1.0):
+        out, rep = orc.tv_prox3(b, w, 50, 1e-10)
+        assert orc._prox_energy3(out, b, w) <= orc._prox_energy3(b, b, w)
+        duals = rep.dual_objectives
+        assert all(duals[k + 1] <= duals[k] for k in range(len(duals) - 1))
+
+
+def test_oracle_3d_epoch_runs():
+    """run_bsgd on a slice-stacked system uses the 3-D prox (hw of length 3)."""
+    from scipy import sparse
+    from paper_1812_01307_b200 import problems
+    a2 = problems.parallel_beam_matrix(8, 6, 11)
+    d = 3
+    a = sparse.csr_array(sparse.kron(a2, sparse.identity(d), format="csr"))
+    a.sort_indices()
+    n = a2.shape[1]
+    perm = np.array([z * n + p for p in range(n) for z in range(d)])
+    op = orc.OracleOperator(a, 2, 2)
+    x_true = np.random.default_rng(0).random(a.shape[1])
+    y = a @ x_true
+    eig, _, _ = orc.largest_eigenvalue(op)
+    prm = orc.Params(mu=0.9 / (2 * eig), lam=0.01, epochs=3, max_inner_iters=5)
+    res = orc.run_bsgd(op, y, prm, x_true=x_true, perm=perm, hw=(d, 8, 8))
+    assert len(res.samples) == 4 and res.samples[-1][1] < res.samples[0][1]
