@@ -115,6 +115,25 @@ int bsgd_plan_create_device(bsgd_plan **out, int device, int64_t rows, int64_t c
                             int64_t *indptr, int32_t *indices, void *values, int value_dtype,
                             int64_t num_row_blocks, int64_t num_col_blocks, const int64_t *row_bounds,
                             const int64_t *col_bounds, void *stream);
+/* Slice-stacked plan (configs[4], 3-D parallel-beam CT): A = A2 (x) I_depth,
+ * block-diagonal with the same 2-D matrix A2 (rows2 x cols2 CSR, canonical)
+ * on every slice, in the INTERLEAVED order row r*depth + z, column
+ * c*depth + z (csrc/stacked.cuh).  Only A2 and A2^T are stored; every other
+ * entry point takes the logical (rows2*depth) x (cols2*depth) operator, and
+ * products follow the reference's block-sequential arithmetic order exactly.
+ * Partition bounds are over the logical rows / columns.  The _device variant
+ * adopts the arrays like bsgd_plan_create_device. */
+int bsgd_plan_create_stacked(bsgd_plan **out, int device, int64_t depth, int64_t rows2, int64_t cols2,
+                             int64_t nnz2, const int64_t *indptr, const int32_t *indices, const void *values,
+                             int value_dtype, int64_t num_row_blocks, int64_t num_col_blocks,
+                             const int64_t *row_bounds, const int64_t *col_bounds, void *stream);
+int bsgd_plan_create_stacked_device(bsgd_plan **out, int device, int64_t depth, int64_t rows2, int64_t cols2,
+                                    int64_t nnz2, int64_t *indptr, int32_t *indices, void *values,
+                                    int value_dtype, int64_t num_row_blocks, int64_t num_col_blocks,
+                                    const int64_t *row_bounds, const int64_t *col_bounds, void *stream);
+/* depth (1 for ordinary plans) and the stored CSR's shape / nnz */
+int bsgd_plan_stacked_info(const bsgd_plan *plan, int64_t *depth, int64_t *rows2, int64_t *cols2,
+                           int64_t *nnz2);
 int bsgd_plan_destroy(bsgd_plan *plan);
 /* tocsr (blockops.py:185-186): A's CSR copied to HOST buffers (rows+1, nnz, nnz) */
 int bsgd_plan_csr_copy(const bsgd_plan *plan, int64_t *indptr_out, int32_t *indices_out, void *values_out,

@@ -180,12 +180,52 @@ class BlockOperator:
         self._load_block_table()
 
     @classmethod
+    def stacked(cls, slice_matrix, depth: int, partition: BlockPartition | None = None, *, device=None,
+                dtype=None) -> "BlockOperator":
+        """Slice-stacked operator A = A2 (x) I_depth (configs[4], `csrc/stacked.cuh`).
+
+        Block-diagonal with the same 2-D matrix ``slice_matrix`` on every slice,
+        in the interleaved order (row r*depth + z, column c*depth + z).  Only A2
+        and A2^T live on the device; ``partition`` is over the logical
+        (rows2*depth) x (cols2*depth) operator.  Products run in the reference's
+        block-sequential order (bit-identical to the oracle on the expanded CSR).
+        """
+        csr = _canonical_csr(slice_matrix, dtype)
+        if csr.nnz == 0:
+            raise ValueError("matrix has no nonzeros")
+        if depth < 2:
+            raise ValueError("depth must be >= 2 (a single slice is an ordinary BlockOperator)")
+        rows2, cols2 = csr.shape
+        rows, cols = rows2 * depth, cols2 * depth
+        if partition is None:
+            partition = make_partition(rows, cols, 1, 1)
+        if partition.rows != rows or partition.cols != cols:
+            raise ValueError(f"partition covers {partition.rows}x{partition.cols}, operator is {rows}x{cols}")
+        self = cls.__new__(cls)
+        self._device = nat.require_cuda(device)
+        indptr = np.ascontiguousarray(csr.indptr, dtype=np.int64)
+        indices = np.ascontiguousarray(csr.indices, dtype=np.int32)
+        values = np.ascontiguousarray(csr.data)
+        rb, cb = partition.row_edges(), partition.col_edges()
+        handle = nat.c_p()
+        t = nat.torch()
+        with t.cuda.device(self._device):
+            nat.call("bsgd_plan_create_stacked", nat.ctypes.byref(handle), self._device.index, depth, rows2, cols2,
+                     csr.nnz, indptr.ctypes.data, indices.ctypes.data, values.ctypes.data, values.dtype.itemsize,
+                     partition.num_row_blocks, partition.num_col_blocks, rb.ctypes.data, cb.ctypes.data,
+                     nat.stream_ptr(self._device))
+        self._init_fields(handle, (rows, cols), csr.dtype, partition, int(csr.nnz) * depth, depth=depth)
+        self._slice_source = ("host", csr)
+        return self
+
+    @classmethod
     def from_parallel_beam(cls, n: int, num_angles: int, num_bins: int, num_row_blocks: int = 1,
-                           num_col_blocks: int = 1, dtype=np.float32, device=None) -> "BlockOperator":
+                           num_col_blocks: int = 1, dtype=np.float32, device=None, depth: int = 1) -> "BlockOperator":
         """Siddon parallel-beam projector generated on the GPU (`bsgd_siddon_csr`).
 
         Same matrix as `problems.parallel_beam_matrix` (bit-identical); the host
         never holds it, so configs[3]-size problems (~2e9 nonzeros) are possible.
+        ``depth`` > 1 stacks it over that many slices (configs[4]), see `stacked`.
         """
         import math
         self = cls.__new__(cls)
@@ -194,7 +234,8 @@ class BlockOperator:
         ang = [math.pi * a / num_angles for a in range(num_angles)]
         cs = np.array([math.cos(t) for t in ang], dtype=np.float64)
         sn = np.array([math.sin(t) for t in ang], dtype=np.float64)
-        rows, cols = num_angles * num_bins, n * n
+        rows2, cols2 = num_angles * num_bins, n * n
+        rows, cols = rows2 * depth, cols2 * depth
         partition = make_partition(rows, cols, num_row_blocks, num_col_blocks)
         ip, ix, vv = nat.c_p(), nat.c_p(), nat.c_p()
         nnz = nat.c_i64()
@@ -210,24 +251,34 @@ class BlockOperator:
                 raise ValueError("matrix has no nonzeros")
             rb, cb = partition.row_edges(), partition.col_edges()
             handle = nat.c_p()
-            rc = nat.load().bsgd_plan_create_device(nat.ctypes.byref(handle), self._device.index, rows, cols,
-                                                    nnz.value, ip, ix, vv, dt.itemsize, partition.num_row_blocks,
-                                                    partition.num_col_blocks, rb.ctypes.data, cb.ctypes.data, st)
+            if depth > 1:
+                rc = nat.load().bsgd_plan_create_stacked_device(
+                    nat.ctypes.byref(handle), self._device.index, depth, rows2, cols2, nnz.value, ip, ix, vv,
+                    dt.itemsize, partition.num_row_blocks, partition.num_col_blocks, rb.ctypes.data, cb.ctypes.data, st)
+            else:
+                rc = nat.load().bsgd_plan_create_device(
+                    nat.ctypes.byref(handle), self._device.index, rows, cols, nnz.value, ip, ix, vv, dt.itemsize,
+                    partition.num_row_blocks, partition.num_col_blocks, rb.ctypes.data, cb.ctypes.data, st)
             if rc != nat.OK:
                 for q in (ip, ix, vv):
                     nat.load().bsgd_device_free(q)
                 nat.check(rc)
+        self._init_fields(handle, (rows, cols), dt, partition, int(nnz.value) * depth, depth=depth)
+        self._slice_source = ("siddon", (n, num_angles, num_bins, dt))
+        return self
+
+    def _init_fields(self, handle, shape, dtype, partition, nnz_total, depth=1, csr=None) -> None:
         self._plan = handle
-        self._csr = None
-        self._shape = (rows, cols)
-        self._dtype = dt
+        self._csr = csr
+        self._shape = shape
+        self._dtype = np.dtype(dtype)
         self._partition = partition
-        self._nnz_total = int(nnz.value)
+        self._nnz_total = nnz_total
         self._nnz_applied = 0
         self._lock = threading.Lock()
         self._scratch = None
+        self._depth = depth
         self._load_block_table()
-        return self
 
     def _load_block_table(self) -> None:
         partition = self._partition
@@ -264,6 +315,11 @@ class BlockOperator:
     @property
     def partition(self) -> BlockPartition:
         return self._partition
+
+    @property
+    def depth(self) -> int:
+        """Slices of a stacked operator (1 for an ordinary one)."""
+        return getattr(self, "_depth", 1)
 
     @property
     def num_row_blocks(self) -> int:
@@ -330,6 +386,14 @@ class BlockOperator:
 
     def repartition(self, num_row_blocks: int, num_col_blocks: int) -> "BlockOperator":
         rows, cols = self.shape
+        if self.depth > 1:
+            kind, src = self._slice_source
+            if kind == "host":
+                return BlockOperator.stacked(src, self.depth, make_partition(rows, cols, num_row_blocks,
+                                                                             num_col_blocks), device=self._device)
+            n, ang, nb, dt = src
+            return BlockOperator.from_parallel_beam(n, ang, nb, num_row_blocks, num_col_blocks, dtype=dt,
+                                                    device=self._device, depth=self.depth)
         return BlockOperator(self.tocsr(), make_partition(rows, cols, num_row_blocks, num_col_blocks),
                              device=self._device)
 

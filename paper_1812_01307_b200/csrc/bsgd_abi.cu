@@ -26,6 +26,7 @@
 #include "spmv.cuh"
 #include "tiled.cuh"
 #include "siddon.cuh"
+#include "stacked.cuh"
 
 using namespace bsgd;
 
@@ -171,6 +172,12 @@ struct bsgd_plan {
         double *pout = nullptr; // [H][nrows] partial sums when H > 1
     } tf, tt;
     bool use_tiled = true;
+    // slice-stacked plans (stacked.cuh): A = A2 (x) I_depth in interleaved order;
+    // f_* / t_* then hold A2 / A2^T and rows/cols/nnz above are the logical sizes
+    int64_t depth = 1;
+    int64_t srows = 0, scols = 0, snnz = 0;  // stored CSR (A itself, or A2)
+    int lanes = 32, kz_fwd = 1, kz_tr = 1;
+    bool stacked() const { return depth > 1; }
 };
 
 struct DeviceGuard {
@@ -269,14 +276,14 @@ static int grid_1d(int64_t n, int per_cta_items = kThreads) {
 
 template <typename V>
 static int build_transpose(bsgd_plan *p, cudaStream_t st) {
-    const int64_t nnz = p->nnz;
+    const int64_t nnz = p->snnz;
     int32_t *rowid = nullptr;
     uint32_t *keys_out = nullptr, *pos_in = nullptr, *pos_out = nullptr;
     void *temp = nullptr;
     size_t temp_bytes = 0;
     int rc = BSGD_OK;
     int end_bit = 1;
-    while (end_bit < 32 && ((int64_t)1 << end_bit) <= p->cols) ++end_bit;
+    while (end_bit < 32 && ((int64_t)1 << end_bit) <= p->scols) ++end_bit;
     auto cleanup = [&]() { cudaFree(rowid); cudaFree(keys_out); cudaFree(pos_in); cudaFree(pos_out); cudaFree(temp); };
 #define TRY(call)                                                                        \
     do {                                                                                 \
@@ -292,7 +299,7 @@ static int build_transpose(bsgd_plan *p, cudaStream_t st) {
     TRY(cudaMalloc(&keys_out, sizeof(uint32_t) * nnz));
     TRY(cudaMalloc(&pos_in, sizeof(uint32_t) * nnz));
     TRY(cudaMalloc(&pos_out, sizeof(uint32_t) * nnz));
-    expand_rows_kernel<<<grid_1d(p->rows), kThreads, 0, st>>>(p->rows, p->f_ptr, rowid);
+    expand_rows_kernel<<<grid_1d(p->srows), kThreads, 0, st>>>(p->srows, p->f_ptr, rowid);
     iota_kernel<<<grid_1d(nnz), kThreads, 0, st>>>(nnz, pos_in);
     TRY(cudaGetLastError());
     const uint32_t *keys_in = reinterpret_cast<const uint32_t *>(p->f_idx);
@@ -303,7 +310,7 @@ static int build_transpose(bsgd_plan *p, cudaStream_t st) {
                                         end_bit, st));
     gather_transpose_kernel<V><<<grid_1d(nnz), kThreads, 0, st>>>(nnz, pos_out, rowid, (const V *)p->f_val,
                                                                   p->t_idx, (V *)p->t_val);
-    col_ptr_kernel<<<grid_1d(p->cols + 1), kThreads, 0, st>>>(p->cols, nnz, keys_out, p->t_ptr);
+    col_ptr_kernel<<<grid_1d(p->scols + 1), kThreads, 0, st>>>(p->scols, nnz, keys_out, p->t_ptr);
     TRY(cudaGetLastError());
     TRY(cudaStreamSynchronize(st));
 #undef TRY
@@ -593,14 +600,63 @@ static int autotune_direction(bsgd_plan *p, bool transposed, cudaStream_t st) {
     return BSGD_OK;
 }
 
+// slice-stacked products (stacked.cuh).  EpiResid becomes the in-kernel
+// y - z_0 - z_1 - ... chain with a plain store epilogue.
+template <typename V, int KZ, bool RESID, class E>
+static int launch_stacked_kz(const Stk<V> &A, const E &e, double *part, int64_t *cnt, cudaStream_t st) {
+    auto kern = stacked_kernel<V, KZ, RESID, E>;
+    const int rpw = 32 / A.L;
+    const int64_t items = cdiv(A.nrows, rpw) * cdiv(A.D, (int64_t)A.L * KZ);
+    const int cap = std::min(occupancy(kern) * num_sms(), kMaxPartials);
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(items, kThreads / 32), cap));
+    kern<<<grid, kThreads, 0, st>>>(A, e, part, cnt);
+    LAUNCHED();
+    return BSGD_OK;
+}
+
+template <typename V, bool RESID, class E>
+static int launch_stacked(const Stk<V> &A, int kz, const E &e, double *part, int64_t *cnt, cudaStream_t st) {
+    switch (kz) {
+        case 8: return launch_stacked_kz<V, 8, RESID>(A, e, part, cnt, st);
+        case 4: return launch_stacked_kz<V, 4, RESID>(A, e, part, cnt, st);
+        case 2: return launch_stacked_kz<V, 2, RESID>(A, e, part, cnt, st);
+        default: return launch_stacked_kz<V, 1, RESID>(A, e, part, cnt, st);
+    }
+}
+
+template <typename V, class E>
+static int launch_stacked_dir(const bsgd_plan *p, bool transposed, const double *vec, const E &e, double *part,
+                              int64_t *cnt, cudaStream_t st) {
+    Stk<V> A;
+    A.nrows = transposed ? p->scols : p->srows;
+    A.ptr = transposed ? p->t_ptr : p->f_ptr;
+    A.idx = transposed ? p->t_idx : p->f_idx;
+    A.val = (const V *)(transposed ? p->t_val : p->f_val);
+    A.vec = vec;
+    A.D = p->depth;
+    A.bounds = transposed ? p->d_row_bounds : p->d_col_bounds;
+    A.nb = transposed ? p->M : p->N;
+    A.y = nullptr;
+    A.L = p->lanes;
+    const int kz = transposed ? p->kz_tr : p->kz_fwd;
+    if constexpr (std::is_same<E, EpiResid>::value) {
+        A.y = e.y;
+        return launch_stacked<V, true>(A, kz, EpiResidFinal{e.r}, part, cnt, st);
+    } else {
+        return launch_stacked<V, false>(A, kz, e, part, cnt, st);
+    }
+}
+
 template <typename V, class E>
 static int launch_fwd(const bsgd_plan *p, const double *vec, const E &e, double *part, int64_t *cnt, cudaStream_t st) {
+    if (p->stacked()) return launch_stacked_dir<V>(p, false, vec, e, part, cnt, st);
     if (tiled_usable(p, p->tf, vec)) return launch_tiled<V>(p->tf, vec, e, part, cnt, st);
     return launch_one<V>(fwd_csr<V>(p, vec), p->g_fwd, e, part, cnt, p->nnz, st);
 }
 
 template <typename V, class E>
 static int launch_tr(const bsgd_plan *p, const double *vec, const E &e, double *part, int64_t *cnt, cudaStream_t st) {
+    if (p->stacked()) return launch_stacked_dir<V>(p, true, vec, e, part, cnt, st);
     if (tiled_usable(p, p->tt, vec)) return launch_tiled<V>(p->tt, vec, e, part, cnt, st);
     return launch_one<V>(tr_csr<V>(p, vec), p->g_tr, e, part, cnt, p->nnz, st);
 }
@@ -810,7 +866,8 @@ int bsgd_device_count(int *out) {
 
 // everything after A's CSR is on the device: validation, A^T, tiled copies, block table
 static int plan_finish(bsgd_plan *p, cudaStream_t st) {
-    const int64_t rows = p->rows, cols = p->cols, nnz = p->nnz;
+    // stored CSR sizes (A2 for stacked plans)
+    const int64_t rows = p->srows, cols = p->scols, nnz = p->snnz;
     const int value_dtype = p->vdt;
     const int64_t num_row_blocks = p->M, num_col_blocks = p->N;
     int rc = BSGD_OK;
@@ -849,7 +906,7 @@ static int plan_finish(bsgd_plan *p, cudaStream_t st) {
     if (rc != BSGD_OK) return rc;
     {
         const char *env = getenv("BSGD_TILED");
-        p->use_tiled = !(env && env[0] == '0');
+        p->use_tiled = !(env && env[0] == '0') && !p->stacked();
     }
     if (p->use_tiled) {
         // the tiled kernel sums each tile row with one lane: only short rows can win
@@ -883,8 +940,13 @@ static int plan_finish(bsgd_plan *p, cudaStream_t st) {
     const int64_t nb = num_row_blocks * num_col_blocks;
     PTRY(cudaMalloc(&d_cnt, sizeof(unsigned long long) * nb));
     PTRY(cudaMemsetAsync(d_cnt, 0, sizeof(unsigned long long) * nb, st));
-    block_nnz_kernel<<<grid_1d(rows), kThreads, 0, st>>>(rows, p->f_ptr, p->f_idx, num_row_blocks, p->d_row_bounds,
-                                                         num_col_blocks, p->d_col_bounds, d_cnt);
+    if (p->stacked())
+        stacked_block_nnz_kernel<<<grid_1d(p->rows), kThreads, 0, st>>>(p->f_ptr, p->f_idx, p->depth, p->rows,
+                                                                        p->d_row_bounds, num_row_blocks,
+                                                                        p->d_col_bounds, num_col_blocks, d_cnt);
+    else
+        block_nnz_kernel<<<grid_1d(rows), kThreads, 0, st>>>(rows, p->f_ptr, p->f_idx, num_row_blocks,
+                                                             p->d_row_bounds, num_col_blocks, p->d_col_bounds, d_cnt);
     std::vector<unsigned long long> cnt(nb);
     PTRY(cudaMemcpyAsync(cnt.data(), d_cnt, sizeof(unsigned long long) * nb, cudaMemcpyDeviceToHost, st));
     PTRY(cudaStreamSynchronize(st));
@@ -934,27 +996,57 @@ static bsgd_plan *plan_new(int device, int64_t rows, int64_t cols, int64_t nnz, 
     p->M = M; p->N = N;
     p->row_bounds.assign(row_bounds, row_bounds + M + 1);
     p->col_bounds.assign(col_bounds, col_bounds + N + 1);
+    p->srows = rows; p->scols = cols; p->snnz = nnz;
     const double mean_r = (double)nnz / rows, mean_c = (double)nnz / cols;
     p->g_fwd = mean_r < 64.0 ? 8 : 32;
     p->g_tr = mean_c < 64.0 ? 8 : 32;
     return p;
 }
 
-int bsgd_plan_create(bsgd_plan **out, int device, int64_t rows, int64_t cols, int64_t nnz,
-                     const int64_t *indptr, const int32_t *indices, const void *values, int value_dtype,
-                     int64_t num_row_blocks, int64_t num_col_blocks, const int64_t *row_bounds,
-                     const int64_t *col_bounds, void *stream) {
+// depth > 1: slice-stacked plan, (rows, cols, nnz) describe the stored A2
+static int stacked_check(int64_t depth, int64_t rows, int64_t cols) {
+    if (depth < 2) return fail(BSGD_EINVAL, "depth must be >= 2 (a single slice is an ordinary plan)");
+    if (rows > (((int64_t)1 << 31) - 1) / depth || cols > (((int64_t)1 << 31) - 1) / depth)
+        return fail(BSGD_EINVAL, "stacked dimensions must be < 2^31");
+    return BSGD_OK;
+}
+
+static void stacked_setup(bsgd_plan *p, int64_t depth, int64_t rows2, int64_t cols2, int64_t nnz2) {
+    p->depth = depth;
+    p->srows = rows2; p->scols = cols2; p->snnz = nnz2;
+    int L = 1;
+    while (L < 32 && L < depth) L <<= 1;
+    p->lanes = L;
+    // slices per chunk: keep (vector rows) x (chunk) x 8 bytes <= ~40 MB of L2
+    auto pick = [&](int64_t vec_rows) {
+        const int64_t zc_max = std::max<int64_t>(1, (int64_t)40000000 / (vec_rows * 8));
+        int kz = 8;
+        while (kz > 1 && ((int64_t)L * kz > zc_max || (int64_t)L * (kz / 2) >= depth)) kz /= 2;
+        return kz;
+    };
+    p->kz_fwd = pick(cols2);
+    p->kz_tr = pick(rows2);
+}
+
+static int plan_create_host(bsgd_plan **out, int device, int64_t depth, int64_t rows, int64_t cols, int64_t nnz,
+                            const int64_t *indptr, const int32_t *indices, const void *values, int value_dtype,
+                            int64_t num_row_blocks, int64_t num_col_blocks, const int64_t *row_bounds,
+                            const int64_t *col_bounds, void *stream) {
     if (!out) return fail(BSGD_EINVAL, "out is NULL");
     *out = nullptr;
-    int rc = plan_args_check(rows, cols, nnz, value_dtype, num_row_blocks, num_col_blocks, row_bounds, col_bounds,
-                             device);
+    int rc = depth > 1 ? stacked_check(depth, rows, cols) : BSGD_OK;
+    if (rc) return rc;
+    rc = plan_args_check(rows * depth, cols * depth, nnz, value_dtype, num_row_blocks, num_col_blocks, row_bounds,
+                         col_bounds, device);
     if (rc) return rc;
     if (!indptr || !indices || !values) return fail(BSGD_EINVAL, "NULL array");
     if (indptr[0] != 0 || indptr[rows] != nnz) return fail(BSGD_EINVAL, "indptr must run from 0 to nnz");
     DeviceGuard guard(device);
     cudaStream_t st = (cudaStream_t)stream;
-    bsgd_plan *p = plan_new(device, rows, cols, nnz, value_dtype, num_row_blocks, num_col_blocks, row_bounds,
-                            col_bounds);
+    bsgd_plan *p = plan_new(device, rows * depth, cols * depth, nnz * depth, value_dtype, num_row_blocks,
+                            num_col_blocks, row_bounds, col_bounds);
+    if (depth > 1) stacked_setup(p, depth, rows, cols, nnz);
+    else { p->srows = rows; p->scols = cols; p->snnz = nnz; }
     const size_t vb = (size_t)value_dtype;
     cudaError_t e = cudaSuccess;
     if (e == cudaSuccess) e = cudaMalloc(&p->f_ptr, sizeof(int64_t) * (rows + 1));
@@ -974,14 +1066,16 @@ int bsgd_plan_create(bsgd_plan **out, int device, int64_t rows, int64_t cols, in
     return BSGD_OK;
 }
 
-int bsgd_plan_create_device(bsgd_plan **out, int device, int64_t rows, int64_t cols, int64_t nnz, int64_t *indptr,
-                            int32_t *indices, void *values, int value_dtype, int64_t num_row_blocks,
-                            int64_t num_col_blocks, const int64_t *row_bounds, const int64_t *col_bounds,
-                            void *stream) {
+static int plan_create_adopt(bsgd_plan **out, int device, int64_t depth, int64_t rows, int64_t cols, int64_t nnz,
+                             int64_t *indptr, int32_t *indices, void *values, int value_dtype,
+                             int64_t num_row_blocks, int64_t num_col_blocks, const int64_t *row_bounds,
+                             const int64_t *col_bounds, void *stream) {
     if (!out) return fail(BSGD_EINVAL, "out is NULL");
     *out = nullptr;
-    int rc = plan_args_check(rows, cols, nnz, value_dtype, num_row_blocks, num_col_blocks, row_bounds, col_bounds,
-                             device);
+    int rc = depth > 1 ? stacked_check(depth, rows, cols) : BSGD_OK;
+    if (rc) return rc;
+    rc = plan_args_check(rows * depth, cols * depth, nnz, value_dtype, num_row_blocks, num_col_blocks, row_bounds,
+                         col_bounds, device);
     if (rc) return rc;
     if (!indptr || !indices || !values) return fail(BSGD_EINVAL, "NULL array");
     DeviceGuard guard(device);
@@ -991,14 +1085,59 @@ int bsgd_plan_create_device(bsgd_plan **out, int device, int64_t rows, int64_t c
     CU(cudaMemcpyAsync(&ends[1], indptr + rows, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));
     if (ends[0] != 0 || ends[1] != nnz) return fail(BSGD_EINVAL, "indptr must run from 0 to nnz");
-    bsgd_plan *p = plan_new(device, rows, cols, nnz, value_dtype, num_row_blocks, num_col_blocks, row_bounds,
-                            col_bounds);
+    bsgd_plan *p = plan_new(device, rows * depth, cols * depth, nnz * depth, value_dtype, num_row_blocks,
+                            num_col_blocks, row_bounds, col_bounds);
+    if (depth > 1) stacked_setup(p, depth, rows, cols, nnz);
+    else { p->srows = rows; p->scols = cols; p->snnz = nnz; }
     p->f_ptr = indptr;   // adopted: freed with the plan
     p->f_idx = indices;
     p->f_val = values;
     rc = plan_finish(p, st);
     if (rc) { plan_free(p); return rc; }
     *out = p;
+    return BSGD_OK;
+}
+
+int bsgd_plan_create(bsgd_plan **out, int device, int64_t rows, int64_t cols, int64_t nnz,
+                     const int64_t *indptr, const int32_t *indices, const void *values, int value_dtype,
+                     int64_t num_row_blocks, int64_t num_col_blocks, const int64_t *row_bounds,
+                     const int64_t *col_bounds, void *stream) {
+    return plan_create_host(out, device, 1, rows, cols, nnz, indptr, indices, values, value_dtype, num_row_blocks,
+                            num_col_blocks, row_bounds, col_bounds, stream);
+}
+
+int bsgd_plan_create_device(bsgd_plan **out, int device, int64_t rows, int64_t cols, int64_t nnz, int64_t *indptr,
+                            int32_t *indices, void *values, int value_dtype, int64_t num_row_blocks,
+                            int64_t num_col_blocks, const int64_t *row_bounds, const int64_t *col_bounds,
+                            void *stream) {
+    return plan_create_adopt(out, device, 1, rows, cols, nnz, indptr, indices, values, value_dtype, num_row_blocks,
+                             num_col_blocks, row_bounds, col_bounds, stream);
+}
+
+int bsgd_plan_create_stacked(bsgd_plan **out, int device, int64_t depth, int64_t rows2, int64_t cols2, int64_t nnz2,
+                             const int64_t *indptr, const int32_t *indices, const void *values, int value_dtype,
+                             int64_t num_row_blocks, int64_t num_col_blocks, const int64_t *row_bounds,
+                             const int64_t *col_bounds, void *stream) {
+    if (depth < 2) return fail(BSGD_EINVAL, "depth must be >= 2 (a single slice is an ordinary plan)");
+    return plan_create_host(out, device, depth, rows2, cols2, nnz2, indptr, indices, values, value_dtype,
+                            num_row_blocks, num_col_blocks, row_bounds, col_bounds, stream);
+}
+
+int bsgd_plan_create_stacked_device(bsgd_plan **out, int device, int64_t depth, int64_t rows2, int64_t cols2,
+                                    int64_t nnz2, int64_t *indptr, int32_t *indices, void *values, int value_dtype,
+                                    int64_t num_row_blocks, int64_t num_col_blocks, const int64_t *row_bounds,
+                                    const int64_t *col_bounds, void *stream) {
+    if (depth < 2) return fail(BSGD_EINVAL, "depth must be >= 2 (a single slice is an ordinary plan)");
+    return plan_create_adopt(out, device, depth, rows2, cols2, nnz2, indptr, indices, values, value_dtype,
+                             num_row_blocks, num_col_blocks, row_bounds, col_bounds, stream);
+}
+
+int bsgd_plan_stacked_info(const bsgd_plan *p, int64_t *depth, int64_t *rows2, int64_t *cols2, int64_t *nnz2) {
+    if (!p) return fail(BSGD_EINVAL, "plan is NULL");
+    if (depth) *depth = p->depth;
+    if (rows2) *rows2 = p->srows;
+    if (cols2) *cols2 = p->scols;
+    if (nnz2) *nnz2 = p->snnz;
     return BSGD_OK;
 }
 
@@ -1067,10 +1206,40 @@ int bsgd_device_free(void *ptr) {
     return BSGD_OK;
 }
 
+// host expansion of a stacked plan's logical CSR (A or A^T) restricted to
+// outputs [o0, o1) and entries [e0, e1): test / inspection paths only
+static int stacked_expand(const bsgd_plan *p, bool tr, int64_t o0, int64_t o1, int64_t e0, int64_t e1,
+                          int64_t *indptr_out, int32_t *indices_out, void *values_out, cudaStream_t st) {
+    const int64_t nr = tr ? p->scols : p->srows, D = p->depth, vb = p->vdt;
+    std::vector<int64_t> ptr(nr + 1);
+    std::vector<int32_t> idx(p->snnz);
+    std::vector<char> val((size_t)p->snnz * vb);
+    CU(cudaMemcpyAsync(ptr.data(), tr ? p->t_ptr : p->f_ptr, sizeof(int64_t) * (nr + 1), cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(idx.data(), tr ? p->t_idx : p->f_idx, sizeof(int32_t) * p->snnz, cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(val.data(), tr ? p->t_val : p->f_val, (size_t)p->snnz * vb, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    int64_t w = 0;
+    indptr_out[0] = 0;
+    for (int64_t O = o0; O < o1; ++O) {
+        const int64_t r = O / D, z = O - r * D;
+        for (int64_t k = ptr[r]; k < ptr[r + 1]; ++k) {
+            const int64_t E = (int64_t)idx[k] * D + z;
+            if (E >= e1) break;
+            if (E < e0) continue;
+            indices_out[w] = (int32_t)(E - e0);
+            memcpy((char *)values_out + (size_t)w * vb, val.data() + (size_t)k * vb, vb);
+            ++w;
+        }
+        indptr_out[O - o0 + 1] = w;
+    }
+    return BSGD_OK;
+}
+
 int bsgd_plan_csr_copy(const bsgd_plan *p, int64_t *indptr_out, int32_t *indices_out, void *values_out, void *stream) {
     if (!p || !indptr_out || !indices_out || !values_out) return fail(BSGD_EINVAL, "NULL argument");
     DeviceGuard guard(p->device);
     cudaStream_t st = (cudaStream_t)stream;
+    if (p->stacked()) return stacked_expand(p, false, 0, p->rows, 0, p->cols, indptr_out, indices_out, values_out, st);
     CU(cudaMemcpyAsync(indptr_out, p->f_ptr, sizeof(int64_t) * (p->rows + 1), cudaMemcpyDeviceToHost, st));
     CU(cudaMemcpyAsync(indices_out, p->f_idx, sizeof(int32_t) * p->nnz, cudaMemcpyDeviceToHost, st));
     CU(cudaMemcpyAsync(values_out, p->f_val, (size_t)p->vdt * p->nnz, cudaMemcpyDeviceToHost, st));
@@ -1119,6 +1288,7 @@ int bsgd_plan_block_copy(const bsgd_plan *p, int64_t i, int64_t j, int64_t *indp
     cudaStream_t st = (cudaStream_t)stream;
     const int64_t r0 = p->row_bounds[i], r1 = p->row_bounds[i + 1];
     const int64_t c0 = p->col_bounds[j], c1 = p->col_bounds[j + 1];
+    if (p->stacked()) return stacked_expand(p, false, r0, r1, c0, c1, indptr_out, indices_out, values_out, st);
     std::vector<int64_t> ptr(r1 - r0 + 1);
     CU(cudaMemcpyAsync(ptr.data(), p->f_ptr + r0, sizeof(int64_t) * (r1 - r0 + 1), cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));
@@ -1152,6 +1322,7 @@ int bsgd_plan_transpose_copy(const bsgd_plan *p, int64_t *indptr_out, int32_t *i
     if (!indptr_out || !indices_out || !values_out) return fail(BSGD_EINVAL, "NULL output");
     DeviceGuard guard(p->device);
     cudaStream_t st = (cudaStream_t)stream;
+    if (p->stacked()) return stacked_expand(p, true, 0, p->cols, 0, p->rows, indptr_out, indices_out, values_out, st);
     CU(cudaMemcpyAsync(indptr_out, p->t_ptr, sizeof(int64_t) * (p->cols + 1), cudaMemcpyDeviceToHost, st));
     CU(cudaMemcpyAsync(indices_out, p->t_idx, sizeof(int32_t) * p->nnz, cudaMemcpyDeviceToHost, st));
     CU(cudaMemcpyAsync(values_out, p->t_val, (size_t)p->vdt * p->nnz, cudaMemcpyDeviceToHost, st));
@@ -1166,6 +1337,17 @@ int bsgd_block_matvec(const bsgd_plan *p, int64_t i, int64_t j, const double *x_
     DeviceGuard guard(p->device);
     const int64_t r0 = p->row_bounds[i], r1 = p->row_bounds[i + 1];
     const int64_t c0 = p->col_bounds[j], c1 = p->col_bounds[j + 1];
+    if (p->stacked()) {
+        const int g = grid_1d(r1 - r0);
+        if (p->vdt == BSGD_F32)
+            stacked_block_kernel<float><<<g, kThreads, 0, (cudaStream_t)stream>>>(
+                p->f_ptr, p->f_idx, (const float *)p->f_val, p->depth, r0, r1, c0, c1, x_j, out);
+        else
+            stacked_block_kernel<double><<<g, kThreads, 0, (cudaStream_t)stream>>>(
+                p->f_ptr, p->f_idx, (const double *)p->f_val, p->depth, r0, r1, c0, c1, x_j, out);
+        LAUNCHED();
+        return BSGD_OK;
+    }
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(r1 - r0, kThreads / 32), num_sms() * 8));
     if (p->vdt == BSGD_F32)
         block_seg_kernel<float><<<grid, kThreads, 0, (cudaStream_t)stream>>>(p->f_ptr, p->f_idx, (const float *)p->f_val,
@@ -1185,6 +1367,17 @@ int bsgd_block_matvec_transpose(const bsgd_plan *p, int64_t i, int64_t j, const 
     DeviceGuard guard(p->device);
     const int64_t r0 = p->row_bounds[i], r1 = p->row_bounds[i + 1];
     const int64_t c0 = p->col_bounds[j], c1 = p->col_bounds[j + 1];
+    if (p->stacked()) {
+        const int g = grid_1d(c1 - c0);
+        if (p->vdt == BSGD_F32)
+            stacked_block_kernel<float><<<g, kThreads, 0, (cudaStream_t)stream>>>(
+                p->t_ptr, p->t_idx, (const float *)p->t_val, p->depth, c0, c1, r0, r1, r_i, out);
+        else
+            stacked_block_kernel<double><<<g, kThreads, 0, (cudaStream_t)stream>>>(
+                p->t_ptr, p->t_idx, (const double *)p->t_val, p->depth, c0, c1, r0, r1, r_i, out);
+        LAUNCHED();
+        return BSGD_OK;
+    }
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(c1 - c0, kThreads / 32), num_sms() * 8));
     // A^T rows [c0, c1), entries with A-row index in [r0, r1)
     if (p->vdt == BSGD_F32)
@@ -1263,6 +1456,26 @@ int bsgd_pair_products(const bsgd_plan *p, int64_t n_rows_sel, const int64_t *ro
     }
     DeviceGuard guard(p->device);
     cudaStream_t st = (cudaStream_t)stream;
+    if (p->stacked()) {
+        const int gr = grid_1d(p->rows), gc = grid_1d(p->cols);
+        if (p->vdt == BSGD_F32) {
+            stacked_pair_grad_kernel<float><<<gc, kThreads, 0, st>>>(p->t_ptr, p->t_idx, (const float *)p->t_val,
+                                                                     p->depth, p->cols, p->d_row_bounds, p->M,
+                                                                     p->d_col_bounds, p->N, rs, cs, r_k, g);
+            stacked_pair_forward_kernel<float><<<gr, kThreads, 0, st>>>(
+                p->f_ptr, p->f_idx, (const float *)p->f_val, p->depth, p->rows, p->d_row_bounds, p->M,
+                p->d_col_bounds, p->N, rs, cs, x_k, y, z_cache, r_next);
+        } else {
+            stacked_pair_grad_kernel<double><<<gc, kThreads, 0, st>>>(p->t_ptr, p->t_idx, (const double *)p->t_val,
+                                                                      p->depth, p->cols, p->d_row_bounds, p->M,
+                                                                      p->d_col_bounds, p->N, rs, cs, r_k, g);
+            stacked_pair_forward_kernel<double><<<gr, kThreads, 0, st>>>(
+                p->f_ptr, p->f_idx, (const double *)p->f_val, p->depth, p->rows, p->d_row_bounds, p->M,
+                p->d_col_bounds, p->N, rs, cs, x_k, y, z_cache, r_next);
+        }
+        LAUNCHED();
+        return BSGD_OK;
+    }
     const int gr = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(p->rows, kThreads / 32), num_sms() * 8));
     const int gc = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(p->cols, kThreads / 32), num_sms() * 8));
     if (p->vdt == BSGD_F32) {
@@ -1524,7 +1737,7 @@ int bsgd_epoch(const bsgd_plan *p, const bsgd_epoch_args *a, void *stream) {
         rc = run_step(p->cols, a, ws, st);
         if (!rc && (fl & BSGD_EP_R_NEXT))
             rc = DISPATCH_V(p, launch_fwd<V>(p, a->x_k, EpiResid{a->y, a->r_next}, ws.rpart, ws.ctl + 2, st));
-    } else if ((fl & BSGD_EP_R_NEXT) && tiled) {
+    } else if ((fl & BSGD_EP_R_NEXT) && (tiled || p->stacked())) {
         rc = DISPATCH_V(p, launch_fwd<V>(p, a->x_k, EpiResid{a->y, a->r_next}, ws.rpart, ws.ctl + 2, st));
         if (!rc) rc = DISPATCH_V(p, launch_tr<V>(p, a->r_k, es, ws.xpart, ws.ctl, st));
     } else if (fl & BSGD_EP_R_NEXT) {

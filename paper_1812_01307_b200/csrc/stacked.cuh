@@ -1,0 +1,303 @@
+// Slice-stacked operator for 3-D parallel-beam CT (configs[4], SURVEY.md §8 row f).
+//
+// configs[4]'s A is block-diagonal per slice with the same 2-D Siddon matrix
+// A2 on every slice.  Stored as such it is ~1e10 nonzeros (~80 GB, twice that
+// with A^T); stored as A2 (~4e7 nonzeros, ~0.3 GB) it fits next to everything
+// else in one GPU's HBM.  The plan keeps A2 and A2^T and applies them to all
+// slices at once in the INTERLEAVED order
+//
+//     row R = r * D + z,   column C = c * D + z,   A[R, C] = A2[r, c],
+//
+// i.e. A = A2 (x) I_D.  A product is then a sparse-times-tall-skinny product:
+// one (c, A2[r, c]) entry is read once and applied to D contiguous vector
+// values x[c*D .. c*D + D), so vector traffic is coalesced 8-byte-per-lane
+// rows instead of random 8-byte gathers, and matrix traffic is D times
+// smaller.  The solver vector's interleaved order maps to the z-major volume
+// through the ordinary layout permutation (tv.VolumeLayout).
+//
+// Arithmetic order.  Every output is accumulated in the reference's exact
+// order (oracle/bsgd_oracle.c, scipy's csr_matvec / csc_matvec restated):
+// sequential products inside each block segment, one multiply and one add per
+// term (no FMA), block segments folded in ascending block order -- so the
+// stacked products, block products and pair products are bit-identical to the
+// oracle's, and the K1 residual is y - z_0 - z_1 - ... exactly as
+// assemble_residual (blockops.py:264-278).
+//
+// Work decomposition.  A work item is one stored row and a chunk of ZC = L*KZ
+// slices: L lanes per row (L = min(32, pow2ceil(D))), KZ slices per lane,
+// lane g handling z = z0 + g + L*s.  Items run chunk-major, so the warps in
+// flight all read the same slice chunk of the vector and its working set
+// (stored columns x ZC x 8 bytes) stays L2-resident; the host picks KZ so that
+// this is <= ~40 MB.  The L lanes of a row load L entries cooperatively and
+// broadcast them with width-L shuffles.
+#pragma once
+
+#include "common.cuh"
+
+namespace bsgd {
+
+template <typename V>
+struct Stk {
+    int64_t nrows;          // stored rows (A2 rows for K1, A2^T rows for K2)
+    const int64_t *ptr;
+    const int32_t *idx;
+    const V *val;
+    const double *vec;      // interleaved input, indexed by the entry's interleaved index
+    int64_t D;              // slices
+    const int64_t *bounds;  // block bounds over the entries' interleaved index (col bounds for K1, row bounds for K2)
+    int64_t nb;             // number of blocks
+    const double *y;        // residual mode: measurements (interleaved rows)
+    int L;                  // lanes per stored row (power of two <= 32)
+};
+
+// residual-mode epilogue target: the kernel already formed y - z_0 - z_1 - ...
+struct EpiResidFinal {
+    double *r;
+    double acc = 0.0;
+    static constexpr int K = 1;
+    __device__ __forceinline__ void operator()(int64_t row, double v) {
+        r[row] = v;
+        acc += v * v;
+    }
+    __device__ __forceinline__ void flush(double *v) { v[0] = acc; }
+};
+
+// RESID = false: out = ((s_0 + s_1) + s_2) + ...   (blockops.py:237-243 / 254-260)
+// RESID = true : out = ((y - s_0) - s_1) - ...     (assemble_residual)
+template <typename V, int KZ, bool RESID, class Epi>
+__global__ void __launch_bounds__(kThreads) stacked_kernel(Stk<V> A, Epi epi, double *part, int64_t *cnt) {
+    __shared__ double sm[8 * (kThreads / 32)];
+    const int lane = threadIdx.x & 31;
+    const int L = A.L;
+    const int rpw = 32 / L;
+    const int sub = lane / L, gl = lane - sub * L;
+    const unsigned gmask = (L == 32) ? 0xffffffffu : (((1u << L) - 1u) << (sub * L));
+    const int64_t D = A.D;
+    const int64_t ZC = (int64_t)L * KZ;
+    const int64_t nchunks = (D + ZC - 1) / ZC;
+    const int64_t ngroups = (A.nrows + rpw - 1) / rpw;
+    const int64_t items = ngroups * nchunks;
+    const int64_t nwarps = (int64_t)gridDim.x * (kThreads / 32);
+    const uint64_t pol = policy_evict_first();
+    const double *__restrict__ vec = A.vec;
+    const int64_t b1 = __ldg(A.bounds + 1);
+
+    for (int64_t it = (int64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5); it < items; it += nwarps) {
+        const int64_t ch = it / ngroups, grp = it - ch * ngroups;
+        const int64_t r = grp * rpw + sub;
+        const bool live = r < A.nrows;
+        const int64_t zb = ch * ZC + gl;
+        double seg[KZ], acc[KZ];
+        int64_t nbnd[KZ];
+        int jb[KZ];
+#pragma unroll
+        for (int s = 0; s < KZ; ++s) {
+            const int64_t z = zb + (int64_t)s * L;
+            seg[s] = 0.0;
+            acc[s] = (RESID && live && z < D) ? A.y[r * D + z] : 0.0;
+            nbnd[s] = b1;
+            jb[s] = 0;
+        }
+        auto fold = [&](int s) {
+            if constexpr (RESID) acc[s] = rn_sub(acc[s], seg[s]);
+            else acc[s] = (jb[s] == 0) ? seg[s] : rn_add(acc[s], seg[s]);
+            seg[s] = 0.0;
+        };
+        auto consume = [&](int32_t ce, double ve, const double (&xs)[KZ]) {
+#pragma unroll
+            for (int s = 0; s < KZ; ++s) {
+                const int64_t z = zb + (int64_t)s * L;
+                if (z < D) {
+                    const int64_t C = (int64_t)ce * D + z;
+                    while (C >= nbnd[s]) {
+                        fold(s);
+                        ++jb[s];
+                        nbnd[s] = __ldg(A.bounds + jb[s] + 1);
+                    }
+                    seg[s] = rn_add(seg[s], rn_mul(ve, xs[s]));
+                }
+            }
+        };
+        const int64_t beg = live ? A.ptr[r] : 0, end = live ? A.ptr[r + 1] : 0;
+        for (int64_t k0 = beg; k0 < end; k0 += L) {
+            const int64_t k = k0 + gl;
+            int32_t c = 0;
+            double v = 0.0;
+            if (k < end) {
+                c = ld_stream(A.idx + k, pol);
+                v = (double)ld_stream(A.val + k, pol);
+            }
+            const int n = (int)((end - k0) < L ? (end - k0) : L);
+            int e = 0;
+            for (; e + 4 <= n; e += 4) {
+                int32_t cc[4];
+                double vv[4], xx[4][KZ];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    cc[u] = __shfl_sync(gmask, c, e + u, L);
+                    vv[u] = __shfl_sync(gmask, v, e + u, L);
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+#pragma unroll
+                    for (int s = 0; s < KZ; ++s) {
+                        const int64_t z = zb + (int64_t)s * L;
+                        xx[u][s] = (z < D) ? __ldg(vec + (int64_t)cc[u] * D + z) : 0.0;
+                    }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) consume(cc[u], vv[u], xx[u]);
+            }
+            for (; e < n; ++e) {
+                const int32_t ce = __shfl_sync(gmask, c, e, L);
+                const double ve = __shfl_sync(gmask, v, e, L);
+                double xs[KZ];
+#pragma unroll
+                for (int s = 0; s < KZ; ++s) {
+                    const int64_t z = zb + (int64_t)s * L;
+                    xs[s] = (z < D) ? __ldg(vec + (int64_t)ce * D + z) : 0.0;
+                }
+                consume(ce, ve, xs);
+            }
+        }
+#pragma unroll
+        for (int s = 0; s < KZ; ++s) {
+            const int64_t z = zb + (int64_t)s * L;
+            if (live && z < D) {
+                for (; jb[s] < A.nb; ++jb[s]) fold(s);  // the open segment, then empty trailing blocks
+                epi(r * D + z, acc[s]);
+            }
+        }
+    }
+    if constexpr (Epi::K > 0) {
+        double v[Epi::K];
+        epi.flush(v);
+        block_sum<Epi::K>(v, sm);
+        if (threadIdx.x == 0 && part != nullptr)
+            for (int k = 0; k < Epi::K; ++k) part[(size_t)blockIdx.x * Epi::K + k] = v[k];
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0 && cnt != nullptr) cnt[0] = gridDim.x;
+}
+
+// ---------------------------------------------------------------------------
+// block-restricted and stochastic-pair products (thread per interleaved output)
+// ---------------------------------------------------------------------------
+
+// out[O - o0] = sum over stored row O / D, entries with E = e*D + O%D in [e0, e1):
+// A2[.,.] vec[E - e0]   (orc_block_matvec / orc_block_rmatvec order)
+template <typename V>
+__global__ void __launch_bounds__(kThreads) stacked_block_kernel(const int64_t *ptr, const int32_t *idx,
+                                                                 const V *val, int64_t D, int64_t o0,
+                                                                 int64_t o1, int64_t e0, int64_t e1,
+                                                                 const double *vec, double *out) {
+    for (int64_t O = o0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; O < o1;
+         O += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = O / D, z = O - r * D;
+        double s = 0.0;
+        for (int64_t k = ptr[r]; k < ptr[r + 1]; ++k) {
+            const int64_t E = (int64_t)idx[k] * D + z;
+            if (E >= e1) break;
+            if (E >= e0) s = rn_add(s, rn_mul((double)val[k], vec[E - e0]));
+        }
+        out[O - o0] = s;
+    }
+}
+
+// z_cache[j, R] for the selected (row block of R, j) pairs; then r_next[R] =
+// y[R] - z_cache[0, R] - ... for every R (solvers.py:274-297, alpha/gamma < 1)
+template <typename V>
+__global__ void __launch_bounds__(kThreads) stacked_pair_forward_kernel(
+    const int64_t *ptr, const int32_t *idx, const V *val, int64_t D, int64_t rows, const int64_t *rb, int64_t M,
+    const int64_t *cb, int64_t N, BlockMask rsel, BlockMask csel, const double *x, const double *y,
+    double *z_cache, double *r_next) {
+    for (int64_t R = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; R < rows; R += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = R / D, z = R - r * D;
+        if (rsel.has(block_of(rb, M, R))) {
+            int64_t j = 0;
+            double s = 0.0;
+            for (int64_t k = ptr[r]; k < ptr[r + 1]; ++k) {
+                const int64_t C = (int64_t)idx[k] * D + z;
+                while (C >= cb[j + 1]) {
+                    if (csel.has(j)) z_cache[j * rows + R] = s;
+                    s = 0.0;
+                    ++j;
+                }
+                s = rn_add(s, rn_mul((double)val[k], x[C]));
+            }
+            for (; j < N; ++j) {
+                if (csel.has(j)) z_cache[j * rows + R] = s;
+                s = 0.0;
+            }
+        }
+        double acc = y[R];
+        for (int64_t j = 0; j < N; ++j) acc = rn_sub(acc, z_cache[j * rows + R]);
+        r_next[R] = acc;
+    }
+}
+
+// g[C] = 2 * (0 + t_i1 + t_i2 + ...) over the selected row blocks in ascending
+// order for columns of selected column blocks, 0 elsewhere (solvers.py:299-303)
+template <typename V>
+__global__ void __launch_bounds__(kThreads) stacked_pair_grad_kernel(
+    const int64_t *tptr, const int32_t *tidx, const V *tval, int64_t D, int64_t cols, const int64_t *rb, int64_t M,
+    const int64_t *cb, int64_t N, BlockMask rsel, BlockMask csel, const double *r, double *g) {
+    for (int64_t C = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; C < cols; C += (int64_t)gridDim.x * blockDim.x) {
+        double acc = 0.0;
+        if (csel.has(block_of(cb, N, C))) {
+            const int64_t c = C / D, z = C - c * D;
+            int64_t i = 0;
+            double s = 0.0;
+            for (int64_t k = tptr[c]; k < tptr[c + 1]; ++k) {
+                const int64_t R = (int64_t)tidx[k] * D + z;
+                while (R >= rb[i + 1]) {
+                    if (rsel.has(i)) acc = rn_add(acc, s);
+                    s = 0.0;
+                    ++i;
+                }
+                s = rn_add(s, rn_mul((double)tval[k], r[R]));
+            }
+            for (; i < M; ++i) {
+                if (rsel.has(i)) acc = rn_add(acc, s);
+                s = 0.0;
+            }
+        }
+        g[C] = 2.0 * acc;
+    }
+}
+
+// nnz of every (row block, column block) of A2 (x) I_D; tbl in shared memory
+// when M*N <= kStkTbl, else global atomics
+constexpr int kStkTbl = 4096;
+__global__ void __launch_bounds__(kThreads) stacked_block_nnz_kernel(const int64_t *ptr, const int32_t *idx, int64_t D,
+                                                                     int64_t rows, const int64_t *rb, int64_t M,
+                                                                     const int64_t *cb, int64_t N,
+                                                                     unsigned long long *cnt) {
+    __shared__ unsigned long long tbl[kStkTbl];
+    const bool local = M * N <= kStkTbl;
+    if (local)
+        for (int64_t t = threadIdx.x; t < M * N; t += blockDim.x) tbl[t] = 0;
+    __syncthreads();
+    unsigned long long *dst = local ? tbl : cnt;
+    for (int64_t R = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; R < rows; R += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = R / D, z = R - r * D;
+        const int64_t i = block_of(rb, M, R);
+        int64_t j = 0;
+        unsigned long long run = 0;
+        for (int64_t k = ptr[r]; k < ptr[r + 1]; ++k) {
+            const int64_t C = (int64_t)idx[k] * D + z;
+            while (C >= cb[j + 1]) {
+                if (run) atomicAdd(dst + i * N + j, run);
+                run = 0;
+                ++j;
+            }
+            ++run;
+        }
+        if (run) atomicAdd(dst + i * N + j, run);
+    }
+    if (local) {
+        __syncthreads();
+        for (int64_t t = threadIdx.x; t < M * N; t += blockDim.x)
+            if (tbl[t]) atomicAdd(cnt + t, tbl[t]);
+    }
+}
+
+}  // namespace bsgd

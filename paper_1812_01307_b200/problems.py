@@ -68,6 +68,58 @@ def ellipse_phantom(n: int, num_ellipses: int, seed: int) -> np.ndarray:
     return img
 
 
+def ellipsoid_parameters(num_ellipsoids: int, seed: int) -> np.ndarray:
+    """(k, 8): centre x, y, z, semi-axes a, b, c, rotation about z, intensity.
+
+    3-D analogue of `ellipse_parameters` for configs[4] ("3D random ellipsoids
+    (40, seeded)"): centres uniform in the unit ball, semi-axes U[0.05, 0.4],
+    in-plane rotation U[0, pi), additive intensity U[0, 1].
+    """
+    rng = np.random.default_rng(seed)
+    u = rng.random((num_ellipsoids, 8))
+    rad = np.cbrt(u[:, 0])
+    cos_pol = 2.0 * u[:, 1] - 1.0
+    sin_pol = np.sqrt(np.maximum(0.0, 1.0 - cos_pol * cos_pol))
+    az = 2.0 * math.pi * u[:, 2]
+    out = np.empty_like(u)
+    out[:, 0] = rad * sin_pol * np.cos(az)
+    out[:, 1] = rad * sin_pol * np.sin(az)
+    out[:, 2] = rad * cos_pol
+    out[:, 3:6] = 0.05 + 0.35 * u[:, 3:6]
+    out[:, 6] = math.pi * u[:, 6]
+    out[:, 7] = u[:, 7]
+    return out
+
+
+def ellipsoid_phantom(n: int, depth: int, num_ellipsoids: int, seed: int) -> np.ndarray:
+    """Random-ellipsoid phantom at voxel centres, shape (depth, n, n), float64.
+
+    In-plane coordinates as `ellipse_phantom`; slice z sits at (2z + 1 - depth)/depth.
+    """
+    params = ellipsoid_parameters(num_ellipsoids, seed)
+    cols = (2.0 * np.arange(n) + 1.0 - n) / n
+    rows = (n - 2.0 * np.arange(n) - 1.0) / n
+    zs = (2.0 * np.arange(depth) + 1.0 - depth) / depth
+    xu, yu = np.meshgrid(cols, rows)
+    vol = np.zeros((depth, n, n))
+    for cx, cy, cz, a, b, c, phi, val in params:
+        ct, st = math.cos(phi), math.sin(phi)
+        xr = (xu - cx) * ct + (yu - cy) * st
+        yr = -(xu - cx) * st + (yu - cy) * ct
+        plane = (xr / a) ** 2 + (yr / b) ** 2
+        for z in range(depth):
+            dz = ((zs[z] - cz) / c) ** 2
+            if dz <= 1.0:
+                vol[z][plane + dz <= 1.0] += val
+    return vol
+
+
+def interleaved_perm(n_pixels: int, depth: int) -> np.ndarray:
+    """Solver position k = pixel*depth + z  ->  z-major voxel z*n_pixels + pixel."""
+    k = np.arange(n_pixels * depth, dtype=np.int64)
+    return (k % depth) * n_pixels + k // depth
+
+
 # --- parallel-beam Siddon projector --------------------------------------
 
 
@@ -281,6 +333,15 @@ class DeviceProblem:
     max_inner_iters: int
     epochs: int
     seeds: dict
+    depth: int = 1                  # > 1: slice-stacked volume (solver order interleaved, see layout())
+
+    def layout(self):
+        """Pixel / voxel layout of the solver vector (tv.PixelLayout or tv.VolumeLayout)."""
+        from . import tv
+        if self.depth > 1:
+            return tv.VolumeLayout(self.depth, self.height, self.width,
+                                   interleaved_perm(self.height * self.width, self.depth))
+        return tv.PixelLayout.row_major(self.height, self.width)
 
 
 def ct_problem_device(name: str, n: int, num_angles: int, num_bins: int, num_ellipses: int, noise_frac: float,
@@ -303,8 +364,37 @@ def ct_problem_device(name: str, n: int, num_angles: int, num_bins: int, num_ell
                          epochs, {"phantom": phantom_seed, "noise": noise_seed, "solver": 0})
 
 
+def stacked_ct_problem_device(name: str, n: int, depth: int, num_angles: int, num_bins: int, num_ellipsoids: int,
+                              noise_frac: float, num_blocks: int, lam: float, max_inner_iters: int, epochs: int,
+                              dtype=np.float32, phantom_seed: int = 0, noise_seed: int = 1,
+                              device=None) -> DeviceProblem:
+    """3-D slice-stacked parallel-beam CT (configs[4]): A = A2 (x) I_depth on the GPU.
+
+    x_true is the ellipsoid phantom in the interleaved solver order (voxel
+    (z, s, t) at position (s*n + t)*depth + z); y = A x_true + N(0, sigma^2),
+    sigma = noise_frac * max(A x_true).
+    """
+    from .blockops import BlockOperator
+    op = BlockOperator.from_parallel_beam(n, num_angles, num_bins, num_blocks, num_blocks, dtype=dtype,
+                                          device=device, depth=depth)
+    vol = ellipsoid_phantom(n, depth, num_ellipsoids, phantom_seed)
+    x_true = np.ascontiguousarray(vol.reshape(depth, n * n).T).ravel()
+    clean = op.matvec(x_true, charge=False)
+    sigma = noise_frac * float(np.max(clean))
+    noise = np.random.default_rng(noise_seed).standard_normal(clean.shape[0]) * sigma
+    return DeviceProblem(name, op, clean + noise, x_true, n, n, num_blocks, num_blocks, lam, max_inner_iters,
+                         epochs, {"phantom": phantom_seed, "noise": noise_seed, "solver": 0}, depth=depth)
+
+
 def config_device(index: int, scale: float = 1.0, device=None) -> DeviceProblem:
-    """configs[0], [2] or [3] with the projector generated on the GPU."""
+    """configs[0], [2], [3] or [4] with the projector generated on the GPU."""
+    if index == 4:
+        n = max(16, int(round(256 * scale)))
+        depth = max(2, int(round(256 * scale)))
+        ang = max(8, int(round(360 * scale)))
+        nb = max(9, int(round(363 * scale)) | 1)
+        return stacked_ct_problem_device("C5", n, depth, ang, nb, 40, 0.01, 16, 0.01, 10, 30, np.float32,
+                                         device=device)
     table = {0: ("C1", 128, 180, 183, 10, 0.01, 4, 0.02, 20, 100, np.float64),
              2: ("C3", 512, 720, 727, 30, 0.005, 8, 0.01, 20, 100, np.float32),
              3: ("C4", 1024, 1440, 1449, 60, 0.005, 8, 0.01, 20, 50, np.float32)}

@@ -1,0 +1,131 @@
+"""Slice-stacked operator (configs[4]) against the oracle on the expanded CSR.
+
+`BlockOperator.stacked(A2, D)` stores only the 2-D slice matrix; the oracle
+gets the full interleaved matrix kron(A2, I_D).  The stacked kernels follow the
+reference's block-sequential arithmetic (one multiply and one add per term,
+block segments folded in order), so every product is BIT-EXACT against the
+oracle, and so is the x trajectory of a TV-regularised run (3-D prox included);
+only the Eq. 9 monitor value and sampled objectives use a different reduction
+order (1e-12 relative).
+"""
+
+import numpy as np
+import pytest
+from scipy import sparse
+
+from oracle import oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def M(cuda_ok):
+    from paper_1812_01307_b200 import blockops, problems, solvers, spectral, tv
+    return blockops, problems, solvers, spectral, tv
+
+
+def _expanded(a2, depth):
+    a = sparse.csr_array(sparse.kron(sparse.csr_array(a2), sparse.identity(depth, format="csr"), format="csr"))
+    a.sort_indices()
+    return a
+
+
+CASES = [(8, 6, 11, 3, 2, 3, np.float64), (8, 6, 11, 16, 3, 2, np.float32), (6, 5, 9, 40, 4, 4, np.float64),
+         (10, 8, 15, 64, 16, 16, np.float32), (5, 4, 7, 33, 1, 1, np.float64)]
+
+
+@pytest.mark.parametrize("n,ang,nb,depth,m,nblk,dt", CASES)
+def test_stacked_products_bit_exact(M, n, ang, nb, depth, m, nblk, dt):
+    blockops, problems = M[0], M[1]
+    a2 = problems.parallel_beam_matrix(n, ang, nb, dtype=dt)
+    a = _expanded(a2, depth)
+    part = blockops.make_partition(a.shape[0], a.shape[1], m, nblk)
+    op = blockops.BlockOperator.stacked(a2, depth, part)
+    oop = orc.OracleOperator(a, m, nblk)
+    assert op.shape == a.shape and op.nnz == a.nnz and op.depth == depth
+    rng = np.random.default_rng(depth)
+    x = rng.standard_normal(a.shape[1])
+    r = rng.standard_normal(a.shape[0])
+    assert np.array_equal(op.matvec(x), oop.matvec(x))
+    assert np.array_equal(op.rmatvec(r), oop.rmatvec(r))
+    for i in range(m):
+        for j in range(nblk):
+            assert op.block_nnz(i, j) == oop.block_nnz(i, j)
+            r0, r1 = part.row_range(i)
+            c0, c1 = part.col_range(j)
+            blk = oop.block_csr(i, j)
+            got = op.block(i, j)
+            assert np.array_equal(got.indptr, blk.indptr) and np.array_equal(got.indices, blk.indices)
+            assert np.array_equal(got.data, blk.data)
+            zs, gs = oop.pair_products([(i, j)], x, r)
+            assert np.array_equal(op.block_matvec(i, j, x[c0:c1]), zs[0])
+            assert np.array_equal(op.block_matvec_transpose(i, j, r[r0:r1]), gs[0])
+    csr = op.tocsr()
+    assert np.array_equal(csr.indptr, a.indptr) and np.array_equal(csr.indices, a.indices)
+    assert np.array_equal(csr.data, a.data)
+    ip, ix, vv = op.transpose_pattern()
+    at = sparse.csr_array(a.T)
+    at.sort_indices()
+    assert np.array_equal(ip, at.indptr) and np.array_equal(ix, at.indices) and np.array_equal(vv, at.data)
+
+
+def test_stacked_residual_and_errors(M):
+    blockops, problems = M[0], M[1]
+    a2 = problems.parallel_beam_matrix(8, 6, 11)
+    depth = 5
+    a = _expanded(a2, depth)
+    op = blockops.BlockOperator.stacked(a2, depth, blockops.make_partition(*a.shape, 2, 2))
+    rng = np.random.default_rng(1)
+    x, y = rng.standard_normal(a.shape[1]), rng.standard_normal(a.shape[0])
+    r, s = op.residual_sumsq(x, y)
+    want = y - a @ x
+    assert np.allclose(r.cpu().numpy(), want, rtol=0, atol=1e-12 * np.abs(want).max())
+    assert float(s.item()) == pytest.approx(float(want @ want), rel=1e-12)
+    with pytest.raises(ValueError):
+        blockops.BlockOperator.stacked(a2, 1)
+    with pytest.raises(ValueError):
+        blockops.BlockOperator.stacked(a2, depth, blockops.make_partition(a.shape[0] + 1, a.shape[1], 1, 1))
+
+
+@pytest.mark.parametrize("lam,alpha,epochs", [(0.01, 1.0, 6), (0.0, 1.0, 5), (0.02, 0.5, 6)])
+def test_stacked_run_vs_oracle_bit_exact(M, lam, alpha, epochs):
+    """TV-regularised (3-D prox) and least-squares runs: x bit-identical to the oracle."""
+    blockops, problems, solvers, spectral, tv = M
+    n, depth, m = 12, 8, 4
+    a2 = problems.parallel_beam_matrix(n, 10, 17)
+    a = _expanded(a2, depth)
+    op = blockops.BlockOperator.stacked(a2, depth, blockops.make_partition(*a.shape, m, m))
+    vol = problems.ellipsoid_phantom(n, depth, 6, 0)
+    x_true = np.ascontiguousarray(vol.reshape(depth, n * n).T).ravel()
+    y = a @ x_true + np.random.default_rng(1).standard_normal(a.shape[0]) * 0.01
+    oop = orc.OracleOperator(a, m, m)
+    u, _, _ = orc.largest_eigenvalue(oop)
+    mu = 0.9 / (2.0 * u)
+    perm = problems.interleaved_perm(n * n, depth)
+    layout = tv.VolumeLayout(depth, n, n, perm) if lam > 0 else None
+    cfg = solvers.SolverConfig(mu=mu, lam=lam, alpha=alpha, gamma=alpha, epochs=epochs, seed=3,
+                               prox=tv.ProxSettings(10, 1e-5))
+    tr = solvers.run_solver("bsgd", solvers.Problem(op, y, x_true, layout), cfg)
+    prm = orc.Params(mu=mu, lam=lam, alpha=alpha, gamma=alpha, epochs=epochs, seed=3, max_inner_iters=10, tol=1e-5)
+    ref = orc.run_bsgd(oop, y, prm, x_true=x_true, perm=perm if lam > 0 else None, hw=(depth, n, n))
+    assert np.array_equal(tr.final_x, ref.final_x)
+    got = np.array([tuple(s) for s in tr.samples])
+    want = np.array(ref.samples)
+    assert np.array_equal(got[:, 0], want[:, 0])
+    assert np.allclose(got[:, 1], want[:, 1], rtol=1e-12)
+    assert np.allclose(got[:, 2], want[:, 2], rtol=1e-12)
+
+
+def test_stacked_device_generator_matches_host(M):
+    """from_parallel_beam(depth=D) == BlockOperator.stacked(parallel_beam_matrix(...), D)."""
+    blockops, problems = M[0], M[1]
+    n, ang, nb, depth = 16, 12, 23, 7
+    dev = blockops.BlockOperator.from_parallel_beam(n, ang, nb, 2, 2, dtype=np.float32, depth=depth)
+    a2 = problems.parallel_beam_matrix(n, ang, nb, dtype=np.float32)
+    host = blockops.BlockOperator.stacked(a2, depth, blockops.make_partition(*dev.shape, 2, 2))
+    assert dev.nnz == host.nnz
+    x = np.random.default_rng(2).random(dev.shape[1])
+    assert np.array_equal(dev.matvec(x), host.matvec(x))
+    d = problems.config_device(4, scale=0.0625)
+    assert d.op.depth == d.depth == 16 and d.op.shape[1] == 16 * 16 * 16
+    assert d.layout().size == d.op.shape[1]
