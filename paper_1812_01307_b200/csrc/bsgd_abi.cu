@@ -673,7 +673,7 @@ struct Ws {
     double *scal;    // prox scalars + reduction results
     double *xpart;   // [kMaxPartials * 4]
     double *rpart;   // [kMaxPartials]
-    double *red;     // [2 * kMaxPartials * 4]
+    double *red;     // [2 * kMaxPartials * kPwMaxK]
     double *uimg;    // [cols]
     double *fields;  // [9 * n]: p, q, c for up to three axes
 };
@@ -687,7 +687,7 @@ static size_t ws_layout(void *base, int64_t cols, int64_t hw, Ws *ws) {
     char *scal = take(sizeof(double) * 32);
     char *xpart = take(sizeof(double) * kMaxPartials * 4);
     char *rpart = take(sizeof(double) * kMaxPartials);
-    char *red = take(sizeof(double) * 2 * kMaxPartials * 4);
+    char *red = take(sizeof(double) * 2 * kMaxPartials * kPwMaxK);
     char *uimg = take(sizeof(double) * (size_t)std::max<int64_t>(cols, 1));
     char *fields = take(sizeof(double) * 9 * (size_t)std::max<int64_t>(hw, 0));
     if (ws) {
@@ -798,7 +798,7 @@ __global__ void tail_kernel(TailArgs t) {
 // prox launch
 // ---------------------------------------------------------------------------
 template <int DIM>
-static size_t prox_dyn_smem() { return sizeof(double) * 2 * DIM * kPwChunk * 128; }
+static size_t prox_dyn_smem() { return sizeof(double) * 2 * DIM * fgp_chunk<DIM>() * 128; }
 
 template <int DIM>
 static int prox_occupancy() {
@@ -820,7 +820,9 @@ static int launch_prox_dim(ProxArgs &a, cudaStream_t st) {
     // G: a power of two (numpy-order top tree), co-resident, <= 512
     int grid = pow2_floor(std::max<int64_t>(1, std::min<int64_t>((int64_t)occ * num_sms(), 512)));
     const int64_t S = (int64_t)1 << a.ds;
-    if (S / grid > kPwMaxQ) return fail(BSGD_EINVAL, "image too large for the pairwise tree (%lld pixels)", (long long)a.N);
+    const int64_t per_slot = a.fast ? fgp_chunk<DIM>() : kThreads / 8;  // subtrees folded per smem slot
+    if (S / grid > kPwMaxQ * per_slot)
+        return fail(BSGD_EINVAL, "image too large for the pairwise tree (%lld pixels)", (long long)a.N);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(kThreads);
@@ -1589,7 +1591,7 @@ static int tv_value_any(int64_t depth, int64_t height, int64_t width, const doub
     if (rc) return rc;
     const int64_t S = (int64_t)1 << ds;
     const int G = (int)std::min<int64_t>(S, 256);
-    if (S / G > kPwMaxQ) return fail(BSGD_EINVAL, "image too large for tv_value (%lld pixels)", (long long)n);
+    if (S / G > kPwMaxQ * (kThreads / 8)) return fail(BSGD_EINVAL, "image too large for tv_value (%lld pixels)", (long long)n);
     if (depth > 1) tv_value_part_kernel<3><<<G, kThreads, 0, st>>>(depth, height, width, img, ds, (double *)scratch);
     else tv_value_part_kernel<2><<<G, kThreads, 0, st>>>(1, height, width, img, ds, (double *)scratch);
     pw_top_kernel<<<1, kThreads, 0, st>>>(ds, G, (const double *)scratch, out);

@@ -34,7 +34,7 @@ struct ProxArgs {
     int64_t D, H, W, N;    // D = 1 for images; 3D volumes are z-major (z, row, column)
     const double *b;       // input image (row-major)
     double *f[9];          // p[DIM], q[DIM], c[DIM] (workspace); 2D: pv, ph, qv, qh, cv, ch
-    double *red;           // [2][kMaxPartials * 4] reduction partials
+    double *red;           // [2][kMaxPartials * kPwMaxK] reduction partials
     double w, step, tol;
     int32_t max_iters;
     int32_t ds;            // numpy pairwise depth for N (pw_depth)
@@ -154,11 +154,15 @@ __device__ __forceinline__ double tv_term(const double *u, int64_t p, int64_t W,
 
 // numpy-order grid sum of K per-pixel terms (pairwise.cuh); all threads get the
 // totals.  Term functors may write outputs: each pixel is visited once.
-template <int K, class F>
+// leaves per term chunk of the fast path: 2D 16, 3D 8 (keeps 2 CTAs per SM)
+template <int DIM>
+__host__ __device__ constexpr int fgp_chunk() { return DIM == 3 ? 8 : kPwChunk; }
+
+template <int K, int CH, class F>
 __device__ __forceinline__ void np_sum(cg::grid_group &grid, int64_t N, int ds, F &f, double *red, int &round,
                                        double *sm, double (&out)[K], int fast, double *T) {
-    double *buf = red + (size_t)(round & 1) * kMaxPartials * 4;
-    if (fast) pw_cta_fast<K>(ds, f, T, sm, buf);
+    double *buf = red + (size_t)(round & 1) * kMaxPartials * kPwMaxK;
+    if (fast) pw_cta_fast<K, F, CH>(ds, f, T, sm, buf);
     else pw_cta<K>(N, ds, f, sm, buf);
     grid.sync();
     pw_top<K>(ds, gridDim.x, buf, sm, out);
@@ -169,7 +173,8 @@ template <int DIM>
 __global__ void __launch_bounds__(kThreads, 2) fgp_kernel(ProxArgs a) {
     cg::grid_group grid = cg::this_grid();
     __shared__ double sm[kPwMaxQ * kPwMaxK];
-    extern __shared__ double Tsm[];   // 2*DIM * kPwChunk * 128 doubles (fast path)
+    extern __shared__ double Tsm[];   // 2*DIM * CH * 128 doubles (fast path)
+    constexpr int CH = fgp_chunk<DIM>();
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
     const int64_t N = a.N, W = a.W, H = a.H, D = a.D;
@@ -191,7 +196,7 @@ __global__ void __launch_bounds__(kThreads, 2) fgp_kernel(ProxArgs a) {
             t[0] = rn_mul(bb, bb);
             t[1] = tv_term<DIM>(b, p, H, W, false);
         };
-        np_sum<2>(grid, N, a.ds, f0, a.red, round, sm, v2, a.fast, Tsm);
+        np_sum<2, CH>(grid, N, a.ds, f0, a.red, round, sm, v2, a.fast, Tsm);
     }
     double phi_prev = v2[0];
     const double tv_b = v2[1];
@@ -216,7 +221,7 @@ __global__ void __launch_bounds__(kThreads, 2) fgp_kernel(ProxArgs a) {
         grid.sync();
         // B: phi = np.sum(resid * resid) (tv.py:215-216)
         double v1[1];
-        np_sum<1>(grid, N, a.ds, fphi, a.red, round, sm, v1, a.fast, Tsm);
+        np_sum<1, CH>(grid, N, a.ds, fphi, a.red, round, sm, v1, a.fast, Tsm);
         double phi = v1[0];
         if (phi > phi_prev) {  // restart from the last accepted point (tv.py:217-231)
             ++restarts;
@@ -228,7 +233,7 @@ __global__ void __launch_bounds__(kThreads, 2) fgp_kernel(ProxArgs a) {
                 for (int k = 0; k < DIM; ++k) C[k][p] = c[k];
             }
             grid.sync();
-            np_sum<1>(grid, N, a.ds, fphi, a.red, round, sm, v1, a.fast, Tsm);
+            np_sum<1, CH>(grid, N, a.ds, fphi, a.red, round, sm, v1, a.fast, Tsm);
             phi = v1[0];
         }
         // C: momentum commit (tv.py:233-245): q = c + beta (c - p);
@@ -246,7 +251,7 @@ __global__ void __launch_bounds__(kThreads, 2) fgp_kernel(ProxArgs a) {
             }
         };
         double vc[2 * DIM];
-        np_sum<2 * DIM>(grid, N, a.ds, fcom, a.red, round, sm, vc, a.fast, Tsm);
+        np_sum<2 * DIM, CH>(grid, N, a.ds, fcom, a.red, round, sm, vc, a.fast, Tsm);
 #pragma unroll
         for (int k = 0; k < DIM; ++k) { double *tmp_ = P[k]; P[k] = C[k]; C[k] = tmp_; }  // p <- c
         phi_prev = (phi_prev < phi) ? phi_prev : phi;  // Python min(phi, phi_prev)
@@ -275,7 +280,7 @@ __global__ void __launch_bounds__(kThreads, 2) fgp_kernel(ProxArgs a) {
         t[1] = tv_term<DIM>(tmp, p, H, W, true);
     };
     double e2[2];
-    np_sum<2>(grid, N, a.ds, fen, a.red, round, sm, e2, a.fast, Tsm);
+    np_sum<2, CH>(grid, N, a.ds, fen, a.red, round, sm, e2, a.fast, Tsm);
     const double two_w = 2.0 * w;
     const double obj_out = rn_add(e2[0], rn_mul(two_w, e2[1]));
     const double obj_b = rn_add(0.0, rn_mul(two_w, tv_b));

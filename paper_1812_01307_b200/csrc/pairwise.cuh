@@ -122,9 +122,13 @@ __device__ __forceinline__ void pw_smem_tree(double *v, int count) {
 
 // CTA part: this CTA's subtrees -> one K-vector (written to part[blockIdx.x]).
 // Returns the number of subtrees this CTA owned (0 means it wrote nothing).
-// `sm` holds kPwMaxQ * K doubles.
+// Subtrees are evaluated in rounds of one per 8-lane group; each round's
+// (power-of-two, aligned) run is folded by a balanced tree -- exactly the
+// lower levels of the balanced tree over all Q -- so `sm` only holds one
+// K-vector per round: Q <= kPwMaxQ * (blockDim.x / 8).
 template <int K, class F>
 __device__ __forceinline__ int pw_cta(int64_t N, int ds, F &f, double *sm, double *part) {
+    __shared__ double lv[(kThreads / 8) * kPwMaxK];
     const int64_t S = (int64_t)1 << ds;
     const int G = gridDim.x;
     int64_t first;
@@ -141,18 +145,27 @@ __device__ __forceinline__ int pw_cta(int64_t N, int ds, F &f, double *sm, doubl
     const unsigned gm = 0xFFu << (lane & 24);
     const int group = threadIdx.x >> 3;
     const int ngroups = blockDim.x >> 3;
-    for (int q = group; q < Q; q += ngroups) {
-        int64_t lo, n;
-        pw_subtree(N, ds, first + q, lo, n);
-        double v[K];
-        pw_node<K, F, 4>(lo, n, f, gm, j, v);
-        if (j == 0)
+    int rounds = 0;
+    for (int q0 = 0; q0 < Q; q0 += ngroups, ++rounds) {
+        const int nq = (Q - q0 < ngroups) ? Q - q0 : ngroups;
+        if (group < nq) {
+            int64_t lo, n;
+            pw_subtree(N, ds, first + q0 + group, lo, n);
+            double v[K];
+            pw_node<K, F, 4>(lo, n, f, gm, j, v);
+            if (j == 0)
 #pragma unroll
-            for (int k = 0; k < K; ++k) sm[q * K + k] = v[k];
+                for (int k = 0; k < K; ++k) lv[group * K + k] = v[k];
+        }
+        __syncthreads();
+        pw_smem_tree<K>(lv, nq);
+        if (threadIdx.x == 0)
+#pragma unroll
+            for (int k = 0; k < K; ++k) sm[rounds * K + k] = lv[k];
+        __syncthreads();
     }
-    __syncthreads();
     if (Q > 0) {
-        pw_smem_tree<K>(sm, Q);
+        pw_smem_tree<K>(sm, rounds);
         if (threadIdx.x == 0)
 #pragma unroll
             for (int k = 0; k < K; ++k) part[(size_t)blockIdx.x * K + k] = sm[k];
@@ -179,13 +192,18 @@ __device__ __forceinline__ void pw_top(int ds, int G, const double *part, double
 
 // Fast path for N = 128 * 2^ds (every power-of-two image >= 16 x 16): each
 // subtree is one full 128-element leaf.  Terms are produced by all threads in
-// coalesced order into shared memory (kPwChunk leaves at a time), then thread
+// coalesced order into shared memory (CH leaves at a time), then thread
 // (leaf, j) runs accumulator j's sequential chain over the leaf's 16 strided
 // terms and an 8-lane butterfly forms ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)).
-constexpr int kPwChunk = 16;   // leaves per chunk: K * 16 * 128 doubles of smem
+// Each chunk's CH leaves (an aligned power-of-two run) are folded by a
+// balanced tree at once, so `leafv` holds one K-vector per chunk:
+// Q <= kPwMaxQ * CH.  T holds K * CH * 128 doubles.
+constexpr int kPwChunk = 16;   // default leaves per chunk
 
-template <int K, class F>
+template <int K, class F, int CH = kPwChunk>
 __device__ __forceinline__ int pw_cta_fast(int ds, F &f, double *T, double *leafv, double *part) {
+    __shared__ double lv[kPwChunk * kPwMaxK];
+    static_assert(CH <= kPwChunk && CH * 8 <= kThreads, "chunk too large");
     const int64_t S = (int64_t)1 << ds;
     const int G = gridDim.x;
     int64_t first;
@@ -199,15 +217,16 @@ __device__ __forceinline__ int pw_cta_fast(int ds, F &f, double *T, double *leaf
     }
     const int tid = threadIdx.x;
     const int lane = tid & 31;
-    for (int c0 = 0; c0 < Q; c0 += kPwChunk) {
-        const int nl = (Q - c0 < kPwChunk) ? Q - c0 : kPwChunk;
+    int chunks = 0;
+    for (int c0 = 0; c0 < Q; c0 += CH, ++chunks) {
+        const int nl = (Q - c0 < CH) ? Q - c0 : CH;
         const int npx = nl * 128;
         const int64_t px0 = (first + c0) * 128;
         for (int i = tid; i < npx; i += blockDim.x) {
             double t[K];
             f(px0 + i, t);
 #pragma unroll
-            for (int k = 0; k < K; ++k) T[k * (kPwChunk * 128) + i] = t[k];
+            for (int k = 0; k < K; ++k) T[k * (CH * 128) + i] = t[k];
         }
         __syncthreads();
         if (tid < nl * 8) {
@@ -216,7 +235,7 @@ __device__ __forceinline__ int pw_cta_fast(int ds, F &f, double *T, double *leaf
             double r[K];
 #pragma unroll
             for (int k = 0; k < K; ++k) {
-                const double *src = T + k * (kPwChunk * 128) + leaf * 128 + j;
+                const double *src = T + k * (CH * 128) + leaf * 128 + j;
                 double acc = src[0];
 #pragma unroll
                 for (int i = 1; i < 16; ++i) acc = rn_add(acc, src[8 * i]);
@@ -230,12 +249,17 @@ __device__ __forceinline__ int pw_cta_fast(int ds, F &f, double *T, double *leaf
             }
             if (j == 0)
 #pragma unroll
-                for (int k = 0; k < K; ++k) leafv[(c0 + leaf) * K + k] = r[k];
+                for (int k = 0; k < K; ++k) lv[leaf * K + k] = r[k];
         }
+        __syncthreads();
+        pw_smem_tree<K>(lv, nl);
+        if (tid == 0)
+#pragma unroll
+            for (int k = 0; k < K; ++k) leafv[chunks * K + k] = lv[k];
         __syncthreads();
     }
     if (Q > 0) {
-        pw_smem_tree<K>(leafv, Q);
+        pw_smem_tree<K>(leafv, chunks);
         if (threadIdx.x == 0)
 #pragma unroll
             for (int k = 0; k < K; ++k) part[(size_t)blockIdx.x * K + k] = leafv[k];

@@ -199,7 +199,7 @@ def test_tv_prox_vs_reference_golden(B):
 
 
 @pytest.mark.parametrize("shape,w", [((64, 64), 1e-3), ((64, 64), 0.05), ((37, 101), 0.2), ((200, 3), 1.0),
-                                     ((256, 256), 0.01)])
+                                     ((256, 256), 0.01), ((1024, 1024), 0.01), ((1000, 999), 0.02)])
 def test_tv_prox_vs_oracle_random(B, shape, w):
     tv = B[1]
     img = np.random.default_rng(sum(shape)).random(shape) * 2.0

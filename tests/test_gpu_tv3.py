@@ -23,7 +23,8 @@ def tv(cuda_ok):
 
 @pytest.mark.parametrize("shape,w,iters", [((4, 3, 5), 0.3, 20), ((8, 12, 16), 0.05, 20), ((16, 16, 16), 0.02, 20),
                                            ((2, 64, 64), 0.1, 10), ((32, 32, 32), 0.01, 10),
-                                           ((5, 40, 7), 1e-3, 30)])
+                                           ((5, 40, 7), 1e-3, 30), ((64, 128, 128), 0.02, 8),
+                                           ((100, 100, 100), 0.05, 6)])
 def test_tv_prox3_bit_exact(tv, shape, w, iters):
     vol = np.random.default_rng(sum(shape)).random(shape) * 2.0
     out, info = tv.tv_prox(tv.VolumeGrid.from_array(vol), w, tv.ProxSettings(iters, 1e-12), return_info=True)
