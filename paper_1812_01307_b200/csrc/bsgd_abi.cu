@@ -177,6 +177,7 @@ struct bsgd_plan {
     int64_t depth = 1;
     int64_t srows = 0, scols = 0, snnz = 0;  // stored CSR (A itself, or A2)
     int lanes = 32, kz_fwd = 1, kz_tr = 1;
+    int64_t *d_col_sbounds = nullptr, *d_row_sbounds = nullptr;  // bounds / depth when all are multiples of it
     bool stacked() const { return depth > 1; }
 };
 
@@ -267,6 +268,7 @@ static void plan_free(bsgd_plan *p) {
     cudaFree(p->f_ptr); cudaFree(p->f_idx); cudaFree(p->f_val);
     cudaFree(p->t_ptr); cudaFree(p->t_idx); cudaFree(p->t_val);
     cudaFree(p->d_row_bounds); cudaFree(p->d_col_bounds);
+    cudaFree(p->d_col_sbounds); cudaFree(p->d_row_sbounds);
     delete p;
 }
 
@@ -602,9 +604,9 @@ static int autotune_direction(bsgd_plan *p, bool transposed, cudaStream_t st) {
 
 // slice-stacked products (stacked.cuh).  EpiResid becomes the in-kernel
 // y - z_0 - z_1 - ... chain with a plain store epilogue.
-template <typename V, int KZ, bool RESID, class E>
-static int launch_stacked_kz(const Stk<V> &A, const E &e, double *part, int64_t *cnt, cudaStream_t st) {
-    auto kern = stacked_kernel<V, KZ, RESID, E>;
+template <typename V, int KZ, bool RESID, bool ALIGNED, bool W, class E>
+static int launch_stacked_k(const Stk<V> &A, const E &e, double *part, int64_t *cnt, cudaStream_t st) {
+    auto kern = stacked_kernel<V, KZ, RESID, ALIGNED, W, E>;
     const int rpw = 32 / A.L;
     const int64_t items = cdiv(A.nrows, rpw) * cdiv(A.D, (int64_t)A.L * KZ);
     const int cap = std::min(occupancy(kern) * num_sms(), kMaxPartials);
@@ -614,10 +616,19 @@ static int launch_stacked_kz(const Stk<V> &A, const E &e, double *part, int64_t 
     return BSGD_OK;
 }
 
+template <typename V, int KZ, bool RESID, class E>
+static int launch_stacked_kz(const Stk<V> &A, const E &e, double *part, int64_t *cnt, cudaStream_t st) {
+    const bool aligned = A.sbounds != nullptr;
+    const bool wide = A.L == 32 && A.D % (32 * KZ) == 0;
+    if (aligned && wide) return launch_stacked_k<V, KZ, RESID, true, true>(A, e, part, cnt, st);
+    if (wide) return launch_stacked_k<V, KZ, RESID, false, true>(A, e, part, cnt, st);
+    if (aligned) return launch_stacked_k<V, KZ, RESID, true, false>(A, e, part, cnt, st);
+    return launch_stacked_k<V, KZ, RESID, false, false>(A, e, part, cnt, st);
+}
+
 template <typename V, bool RESID, class E>
 static int launch_stacked(const Stk<V> &A, int kz, const E &e, double *part, int64_t *cnt, cudaStream_t st) {
     switch (kz) {
-        case 8: return launch_stacked_kz<V, 8, RESID>(A, e, part, cnt, st);
         case 4: return launch_stacked_kz<V, 4, RESID>(A, e, part, cnt, st);
         case 2: return launch_stacked_kz<V, 2, RESID>(A, e, part, cnt, st);
         default: return launch_stacked_kz<V, 1, RESID>(A, e, part, cnt, st);
@@ -635,6 +646,7 @@ static int launch_stacked_dir(const bsgd_plan *p, bool transposed, const double 
     A.vec = vec;
     A.D = p->depth;
     A.bounds = transposed ? p->d_row_bounds : p->d_col_bounds;
+    A.sbounds = transposed ? p->d_row_sbounds : p->d_col_sbounds;
     A.nb = transposed ? p->M : p->N;
     A.y = nullptr;
     A.L = p->lanes;
@@ -892,6 +904,20 @@ static int plan_finish(bsgd_plan *p, cudaStream_t st) {
                          cudaMemcpyHostToDevice, st));
     PTRY(cudaMemcpyAsync(p->d_col_bounds, p->col_bounds.data(), sizeof(int64_t) * (num_col_blocks + 1),
                          cudaMemcpyHostToDevice, st));
+    if (p->stacked()) {  // block bounds in stored-index units when every bound is a multiple of depth
+        auto upload = [&](const std::vector<int64_t> &b, int64_t **dst) -> int {
+            for (int64_t v : b)
+                if (v % p->depth) return BSGD_OK;
+            std::vector<int64_t> q(b.size());
+            for (size_t i = 0; i < b.size(); ++i) q[i] = b[i] / p->depth;
+            PTRY(cudaMalloc(dst, sizeof(int64_t) * q.size()));
+            PTRY(cudaMemcpy(*dst, q.data(), sizeof(int64_t) * q.size(), cudaMemcpyHostToDevice));
+            return BSGD_OK;
+        };
+        rc = upload(p->col_bounds, &p->d_col_sbounds);
+        if (!rc) rc = upload(p->row_bounds, &p->d_row_sbounds);
+        if (rc) return rc;
+    }
     // structural check (canonical form: sorted unique in-range indices per row)
     int *d_bad = nullptr;
     PTRY(cudaMalloc(&d_bad, sizeof(int)));
@@ -1019,10 +1045,10 @@ static void stacked_setup(bsgd_plan *p, int64_t depth, int64_t rows2, int64_t co
     int L = 1;
     while (L < 32 && L < depth) L <<= 1;
     p->lanes = L;
-    // slices per chunk: keep (vector rows) x (chunk) x 8 bytes <= ~40 MB of L2
+    // slices per chunk: keep (vector rows) x (chunk) x 8 bytes <= ~64 MB of L2
     auto pick = [&](int64_t vec_rows) {
-        const int64_t zc_max = std::max<int64_t>(1, (int64_t)40000000 / (vec_rows * 8));
-        int kz = 8;
+        const int64_t zc_max = std::max<int64_t>(1, (int64_t)64000000 / (vec_rows * 8));
+        int kz = 4;
         while (kz > 1 && ((int64_t)L * kz > zc_max || (int64_t)L * (kz / 2) >= depth)) kz /= 2;
         return kz;
     };

@@ -58,6 +58,13 @@ __device__ __forceinline__ float4 ld_stream4(const float *p, uint64_t pol) {
     return v;
 }
 
+__device__ __forceinline__ double2 ld_stream2(const double *p, uint64_t pol) {
+    double2 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
+                 : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(pol));
+    return v;
+}
+
 // ---- deterministic reductions: fixed shuffle tree, fixed warp order.
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll

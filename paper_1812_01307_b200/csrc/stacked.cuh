@@ -27,9 +27,11 @@
 // slices: L lanes per row (L = min(32, pow2ceil(D))), KZ slices per lane,
 // lane g handling z = z0 + g + L*s.  Items run chunk-major, so the warps in
 // flight all read the same slice chunk of the vector and its working set
-// (stored columns x ZC x 8 bytes) stays L2-resident; the host picks KZ so that
-// this is <= ~40 MB.  The L lanes of a row load L entries cooperatively and
-// broadcast them with width-L shuffles.
+// (stored columns x ZC x 8 bytes) stays L2-resident; the host picks KZ to
+// bound it.  The L lanes of a row read its entries with 16-byte broadcast
+// loads (4 entries per request) and issue 4*KZ independent vector loads before
+// the in-order multiply/add chain, so the loop is a few instructions per
+// (entry, slice) rather than per-lane shuffles and index arithmetic.
 #pragma once
 
 #include "common.cuh"
@@ -38,16 +40,17 @@ namespace bsgd {
 
 template <typename V>
 struct Stk {
-    int64_t nrows;          // stored rows (A2 rows for K1, A2^T rows for K2)
+    int64_t nrows;           // stored rows (A2 rows for K1, A2^T rows for K2)
     const int64_t *ptr;
     const int32_t *idx;
     const V *val;
-    const double *vec;      // interleaved input, indexed by the entry's interleaved index
-    int64_t D;              // slices
-    const int64_t *bounds;  // block bounds over the entries' interleaved index (col bounds for K1, row bounds for K2)
-    int64_t nb;             // number of blocks
-    const double *y;        // residual mode: measurements (interleaved rows)
-    int L;                  // lanes per stored row (power of two <= 32)
+    const double *vec;       // interleaved input, indexed by the entry's interleaved index
+    int64_t D;               // slices
+    const int64_t *bounds;   // block bounds over the entries' interleaved index (col bounds for K1, row bounds for K2)
+    const int64_t *sbounds;  // ALIGNED: the same bounds / D (every bound a multiple of D)
+    int64_t nb;              // number of blocks
+    const double *y;         // residual mode: measurements (interleaved rows)
+    int L;                   // lanes per stored row (power of two <= 32)
 };
 
 // residual-mode epilogue target: the kernel already formed y - z_0 - z_1 - ...
@@ -62,109 +65,153 @@ struct EpiResidFinal {
     __device__ __forceinline__ void flush(double *v) { v[0] = acc; }
 };
 
+// four consecutive entries (k 4-aligned) with 16-byte streaming loads; every
+// lane of a row group reads the same addresses (one broadcast request)
+template <typename V>
+__device__ __forceinline__ void stk_load4(const int32_t *idx, const V *val, int64_t k, uint64_t pol, int32_t (&c)[4],
+                                          double (&v)[4]) {
+    const int4 c4 = ld_stream4(idx + k, pol);
+    c[0] = c4.x; c[1] = c4.y; c[2] = c4.z; c[3] = c4.w;
+    if constexpr (sizeof(V) == 4) {
+        const float4 v4 = ld_stream4(reinterpret_cast<const float *>(val) + k, pol);
+        v[0] = v4.x; v[1] = v4.y; v[2] = v4.z; v[3] = v4.w;
+    } else {
+        const double2 a = ld_stream2(reinterpret_cast<const double *>(val) + k, pol);
+        const double2 b = ld_stream2(reinterpret_cast<const double *>(val) + k + 2, pol);
+        v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+    }
+}
+
 // RESID = false: out = ((s_0 + s_1) + s_2) + ...   (blockops.py:237-243 / 254-260)
 // RESID = true : out = ((y - s_0) - s_1) - ...     (assemble_residual)
-template <typename V, int KZ, bool RESID, class Epi>
+// ALIGNED: every block bound is a multiple of D, so an entry's block depends on
+//          its stored index only: one test per entry serves all slices.
+//          Otherwise each slice keeps its own stored-index threshold
+//          ceil((bound - z) / D), still one 32-bit compare per slice.
+// W: one row per warp (L = 32) and D a multiple of 32*KZ: slice offsets are
+//    compile-time and no slice predicates are needed.
+// Interleaved indices are < 2^31 (checked at plan creation), so all index
+// arithmetic is 32-bit.
+template <typename V, int KZ, bool RESID, bool ALIGNED, bool W, class Epi>
 __global__ void __launch_bounds__(kThreads) stacked_kernel(Stk<V> A, Epi epi, double *part, int64_t *cnt) {
     __shared__ double sm[8 * (kThreads / 32)];
     const int lane = threadIdx.x & 31;
-    const int L = A.L;
+    const int L = W ? 32 : A.L;
     const int rpw = 32 / L;
     const int sub = lane / L, gl = lane - sub * L;
-    const unsigned gmask = (L == 32) ? 0xffffffffu : (((1u << L) - 1u) << (sub * L));
-    const int64_t D = A.D;
-    const int64_t ZC = (int64_t)L * KZ;
+    const int32_t D = (int32_t)A.D;
+    const uint32_t D8 = 8u * (uint32_t)D;
+    const int32_t ZC = L * KZ;
     const int64_t nchunks = (D + ZC - 1) / ZC;
     const int64_t ngroups = (A.nrows + rpw - 1) / rpw;
     const int64_t items = ngroups * nchunks;
     const int64_t nwarps = (int64_t)gridDim.x * (kThreads / 32);
     const uint64_t pol = policy_evict_first();
-    const double *__restrict__ vec = A.vec;
-    const int64_t b1 = __ldg(A.bounds + 1);
+    const int32_t *__restrict__ idx = A.idx;
+    const V *__restrict__ val = A.val;
 
     for (int64_t it = (int64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5); it < items; it += nwarps) {
         const int64_t ch = it / ngroups, grp = it - ch * ngroups;
         const int64_t r = grp * rpw + sub;
         const bool live = r < A.nrows;
-        const int64_t zb = ch * ZC + gl;
+        const int32_t zb = (int32_t)ch * ZC + gl;
+        const double *__restrict__ xb = A.vec + zb;
         double seg[KZ], acc[KZ];
-        int64_t nbnd[KZ];
+        int32_t thr[KZ];
         int jb[KZ];
+        bool zok[KZ];
 #pragma unroll
         for (int s = 0; s < KZ; ++s) {
-            const int64_t z = zb + (int64_t)s * L;
+            const int32_t z = zb + s * L;
+            zok[s] = W ? live : (live && z < D);
             seg[s] = 0.0;
-            acc[s] = (RESID && live && z < D) ? A.y[r * D + z] : 0.0;
-            nbnd[s] = b1;
+            acc[s] = (RESID && zok[s]) ? A.y[r * D + z] : 0.0;
             jb[s] = 0;
+            if constexpr (ALIGNED) thr[s] = (int32_t)__ldg(A.sbounds + 1);
+            else thr[s] = (int32_t)((__ldg(A.bounds + 1) - z + D - 1) / D);
         }
         auto fold = [&](int s) {
             if constexpr (RESID) acc[s] = rn_sub(acc[s], seg[s]);
             else acc[s] = (jb[s] == 0) ? seg[s] : rn_add(acc[s], seg[s]);
             seg[s] = 0.0;
         };
-        auto consume = [&](int32_t ce, double ve, const double (&xs)[KZ]) {
+        auto loadx = [&](int32_t c, double (&xs)[KZ]) {
+            // one IMAD.WIDE.U32: base + c * (8 D) bytes (offsets < 2^32 bytes)
+            const double *xp = reinterpret_cast<const double *>(reinterpret_cast<const char *>(xb) +
+                                                                (uint64_t)(uint32_t)c * (uint32_t)D8);
 #pragma unroll
             for (int s = 0; s < KZ; ++s) {
-                const int64_t z = zb + (int64_t)s * L;
-                if (z < D) {
-                    const int64_t C = (int64_t)ce * D + z;
-                    while (C >= nbnd[s]) {
-                        fold(s);
-                        ++jb[s];
-                        nbnd[s] = __ldg(A.bounds + jb[s] + 1);
-                    }
-                    seg[s] = rn_add(seg[s], rn_mul(ve, xs[s]));
-                }
+                if constexpr (W) xs[s] = __ldg(xp + s * 32);
+                else xs[s] = zok[s] ? __ldg(xp + s * L) : 0.0;
             }
         };
-        const int64_t beg = live ? A.ptr[r] : 0, end = live ? A.ptr[r + 1] : 0;
-        for (int64_t k0 = beg; k0 < end; k0 += L) {
-            const int64_t k = k0 + gl;
-            int32_t c = 0;
-            double v = 0.0;
-            if (k < end) {
-                c = ld_stream(A.idx + k, pol);
-                v = (double)ld_stream(A.val + k, pol);
-            }
-            const int n = (int)((end - k0) < L ? (end - k0) : L);
-            int e = 0;
-            for (; e + 4 <= n; e += 4) {
-                int32_t cc[4];
-                double vv[4], xx[4][KZ];
+        auto step = [&](int32_t c, double v, const double (&xs)[KZ]) {
+            if constexpr (ALIGNED) {
+                while (c >= thr[0]) {
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    cc[u] = __shfl_sync(gmask, c, e + u, L);
-                    vv[u] = __shfl_sync(gmask, v, e + u, L);
+                    for (int s = 0; s < KZ; ++s) { fold(s); ++jb[s]; }
+                    thr[0] = (int32_t)__ldg(A.sbounds + jb[0] + 1);
                 }
+            } else {
+#pragma unroll
+                for (int s = 0; s < KZ; ++s) {
+                    while (c >= thr[s]) {
+                        fold(s);
+                        ++jb[s];
+                        thr[s] = (int32_t)((__ldg(A.bounds + jb[s] + 1) - (zb + s * L) + D - 1) / D);
+                    }
+                }
+            }
+#pragma unroll
+            for (int s = 0; s < KZ; ++s) seg[s] = rn_add(seg[s], rn_mul(v, xs[s]));
+        };
+        // entries of a row are in ascending stored index: if the last of four
+        // is below every threshold, none of them crosses a block bound
+        auto below = [&](int32_t c) {
+            bool b = c < thr[0];
+            if constexpr (!ALIGNED)
+#pragma unroll
+                for (int s = 1; s < KZ; ++s) b = b && c < thr[s];
+            return b;
+        };
+        const int64_t beg = live ? A.ptr[r] : 0, end = live ? A.ptr[r + 1] : 0;
+        int64_t k = beg;
+        const int64_t kh = ((beg + 3) & ~(int64_t)3) < end ? ((beg + 3) & ~(int64_t)3) : end;
+        for (; k < kh; ++k) {
+            const int32_t c = ld_stream(idx + k, pol);
+            const double v = (double)ld_stream(val + k, pol);
+            double xs[KZ];
+            loadx(c, xs);
+            step(c, v, xs);
+        }
+        for (; k + 4 <= end; k += 4) {
+            int32_t c[4];
+            double v[4], xs[4][KZ];
+            stk_load4<V>(idx, val, k, pol, c, v);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) loadx(c[u], xs[u]);
+            if (below(c[3])) {
 #pragma unroll
                 for (int u = 0; u < 4; ++u)
 #pragma unroll
-                    for (int s = 0; s < KZ; ++s) {
-                        const int64_t z = zb + (int64_t)s * L;
-                        xx[u][s] = (z < D) ? __ldg(vec + (int64_t)cc[u] * D + z) : 0.0;
-                    }
+                    for (int s = 0; s < KZ; ++s) seg[s] = rn_add(seg[s], rn_mul(v[u], xs[u][s]));
+            } else {
 #pragma unroll
-                for (int u = 0; u < 4; ++u) consume(cc[u], vv[u], xx[u]);
+                for (int u = 0; u < 4; ++u) step(c[u], v[u], xs[u]);
             }
-            for (; e < n; ++e) {
-                const int32_t ce = __shfl_sync(gmask, c, e, L);
-                const double ve = __shfl_sync(gmask, v, e, L);
-                double xs[KZ];
-#pragma unroll
-                for (int s = 0; s < KZ; ++s) {
-                    const int64_t z = zb + (int64_t)s * L;
-                    xs[s] = (z < D) ? __ldg(vec + (int64_t)ce * D + z) : 0.0;
-                }
-                consume(ce, ve, xs);
-            }
+        }
+        for (; k < end; ++k) {
+            const int32_t c = ld_stream(idx + k, pol);
+            const double v = (double)ld_stream(val + k, pol);
+            double xs[KZ];
+            loadx(c, xs);
+            step(c, v, xs);
         }
 #pragma unroll
         for (int s = 0; s < KZ; ++s) {
-            const int64_t z = zb + (int64_t)s * L;
-            if (live && z < D) {
+            if (zok[s]) {
                 for (; jb[s] < A.nb; ++jb[s]) fold(s);  // the open segment, then empty trailing blocks
-                epi(r * D + z, acc[s]);
+                epi(r * D + zb + s * L, acc[s]);
             }
         }
     }
