@@ -388,7 +388,7 @@ def run_ct_secondary(args, index):
     dim = len(shape)
     # per FGP iteration: candidate (read q, b; write c), dual value (read c, b),
     # momentum (read c, p; write q): 6*dim + 2 fields of 8 bytes per voxel per iteration
-    pbytes = 8 * npx * ((2 * dim + 1 + dim + 1 + 3 * dim) * d.max_inner_iters + 10)
+    pbytes = 8 * npx * ((6 * dim + 2) * d.max_inner_iters + 10)
     rows, cols = op.shape
     out = {"nnz": int(op.nnz), "epochs_per_s": round(1000.0 / ms, 2), "ms_per_epoch": round(ms, 4),
            "monitor_decrease": False, "mean_fgp_iterations": round(fgp_iters, 2),

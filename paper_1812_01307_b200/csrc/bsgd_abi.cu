@@ -812,27 +812,31 @@ __global__ void tail_kernel(TailArgs t) {
 template <int DIM>
 static size_t prox_dyn_smem() { return sizeof(double) * 2 * DIM * fgp_chunk<DIM>() * 128; }
 
-template <int DIM>
+template <int DIM, bool FAST>
 static int prox_occupancy() {
     static int occ = 0;
     if (occ == 0) {
-        cudaFuncSetAttribute(fgp_kernel<DIM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)prox_dyn_smem<DIM>());
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fgp_kernel<DIM>, kThreads, prox_dyn_smem<DIM>());
+        cudaFuncSetAttribute(fgp_kernel<DIM, FAST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)prox_dyn_smem<DIM>());
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fgp_kernel<DIM, FAST>, kThreads, prox_dyn_smem<DIM>());
         if (occ < 1) occ = 1;
     }
     return occ;
 }
 
 template <int DIM>
+static void prox_warm() {
+    (void)prox_occupancy<DIM, true>();
+    (void)prox_occupancy<DIM, false>();
+}
+
+template <int DIM, bool FAST>
 static int launch_prox_dim(ProxArgs &a, cudaStream_t st) {
-    const int occ = prox_occupancy<DIM>();
-    int rc = pw_depth(a.N, &a.ds);
-    if (rc) return rc;
-    a.fast = (a.N % 128 == 0 && a.N / 128 == ((int64_t)1 << a.ds)) ? 1 : 0;
+    const int occ = prox_occupancy<DIM, FAST>();
     // G: a power of two (numpy-order top tree), co-resident, <= 512
     int grid = pow2_floor(std::max<int64_t>(1, std::min<int64_t>((int64_t)occ * num_sms(), 512)));
     const int64_t S = (int64_t)1 << a.ds;
-    const int64_t per_slot = a.fast ? fgp_chunk<DIM>() : kThreads / 8;  // subtrees folded per smem slot
+    const int64_t per_slot = FAST ? fgp_chunk<DIM>() : kThreads / 8;  // subtrees folded per smem slot
     if (S / grid > kPwMaxQ * per_slot)
         return fail(BSGD_EINVAL, "image too large for the pairwise tree (%lld pixels)", (long long)a.N);
     cudaLaunchConfig_t cfg = {};
@@ -845,14 +849,20 @@ static int launch_prox_dim(ProxArgs &a, cudaStream_t st) {
     attr[0].val.cooperative = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    CU(cudaLaunchKernelEx(&cfg, fgp_kernel<DIM>, a));
+    CU(cudaLaunchKernelEx(&cfg, fgp_kernel<DIM, FAST>, a));
     return BSGD_OK;
 }
 
 // a.D <= 1: 2D image (tv.py); a.D >= 2: 3D volume (oracle tv_prox3)
 static int launch_prox(ProxArgs &a, cudaStream_t st) {
-    if (a.D <= 1) { a.D = 1; return launch_prox_dim<2>(a, st); }
-    return launch_prox_dim<3>(a, st);
+    int rc = pw_depth(a.N, &a.ds);
+    if (rc) return rc;
+    a.fast = (a.N % 128 == 0 && a.N / 128 == ((int64_t)1 << a.ds)) ? 1 : 0;
+    if (a.D <= 1) {
+        a.D = 1;
+        return a.fast ? launch_prox_dim<2, true>(a, st) : launch_prox_dim<2, false>(a, st);
+    }
+    return a.fast ? launch_prox_dim<3, true>(a, st) : launch_prox_dim<3, false>(a, st);
 }
 
 static void prox_fields(ProxArgs &a, const Ws &ws, int64_t n) {
@@ -982,8 +992,8 @@ static int plan_finish(bsgd_plan *p, cudaStream_t st) {
     p->block_nnz.assign(cnt.begin(), cnt.end());
 #undef PTRY
     // warm occupancy caches outside any graph capture
-    (void)prox_occupancy<2>();
-    (void)prox_occupancy<3>();
+    prox_warm<2>();
+    prox_warm<3>();
     return BSGD_OK;
 }
 

@@ -158,18 +158,51 @@ __device__ __forceinline__ double tv_term(const double *u, int64_t p, int64_t W,
 template <int DIM>
 __host__ __device__ constexpr int fgp_chunk() { return DIM == 3 ? 8 : kPwChunk; }
 
-template <int K, int CH, class F>
+// FAST is a template parameter so that the fast-path kernel never passes the
+// term functors to the out-of-line pw_node: functors that escape to a call keep
+// their captured field pointers in local memory (LDL in the hot loops).
+template <int K, int CH, bool FAST, class F>
 __device__ __forceinline__ void np_sum(cg::grid_group &grid, int64_t N, int ds, F &f, double *red, int &round,
-                                       double *sm, double (&out)[K], int fast, double *T) {
+                                       double *sm, double (&out)[K], double *T) {
     double *buf = red + (size_t)(round & 1) * kMaxPartials * kPwMaxK;
-    if (fast) pw_cta_fast<K, F, CH>(ds, f, T, sm, buf);
+    if constexpr (FAST) pw_cta_fast<K, F, CH>(ds, f, T, sm, buf);
     else pw_cta<K>(N, ds, f, sm, buf);
     grid.sync();
     pw_top<K>(ds, gridDim.x, buf, sm, out);
     ++round;
 }
 
+// momentum commit terms (tv.py:233-245), two-stage (pairwise.cuh): q = c + beta (c - p),
+// terms (c - p)^2 per axis then c^2 per axis
 template <int DIM>
+struct CommitTerms {
+    static constexpr bool kTwoStage = true;
+    const double *C[DIM];
+    const double *P[DIM];
+    double *Q[DIM];
+    double beta;
+    struct L {
+        double c[DIM], p[DIM];
+    };
+    __device__ __forceinline__ L load(int64_t p) const {
+        L l;
+#pragma unroll
+        for (int k = 0; k < DIM; ++k) { l.c[k] = ldcg(C[k] + p); l.p[k] = ldcg(P[k] + p); }
+        return l;
+    }
+    __device__ __forceinline__ void term(int64_t p, const L &l, double (&t)[2 * DIM]) const {
+#pragma unroll
+        for (int k = 0; k < DIM; ++k) {
+            const double sk = rn_sub(l.c[k], l.p[k]);
+            Q[k][p] = rn_add(l.c[k], rn_mul(beta, sk));
+            t[k] = rn_mul(sk, sk);
+            t[DIM + k] = rn_mul(l.c[k], l.c[k]);
+        }
+    }
+    __device__ __forceinline__ void operator()(int64_t p, double (&t)[2 * DIM]) const { term(p, load(p), t); }
+};
+
+template <int DIM, bool FAST>
 __global__ void __launch_bounds__(kThreads, 2) fgp_kernel(ProxArgs a) {
     cg::grid_group grid = cg::this_grid();
     __shared__ double sm[kPwMaxQ * kPwMaxK];
@@ -189,14 +222,15 @@ __global__ void __launch_bounds__(kThreads, 2) fgp_kernel(ProxArgs a) {
     //     and TV(b) for the fallback test (tv.py:166-169, 251)
     double v2[2];
     {
-        auto f0 = [&](int64_t p, double (&t)[2]) {
+        for (int64_t p = tid; p < N; p += nthr)
 #pragma unroll
             for (int k = 0; k < DIM; ++k) { P[k][p] = 0.0; Q[k][p] = 0.0; }
+        auto f0 = [&](int64_t p, double (&t)[2]) {
             const double bb = __ldg(b + p);
             t[0] = rn_mul(bb, bb);
             t[1] = tv_term<DIM>(b, p, H, W, false);
         };
-        np_sum<2, CH>(grid, N, a.ds, f0, a.red, round, sm, v2, a.fast, Tsm);
+        np_sum<2, CH, FAST>(grid, N, a.ds, f0, a.red, round, sm, v2, Tsm);
     }
     double phi_prev = v2[0];
     const double tv_b = v2[1];
@@ -212,46 +246,51 @@ __global__ void __launch_bounds__(kThreads, 2) fgp_kernel(ProxArgs a) {
     };
     for (int it = 0; it < a.max_iters; ++it) {
         // A: candidate from q (tv.py:207-214)
-        for (int64_t p = tid; p < N; p += nthr) {
-            double c[DIM];
-            candidate<DIM>(a, Q, p, c);
+        // two pixels per pass, both candidates before either store (see pw_two_stage)
+        for (int64_t p0 = tid; p0 < N; p0 += 2 * nthr) {
+            const int64_t p1 = p0 + nthr;
+            double c0[DIM], c1[DIM];
+            candidate<DIM>(a, Q, p0, c0);
+            if (p1 < N) candidate<DIM>(a, Q, p1, c1);
 #pragma unroll
-            for (int k = 0; k < DIM; ++k) C[k][p] = c[k];
+            for (int k = 0; k < DIM; ++k) C[k][p0] = c0[k];
+            if (p1 < N)
+#pragma unroll
+                for (int k = 0; k < DIM; ++k) C[k][p1] = c1[k];
         }
         grid.sync();
         // B: phi = np.sum(resid * resid) (tv.py:215-216)
         double v1[1];
-        np_sum<1, CH>(grid, N, a.ds, fphi, a.red, round, sm, v1, a.fast, Tsm);
+        np_sum<1, CH, FAST>(grid, N, a.ds, fphi, a.red, round, sm, v1, Tsm);
         double phi = v1[0];
         if (phi > phi_prev) {  // restart from the last accepted point (tv.py:217-231)
             ++restarts;
             t_mom = 1.0;
-            for (int64_t p = tid; p < N; p += nthr) {
-                double c[DIM];
-                candidate<DIM>(a, P, p, c);
+            for (int64_t p0 = tid; p0 < N; p0 += 2 * nthr) {
+                const int64_t p1 = p0 + nthr;
+                double c0[DIM], c1[DIM];
+                candidate<DIM>(a, P, p0, c0);
+                if (p1 < N) candidate<DIM>(a, P, p1, c1);
 #pragma unroll
-                for (int k = 0; k < DIM; ++k) C[k][p] = c[k];
+                for (int k = 0; k < DIM; ++k) C[k][p0] = c0[k];
+                if (p1 < N)
+#pragma unroll
+                    for (int k = 0; k < DIM; ++k) C[k][p1] = c1[k];
             }
             grid.sync();
-            np_sum<1, CH>(grid, N, a.ds, fphi, a.red, round, sm, v1, a.fast, Tsm);
+            np_sum<1, CH, FAST>(grid, N, a.ds, fphi, a.red, round, sm, v1, Tsm);
             phi = v1[0];
         }
         // C: momentum commit (tv.py:233-245): q = c + beta (c - p);
         //    change = sqrt(sum_k np.sum(s_k^2)), scale = sqrt(sum_k np.sum(c_k^2)), k in order
         const double t_next = 0.5 * (1.0 + sqrt(rn_add(1.0, rn_mul(rn_mul(4.0, t_mom), t_mom))));
         const double beta = (t_mom - 1.0) / t_next;
-        auto fcom = [&](int64_t p, double (&t)[2 * DIM]) {
+        CommitTerms<DIM> fcom;
 #pragma unroll
-            for (int k = 0; k < DIM; ++k) {
-                const double ck = __ldcg(C[k] + p);
-                const double sk = rn_sub(ck, __ldcg(P[k] + p));
-                Q[k][p] = rn_add(ck, rn_mul(beta, sk));
-                t[k] = rn_mul(sk, sk);
-                t[DIM + k] = rn_mul(ck, ck);
-            }
-        };
+        for (int k = 0; k < DIM; ++k) { fcom.C[k] = C[k]; fcom.P[k] = P[k]; fcom.Q[k] = Q[k]; }
+        fcom.beta = beta;
         double vc[2 * DIM];
-        np_sum<2 * DIM, CH>(grid, N, a.ds, fcom, a.red, round, sm, vc, a.fast, Tsm);
+        np_sum<2 * DIM, CH, FAST>(grid, N, a.ds, fcom, a.red, round, sm, vc, Tsm);
 #pragma unroll
         for (int k = 0; k < DIM; ++k) { double *tmp_ = P[k]; P[k] = C[k]; C[k] = tmp_; }  // p <- c
         phi_prev = (phi_prev < phi) ? phi_prev : phi;  // Python min(phi, phi_prev)
@@ -268,31 +307,39 @@ __global__ void __launch_bounds__(kThreads, 2) fgp_kernel(ProxArgs a) {
     // --- finalize: out = b + w div p (tv.py:250), identity fallback if the primal
     //     objective is worse (tv.py:251-253)
     double *tmp = C[0];  // scratch after the swap
-    for (int64_t p = tid; p < N; p += nthr) {
+    for (int64_t p0 = tid; p0 < N; p0 += 2 * nthr) {
+        const int64_t p1 = p0 + nthr;
         int64_t z, s, t;
-        split_index<DIM>(p, H, W, z, s, t);
-        tmp[p] = rn_add(__ldg(b + p), rn_mul(w, div_at<DIM>(P, z, s, t, D, H, W)));
+        split_index<DIM>(p0, H, W, z, s, t);
+        const double v0 = rn_add(__ldg(b + p0), rn_mul(w, div_at<DIM>(P, z, s, t, D, H, W)));
+        double v1 = 0.0;
+        if (p1 < N) {
+            split_index<DIM>(p1, H, W, z, s, t);
+            v1 = rn_add(__ldg(b + p1), rn_mul(w, div_at<DIM>(P, z, s, t, D, H, W)));
+        }
+        tmp[p0] = v0;
+        if (p1 < N) tmp[p1] = v1;
     }
     grid.sync();
     auto fen = [&](int64_t p, double (&t)[2]) {
-        const double d = rn_sub(__ldcg(tmp + p), __ldg(b + p));
+        const double d = rn_sub(ldcg(tmp + p), __ldg(b + p));
         t[0] = rn_mul(d, d);
         t[1] = tv_term<DIM>(tmp, p, H, W, true);
     };
     double e2[2];
-    np_sum<2, CH>(grid, N, a.ds, fen, a.red, round, sm, e2, a.fast, Tsm);
+    np_sum<2, CH, FAST>(grid, N, a.ds, fen, a.red, round, sm, e2, Tsm);
     const double two_w = 2.0 * w;
     const double obj_out = rn_add(e2[0], rn_mul(two_w, e2[1]));
     const double obj_b = rn_add(0.0, rn_mul(two_w, tv_b));
     const int fell = obj_out > obj_b ? 1 : 0;
 
     if (a.out_img != nullptr) {
-        for (int64_t p = tid; p < N; p += nthr) a.out_img[p] = fell ? __ldg(b + p) : __ldcg(tmp + p);
+        for (int64_t p = tid; p < N; p += nthr) a.out_img[p] = fell ? __ldg(b + p) : ldcg(tmp + p);
     } else {
         double st[4] = {0.0, 0.0, 0.0, 0.0};
         for (int64_t k = tid; k < N; k += nthr) {
             const int64_t p = (a.perm != nullptr) ? a.perm[k] : k;
-            const double xv = fell ? __ldg(b + p) : __ldcg(tmp + p);
+            const double xv = fell ? __ldg(b + p) : ldcg(tmp + p);
             a.x_next[k] = xv;
             const double d = rn_sub(xv, a.x_k[k]);
             st[0] += xv * xv;

@@ -25,9 +25,23 @@
 // decisions and ProxInfo match the reference exactly.
 #pragma once
 
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace bsgd {
+
+// Term functors are called as f(p, t).  A functor that also stores (e.g. the FGP
+// momentum update) can opt into a two-stage form, `static constexpr bool
+// kTwoStage = true;` with `L load(p)` (loads only) and `term(p, const L &, t)`,
+// so the fast path issues the loads of several pixels before any of their
+// stores: otherwise the compiler must keep every load behind the previous
+// pixel's store (it cannot prove the fields do not alias) and each pixel costs
+// a full memory round trip.
+template <class F, class = void>
+struct pw_two_stage : std::false_type {};
+template <class F>
+struct pw_two_stage<F, std::void_t<decltype(F::kTwoStage)>> : std::integral_constant<bool, F::kTwoStage> {};
 
 constexpr int kPwMaxQ = 512;   // subtrees per CTA held in shared memory
 constexpr int kPwMaxK = 6;     // simultaneous sums per pass (3D commit phase)
@@ -222,11 +236,33 @@ __device__ __forceinline__ int pw_cta_fast(int ds, F &f, double *T, double *leaf
         const int nl = (Q - c0 < CH) ? Q - c0 : CH;
         const int npx = nl * 128;
         const int64_t px0 = (first + c0) * 128;
-        for (int i = tid; i < npx; i += blockDim.x) {
-            double t[K];
-            f(px0 + i, t);
+        if constexpr (pw_two_stage<F>::value) {
+            constexpr int U = 4;
+            for (int i0 = tid; i0 < npx; i0 += U * (int)blockDim.x) {
+                typename F::L ld[U];
 #pragma unroll
-            for (int k = 0; k < K; ++k) T[k * (CH * 128) + i] = t[k];
+                for (int u = 0; u < U; ++u) {
+                    const int i = i0 + u * (int)blockDim.x;
+                    if (i < npx) ld[u] = f.load(px0 + i);
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int i = i0 + u * (int)blockDim.x;
+                    if (i < npx) {
+                        double t[K];
+                        f.term(px0 + i, ld[u], t);
+#pragma unroll
+                        for (int k = 0; k < K; ++k) T[k * (CH * 128) + i] = t[k];
+                    }
+                }
+            }
+        } else {
+            for (int i = tid; i < npx; i += blockDim.x) {
+                double t[K];
+                f(px0 + i, t);
+#pragma unroll
+                for (int k = 0; k < K; ++k) T[k * (CH * 128) + i] = t[k];
+            }
         }
         __syncthreads();
         if (tid < nl * 8) {

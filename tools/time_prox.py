@@ -14,10 +14,12 @@ import torch  # noqa: E402
 from paper_1812_01307_b200 import tv  # noqa: E402
 
 
-def prox_bytes(n_pix, iters, restarts=0):
-    # per FGP iteration: read q (2 fields) + b, write c (2); read c (2) for phi; read c, p (4), write q (2)
-    # = 11 field passes; setup 5, finalize ~5; restarts add 4
-    return 8 * n_pix * (11 * iters + 4 * restarts + 10)
+def prox_bytes(n_pix, iters, restarts=0, dim=2):
+    # per FGP iteration: candidate reads q (dim fields) + b and writes c (dim);
+    # dual value reads c (dim) + b; momentum reads c, p (2 dim) and writes q (dim):
+    # 6 dim + 2 field passes; a restart repeats candidate + dual value (3 dim + 2);
+    # setup and finalize ~10
+    return 8 * n_pix * ((6 * dim + 2) * iters + (3 * dim + 2) * restarts + 10)
 
 
 def main():
@@ -26,9 +28,11 @@ def main():
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--weight", type=float, default=0.05)
+    ap.add_argument("--depth", type=int, default=1, help="> 1: n x n x depth volume (3-D TV)")
     a = ap.parse_args()
     rng = np.random.default_rng(0)
-    img = torch.tensor(rng.random((a.n, a.n)), device="cuda")
+    shape = (a.depth, a.n, a.n) if a.depth > 1 else (a.n, a.n)
+    img = torch.tensor(rng.random(shape), device="cuda")
     st = tv.ProxSettings(a.iters, 1e-300)
     out, info = tv.tv_prox(img, a.weight, st, return_info=True)
     torch.cuda.synchronize()
@@ -39,8 +43,8 @@ def main():
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / a.reps
-    b = prox_bytes(a.n * a.n, info.iterations, info.restarts)
-    print(json.dumps({"n": a.n, "iters": info.iterations, "restarts": info.restarts, "ms": round(ms, 4),
+    b = prox_bytes(img.numel(), info.iterations, info.restarts, len(shape))
+    print(json.dumps({"shape": list(shape), "iters": info.iterations, "restarts": info.restarts, "ms": round(ms, 4),
                       "us_per_iter": round(1000 * ms / info.iterations, 2), "bytes": b,
                       "gbs": round(b / (ms * 1e6), 1)}))
 
