@@ -386,9 +386,9 @@ def run_ct_secondary(args, index):
     pms = p0.elapsed_time(p1) / 5
     npx = int(np.prod(shape))
     dim = len(shape)
-    # per FGP iteration: candidate (read q, b; write c), dual value (read c, b),
-    # momentum (read c, p; write q): 6*dim + 2 fields of 8 bytes per voxel per iteration
-    pbytes = 8 * npx * ((6 * dim + 2) * d.max_inner_iters + 10)
+    # per FGP iteration of the fused schedule: candidate (read q, b; write c), dual
+    # value + momentum commit (read c, p, b; write q): 5*dim + 2 fields of 8 bytes
+    pbytes = 8 * npx * ((5 * dim + 2) * d.max_inner_iters + 10)
     rows, cols = op.shape
     out = {"nnz": int(op.nnz), "epochs_per_s": round(1000.0 / ms, 2), "ms_per_epoch": round(ms, 4),
            "monitor_decrease": False, "mean_fgp_iterations": round(fgp_iters, 2),

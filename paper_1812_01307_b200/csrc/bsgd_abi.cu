@@ -810,7 +810,7 @@ __global__ void tail_kernel(TailArgs t) {
 // prox launch
 // ---------------------------------------------------------------------------
 template <int DIM>
-static size_t prox_dyn_smem() { return sizeof(double) * 2 * DIM * fgp_chunk<DIM>() * 128; }
+static size_t prox_dyn_smem() { return sizeof(double) * (1 + 2 * DIM) * fgp_chunk<DIM>() * 128; }
 
 template <int DIM, bool FAST>
 static int prox_occupancy() {

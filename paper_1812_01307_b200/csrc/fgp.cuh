@@ -154,9 +154,9 @@ __device__ __forceinline__ double tv_term(const double *u, int64_t p, int64_t W,
 
 // numpy-order grid sum of K per-pixel terms (pairwise.cuh); all threads get the
 // totals.  Term functors may write outputs: each pixel is visited once.
-// leaves per term chunk of the fast path: 2D 16, 3D 8 (keeps 2 CTAs per SM)
+// leaves per term chunk of the fast path (8: keeps 2 CTAs per SM with 7 sums)
 template <int DIM>
-__host__ __device__ constexpr int fgp_chunk() { return DIM == 3 ? 8 : kPwChunk; }
+__host__ __device__ constexpr int fgp_chunk() { return 8; }
 
 // FAST is a template parameter so that the fast-path kernel never passes the
 // term functors to the out-of-line pw_node: functors that escape to a call keep
@@ -172,34 +172,67 @@ __device__ __forceinline__ void np_sum(cg::grid_group &grid, int64_t N, int ds, 
     ++round;
 }
 
-// momentum commit terms (tv.py:233-245), two-stage (pairwise.cuh): q = c + beta (c - p),
-// terms (c - p)^2 per axis then c^2 per axis
+// One pass for the dual value of the candidate and the momentum commit
+// (tv.py:215-216 and 233-245), two-stage (pairwise.cuh):
+//   t[0]           = (b + w div c)^2                        -> phi
+//   t[1 .. DIM]    = (c_k - p_k)^2                         -> change
+//   t[DIM+1 .. 2D] = c_k^2                                 -> scale
+//   q_k            = c_k + beta (c_k - p_k)
+// The commit is speculative: when phi triggers a restart the kernel recomputes
+// the candidate and runs this pass again, overwriting q (same values and sums
+// as the reference's restart-then-commit order).
 template <int DIM>
-struct CommitTerms {
+struct DualCommitTerms {
     static constexpr bool kTwoStage = true;
+    static constexpr int kUnroll = DIM == 3 ? 1 : 2;  // 3D: 10 loads per pixel already, registers are the limit
+    const double *b;
     const double *C[DIM];
     const double *P[DIM];
     double *Q[DIM];
-    double beta;
+    double w, beta;
+    int64_t D, H, W;
     struct L {
-        double c[DIM], p[DIM];
+        double b, here[DIM], next[DIM], p[DIM];
+        unsigned first;  // bit k: coordinate k is 0 (no backward neighbour)
     };
     __device__ __forceinline__ L load(int64_t p) const {
         L l;
-#pragma unroll
-        for (int k = 0; k < DIM; ++k) { l.c[k] = ldcg(C[k] + p); l.p[k] = ldcg(P[k] + p); }
-        return l;
-    }
-    __device__ __forceinline__ void term(int64_t p, const L &l, double (&t)[2 * DIM]) const {
+        int64_t z, s, t;
+        split_index<DIM>(p, H, W, z, s, t);
+        const int64_t coord[3] = {z, s, t};
+        const int64_t ext[3] = {D, H, W};
+        const int64_t step[3] = {H * W, W, 1};
+        l.b = __ldg(b + p);
+        l.first = 0;
 #pragma unroll
         for (int k = 0; k < DIM; ++k) {
-            const double sk = rn_sub(l.c[k], l.p[k]);
-            Q[k][p] = rn_add(l.c[k], rn_mul(beta, sk));
-            t[k] = rn_mul(sk, sk);
-            t[DIM + k] = rn_mul(l.c[k], l.c[k]);
+            const int ax = 3 - DIM + k;  // 2D: rows, columns; 3D: z, rows, columns
+            l.here[k] = ldcg(C[k] + p);
+            l.next[k] = (coord[ax] + 1 < ext[ax]) ? ldcg(C[k] + p + step[ax]) : 0.0;
+            l.p[k] = ldcg(P[k] + p);
+            if (coord[ax] == 0) l.first |= 1u << k;
+        }
+        return l;
+    }
+    __device__ __forceinline__ void term(int64_t p, const L &l, double (&t)[1 + 2 * DIM]) const {
+        // div c, in div_at's order: ((((az - bz) + av) - bv) + ah) - bh
+        double d = 0.0;
+#pragma unroll
+        for (int k = 0; k < DIM; ++k) {
+            const double back = (l.first >> k) & 1u ? 0.0 : l.here[k];
+            d = (k == 0) ? rn_sub(l.next[k], back) : rn_sub(rn_add(d, l.next[k]), back);
+        }
+        const double res = rn_add(l.b, rn_mul(w, d));
+        t[0] = rn_mul(res, res);
+#pragma unroll
+        for (int k = 0; k < DIM; ++k) {
+            const double sk = rn_sub(l.here[k], l.p[k]);
+            Q[k][p] = rn_add(l.here[k], rn_mul(beta, sk));
+            t[1 + k] = rn_mul(sk, sk);
+            t[1 + DIM + k] = rn_mul(l.here[k], l.here[k]);
         }
     }
-    __device__ __forceinline__ void operator()(int64_t p, double (&t)[2 * DIM]) const { term(p, load(p), t); }
+    __device__ __forceinline__ void operator()(int64_t p, double (&t)[1 + 2 * DIM]) const { term(p, load(p), t); }
 };
 
 template <int DIM, bool FAST>
@@ -238,12 +271,8 @@ __global__ void __launch_bounds__(kThreads, 2) fgp_kernel(ProxArgs a) {
     int iters = 0, restarts = 0, converged = 0;
     if (tid == 0 && a.dual != nullptr) a.dual[0] = phi_prev;
 
-    auto fphi = [&](int64_t p, double (&t)[1]) {
-        int64_t z, s, tt;
-        split_index<DIM>(p, H, W, z, s, tt);
-        const double res = rn_add(__ldg(b + p), rn_mul(w, div_at<DIM>(C, z, s, tt, D, H, W)));
-        t[0] = rn_mul(res, res);
-    };
+    DualCommitTerms<DIM> fdc;
+    fdc.b = b; fdc.w = w; fdc.D = D; fdc.H = H; fdc.W = W;
     for (int it = 0; it < a.max_iters; ++it) {
         // A: candidate from q (tv.py:207-214)
         // two pixels per pass, both candidates before either store (see pw_two_stage)
@@ -259,10 +288,16 @@ __global__ void __launch_bounds__(kThreads, 2) fgp_kernel(ProxArgs a) {
                 for (int k = 0; k < DIM; ++k) C[k][p1] = c1[k];
         }
         grid.sync();
-        // B: phi = np.sum(resid * resid) (tv.py:215-216)
-        double v1[1];
-        np_sum<1, CH, FAST>(grid, N, a.ds, fphi, a.red, round, sm, v1, Tsm);
-        double phi = v1[0];
+        // B+C: phi = np.sum(resid * resid) (tv.py:215-216) and the momentum commit
+        //    (tv.py:233-245) in one pass, the commit speculative on "no restart"
+        double t_next = 0.5 * (1.0 + sqrt(rn_add(1.0, rn_mul(rn_mul(4.0, t_mom), t_mom))));
+        double beta = (t_mom - 1.0) / t_next;
+#pragma unroll
+        for (int k = 0; k < DIM; ++k) { fdc.C[k] = C[k]; fdc.P[k] = P[k]; fdc.Q[k] = Q[k]; }
+        fdc.beta = beta;
+        double vc[1 + 2 * DIM];
+        np_sum<1 + 2 * DIM, CH, FAST>(grid, N, a.ds, fdc, a.red, round, sm, vc, Tsm);
+        double phi = vc[0];
         if (phi > phi_prev) {  // restart from the last accepted point (tv.py:217-231)
             ++restarts;
             t_mom = 1.0;
@@ -278,27 +313,20 @@ __global__ void __launch_bounds__(kThreads, 2) fgp_kernel(ProxArgs a) {
                     for (int k = 0; k < DIM; ++k) C[k][p1] = c1[k];
             }
             grid.sync();
-            np_sum<1, CH, FAST>(grid, N, a.ds, fphi, a.red, round, sm, v1, Tsm);
-            phi = v1[0];
+            t_next = 0.5 * (1.0 + sqrt(rn_add(1.0, rn_mul(rn_mul(4.0, t_mom), t_mom))));
+            beta = (t_mom - 1.0) / t_next;
+            fdc.beta = beta;
+            np_sum<1 + 2 * DIM, CH, FAST>(grid, N, a.ds, fdc, a.red, round, sm, vc, Tsm);
+            phi = vc[0];
         }
-        // C: momentum commit (tv.py:233-245): q = c + beta (c - p);
-        //    change = sqrt(sum_k np.sum(s_k^2)), scale = sqrt(sum_k np.sum(c_k^2)), k in order
-        const double t_next = 0.5 * (1.0 + sqrt(rn_add(1.0, rn_mul(rn_mul(4.0, t_mom), t_mom))));
-        const double beta = (t_mom - 1.0) / t_next;
-        CommitTerms<DIM> fcom;
-#pragma unroll
-        for (int k = 0; k < DIM; ++k) { fcom.C[k] = C[k]; fcom.P[k] = P[k]; fcom.Q[k] = Q[k]; }
-        fcom.beta = beta;
-        double vc[2 * DIM];
-        np_sum<2 * DIM, CH, FAST>(grid, N, a.ds, fcom, a.red, round, sm, vc, Tsm);
 #pragma unroll
         for (int k = 0; k < DIM; ++k) { double *tmp_ = P[k]; P[k] = C[k]; C[k] = tmp_; }  // p <- c
         phi_prev = (phi_prev < phi) ? phi_prev : phi;  // Python min(phi, phi_prev)
         t_mom = t_next;
         iters = it + 1;
         if (tid == 0 && a.dual != nullptr) a.dual[it + 1] = phi_prev;
-        double ch2 = rn_add(vc[0], vc[1]), sc2 = rn_add(vc[DIM], vc[DIM + 1]);
-        if constexpr (DIM == 3) { ch2 = rn_add(ch2, vc[2]); sc2 = rn_add(sc2, vc[5]); }
+        double ch2 = rn_add(vc[1], vc[2]), sc2 = rn_add(vc[1 + DIM], vc[2 + DIM]);
+        if constexpr (DIM == 3) { ch2 = rn_add(ch2, vc[3]); sc2 = rn_add(sc2, vc[6]); }
         const double change = sqrt(ch2), scale = sqrt(sc2);
         const double floor_scale = (1e-30 > scale) ? 1e-30 : scale;  // Python max(scale, 1e-30)
         if (change <= a.tol * floor_scale) { converged = 1; break; }

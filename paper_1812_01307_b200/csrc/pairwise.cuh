@@ -42,9 +42,14 @@ template <class F, class = void>
 struct pw_two_stage : std::false_type {};
 template <class F>
 struct pw_two_stage<F, std::void_t<decltype(F::kTwoStage)>> : std::integral_constant<bool, F::kTwoStage> {};
+// pixels whose loads are issued together (F::kUnroll, default 4)
+template <class F, class = void>
+struct pw_unroll : std::integral_constant<int, 4> {};
+template <class F>
+struct pw_unroll<F, std::void_t<decltype(F::kUnroll)>> : std::integral_constant<int, F::kUnroll> {};
 
 constexpr int kPwMaxQ = 512;   // subtrees per CTA held in shared memory
-constexpr int kPwMaxK = 6;     // simultaneous sums per pass (3D commit phase)
+constexpr int kPwMaxK = 7;     // simultaneous sums per pass (3D dual value + commit)
 
 __host__ __device__ inline int64_t pw_split(int64_t n) {
     const int64_t n2 = n / 2;
@@ -237,7 +242,7 @@ __device__ __forceinline__ int pw_cta_fast(int ds, F &f, double *T, double *leaf
         const int npx = nl * 128;
         const int64_t px0 = (first + c0) * 128;
         if constexpr (pw_two_stage<F>::value) {
-            constexpr int U = 4;
+            constexpr int U = pw_unroll<F>::value;
             for (int i0 = tid; i0 < npx; i0 += U * (int)blockDim.x) {
                 typename F::L ld[U];
 #pragma unroll

@@ -15,11 +15,10 @@ from paper_1812_01307_b200 import tv  # noqa: E402
 
 
 def prox_bytes(n_pix, iters, restarts=0, dim=2):
-    # per FGP iteration: candidate reads q (dim fields) + b and writes c (dim);
-    # dual value reads c (dim) + b; momentum reads c, p (2 dim) and writes q (dim):
-    # 6 dim + 2 field passes; a restart repeats candidate + dual value (3 dim + 2);
-    # setup and finalize ~10
-    return 8 * n_pix * ((6 * dim + 2) * iters + (3 * dim + 2) * restarts + 10)
+    # per FGP iteration of the fused schedule: candidate reads q (dim fields)
+    # + b and writes c (dim); dual value + commit reads c, p (2 dim) + b and writes q (dim):
+    # 5 dim + 2 field passes; a restart repeats both (5 dim + 2); setup and finalize ~10
+    return 8 * n_pix * ((5 * dim + 2) * (iters + restarts) + 10)
 
 
 def main():
