@@ -1056,10 +1056,16 @@ static void stacked_setup(bsgd_plan *p, int64_t depth, int64_t rows2, int64_t co
     while (L < 32 && L < depth) L <<= 1;
     p->lanes = L;
     // slices per chunk: keep (vector rows) x (chunk) x 8 bytes <= ~64 MB of L2
+    int64_t budget = 64000000;
+    if (const char *env = getenv("BSGD_STK_L2_BYTES")) budget = std::max<int64_t>(1, atoll(env));
     auto pick = [&](int64_t vec_rows) {
-        const int64_t zc_max = std::max<int64_t>(1, (int64_t)64000000 / (vec_rows * 8));
+        const int64_t zc_max = std::max<int64_t>(1, budget / (vec_rows * 8));
         int kz = 4;
         while (kz > 1 && ((int64_t)L * kz > zc_max || (int64_t)L * (kz / 2) >= depth)) kz /= 2;
+        // two slices per lane at least when the depth allows: one entry load and
+        // block test then serve two products (configs[4] A^T: 6.8 -> 5.1 ms, the
+        // larger working set still mostly hits L2; tools/stk_sweep.py)
+        if (kz == 1 && (int64_t)L * 2 <= depth) kz = 2;
         return kz;
     };
     p->kz_fwd = pick(cols2);
