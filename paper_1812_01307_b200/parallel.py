@@ -51,16 +51,41 @@ def row_block_ownership(num_row_blocks: int, world: int):
 
 
 class ShardSpec:
-    """Which rows / row blocks a rank owns."""
+    """Which rows / row blocks a rank owns.
 
-    def __init__(self, partition, rank: int, world: int):
+    ``granularity`` > 1 is for slice-stacked operators (A = A2 (x) I_D,
+    granularity D): a rank then owns whole stored rows of A2 (all D slices of
+    each), split near-evenly, and its local block bounds are the global row
+    blocks clipped to that range (configs[4]'s 16 row blocks are not multiples
+    of D, so whole-block ownership would split stored rows).
+    """
+
+    def __init__(self, partition, rank: int, world: int, granularity: int = 1):
         self.partition = partition
         self.rank, self.world = rank, world
-        b0, b1 = row_block_ownership(partition.num_row_blocks, world)[rank]
-        self.block_range = (b0, b1)
-        self.row_range = (partition.row_bounds[b0][0], partition.row_bounds[b1 - 1][1])
-        self.local_row_bounds = tuple((a - self.row_range[0], b - self.row_range[0])
-                                      for a, b in partition.row_bounds[b0:b1])
+        self.granularity = granularity
+        if granularity <= 1:
+            b0, b1 = row_block_ownership(partition.num_row_blocks, world)[rank]
+            self.block_range = (b0, b1)
+            self.row_range = (partition.row_bounds[b0][0], partition.row_bounds[b1 - 1][1])
+            self.local_row_bounds = tuple((a - self.row_range[0], b - self.row_range[0])
+                                          for a, b in partition.row_bounds[b0:b1])
+            return
+        rows = partition.rows
+        if rows % granularity:
+            raise ValueError(f"{rows} rows are not whole stored rows of granularity {granularity}")
+        stored = rows // granularity
+        if world > stored:
+            raise ValueError(f"{world} ranks cannot own whole rows of a {stored}-row slice matrix")
+        base, extra = divmod(stored, world)
+        s0 = rank * base + min(rank, extra)
+        s1 = s0 + base + (1 if rank < extra else 0)
+        r0, r1 = s0 * granularity, s1 * granularity
+        self.row_range = (r0, r1)
+        blocks = [i for i, (a, b) in enumerate(partition.row_bounds) if a < r1 and b > r0]
+        self.block_range = (blocks[0], blocks[-1] + 1)
+        self.local_row_bounds = tuple((max(a, r0) - r0, min(b, r1) - r0)
+                                      for a, b in partition.row_bounds[blocks[0]:blocks[-1] + 1])
 
     @property
     def local_rows(self) -> int:
@@ -72,23 +97,41 @@ class CudaShard:
 
     def __init__(self, matrix, spec: ShardSpec, device=None, lam: float = 0.0, layout=None):
         from scipy import sparse
-        t = nat.torch()
-        self.t = t
-        self.spec = spec
         r0, r1 = spec.row_range
         full = sparse.csr_array(matrix)
         local = sparse.csr_array(full[r0:r1, :])
-        cols = full.shape[1]
         from .blockops import BlockPartition
         part = BlockPartition(spec.local_row_bounds, spec.partition.col_bounds)
-        self.op = BlockOperator(local, part, device=device)
-        self.dev = self.op.device
+        self._finish(spec, BlockOperator(local, part, device=device), full.shape[1], lam, layout)
+
+    @classmethod
+    def stacked(cls, slice_matrix, depth: int, spec: ShardSpec, device=None, lam: float = 0.0,
+                layout=None) -> "CudaShard":
+        """Shard of a slice-stacked operator A2 (x) I_depth: the rank's stored rows of A2."""
+        from scipy import sparse
+        from .blockops import BlockPartition
+        if spec.granularity != depth:
+            raise ValueError("a stacked shard needs ShardSpec(..., granularity=depth)")
+        a2 = sparse.csr_array(slice_matrix)
+        s0, s1 = spec.row_range[0] // depth, spec.row_range[1] // depth
+        part = BlockPartition(spec.local_row_bounds, spec.partition.col_bounds)
+        self = cls.__new__(cls)
+        op = BlockOperator.stacked(sparse.csr_array(a2[s0:s1, :]), depth, part, device=device)
+        self._finish(spec, op, a2.shape[1] * depth, lam, layout)
+        return self
+
+    def _finish(self, spec, op, cols, lam, layout):
+        t = nat.torch()
+        self.t = t
+        self.spec = spec
+        self.op = op
+        self.dev = op.device
         self.cols = cols
-        self.rows = r1 - r0
+        self.rows = spec.row_range[1] - spec.row_range[0]
         self.lam = lam
         self.layout = layout
         hw = (layout.height, layout.width) if (lam > 0 and layout is not None) else (0, 0)
-        nbytes = int(nat.load().bsgd_epoch_workspace_bytes(self.op.plan, hw[0], hw[1]))
+        nbytes = int(nat.load().bsgd_epoch_workspace_bytes(op.plan, hw[0], hw[1]))
         self.ws = t.zeros((nbytes + 7) // 8, dtype=t.float64, device=self.dev)
         self.hw = hw
 

@@ -104,3 +104,65 @@ def test_two_shards_emulated_match_single_gpu(cuda_ok):
     r = np.concatenate([d.r_current.cpu().numpy() for d in drvs])
     assert rel(r, st.r_vec) < 1e-12
     assert drvs[0].history()[-1, 1] == float(st.last_decrease_ok)
+
+
+def test_two_stacked_shards_emulated_match_oracle(cuda_ok):
+    """Slice-stacked shards (whole stored rows per rank, 3-D prox replicated) vs the oracle."""
+    from scipy import sparse
+    from paper_1812_01307_b200 import _native as nat
+    from paper_1812_01307_b200 import parallel, problems, tv
+    from paper_1812_01307_b200.blockops import make_partition
+    from paper_1812_01307_b200.solvers import SolverConfig
+    n, depth = 10, 6
+    a2 = problems.parallel_beam_matrix(n, 8, 15)
+    a = sparse.csr_array(sparse.kron(a2, sparse.identity(depth), format="csr"))
+    a.sort_indices()
+    vol = problems.ellipsoid_phantom(n, depth, 5, 0)
+    x_true = np.ascontiguousarray(vol.reshape(depth, n * n).T).ravel()
+    y = a @ x_true
+    perm = problems.interleaved_perm(n * n, depth)
+    layout = tv.VolumeLayout(depth, n, n, perm)
+    oop = orc.OracleOperator(a, 4, 4)
+    u, _, _ = orc.largest_eigenvalue(oop)
+    lam = 0.02
+    cfg = SolverConfig(mu=0.9 / (2 * u), lam=lam, epochs=6, prox=tv.ProxSettings(10, 1e-5))
+    part = make_partition(a.shape[0], a.shape[1], 4, 4)
+    shards = [parallel.CudaShard.stacked(a2, depth, parallel.ShardSpec(part, p, 2, granularity=depth), lam=lam,
+                                         layout=layout) for p in range(2)]
+    drvs = [parallel.DistributedBSGD(s, y, cfg, history_capacity=16) for s in shards]
+    tot = sum(float(d.f_curr.item()) for d in drvs)
+    for d in drvs:
+        d.f_curr.fill_(tot)
+    epochs = 4
+    for _ in range(epochs):
+        gs = []
+        for d in drvs:
+            d.s.grad(d.r[d.ri], d.g)
+            gs.append(d.g.clone())
+        gsum = gs[0] + gs[1]
+        fparts, argsv = [], []
+        for d in drvs:
+            xi, ri = d.xi, d.ri
+            d.g.copy_(gsum)
+            args = d.s.args(d.x[xi], d.g, d.x[1 - xi], d.mu, cfg, d.f_curr, d.hist, d.counter, d.perm, None,
+                            nat.EP_LOOKAHEAD | nat.EP_MONITOR)
+            d.s.step(args)
+            d.s.forward(d.x[1 - xi], d.y, d.r[ri], args)
+            d.s.forward_sumsq(args, d.fnext)
+            fparts.append(d.fnext.clone())
+            argsv.append(args)
+        fsum = fparts[0] + fparts[1]
+        for d, args in zip(drvs, argsv):
+            d.fnext.copy_(fsum)
+            d.s.tail(args, d.fnext)
+            d.xi, d.ri = 1 - d.xi, 1 - d.ri
+            d.rows_used += 1
+    prm = orc.Params(mu=cfg.mu, lam=lam, epochs=epochs, max_inner_iters=10, tol=1e-5)
+    st = orc.init_state(oop, y, prm)
+    for _ in range(epochs):
+        orc.epoch(st, oop, y, prm, perm, (depth, n, n))
+    x0 = drvs[0].x_current.cpu().numpy()
+    assert np.array_equal(x0, drvs[1].x_current.cpu().numpy())
+    assert rel(x0, st.x) < 1e-12
+    r = np.concatenate([d.r_current.cpu().numpy() for d in drvs])
+    assert rel(r, st.r_vec) < 1e-12

@@ -94,7 +94,20 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, outdir, epochs):
+def _stacked_case():
+    """Small slice-stacked system kron(A2, I_D) (configs[4] structure), host-built."""
+    from scipy import sparse
+    from paper_1812_01307_b200 import problems
+    a2 = problems.parallel_beam_matrix(8, 6, 11)
+    depth = 3
+    a = sparse.csr_array(sparse.kron(a2, sparse.identity(depth), format="csr"))
+    a.sort_indices()
+    rng = np.random.default_rng(5)
+    x_true = rng.random(a.shape[1])
+    return a, a @ x_true, x_true, depth
+
+
+def _worker(rank, world, port, outdir, epochs, stacked=False):
     import sys
     sys.path.insert(0, REPO)
     sys.path.insert(0, os.path.join(REPO, "tests"))
@@ -107,8 +120,14 @@ def _worker(rank, world, port, outdir, epochs):
     c = golden_cfg(z)
     a = golden_csr(z)
     m, n = (int(v) for v in z["mn"])
+    gran = 1
+    if stacked:  # whole stored rows of A2 per rank, clipped row blocks
+        a, y, x_true, gran = _stacked_case()
+        z = {"y": y, "x_true": x_true}
+        m, n = 4, 4
+        c = dict(c, mu=0.9 / (2.0 * 60.0))
     part = make_partition(a.shape[0], a.shape[1], m, n)
-    spec = parallel.ShardSpec(part, rank, world)
+    spec = parallel.ShardSpec(part, rank, world, granularity=gran)
     shard = CpuShard(a, spec)
     u, _, _ = parallel.distributed_largest_eigenvalue(shard, max_iters=50)
     cfg = SolverConfig(mu=c["mu"], lam=0.0, epochs=epochs)
@@ -133,6 +152,48 @@ def test_ownership_covers_row_blocks():
     assert specs[0].row_range[0] == 0 and specs[-1].row_range[1] == 1001
     for s0, s1 in zip(specs, specs[1:]):
         assert s0.row_range[1] == s1.row_range[0]
+
+
+def test_stacked_ownership_whole_stored_rows():
+    """granularity D: ranks own whole rows of A2; row blocks are clipped, not split by owner."""
+    from paper_1812_01307_b200 import parallel
+    from paper_1812_01307_b200.blockops import make_partition
+    part = make_partition(30, 12, 4, 2)            # 10 stored rows x D=3; bounds 8, 16, 23
+    specs = [parallel.ShardSpec(part, p, 3, granularity=3) for p in range(3)]
+    assert [s.row_range for s in specs] == [(0, 12), (12, 21), (21, 30)]
+    assert specs[0].local_row_bounds == ((0, 8), (8, 12))
+    assert specs[1].local_row_bounds == ((0, 4), (4, 9))
+    assert specs[2].local_row_bounds == ((0, 2), (2, 9))
+    assert specs[1].block_range == (1, 3)
+    with pytest.raises(ValueError):
+        parallel.ShardSpec(make_partition(31, 12, 4, 2), 0, 3, granularity=3)
+    with pytest.raises(ValueError):
+        parallel.ShardSpec(part, 0, 11, granularity=3)
+    part5 = make_partition(33454080, 16777216, 16, 16)   # configs[4] at 8 ranks: 2 whole blocks each
+    for p in range(8):
+        sp = parallel.ShardSpec(part5, p, 8, granularity=256)
+        assert sp.local_row_bounds == ((0, 2090880), (2090880, 4181760))
+
+
+def test_world2_gloo_stacked_matches_oracle(tmp_path):
+    from oracle import oracle as orc
+    from paper_1812_01307_b200.blockops import make_partition
+    epochs = 8
+    port = _free_port()
+    mp.spawn(_worker, args=(2, port, str(tmp_path), epochs, True), nprocs=2, join=True)
+    r0 = np.load(tmp_path / "rank0.npz")
+    r1 = np.load(tmp_path / "rank1.npz")
+    assert np.array_equal(r0["x"], r1["x"])
+    assert tuple(r0["rows"]) == (0, 99) and tuple(r1["rows"]) == (99, 198)
+    a, y, x_true, _ = _stacked_case()
+    op = orc.OracleOperator(a, 4, 4)
+    prm = orc.Params(mu=0.9 / (2.0 * 60.0), lam=0.0, epochs=epochs)
+    st = orc.init_state(op, y, prm)
+    for _ in range(epochs):
+        orc.epoch(st, op, y, prm)
+    assert np.linalg.norm(r0["x"] - st.x) / np.linalg.norm(st.x) < 1e-12
+    r_full = np.concatenate([r0["r"], r1["r"]])
+    assert np.linalg.norm(r_full - st.r_vec) / np.linalg.norm(st.r_vec) < 1e-12
 
 
 def test_world2_gloo_matches_single_process_oracle(tmp_path):
