@@ -91,9 +91,12 @@ __device__ __forceinline__ void stk_load4(const int32_t *idx, const V *val, int6
 // W: one row per warp (L = 32) and D a multiple of 32*KZ: slice offsets are
 //    compile-time and no slice predicates are needed.
 // Interleaved indices are < 2^31 (checked at plan creation), so all index
-// arithmetic is 32-bit.
+// arithmetic is 32-bit.  Occupancy: 4 CTAs/SM (64 registers) wherever that
+// costs no more than a few spills -- the loop is latency-bound on L2, so warps
+// matter more than registers (configs[4] epoch 17.3 -> 14.2 ms); the unaligned
+// plain product keeps 3 (it spills at 64).
 template <typename V, int KZ, bool RESID, bool ALIGNED, bool W, class Epi>
-__global__ void __launch_bounds__(kThreads) stacked_kernel(Stk<V> A, Epi epi, double *part, int64_t *cnt) {
+__global__ void __launch_bounds__(kThreads, (ALIGNED || Epi::K == 4) ? 4 : 3) stacked_kernel(Stk<V> A, Epi epi, double *part, int64_t *cnt) {
     __shared__ double sm[8 * (kThreads / 32)];
     const int lane = threadIdx.x & 31;
     const int L = W ? 32 : A.L;

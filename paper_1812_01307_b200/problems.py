@@ -335,12 +335,21 @@ class DeviceProblem:
     seeds: dict
     depth: int = 1                  # > 1: slice-stacked volume (solver order interleaved, see layout())
 
-    def layout(self):
-        """Pixel / voxel layout of the solver vector (tv.PixelLayout or tv.VolumeLayout)."""
+    def layout(self, slice_major: bool = False):
+        """Pixel / voxel layout of the solver vector (tv.PixelLayout or tv.VolumeLayout).
+
+        Stacked volumes: by default the interleaved solver vector is itself the
+        C-order (rows, columns, slices) volume, so the 3-D prox needs no
+        permutation (isotropic TV does not depend on which axis is called z;
+        only the rounding order of its sums does).  ``slice_major=True`` gives
+        the (slices, rows, columns) view through `interleaved_perm` instead.
+        """
         from . import tv
         if self.depth > 1:
-            return tv.VolumeLayout(self.depth, self.height, self.width,
-                                   interleaved_perm(self.height * self.width, self.depth))
+            if slice_major:
+                return tv.VolumeLayout(self.depth, self.height, self.width,
+                                       interleaved_perm(self.height * self.width, self.depth))
+            return tv.VolumeLayout.z_major(self.height, self.width, self.depth)
         return tv.PixelLayout.row_major(self.height, self.width)
 
 

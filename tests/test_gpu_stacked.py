@@ -87,8 +87,9 @@ def test_stacked_residual_and_errors(M):
         blockops.BlockOperator.stacked(a2, depth, blockops.make_partition(a.shape[0] + 1, a.shape[1], 1, 1))
 
 
-@pytest.mark.parametrize("lam,alpha,epochs", [(0.01, 1.0, 6), (0.0, 1.0, 5), (0.02, 0.5, 6)])
-def test_stacked_run_vs_oracle_bit_exact(M, lam, alpha, epochs):
+@pytest.mark.parametrize("lam,alpha,epochs,view", [(0.01, 1.0, 6, "slice_major"), (0.0, 1.0, 5, "slice_major"),
+                                                    (0.02, 0.5, 6, "slice_major"), (0.01, 1.0, 6, "native")])
+def test_stacked_run_vs_oracle_bit_exact(M, lam, alpha, epochs, view):
     """TV-regularised (3-D prox) and least-squares runs: x bit-identical to the oracle."""
     blockops, problems, solvers, spectral, tv = M
     n, depth, m = 12, 8, 4
@@ -101,13 +102,18 @@ def test_stacked_run_vs_oracle_bit_exact(M, lam, alpha, epochs):
     oop = orc.OracleOperator(a, m, m)
     u, _, _ = orc.largest_eigenvalue(oop)
     mu = 0.9 / (2.0 * u)
-    perm = problems.interleaved_perm(n * n, depth)
-    layout = tv.VolumeLayout(depth, n, n, perm) if lam > 0 else None
+    if view == "slice_major":   # (slices, rows, cols) volume through the permutation
+        perm = problems.interleaved_perm(n * n, depth)
+        shape = (depth, n, n)
+    else:                       # the interleaved vector is the (rows, cols, slices) volume
+        perm = np.arange(n * n * depth)
+        shape = (n, n, depth)
+    layout = tv.VolumeLayout(*shape, perm) if lam > 0 else None
     cfg = solvers.SolverConfig(mu=mu, lam=lam, alpha=alpha, gamma=alpha, epochs=epochs, seed=3,
                                prox=tv.ProxSettings(10, 1e-5))
     tr = solvers.run_solver("bsgd", solvers.Problem(op, y, x_true, layout), cfg)
     prm = orc.Params(mu=mu, lam=lam, alpha=alpha, gamma=alpha, epochs=epochs, seed=3, max_inner_iters=10, tol=1e-5)
-    ref = orc.run_bsgd(oop, y, prm, x_true=x_true, perm=perm if lam > 0 else None, hw=(depth, n, n))
+    ref = orc.run_bsgd(oop, y, prm, x_true=x_true, perm=perm if lam > 0 else None, hw=shape)
     assert np.array_equal(tr.final_x, ref.final_x)
     got = np.array([tuple(s) for s in tr.samples])
     want = np.array(ref.samples)
@@ -128,4 +134,5 @@ def test_stacked_device_generator_matches_host(M):
     assert np.array_equal(dev.matvec(x), host.matvec(x))
     d = problems.config_device(4, scale=0.0625)
     assert d.op.depth == d.depth == 16 and d.op.shape[1] == 16 * 16 * 16
-    assert d.layout().size == d.op.shape[1]
+    assert d.layout().size == d.op.shape[1] and d.layout().is_identity
+    assert d.layout(slice_major=True).size == d.op.shape[1]
