@@ -295,7 +295,7 @@ class BlockOperator:
 
     def __del__(self):
         plan = getattr(self, "_plan", None)
-        if plan is not None and nat._lib is not None:
+        if plan is not None and nat is not None and getattr(nat, "_lib", None) is not None:
             try:
                 nat.load().bsgd_plan_destroy(plan)
             except Exception:

@@ -1781,7 +1781,10 @@ int bsgd_epoch(const bsgd_plan *p, const bsgd_epoch_args *a, void *stream) {
         rc = run_step(p->cols, a, ws, st);
         if (!rc && (fl & BSGD_EP_R_NEXT))
             rc = DISPATCH_V(p, launch_fwd<V>(p, a->x_k, EpiResid{a->y, a->r_next}, ws.rpart, ws.ctl + 2, st));
-    } else if ((fl & BSGD_EP_R_NEXT) && (tiled || p->stacked())) {
+    } else if ((fl & BSGD_EP_R_NEXT) && (tiled || p->stacked() || !getenv("BSGD_MERGE_K1K2"))) {
+        // K1(x_k) then K2(r_k) on the stream.  One merged grid (below, opt-in) reads the
+        // same snapshot but measured slower on configs[1] (0.79 vs 0.66 ms per epoch):
+        // both halves are gather-bound and the CTA split balances them poorly
         rc = DISPATCH_V(p, launch_fwd<V>(p, a->x_k, EpiResid{a->y, a->r_next}, ws.rpart, ws.ctl + 2, st));
         if (!rc) rc = DISPATCH_V(p, launch_tr<V>(p, a->r_k, es, ws.xpart, ws.ctl, st));
     } else if (fl & BSGD_EP_R_NEXT) {

@@ -294,6 +294,12 @@ class SolverState:
     @x.setter
     def x(self, value) -> None:
         self._from_host(self._x[self._xi], value, self._cols)
+        # a new x voids the lookahead product y - A x_next; a caller that writes x
+        # between epochs would void every one, so stop computing it eagerly (without
+        # the monitor, each epoch then runs K1(x_k) and K2(r_k) merged: still two
+        # products, none wasted)
+        if self._la_valid:
+            self._la_policy = False
         self._la_valid = False
 
     @property
