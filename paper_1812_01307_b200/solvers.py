@@ -240,6 +240,10 @@ class SolverState:
         self._ri = 0
         self._la_valid = True
         self._la_policy = True
+        self._version = 0           # bumped by every epoch and every state write
+        self._host_reads = False    # x / r_vec read back since the last epoch
+        self._spec = None           # readback started during the last epoch (see _speculative_epoch)
+        self._side = None
         self._g = t.zeros(cols, **f64)
         self._z = None              # explicit z cache (N, rows) once the stochastic path ran
         self._z_explicit = False
@@ -263,7 +267,22 @@ class SolverState:
     # --- reference-style fields ---------------------------------------------
     # Reads return numpy arrays backed by pinned host memory (torch's caching
     # host allocator), so a read -> modify -> assign round trip moves data by
-    # DMA without an extra host copy; each read is a fresh array.
+    # DMA without an extra host copy; each read is a fresh array.  A caller that
+    # reads x / r_vec after every epoch gets them copied back while the epoch is
+    # still running (r behind K1, x behind the step), see `_speculative_epoch`.
+
+    def _read(self, which: str, dev_tensor) -> np.ndarray:
+        self._host_reads = True
+        sp = self._spec
+        if sp is not None and sp["version"] == self._version and which in sp:
+            h, ev = sp.pop(which)
+            ev.synchronize()
+            return h.numpy()
+        return self._to_host(dev_tensor)
+
+    def _touch(self) -> None:
+        self._version += 1
+        self._spec = None
 
     @staticmethod
     def _to_host(t) -> np.ndarray:
@@ -289,11 +308,12 @@ class SolverState:
 
     @property
     def x(self) -> np.ndarray:
-        return self._to_host(self._x[self._xi])
+        return self._read("x", self._x[self._xi])
 
     @x.setter
     def x(self, value) -> None:
         self._from_host(self._x[self._xi], value, self._cols)
+        self._touch()
         # a new x voids the lookahead product y - A x_next; a caller that writes x
         # between epochs would void every one, so stop computing it eagerly (without
         # the monitor, each epoch then runs K1(x_k) and K2(r_k) merged: still two
@@ -304,11 +324,12 @@ class SolverState:
 
     @property
     def r_vec(self) -> np.ndarray:
-        return self._to_host(self._r[self._ri])
+        return self._read("r", self._r[self._ri])
 
     @r_vec.setter
     def r_vec(self, value) -> None:
         self._from_host(self._r[self._ri], value, self._rows)
+        self._touch()
 
     @property
     def g(self) -> np.ndarray:
@@ -317,6 +338,7 @@ class SolverState:
     @g.setter
     def g(self, value) -> None:
         self._from_host(self._g, value, self._cols)
+        self._touch()
 
     @property
     def z_cache(self) -> np.ndarray:
@@ -498,8 +520,15 @@ def bsgd_tv_iteration(state: SolverState, op: BlockOperator, y, cfg: SolverConfi
         _pair_products(state, op, pairs, y_dev, xi, ri)
         flags |= nat.EP_SKIP_GRAD
     mu = state.mu_eff
-    args = _epoch_args(state, cfg, layout, y_dev, xi, ri, flags, mu, ws)
-    _launch(state, args)
+    speculate = (state._host_reads and full and not monitor and bool(flags & nat.EP_R_NEXT)
+                 and not (flags & nat.EP_LOOKAHEAD))
+    state._host_reads = False
+    state._touch()
+    if speculate:
+        _speculative_epoch(state, cfg, layout, y_dev, xi, ri, flags, mu, ws)
+    else:
+        args = _epoch_args(state, cfg, layout, y_dev, xi, ri, flags, mu, ws)
+        _launch(state, args)
     row = state._rows_used
     state._rows_used += 1
     if cfg.enforce_decrease:
@@ -523,7 +552,55 @@ def bsgd_tv_iteration(state: SolverState, op: BlockOperator, y, cfg: SolverConfi
     state._last_row = row if monitor else None
     state._last_ok_static = None
     state.epoch += len(pairs) / (m * n)
+    pend = getattr(state, "_spec_pending", None)
+    if pend is not None:
+        pend["version"] = state._version
+        state._spec = pend
+        state._spec_pending = None
     return state
+
+
+def _speculative_epoch(state: SolverState, cfg: SolverConfig, layout, y_dev, xi: int, ri: int, flags: int,
+                       mu: float, ws) -> None:
+    """The same epoch as one `bsgd_epoch` with R_NEXT, split so the host copies overlap it.
+
+    The caller read x / r_vec back after the previous epoch, so it will again:
+    K1 (r_next = y - A x_k, `bsgd_epoch_forward`) runs first and r_next starts
+    streaming to pinned host memory on a side stream while K2, the step and the
+    prox run; x_next follows as soon as it exists.  The getters hand these
+    buffers out (once) while the state version is unchanged.
+    """
+    t = nat.torch()
+    dev = state._dev
+    cur = t.cuda.current_stream(dev)
+    if state._side is None:
+        state._side = t.cuda.Stream(device=dev)
+    side = state._side
+    args = _epoch_args(state, cfg, layout, y_dev, xi, ri, flags & ~nat.EP_R_NEXT, mu, ws)
+    r_next, x_next = state._r[1 - ri], state._x[1 - xi]
+    nat.call("bsgd_epoch_forward", state._op.plan, nat.ptr(state._x[xi]), nat.ptr(y_dev), nat.ptr(r_next),
+             ctypes.byref(args), nat.stream_ptr(dev))
+    ev_r = t.cuda.Event()
+    ev_r.record(cur)
+    rh = t.empty(r_next.shape, dtype=t.float64, pin_memory=True)
+    with t.cuda.stream(side):
+        side.wait_event(ev_r)
+        rh.copy_(r_next, non_blocking=True)
+        done_r = t.cuda.Event()
+        done_r.record(side)
+    _launch(state, args)
+    ev_x = t.cuda.Event()
+    ev_x.record(cur)
+    xh = t.empty(x_next.shape, dtype=t.float64, pin_memory=True)
+    with t.cuda.stream(side):
+        side.wait_event(ev_x)
+        xh.copy_(x_next, non_blocking=True)
+        done_x = t.cuda.Event()
+        done_x.record(side)
+    # no wait on the main stream: the next epoch writes the other ring slots, and
+    # anything that does overwrite these (a setter, the epoch after next) bumps the
+    # state version first, so a copy it could race with is never handed out
+    state._spec_pending = {"x": (xh, done_x), "r": (rh, done_r)}
 
 
 def _pair_products(state: SolverState, op: BlockOperator, pairs, y_dev, xi: int, ri: int) -> None:

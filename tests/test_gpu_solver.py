@@ -215,3 +215,34 @@ def test_merged_and_sequential_first_epoch_agree(S, monkeypatch):
             hx = st.x
         outs.append((st.x, st.r_vec))
     assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+
+
+def test_host_readback_overlap_matches_plain_path(S):
+    """Reading x / r_vec after every epoch turns on overlapped readback; values are
+    the plain path's, bit for bit, and stale buffers are never handed out."""
+    blockops, solvers, tv = S
+    z = load_golden("p3_ls")
+    runs = []
+    for read_each in (False, True):
+        op, cfg, layout, c = _setup(S, z)
+        st = solvers.init_bsgd_state(op, z["y"], cfg)
+        hx = np.zeros(op.shape[1])
+        xs, rs = [], []
+        for e in range(4):
+            st.x = hx
+            solvers.bsgd_tv_iteration(st, op, z["y"], cfg, layout=layout)
+            if read_each or e == 3:
+                hx = st.x
+                xs.append(hx.copy())
+                rs.append(st.r_vec.copy())
+            else:
+                hx = st.x_device.cpu().numpy()
+        runs.append((xs[-1], rs[-1]))
+        if read_each:
+            # second read of the same epoch: a fresh, equal array
+            again = st.x
+            assert np.array_equal(again, xs[-1]) and again is not xs[-1]
+            # a write invalidates: the next read reflects it
+            st.r_vec = np.zeros(op.shape[0])
+            assert not st.r_vec.any()
+    assert np.array_equal(runs[0][0], runs[1][0]) and np.array_equal(runs[0][1], runs[1][1])
