@@ -692,6 +692,14 @@ struct Ws {
 
 static size_t a256(size_t x) { return (x + 255) & ~(size_t)255; }
 
+// Stride between the prox's dual fields, in doubles.  Fields read at the same
+// voxel index in one pass (p, q, c per axis, u) must not sit a power of two
+// apart: at 256^3 a field is exactly 128 MiB, and equal-offset addresses then
+// collide in the L2 / HBM channel hashing -- the 3-D prox ran 12.2 ms or
+// 16-29 ms depending on where the workspace landed.  An odd multiple of 256 B
+// between fields breaks the alignment.
+static int64_t field_stride(int64_t n) { return ((n + 31) & ~(int64_t)31) + 96; }
+
 static size_t ws_layout(void *base, int64_t cols, int64_t hw, Ws *ws) {
     size_t off = 0;
     auto take = [&](size_t bytes) { size_t o = off; off += a256(bytes); return (char *)base + o; };
@@ -700,8 +708,9 @@ static size_t ws_layout(void *base, int64_t cols, int64_t hw, Ws *ws) {
     char *xpart = take(sizeof(double) * kMaxPartials * 4);
     char *rpart = take(sizeof(double) * kMaxPartials);
     char *red = take(sizeof(double) * 2 * kMaxPartials * kPwMaxK);
+    (void)take(sizeof(double) * 96);  // keep uimg off the fields' alignment (see field_stride)
     char *uimg = take(sizeof(double) * (size_t)std::max<int64_t>(cols, 1));
-    char *fields = take(sizeof(double) * 9 * (size_t)std::max<int64_t>(hw, 0));
+    char *fields = take(sizeof(double) * 9 * (size_t)(hw > 0 ? field_stride(hw) : 0));
     if (ws) {
         ws->ctl = (int64_t *)ctl; ws->scal = (double *)scal; ws->xpart = (double *)xpart;
         ws->rpart = (double *)rpart; ws->red = (double *)red; ws->uimg = (double *)uimg;
@@ -866,7 +875,7 @@ static int launch_prox(ProxArgs &a, cudaStream_t st) {
 }
 
 static void prox_fields(ProxArgs &a, const Ws &ws, int64_t n) {
-    for (int k = 0; k < 9; ++k) a.f[k] = ws.fields + (size_t)k * n;
+    for (int k = 0; k < 9; ++k) a.f[k] = ws.fields + (size_t)k * field_stride(n);
     a.red = ws.red;
 }
 

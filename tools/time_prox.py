@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--weight", type=float, default=0.05)
     ap.add_argument("--depth", type=int, default=1, help="> 1: n x n x depth volume (3-D TV)")
+    ap.add_argument("--trials", type=int, default=1, help="repeat with a fresh workspace allocation")
     a = ap.parse_args()
     rng = np.random.default_rng(0)
     shape = (a.depth, a.n, a.n) if a.depth > 1 else (a.n, a.n)
@@ -35,16 +36,27 @@ def main():
     st = tv.ProxSettings(a.iters, 1e-300)
     out, info = tv.tv_prox(img, a.weight, st, return_info=True)
     torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(a.reps):
-        tv.tv_prox(img, a.weight, st)
-    e1.record()
-    torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / a.reps
+    trials = []
+    keep = []
+    for _ in range(a.trials):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(a.reps):
+            tv.tv_prox(img, a.weight, st)
+        e1.record()
+        torch.cuda.synchronize()
+        trials.append(e0.elapsed_time(e1) / a.reps)
+        if a.trials > 1:
+            w = next(iter(tv._ws_cache.values()))
+            print(f"trial {len(trials)}: ws {w.data_ptr():#x} (mod 1 GiB {w.data_ptr() % (1 << 30):#x}) "
+                  f"{trials[-1]:.3f} ms", file=sys.stderr)
+        keep.append(tv._ws_cache.copy())   # keep old workspaces alive: the next trial gets new addresses
+        tv._ws_cache.clear()
+    ms = min(trials)
     b = prox_bytes(img.numel(), info.iterations, info.restarts, len(shape))
     print(json.dumps({"shape": list(shape), "iters": info.iterations, "restarts": info.restarts, "ms": round(ms, 4),
                       "us_per_iter": round(1000 * ms / info.iterations, 2), "bytes": b,
+                      "trials_ms": [round(t, 3) for t in trials],
                       "gbs": round(b / (ms * 1e6), 1)}))
 
 
