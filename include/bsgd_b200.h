@@ -131,6 +131,14 @@ int bsgd_plan_create_stacked_device(bsgd_plan **out, int device, int64_t depth, 
                                     int64_t nnz2, int64_t *indptr, int32_t *indices, void *values,
                                     int value_dtype, int64_t num_row_blocks, int64_t num_col_blocks,
                                     const int64_t *row_bounds, const int64_t *col_bounds, void *stream);
+/* Tile-staged products for a stacked plan: group the stored rows of A2
+ * (transposed = 0) or A2^T (1) into tiles of <= 16 rows that share columns
+ * (tile t = rows tile_rows[tile_ptr[t] .. tile_ptr[t+1]), a permutation of all
+ * stored rows; host arrays).  Products then stream each tile's distinct vector
+ * rows through shared memory once instead of once per entry; results are
+ * unchanged bit for bit.  ntiles = 0 removes the tiles. */
+int bsgd_plan_stacked_tiles(bsgd_plan *plan, int transposed, int64_t ntiles, const int64_t *tile_ptr,
+                            const int64_t *tile_rows, void *stream);
 /* depth (1 for ordinary plans) and the stored CSR's shape / nnz */
 int bsgd_plan_stacked_info(const bsgd_plan *plan, int64_t *depth, int64_t *rows2, int64_t *cols2,
                            int64_t *nnz2);

@@ -110,6 +110,25 @@ def make_partition(rows: int, cols: int, num_row_blocks: int, num_col_blocks: in
     return BlockPartition(_split_even(rows, num_row_blocks), _split_even(cols, num_col_blocks))
 
 
+def grid_tiles(height: int, width: int, tile_h: int = 4, tile_w: int = 4):
+    """Row grouping of a row-major height x width grid into tile_h x tile_w tiles.
+
+    Returns (tile_ptr, tile_rows) for `BlockOperator.set_stacked_tiles`: pixels of
+    one image tile (rows of A2^T), or rays of tile_h angles x tile_w bins (rows of
+    an angle-major A2), share most of their columns.
+    """
+    if tile_h * tile_w > 16:
+        raise ValueError("tiles hold at most 16 rows")
+    rows, ptr = [], [0]
+    for y0 in range(0, height, tile_h):
+        for x0 in range(0, width, tile_w):
+            ys = np.arange(y0, min(y0 + tile_h, height))
+            xs = np.arange(x0, min(x0 + tile_w, width))
+            rows.append((ys[:, None] * width + xs[None, :]).ravel())
+            ptr.append(ptr[-1] + rows[-1].size)
+    return np.asarray(ptr, dtype=np.int64), np.concatenate(rows).astype(np.int64)
+
+
 def _canonical_csr(matrix, dtype=None) -> sparse.csr_array:
     """float CSR with summed duplicates and sorted indices (`blockops.py:124-126`).
 
@@ -220,12 +239,14 @@ class BlockOperator:
 
     @classmethod
     def from_parallel_beam(cls, n: int, num_angles: int, num_bins: int, num_row_blocks: int = 1,
-                           num_col_blocks: int = 1, dtype=np.float32, device=None, depth: int = 1) -> "BlockOperator":
+                           num_col_blocks: int = 1, dtype=np.float32, device=None, depth: int = 1,
+                           tiles: bool = False) -> "BlockOperator":
         """Siddon parallel-beam projector generated on the GPU (`bsgd_siddon_csr`).
 
         Same matrix as `problems.parallel_beam_matrix` (bit-identical); the host
         never holds it, so configs[3]-size problems (~2e9 nonzeros) are possible.
-        ``depth`` > 1 stacks it over that many slices (configs[4]), see `stacked`.
+        ``depth`` > 1 stacks it over that many slices (configs[4]), see `stacked`;
+        with ``tiles`` the stacked products are tile-staged (`set_stacked_tiles`).
         """
         import math
         self = cls.__new__(cls)
@@ -265,7 +286,31 @@ class BlockOperator:
                 nat.check(rc)
         self._init_fields(handle, (rows, cols), dt, partition, int(nnz.value) * depth, depth=depth)
         self._slice_source = ("siddon", (n, num_angles, num_bins, dt))
+        if depth > 1 and tiles:
+            # A2^T rows are pixels: 4 x 4 image tiles; A2 rows are rays: 4 angles x 4 bins
+            self.set_stacked_tiles(True, grid_tiles(n, n))
+            self.set_stacked_tiles(False, grid_tiles(num_angles, num_bins))
         return self
+
+    def set_stacked_tiles(self, transposed: bool, tiles) -> None:
+        """Tile-staged products for a stacked operator (`bsgd_plan_stacked_tiles`).
+
+        ``tiles`` = (tile_ptr, tile_rows) grouping the stored rows of A2
+        (``transposed`` False) or A2^T (True) into tiles of <= 16 rows that share
+        columns (`grid_tiles`); None removes them.  Results are unchanged bit for bit.
+        """
+        if self.depth <= 1:
+            raise ValueError("tiles apply to slice-stacked operators only")
+        t = nat.torch()
+        with t.cuda.device(self._device):
+            if tiles is None:
+                nat.call("bsgd_plan_stacked_tiles", self._plan, int(bool(transposed)), 0, None, None,
+                         nat.stream_ptr(self._device))
+                return
+            ptr = np.ascontiguousarray(tiles[0], dtype=np.int64)
+            rows = np.ascontiguousarray(tiles[1], dtype=np.int64)
+            nat.call("bsgd_plan_stacked_tiles", self._plan, int(bool(transposed)), ptr.size - 1, ptr.ctypes.data,
+                     rows.ctypes.data, nat.stream_ptr(self._device))
 
     def _init_fields(self, handle, shape, dtype, partition, nnz_total, depth=1, csr=None) -> None:
         self._plan = handle

@@ -12,6 +12,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <type_traits>
 #include <unordered_map>
 #include <vector>
@@ -178,8 +179,25 @@ struct bsgd_plan {
     int64_t srows = 0, scols = 0, snnz = 0;  // stored CSR (A itself, or A2)
     int lanes = 32, kz_fwd = 1, kz_tr = 1;
     int64_t *d_col_sbounds = nullptr, *d_row_sbounds = nullptr;  // bounds / depth when all are multiples of it
+    // tile-staged copies of A2 / A2^T (stacked.cuh, stacked_tile_kernel), set by
+    // bsgd_plan_stacked_tiles
+    struct StkTileStore {
+        bool ok = false;
+        int64_t ntiles = 0;
+        int64_t *tile_ptr = nullptr, *row_ptr = nullptr, *uni_ptr = nullptr;
+        int32_t *tile_rows = nullptr, *uni = nullptr;
+        uint16_t *loc = nullptr;
+        void *val = nullptr;
+        size_t bytes = 0;
+    } sf, stt;
     bool stacked() const { return depth > 1; }
 };
+
+static void stk_tiles_free(bsgd_plan::StkTileStore &t) {
+    cudaFree(t.tile_ptr); cudaFree(t.row_ptr); cudaFree(t.uni_ptr); cudaFree(t.tile_rows); cudaFree(t.uni);
+    cudaFree(t.loc); cudaFree(t.val);
+    t = bsgd_plan::StkTileStore();
+}
 
 struct DeviceGuard {
     int prev = -1;
@@ -269,6 +287,8 @@ static void plan_free(bsgd_plan *p) {
     cudaFree(p->t_ptr); cudaFree(p->t_idx); cudaFree(p->t_val);
     cudaFree(p->d_row_bounds); cudaFree(p->d_col_bounds);
     cudaFree(p->d_col_sbounds); cudaFree(p->d_row_sbounds);
+    stk_tiles_free(p->sf);
+    stk_tiles_free(p->stt);
     delete p;
 }
 
@@ -635,6 +655,29 @@ static int launch_stacked(const Stk<V> &A, int kz, const E &e, double *part, int
     }
 }
 
+constexpr int kStkTileKZ = 2;  // 32 slices per tile window (33 MB of A^T's vector chunk at 256^3)
+
+template <typename V, bool RESID, bool ALIGNED, class E>
+static int launch_stk_tile(const Stk<V> &A, const bsgd_plan::StkTileStore &S, const E &e, double *part, int64_t *cnt,
+                           cudaStream_t st) {
+    auto kern = stacked_tile_kernel<V, kStkTileKZ, RESID, ALIGNED, E>;
+    const size_t smem = stk_tile_smem<kStkTileKZ>();
+    static bool attr_set = false;  // per instantiation
+    if (!attr_set) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr_set = true;
+    }
+    StkTiles T{S.ntiles, S.tile_ptr, S.tile_rows, S.row_ptr, S.loc, S.val, S.uni_ptr, S.uni};
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, smem);
+    const int64_t items = S.ntiles * (A.D / (16 * kStkTileKZ));
+    const int cap = std::min(std::max(occ, 1) * num_sms(), kMaxPartials);
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(items, cap));
+    kern<<<grid, kThreads, smem, st>>>(A, T, e, part, cnt);
+    LAUNCHED();
+    return BSGD_OK;
+}
+
 template <typename V, class E>
 static int launch_stacked_dir(const bsgd_plan *p, bool transposed, const double *vec, const E &e, double *part,
                               int64_t *cnt, cudaStream_t st) {
@@ -651,6 +694,17 @@ static int launch_stacked_dir(const bsgd_plan *p, bool transposed, const double 
     A.y = nullptr;
     A.L = p->lanes;
     const int kz = transposed ? p->kz_tr : p->kz_fwd;
+    const bsgd_plan::StkTileStore &S = transposed ? p->stt : p->sf;
+    if (S.ok && A.D % (16 * kStkTileKZ) == 0 && !getenv("BSGD_NO_STK_TILES")) {
+        if constexpr (std::is_same<E, EpiResid>::value) {
+            A.y = e.y;
+            return A.sbounds ? launch_stk_tile<V, true, true>(A, S, EpiResidFinal{e.r}, part, cnt, st)
+                             : launch_stk_tile<V, true, false>(A, S, EpiResidFinal{e.r}, part, cnt, st);
+        } else {
+            return A.sbounds ? launch_stk_tile<V, false, true>(A, S, e, part, cnt, st)
+                             : launch_stk_tile<V, false, false>(A, S, e, part, cnt, st);
+        }
+    }
     if constexpr (std::is_same<E, EpiResid>::value) {
         A.y = e.y;
         return launch_stacked<V, true>(A, kz, EpiResidFinal{e.r}, part, cnt, st);
@@ -877,6 +931,108 @@ static int launch_prox(ProxArgs &a, cudaStream_t st) {
 static void prox_fields(ProxArgs &a, const Ws &ws, int64_t n) {
     for (int k = 0; k < 9; ++k) a.f[k] = ws.fields + (size_t)k * field_stride(n);
     a.red = ws.red;
+}
+
+// Build the tile-staged copy of A2 (transposed = 0) or A2^T (1) from a host row
+// grouping: tile t holds stored rows tile_rows[tile_ptr[t] .. tile_ptr[t+1]).
+template <typename V>
+static int build_stk_tiles(bsgd_plan *p, bool tr, int64_t ntiles, const int64_t *tptr, const int64_t *trows,
+                           cudaStream_t st) {
+    const int64_t nrows = tr ? p->scols : p->srows, nnz = p->snnz;
+    if (tptr[0] != 0) return fail(BSGD_EINVAL, "tile_ptr must start at 0");
+    const int64_t ntr = tptr[ntiles];
+    if (ntr != nrows) return fail(BSGD_EINVAL, "tiles must cover every stored row exactly once (%lld of %lld)",
+                                  (long long)ntr, (long long)nrows);
+    std::vector<char> seen(nrows, 0);
+    for (int64_t t = 0; t < ntiles; ++t) {
+        const int64_t n = tptr[t + 1] - tptr[t];
+        if (n < 1 || n > kTileRows) return fail(BSGD_EINVAL, "tile %lld has %lld rows (1..%d)", (long long)t, (long long)n, kTileRows);
+    }
+    for (int64_t i = 0; i < ntr; ++i) {
+        const int64_t r = trows[i];
+        if (r < 0 || r >= nrows || seen[r]) return fail(BSGD_EINVAL, "tile rows must be a permutation of the stored rows");
+        seen[r] = 1;
+    }
+    std::vector<int64_t> ptr(nrows + 1);
+    std::vector<int32_t> idx(nnz);
+    std::vector<V> val(nnz);
+    CU(cudaMemcpyAsync(ptr.data(), tr ? p->t_ptr : p->f_ptr, sizeof(int64_t) * (nrows + 1), cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(idx.data(), tr ? p->t_idx : p->f_idx, sizeof(int32_t) * nnz, cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(val.data(), tr ? p->t_val : p->f_val, sizeof(V) * nnz, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    // tile-row entry offsets, padded to multiples of 4
+    std::vector<int64_t> rptr(ntr + 1, 0);
+    for (int64_t i = 0; i < ntr; ++i) {
+        const int64_t r = trows[i];
+        rptr[i + 1] = rptr[i] + ((ptr[r + 1] - ptr[r] + 3) & ~(int64_t)3);
+    }
+    const int64_t npad = rptr[ntr];
+    std::vector<int64_t> ucnt(ntiles + 1, 0);
+    std::vector<uint16_t> loc(npad, 0xFFFF);
+    std::vector<V> pval(npad, (V)0);
+    std::vector<std::vector<int32_t>> unions(ntiles);
+    unsigned nth = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    std::vector<std::thread> pool;
+    std::vector<int> bad(nth, 0);
+    for (unsigned w = 0; w < nth; ++w) {
+        pool.emplace_back([&, w]() {
+            std::vector<int32_t> cols;
+            for (int64_t t = w; t < ntiles; t += nth) {
+                cols.clear();
+                for (int64_t i = tptr[t]; i < tptr[t + 1]; ++i) {
+                    const int64_t r = trows[i];
+                    cols.insert(cols.end(), idx.begin() + ptr[r], idx.begin() + ptr[r + 1]);
+                }
+                std::sort(cols.begin(), cols.end());
+                cols.erase(std::unique(cols.begin(), cols.end()), cols.end());
+                if (cols.size() > 65000) { bad[w] = 1; continue; }
+                for (int64_t i = tptr[t]; i < tptr[t + 1]; ++i) {
+                    const int64_t r = trows[i];
+                    int64_t o = rptr[i];
+                    for (int64_t k = ptr[r]; k < ptr[r + 1]; ++k, ++o) {
+                        loc[o] = (uint16_t)(std::lower_bound(cols.begin(), cols.end(), idx[k]) - cols.begin());
+                        pval[o] = val[k];
+                    }
+                }
+                unions[t] = cols;
+            }
+        });
+    }
+    for (auto &th : pool) th.join();
+    for (int b : bad)
+        if (b) return fail(BSGD_EINVAL, "a tile's rows touch more than 65000 distinct columns");
+    for (int64_t t = 0; t < ntiles; ++t) ucnt[t + 1] = ucnt[t] + (int64_t)unions[t].size();
+    std::vector<int32_t> uni(std::max<int64_t>(ucnt[ntiles], 1));
+    for (int64_t t = 0; t < ntiles; ++t) std::copy(unions[t].begin(), unions[t].end(), uni.begin() + ucnt[t]);
+    std::vector<int32_t> trows32(ntr);
+    for (int64_t i = 0; i < ntr; ++i) trows32[i] = (int32_t)trows[i];
+    bsgd_plan::StkTileStore &S = tr ? p->stt : p->sf;
+    stk_tiles_free(S);
+    bsgd_plan::StkTileStore N;
+    auto up = [&](void **dst, const void *src, size_t bytes) -> cudaError_t {
+        cudaError_t e = cudaMalloc(dst, std::max<size_t>(bytes, 16));
+        if (e == cudaSuccess) e = cudaMemcpyAsync(*dst, src, bytes, cudaMemcpyHostToDevice, st);
+        N.bytes += bytes;
+        return e;
+    };
+    cudaError_t e = up((void **)&N.tile_ptr, tptr, sizeof(int64_t) * (ntiles + 1));
+    if (e == cudaSuccess) e = up((void **)&N.tile_rows, trows32.data(), sizeof(int32_t) * ntr);
+    if (e == cudaSuccess) e = up((void **)&N.row_ptr, rptr.data(), sizeof(int64_t) * (ntr + 1));
+    if (e == cudaSuccess) e = up((void **)&N.loc, loc.data(), sizeof(uint16_t) * npad);
+    if (e == cudaSuccess) e = up(&N.val, pval.data(), sizeof(V) * npad);
+    if (e == cudaSuccess) e = up((void **)&N.uni_ptr, ucnt.data(), sizeof(int64_t) * (ntiles + 1));
+    if (e == cudaSuccess) e = up((void **)&N.uni, uni.data(), sizeof(int32_t) * ucnt[ntiles]);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) {
+        stk_tiles_free(N);
+        return fail(e == cudaErrorMemoryAllocation ? BSGD_ENOMEM : BSGD_ECUDA, "tile upload failed: %s",
+                    cudaGetErrorString(e));
+    }
+    N.ntiles = ntiles;
+    N.ok = true;
+    S = N;
+    p->device_bytes += N.bytes;
+    return BSGD_OK;
 }
 
 // ---------------------------------------------------------------------------
@@ -1183,6 +1339,23 @@ int bsgd_plan_create_stacked_device(bsgd_plan **out, int device, int64_t depth, 
     if (depth < 2) return fail(BSGD_EINVAL, "depth must be >= 2 (a single slice is an ordinary plan)");
     return plan_create_adopt(out, device, depth, rows2, cols2, nnz2, indptr, indices, values, value_dtype,
                              num_row_blocks, num_col_blocks, row_bounds, col_bounds, stream);
+}
+
+int bsgd_plan_stacked_tiles(bsgd_plan *p, int transposed, int64_t ntiles, const int64_t *tile_ptr,
+                            const int64_t *tile_rows, void *stream) {
+    if (!p) return fail(BSGD_EINVAL, "plan is NULL");
+    if (!p->stacked()) return fail(BSGD_EINVAL, "tiles apply to slice-stacked plans only");
+    DeviceGuard guard(p->device);
+    bsgd_plan::StkTileStore &S = transposed ? p->stt : p->sf;
+    if (ntiles == 0) {
+        p->device_bytes -= S.bytes;
+        stk_tiles_free(S);
+        return BSGD_OK;
+    }
+    if (ntiles < 0 || !tile_ptr || !tile_rows) return fail(BSGD_EINVAL, "bad tile arguments");
+    cudaStream_t st = (cudaStream_t)stream;
+    return p->vdt == BSGD_F32 ? build_stk_tiles<float>(p, transposed != 0, ntiles, tile_ptr, tile_rows, st)
+                              : build_stk_tiles<double>(p, transposed != 0, ntiles, tile_ptr, tile_rows, st);
 }
 
 int bsgd_plan_stacked_info(const bsgd_plan *p, int64_t *depth, int64_t *rows2, int64_t *cols2, int64_t *nnz2) {

@@ -229,6 +229,196 @@ __global__ void __launch_bounds__(kThreads, (ALIGNED || Epi::K == 4) ? 4 : 3) st
 }
 
 // ---------------------------------------------------------------------------
+// Tile-staged products.  Stored rows are grouped into tiles of <= 16 rows that
+// share most of their columns (4x4 pixel tiles of A2^T: 4.0 entries per
+// distinct ray; 4 angles x 4 bins of A2: 3.45 entries per distinct pixel,
+// measured at 256^2 x 360 x 363).  Per tile the plan keeps the sorted union of
+// the tile's columns and, per entry, its position in that union (uint16, rows
+// padded to multiples of 4 with a sentinel).  A CTA takes one (tile, slice
+// chunk): the vector rows of the union stream through a double-buffered
+// shared-memory window with cp.async (one global read per distinct column
+// instead of one per entry), and 16 lanes per tile row accumulate from shared
+// memory.  Entries are still consumed in the row's stored order, so every
+// output keeps the exact block-sequential arithmetic of the kernel above.
+// ---------------------------------------------------------------------------
+struct StkTiles {
+    int64_t ntiles;
+    const int64_t *tile_ptr;   // [ntiles + 1] -> tile rows
+    const int32_t *tile_rows;  // stored row id of each tile row
+    const int64_t *row_ptr;    // [tile rows + 1] entry ranges, multiples of 4
+    const uint16_t *loc;       // position of the entry's column in the tile union; 0xFFFF = padding
+    const void *val;           // entry values (V), 0 for padding
+    const int64_t *uni_ptr;    // [ntiles + 1]
+    const int32_t *uni;        // sorted distinct stored columns per tile
+};
+
+constexpr int kTileRows = 16;   // rows per tile (one per 16-lane group)
+constexpr int kTileSeg = 64;    // union columns per shared-memory window
+
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)),
+                 "l"(gmem)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+template <int KZ>
+constexpr size_t stk_tile_smem() {
+    return sizeof(double) * 2 * kTileSeg * 16 * KZ + sizeof(int32_t) * 2 * kTileSeg;
+}
+
+template <typename V, int KZ, bool RESID, bool ALIGNED, class Epi>
+__global__ void __launch_bounds__(kThreads, 2) stacked_tile_kernel(Stk<V> A, StkTiles T, Epi epi, double *part,
+                                                                    int64_t *cnt) {
+    constexpr int ZC = 16 * KZ;
+    extern __shared__ double win[];                    // [2][kTileSeg][ZC]
+    int32_t *wcol = reinterpret_cast<int32_t *>(win + 2 * kTileSeg * ZC);  // [2][kTileSeg]
+    __shared__ double sm[8 * (kThreads / 32)];
+    const int tr = threadIdx.x >> 4, lane = threadIdx.x & 15;
+    const int32_t D = (int32_t)A.D;
+    const int64_t nchunks = D / ZC;
+    const int64_t items = T.ntiles * nchunks;
+    const uint64_t pol = policy_evict_first();
+    const V *__restrict__ val = reinterpret_cast<const V *>(T.val);
+
+    for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+        const int64_t ch = it / T.ntiles, t = it - ch * T.ntiles;
+        const int32_t z0 = (int32_t)ch * ZC;
+        const int64_t r0 = T.tile_ptr[t], nr = T.tile_ptr[t + 1] - r0;
+        const int64_t u0 = T.uni_ptr[t];
+        const int nu = (int)(T.uni_ptr[t + 1] - u0);
+        const bool live = tr < nr;
+        const int64_t srow = live ? T.tile_rows[r0 + tr] : 0;
+        int64_t e = live ? T.row_ptr[r0 + tr] : 0;
+        const int64_t e_end = live ? T.row_ptr[r0 + tr + 1] : 0;
+        double seg[KZ], acc[KZ];
+        int32_t thr[KZ];
+        int jb[KZ];
+#pragma unroll
+        for (int s = 0; s < KZ; ++s) {
+            const int32_t z = z0 + lane + 16 * s;
+            seg[s] = 0.0;
+            acc[s] = (RESID && live) ? A.y[srow * D + z] : 0.0;
+            jb[s] = 0;
+            if constexpr (ALIGNED) thr[s] = (int32_t)__ldg(A.sbounds + 1);
+            else thr[s] = (int32_t)((__ldg(A.bounds + 1) - z + D - 1) / D);
+        }
+        auto fold = [&](int s) {
+            if constexpr (RESID) acc[s] = rn_sub(acc[s], seg[s]);
+            else acc[s] = (jb[s] == 0) ? seg[s] : rn_add(acc[s], seg[s]);
+            seg[s] = 0.0;
+        };
+        // stage union columns [j0, j0 + kTileSeg) of the vector chunk into buffer b
+        auto stage = [&](int j0, int b) {
+            const int nj = (nu - j0) < kTileSeg ? (nu - j0) : kTileSeg;
+            constexpr int PER = ZC / 2;  // 16-byte pieces per union column
+            for (int q = threadIdx.x; q < nj * PER; q += kThreads) {
+                const int j = q / PER, piece = q - j * PER;
+                const int32_t col = __ldg(T.uni + u0 + j0 + j);
+                cp_async16(win + ((size_t)b * kTileSeg + j) * ZC + 2 * piece, A.vec + (int64_t)col * D + z0 + 2 * piece);
+            }
+            for (int j = threadIdx.x; j < nj; j += kThreads) wcol[b * kTileSeg + j] = __ldg(T.uni + u0 + j0 + j);
+            cp_async_commit();
+        };
+        const int nseg = (nu + kTileSeg - 1) / kTileSeg;
+        // entry cursor: 4 entries at a time (rows are padded to multiples of 4)
+        uint16_t lb[4] = {0xFFFF, 0xFFFF, 0xFFFF, 0xFFFF};
+        double vb[4] = {0.0, 0.0, 0.0, 0.0};
+        int pos = 4;
+        auto refill = [&]() {
+            const uint2 l2 = __ldg(reinterpret_cast<const uint2 *>(T.loc + e));
+            lb[0] = (uint16_t)(l2.x & 0xFFFF); lb[1] = (uint16_t)(l2.x >> 16);
+            lb[2] = (uint16_t)(l2.y & 0xFFFF); lb[3] = (uint16_t)(l2.y >> 16);
+            if constexpr (sizeof(V) == 4) {
+                const float4 v4 = ld_stream4(reinterpret_cast<const float *>(val) + e, pol);
+                vb[0] = v4.x; vb[1] = v4.y; vb[2] = v4.z; vb[3] = v4.w;
+            } else {
+                const double2 a2 = ld_stream2(reinterpret_cast<const double *>(val) + e, pol);
+                const double2 b2 = ld_stream2(reinterpret_cast<const double *>(val) + e + 2, pol);
+                vb[0] = a2.x; vb[1] = a2.y; vb[2] = b2.x; vb[3] = b2.y;
+            }
+            e += 4;
+            pos = 0;
+        };
+        if (nseg > 0) stage(0, 0);
+        for (int sg = 0; sg < nseg; ++sg) {
+            const int b = sg & 1;
+            if (sg + 1 < nseg) {
+                stage((sg + 1) * kTileSeg, b ^ 1);
+                cp_async_wait<1>();
+            } else {
+                cp_async_wait<0>();
+            }
+            __syncthreads();
+            const int j0 = sg * kTileSeg;
+            const int jend = j0 + kTileSeg;
+            const double *wb = win + (size_t)b * kTileSeg * ZC + lane;
+            const int32_t *cb = wcol + b * kTileSeg;
+            if (live) {
+                for (;;) {
+                    if (pos == 4) {
+                        if (e >= e_end) break;
+                        refill();
+                    }
+                    int done = 4;
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        if (u >= pos && done == 4) {
+                            const int l = lb[u];
+                            if (l >= jend) {
+                                done = u;
+                            } else {
+                                const int jl = l - j0;
+                                const int32_t c = cb[jl];
+                                if constexpr (ALIGNED) {
+                                    while (c >= thr[0]) {
+#pragma unroll
+                                        for (int s = 0; s < KZ; ++s) { fold(s); ++jb[s]; }
+                                        thr[0] = (int32_t)__ldg(A.sbounds + jb[0] + 1);
+                                    }
+                                } else {
+#pragma unroll
+                                    for (int s = 0; s < KZ; ++s) {
+                                        while (c >= thr[s]) {
+                                            fold(s);
+                                            ++jb[s];
+                                            thr[s] = (int32_t)((__ldg(A.bounds + jb[s] + 1) - (z0 + lane + 16 * s) + D - 1) / D);
+                                        }
+                                    }
+                                }
+                                const double v = vb[u];
+#pragma unroll
+                                for (int s = 0; s < KZ; ++s) seg[s] = rn_add(seg[s], rn_mul(v, wb[jl * ZC + 16 * s]));
+                            }
+                        }
+                    }
+                    if (done < 4) { pos = done; break; }
+                    pos = 4;
+                }
+            }
+            __syncthreads();  // buffer b is restaged two windows later
+        }
+        if (live) {
+#pragma unroll
+            for (int s = 0; s < KZ; ++s) {
+                for (; jb[s] < A.nb; ++jb[s]) fold(s);
+                epi(srow * D + z0 + lane + 16 * s, acc[s]);
+            }
+        }
+    }
+    if constexpr (Epi::K > 0) {
+        double v[Epi::K];
+        epi.flush(v);
+        block_sum<Epi::K>(v, sm);
+        if (threadIdx.x == 0 && part != nullptr)
+            for (int k = 0; k < Epi::K; ++k) part[(size_t)blockIdx.x * Epi::K + k] = v[k];
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0 && cnt != nullptr) cnt[0] = gridDim.x;
+}
+
+// ---------------------------------------------------------------------------
 // block-restricted and stochastic-pair products (thread per interleaved output)
 // ---------------------------------------------------------------------------
 

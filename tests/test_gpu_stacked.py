@@ -136,3 +136,53 @@ def test_stacked_device_generator_matches_host(M):
     assert d.op.depth == d.depth == 16 and d.op.shape[1] == 16 * 16 * 16
     assert d.layout().size == d.op.shape[1] and d.layout().is_identity
     assert d.layout(slice_major=True).size == d.op.shape[1]
+
+
+@pytest.mark.parametrize("depth,m", [(32, 4), (64, 16), (96, 3)])
+def test_tile_staged_products_bit_exact(M, depth, m):
+    """Tile-staged stacked products (shared-memory windows over each tile's distinct
+    columns) equal the untiled kernel and the oracle bit for bit."""
+    blockops, problems = M[0], M[1]
+    n, ang, nb = 12, 10, 17
+    a2 = problems.parallel_beam_matrix(n, ang, nb, dtype=np.float32)
+    a = _expanded(a2, depth)
+    part = blockops.make_partition(a.shape[0], a.shape[1], m, m)
+    plain = blockops.BlockOperator.stacked(a2, depth, part)
+    tiled = blockops.BlockOperator.stacked(a2, depth, part)
+    tiled.set_stacked_tiles(True, blockops.grid_tiles(n, n))
+    tiled.set_stacked_tiles(False, blockops.grid_tiles(ang, nb, 4, 4))
+    oop = orc.OracleOperator(a, m, m)
+    rng = np.random.default_rng(depth)
+    x = rng.standard_normal(a.shape[1])
+    r = rng.standard_normal(a.shape[0])
+    assert np.array_equal(tiled.matvec(x), oop.matvec(x))
+    assert np.array_equal(tiled.rmatvec(r), oop.rmatvec(r))
+    assert np.array_equal(tiled.matvec(x), plain.matvec(x))
+    y = rng.standard_normal(a.shape[0])
+    rt, st = tiled.residual_sumsq(x, y)
+    rp, sp = plain.residual_sumsq(x, y)
+    assert np.array_equal(rt.cpu().numpy(), rp.cpu().numpy())
+    tiled.set_stacked_tiles(False, None)   # removable
+    assert np.array_equal(tiled.matvec(x), oop.matvec(x))
+    with pytest.raises(ValueError):
+        tiled.set_stacked_tiles(True, (np.array([0, 3]), np.array([0, 1, 2])))   # must cover all rows
+
+
+def test_tile_staged_run_bit_exact(M):
+    """Device-generated stacked operator with tiles (the configs[4] path): run == oracle."""
+    blockops, problems, solvers, spectral, tv = M
+    n, depth, ang, nb = 12, 32, 10, 17
+    op = blockops.BlockOperator.from_parallel_beam(n, ang, nb, 4, 4, dtype=np.float32, depth=depth, tiles=True)
+    a2 = problems.parallel_beam_matrix(n, ang, nb, dtype=np.float32)
+    a = _expanded(a2, depth)
+    vol = problems.ellipsoid_phantom(n, depth, 6, 0)
+    x_true = np.ascontiguousarray(vol.reshape(depth, n * n).T).ravel()
+    y = a @ x_true + np.random.default_rng(1).standard_normal(a.shape[0]) * 0.01
+    oop = orc.OracleOperator(a, 4, 4)
+    u, _, _ = orc.largest_eigenvalue(oop)
+    layout = tv.VolumeLayout.z_major(n, n, depth)
+    cfg = solvers.SolverConfig(mu=0.9 / (2 * u), lam=0.01, epochs=5, seed=3, prox=tv.ProxSettings(10, 1e-5))
+    tr = solvers.run_solver("bsgd", solvers.Problem(op, y, x_true, layout), cfg)
+    prm = orc.Params(mu=cfg.mu, lam=0.01, epochs=5, seed=3, max_inner_iters=10, tol=1e-5)
+    ref = orc.run_bsgd(oop, y, prm, x_true=x_true, perm=np.arange(a.shape[1]), hw=(n, n, depth))
+    assert np.array_equal(tr.final_x, ref.final_x)
