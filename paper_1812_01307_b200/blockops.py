@@ -240,7 +240,7 @@ class BlockOperator:
     @classmethod
     def from_parallel_beam(cls, n: int, num_angles: int, num_bins: int, num_row_blocks: int = 1,
                            num_col_blocks: int = 1, dtype=np.float32, device=None, depth: int = 1,
-                           tiles: bool = False) -> "BlockOperator":
+                           tiles: bool = True) -> "BlockOperator":
         """Siddon parallel-beam projector generated on the GPU (`bsgd_siddon_csr`).
 
         Same matrix as `problems.parallel_beam_matrix` (bit-identical); the host

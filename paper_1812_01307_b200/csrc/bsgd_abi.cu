@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -184,9 +185,10 @@ struct bsgd_plan {
     struct StkTileStore {
         bool ok = false;
         int64_t ntiles = 0;
-        int64_t *tile_ptr = nullptr, *row_ptr = nullptr, *uni_ptr = nullptr;
-        int32_t *tile_rows = nullptr, *uni = nullptr;
-        uint16_t *loc = nullptr;
+        int64_t *tile_ptr = nullptr, *seg_ptr = nullptr, *seg_uni = nullptr, *seg_ent = nullptr;
+        int32_t *tile_rows = nullptr, *seg_nj = nullptr, *uni = nullptr;
+        uint16_t *seg_row = nullptr;
+        uint8_t *loc = nullptr;
         void *val = nullptr;
         size_t bytes = 0;
     } sf, stt;
@@ -194,8 +196,8 @@ struct bsgd_plan {
 };
 
 static void stk_tiles_free(bsgd_plan::StkTileStore &t) {
-    cudaFree(t.tile_ptr); cudaFree(t.row_ptr); cudaFree(t.uni_ptr); cudaFree(t.tile_rows); cudaFree(t.uni);
-    cudaFree(t.loc); cudaFree(t.val);
+    cudaFree(t.tile_ptr); cudaFree(t.seg_ptr); cudaFree(t.seg_uni); cudaFree(t.seg_ent); cudaFree(t.tile_rows);
+    cudaFree(t.seg_nj); cudaFree(t.uni); cudaFree(t.seg_row); cudaFree(t.loc); cudaFree(t.val);
     t = bsgd_plan::StkTileStore();
 }
 
@@ -655,25 +657,23 @@ static int launch_stacked(const Stk<V> &A, int kz, const E &e, double *part, int
     }
 }
 
-constexpr int kStkTileKZ = 2;  // 32 slices per tile window (33 MB of A^T's vector chunk at 256^3)
-
 template <typename V, bool RESID, bool ALIGNED, class E>
 static int launch_stk_tile(const Stk<V> &A, const bsgd_plan::StkTileStore &S, const E &e, double *part, int64_t *cnt,
                            cudaStream_t st) {
-    auto kern = stacked_tile_kernel<V, kStkTileKZ, RESID, ALIGNED, E>;
-    const size_t smem = stk_tile_smem<kStkTileKZ>();
+    auto kern = stacked_tile_kernel<V, RESID, ALIGNED, E>;
+    const size_t smem = stk_tile_smem<V>();
     static bool attr_set = false;  // per instantiation
     if (!attr_set) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr_set = true;
     }
-    StkTiles T{S.ntiles, S.tile_ptr, S.tile_rows, S.row_ptr, S.loc, S.val, S.uni_ptr, S.uni};
+    StkTiles T{S.ntiles, S.tile_ptr, S.tile_rows, S.seg_ptr, S.seg_nj, S.seg_ent, S.seg_row, S.uni, S.loc, S.val};
     int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, smem);
-    const int64_t items = S.ntiles * (A.D / (16 * kStkTileKZ));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kStkTileThreads, smem);
+    const int64_t items = S.ntiles * (A.D / kTileZC);
     const int cap = std::min(std::max(occ, 1) * num_sms(), kMaxPartials);
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(items, cap));
-    kern<<<grid, kThreads, smem, st>>>(A, T, e, part, cnt);
+    kern<<<grid, kStkTileThreads, smem, st>>>(A, T, e, part, cnt);
     LAUNCHED();
     return BSGD_OK;
 }
@@ -695,7 +695,7 @@ static int launch_stacked_dir(const bsgd_plan *p, bool transposed, const double 
     A.L = p->lanes;
     const int kz = transposed ? p->kz_tr : p->kz_fwd;
     const bsgd_plan::StkTileStore &S = transposed ? p->stt : p->sf;
-    if (S.ok && A.D % (16 * kStkTileKZ) == 0 && !getenv("BSGD_NO_STK_TILES")) {
+    if (S.ok && A.D % kTileZC == 0 && !getenv("BSGD_NO_STK_TILES")) {
         if constexpr (std::is_same<E, EpiResid>::value) {
             A.y = e.y;
             return A.sbounds ? launch_stk_tile<V, true, true>(A, S, EpiResidFinal{e.r}, part, cnt, st)
@@ -960,24 +960,24 @@ static int build_stk_tiles(bsgd_plan *p, bool tr, int64_t ntiles, const int64_t 
     CU(cudaMemcpyAsync(idx.data(), tr ? p->t_idx : p->f_idx, sizeof(int32_t) * nnz, cudaMemcpyDeviceToHost, st));
     CU(cudaMemcpyAsync(val.data(), tr ? p->t_val : p->f_val, sizeof(V) * nnz, cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));
-    // tile-row entry offsets, padded to multiples of 4
-    std::vector<int64_t> rptr(ntr + 1, 0);
-    for (int64_t i = 0; i < ntr; ++i) {
-        const int64_t r = trows[i];
-        rptr[i + 1] = rptr[i] + ((ptr[r + 1] - ptr[r] + 3) & ~(int64_t)3);
-    }
-    const int64_t npad = rptr[ntr];
-    std::vector<int64_t> ucnt(ntiles + 1, 0);
-    std::vector<uint16_t> loc(npad, 0xFFFF);
-    std::vector<V> pval(npad, (V)0);
-    std::vector<std::vector<int32_t>> unions(ntiles);
+    // per tile: sorted distinct columns, cut into segments of kTileSeg; per segment
+    // the tile rows' entries inside it (row-major, position in the segment as uint8)
+    struct TileOut {
+        std::vector<int32_t> uni;
+        std::vector<int32_t> nj;
+        std::vector<std::array<uint16_t, 24>> rows;
+        std::vector<uint8_t> loc;   // per segment, padded to 16
+        std::vector<V> val;
+        std::vector<int64_t> ent;   // per segment entry offset inside this tile's arrays
+    };
+    std::vector<TileOut> outs(ntiles);
     unsigned nth = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
     std::vector<std::thread> pool;
-    std::vector<int> bad(nth, 0);
     for (unsigned w = 0; w < nth; ++w) {
         pool.emplace_back([&, w]() {
             std::vector<int32_t> cols;
             for (int64_t t = w; t < ntiles; t += nth) {
+                TileOut &o = outs[t];
                 cols.clear();
                 for (int64_t i = tptr[t]; i < tptr[t + 1]; ++i) {
                     const int64_t r = trows[i];
@@ -985,25 +985,69 @@ static int build_stk_tiles(bsgd_plan *p, bool tr, int64_t ntiles, const int64_t 
                 }
                 std::sort(cols.begin(), cols.end());
                 cols.erase(std::unique(cols.begin(), cols.end()), cols.end());
-                if (cols.size() > 65000) { bad[w] = 1; continue; }
-                for (int64_t i = tptr[t]; i < tptr[t + 1]; ++i) {
-                    const int64_t r = trows[i];
-                    int64_t o = rptr[i];
-                    for (int64_t k = ptr[r]; k < ptr[r + 1]; ++k, ++o) {
-                        loc[o] = (uint16_t)(std::lower_bound(cols.begin(), cols.end(), idx[k]) - cols.begin());
-                        pval[o] = val[k];
+                o.uni = cols;
+                const int64_t nu = (int64_t)cols.size();
+                const int64_t nseg = std::max<int64_t>(1, (nu + kTileSeg - 1) / kTileSeg);
+                const int64_t nrt = tptr[t + 1] - tptr[t];
+                std::vector<int64_t> cur(nrt);
+                for (int64_t i = 0; i < nrt; ++i) cur[i] = ptr[trows[tptr[t] + i]];
+                for (int64_t sg = 0; sg < nseg; ++sg) {
+                    const int64_t j0 = sg * kTileSeg, j1 = std::min<int64_t>(nu, j0 + kTileSeg);
+                    const int32_t cmax = j1 > j0 ? cols[j1 - 1] : -1;
+                    std::array<uint16_t, 24> ro{};
+                    o.ent.push_back((int64_t)o.loc.size());
+                    int n = 0;
+                    for (int64_t i = 0; i < nrt; ++i) {
+                        const int64_t r = trows[tptr[t] + i];
+                        ro[i] = (uint16_t)n;
+                        while (cur[i] < ptr[r + 1] && idx[cur[i]] <= cmax) {
+                            const int64_t pos = std::lower_bound(cols.begin() + j0, cols.begin() + j1, idx[cur[i]]) - cols.begin();
+                            o.loc.push_back((uint8_t)(pos - j0));
+                            o.val.push_back(val[cur[i]]);
+                            ++cur[i];
+                            ++n;
+                        }
                     }
+                    for (int64_t i = nrt; i <= kTileRows; ++i) ro[i] = (uint16_t)n;
+                    while (o.loc.size() % 16) { o.loc.push_back(0); o.val.push_back((V)0); }
+                    o.rows.push_back(ro);
+                    o.nj.push_back((int32_t)(j1 - j0));
                 }
-                unions[t] = cols;
             }
         });
     }
     for (auto &th : pool) th.join();
-    for (int b : bad)
-        if (b) return fail(BSGD_EINVAL, "a tile's rows touch more than 65000 distinct columns");
-    for (int64_t t = 0; t < ntiles; ++t) ucnt[t + 1] = ucnt[t] + (int64_t)unions[t].size();
-    std::vector<int32_t> uni(std::max<int64_t>(ucnt[ntiles], 1));
-    for (int64_t t = 0; t < ntiles; ++t) std::copy(unions[t].begin(), unions[t].end(), uni.begin() + ucnt[t]);
+    // flatten: segment g's column ids at uni[g * kTileSeg ..] (zero padded)
+    int64_t nseg_all = 0, nent = 0;
+    std::vector<int64_t> seg_ptr(ntiles + 1, 0);
+    for (int64_t t = 0; t < ntiles; ++t) {
+        seg_ptr[t + 1] = seg_ptr[t] + (int64_t)outs[t].nj.size();
+        nent += (int64_t)outs[t].loc.size();
+    }
+    nseg_all = seg_ptr[ntiles];
+    std::vector<int64_t> seg_uni(nseg_all), seg_ent(nseg_all);
+    std::vector<int32_t> seg_nj(nseg_all), uni((size_t)std::max<int64_t>(nseg_all, 1) * kTileSeg, 0);
+    std::vector<uint16_t> seg_row((size_t)nseg_all * 24);
+    std::vector<uint8_t> loc(std::max<int64_t>(nent, 16));
+    std::vector<V> pval(std::max<int64_t>(nent, 16));
+    int64_t eo = 0;
+    for (int64_t t = 0; t < ntiles; ++t) {
+        const TileOut &o = outs[t];
+        int64_t src = 0;
+        for (size_t sg = 0; sg < o.nj.size(); ++sg) {
+            const int64_t g = seg_ptr[t] + (int64_t)sg;
+            const int32_t nj = o.nj[sg];
+            seg_uni[g] = g * kTileSeg;
+            seg_nj[g] = nj;
+            seg_ent[g] = eo + o.ent[sg];
+            std::copy(o.rows[sg].begin(), o.rows[sg].end(), seg_row.begin() + g * 24);
+            std::copy(o.uni.begin() + src, o.uni.begin() + src + nj, uni.begin() + g * kTileSeg);
+            src += nj;
+        }
+        std::copy(o.loc.begin(), o.loc.end(), loc.begin() + eo);
+        std::copy(o.val.begin(), o.val.end(), pval.begin() + eo);
+        eo += (int64_t)o.loc.size();
+    }
     std::vector<int32_t> trows32(ntr);
     for (int64_t i = 0; i < ntr; ++i) trows32[i] = (int32_t)trows[i];
     bsgd_plan::StkTileStore &S = tr ? p->stt : p->sf;
@@ -1017,11 +1061,14 @@ static int build_stk_tiles(bsgd_plan *p, bool tr, int64_t ntiles, const int64_t 
     };
     cudaError_t e = up((void **)&N.tile_ptr, tptr, sizeof(int64_t) * (ntiles + 1));
     if (e == cudaSuccess) e = up((void **)&N.tile_rows, trows32.data(), sizeof(int32_t) * ntr);
-    if (e == cudaSuccess) e = up((void **)&N.row_ptr, rptr.data(), sizeof(int64_t) * (ntr + 1));
-    if (e == cudaSuccess) e = up((void **)&N.loc, loc.data(), sizeof(uint16_t) * npad);
-    if (e == cudaSuccess) e = up(&N.val, pval.data(), sizeof(V) * npad);
-    if (e == cudaSuccess) e = up((void **)&N.uni_ptr, ucnt.data(), sizeof(int64_t) * (ntiles + 1));
-    if (e == cudaSuccess) e = up((void **)&N.uni, uni.data(), sizeof(int32_t) * ucnt[ntiles]);
+    if (e == cudaSuccess) e = up((void **)&N.seg_ptr, seg_ptr.data(), sizeof(int64_t) * (ntiles + 1));
+    if (e == cudaSuccess) e = up((void **)&N.seg_uni, seg_uni.data(), sizeof(int64_t) * nseg_all);
+    if (e == cudaSuccess) e = up((void **)&N.seg_nj, seg_nj.data(), sizeof(int32_t) * nseg_all);
+    if (e == cudaSuccess) e = up((void **)&N.seg_ent, seg_ent.data(), sizeof(int64_t) * nseg_all);
+    if (e == cudaSuccess) e = up((void **)&N.seg_row, seg_row.data(), sizeof(uint16_t) * seg_row.size());
+    if (e == cudaSuccess) e = up((void **)&N.uni, uni.data(), sizeof(int32_t) * uni.size());
+    if (e == cudaSuccess) e = up((void **)&N.loc, loc.data(), loc.size());
+    if (e == cudaSuccess) e = up(&N.val, pval.data(), sizeof(V) * pval.size());
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) {
         stk_tiles_free(N);

@@ -35,6 +35,7 @@
 #pragma once
 
 #include "common.cuh"
+#include "sm100.cuh"
 
 namespace bsgd {
 
@@ -233,178 +234,271 @@ __global__ void __launch_bounds__(kThreads, (ALIGNED || Epi::K == 4) ? 4 : 3) st
 // share most of their columns (4x4 pixel tiles of A2^T: 4.0 entries per
 // distinct ray; 4 angles x 4 bins of A2: 3.45 entries per distinct pixel,
 // measured at 256^2 x 360 x 363).  Per tile the plan keeps the sorted union of
-// the tile's columns and, per entry, its position in that union (uint16, rows
-// padded to multiples of 4 with a sentinel).  A CTA takes one (tile, slice
-// chunk): the vector rows of the union stream through a double-buffered
-// shared-memory window with cp.async (one global read per distinct column
-// instead of one per entry), and 16 lanes per tile row accumulate from shared
-// memory.  Entries are still consumed in the row's stored order, so every
-// output keeps the exact block-sequential arithmetic of the kernel above.
+// the tile's columns cut into segments of kTileSeg columns, and per segment the
+// tile rows' entries that fall in it (row-major, uint8 position in the segment
+// + value).  Warp-specialised CTA: one producer warp walks the CTA's stream of
+// (tile, slice chunk, segment) stages and fills a kTileStages-deep ring with
+// TMA bulk copies -- one 256-byte vector row per distinct column (instead of
+// one gather per entry), the column ids, the entries -- completing on a
+// full-barrier per slot; eight consumer warps (two tile rows each, one slice
+// per lane) accumulate from shared memory and release the slot on an
+// empty-barrier.  Each row still consumes its entries in stored order, so every
+// output keeps the exact block-sequential arithmetic of the direct kernel.
 // ---------------------------------------------------------------------------
+constexpr int kTileRows = 16;      // rows per tile
+constexpr int kTileSeg = 32;       // union columns per segment
+constexpr int kTileStages = 4;     // ring depth
+constexpr int kTileSegEnt = kTileRows * kTileSeg;  // entries per segment, upper bound
+constexpr int kTileKZ = 4;         // slices per lane
+constexpr int kTileZC = 32 * kTileKZ;  // slices per item
+constexpr int kTileProducers = 4;
+constexpr int kStkTileThreads = 32 * (16 + kTileProducers);  // 16 consumer warps (one tile row each) + producers
+
 struct StkTiles {
     int64_t ntiles;
     const int64_t *tile_ptr;   // [ntiles + 1] -> tile rows
     const int32_t *tile_rows;  // stored row id of each tile row
-    const int64_t *row_ptr;    // [tile rows + 1] entry ranges, multiples of 4
-    const uint16_t *loc;       // position of the entry's column in the tile union; 0xFFFF = padding
-    const void *val;           // entry values (V), 0 for padding
-    const int64_t *uni_ptr;    // [ntiles + 1]
-    const int32_t *uni;        // sorted distinct stored columns per tile
+    const int64_t *seg_ptr;    // [ntiles + 1] -> segments (>= 1 per tile)
+    const int32_t *seg_nj;     // [segments] columns in the segment
+    const int64_t *seg_ent;    // [segments] first entry (multiple of 16)
+    const uint16_t *seg_row;   // [segments][24] cumulative entry counts per tile row ([16] = total, padded)
+    const int32_t *uni;        // [segments][kTileSeg] distinct stored columns, per tile ascending (padded)
+    const uint8_t *loc;        // entry -> column position in its segment
+    const void *val;           // entry values (V)
 };
 
-constexpr int kTileRows = 16;   // rows per tile (one per 16-lane group)
-constexpr int kTileSeg = 64;    // union columns per shared-memory window
+template <typename V>
+struct TileStage {
+    static constexpr size_t win = sizeof(double) * kTileSeg * kTileZC;
+    static constexpr size_t col = sizeof(int32_t) * kTileSeg;
+    static constexpr size_t val = sizeof(V) * kTileSegEnt;
+    static constexpr size_t loc = kTileSegEnt;
+    static constexpr size_t row = 48;
+    static constexpr size_t bytes = win + col + val + loc + row;
+};
 
-__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)),
-                 "l"(gmem)
-                 : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
-
-template <int KZ>
+template <typename V>
 constexpr size_t stk_tile_smem() {
-    return sizeof(double) * 2 * kTileSeg * 16 * KZ + sizeof(int32_t) * 2 * kTileSeg;
+    return TileStage<V>::bytes * kTileStages + 2 * kTileStages * sizeof(uint64_t);
 }
 
-template <typename V, int KZ, bool RESID, bool ALIGNED, class Epi>
-__global__ void __launch_bounds__(kThreads, 2) stacked_tile_kernel(Stk<V> A, StkTiles T, Epi epi, double *part,
-                                                                    int64_t *cnt) {
-    constexpr int ZC = 16 * KZ;
-    extern __shared__ double win[];                    // [2][kTileSeg][ZC]
-    int32_t *wcol = reinterpret_cast<int32_t *>(win + 2 * kTileSeg * ZC);  // [2][kTileSeg]
-    __shared__ double sm[8 * (kThreads / 32)];
-    const int tr = threadIdx.x >> 4, lane = threadIdx.x & 15;
+template <typename V, bool RESID, bool ALIGNED, class Epi>
+__global__ void __launch_bounds__(kStkTileThreads, 1) stacked_tile_kernel(Stk<V> A, StkTiles T, Epi epi, double *part,
+                                                                        int64_t *cnt) {
+    using ST = TileStage<V>;
+    constexpr int ZC = kTileZC;
+    extern __shared__ __align__(128) unsigned char smraw[];
+    __shared__ double sm[4 * 18];
+    uint64_t *full = reinterpret_cast<uint64_t *>(smraw + ST::bytes * kTileStages);
+    uint64_t *empty = full + kTileStages;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int32_t D = (int32_t)A.D;
     const int64_t nchunks = D / ZC;
     const int64_t items = T.ntiles * nchunks;
-    const uint64_t pol = policy_evict_first();
-    const V *__restrict__ val = reinterpret_cast<const V *>(T.val);
+    auto slot = [&](int k) { return smraw + (size_t)k * ST::bytes; };
 
-    for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
-        const int64_t ch = it / T.ntiles, t = it - ch * T.ntiles;
-        const int32_t z0 = (int32_t)ch * ZC;
-        const int64_t r0 = T.tile_ptr[t], nr = T.tile_ptr[t + 1] - r0;
-        const int64_t u0 = T.uni_ptr[t];
-        const int nu = (int)(T.uni_ptr[t + 1] - u0);
-        const bool live = tr < nr;
-        const int64_t srow = live ? T.tile_rows[r0 + tr] : 0;
-        int64_t e = live ? T.row_ptr[r0 + tr] : 0;
-        const int64_t e_end = live ? T.row_ptr[r0 + tr + 1] : 0;
-        double seg[KZ], acc[KZ];
-        int32_t thr[KZ];
-        int jb[KZ];
-#pragma unroll
-        for (int s = 0; s < KZ; ++s) {
-            const int32_t z = z0 + lane + 16 * s;
-            seg[s] = 0.0;
-            acc[s] = (RESID && live) ? A.y[srow * D + z] : 0.0;
-            jb[s] = 0;
-            if constexpr (ALIGNED) thr[s] = (int32_t)__ldg(A.sbounds + 1);
-            else thr[s] = (int32_t)((__ldg(A.bounds + 1) - z + D - 1) / D);
+    if (threadIdx.x == 0) {
+        for (int k = 0; k < kTileStages; ++k) {
+            mbar_init(&full[k], 1);
+            mbar_init(&empty[k], 16);
         }
-        auto fold = [&](int s) {
-            if constexpr (RESID) acc[s] = rn_sub(acc[s], seg[s]);
-            else acc[s] = (jb[s] == 0) ? seg[s] : rn_add(acc[s], seg[s]);
-            seg[s] = 0.0;
-        };
-        // stage union columns [j0, j0 + kTileSeg) of the vector chunk into buffer b
-        auto stage = [&](int j0, int b) {
-            const int nj = (nu - j0) < kTileSeg ? (nu - j0) : kTileSeg;
-            constexpr int PER = ZC / 2;  // 16-byte pieces per union column
-            for (int q = threadIdx.x; q < nj * PER; q += kThreads) {
-                const int j = q / PER, piece = q - j * PER;
-                const int32_t col = __ldg(T.uni + u0 + j0 + j);
-                cp_async16(win + ((size_t)b * kTileSeg + j) * ZC + 2 * piece, A.vec + (int64_t)col * D + z0 + 2 * piece);
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    if (warp >= 16) {
+        // ---------------- producers ----------------
+        const int pw = warp - 16;  // producer pw issues stream positions pw, pw + kTileProducers, ...
+        // Segments are issued in batches of four.  A batch's metadata (one
+        // segment per lane, shuffled out) and column ids (segment g's ids sit at
+        // uni[32 g ..], one per lane) have no dependent loads, and the next
+        // batch's are fetched before this batch is issued, so the producer never
+        // waits on its own loads.
+        constexpr int B = 4;
+        int64_t seq = 0;  // stream position of the cursor
+        int64_t it = blockIdx.x, g = 0, g1 = 0;
+        int32_t z0 = 0;
+        auto load_item = [&]() {
+            if (it < items) {
+                const int64_t t = it % T.ntiles;
+                g = T.seg_ptr[t];
+                g1 = T.seg_ptr[t + 1];
+                z0 = (int32_t)(it / T.ntiles) * ZC;
             }
-            for (int j = threadIdx.x; j < nj; j += kThreads) wcol[b * kTileSeg + j] = __ldg(T.uni + u0 + j0 + j);
-            cp_async_commit();
         };
-        const int nseg = (nu + kTileSeg - 1) / kTileSeg;
-        // entry cursor: 4 entries at a time (rows are padded to multiples of 4)
-        uint16_t lb[4] = {0xFFFF, 0xFFFF, 0xFFFF, 0xFFFF};
-        double vb[4] = {0.0, 0.0, 0.0, 0.0};
-        int pos = 4;
-        auto refill = [&]() {
-            const uint2 l2 = __ldg(reinterpret_cast<const uint2 *>(T.loc + e));
-            lb[0] = (uint16_t)(l2.x & 0xFFFF); lb[1] = (uint16_t)(l2.x >> 16);
-            lb[2] = (uint16_t)(l2.y & 0xFFFF); lb[3] = (uint16_t)(l2.y >> 16);
-            if constexpr (sizeof(V) == 4) {
-                const float4 v4 = ld_stream4(reinterpret_cast<const float *>(val) + e, pol);
-                vb[0] = v4.x; vb[1] = v4.y; vb[2] = v4.z; vb[3] = v4.w;
-            } else {
-                const double2 a2 = ld_stream2(reinterpret_cast<const double *>(val) + e, pol);
-                const double2 b2 = ld_stream2(reinterpret_cast<const double *>(val) + e + 2, pol);
-                vb[0] = a2.x; vb[1] = a2.y; vb[2] = b2.x; vb[3] = b2.y;
-            }
-            e += 4;
-            pos = 0;
+        load_item();
+        struct Batch {
+            int64_t gb[B];
+            int64_t sq[B];
+            int32_t zb[B];
+            int nb;
+            int64_t m_eb;
+            int m_nj, m_ne;
+            int32_t col[B];
         };
-        if (nseg > 0) stage(0, 0);
-        for (int sg = 0; sg < nseg; ++sg) {
-            const int b = sg & 1;
-            if (sg + 1 < nseg) {
-                stage((sg + 1) * kTileSeg, b ^ 1);
-                cp_async_wait<1>();
-            } else {
-                cp_async_wait<0>();
-            }
-            __syncthreads();
-            const int j0 = sg * kTileSeg;
-            const int jend = j0 + kTileSeg;
-            const double *wb = win + (size_t)b * kTileSeg * ZC + lane;
-            const int32_t *cb = wcol + b * kTileSeg;
-            if (live) {
-                for (;;) {
-                    if (pos == 4) {
-                        if (e >= e_end) break;
-                        refill();
+        auto fetch = [&](Batch &bt) {
+            bt.nb = 0;
+#pragma unroll
+            for (int q = 0; q < B; ++q) {
+                bt.gb[q] = -1;
+                bt.zb[q] = 0;
+                bt.sq[q] = 0;
+                // skip the other producers' positions
+                while (it < items && seq % kTileProducers != pw) {
+                    ++seq;
+                    if (++g == g1) {
+                        it += gridDim.x;
+                        load_item();
                     }
-                    int done = 4;
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        if (u >= pos && done == 4) {
-                            const int l = lb[u];
-                            if (l >= jend) {
-                                done = u;
-                            } else {
-                                const int jl = l - j0;
-                                const int32_t c = cb[jl];
-                                if constexpr (ALIGNED) {
-                                    while (c >= thr[0]) {
-#pragma unroll
-                                        for (int s = 0; s < KZ; ++s) { fold(s); ++jb[s]; }
-                                        thr[0] = (int32_t)__ldg(A.sbounds + jb[0] + 1);
-                                    }
-                                } else {
-#pragma unroll
-                                    for (int s = 0; s < KZ; ++s) {
-                                        while (c >= thr[s]) {
-                                            fold(s);
-                                            ++jb[s];
-                                            thr[s] = (int32_t)((__ldg(A.bounds + jb[s] + 1) - (z0 + lane + 16 * s) + D - 1) / D);
-                                        }
-                                    }
-                                }
-                                const double v = vb[u];
-#pragma unroll
-                                for (int s = 0; s < KZ; ++s) seg[s] = rn_add(seg[s], rn_mul(v, wb[jl * ZC + 16 * s]));
-                            }
-                        }
+                }
+                if (it < items) {
+                    bt.gb[q] = g;
+                    bt.zb[q] = z0;
+                    bt.sq[q] = seq;
+                    ++bt.nb;
+                    ++seq;
+                    if (++g == g1) {
+                        it += gridDim.x;
+                        load_item();
                     }
-                    if (done < 4) { pos = done; break; }
-                    pos = 4;
                 }
             }
-            __syncthreads();  // buffer b is restaged two windows later
-        }
-        if (live) {
+            int64_t mine = -1;
 #pragma unroll
-            for (int s = 0; s < KZ; ++s) {
-                for (; jb[s] < A.nb; ++jb[s]) fold(s);
-                epi(srow * D + z0 + lane + 16 * s, acc[s]);
+            for (int q = 0; q < B; ++q)
+                if (lane == q) mine = bt.gb[q];
+            bt.m_eb = 0; bt.m_nj = 0; bt.m_ne = 0;
+            if (mine >= 0) {
+                bt.m_eb = T.seg_ent[mine];
+                bt.m_nj = T.seg_nj[mine];
+                bt.m_ne = (T.seg_row[mine * 24 + 16] + 15) & ~15;
+            }
+#pragma unroll
+            for (int q = 0; q < B; ++q) bt.col[q] = bt.gb[q] >= 0 ? __ldg(T.uni + bt.gb[q] * kTileSeg + lane) : 0;
+        };
+        Batch cur, nxt;
+        fetch(cur);
+        while (cur.nb > 0) {
+            fetch(nxt);
+#pragma unroll
+            for (int q = 0; q < B; ++q) {
+                if (q >= cur.nb) break;
+                const int64_t eb = __shfl_sync(0xffffffffu, cur.m_eb, q);
+                const int nj = __shfl_sync(0xffffffffu, cur.m_nj, q);
+                const int ne = __shfl_sync(0xffffffffu, cur.m_ne, q);
+                const int k = (int)(cur.sq[q] % kTileStages);
+                const uint32_t round = (uint32_t)(cur.sq[q] / kTileStages);
+                if (round > 0) mbar_wait(&empty[k], (round - 1) & 1);
+                const int njp = (nj + 3) & ~3;
+                unsigned char *sb = slot(k);
+                const uint32_t bytes = (uint32_t)(nj * ZC * 8 + njp * 4 + ne * (int)sizeof(V) + ne + 48);
+                if (lane == 0) mbar_arrive_expect_tx(&full[k], bytes);
+                __syncwarp();
+                if (lane < nj)
+                    bulk_g2s(sb + (size_t)lane * ZC * 8, A.vec + (int64_t)cur.col[q] * D + cur.zb[q], ZC * 8, &full[k]);
+                if (lane == 0 && njp > 0) bulk_g2s(sb + ST::win, T.uni + cur.gb[q] * kTileSeg, njp * 4, &full[k]);
+                if (lane == 1 && ne > 0)
+                    bulk_g2s(sb + ST::win + ST::col, reinterpret_cast<const V *>(T.val) + eb, ne * sizeof(V), &full[k]);
+                if (lane == 2 && ne > 0) bulk_g2s(sb + ST::win + ST::col + ST::val, T.loc + eb, ne, &full[k]);
+                if (lane == 3)
+                    bulk_g2s(sb + ST::win + ST::col + ST::val + ST::loc, T.seg_row + cur.gb[q] * 24, 48, &full[k]);
+                __syncwarp();
+            }
+            cur = nxt;
+        }
+    } else {
+        // ---------------- consumers: tile row = warp, slices z0 + lane + 32 s ----------------
+        constexpr int KZ = kTileKZ;
+        constexpr int NH = 1;
+        int k = 0;
+        uint32_t round = 0;
+        for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+            const int64_t t = it % T.ntiles, ch = it / T.ntiles;
+            const int32_t zl = (int32_t)ch * ZC + lane;
+            const int64_t r0 = T.tile_ptr[t], nr = T.tile_ptr[t + 1] - r0;
+            const int64_t g0 = T.seg_ptr[t], g1 = T.seg_ptr[t + 1];
+            double seg[NH][KZ], acc[NH][KZ];
+            int32_t thr[NH][KZ], tmin[NH];
+            int jb[NH][KZ];
+            int64_t srow[NH];
+            bool live[NH];
+#pragma unroll
+            for (int h = 0; h < NH; ++h) {
+                const int rr = warp + 16 * h;
+                live[h] = rr < nr;
+                srow[h] = live[h] ? T.tile_rows[r0 + rr] : 0;
+#pragma unroll
+                for (int s = 0; s < KZ; ++s) {
+                    const int32_t z = zl + 32 * s;
+                    seg[h][s] = 0.0;
+                    acc[h][s] = (RESID && live[h]) ? A.y[srow[h] * D + z] : 0.0;
+                    jb[h][s] = 0;
+                    if constexpr (ALIGNED) thr[h][s] = (int32_t)__ldg(A.sbounds + 1);
+                    else thr[h][s] = (int32_t)((__ldg(A.bounds + 1) - z + D - 1) / D);
+                }
+                tmin[h] = thr[h][0];
+#pragma unroll
+                for (int s = 1; s < KZ; ++s) tmin[h] = thr[h][s] < tmin[h] ? thr[h][s] : tmin[h];
+            }
+            auto fold = [&](int h, int s) {
+                if constexpr (RESID) acc[h][s] = rn_sub(acc[h][s], seg[h][s]);
+                else acc[h][s] = (jb[h][s] == 0) ? seg[h][s] : rn_add(acc[h][s], seg[h][s]);
+                seg[h][s] = 0.0;
+            };
+            for (int64_t g = g0; g < g1; ++g) {
+                mbar_wait(&full[k], round & 1);
+                const unsigned char *sb = slot(k);
+                const double *w = reinterpret_cast<const double *>(sb) + lane;
+                const int32_t *cols = reinterpret_cast<const int32_t *>(sb + ST::win);
+                const V *vals = reinterpret_cast<const V *>(sb + ST::win + ST::col);
+                const uint8_t *locs = sb + ST::win + ST::col + ST::val;
+                const uint16_t *ro = reinterpret_cast<const uint16_t *>(sb + ST::win + ST::col + ST::val + ST::loc);
+#pragma unroll
+                for (int h = 0; h < NH; ++h) {
+                    if (!live[h]) continue;
+                    const int rr = warp + 16 * h;
+                    const int e1 = ro[rr + 1];
+                    for (int e = ro[rr]; e < e1; ++e) {
+                        const int l = locs[e];
+                        const int32_t c = cols[l];
+                        if constexpr (ALIGNED) {
+                            while (c >= thr[h][0]) {
+#pragma unroll
+                                for (int s = 0; s < KZ; ++s) { fold(h, s); ++jb[h][s]; }
+                                thr[h][0] = (int32_t)__ldg(A.sbounds + jb[h][0] + 1);
+                            }
+                        } else if (c >= tmin[h]) {
+                            // one compare against the smallest threshold guards all slices
+#pragma unroll
+                            for (int s = 0; s < KZ; ++s) {
+                                while (c >= thr[h][s]) {
+                                    fold(h, s);
+                                    ++jb[h][s];
+                                    thr[h][s] = (int32_t)((__ldg(A.bounds + jb[h][s] + 1) - (zl + 32 * s) + D - 1) / D);
+                                }
+                            }
+                            tmin[h] = thr[h][0];
+#pragma unroll
+                            for (int s = 1; s < KZ; ++s) tmin[h] = thr[h][s] < tmin[h] ? thr[h][s] : tmin[h];
+                        }
+                        const double v = (double)vals[e];
+                        const double *wl = w + l * ZC;
+#pragma unroll
+                        for (int s = 0; s < KZ; ++s) seg[h][s] = rn_add(seg[h][s], rn_mul(v, wl[32 * s]));
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[k]);
+                if (++k == kTileStages) { k = 0; ++round; }
+            }
+#pragma unroll
+            for (int h = 0; h < NH; ++h) {
+                if (!live[h]) continue;
+#pragma unroll
+                for (int s = 0; s < KZ; ++s) {
+                    for (; jb[h][s] < A.nb; ++jb[h][s]) fold(h, s);
+                    epi(srow[h] * D + zl + 32 * s, acc[h][s]);
+                }
             }
         }
     }
@@ -413,7 +507,7 @@ __global__ void __launch_bounds__(kThreads, 2) stacked_tile_kernel(Stk<V> A, Stk
         epi.flush(v);
         block_sum<Epi::K>(v, sm);
         if (threadIdx.x == 0 && part != nullptr)
-            for (int k = 0; k < Epi::K; ++k) part[(size_t)blockIdx.x * Epi::K + k] = v[k];
+            for (int q = 0; q < Epi::K; ++q) part[(size_t)blockIdx.x * Epi::K + q] = v[q];
     }
     if (blockIdx.x == 0 && threadIdx.x == 0 && cnt != nullptr) cnt[0] = gridDim.x;
 }

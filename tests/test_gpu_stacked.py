@@ -138,7 +138,7 @@ def test_stacked_device_generator_matches_host(M):
     assert d.layout(slice_major=True).size == d.op.shape[1]
 
 
-@pytest.mark.parametrize("depth,m", [(32, 4), (64, 16), (96, 3)])
+@pytest.mark.parametrize("depth,m", [(128, 4), (256, 16), (128, 3)])
 def test_tile_staged_products_bit_exact(M, depth, m):
     """Tile-staged stacked products (shared-memory windows over each tile's distinct
     columns) equal the untiled kernel and the oracle bit for bit."""
@@ -171,7 +171,7 @@ def test_tile_staged_products_bit_exact(M, depth, m):
 def test_tile_staged_run_bit_exact(M):
     """Device-generated stacked operator with tiles (the configs[4] path): run == oracle."""
     blockops, problems, solvers, spectral, tv = M
-    n, depth, ang, nb = 12, 32, 10, 17
+    n, depth, ang, nb = 8, 128, 6, 11
     op = blockops.BlockOperator.from_parallel_beam(n, ang, nb, 4, 4, dtype=np.float32, depth=depth, tiles=True)
     a2 = problems.parallel_beam_matrix(n, ang, nb, dtype=np.float32)
     a = _expanded(a2, depth)

@@ -21,7 +21,7 @@ def main():
     ap.add_argument("--depth", type=int, default=256)
     ap.add_argument("--reps", type=int, default=5)
     a = ap.parse_args()
-    op = blockops.BlockOperator.from_parallel_beam(a.n, 360 * a.n // 256, (363 * a.n // 256) | 1, 16, 16,
+    op = blockops.BlockOperator.from_parallel_beam(a.n, 360 * a.n // 256, (363 * a.n // 256) | 1, 16, 16, tiles=not os.environ.get("STK_NO_TILES"),
                                                    dtype=np.float32, depth=a.depth)
     rows, cols = op.shape
     x = torch.rand(cols, dtype=torch.float64, device="cuda")
