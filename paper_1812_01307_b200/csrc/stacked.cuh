@@ -247,7 +247,7 @@ __global__ void __launch_bounds__(kThreads, (ALIGNED || Epi::K == 4) ? 4 : 3) st
 // ---------------------------------------------------------------------------
 constexpr int kTileRows = 16;      // rows per tile
 constexpr int kTileSeg = 32;       // union columns per segment
-constexpr int kTileStages = 4;     // ring depth
+constexpr int kTileStages = 6;     // ring depth
 constexpr int kTileSegEnt = kTileRows * kTileSeg;  // entries per segment, upper bound
 constexpr int kTileKZ = 4;         // slices per lane
 constexpr int kTileZC = 32 * kTileKZ;  // slices per item
@@ -458,15 +458,15 @@ __global__ void __launch_bounds__(kStkTileThreads, 1) stacked_tile_kernel(Stk<V>
                     if (!live[h]) continue;
                     const int rr = warp + 16 * h;
                     const int e1 = ro[rr + 1];
-                    for (int e = ro[rr]; e < e1; ++e) {
-                        const int l = locs[e];
-                        const int32_t c = cols[l];
+                    // block-boundary test of one entry (stored column c), then its products
+                    auto cross = [&](int32_t c) {
                         if constexpr (ALIGNED) {
                             while (c >= thr[h][0]) {
 #pragma unroll
                                 for (int s = 0; s < KZ; ++s) { fold(h, s); ++jb[h][s]; }
                                 thr[h][0] = (int32_t)__ldg(A.sbounds + jb[h][0] + 1);
                             }
+                            tmin[h] = thr[h][0];
                         } else if (c >= tmin[h]) {
                             // one compare against the smallest threshold guards all slices
 #pragma unroll
@@ -481,6 +481,36 @@ __global__ void __launch_bounds__(kStkTileThreads, 1) stacked_tile_kernel(Stk<V>
 #pragma unroll
                             for (int s = 1; s < KZ; ++s) tmin[h] = thr[h][s] < tmin[h] ? thr[h][s] : tmin[h];
                         }
+                    };
+                    int e = ro[rr];
+                    // pairs: both entries' shared-memory reads first; entries ascend, so
+                    // when the second is below every threshold the first is too
+                    for (; e + 1 < e1; e += 2) {
+                        const int l0 = locs[e], l1 = locs[e + 1];
+                        const int32_t c0 = cols[l0], c1 = cols[l1];
+                        const double v0 = (double)vals[e], v1 = (double)vals[e + 1];
+                        const double *w0 = w + l0 * ZC, *w1 = w + l1 * ZC;
+                        double x0[KZ], x1[KZ];
+#pragma unroll
+                        for (int s = 0; s < KZ; ++s) { x0[s] = w0[32 * s]; x1[s] = w1[32 * s]; }
+                        if (c1 < (ALIGNED ? thr[h][0] : tmin[h])) {
+#pragma unroll
+                            for (int s = 0; s < KZ; ++s) {
+                                seg[h][s] = rn_add(seg[h][s], rn_mul(v0, x0[s]));
+                                seg[h][s] = rn_add(seg[h][s], rn_mul(v1, x1[s]));
+                            }
+                        } else {
+                            cross(c0);
+#pragma unroll
+                            for (int s = 0; s < KZ; ++s) seg[h][s] = rn_add(seg[h][s], rn_mul(v0, x0[s]));
+                            cross(c1);
+#pragma unroll
+                            for (int s = 0; s < KZ; ++s) seg[h][s] = rn_add(seg[h][s], rn_mul(v1, x1[s]));
+                        }
+                    }
+                    if (e < e1) {
+                        const int l = locs[e];
+                        cross(cols[l]);
                         const double v = (double)vals[e];
                         const double *wl = w + l * ZC;
 #pragma unroll
