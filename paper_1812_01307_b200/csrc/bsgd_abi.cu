@@ -188,8 +188,7 @@ struct bsgd_plan {
         int64_t *tile_ptr = nullptr, *seg_ptr = nullptr, *seg_uni = nullptr, *seg_ent = nullptr;
         int32_t *tile_rows = nullptr, *seg_nj = nullptr, *uni = nullptr;
         uint16_t *seg_row = nullptr;
-        uint8_t *loc = nullptr;
-        void *val = nullptr;
+        void *ent = nullptr;
         size_t bytes = 0;
     } sf, stt;
     bool stacked() const { return depth > 1; }
@@ -197,7 +196,7 @@ struct bsgd_plan {
 
 static void stk_tiles_free(bsgd_plan::StkTileStore &t) {
     cudaFree(t.tile_ptr); cudaFree(t.seg_ptr); cudaFree(t.seg_uni); cudaFree(t.seg_ent); cudaFree(t.tile_rows);
-    cudaFree(t.seg_nj); cudaFree(t.uni); cudaFree(t.seg_row); cudaFree(t.loc); cudaFree(t.val);
+    cudaFree(t.seg_nj); cudaFree(t.uni); cudaFree(t.seg_row); cudaFree(t.ent);
     t = bsgd_plan::StkTileStore();
 }
 
@@ -667,7 +666,7 @@ static int launch_stk_tile(const Stk<V> &A, const bsgd_plan::StkTileStore &S, co
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr_set = true;
     }
-    StkTiles T{S.ntiles, S.tile_ptr, S.tile_rows, S.seg_ptr, S.seg_nj, S.seg_ent, S.seg_row, S.uni, S.loc, S.val};
+    StkTiles T{S.ntiles, S.tile_ptr, S.tile_rows, S.seg_ptr, S.seg_nj, S.seg_ent, S.seg_row, S.uni, S.ent};
     int occ = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kStkTileThreads, smem);
     const int64_t items = S.ntiles * (A.D / kTileZC);
@@ -940,6 +939,8 @@ static int build_stk_tiles(bsgd_plan *p, bool tr, int64_t ntiles, const int64_t 
                            cudaStream_t st) {
     const int64_t nrows = tr ? p->scols : p->srows, nnz = p->snnz;
     if (tptr[0] != 0) return fail(BSGD_EINVAL, "tile_ptr must start at 0");
+    if ((tr ? p->srows : p->scols) >= ((int64_t)1 << 24))
+        return fail(BSGD_EINVAL, "tile-staged products need fewer than 2^24 stored columns");
     const int64_t ntr = tptr[ntiles];
     if (ntr != nrows) return fail(BSGD_EINVAL, "tiles must cover every stored row exactly once (%lld of %lld)",
                                   (long long)ntr, (long long)nrows);
@@ -968,6 +969,7 @@ static int build_stk_tiles(bsgd_plan *p, bool tr, int64_t ntiles, const int64_t 
         std::vector<std::array<uint16_t, 24>> rows;
         std::vector<uint8_t> loc;   // per segment, padded to 16
         std::vector<V> val;
+        std::vector<int32_t> col;
         std::vector<int64_t> ent;   // per segment entry offset inside this tile's arrays
     };
     std::vector<TileOut> outs(ntiles);
@@ -1004,12 +1006,13 @@ static int build_stk_tiles(bsgd_plan *p, bool tr, int64_t ntiles, const int64_t 
                             const int64_t pos = std::lower_bound(cols.begin() + j0, cols.begin() + j1, idx[cur[i]]) - cols.begin();
                             o.loc.push_back((uint8_t)(pos - j0));
                             o.val.push_back(val[cur[i]]);
+                            o.col.push_back(idx[cur[i]]);
                             ++cur[i];
                             ++n;
                         }
                     }
                     for (int64_t i = nrt; i <= kTileRows; ++i) ro[i] = (uint16_t)n;
-                    while (o.loc.size() % 16) { o.loc.push_back(0); o.val.push_back((V)0); }
+                    while (o.loc.size() % 16) { o.loc.push_back(0); o.val.push_back((V)0); o.col.push_back(0); }
                     o.rows.push_back(ro);
                     o.nj.push_back((int32_t)(j1 - j0));
                 }
@@ -1028,8 +1031,7 @@ static int build_stk_tiles(bsgd_plan *p, bool tr, int64_t ntiles, const int64_t 
     std::vector<int64_t> seg_uni(nseg_all), seg_ent(nseg_all);
     std::vector<int32_t> seg_nj(nseg_all), uni((size_t)std::max<int64_t>(nseg_all, 1) * kTileSeg, 0);
     std::vector<uint16_t> seg_row((size_t)nseg_all * 24);
-    std::vector<uint8_t> loc(std::max<int64_t>(nent, 16));
-    std::vector<V> pval(std::max<int64_t>(nent, 16));
+    std::vector<TileEnt<V>> ents(std::max<int64_t>(nent, 16));
     int64_t eo = 0;
     for (int64_t t = 0; t < ntiles; ++t) {
         const TileOut &o = outs[t];
@@ -1044,8 +1046,10 @@ static int build_stk_tiles(bsgd_plan *p, bool tr, int64_t ntiles, const int64_t 
             std::copy(o.uni.begin() + src, o.uni.begin() + src + nj, uni.begin() + g * kTileSeg);
             src += nj;
         }
-        std::copy(o.loc.begin(), o.loc.end(), loc.begin() + eo);
-        std::copy(o.val.begin(), o.val.end(), pval.begin() + eo);
+        for (size_t q = 0; q < o.loc.size(); ++q) {
+            ents[eo + q].val = o.val[q];
+            ents[eo + q].cl = (uint32_t)o.col[q] << 8 | o.loc[q];
+        }
         eo += (int64_t)o.loc.size();
     }
     std::vector<int32_t> trows32(ntr);
@@ -1067,8 +1071,7 @@ static int build_stk_tiles(bsgd_plan *p, bool tr, int64_t ntiles, const int64_t 
     if (e == cudaSuccess) e = up((void **)&N.seg_ent, seg_ent.data(), sizeof(int64_t) * nseg_all);
     if (e == cudaSuccess) e = up((void **)&N.seg_row, seg_row.data(), sizeof(uint16_t) * seg_row.size());
     if (e == cudaSuccess) e = up((void **)&N.uni, uni.data(), sizeof(int32_t) * uni.size());
-    if (e == cudaSuccess) e = up((void **)&N.loc, loc.data(), loc.size());
-    if (e == cudaSuccess) e = up(&N.val, pval.data(), sizeof(V) * pval.size());
+    if (e == cudaSuccess) e = up(&N.ent, ents.data(), sizeof(TileEnt<V>) * ents.size());
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) {
         stk_tiles_free(N);

@@ -237,7 +237,7 @@ __global__ void __launch_bounds__(kThreads, (ALIGNED || Epi::K == 4) ? 4 : 3) st
 // the tile's columns cut into segments of kTileSeg columns, and per segment the
 // tile rows' entries that fall in it (row-major, uint8 position in the segment
 // + value).  Warp-specialised CTA: one producer warp walks the CTA's stream of
-// (tile, slice chunk, segment) stages and fills a kTileStages-deep ring with
+// (tile, slice chunk, segment) stages and fills a tile_stages()-deep ring with
 // TMA bulk copies -- one 256-byte vector row per distinct column (instead of
 // one gather per entry), the column ids, the entries -- completing on a
 // full-barrier per slot; eight consumer warps (two tile rows each, one slice
@@ -247,7 +247,9 @@ __global__ void __launch_bounds__(kThreads, (ALIGNED || Epi::K == 4) ? 4 : 3) st
 // ---------------------------------------------------------------------------
 constexpr int kTileRows = 16;      // rows per tile
 constexpr int kTileSeg = 32;       // union columns per segment
-constexpr int kTileStages = 6;     // ring depth
+// ring depth (227 KB of shared memory per CTA: 6 stages with float values, 5 with double)
+template <typename V>
+__host__ __device__ constexpr int tile_stages() { return sizeof(V) == 4 ? 6 : 5; }
 constexpr int kTileSegEnt = kTileRows * kTileSeg;  // entries per segment, upper bound
 constexpr int kTileKZ = 4;         // slices per lane
 constexpr int kTileZC = 32 * kTileKZ;  // slices per item
@@ -263,23 +265,28 @@ struct StkTiles {
     const int64_t *seg_ent;    // [segments] first entry (multiple of 16)
     const uint16_t *seg_row;   // [segments][24] cumulative entry counts per tile row ([16] = total, padded)
     const int32_t *uni;        // [segments][kTileSeg] distinct stored columns, per tile ascending (padded)
-    const uint8_t *loc;        // entry -> column position in its segment
-    const void *val;           // entry values (V)
+    const void *ent;           // TileEnt<V> records, per segment padded to 16
+};
+
+// one entry: value and (stored column << 8 | position in the segment), one
+// shared-memory read per entry
+template <typename V>
+struct alignas(sizeof(V) == 4 ? 8 : 16) TileEnt {
+    V val;
+    uint32_t cl;
 };
 
 template <typename V>
 struct TileStage {
     static constexpr size_t win = sizeof(double) * kTileSeg * kTileZC;
-    static constexpr size_t col = sizeof(int32_t) * kTileSeg;
-    static constexpr size_t val = sizeof(V) * kTileSegEnt;
-    static constexpr size_t loc = kTileSegEnt;
+    static constexpr size_t ent = sizeof(TileEnt<V>) * kTileSegEnt;
     static constexpr size_t row = 48;
-    static constexpr size_t bytes = win + col + val + loc + row;
+    static constexpr size_t bytes = win + ent + row;
 };
 
 template <typename V>
-constexpr size_t stk_tile_smem() {
-    return TileStage<V>::bytes * kTileStages + 2 * kTileStages * sizeof(uint64_t);
+__host__ __device__ constexpr size_t stk_tile_smem() {
+    return TileStage<V>::bytes * tile_stages<V>() + 2 * tile_stages<V>() * sizeof(uint64_t);
 }
 
 template <typename V, bool RESID, bool ALIGNED, class Epi>
@@ -287,6 +294,7 @@ __global__ void __launch_bounds__(kStkTileThreads, 1) stacked_tile_kernel(Stk<V>
                                                                         int64_t *cnt) {
     using ST = TileStage<V>;
     constexpr int ZC = kTileZC;
+    constexpr int kTileStages = tile_stages<V>();
     extern __shared__ __align__(128) unsigned char smraw[];
     __shared__ double sm[4 * 18];
     uint64_t *full = reinterpret_cast<uint64_t *>(smraw + ST::bytes * kTileStages);
@@ -389,19 +397,16 @@ __global__ void __launch_bounds__(kStkTileThreads, 1) stacked_tile_kernel(Stk<V>
                 const int k = (int)(cur.sq[q] % kTileStages);
                 const uint32_t round = (uint32_t)(cur.sq[q] / kTileStages);
                 if (round > 0) mbar_wait(&empty[k], (round - 1) & 1);
-                const int njp = (nj + 3) & ~3;
                 unsigned char *sb = slot(k);
-                const uint32_t bytes = (uint32_t)(nj * ZC * 8 + njp * 4 + ne * (int)sizeof(V) + ne + 48);
+                const uint32_t bytes = (uint32_t)(nj * ZC * 8 + ne * (int)sizeof(TileEnt<V>) + 48);
                 if (lane == 0) mbar_arrive_expect_tx(&full[k], bytes);
                 __syncwarp();
                 if (lane < nj)
                     bulk_g2s(sb + (size_t)lane * ZC * 8, A.vec + (int64_t)cur.col[q] * D + cur.zb[q], ZC * 8, &full[k]);
-                if (lane == 0 && njp > 0) bulk_g2s(sb + ST::win, T.uni + cur.gb[q] * kTileSeg, njp * 4, &full[k]);
                 if (lane == 1 && ne > 0)
-                    bulk_g2s(sb + ST::win + ST::col, reinterpret_cast<const V *>(T.val) + eb, ne * sizeof(V), &full[k]);
-                if (lane == 2 && ne > 0) bulk_g2s(sb + ST::win + ST::col + ST::val, T.loc + eb, ne, &full[k]);
-                if (lane == 3)
-                    bulk_g2s(sb + ST::win + ST::col + ST::val + ST::loc, T.seg_row + cur.gb[q] * 24, 48, &full[k]);
+                    bulk_g2s(sb + ST::win, reinterpret_cast<const TileEnt<V> *>(T.ent) + eb, ne * sizeof(TileEnt<V>),
+                             &full[k]);
+                if (lane == 3) bulk_g2s(sb + ST::win + ST::ent, T.seg_row + cur.gb[q] * 24, 48, &full[k]);
                 __syncwarp();
             }
             cur = nxt;
@@ -449,10 +454,8 @@ __global__ void __launch_bounds__(kStkTileThreads, 1) stacked_tile_kernel(Stk<V>
                 mbar_wait(&full[k], round & 1);
                 const unsigned char *sb = slot(k);
                 const double *w = reinterpret_cast<const double *>(sb) + lane;
-                const int32_t *cols = reinterpret_cast<const int32_t *>(sb + ST::win);
-                const V *vals = reinterpret_cast<const V *>(sb + ST::win + ST::col);
-                const uint8_t *locs = sb + ST::win + ST::col + ST::val;
-                const uint16_t *ro = reinterpret_cast<const uint16_t *>(sb + ST::win + ST::col + ST::val + ST::loc);
+                const TileEnt<V> *ents = reinterpret_cast<const TileEnt<V> *>(sb + ST::win);
+                const uint16_t *ro = reinterpret_cast<const uint16_t *>(sb + ST::win + ST::ent);
 #pragma unroll
                 for (int h = 0; h < NH; ++h) {
                     if (!live[h]) continue;
@@ -486,9 +489,10 @@ __global__ void __launch_bounds__(kStkTileThreads, 1) stacked_tile_kernel(Stk<V>
                     // pairs: both entries' shared-memory reads first; entries ascend, so
                     // when the second is below every threshold the first is too
                     for (; e + 1 < e1; e += 2) {
-                        const int l0 = locs[e], l1 = locs[e + 1];
-                        const int32_t c0 = cols[l0], c1 = cols[l1];
-                        const double v0 = (double)vals[e], v1 = (double)vals[e + 1];
+                        const TileEnt<V> r0 = ents[e], r1 = ents[e + 1];
+                        const int l0 = r0.cl & 255, l1 = r1.cl & 255;
+                        const int32_t c0 = (int32_t)(r0.cl >> 8), c1 = (int32_t)(r1.cl >> 8);
+                        const double v0 = (double)r0.val, v1 = (double)r1.val;
                         const double *w0 = w + l0 * ZC, *w1 = w + l1 * ZC;
                         double x0[KZ], x1[KZ];
 #pragma unroll
@@ -509,9 +513,10 @@ __global__ void __launch_bounds__(kStkTileThreads, 1) stacked_tile_kernel(Stk<V>
                         }
                     }
                     if (e < e1) {
-                        const int l = locs[e];
-                        cross(cols[l]);
-                        const double v = (double)vals[e];
+                        const TileEnt<V> r = ents[e];
+                        const int l = r.cl & 255;
+                        cross((int32_t)(r.cl >> 8));
+                        const double v = (double)r.val;
                         const double *wl = w + l * ZC;
 #pragma unroll
                         for (int s = 0; s < KZ; ++s) seg[h][s] = rn_add(seg[h][s], rn_mul(v, wl[32 * s]));

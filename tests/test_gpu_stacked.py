@@ -138,13 +138,14 @@ def test_stacked_device_generator_matches_host(M):
     assert d.layout(slice_major=True).size == d.op.shape[1]
 
 
-@pytest.mark.parametrize("depth,m", [(128, 4), (256, 16), (128, 3)])
-def test_tile_staged_products_bit_exact(M, depth, m):
+@pytest.mark.parametrize("depth,m,dt", [(128, 4, np.float32), (256, 16, np.float32), (128, 3, np.float32),
+                                        (128, 5, np.float64)])
+def test_tile_staged_products_bit_exact(M, depth, m, dt):
     """Tile-staged stacked products (shared-memory windows over each tile's distinct
     columns) equal the untiled kernel and the oracle bit for bit."""
     blockops, problems = M[0], M[1]
     n, ang, nb = 12, 10, 17
-    a2 = problems.parallel_beam_matrix(n, ang, nb, dtype=np.float32)
+    a2 = problems.parallel_beam_matrix(n, ang, nb, dtype=dt)
     a = _expanded(a2, depth)
     part = blockops.make_partition(a.shape[0], a.shape[1], m, m)
     plain = blockops.BlockOperator.stacked(a2, depth, part)
