@@ -187,3 +187,36 @@ def test_tile_staged_run_bit_exact(M):
     prm = orc.Params(mu=cfg.mu, lam=0.01, epochs=5, seed=3, max_inner_iters=10, tol=1e-5)
     ref = orc.run_bsgd(oop, y, prm, x_true=x_true, perm=np.arange(a.shape[1]), hw=(n, n, depth))
     assert np.array_equal(tr.final_x, ref.final_x)
+
+
+def test_tile_staged_irregular_tiles_and_empty_rows(M):
+    """Random row groupings (tiles of 1..16 rows, any order), empty rows and columns,
+    and a partition whose bounds are not multiples of D: still bit-exact."""
+    blockops = M[0]
+    rng = np.random.default_rng(11)
+    r2, c2, depth = 90, 70, 128
+    dense = (rng.random((r2, c2)) < 0.08) * rng.standard_normal((r2, c2))
+    dense[[3, 17, 40], :] = 0.0          # empty rows
+    dense[:, [0, 5, 66]] = 0.0           # empty columns
+    a2 = sparse.csr_array(dense.astype(np.float32))
+    a2.eliminate_zeros()
+    a = _expanded(a2, depth)
+    part = blockops.make_partition(a.shape[0], a.shape[1], 7, 5)
+    op = blockops.BlockOperator.stacked(a2, depth, part)
+
+    def random_tiles(n):
+        perm = rng.permutation(n)
+        sizes, tot = [], 0
+        while tot < n:
+            k = int(min(n - tot, rng.integers(1, 17)))
+            sizes.append(k)
+            tot += k
+        return np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64), perm.astype(np.int64)
+
+    op.set_stacked_tiles(False, random_tiles(r2))
+    op.set_stacked_tiles(True, random_tiles(c2))
+    oop = orc.OracleOperator(a, 7, 5)
+    x = rng.standard_normal(a.shape[1])
+    r = rng.standard_normal(a.shape[0])
+    assert np.array_equal(op.matvec(x), oop.matvec(x))
+    assert np.array_equal(op.rmatvec(r), oop.rmatvec(r))
