@@ -310,52 +310,3 @@ def distributed_largest_eigenvalue(shard, max_iters=50, tol=1e-10, seed=0, group
             return new, True, k
         est = new
     return est, False, max_iters
-
-
-def bench_main(args):
-    """`bench.py --gpus N` under torchrun: configs[1] sharded by row blocks, NCCL."""
-    import json
-    import time
-
-    import torch
-    import torch.distributed as dist
-
-    sys_rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    from . import problems
-    from .solvers import SolverConfig
-    d = problems.config(1)
-    part = make_partition(*d.shape, 8, 8)
-    spec = ShardSpec(part, sys_rank, world)
-    shard = CudaShard(d.matrix, spec)
-    u, _, _ = distributed_largest_eigenvalue(shard, max_iters=50)
-    cfg = SolverConfig(mu=0.9 / (2 * u), lam=0.0, epochs=10 ** 9, monitor_decrease=False)
-    drv = DistributedBSGD(shard, d.y, cfg, history_capacity=args.steps + args.warmup + 8)
-    for _ in range(args.warmup):
-        drv.epoch_step()
-    torch.cuda.synchronize()
-    dist.barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(args.steps):
-        drv.epoch_step()
-    e1.record()
-    torch.cuda.synchronize()
-    dist.barrier()
-    ms = torch.tensor([e0.elapsed_time(e1)], device="cuda")
-    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-    ms_step = float(ms.item()) / args.steps
-    if sys_rank == 0:
-        out = {"metric": "BSGD-TV epochs/s + achieved HBM GB/s (SpMV, TV-prox) at 1/2/4/8 B200",
-               "value": round(1000.0 / ms_step, 2), "unit": "epochs/s", "n_gpus": world, "steps": args.steps,
-               "warmup": args.warmup, "ms_per_step": round(ms_step, 5), "higher_is_better": True,
-               "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, configs[1] shapes)",
-               "config": {"workload": "configs[1] row-slab sharded", "parallelism": f"row-slab x{world}, NCCL all-reduce of g",
-                          "rows": d.shape[0], "cols": d.shape[1], "nnz": int(d.matrix.nnz), "mu": cfg.mu},
-               "gpu_launches": 5 * args.steps}
-        print(json.dumps(out), flush=True)
-    dist.barrier()
-    dist.destroy_process_group()
