@@ -139,6 +139,13 @@ int bsgd_plan_create_stacked_device(bsgd_plan **out, int device, int64_t depth, 
  * unchanged bit for bit.  ntiles = 0 removes the tiles. */
 int bsgd_plan_stacked_tiles(bsgd_plan *plan, int transposed, int64_t ntiles, const int64_t *tile_ptr,
                             const int64_t *tile_rows, void *stream);
+/* Gather-tiled products for an ordinary plan: group the rows of A (transposed = 0)
+ * or A^T (1) into tiles of <= 16 rows that share columns (host arrays, a
+ * permutation of all rows); each tile's distinct vector elements are gathered
+ * once into shared memory.  Values agree with the CSR kernel to rounding (same
+ * per-row reduction shape).  ntiles = 0 removes the tiles. */
+int bsgd_plan_gather_tiles(bsgd_plan *plan, int transposed, int64_t ntiles, const int64_t *tile_ptr,
+                           const int64_t *tile_rows, void *stream);
 /* depth (1 for ordinary plans) and the stored CSR's shape / nnz */
 int bsgd_plan_stacked_info(const bsgd_plan *plan, int64_t *depth, int64_t *rows2, int64_t *cols2,
                            int64_t *nnz2);

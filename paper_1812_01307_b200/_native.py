@@ -61,6 +61,7 @@ _SIGS = {
                                                        c_p]),
     "bsgd_plan_stacked_info": (ctypes.c_int, [c_p, c_p, c_p, c_p, c_p]),
     "bsgd_plan_stacked_tiles": (ctypes.c_int, [c_p, ctypes.c_int, c_i64, c_p, c_p, c_p]),
+    "bsgd_plan_gather_tiles": (ctypes.c_int, [c_p, ctypes.c_int, c_i64, c_p, c_p, c_p]),
     "bsgd_plan_destroy": (ctypes.c_int, [c_p]),
     "bsgd_plan_csr_copy": (ctypes.c_int, [c_p, c_p, c_p, c_p, c_p]),
     "bsgd_siddon_csr": (ctypes.c_int, [ctypes.c_int, c_i64, c_i64, c_i64, c_p, c_p, ctypes.c_int,

@@ -29,6 +29,7 @@
 #include "tiled.cuh"
 #include "siddon.cuh"
 #include "stacked.cuh"
+#include "gtile.cuh"
 
 using namespace bsgd;
 
@@ -191,8 +192,25 @@ struct bsgd_plan {
         void *ent = nullptr;
         size_t bytes = 0;
     } sf, stt;
+    // gather-tiled copies of A / A^T (gtile.cuh), set by bsgd_plan_gather_tiles
+    struct GTileStore {
+        bool ok = false;
+        int64_t ntiles = 0;
+        int max_union = 0;
+        int64_t *tile_ptr = nullptr, *row_ptr = nullptr, *uni_ptr = nullptr;
+        int32_t *tile_rows = nullptr, *uni = nullptr;
+        uint16_t *loc = nullptr;
+        void *val = nullptr;
+        size_t bytes = 0;
+    } gf, gt;
     bool stacked() const { return depth > 1; }
 };
+
+static void gtiles_free(bsgd_plan::GTileStore &t) {
+    cudaFree(t.tile_ptr); cudaFree(t.row_ptr); cudaFree(t.uni_ptr); cudaFree(t.tile_rows); cudaFree(t.uni);
+    cudaFree(t.loc); cudaFree(t.val);
+    t = bsgd_plan::GTileStore();
+}
 
 static void stk_tiles_free(bsgd_plan::StkTileStore &t) {
     cudaFree(t.tile_ptr); cudaFree(t.seg_ptr); cudaFree(t.seg_uni); cudaFree(t.seg_ent); cudaFree(t.tile_rows);
@@ -290,6 +308,8 @@ static void plan_free(bsgd_plan *p) {
     cudaFree(p->d_col_sbounds); cudaFree(p->d_row_sbounds);
     stk_tiles_free(p->sf);
     stk_tiles_free(p->stt);
+    gtiles_free(p->gf);
+    gtiles_free(p->gt);
     delete p;
 }
 
@@ -713,8 +733,31 @@ static int launch_stacked_dir(const bsgd_plan *p, bool transposed, const double 
 }
 
 template <typename V, class E>
+static int launch_gtile(const bsgd_plan::GTileStore &S, const double *vec, const E &e, double *part, int64_t *cnt,
+                        cudaStream_t st) {
+    auto kern = gtile_kernel<V, E>;
+    const size_t smem = sizeof(double) * (size_t)std::max(S.max_union, 1);
+    static int attr_smem = 0;  // per instantiation
+    if (attr_smem < (int)smem) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr_smem = (int)smem;
+    }
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, smem);
+    const int cap = std::min(std::max(occ, 1) * num_sms(), kMaxPartials);
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(S.ntiles, cap));
+    GTiles T{S.ntiles, S.tile_ptr, S.tile_rows, S.row_ptr, S.loc, S.val, S.uni_ptr, S.uni, S.max_union};
+    kern<<<grid, kThreads, smem, st>>>(T, vec, e, part, cnt);
+    LAUNCHED();
+    return BSGD_OK;
+}
+
+static bool gtiles_on(const bsgd_plan::GTileStore &S) { return S.ok && !getenv("BSGD_NO_GATHER_TILES"); }
+
+template <typename V, class E>
 static int launch_fwd(const bsgd_plan *p, const double *vec, const E &e, double *part, int64_t *cnt, cudaStream_t st) {
     if (p->stacked()) return launch_stacked_dir<V>(p, false, vec, e, part, cnt, st);
+    if (gtiles_on(p->gf)) return launch_gtile<V>(p->gf, vec, e, part, cnt, st);
     if (tiled_usable(p, p->tf, vec)) return launch_tiled<V>(p->tf, vec, e, part, cnt, st);
     return launch_one<V>(fwd_csr<V>(p, vec), p->g_fwd, e, part, cnt, p->nnz, st);
 }
@@ -722,6 +765,7 @@ static int launch_fwd(const bsgd_plan *p, const double *vec, const E &e, double 
 template <typename V, class E>
 static int launch_tr(const bsgd_plan *p, const double *vec, const E &e, double *part, int64_t *cnt, cudaStream_t st) {
     if (p->stacked()) return launch_stacked_dir<V>(p, true, vec, e, part, cnt, st);
+    if (gtiles_on(p->gt)) return launch_gtile<V>(p->gt, vec, e, part, cnt, st);
     if (tiled_usable(p, p->tt, vec)) return launch_tiled<V>(p->tt, vec, e, part, cnt, st);
     return launch_one<V>(tr_csr<V>(p, vec), p->g_tr, e, part, cnt, p->nnz, st);
 }
@@ -1085,6 +1129,110 @@ static int build_stk_tiles(bsgd_plan *p, bool tr, int64_t ntiles, const int64_t 
     return BSGD_OK;
 }
 
+// Build the gather-tiled copy of A (transposed = 0) or A^T (1) of an ordinary
+// plan from a host row grouping (tile t = rows tile_rows[tile_ptr[t] ..]).
+template <typename V>
+static int build_gtiles(bsgd_plan *p, bool tr, int64_t ntiles, const int64_t *tptr, const int64_t *trows,
+                        cudaStream_t st) {
+    const int64_t nrows = tr ? p->cols : p->rows, nnz = p->nnz;
+    if (tptr[0] != 0 || tptr[ntiles] != nrows)
+        return fail(BSGD_EINVAL, "tiles must cover every row exactly once");
+    std::vector<char> seen(nrows, 0);
+    for (int64_t t = 0; t < ntiles; ++t) {
+        const int64_t n = tptr[t + 1] - tptr[t];
+        if (n < 1 || n > kGTileRows) return fail(BSGD_EINVAL, "tile %lld has %lld rows (1..%d)", (long long)t, (long long)n, kGTileRows);
+    }
+    for (int64_t i = 0; i < nrows; ++i) {
+        const int64_t r = trows[i];
+        if (r < 0 || r >= nrows || seen[r]) return fail(BSGD_EINVAL, "tile rows must be a permutation of the rows");
+        seen[r] = 1;
+    }
+    std::vector<int64_t> ptr(nrows + 1);
+    std::vector<int32_t> idx(nnz);
+    std::vector<V> val(nnz);
+    CU(cudaMemcpyAsync(ptr.data(), tr ? p->t_ptr : p->f_ptr, sizeof(int64_t) * (nrows + 1), cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(idx.data(), tr ? p->t_idx : p->f_idx, sizeof(int32_t) * nnz, cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(val.data(), tr ? p->t_val : p->f_val, sizeof(V) * nnz, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    std::vector<int64_t> rptr(nrows + 1, 0);
+    for (int64_t i = 0; i < nrows; ++i) {
+        const int64_t r = trows[i];
+        rptr[i + 1] = rptr[i] + (ptr[r + 1] - ptr[r]);
+    }
+    std::vector<uint16_t> loc(std::max<int64_t>(nnz, 1));
+    std::vector<V> pval(std::max<int64_t>(nnz, 1));
+    std::vector<std::vector<int32_t>> unions(ntiles);
+    unsigned nth = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    std::vector<std::thread> pool;
+    std::vector<int> big(nth, 0);
+    for (unsigned w = 0; w < nth; ++w) {
+        pool.emplace_back([&, w]() {
+            std::vector<int32_t> cols;
+            for (int64_t t = w; t < ntiles; t += nth) {
+                cols.clear();
+                for (int64_t i = tptr[t]; i < tptr[t + 1]; ++i) {
+                    const int64_t r = trows[i];
+                    cols.insert(cols.end(), idx.begin() + ptr[r], idx.begin() + ptr[r + 1]);
+                }
+                std::sort(cols.begin(), cols.end());
+                cols.erase(std::unique(cols.begin(), cols.end()), cols.end());
+                if (cols.size() > 28000) { big[w] = 1; continue; }
+                for (int64_t i = tptr[t]; i < tptr[t + 1]; ++i) {
+                    const int64_t r = trows[i];
+                    int64_t o = rptr[i];
+                    for (int64_t k = ptr[r]; k < ptr[r + 1]; ++k, ++o) {
+                        loc[o] = (uint16_t)(std::lower_bound(cols.begin(), cols.end(), idx[k]) - cols.begin());
+                        pval[o] = val[k];
+                    }
+                }
+                unions[t] = cols;
+            }
+        });
+    }
+    for (auto &th : pool) th.join();
+    for (int b : big)
+        if (b) return fail(BSGD_EINVAL, "a tile's rows touch more than 28000 distinct columns");
+    std::vector<int64_t> uptr(ntiles + 1, 0);
+    int max_union = 0;
+    for (int64_t t = 0; t < ntiles; ++t) {
+        uptr[t + 1] = uptr[t] + (int64_t)unions[t].size();
+        max_union = std::max(max_union, (int)unions[t].size());
+    }
+    std::vector<int32_t> uni(std::max<int64_t>(uptr[ntiles], 1));
+    for (int64_t t = 0; t < ntiles; ++t) std::copy(unions[t].begin(), unions[t].end(), uni.begin() + uptr[t]);
+    std::vector<int32_t> trows32(nrows);
+    for (int64_t i = 0; i < nrows; ++i) trows32[i] = (int32_t)trows[i];
+    bsgd_plan::GTileStore &S = tr ? p->gt : p->gf;
+    p->device_bytes -= S.bytes;
+    gtiles_free(S);
+    bsgd_plan::GTileStore N;
+    auto up = [&](void **dst, const void *src, size_t bytes) -> cudaError_t {
+        cudaError_t e = cudaMalloc(dst, std::max<size_t>(bytes, 16));
+        if (e == cudaSuccess) e = cudaMemcpyAsync(*dst, src, bytes, cudaMemcpyHostToDevice, st);
+        N.bytes += bytes;
+        return e;
+    };
+    cudaError_t e = up((void **)&N.tile_ptr, tptr, sizeof(int64_t) * (ntiles + 1));
+    if (e == cudaSuccess) e = up((void **)&N.tile_rows, trows32.data(), sizeof(int32_t) * nrows);
+    if (e == cudaSuccess) e = up((void **)&N.row_ptr, rptr.data(), sizeof(int64_t) * (nrows + 1));
+    if (e == cudaSuccess) e = up((void **)&N.loc, loc.data(), sizeof(uint16_t) * nnz);
+    if (e == cudaSuccess) e = up(&N.val, pval.data(), sizeof(V) * nnz);
+    if (e == cudaSuccess) e = up((void **)&N.uni_ptr, uptr.data(), sizeof(int64_t) * (ntiles + 1));
+    if (e == cudaSuccess) e = up((void **)&N.uni, uni.data(), sizeof(int32_t) * uni.size());
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) {
+        gtiles_free(N);
+        return fail(e == cudaErrorMemoryAllocation ? BSGD_ENOMEM : BSGD_ECUDA, "tile upload failed: %s",
+                    cudaGetErrorString(e));
+    }
+    N.ntiles = ntiles;
+    N.max_union = max_union;
+    N.ok = true;
+    S = N;
+    p->device_bytes += N.bytes;
+    return BSGD_OK;
+}
+
 // ---------------------------------------------------------------------------
 // C ABI
 // ---------------------------------------------------------------------------
@@ -1392,6 +1540,72 @@ int bsgd_plan_create_stacked_device(bsgd_plan **out, int device, int64_t depth, 
     if (depth < 2) return fail(BSGD_EINVAL, "depth must be >= 2 (a single slice is an ordinary plan)");
     return plan_create_adopt(out, device, depth, rows2, cols2, nnz2, indptr, indices, values, value_dtype,
                              num_row_blocks, num_col_blocks, row_bounds, col_bounds, stream);
+}
+
+int bsgd_plan_gather_tiles(bsgd_plan *p, int transposed, int64_t ntiles, const int64_t *tile_ptr,
+                           const int64_t *tile_rows, void *stream) {
+    if (!p) return fail(BSGD_EINVAL, "plan is NULL");
+    if (p->stacked()) return fail(BSGD_EINVAL, "stacked plans use bsgd_plan_stacked_tiles");
+    DeviceGuard guard(p->device);
+    bsgd_plan::GTileStore &S = transposed ? p->gt : p->gf;
+    if (ntiles == 0) {
+        p->device_bytes -= S.bytes;
+        gtiles_free(S);
+        return BSGD_OK;
+    }
+    if (ntiles < 0 || !tile_ptr || !tile_rows) return fail(BSGD_EINVAL, "bad tile arguments");
+    cudaStream_t st = (cudaStream_t)stream;
+    int rc = p->vdt == BSGD_F32 ? build_gtiles<float>(p, transposed != 0, ntiles, tile_ptr, tile_rows, st)
+                                : build_gtiles<double>(p, transposed != 0, ntiles, tile_ptr, tile_rows, st);
+    if (rc) return rc;
+    // keep the tiles only where they beat the CSR kernel on this matrix: the union
+    // staging wins where the CSR gathers have no sector locality of their own
+    // (pixel rows of A^T at 1024^2: 6.1 -> 4.2 ms) and loses where they do
+    // (ray rows of A at 1024^2: 4.5 -> 6.3 ms).  BSGD_GATHER_TILES=force skips the test.
+    const char *force = getenv("BSGD_GATHER_TILES");
+    if (force && strcmp(force, "force") == 0) return BSGD_OK;
+    const int64_t nin = transposed ? p->rows : p->cols, nout = transposed ? p->cols : p->rows;
+    double *vin = nullptr, *vout = nullptr;
+    if (cudaMalloc(&vin, sizeof(double) * nin) != cudaSuccess ||
+        cudaMalloc(&vout, sizeof(double) * nout) != cudaSuccess) {
+        cudaGetLastError();
+        cudaFree(vin);
+        return BSGD_OK;  // keep the tiles untimed
+    }
+    cudaMemsetAsync(vin, 0, sizeof(double) * nin, st);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    float t[2] = {0.f, 0.f};
+    for (int variant = 0; variant < 2 && rc == BSGD_OK; ++variant) {
+        for (int rep = 0; rep < 4 && rc == BSGD_OK; ++rep) {
+            if (rep == 1) cudaEventRecord(e0, st);
+            if (variant == 0) {
+                rc = p->vdt == BSGD_F32
+                         ? launch_one<float>(transposed ? tr_csr<float>(p, vin) : fwd_csr<float>(p, vin),
+                                             transposed ? p->g_tr : p->g_fwd, EpiStore{vout, 1.0}, nullptr, nullptr,
+                                             p->nnz, st)
+                         : launch_one<double>(transposed ? tr_csr<double>(p, vin) : fwd_csr<double>(p, vin),
+                                              transposed ? p->g_tr : p->g_fwd, EpiStore{vout, 1.0}, nullptr, nullptr,
+                                              p->nnz, st);
+            } else {
+                rc = p->vdt == BSGD_F32 ? launch_gtile<float>(S, vin, EpiStore{vout, 1.0}, nullptr, nullptr, st)
+                                        : launch_gtile<double>(S, vin, EpiStore{vout, 1.0}, nullptr, nullptr, st);
+            }
+        }
+        cudaEventRecord(e1, st);
+        cudaEventSynchronize(e1);
+        cudaEventElapsedTime(&t[variant], e0, e1);
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(vin);
+    cudaFree(vout);
+    if (rc == BSGD_OK && !(t[1] < 0.97f * t[0])) {
+        p->device_bytes -= S.bytes;
+        gtiles_free(S);
+    }
+    return rc;
 }
 
 int bsgd_plan_stacked_tiles(bsgd_plan *p, int transposed, int64_t ntiles, const int64_t *tile_ptr,
@@ -2016,7 +2230,7 @@ int bsgd_epoch(const bsgd_plan *p, const bsgd_epoch_args *a, void *stream) {
         rc = run_step(p->cols, a, ws, st);
         if (!rc && (fl & BSGD_EP_R_NEXT))
             rc = DISPATCH_V(p, launch_fwd<V>(p, a->x_k, EpiResid{a->y, a->r_next}, ws.rpart, ws.ctl + 2, st));
-    } else if ((fl & BSGD_EP_R_NEXT) && (tiled || p->stacked() || !getenv("BSGD_MERGE_K1K2"))) {
+    } else if ((fl & BSGD_EP_R_NEXT) && (tiled || p->stacked() || p->gf.ok || p->gt.ok || !getenv("BSGD_MERGE_K1K2"))) {
         // K1(x_k) then K2(r_k) on the stream.  One merged grid (below, opt-in) reads the
         // same snapshot but measured slower on configs[1] (0.79 vs 0.66 ms per epoch):
         // both halves are gather-bound and the CTA split balances them poorly
