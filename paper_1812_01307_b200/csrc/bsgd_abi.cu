@@ -732,11 +732,11 @@ static int launch_stacked_dir(const bsgd_plan *p, bool transposed, const double 
     }
 }
 
-template <typename V, class E>
-static int launch_gtile(const bsgd_plan::GTileStore &S, const double *vec, const E &e, double *part, int64_t *cnt,
-                        cudaStream_t st) {
-    auto kern = gtile_kernel<V, E>;
-    const size_t smem = sizeof(double) * (size_t)std::max(S.max_union, 1);
+template <typename V, bool DB, class E>
+static int launch_gtile_k(const bsgd_plan::GTileStore &S, const double *vec, const E &e, double *part, int64_t *cnt,
+                          cudaStream_t st) {
+    auto kern = gtile_kernel<V, DB, E>;
+    const size_t smem = (DB ? 2 : 1) * sizeof(double) * (size_t)std::max(S.max_union, 1);
     static int attr_smem = 0;  // per instantiation
     if (attr_smem < (int)smem) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -750,6 +750,14 @@ static int launch_gtile(const bsgd_plan::GTileStore &S, const double *vec, const
     kern<<<grid, kThreads, smem, st>>>(T, vec, e, part, cnt);
     LAUNCHED();
     return BSGD_OK;
+}
+
+// double-buffered windows while two of them fit three CTAs per SM
+template <typename V, class E>
+static int launch_gtile(const bsgd_plan::GTileStore &S, const double *vec, const E &e, double *part, int64_t *cnt,
+                        cudaStream_t st) {
+    if (2 * sizeof(double) * (size_t)S.max_union <= 72 * 1024) return launch_gtile_k<V, true>(S, vec, e, part, cnt, st);
+    return launch_gtile_k<V, false>(S, vec, e, part, cnt, st);
 }
 
 static bool gtiles_on(const bsgd_plan::GTileStore &S) { return S.ok && !getenv("BSGD_NO_GATHER_TILES"); }
