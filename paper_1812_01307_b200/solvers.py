@@ -244,6 +244,8 @@ class SolverState:
         self._host_reads = False    # x / r_vec read back since the last epoch
         self._spec = None           # readback started during the last epoch (see _speculative_epoch)
         self._side = None
+        self._pending_r = None      # pinned host r_vec assigned, copy deferred (see r_vec.setter)
+        self._copy = None
         self._g = t.zeros(cols, **f64)
         self._z = None              # explicit z cache (N, rows) once the stochastic path ran
         self._z_explicit = False
@@ -324,12 +326,31 @@ class SolverState:
 
     @property
     def r_vec(self) -> np.ndarray:
+        self._flush_r()
         return self._read("r", self._r[self._ri])
 
     @r_vec.setter
     def r_vec(self, value) -> None:
+        # A pinned, contiguous float64 array (what the getters hand out) is copied
+        # lazily: a full-pass epoch moves it over PCIe while K1, which does not
+        # read r_k, runs, and waits for the copy before it returns, so the caller
+        # may reuse the array afterwards exactly as with an eager copy.
+        t = nat.torch()
+        self._pending_r = None
+        if not isinstance(value, t.Tensor):
+            arr = np.asarray(value)
+            if (arr.dtype == np.float64 and arr.shape == (self._rows,) and arr.flags.c_contiguous
+                    and t.from_numpy(arr).is_pinned()):
+                self._pending_r = arr
+                self._touch()
+                return
         self._from_host(self._r[self._ri], value, self._rows)
         self._touch()
+
+    def _flush_r(self) -> None:
+        if self._pending_r is not None:
+            arr, self._pending_r = self._pending_r, None
+            self._from_host(self._r[self._ri], arr, self._rows)
 
     @property
     def g(self) -> np.ndarray:
@@ -381,6 +402,7 @@ class SolverState:
 
     @property
     def r_device(self):
+        self._flush_r()
         return self._r[self._ri]
 
     @property
@@ -517,15 +539,20 @@ def bsgd_tv_iteration(state: SolverState, op: BlockOperator, y, cfg: SolverConfi
             flags |= nat.EP_R_NEXT
         op._charge(2 * op.nnz)
     else:
+        state._flush_r()
         _pair_products(state, op, pairs, y_dev, xi, ri)
         flags |= nat.EP_SKIP_GRAD
     mu = state.mu_eff
-    speculate = (state._host_reads and full and not monitor and bool(flags & nat.EP_R_NEXT)
-                 and not (flags & nat.EP_LOOKAHEAD))
+    split = full and not monitor and bool(flags & nat.EP_R_NEXT) and not (flags & nat.EP_LOOKAHEAD)
+    speculate = state._host_reads and split
+    pending_r = state._pending_r if split else None
+    if pending_r is None:
+        state._flush_r()
+    state._pending_r = None
     state._host_reads = False
     state._touch()
-    if speculate:
-        _speculative_epoch(state, cfg, layout, y_dev, xi, ri, flags, mu, ws)
+    if speculate or pending_r is not None:
+        _speculative_epoch(state, cfg, layout, y_dev, xi, ri, flags, mu, ws, pending_r, speculate)
     else:
         args = _epoch_args(state, cfg, layout, y_dev, xi, ri, flags, mu, ws)
         _launch(state, args)
@@ -561,14 +588,16 @@ def bsgd_tv_iteration(state: SolverState, op: BlockOperator, y, cfg: SolverConfi
 
 
 def _speculative_epoch(state: SolverState, cfg: SolverConfig, layout, y_dev, xi: int, ri: int, flags: int,
-                       mu: float, ws) -> None:
+                       mu: float, ws, pending_r=None, readback: bool = True) -> None:
     """The same epoch as one `bsgd_epoch` with R_NEXT, split so the host copies overlap it.
 
     The caller read x / r_vec back after the previous epoch, so it will again:
     K1 (r_next = y - A x_k, `bsgd_epoch_forward`) runs first and r_next starts
     streaming to pinned host memory on a side stream while K2, the step and the
     prox run; x_next follows as soon as it exists.  The getters hand these
-    buffers out (once) while the state version is unchanged.
+    buffers out (once) while the state version is unchanged.  An r_vec assigned
+    from pinned host memory (``pending_r``) crosses PCIe on a copy stream while
+    K1 runs; K2 waits for it.
     """
     t = nat.torch()
     dev = state._dev
@@ -578,29 +607,46 @@ def _speculative_epoch(state: SolverState, cfg: SolverConfig, layout, y_dev, xi:
     side = state._side
     args = _epoch_args(state, cfg, layout, y_dev, xi, ri, flags & ~nat.EP_R_NEXT, mu, ws)
     r_next, x_next = state._r[1 - ri], state._x[1 - xi]
+    copied = None
+    if pending_r is not None:
+        if state._copy is None:
+            state._copy = t.cuda.Stream(device=dev)
+        start = t.cuda.Event()
+        start.record(cur)   # work queued earlier may still read the r_k slot
+        with t.cuda.stream(state._copy):
+            state._copy.wait_event(start)
+            state._r[ri].copy_(t.from_numpy(pending_r), non_blocking=True)
+            copied = t.cuda.Event()
+            copied.record(state._copy)
     nat.call("bsgd_epoch_forward", state._op.plan, nat.ptr(state._x[xi]), nat.ptr(y_dev), nat.ptr(r_next),
              ctypes.byref(args), nat.stream_ptr(dev))
-    ev_r = t.cuda.Event()
-    ev_r.record(cur)
-    rh = t.empty(r_next.shape, dtype=t.float64, pin_memory=True)
-    with t.cuda.stream(side):
-        side.wait_event(ev_r)
-        rh.copy_(r_next, non_blocking=True)
-        done_r = t.cuda.Event()
-        done_r.record(side)
+    if readback:
+        ev_r = t.cuda.Event()
+        ev_r.record(cur)
+        rh = t.empty(r_next.shape, dtype=t.float64, pin_memory=True)
+        with t.cuda.stream(side):
+            side.wait_event(ev_r)
+            rh.copy_(r_next, non_blocking=True)
+            done_r = t.cuda.Event()
+            done_r.record(side)
+    if copied is not None:
+        cur.wait_event(copied)
     _launch(state, args)
-    ev_x = t.cuda.Event()
-    ev_x.record(cur)
-    xh = t.empty(x_next.shape, dtype=t.float64, pin_memory=True)
-    with t.cuda.stream(side):
-        side.wait_event(ev_x)
-        xh.copy_(x_next, non_blocking=True)
-        done_x = t.cuda.Event()
-        done_x.record(side)
-    # no wait on the main stream: the next epoch writes the other ring slots, and
-    # anything that does overwrite these (a setter, the epoch after next) bumps the
-    # state version first, so a copy it could race with is never handed out
-    state._spec_pending = {"x": (xh, done_x), "r": (rh, done_r)}
+    if readback:
+        ev_x = t.cuda.Event()
+        ev_x.record(cur)
+        xh = t.empty(x_next.shape, dtype=t.float64, pin_memory=True)
+        with t.cuda.stream(side):
+            side.wait_event(ev_x)
+            xh.copy_(x_next, non_blocking=True)
+            done_x = t.cuda.Event()
+            done_x.record(side)
+        # no wait on the main stream: the next epoch writes the other ring slots, and
+        # anything that does overwrite these (a setter, the epoch after next) bumps the
+        # state version first, so a copy it could race with is never handed out
+        state._spec_pending = {"x": (xh, done_x), "r": (rh, done_r)}
+    if copied is not None:
+        copied.synchronize()   # the caller may reuse its r_vec array from here on
 
 
 def _pair_products(state: SolverState, op: BlockOperator, pairs, y_dev, xi: int, ri: int) -> None:
@@ -644,6 +690,7 @@ class _GraphRunner:
     def capture(self, monitor: bool) -> bool:
         t = nat.torch()
         st = self.state
+        st._flush_r()
         ws = st._workspace(self.layout, self.cfg.lam)
         xi, ri = st._xi, st._ri
         args = [_epoch_args(st, self.cfg, self.layout, self.y_dev, (xi + e) % 2, (ri + e) % 2,

@@ -246,3 +246,42 @@ def test_host_readback_overlap_matches_plain_path(S):
             st.r_vec = np.zeros(op.shape[0])
             assert not st.r_vec.any()
     assert np.array_equal(runs[0][0], runs[1][0]) and np.array_equal(runs[0][1], runs[1][1])
+
+
+def test_deferred_r_vec_copy_matches_eager(S):
+    """An r_vec assigned from pinned host memory is copied during the next epoch
+    (overlapping K1); results equal an eager copy bit for bit, on both the split
+    full-pass path (x written each epoch) and the lookahead path."""
+    import torch as t
+    _, solvers, _ = S
+    z = load_golden("p3_ls")
+    for write_x in (True, False):
+        runs = []
+        for pinned in (False, True):
+            op, cfg, layout, _ = _setup(S, z)
+            st = solvers.init_bsgd_state(op, z["y"], cfg)
+            rows = op.shape[0]
+            buf = t.empty(rows, dtype=t.float64, pin_memory=True).numpy() if pinned else np.empty(rows)
+            for e in range(4):
+                if write_x:
+                    st.x = st.x
+                buf[:] = st.r_vec * (0.5 if e % 2 else 1.0)   # a perturbed residual cache
+                st.r_vec = buf
+                if pinned:
+                    assert st._pending_r is buf
+                solvers.bsgd_tv_iteration(st, op, z["y"], cfg, layout=layout)
+                assert st._pending_r is None
+                buf[:] = np.nan   # the caller reuses its array once the epoch returned
+            runs.append((st.x, st.r_vec, st.g))
+        for a, b in zip(*runs):
+            assert np.array_equal(a, b), write_x
+    # a pending value is visible to reads and to the device accessor
+    op, cfg, layout, _ = _setup(S, z)
+    st = solvers.init_bsgd_state(op, z["y"], cfg)
+    buf = t.empty(op.shape[0], dtype=t.float64, pin_memory=True).numpy()
+    buf[:] = 3.0
+    st.r_vec = buf
+    assert st._pending_r is buf
+    assert (st.r_vec == 3.0).all() and st._pending_r is None
+    st.r_vec = buf
+    assert (st.r_device.cpu().numpy() == 3.0).all()
