@@ -492,7 +492,10 @@ def run_ct_secondary(args, index):
            "monitor_decrease": False, "mean_fgp_iterations": round(fgp_iters, 2),
            "tv_prox": {"image": "x".join(str(v) for v in shape), "iterations": d.max_inner_iters,
                        "ms": round(pms, 4), "algorithmic_bytes": pbytes, "gbs": round(pbytes / (pms * 1e6), 1),
-                       "note": "fields are L2-resident at 2D sizes; bound by grid barriers / latency, not HBM"}}
+                       "note": ("fields are L2-resident at 2D sizes; bound by grid barriers / latency, not HBM"
+                                if dim == 2 else
+                                "fields stream from HBM (134 MB each); latency-bound at 16 warps/SM, "
+                                "profiles/r01_c5.md")}}
     if d.depth > 1:
         # stacked operator: two products per epoch, each applies every logical nonzero
         # once (a multiply and an add in float64) reading its vector value from L2
