@@ -261,6 +261,57 @@ int bsgd_epoch_reduce_forward(const bsgd_plan *plan, const bsgd_epoch_args *args
 int bsgd_epoch_tail(const bsgd_plan *plan, const bsgd_epoch_args *args, const double *fnext_dev,
                     void *stream);
 
+/* --- slab-decomposed TV prox (multi-GPU, SURVEY.md §8 e "Prox") ---------
+ * Replaces, on rank p of a multi-GPU run, the replicated prox inside
+ * bsgd_step: tv_prox (tv.py:172-255, 3-D: oracle tv_prox3) over the rank's
+ * voxels [offset, offset + count) of the C-order volume, with one-plane halos
+ * (height*width voxels in 3-D, width in 2-D) exchanged by the caller between
+ * passes.  Each pass that the FGP decisions need returns this slab's
+ * numpy-order partial sums; when the slabs are nodes of numpy's pairwise
+ * recursion over the whole volume the caller combines them in that order and
+ * every decision is bit-identical to bsgd_tv_prox / bsgd_tv_prox3
+ * (paper_1812_01307_b200/parallel.py: prox_slabs, pw_combine, SlabProx). */
+typedef struct bsgd_slab {
+    int64_t depth, height, width; /* global volume; depth 1 for an image */
+    int64_t offset, count;        /* own voxels, C order */
+    double weight;                /* prox weight w > 0 (mu * lam) */
+    int32_t parity;               /* dual buffer (0 / 1) holding p; the other holds c */
+    int32_t reserved;
+    void *workspace;              /* bsgd_slab_workspace_bytes, device */
+    size_t workspace_bytes;
+} bsgd_slab;
+
+#define BSGD_SLAB_SLOTS 12
+/* offsets_out[BSGD_SLAB_SLOTS] (doubles from the workspace start) of the local
+ * buffers, each count + 2*halo long and covering voxels
+ * [offset - halo, offset + count + halo):
+ *   [0] b   [1..3] dual buffer 0   [4..6] dual buffer 1   [7..9] q   [10] u
+ * (2-D: entries 3, 6 and 9 are -1); [11] = a 16-double slot for sums. */
+size_t bsgd_slab_workspace_bytes(int64_t depth, int64_t height, int64_t width, int64_t count);
+int bsgd_slab_layout(int64_t depth, int64_t height, int64_t width, int64_t count, int64_t *offsets_out,
+                     int64_t *halo_out);
+/* b = x_k + mu g on the own voxels (x_k, g: full-length vectors in volume order) */
+int bsgd_slab_step(const bsgd_slab *s, const double *x_k, const double *g, double mu, void *stream);
+/* p = q = 0 (halos included); sums_out[0..2) = np.sum(b*b), TV(b)  (needs b's lower halo) */
+int bsgd_slab_init(const bsgd_slab *s, double *sums_out, void *stream);
+/* c = proj(src + step grad(b + w div src)), src = p (from_p) or q  (needs src halos) */
+int bsgd_slab_candidate(const bsgd_slab *s, int32_t from_p, void *stream);
+/* q = c + beta (c - p); sums_out[0 .. 1 + 2*DIM) = phi, |c_k - p_k|^2, |c_k|^2  (needs c's upper halo) */
+int bsgd_slab_dual(const bsgd_slab *s, double beta, double *sums_out, void *stream);
+/* u = b + w div p  (needs p's upper halo) */
+int bsgd_slab_finalize(const bsgd_slab *s, void *stream);
+/* sums_out[0..2) = np.sum((u - b)^2), TV(u)  (needs u's lower halo) */
+int bsgd_slab_energy(const bsgd_slab *s, double *sums_out, void *stream);
+/* x_next = fell_back ? b : u on the own voxels; stats_out[4] = partial |x|^2,
+ * |x - x*|^2, (x - x_k).g, |x - x_k|^2 over them (x_true may be NULL) */
+int bsgd_slab_output(const bsgd_slab *s, int32_t fell_back, double *x_next, const double *x_k, const double *g,
+                     const double *x_true, double *stats_out, void *stream);
+/* hand a distributed step's results to bsgd_epoch_tail: the all-reduced
+ * statistics (device, 4 doubles) and the prox scalars */
+int bsgd_epoch_set_step(int64_t cols, const bsgd_epoch_args *args, const double *stats_dev, double tv,
+                        int32_t iterations, int32_t restarts, int32_t converged, int32_t fell_back,
+                        void *stream);
+
 #ifdef __cplusplus
 }
 #endif

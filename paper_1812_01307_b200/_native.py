@@ -33,6 +33,18 @@ class ProxInfoC(ctypes.Structure):
                 ("restarts", ctypes.c_int32), ("fell_back", ctypes.c_int32)]
 
 
+class SlabArgs(ctypes.Structure):
+    """bsgd_slab (include/bsgd_b200.h)."""
+    _fields_ = [
+        ("depth", c_i64), ("height", c_i64), ("width", c_i64), ("offset", c_i64), ("count", c_i64),
+        ("weight", ctypes.c_double), ("parity", ctypes.c_int32), ("reserved", ctypes.c_int32),
+        ("workspace", c_p), ("workspace_bytes", ctypes.c_size_t),
+    ]
+
+
+SLAB_SLOTS = 12
+
+
 class EpochArgs(ctypes.Structure):
     _fields_ = [
         ("x_k", c_p), ("r_k", c_p), ("y", c_p), ("g", c_p), ("x_next", c_p), ("r_next", c_p),
@@ -89,6 +101,17 @@ _SIGS = {
     "bsgd_tv_prox3": (ctypes.c_int, [c_i64, c_i64, c_i64, c_p, c_p, ctypes.c_double, ctypes.c_int32,
                                      ctypes.c_double, c_p, ctypes.c_size_t, c_p, c_p, c_p]),
     "bsgd_tv_value3": (ctypes.c_int, [c_i64, c_i64, c_i64, c_p, c_p, c_p, c_p]),
+    "bsgd_slab_workspace_bytes": (ctypes.c_size_t, [c_i64, c_i64, c_i64, c_i64]),
+    "bsgd_slab_layout": (ctypes.c_int, [c_i64, c_i64, c_i64, c_i64, c_p, c_p]),
+    "bsgd_slab_step": (ctypes.c_int, [ctypes.POINTER(SlabArgs), c_p, c_p, ctypes.c_double, c_p]),
+    "bsgd_slab_init": (ctypes.c_int, [ctypes.POINTER(SlabArgs), c_p, c_p]),
+    "bsgd_slab_candidate": (ctypes.c_int, [ctypes.POINTER(SlabArgs), ctypes.c_int32, c_p]),
+    "bsgd_slab_dual": (ctypes.c_int, [ctypes.POINTER(SlabArgs), ctypes.c_double, c_p, c_p]),
+    "bsgd_slab_finalize": (ctypes.c_int, [ctypes.POINTER(SlabArgs), c_p]),
+    "bsgd_slab_energy": (ctypes.c_int, [ctypes.POINTER(SlabArgs), c_p, c_p]),
+    "bsgd_slab_output": (ctypes.c_int, [ctypes.POINTER(SlabArgs), ctypes.c_int32, c_p, c_p, c_p, c_p, c_p, c_p]),
+    "bsgd_epoch_set_step": (ctypes.c_int, [c_i64, ctypes.POINTER(EpochArgs), c_p, ctypes.c_double, ctypes.c_int32,
+                                           ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, c_p]),
     "bsgd_discrete_gradient3": (ctypes.c_int, [c_i64, c_i64, c_i64, c_p, c_p, c_p, c_p, c_p]),
     "bsgd_discrete_divergence3": (ctypes.c_int, [c_i64, c_i64, c_i64, c_p, c_p, c_p, c_p, c_p]),
     "bsgd_dot": (ctypes.c_int, [c_i64, c_p, c_p, c_p, c_p, c_p]),

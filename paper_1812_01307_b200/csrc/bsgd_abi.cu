@@ -30,10 +30,11 @@
 #include "siddon.cuh"
 #include "stacked.cuh"
 #include "gtile.cuh"
+#include "slab.cuh"
 
 using namespace bsgd;
 
-#define BSGD_VERSION 110
+#define BSGD_VERSION 111
 
 // ---------------------------------------------------------------------------
 // errors
@@ -1244,6 +1245,98 @@ static int build_gtiles(bsgd_plan *p, bool tr, int64_t ntiles, const int64_t *tp
 // ---------------------------------------------------------------------------
 // C ABI
 // ---------------------------------------------------------------------------
+// ---------------------------------------------------------------------------
+// slab-decomposed prox (multi-GPU): workspace layout and launch helpers
+// ---------------------------------------------------------------------------
+constexpr int kSlabPartials = 8192;   // doubles: G <= 512 CTAs x K <= 7 sums, or G x 4 stats
+
+static int64_t slab_halo(int64_t depth, int64_t height, int64_t width) {
+    return depth > 1 ? height * width : width;
+}
+
+// offsets in doubles; returns the total size in doubles
+static int64_t slab_offsets(int64_t depth, int64_t height, int64_t width, int64_t count, int64_t *off) {
+    const int dim = depth > 1 ? 3 : 2;
+    const int64_t len = count + 2 * slab_halo(depth, height, width);
+    const int64_t stride = field_stride(len);
+    int64_t o = kSlabPartials + 32;   // partials, then the sums slot (16) and stats (16)
+    off[11] = kSlabPartials;
+    o += 96;
+    off[0] = o; o += stride;
+    for (int grp = 0; grp < 3; ++grp)
+        for (int k = 0; k < 3; ++k) {
+            if (k < dim) { off[1 + 3 * grp + k] = o; o += stride; }
+            else off[1 + 3 * grp + k] = -1;
+        }
+    off[10] = o; o += stride;
+    return o;
+}
+
+struct SlabCtx {
+    SlabView v;
+    double *part;
+    double *stats;
+    int dim;
+    int G;        // CTAs of the sum passes (power of two)
+    int grid;     // CTAs of the elementwise passes
+};
+
+static int slab_ctx(const bsgd_slab *s, SlabCtx &c, bool need_weight = true) {
+    if (!s) return fail(BSGD_EINVAL, "slab is NULL");
+    const int64_t D = s->depth < 1 ? 1 : s->depth;
+    if (s->height < 1 || s->width < 1) return fail(BSGD_EINVAL, "slab dimensions must be positive");
+    const int64_t N = D * s->height * s->width;
+    if (N >= ((int64_t)1 << 31)) return fail(BSGD_EINVAL, "volume too large (%lld voxels)", (long long)N);
+    if (s->offset < 0 || s->count < 1 || s->offset + s->count > N)
+        return fail(BSGD_EINVAL, "slab [%lld, +%lld) outside the volume", (long long)s->offset, (long long)s->count);
+    if (need_weight && !(s->weight > 0.0)) return fail(BSGD_EINVAL, "slab prox weight must be positive");
+    if (s->parity != 0 && s->parity != 1) return fail(BSGD_EINVAL, "parity must be 0 or 1");
+    int64_t off[BSGD_SLAB_SLOTS];
+    const int64_t total = slab_offsets(D, s->height, s->width, s->count, off);
+    if (!s->workspace || s->workspace_bytes < (size_t)total * sizeof(double))
+        return fail(BSGD_EINVAL, "slab workspace too small");
+    double *base = (double *)s->workspace;
+    const int64_t h = slab_halo(D, s->height, s->width);
+    // shifted so that ptr[p] addresses global voxel p (valid for p in [offset - h, offset + count + h))
+    auto at = [&](int slot) { return base + off[slot] + h - s->offset; };
+    c.dim = D > 1 ? 3 : 2;
+    ProxArgs &a = c.v.a;
+    a = ProxArgs{};
+    a.D = D; a.H = s->height; a.W = s->width; a.N = N;
+    a.b = at(0);
+    a.w = s->weight;
+    a.step = 1.0 / ((D > 1 ? 12.0 : 8.0) * s->weight);
+    const int pb = 1 + 3 * s->parity, cb = 1 + 3 * (1 - s->parity);
+    for (int k = 0; k < c.dim; ++k) {
+        a.f[k] = at(pb + k);
+        a.f[c.dim + k] = at(7 + k);
+        a.f[2 * c.dim + k] = at(cb + k);
+    }
+    c.v.u = at(10);
+    c.v.off = s->offset;
+    c.v.n = s->count;
+    int rc = pw_depth(s->count, &c.v.ds);
+    if (rc) return rc;
+    c.v.fast = (s->count % 128 == 0 && s->count / 128 == ((int64_t)1 << c.v.ds)) ? 1 : 0;
+    const int64_t S = (int64_t)1 << c.v.ds;
+    c.G = (int)std::min<int64_t>(S, 256);
+    const int64_t per_slot = c.v.fast ? 8 : kThreads / 8;
+    if (S / c.G > kPwMaxQ * per_slot) return fail(BSGD_EINVAL, "slab too large for the pairwise tree");
+    c.part = base;
+    c.stats = base + off[11] + 16;
+    c.grid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(s->count, kThreads), (int64_t)num_sms() * 8));
+    return BSGD_OK;
+}
+
+template <int K, class Kern>
+static int slab_sum_launch(const SlabCtx &c, Kern kern, size_t smem, double *out, cudaStream_t st) {
+    if (smem > 0) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kern<<<c.G, kThreads, smem, st>>>(c.v, c.part);
+    slab_top_kernel<K><<<1, kThreads, 0, st>>>(c.v.ds, c.G, c.part, out);
+    LAUNCHED();
+    return BSGD_OK;
+}
+
 extern "C" {
 
 const char *bsgd_last_error(void) { return g_err.c_str(); }
@@ -2302,6 +2395,145 @@ int bsgd_epoch_tail(const bsgd_plan *p, const bsgd_epoch_args *a, const double *
     if (rc) return rc;
     if (!a->history || !a->epoch_counter) return fail(BSGD_EINVAL, "history and epoch_counter are required");
     return run_tail(a, ws, fnext_dev ? 2 : 0, fnext_dev, (cudaStream_t)stream);
+}
+
+// ---- slab-decomposed prox (multi-GPU) ----
+size_t bsgd_slab_workspace_bytes(int64_t depth, int64_t height, int64_t width, int64_t count) {
+    if (height < 1 || width < 1 || count < 1) return 0;
+    int64_t off[BSGD_SLAB_SLOTS];
+    return sizeof(double) * (size_t)slab_offsets(depth < 1 ? 1 : depth, height, width, count, off);
+}
+
+int bsgd_slab_layout(int64_t depth, int64_t height, int64_t width, int64_t count, int64_t *offsets_out,
+                     int64_t *halo_out) {
+    if (height < 1 || width < 1 || count < 1 || !offsets_out || !halo_out) return fail(BSGD_EINVAL, "bad slab layout query");
+    slab_offsets(depth < 1 ? 1 : depth, height, width, count, offsets_out);
+    *halo_out = slab_halo(depth < 1 ? 1 : depth, height, width);
+    return BSGD_OK;
+}
+
+int bsgd_slab_step(const bsgd_slab *s, const double *x_k, const double *g, double mu, void *stream) {
+    SlabCtx c;
+    int rc = slab_ctx(s, c, false);
+    if (rc) return rc;
+    if (!x_k || !g) return fail(BSGD_EINVAL, "x_k and g are required");
+    slab_step_kernel<<<c.grid, kThreads, 0, (cudaStream_t)stream>>>(c.v, x_k, g, mu);
+    LAUNCHED();
+    return BSGD_OK;
+}
+
+int bsgd_slab_init(const bsgd_slab *s, double *sums_out, void *stream) {
+    SlabCtx c;
+    int rc = slab_ctx(s, c);
+    if (rc) return rc;
+    if (!sums_out) return fail(BSGD_EINVAL, "sums_out is NULL");
+    cudaStream_t st = (cudaStream_t)stream;
+    // p and q of both parities, halos included (tv.py:198-201)
+    const int64_t len = s->count + 2 * slab_halo(c.v.a.D, s->height, s->width);
+    int64_t off[BSGD_SLAB_SLOTS];
+    slab_offsets(c.v.a.D, s->height, s->width, s->count, off);
+    for (int slot = 1; slot <= 9; ++slot)
+        if (off[slot] >= 0) CU(cudaMemsetAsync((double *)s->workspace + off[slot], 0, sizeof(double) * len, st));
+    const size_t smem = sizeof(double) * 2 * 8 * 128;
+    if (c.dim == 3)
+        return c.v.fast ? slab_sum_launch<2>(c, slab_init_kernel<3, true>, smem, sums_out, st)
+                        : slab_sum_launch<2>(c, slab_init_kernel<3, false>, 0, sums_out, st);
+    return c.v.fast ? slab_sum_launch<2>(c, slab_init_kernel<2, true>, smem, sums_out, st)
+                    : slab_sum_launch<2>(c, slab_init_kernel<2, false>, 0, sums_out, st);
+}
+
+int bsgd_slab_candidate(const bsgd_slab *s, int32_t from_p, void *stream) {
+    SlabCtx c;
+    int rc = slab_ctx(s, c);
+    if (rc) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (c.dim == 3) slab_candidate_kernel<3><<<c.grid, kThreads, 0, st>>>(c.v, from_p ? 1 : 0);
+    else slab_candidate_kernel<2><<<c.grid, kThreads, 0, st>>>(c.v, from_p ? 1 : 0);
+    LAUNCHED();
+    return BSGD_OK;
+}
+
+int bsgd_slab_dual(const bsgd_slab *s, double beta, double *sums_out, void *stream) {
+    SlabCtx c;
+    int rc = slab_ctx(s, c);
+    if (rc) return rc;
+    if (!sums_out) return fail(BSGD_EINVAL, "sums_out is NULL");
+    cudaStream_t st = (cudaStream_t)stream;
+    if (c.dim == 3) {
+        const size_t smem = c.v.fast ? sizeof(double) * 7 * 8 * 128 : 0;
+        auto kern = c.v.fast ? slab_dual_kernel<3, true> : slab_dual_kernel<3, false>;
+        if (smem > 0) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        kern<<<c.G, kThreads, smem, st>>>(c.v, beta, c.part);
+        slab_top_kernel<7><<<1, kThreads, 0, st>>>(c.v.ds, c.G, c.part, sums_out);
+    } else {
+        const size_t smem = c.v.fast ? sizeof(double) * 5 * 8 * 128 : 0;
+        auto kern = c.v.fast ? slab_dual_kernel<2, true> : slab_dual_kernel<2, false>;
+        if (smem > 0) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        kern<<<c.G, kThreads, smem, st>>>(c.v, beta, c.part);
+        slab_top_kernel<5><<<1, kThreads, 0, st>>>(c.v.ds, c.G, c.part, sums_out);
+    }
+    LAUNCHED();
+    return BSGD_OK;
+}
+
+int bsgd_slab_finalize(const bsgd_slab *s, void *stream) {
+    SlabCtx c;
+    int rc = slab_ctx(s, c);
+    if (rc) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (c.dim == 3) slab_finalize_kernel<3><<<c.grid, kThreads, 0, st>>>(c.v);
+    else slab_finalize_kernel<2><<<c.grid, kThreads, 0, st>>>(c.v);
+    LAUNCHED();
+    return BSGD_OK;
+}
+
+int bsgd_slab_energy(const bsgd_slab *s, double *sums_out, void *stream) {
+    SlabCtx c;
+    int rc = slab_ctx(s, c);
+    if (rc) return rc;
+    if (!sums_out) return fail(BSGD_EINVAL, "sums_out is NULL");
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t smem = sizeof(double) * 2 * 8 * 128;
+    if (c.dim == 3)
+        return c.v.fast ? slab_sum_launch<2>(c, slab_energy_kernel<3, true>, smem, sums_out, st)
+                        : slab_sum_launch<2>(c, slab_energy_kernel<3, false>, 0, sums_out, st);
+    return c.v.fast ? slab_sum_launch<2>(c, slab_energy_kernel<2, true>, smem, sums_out, st)
+                    : slab_sum_launch<2>(c, slab_energy_kernel<2, false>, 0, sums_out, st);
+}
+
+int bsgd_slab_output(const bsgd_slab *s, int32_t fell_back, double *x_next, const double *x_k, const double *g,
+                     const double *x_true, double *stats_out, void *stream) {
+    SlabCtx c;
+    int rc = slab_ctx(s, c, false);
+    if (rc) return rc;
+    if (!x_next || !x_k || !g || !stats_out) return fail(BSGD_EINVAL, "x_next, x_k, g and stats_out are required");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int grid = std::min(c.grid, kSlabPartials / 4);
+    slab_output_kernel<<<grid, kThreads, 0, st>>>(c.v, fell_back ? 1 : 0, x_next, x_k, g, x_true, c.part);
+    slab_sum4_kernel<<<1, 32, 0, st>>>(c.part, grid, stats_out);
+    LAUNCHED();
+    return BSGD_OK;
+}
+
+__global__ void set_step_kernel(int64_t *ctl, double *xpart, double *scal, const double *stats, double tv,
+                                double iters, double restarts, double conv, double fell) {
+    if (threadIdx.x == 0) {
+        for (int k = 0; k < 4; ++k) xpart[k] = stats[k];
+        ctl[0] = 1;
+        scal[0] = tv; scal[1] = iters; scal[2] = restarts; scal[3] = conv; scal[4] = fell;
+    }
+}
+
+int bsgd_epoch_set_step(int64_t cols, const bsgd_epoch_args *a, const double *stats_dev, double tv,
+                        int32_t iterations, int32_t restarts, int32_t converged, int32_t fell_back, void *stream) {
+    Ws ws;
+    int rc = check_epoch_args(cols, a, &ws);
+    if (rc) return rc;
+    if (!stats_dev) return fail(BSGD_EINVAL, "stats_dev is NULL");
+    set_step_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(ws.ctl, ws.xpart, ws.scal, stats_dev, tv, iterations,
+                                                        restarts, converged, fell_back);
+    LAUNCHED();
+    return BSGD_OK;
 }
 
 }  // extern "C"

@@ -177,6 +177,19 @@ class CudaShard:
     def tail(self, args, fnext1):
         nat.call("bsgd_epoch_tail", self.op.plan, ctypes.byref(args), nat.ptr(fnext1), self.stream())
 
+    def prox_dims(self):
+        """(depth, height, width) of the prox volume, or None without a prox."""
+        if not self.hw[0]:
+            return None
+        return (max(1, int(getattr(self.layout, "depth", 1))), self.hw[0], self.hw[1])
+
+    def slab_backend(self, offset, count):
+        return CudaSlab(self.prox_dims(), offset, count, self.dev)
+
+    def set_step(self, args, stats, info):
+        nat.call("bsgd_epoch_set_step", self.cols, ctypes.byref(args), nat.ptr(stats), float(info["tv"]),
+                 info["iterations"], info["restarts"], info["converged"], info["fell_back"], self.stream())
+
     def dot(self, a, b, out1):
         scratch = self.t.empty(nat.SCRATCH_BYTES // 8, dtype=self.t.float64, device=self.dev)
         nat.call("bsgd_dot", a.numel(), nat.ptr(a), nat.ptr(b), nat.ptr(out1), nat.ptr(scratch), self.stream())
@@ -195,7 +208,11 @@ class DistributedBSGD:
     same layout as the single-GPU path (`BSGD_H_*`), replicated on every rank.
     """
 
-    def __init__(self, shard, y_full, cfg, x_true=None, group=None, history_capacity=1024):
+    def __init__(self, shard, y_full, cfg, x_true=None, group=None, history_capacity=1024, prox: str = "auto"):
+        """``prox``: "replicated" runs the whole prox on every rank (bsgd_step);
+        "slab" decomposes it over the ranks (SlabProx; needs an identity layout
+        and slabs at least one halo plane thick); "auto" takes "slab" on more
+        than one rank when it applies."""
         import torch.distributed as dist
         self.dist = dist
         self.group = group
@@ -226,6 +243,31 @@ class DistributedBSGD:
         if cfg.lam > 0 and shard.layout is not None and not shard.layout.is_identity:
             perm = shard.t.from_numpy(shard.layout.perm.astype(np.int64)).to(self.y.device)
         self.perm = perm
+        self.slab = None
+        self.slabs = None
+        if prox not in ("auto", "slab", "replicated"):
+            raise ValueError(f"unknown prox mode {prox!r}")
+        dims = shard.prox_dims() if (cfg.lam > 0 and hasattr(shard, "prox_dims")) else None
+        if dims is not None and prox != "replicated":
+            comm = TorchComm(group)
+            why = None
+            if not shard.layout.is_identity:
+                why = "slab prox needs an identity pixel layout"
+            else:
+                try:
+                    slabs = prox_slabs(int(np.prod(dims)), comm.world, dims[1] * dims[2] if dims[0] > 1 else dims[2])
+                except ValueError as e:
+                    why = str(e)
+            if why is None and (prox == "slab" or comm.world > 1):
+                lo, n = slabs[comm.rank]
+                self.slab = SlabProx(shard.slab_backend(lo, n), comm, slabs)
+                self.slabs = slabs
+                self.comm = comm
+            elif prox == "slab":
+                raise ValueError(why or "slab prox unavailable")
+        elif prox == "slab":
+            raise ValueError("slab prox needs lam > 0 and a layout")
+        self.prox_info = None
 
     def _allreduce(self, tensor):
         if self.dist.is_initialized() and self.dist.get_world_size(self.group) > 1:
@@ -246,8 +288,11 @@ class DistributedBSGD:
         args = s.args(x_k, self.g, x_next, self.mu, cfg, self.f_curr, self.hist, self.counter, self.perm,
                       self.x_true, flags)
         s.grad(r_k, self.g)                       # local 2 A_p^T r_p
-        self._allreduce(self.g)                   # g = sum_p
-        s.step(args)                              # x_next = prox(x_k + mu g), stats
+        if self.slab is None:
+            self._allreduce(self.g)               # g = sum_p
+            s.step(args)                          # x_next = prox(x_k + mu g), stats
+        else:
+            self._slab_step(args, x_k, x_next)
         s.forward(x_next, self.y, r_ahead, args)  # r_{k+2}[I_p] into the consumed r_k slot
         s.forward_sumsq(args, self.fnext)
         self._allreduce(self.fnext)               # f_next = sum_p ||r_p||^2
@@ -257,6 +302,19 @@ class DistributedBSGD:
         self.xi, self.ri = 1 - xi, 1 - ri
         self.epoch += 1.0
         return row
+
+    def _slab_step(self, args, x_k, x_next):
+        """x_next = prox(x_k + mu g) with the prox decomposed over the ranks."""
+        cfg = self.cfg
+        comm, slabs, be = self.comm, self.slabs, self.slab.be
+        comm.reduce_scatter(self.g, slabs)        # this rank's share of g = sum_p g_p
+        be.step(x_k, self.g, self.mu)             # b = x_k + mu g on the slab
+        info = self.slab.run(self.mu * cfg.lam, cfg.prox.max_inner_iters, cfg.prox.tol)
+        stats = be.output(info["fell_back"], x_next, x_k, self.g, self.x_true)
+        comm.allreduce(stats)
+        self.s.set_step(args, stats, info)
+        comm.allgather_slabs(x_next, slabs)       # the next forward product reads all of x
+        self.prox_info = info
 
     @property
     def x_current(self):
@@ -310,3 +368,292 @@ def distributed_largest_eigenvalue(shard, max_iters=50, tol=1e-10, seed=0, group
             return new, True, k
         est = new
     return est, False, max_iters
+
+
+# ---------------------------------------------------------------------------
+# slab-decomposed TV prox (SURVEY.md §8 e, "Prox")
+# ---------------------------------------------------------------------------
+#
+# With the replicated prox every rank runs the whole FGP; here rank p runs it
+# on its own voxels only.  Slabs are contiguous voxel ranges of the C-order
+# volume chosen as nodes of numpy's pairwise recursion over the whole volume
+# (`prox_slabs`), so the per-slab numpy-order sums combine in the recursion's
+# order (`pw_combine`) into exactly the values np.sum gives: every restart,
+# stop and fallback decision, and the result, are bit-identical to the
+# single-GPU prox (tv.py:172-255; 3-D: the oracle restatement).  Per FGP
+# iteration the exchange is one halo plane per neighbour for q and for c and
+# one all-gather of 1 + 2 DIM doubles.  The step x_k + mu g needs only the
+# rank's share of g (reduce-scatter instead of all-reduce) and the new x is
+# all-gathered for the next forward product.
+
+def _pw_split(n: int) -> int:
+    n2 = n // 2
+    return n2 - n2 % 8
+
+
+def prox_slabs(nvox: int, world: int, halo: int):
+    """Own voxel ranges (lo, count) per rank: nodes of numpy's pairwise recursion.
+
+    Starting from the root, the largest node (leftmost on ties) is split at
+    numpy's split point until there are ``world`` of them; for power-of-two
+    volumes and rank counts these are equal slabs.  Raises ValueError when a
+    node would have to split inside a pairwise leaf or a slab is thinner than
+    one halo plane (the exchange only reaches neighbouring ranks)."""
+    if world < 1:
+        raise ValueError("world size must be >= 1")
+    nodes = [(0, nvox)]
+    while len(nodes) < world:
+        k = max(range(len(nodes)), key=lambda i: (nodes[i][1], -i))
+        lo, n = nodes[k]
+        if n <= 128:
+            raise ValueError(f"cannot split a {nvox}-voxel volume into {world} pairwise nodes")
+        n2 = _pw_split(n)
+        nodes[k:k + 1] = [(lo, n2), (lo + n2, n - n2)]
+    if world > 1 and min(n for _, n in nodes) < halo:
+        raise ValueError(f"slabs of {min(n for _, n in nodes)} voxels are thinner than the {halo}-voxel halo")
+    return nodes
+
+
+def pw_combine(nvox: int, slabs, values):
+    """Combine per-slab numpy-order sums (one K-list per slab, slab order) into
+    np.sum's values over the whole volume by walking numpy's recursion."""
+    index = {tuple(s): i for i, s in enumerate(slabs)}
+
+    def rec(lo, n):
+        i = index.get((lo, n))
+        if i is not None:
+            return [float(v) for v in values[i]]
+        if n <= 128:
+            raise ValueError("slab boundary inside a pairwise leaf")
+        n2 = _pw_split(n)
+        a, b = rec(lo, n2), rec(lo + n2, n - n2)
+        return [x + y for x, y in zip(a, b)]
+
+    return rec(0, nvox)
+
+
+class TorchComm:
+    """Halo / gather / reduce exchanges of the slab prox over torch.distributed
+    (NCCL in production, gloo in the CPU tests)."""
+
+    def __init__(self, group=None):
+        import torch
+        import torch.distributed as dist
+        self.torch = torch
+        self.dist = dist
+        self.group = group
+        self.active = dist.is_initialized()
+        self.rank = dist.get_rank(group) if self.active else 0
+        self.world = dist.get_world_size(group) if self.active else 1
+        self.nccl = self.active and dist.get_backend(group) == "nccl"
+
+    def _peer(self, r):
+        return self.dist.get_global_rank(self.group, r) if self.group is not None else r
+
+    def halo(self, bufs, n: int, h: int, lower: bool = True, upper: bool = True):
+        """Fill the halos of local buffers laid out [h halo | n own | h halo]:
+        ``lower`` receives the previous rank's last h own values, ``upper`` the
+        next rank's first h."""
+        if self.world == 1:
+            return
+        d = self.dist
+        ops = []
+        for b in bufs:
+            if lower:
+                if self.rank + 1 < self.world:
+                    ops.append(d.P2POp(d.isend, b[n:n + h], self._peer(self.rank + 1), self.group))
+                if self.rank > 0:
+                    ops.append(d.P2POp(d.irecv, b[0:h], self._peer(self.rank - 1), self.group))
+            if upper:
+                if self.rank > 0:
+                    ops.append(d.P2POp(d.isend, b[h:2 * h], self._peer(self.rank - 1), self.group))
+                if self.rank + 1 < self.world:
+                    ops.append(d.P2POp(d.irecv, b[n + h:n + 2 * h], self._peer(self.rank + 1), self.group))
+        if ops:
+            for req in d.batch_isend_irecv(ops):
+                req.wait()
+
+    def gather(self, t):
+        """All ranks' copies of a small tensor, as a host array [world, len]."""
+        if self.world == 1:
+            return t.cpu().numpy()[None, :]
+        out = [self.torch.empty_like(t) for _ in range(self.world)]
+        self.dist.all_gather(out, t.contiguous(), group=self.group)
+        return np.stack([o.cpu().numpy() for o in out])
+
+    def allreduce(self, t):
+        if self.world > 1:
+            self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM, group=self.group)
+
+    def reduce_scatter(self, full, slabs):
+        """Sum ``full`` over ranks; at least this rank's slab ends up correct."""
+        if self.world == 1:
+            return
+        lo, n = slabs[self.rank]
+        if self.nccl and len({c for _, c in slabs}) == 1:
+            out = self.torch.empty(n, dtype=full.dtype, device=full.device)
+            self.dist.reduce_scatter_tensor(out, full, op=self.dist.ReduceOp.SUM, group=self.group)
+            full[lo:lo + n].copy_(out)
+        else:
+            self.allreduce(full)
+
+    def allgather_slabs(self, full, slabs):
+        """Every rank's own slab of ``full`` into everyone's copy."""
+        if self.world == 1:
+            return
+        lo, n = slabs[self.rank]
+        if self.nccl and len({c for _, c in slabs}) == 1:
+            self.dist.all_gather_into_tensor(full, full[lo:lo + n].clone(), group=self.group)
+            return
+        for r, (a, c) in enumerate(slabs):
+            self.dist.broadcast(full[a:a + c], self._peer(r), group=self.group)
+
+
+class CudaSlab:
+    """The rank's slab of the prox on its GPU (bsgd_slab_* in the C ABI)."""
+
+    def __init__(self, dims, offset: int, count: int, device=None):
+        t = nat.torch()
+        self.t = t
+        self.dev = device if device is not None else nat.require_cuda()
+        self.dims = tuple(int(v) for v in dims)
+        depth, height, width = self.dims
+        self.dim = 3 if depth > 1 else 2
+        self.nvox = depth * height * width
+        self.offset, self.count = int(offset), int(count)
+        lib = nat.load()
+        nbytes = int(lib.bsgd_slab_workspace_bytes(depth, height, width, count))
+        self.ws = t.zeros((nbytes + 7) // 8, dtype=t.float64, device=self.dev)
+        offs = (ctypes.c_int64 * nat.SLAB_SLOTS)()
+        halo = ctypes.c_int64()
+        nat.call("bsgd_slab_layout", depth, height, width, count, offs, ctypes.byref(halo))
+        self.halo = int(halo.value)
+        length = count + 2 * self.halo
+        self._buf = {k: self.ws[o:o + length] for k, o in enumerate(offs[:11]) if o >= 0}
+        self._sums = self.ws[offs[11]:offs[11] + 16]
+        self._stats = self.ws[offs[11] + 16:offs[11] + 20]
+        self.args = nat.SlabArgs(depth, height, width, offset, count, 0.0, 0, 0, nat.ptr(self.ws), self.ws.numel() * 8)
+        self.parity = 0
+
+    def _a(self):
+        self.args.parity = self.parity
+        return ctypes.byref(self.args)
+
+    def _st(self):
+        return nat.stream_ptr(self.dev)
+
+    def set_weight(self, w: float):
+        self.args.weight = float(w)
+
+    def fields(self, name: str):
+        d = self.dim
+        if name == "b":
+            return [self._buf[0]]
+        if name == "u":
+            return [self._buf[10]]
+        if name == "q":
+            return [self._buf[7 + k] for k in range(d)]
+        grp = self.parity if name == "p" else 1 - self.parity
+        return [self._buf[1 + 3 * grp + k] for k in range(d)]
+
+    def own(self, name: str):
+        h = self.halo
+        return [b[h:h + self.count] for b in self.fields(name)]
+
+    def step(self, x_k, g, mu: float):
+        nat.call("bsgd_slab_step", self._a(), nat.ptr(x_k), nat.ptr(g), float(mu), self._st())
+
+    def init(self):
+        nat.call("bsgd_slab_init", self._a(), nat.ptr(self._sums), self._st())
+        return self._sums[:2]
+
+    def candidate(self, from_p: bool):
+        nat.call("bsgd_slab_candidate", self._a(), 1 if from_p else 0, self._st())
+
+    def dual(self, beta: float):
+        nat.call("bsgd_slab_dual", self._a(), float(beta), nat.ptr(self._sums), self._st())
+        return self._sums[:1 + 2 * self.dim]
+
+    def finalize(self):
+        nat.call("bsgd_slab_finalize", self._a(), self._st())
+
+    def energy(self):
+        nat.call("bsgd_slab_energy", self._a(), nat.ptr(self._sums), self._st())
+        return self._sums[:2]
+
+    def output(self, fell: bool, x_next, x_k, g, x_true):
+        nat.call("bsgd_slab_output", self._a(), 1 if fell else 0, nat.ptr(x_next), nat.ptr(x_k), nat.ptr(g),
+                 nat.ptr(x_true) if x_true is not None else None, nat.ptr(self._stats), self._st())
+        return self._stats
+
+
+class SlabProx:
+    """Host loop of the slab-decomposed prox: the FGP of tv.py:172-255 with the
+    passes on the rank's slab (``backend``) and the sums combined across ranks.
+
+    Mirrors `fgp_kernel` (csrc/fgp.cuh) decision for decision; the scalar
+    arithmetic is Python float (IEEE double), the same operations in the same
+    order, so the outcome is bit-identical to the single-GPU prox."""
+
+    def __init__(self, backend, comm, slabs):
+        self.be = backend
+        self.comm = comm
+        self.slabs = [tuple(s) for s in slabs]
+        if self.slabs[comm.rank] != (backend.offset, backend.count):
+            raise ValueError("backend slab does not match this rank's slab")
+
+    def _sums(self, t):
+        return pw_combine(self.be.nvox, self.slabs, self.comm.gather(t))
+
+    def _halo(self, name, lower=True, upper=True):
+        self.comm.halo(self.be.fields(name), self.be.count, self.be.halo, lower, upper)
+
+    def run(self, weight: float, max_iters: int, tol: float):
+        """Prox of the b already stored by ``backend.step``; returns ProxInfo-style fields."""
+        be = self.be
+        if not weight > 0:
+            raise ValueError("slab prox needs a positive weight")
+        be.set_weight(weight)
+        be.parity = 0
+        dim = be.dim
+        self._halo("b")
+        phi_prev, tv_b = self._sums(be.init())
+        t_mom = 1.0
+        iters = restarts = converged = 0
+        for it in range(max_iters):
+            self._halo("q")
+            be.candidate(False)                       # tv.py:207-214
+            self._halo("c")
+            t_next = 0.5 * (1.0 + math.sqrt(1.0 + (4.0 * t_mom) * t_mom))
+            beta = (t_mom - 1.0) / t_next
+            vc = self._sums(be.dual(beta))            # tv.py:215-216, commit speculative
+            phi = vc[0]
+            if phi > phi_prev:                        # restart (tv.py:217-231)
+                restarts += 1
+                t_mom = 1.0
+                be.candidate(True)
+                self._halo("c")
+                t_next = 0.5 * (1.0 + math.sqrt(1.0 + (4.0 * t_mom) * t_mom))
+                beta = (t_mom - 1.0) / t_next
+                vc = self._sums(be.dual(beta))
+                phi = vc[0]
+            be.parity ^= 1                            # p <- c
+            phi_prev = phi_prev if phi_prev < phi else phi
+            t_mom = t_next
+            iters = it + 1
+            ch2, sc2 = vc[1] + vc[2], vc[1 + dim] + vc[2 + dim]
+            if dim == 3:
+                ch2, sc2 = ch2 + vc[3], sc2 + vc[6]
+            change, scale = math.sqrt(ch2), math.sqrt(sc2)
+            if change <= tol * (1e-30 if 1e-30 > scale else scale):   # tv.py:239-248
+                converged = 1
+                break
+        be.finalize()                                 # tv.py:250
+        self._halo("u", upper=False)
+        e = self._sums(be.energy())
+        two_w = 2.0 * weight
+        obj_out = e[0] + two_w * e[1]
+        obj_b = 0.0 + two_w * tv_b
+        fell = 1 if obj_out > obj_b else 0            # tv.py:251-253
+        return {"iterations": iters, "converged": converged, "restarts": restarts, "fell_back": fell,
+                "tv": tv_b if fell else e[1]}
