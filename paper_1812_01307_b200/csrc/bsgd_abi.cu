@@ -939,10 +939,92 @@ static int prox_occupancy() {
     return occ;
 }
 
+// dynamic shared memory of the split / slab sum passes (pw_cta_fast chunks of 8 leaves)
+template <int K>
+static size_t slab_smem(bool fast) { return fast ? sizeof(double) * K * 8 * 128 : 0; }
+
+template <int DIM>
+static void split_attrs() {
+    static bool done = false;
+    if (done) return;
+    done = true;
+    cudaFuncSetAttribute(slab_init_kernel<DIM, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)slab_smem<2>(true));
+    cudaFuncSetAttribute(slab_energy_kernel<DIM, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)slab_smem<2>(true));
+    cudaFuncSetAttribute(slab_dual_kernel<DIM, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)slab_smem<1 + 2 * DIM>(true));
+}
+
 template <int DIM>
 static void prox_warm() {
     (void)prox_occupancy<DIM, true>();
     (void)prox_occupancy<DIM, false>();
+    split_attrs<DIM>();
+}
+
+// Split prox (slab.cuh): one kernel per FGP pass with the decisions on the
+// device, for volumes whose fields do not stay in L2.  A fixed launch sequence
+// (passes that do not apply return at once), so it is graph-capturable.
+template <int DIM>
+static int launch_prox_split(const ProxArgs &a, cudaStream_t st) {
+    split_attrs<DIM>();
+    SlabView v = {};
+    v.a = a;
+    v.off = 0;
+    v.n = a.N;
+    v.ds = a.ds;
+    v.fast = a.fast;
+    const int64_t S = (int64_t)1 << a.ds;
+    v.G = (int)std::min<int64_t>(S, 256);
+    if (S / v.G > kPwMaxQ * (int64_t)(a.fast ? 8 : kThreads / 8))
+        return fail(BSGD_EINVAL, "image too large for the pairwise tree (%lld voxels)", (long long)a.N);
+    v.ctl = (FgpCtl *)(a.red + (size_t)kMaxPartials * kPwMaxK);
+    double *part = a.red;
+    for (int k = 0; k < DIM; ++k) {  // p = q = 0 (tv.py:198-201)
+        CU(cudaMemsetAsync(a.f[k], 0, sizeof(double) * a.N, st));
+        CU(cudaMemsetAsync(a.f[DIM + k], 0, sizeof(double) * a.N, st));
+    }
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(a.N, kThreads), (int64_t)num_sms() * 8));
+    constexpr int KD = 1 + 2 * DIM;
+    const bool fast = a.fast != 0;
+    auto sums2 = [&](bool energy) {
+        if (energy) {
+            if (fast) slab_energy_kernel<DIM, true><<<v.G, kThreads, slab_smem<2>(true), st>>>(v, part);
+            else slab_energy_kernel<DIM, false><<<v.G, kThreads, 0, st>>>(v, part);
+        } else {
+            if (fast) slab_init_kernel<DIM, true><<<v.G, kThreads, slab_smem<2>(true), st>>>(v, part);
+            else slab_init_kernel<DIM, false><<<v.G, kThreads, 0, st>>>(v, part);
+        }
+    };
+    auto dual = [&]() {
+        if (fast) slab_dual_kernel<DIM, true><<<v.G, kThreads, slab_smem<KD>(true), st>>>(v, 0.0, part);
+        else slab_dual_kernel<DIM, false><<<v.G, kThreads, 0, st>>>(v, 0.0, part);
+    };
+    v.when = 0;
+    sums2(false);
+    split_decide_kernel<DIM, 2><<<1, kThreads, 0, st>>>(v, 0, 0, part);
+    for (int it = 0; it < a.max_iters; ++it) {
+        v.when = 1;  // unless converged
+        slab_candidate_kernel<DIM><<<grid, kThreads, 0, st>>>(v, 0);
+        dual();
+        split_decide_kernel<DIM, KD><<<1, kThreads, 0, st>>>(v, 1, it, part);
+        v.when = 2;  // only on a restart
+        slab_candidate_kernel<DIM><<<grid, kThreads, 0, st>>>(v, 1);
+        dual();
+        split_decide_kernel<DIM, KD><<<1, kThreads, 0, st>>>(v, 2, it, part);
+    }
+    v.when = 0;
+    slab_finalize_kernel<DIM><<<grid, kThreads, 0, st>>>(v);
+    sums2(true);
+    split_decide_kernel<DIM, 2><<<1, kThreads, 0, st>>>(v, 3, 0, part);
+    split_output_kernel<DIM><<<grid, kThreads, 0, st>>>(v);
+    LAUNCHED();
+    return BSGD_OK;
+}
+
+static bool prox_split_on(const ProxArgs &a) {
+    const char *e = getenv("BSGD_PROX_SPLIT");
+    if (e && e[0]) return e[0] == '1';
+    return a.N >= ((int64_t)1 << 21);
 }
 
 template <int DIM, bool FAST>
@@ -973,10 +1055,13 @@ static int launch_prox(ProxArgs &a, cudaStream_t st) {
     int rc = pw_depth(a.N, &a.ds);
     if (rc) return rc;
     a.fast = (a.N % 128 == 0 && a.N / 128 == ((int64_t)1 << a.ds)) ? 1 : 0;
+    const bool split = prox_split_on(a);
     if (a.D <= 1) {
         a.D = 1;
+        if (split) return launch_prox_split<2>(a, st);
         return a.fast ? launch_prox_dim<2, true>(a, st) : launch_prox_dim<2, false>(a, st);
     }
+    if (split) return launch_prox_split<3>(a, st);
     return a.fast ? launch_prox_dim<3, true>(a, st) : launch_prox_dim<3, false>(a, st);
 }
 
@@ -1306,12 +1391,14 @@ static int slab_ctx(const bsgd_slab *s, SlabCtx &c, bool need_weight = true) {
     a.b = at(0);
     a.w = s->weight;
     a.step = 1.0 / ((D > 1 ? 12.0 : 8.0) * s->weight);
-    const int pb = 1 + 3 * s->parity, cb = 1 + 3 * (1 - s->parity);
-    for (int k = 0; k < c.dim; ++k) {
-        a.f[k] = at(pb + k);
+    for (int k = 0; k < c.dim; ++k) {  // dual buffer 0, q, dual buffer 1 (slab_roles resolves p / c)
+        a.f[k] = at(1 + k);
         a.f[c.dim + k] = at(7 + k);
-        a.f[2 * c.dim + k] = at(cb + k);
+        a.f[2 * c.dim + k] = at(4 + k);
     }
+    c.v.parity = s->parity;
+    c.v.when = 0;
+    c.v.ctl = nullptr;
     c.v.u = at(10);
     c.v.off = s->offset;
     c.v.n = s->count;
@@ -1320,6 +1407,7 @@ static int slab_ctx(const bsgd_slab *s, SlabCtx &c, bool need_weight = true) {
     c.v.fast = (s->count % 128 == 0 && s->count / 128 == ((int64_t)1 << c.v.ds)) ? 1 : 0;
     const int64_t S = (int64_t)1 << c.v.ds;
     c.G = (int)std::min<int64_t>(S, 256);
+    c.v.G = c.G;
     const int64_t per_slot = c.v.fast ? 8 : kThreads / 8;
     if (S / c.G > kPwMaxQ * per_slot) return fail(BSGD_EINVAL, "slab too large for the pairwise tree");
     c.part = base;
@@ -2509,7 +2597,8 @@ int bsgd_slab_output(const bsgd_slab *s, int32_t fell_back, double *x_next, cons
     if (!x_next || !x_k || !g || !stats_out) return fail(BSGD_EINVAL, "x_next, x_k, g and stats_out are required");
     cudaStream_t st = (cudaStream_t)stream;
     const int grid = std::min(c.grid, kSlabPartials / 4);
-    slab_output_kernel<<<grid, kThreads, 0, st>>>(c.v, fell_back ? 1 : 0, x_next, x_k, g, x_true, c.part);
+    if (c.dim == 3) slab_output_kernel<3><<<grid, kThreads, 0, st>>>(c.v, fell_back ? 1 : 0, x_next, x_k, g, x_true, c.part);
+    else slab_output_kernel<2><<<grid, kThreads, 0, st>>>(c.v, fell_back ? 1 : 0, x_next, x_k, g, x_true, c.part);
     slab_sum4_kernel<<<1, 32, 0, st>>>(c.part, grid, stats_out);
     LAUNCHED();
     return BSGD_OK;

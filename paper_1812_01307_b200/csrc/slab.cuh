@@ -1,21 +1,31 @@
-// Slab-decomposed TV prox for multi-GPU runs (SURVEY.md §8 e, "Prox").
+// Pass-per-kernel TV prox: the FGP of fgp.cuh split into one kernel per pass.
 //
-// Rank p owns the voxels [off, off + n) of the C-order volume (2-D: image) and
-// holds every field over [off - h, off + n + h), h = one plane (H*W in 3-D, W
-// in 2-D): the stencils of tv.py:115-132 (and their 3-D restatement) reach one
-// plane either way, so a one-plane halo exchanged between neighbouring ranks
-// is all a pass needs.  Field pointers are shifted so that ptr[p] addresses
-// global voxel p; boundary tests use global coordinates, so halos outside the
-// volume are never read.
+// Two users:
 //
-// The FGP control flow (restart, stop, fallback: tv.py:203-253) needs global
-// sums.  Slabs are nodes of numpy's pairwise recursion over the whole volume
-// (parallel.prox_slabs), so a slab's local numpy-order sum is exactly that
-// node's value; the host gathers the per-rank values and combines them in the
-// recursion's order (parallel.pw_combine): every decision is bit-identical to
-// the single-GPU kernel and to the reference.  The kernels here are the FGP
-// passes of fgp.cuh on a slab; the host loop (parallel.SlabProx) sequences
-// them between halo exchanges.
+// 1. Multi-GPU slab decomposition (SURVEY.md §8 e, "Prox").  Rank p owns the
+//    voxels [off, off + n) of the C-order volume (2-D: image) and holds every
+//    field over [off - h, off + n + h), h = one plane (H*W in 3-D, W in 2-D):
+//    the stencils of tv.py:115-132 (and their 3-D restatement) reach one plane
+//    either way, so a one-plane halo exchanged between neighbouring ranks is all
+//    a pass needs.  Field pointers are shifted so that ptr[p] addresses global
+//    voxel p; boundary tests use global coordinates, so halos outside the
+//    volume are never read.  The FGP decisions (restart, stop, fallback:
+//    tv.py:203-253) need global sums: slabs are nodes of numpy's pairwise
+//    recursion over the whole volume (parallel.prox_slabs), so a slab's local
+//    numpy-order sum is exactly that node's value, and the host combines the
+//    per-rank values in the recursion's order (parallel.pw_combine).  The host
+//    loop (parallel.SlabProx) sequences the passes between halo exchanges.
+//
+// 2. Single-GPU prox of large volumes ("split" prox, launch_prox_split).  The
+//    persistent cooperative fgp_kernel must keep every CTA resident and is
+//    capped at 16 warps/SM by its 128-register dual pass; the candidate pass
+//    alone fits in 64 registers and runs at twice the occupancy.  Here the
+//    whole volume is one slab and the decisions are taken on the device by
+//    one-CTA "decide" kernels into an FgpCtl block; every later pass reads the
+//    block and returns at once when it does not apply (converged, or no
+//    restart), so the launch sequence is fixed -- max_iters x 6 kernels -- and
+//    can be captured in a CUDA graph.  Same operations in the same order as
+//    fgp_kernel: bit-identical results.
 #pragma once
 
 #include "common.cuh"
@@ -24,13 +34,54 @@
 
 namespace bsgd {
 
+// device-side FGP state of the split prox (fgp_kernel's registers)
+struct FgpCtl {
+    double phi_prev, tv_b, t_mom, t_next, beta;
+    int32_t iters, restarts, done, parity, restart, fell;
+};
+
 struct SlabView {
-    ProxArgs a;       // global D, H, W, N; b and f[] shifted to global indexing; w, step
+    ProxArgs a;       // global D, H, W, N; b, w, step (and the split prox's outputs);
+                      // f[0..DIM) dual buffer 0, f[DIM..2DIM) q, f[2DIM..3DIM) dual buffer 1,
+                      // all addressed by global voxel index
     int64_t off, n;   // own voxels
     int ds;           // pairwise depth of n
     int fast;         // n == 128 * 2^ds
-    double *u;        // finalize output (shifted)
+    int G;            // CTAs of the sum passes (entries in part)
+    int parity;       // host loop: dual buffer holding p
+    int when;         // split prox: 0 always, 1 unless converged, 2 only on a restart
+    double *u;        // finalize output; NULL: the dual buffer not holding p
+    FgpCtl *ctl;      // split prox control block, NULL for the host loop
 };
+
+__device__ __forceinline__ bool slab_skip(const SlabView &s) {
+    if (s.ctl == nullptr || s.when == 0) return false;
+    const FgpCtl *c = s.ctl;
+    if (s.when == 1) return c->done != 0;
+    return c->done != 0 || c->restart == 0;
+}
+
+template <int DIM>
+struct SlabRoles {
+    const double *P[DIM];
+    double *C[DIM];
+    double *Q[DIM];
+    double *u;
+};
+
+template <int DIM>
+__device__ __forceinline__ SlabRoles<DIM> slab_roles(const SlabView &s) {
+    const int par = s.ctl != nullptr ? s.ctl->parity : s.parity;
+    SlabRoles<DIM> r;
+#pragma unroll
+    for (int k = 0; k < DIM; ++k) {
+        r.P[k] = par ? s.a.f[2 * DIM + k] : s.a.f[k];
+        r.C[k] = par ? s.a.f[k] : s.a.f[2 * DIM + k];
+        r.Q[k] = s.a.f[DIM + k];
+    }
+    r.u = s.u != nullptr ? s.u : r.C[0];
+    return r;
+}
 
 // DualCommitTerms over the slab: local index i -> voxel off + i
 template <int DIM>
@@ -91,31 +142,32 @@ __global__ void __launch_bounds__(kThreads) slab_init_kernel(SlabView s, double 
 // c = proj(src + step grad(b + w div src)) on the own voxels (tv.py:207-214)
 template <int DIM>
 __global__ void __launch_bounds__(kThreads) slab_candidate_kernel(SlabView s, int from_p) {
+    if (slab_skip(s)) return;
+    const SlabRoles<DIM> r = slab_roles<DIM>(s);
     const double *src[DIM];
-    double *C[DIM];
 #pragma unroll
-    for (int k = 0; k < DIM; ++k) {
-        src[k] = from_p ? s.a.f[k] : s.a.f[DIM + k];
-        C[k] = s.a.f[2 * DIM + k];
-    }
+    for (int k = 0; k < DIM; ++k) src[k] = from_p ? r.P[k] : r.Q[k];
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < s.n; i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t p = s.off + i;
         double c[DIM];
         candidate<DIM>(s.a, src, p, c);
 #pragma unroll
-        for (int k = 0; k < DIM; ++k) C[k][p] = c[k];
+        for (int k = 0; k < DIM; ++k) r.C[k][p] = c[k];
     }
 }
 
 // dual value of c and the speculative momentum commit q = c + beta (c - p)
-// (tv.py:215-216, 233-245): 1 + 2 DIM sums
+// (tv.py:215-216, 233-245): 1 + 2 DIM sums.  beta from the control block when set.
 template <int DIM, bool FAST>
 __global__ void __launch_bounds__(kThreads, 2) slab_dual_kernel(SlabView s, double beta, double *part) {
+    if (slab_skip(s)) return;
+    const SlabRoles<DIM> r = slab_roles<DIM>(s);
     DualSlabTerms<DIM> f;
-    f.b = s.a.b; f.w = s.a.w; f.beta = beta;
+    f.b = s.a.b; f.w = s.a.w;
+    f.beta = s.ctl != nullptr ? s.ctl->beta : beta;
     f.D = s.a.D; f.H = s.a.H; f.W = s.a.W;
 #pragma unroll
-    for (int k = 0; k < DIM; ++k) { f.P[k] = s.a.f[k]; f.Q[k] = s.a.f[DIM + k]; f.C[k] = s.a.f[2 * DIM + k]; }
+    for (int k = 0; k < DIM; ++k) { f.P[k] = r.P[k]; f.Q[k] = r.Q[k]; f.C[k] = r.C[k]; }
     f.off = s.off;
     slab_sum<1 + 2 * DIM, FAST>(s, f, part);
 }
@@ -123,21 +175,20 @@ __global__ void __launch_bounds__(kThreads, 2) slab_dual_kernel(SlabView s, doub
 // u = b + w div p (tv.py:250)
 template <int DIM>
 __global__ void __launch_bounds__(kThreads) slab_finalize_kernel(SlabView s) {
-    const double *P[DIM];
-#pragma unroll
-    for (int k = 0; k < DIM; ++k) P[k] = s.a.f[k];
+    const SlabRoles<DIM> r = slab_roles<DIM>(s);
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < s.n; i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t p = s.off + i;
-        int64_t z, r, t;
-        split_index<DIM>(p, s.a.H, s.a.W, z, r, t);
-        s.u[p] = rn_add(__ldg(s.a.b + p), rn_mul(s.a.w, div_at<DIM>(P, z, r, t, s.a.D, s.a.H, s.a.W)));
+        int64_t z, y, t;
+        split_index<DIM>(p, s.a.H, s.a.W, z, y, t);
+        r.u[p] = rn_add(__ldg(s.a.b + p), rn_mul(s.a.w, div_at<DIM>(r.P, z, y, t, s.a.D, s.a.H, s.a.W)));
     }
 }
 
 // np.sum((u - b)^2) and TV(u) (tv.py:166-169, 251)
 template <int DIM, bool FAST>
 __global__ void __launch_bounds__(kThreads) slab_energy_kernel(SlabView s, double *part) {
-    const double *b = s.a.b, *u = s.u;
+    const SlabRoles<DIM> r = slab_roles<DIM>(s);
+    const double *b = s.a.b, *u = r.u;
     const int64_t H = s.a.H, W = s.a.W, off = s.off;
     auto f = [&](int64_t i, double (&t)[2]) {
         const int64_t p = off + i;
@@ -150,13 +201,15 @@ __global__ void __launch_bounds__(kThreads) slab_energy_kernel(SlabView s, doubl
 
 // x_next on the own voxels (identity fallback when fell) and the epoch
 // statistics partials |x|^2, |x - x*|^2, d.g, |d|^2 (as fgp_kernel's epoch mode)
+template <int DIM>
 __global__ void __launch_bounds__(kThreads) slab_output_kernel(SlabView s, int fell, double *xn, const double *xk,
                                                                const double *g, const double *xtrue, double *part) {
     __shared__ double sm[4 * (kThreads / 32)];
+    const SlabRoles<DIM> r = slab_roles<DIM>(s);
     double st[4] = {0.0, 0.0, 0.0, 0.0};
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < s.n; i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t p = s.off + i;
-        const double xv = fell ? __ldg(s.a.b + p) : __ldg(s.u + p);
+        const double xv = fell ? __ldg(s.a.b + p) : __ldg(r.u + p);
         xn[p] = xv;
         const double d = rn_sub(xv, xk[p]);
         st[0] += xv * xv;
@@ -174,6 +227,101 @@ __global__ void slab_sum4_kernel(const double *part, int n, double *out) {
     warp_sum_partials<4>(part, n, v);
     if (threadIdx.x == 0)
         for (int k = 0; k < 4; ++k) out[k] = v[k];
+}
+
+// ---- split prox: device-side decisions ----
+
+__device__ __forceinline__ void fgp_next_beta(FgpCtl &c) {
+    c.t_next = 0.5 * (1.0 + sqrt(rn_add(1.0, rn_mul(rn_mul(4.0, c.t_mom), c.t_mom))));
+    c.beta = (c.t_mom - 1.0) / c.t_next;
+}
+
+// stage 0: after the setup sums; 1: after the candidate's dual pass; 2: after
+// the restart's dual pass; 3: after the energy sums (fallback decision, outputs).
+// The same scalar code as fgp_kernel.
+template <int DIM, int K>
+__global__ void __launch_bounds__(kThreads) split_decide_kernel(SlabView s, int stage, int it, const double *part) {
+    if (slab_skip(s)) return;
+    __shared__ double sm[kPwMaxQ * kPwMaxK];
+    double v[K];
+    pw_top<K>(s.ds, s.G, part, sm, v);
+    if (threadIdx.x != 0) return;
+    FgpCtl &c = *s.ctl;
+    const ProxArgs &a = s.a;
+    if (stage == 0) {
+        c.phi_prev = v[0];
+        c.tv_b = v[1];
+        c.t_mom = 1.0;
+        c.iters = c.restarts = c.done = c.parity = c.restart = c.fell = 0;
+        fgp_next_beta(c);
+        if (a.dual != nullptr) a.dual[0] = c.phi_prev;
+        return;
+    }
+    if (stage == 3) {
+        const double two_w = 2.0 * a.w;
+        const double obj_out = rn_add(v[0], rn_mul(two_w, v[1]));
+        const double obj_b = rn_add(0.0, rn_mul(two_w, c.tv_b));
+        c.fell = obj_out > obj_b ? 1 : 0;
+        if (a.scal != nullptr) {
+            a.scal[0] = c.fell ? c.tv_b : v[1];
+            a.scal[1] = c.iters; a.scal[2] = c.restarts; a.scal[3] = c.done; a.scal[4] = c.fell;
+        }
+        if (a.info != nullptr) {
+            a.info[0] = c.iters; a.info[1] = c.done; a.info[2] = c.restarts; a.info[3] = c.fell;
+        }
+        return;
+    }
+    const double phi = v[0];
+    if (stage == 1 && phi > c.phi_prev) {  // restart from the last accepted point (tv.py:217-231)
+        c.restart = 1;
+        ++c.restarts;
+        c.t_mom = 1.0;
+        fgp_next_beta(c);
+        return;
+    }
+    c.restart = 0;
+    c.parity ^= 1;  // p <- c
+    c.phi_prev = (c.phi_prev < phi) ? c.phi_prev : phi;
+    c.t_mom = c.t_next;
+    c.iters = it + 1;
+    if (a.dual != nullptr) a.dual[it + 1] = c.phi_prev;
+    double ch2 = rn_add(v[1], v[2]), sc2 = rn_add(v[1 + DIM], v[2 + DIM]);
+    if constexpr (DIM == 3) { ch2 = rn_add(ch2, v[3]); sc2 = rn_add(sc2, v[6]); }
+    const double change = sqrt(ch2), scale = sqrt(sc2);
+    const double floor_scale = (1e-30 > scale) ? 1e-30 : scale;
+    if (change <= a.tol * floor_scale) c.done = 1;
+    else fgp_next_beta(c);
+}
+
+// outputs of the split prox: the image (standalone) or x_next in vector order
+// with the epoch statistics (fgp_kernel's epoch mode)
+template <int DIM>
+__global__ void __launch_bounds__(kThreads) split_output_kernel(SlabView s) {
+    __shared__ double sm[4 * (kThreads / 32)];
+    const SlabRoles<DIM> r = slab_roles<DIM>(s);
+    const ProxArgs &a = s.a;
+    const int fell = s.ctl->fell;
+    const int64_t N = a.N;
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, nthr = (int64_t)gridDim.x * blockDim.x;
+    if (a.out_img != nullptr) {
+        for (int64_t p = tid; p < N; p += nthr) a.out_img[p] = fell ? __ldg(a.b + p) : __ldg(r.u + p);
+        return;
+    }
+    double st[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int64_t k = tid; k < N; k += nthr) {
+        const int64_t p = (a.perm != nullptr) ? a.perm[k] : k;
+        const double xv = fell ? __ldg(a.b + p) : __ldg(r.u + p);
+        a.x_next[k] = xv;
+        const double d = rn_sub(xv, a.x_k[k]);
+        st[0] += xv * xv;
+        if (a.x_true != nullptr) { const double e = xv - a.x_true[k]; st[1] += e * e; }
+        st[2] += d * a.g[k];
+        st[3] += d * d;
+    }
+    block_sum<4>(st, sm);
+    if (threadIdx.x == 0)
+        for (int k = 0; k < 4; ++k) a.xpart[(size_t)blockIdx.x * 4 + k] = st[k];
+    if (blockIdx.x == 0 && threadIdx.x == 0 && a.nx != nullptr) a.nx[0] = gridDim.x;
 }
 
 }  // namespace bsgd

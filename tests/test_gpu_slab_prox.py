@@ -225,3 +225,72 @@ def test_world1_driver_slab_prox_matches_replicated(cuda_ok):
     assert np.array_equal(ha[:, 0], hb[:, 0]) and np.array_equal(ha[:, 1], hb[:, 1])   # f_next, holds
     assert np.array_equal(ha[:, 4:9], hb[:, 4:9])   # TV, prox iterations / restarts / converged / fell back
     assert np.allclose(ha[:, 2:4], hb[:, 2:4], rtol=1e-12)   # |x|^2, |x - x*|^2 (summation order)
+
+
+SPLIT_CASES = [((1, 64, 48), 0.3, 30, 1e-6), ((1, 128, 128), 2.0, 20, 1e-12), ((16, 12, 10), 0.4, 20, 1e-6),
+               ((32, 32, 32), 0.05, 40, 1e-12), ((8, 8, 8), 1.0, 40, 1e-12)]
+
+
+@pytest.mark.parametrize("dims,w,iters,tol", SPLIT_CASES)
+def test_split_prox_matches_fused_bit_exact(cuda_ok, monkeypatch, dims, w, iters, tol):
+    """The pass-per-kernel prox with device-side decisions (chosen for large
+    volumes) equals the fused cooperative kernel: image, info, dual objectives."""
+    import torch
+    from paper_1812_01307_b200 import tv
+    dev = torch.device("cuda", 0)
+    vol = _volume(dims, 3)
+    img = torch.from_numpy(vol if dims[0] > 1 else vol[0]).to(dev)
+    out = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("BSGD_PROX_SPLIT", mode)
+        res, info = tv.tv_prox(img, w, tv.ProxSettings(iters, tol), return_info=True)
+        out[mode] = (res.cpu().numpy(), info)
+    (a, ia), (b, ib) = out["0"], out["1"]
+    assert np.array_equal(a, b)
+    assert (ia.iterations, ia.converged, ia.restarts, ia.fell_back) == (ib.iterations, ib.converged, ib.restarts,
+                                                                         ib.fell_back)
+    assert ia.dual_objectives == ib.dual_objectives
+    if vol.size <= 4096:
+        o, rep = orc.tv_prox3(vol, w, iters, tol) if dims[0] > 1 else orc.tv_prox(vol[0], w, iters, tol)
+        assert np.array_equal(b, o) and ib.restarts == rep.restarts
+
+
+def test_split_prox_fallback_matches_golden(cuda_ok, monkeypatch):
+    import torch
+    from paper_1812_01307_b200 import tv
+    monkeypatch.setenv("BSGD_PROX_SPLIT", "1")
+    z = load_golden("prox")
+    for k in range(int(z["count"])):
+        w, mi, tol = (float(v) for v in z[f"par{k}"])
+        img = torch.from_numpy(z[f"in{k}"]).cuda()
+        res, info = tv.tv_prox(img, w, tv.ProxSettings(int(mi), tol), return_info=True)
+        assert np.array_equal(res.cpu().numpy(), z[f"out{k}"]), k
+        assert [info.iterations, int(info.converged), info.restarts, int(info.fell_back)] == list(z[f"info{k}"]), k
+
+
+def test_split_prox_epochs_match_fused(cuda_ok, monkeypatch):
+    """Whole epochs (prox inside bsgd_epoch, graph-replayed run_solver) with the
+    split prox equal the fused prox bit for bit."""
+    from paper_1812_01307_b200 import blockops, solvers, tv
+    z = load_golden("p1_ct")
+    c = golden_cfg(z)
+    a = golden_csr(z)
+    m, n = (int(v) for v in z["mn"])
+    hw = tuple(int(v) for v in z["hw"])
+    layout = tv.PixelLayout(*hw, z["perm"])
+    cfg = solvers.SolverConfig(mu=c["mu"], lam=max(c["lam"], 0.05), epochs=6,
+                               prox=tv.ProxSettings(c["max_inner_iters"], c["tol"]))
+    runs = []
+    for mode in ("0", "1"):
+        monkeypatch.setenv("BSGD_PROX_SPLIT", mode)
+        op = blockops.BlockOperator(a, blockops.make_partition(a.shape[0], a.shape[1], m, n))
+        st = solvers.init_bsgd_state(op, z["y"], cfg)
+        xs = []
+        for _ in range(3):
+            solvers.bsgd_tv_iteration(st, op, z["y"], cfg, layout=layout)
+            xs.append(st.x.copy())
+        tr = solvers.run_solver("bsgd", solvers.Problem(op, z["y"], z["x_true"], layout), cfg)
+        runs.append((xs, tr.final_x, [(s.epoch, s.relative_error, s.objective) for s in tr.samples]))
+    for xa, xb in zip(runs[0][0], runs[1][0]):
+        assert np.array_equal(xa, xb)
+    assert np.array_equal(runs[0][1], runs[1][1]) and runs[0][2] == runs[1][2]
