@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 #include <cstdio>
 #include <cstdint>
+#include <cstdlib>
 
 #include "../paper_1812_01307_b200/csrc/sm100.cuh"
 
@@ -44,7 +45,9 @@ template <int W, int MODE>  // MODE 0: gather4, 1: 1-D bulk copy of W doubles pe
 __global__ void tma_gather(const __grid_constant__ CUtensorMap map, const double *tab, double *out) {
     extern __shared__ __align__(128) unsigned char sm[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    constexpr int SLOT_BYTES = G * 4 * W * 8;
+    // gather4 destinations must be 128-byte aligned: one 128 B cell per op
+    constexpr int OPB = (MODE == 0 && 4 * W * 8 < 128) ? 128 : 4 * W * 8;
+    constexpr int SLOT_BYTES = G * OPB;
     unsigned char *ring = sm + 1024 + warp * DEPTH * SLOT_BYTES;
     uint64_t *full = reinterpret_cast<uint64_t *>(sm) + warp * DEPTH;
     if (lane == 0)
@@ -56,14 +59,15 @@ __global__ void tma_gather(const __grid_constant__ CUtensorMap map, const double
     auto issue = [&](int slot) {
         // every lane draws its own row; lane 0 issues all the copies
         const uint32_t row = xs(s) & mask;
-        if (lane == 0) mbar_arrive_expect_tx(full + slot, SLOT_BYTES);
+        if (lane == 0) mbar_arrive_expect_tx(full + slot, G * 4 * W * 8);
+        __syncwarp();
         unsigned char *dst = ring + slot * SLOT_BYTES;
         if (MODE == 0) {
 #pragma unroll
             for (int k = 0; k < G; ++k) {
                 const int r0 = __shfl_sync(~0u, row, 4 * k), r1 = __shfl_sync(~0u, row, 4 * k + 1);
                 const int r2 = __shfl_sync(~0u, row, 4 * k + 2), r3 = __shfl_sync(~0u, row, 4 * k + 3);
-                if (lane == 0) gather4(dst + k * 4 * W * 8, &map, 0, r0, r1, r2, r3, full + slot);
+                if (lane == 0) gather4(dst + k * OPB, &map, 0, r0, r1, r2, r3, full + slot);
             }
         } else {
             // each lane issues its own 1-D bulk copy (32 issuing lanes)
@@ -75,7 +79,7 @@ __global__ void tma_gather(const __grid_constant__ CUtensorMap map, const double
     for (int st = 0; st < STEPS; ++st) {
         const int slot = st % DEPTH;
         mbar_wait(full + slot, (st / DEPTH) & 1);
-        acc += reinterpret_cast<const double *>(ring + slot * SLOT_BYTES)[lane * W];
+        acc += reinterpret_cast<const double *>(ring + slot * SLOT_BYTES + (lane >> 2) * OPB)[(lane & 3) * W];
         __syncwarp();
         if (st + DEPTH < STEPS) issue(slot);
     }
@@ -119,7 +123,9 @@ static CUtensorMap make_map(EncodeFn enc, double *tab, int w) {
     return m;
 }
 
-int main() {
+int main(int argc, char **argv) {
+    const int only = argc > 1 ? atoi(argv[1]) : -1;  // run one variant (a fault is sticky)
+    int id = 0;
     int sms = 0, clk = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
@@ -149,8 +155,9 @@ int main() {
                e == cudaSuccess ? "" : cudaGetErrorString(e));
     };
     auto run_tma = [&](auto kern, int w, int mode, int warps, int ctas_per_sm) {
+        if (only >= 0 && id++ != only) return;
         CUtensorMap m = make_map(enc, tab, w);
-        const int smem = 1024 + warps * DEPTH * G * 4 * w * 8;
+        const int smem = 1024 + warps * DEPTH * G * (mode == 0 && 4 * w * 8 < 128 ? 128 : 4 * w * 8);
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         const int grid = sms * ctas_per_sm;
         char nm[96];
@@ -165,6 +172,7 @@ int main() {
             run_tma(tma_gather<2, 1>, 2, 1, warps, cps);
         }
     const int grid = sms * 8;
+    if (only >= 0 && only < 18) return 0;
     timed("LDG.nc random 8 B", (double)grid * 256 * 4096, [&] { lsu_kernel<0><<<grid, 256>>>(tab, out); });
     timed("LDG.cg random 8 B", (double)grid * 256 * 4096, [&] { lsu_kernel<1><<<grid, 256>>>(tab, out); });
     timed("RED.add.f64 random 8 B", (double)grid * 256 * 4096, [&] { lsu_kernel<2><<<grid, 256>>>(tab, out); });
