@@ -1248,13 +1248,17 @@ static int build_gtiles(bsgd_plan *p, bool tr, int64_t ntiles, const int64_t *tp
     CU(cudaMemcpyAsync(idx.data(), tr ? p->t_idx : p->f_idx, sizeof(int32_t) * nnz, cudaMemcpyDeviceToHost, st));
     CU(cudaMemcpyAsync(val.data(), tr ? p->t_val : p->f_val, sizeof(V) * nnz, cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));
+    // rows padded to whole stream blocks (gtile.cuh: entry e = 16 m + l of a block at 8 l + m)
     std::vector<int64_t> rptr(nrows + 1, 0);
     for (int64_t i = 0; i < nrows; ++i) {
         const int64_t r = trows[i];
-        rptr[i + 1] = rptr[i] + (ptr[r + 1] - ptr[r]);
+        const int64_t len = ptr[r + 1] - ptr[r];
+        rptr[i + 1] = rptr[i] + (len + kGTileBlock - 1) / kGTileBlock * kGTileBlock;
     }
-    std::vector<uint16_t> loc(std::max<int64_t>(nnz, 1));
-    std::vector<V> pval(std::max<int64_t>(nnz, 1));
+    const int64_t nstore = rptr[nrows];
+    auto slot = [](int64_t k) { const int64_t e = k % kGTileBlock; return k - e + (e % 16) * 8 + e / 16; };
+    std::vector<uint16_t> loc(std::max<int64_t>(nstore, 1), 0);
+    std::vector<V> pval(std::max<int64_t>(nstore, 1), V(0));
     std::vector<std::vector<int32_t>> unions(ntiles);
     unsigned nth = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
     std::vector<std::thread> pool;
@@ -1273,8 +1277,8 @@ static int build_gtiles(bsgd_plan *p, bool tr, int64_t ntiles, const int64_t *tp
                 if (cols.size() > 28000) { big[w] = 1; continue; }
                 for (int64_t i = tptr[t]; i < tptr[t + 1]; ++i) {
                     const int64_t r = trows[i];
-                    int64_t o = rptr[i];
-                    for (int64_t k = ptr[r]; k < ptr[r + 1]; ++k, ++o) {
+                    for (int64_t k = ptr[r]; k < ptr[r + 1]; ++k) {
+                        const int64_t o = rptr[i] + slot(k - ptr[r]);
                         loc[o] = (uint16_t)(std::lower_bound(cols.begin(), cols.end(), idx[k]) - cols.begin());
                         pval[o] = val[k];
                     }
@@ -1309,8 +1313,8 @@ static int build_gtiles(bsgd_plan *p, bool tr, int64_t ntiles, const int64_t *tp
     cudaError_t e = up((void **)&N.tile_ptr, tptr, sizeof(int64_t) * (ntiles + 1));
     if (e == cudaSuccess) e = up((void **)&N.tile_rows, trows32.data(), sizeof(int32_t) * nrows);
     if (e == cudaSuccess) e = up((void **)&N.row_ptr, rptr.data(), sizeof(int64_t) * (nrows + 1));
-    if (e == cudaSuccess) e = up((void **)&N.loc, loc.data(), sizeof(uint16_t) * nnz);
-    if (e == cudaSuccess) e = up(&N.val, pval.data(), sizeof(V) * nnz);
+    if (e == cudaSuccess) e = up((void **)&N.loc, loc.data(), sizeof(uint16_t) * nstore);
+    if (e == cudaSuccess) e = up(&N.val, pval.data(), sizeof(V) * nstore);
     if (e == cudaSuccess) e = up((void **)&N.uni_ptr, uptr.data(), sizeof(int64_t) * (ntiles + 1));
     if (e == cudaSuccess) e = up((void **)&N.uni, uni.data(), sizeof(int32_t) * uni.size());
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);

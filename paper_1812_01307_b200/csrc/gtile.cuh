@@ -12,6 +12,14 @@
 // gathers drop by the tile's reuse factor.  Per-row arithmetic is the CSR
 // kernel's G = 16 form: lane-strided float64 partial sums and a fixed
 // shuffle tree, deterministic run to run.
+//
+// Stream layout: each row is padded (position 0, value 0) to whole blocks of
+// 128 entries, and inside a block entry e = 16 m + l is stored at 8 l + m, so
+// lane l fetches its eight lane-strided entries l, l + 16, ..., l + 112 with one
+// 16-byte position load and 16-byte value loads.  The stream loads were the
+// kernel's latency wall (profiles/r01_ct_spmv.md: the shared-memory address
+// computations waited on 2-byte position loads); the summation order is the
+// lane-strided order of the unblocked form.
 #pragma once
 
 #include "common.cuh"
@@ -36,6 +44,33 @@ __device__ __forceinline__ void gt_cp_async8(void *smem, const void *gmem) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)),
                  "l"(gmem)
                  : "memory");
+}
+
+constexpr int kGTileBlock = 128;   // stream block (entries) of one 16-lane row group
+
+// eight consecutive stored values of a block as float64
+__device__ __forceinline__ void gt_load8(const float *p, double (&v)[8], uint64_t pol) {
+    const float4 a = ld_stream4(p, pol), b = ld_stream4(p + 4, pol);
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+}
+__device__ __forceinline__ void gt_load8(const double *p, double (&v)[8], uint64_t pol) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const double2 a = ld_stream2(p + 2 * q, pol);
+        v[2 * q] = a.x;
+        v[2 * q + 1] = a.y;
+    }
+}
+
+// s += v[m] * w[pos[m]] for the eight packed uint16 positions, in order m = 0..7
+__device__ __forceinline__ double gt_fma8(const int4 l, const double (&v)[8], const double *w, double s) {
+    const uint32_t q[4] = {(uint32_t)l.x, (uint32_t)l.y, (uint32_t)l.z, (uint32_t)l.w};
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+        s = fma(v[2 * m], w[q[m] & 0xFFFFu], s);
+        s = fma(v[2 * m + 1], w[q[m] >> 16], s);
+    }
+    return s;
 }
 
 // DB: two windows, and while the CTA computes tile i from one, cp.async gathers
@@ -78,19 +113,23 @@ __global__ void __launch_bounds__(kThreads) gtile_kernel(GTiles T, const double 
         int64_t row = -1;
         if (tr < nr) {
             row = T.tile_rows[r0 + tr];
-            const int64_t beg = T.row_ptr[r0 + tr], end = T.row_ptr[r0 + tr + 1];
-            int64_t k = beg + gl;
-            for (; k + 48 < end; k += 64) {
-                const uint16_t l0 = __ldg(T.loc + k), l1 = __ldg(T.loc + k + 16);
-                const uint16_t l2 = __ldg(T.loc + k + 32), l3 = __ldg(T.loc + k + 48);
-                const V v0 = ld_stream(val + k, pol), v1 = ld_stream(val + k + 16, pol);
-                const V v2 = ld_stream(val + k + 32, pol), v3 = ld_stream(val + k + 48, pol);
-                s = fma((double)v0, w[l0], s);
-                s = fma((double)v1, w[l1], s);
-                s = fma((double)v2, w[l2], s);
-                s = fma((double)v3, w[l3], s);
+            const int64_t beg = T.row_ptr[r0 + tr], end = T.row_ptr[r0 + tr + 1];   // multiples of 128
+            int64_t k = beg + 8 * gl;
+            for (; k + 128 < end; k += 256) {   // two blocks in flight
+                const int4 la = ld_stream4(reinterpret_cast<const int32_t *>(T.loc + k), pol);
+                const int4 lb = ld_stream4(reinterpret_cast<const int32_t *>(T.loc + k + 128), pol);
+                double va[8], vb[8];
+                gt_load8(val + k, va, pol);
+                gt_load8(val + k + 128, vb, pol);
+                s = gt_fma8(la, va, w, s);
+                s = gt_fma8(lb, vb, w, s);
             }
-            for (; k < end; k += 16) s = fma((double)ld_stream(val + k, pol), w[__ldg(T.loc + k)], s);
+            if (k < end) {
+                const int4 la = ld_stream4(reinterpret_cast<const int32_t *>(T.loc + k), pol);
+                double va[8];
+                gt_load8(val + k, va, pol);
+                s = gt_fma8(la, va, w, s);
+            }
         }
 #pragma unroll
         for (int off = 8; off > 0; off >>= 1) s += __shfl_xor_sync(gmask, s, off, 16);

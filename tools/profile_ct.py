@@ -23,9 +23,14 @@ def main():
     ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--reps", type=int, default=2)
     ap.add_argument("--time", action="store_true", help="print event-timed ms per product instead")
+    ap.add_argument("--fwd-tiles", action="store_true", help="also gather-tile A (4 angles x 4 bins)")
     a = ap.parse_args()
     d = problems.config_device(a.config)
     op = d.op
+    if a.fwd_tiles:
+        from paper_1812_01307_b200 import blockops
+        n, ang, nb, _ = op._slice_source[1]
+        op.set_gather_tiles(False, blockops.grid_tiles(ang, nb))
     rows, cols = op.shape
     dev = torch.device("cuda", torch.cuda.current_device())
     x = torch.rand(cols, dtype=torch.float64, device=dev)
