@@ -204,8 +204,21 @@ struct bsgd_plan {
         void *val = nullptr;
         size_t bytes = 0;
     } gf, gt;
+    // blocked copy of A's stream for long rows (spmv.cuh csr_blocked_kernel)
+    struct BlkStore {
+        bool ok = false;
+        int64_t *ptr = nullptr;
+        int32_t *idx = nullptr;
+        void *val = nullptr;
+        size_t bytes = 0;
+    } fb;
     bool stacked() const { return depth > 1; }
 };
+
+static void blk_free(bsgd_plan::BlkStore &b) {
+    cudaFree(b.ptr); cudaFree(b.idx); cudaFree(b.val);
+    b = bsgd_plan::BlkStore();
+}
 
 static void gtiles_free(bsgd_plan::GTileStore &t) {
     cudaFree(t.tile_ptr); cudaFree(t.row_ptr); cudaFree(t.uni_ptr); cudaFree(t.tile_rows); cudaFree(t.uni);
@@ -299,6 +312,7 @@ static void tiled_free(bsgd_plan::TiledStore &t) {
 }
 
 static void plan_free(bsgd_plan *p) {
+    blk_free(p->fb);
     if (!p) return;
     DeviceGuard g(p->device);
     tiled_free(p->tf);
@@ -362,6 +376,55 @@ static int build_transpose(bsgd_plan *p, cudaStream_t st) {
     return BSGD_OK;
 }
 
+
+// Blocked copy of A's stream (csr_blocked_kernel) for plans whose rows are long
+// (>= 384 nonzeros on average: CT rays; padding to 128-entry blocks then costs
+// <= ~17% more stream bytes).  Skipped quietly when memory is short.
+// BSGD_BLOCKED=force builds it for any plan (tests), BSGD_NO_BLOCKED=1 never.
+template <typename V>
+static int build_blocked(bsgd_plan *p, cudaStream_t st) {
+    const char *force = getenv("BSGD_BLOCKED");
+    const bool forced = force && strcmp(force, "force") == 0;
+    if (p->stacked() || p->rows == 0 || p->g_fwd != 32 || getenv("BSGD_NO_BLOCKED") ||
+        ((double)p->nnz / (double)p->rows < 384.0 && !forced))
+        return BSGD_OK;
+    bsgd_plan::BlkStore b;
+    void *temp = nullptr;
+    size_t temp_bytes = 0;
+    int64_t total = 0;
+    auto bail = [&](cudaError_t e) -> int {
+        cudaGetLastError();
+        cudaFree(temp);
+        blk_free(b);
+        if (e == cudaErrorMemoryAllocation) return BSGD_OK;   // keep the unblocked kernel
+        return fail(BSGD_ECUDA, "blocked stream build failed: %s", cudaGetErrorString(e));
+    };
+    cudaError_t e = cudaMalloc(&b.ptr, sizeof(int64_t) * (p->rows + 1));
+    if (e != cudaSuccess) return bail(e);
+    blk_len_kernel<<<grid_1d(p->rows), kThreads, 0, st>>>(p->rows, p->f_ptr, b.ptr);
+    e = cub::DeviceScan::ExclusiveSum(nullptr, temp_bytes, b.ptr, b.ptr, p->rows + 1, st);
+    if (e == cudaSuccess) e = cudaMalloc(&temp, temp_bytes);
+    if (e == cudaSuccess) e = cudaMemsetAsync(b.ptr + p->rows, 0, sizeof(int64_t), st);
+    if (e == cudaSuccess) e = cub::DeviceScan::ExclusiveSum(temp, temp_bytes, b.ptr, b.ptr, p->rows + 1, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&total, b.ptr + p->rows, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return bail(e);
+    cudaFree(temp);
+    temp = nullptr;
+    e = cudaMalloc(&b.idx, sizeof(int32_t) * std::max<int64_t>(total, 1));
+    if (e == cudaSuccess) e = cudaMalloc(&b.val, sizeof(V) * std::max<int64_t>(total, 1));
+    if (e != cudaSuccess) return bail(e);
+    blk_fill_kernel<V><<<grid_1d(p->rows, kThreads / 32), kThreads, 0, st>>>(
+        p->rows, p->f_ptr, p->f_idx, (const V *)p->f_val, b.ptr, b.idx, (V *)b.val);
+    e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return bail(e);
+    b.bytes = sizeof(int64_t) * (p->rows + 1) + (sizeof(int32_t) + sizeof(V)) * (size_t)total;
+    b.ok = true;
+    p->fb = b;
+    p->device_bytes += b.bytes;
+    return BSGD_OK;
+}
 
 // ---------------------------------------------------------------------------
 // panel-tiled format (tiled.cuh)
@@ -764,10 +827,27 @@ static int launch_gtile(const bsgd_plan::GTileStore &S, const double *vec, const
 static bool gtiles_on(const bsgd_plan::GTileStore &S) { return S.ok && !getenv("BSGD_NO_GATHER_TILES"); }
 
 template <typename V, class E>
+static int launch_blocked(const bsgd_plan *p, const double *vec, const E &e, double *part, int64_t *cnt,
+                          cudaStream_t st) {
+    auto kern = csr_blocked_kernel<V, E>;
+    const int cap = std::min(occupancy(kern) * num_sms(), kMaxPartials);
+    const int grid = ctas_for(p->rows, 32, cap);
+    kern<<<grid, kThreads, 0, st>>>(CsrB<V>{p->rows, p->fb.ptr, p->fb.idx, (const V *)p->fb.val, vec}, e, part, cnt);
+    LAUNCHED();
+    return BSGD_OK;
+}
+
+static bool blocked_on(const bsgd_plan *p) {
+    static const bool off = getenv("BSGD_NO_BLOCKED") != nullptr;
+    return p->fb.ok && !off;
+}
+
+template <typename V, class E>
 static int launch_fwd(const bsgd_plan *p, const double *vec, const E &e, double *part, int64_t *cnt, cudaStream_t st) {
     if (p->stacked()) return launch_stacked_dir<V>(p, false, vec, e, part, cnt, st);
     if (gtiles_on(p->gf)) return launch_gtile<V>(p->gf, vec, e, part, cnt, st);
     if (tiled_usable(p, p->tf, vec)) return launch_tiled<V>(p->tf, vec, e, part, cnt, st);
+    if (blocked_on(p)) return launch_blocked<V>(p, vec, e, part, cnt, st);
     return launch_one<V>(fwd_csr<V>(p, vec), p->g_fwd, e, part, cnt, p->nnz, st);
 }
 
@@ -1497,6 +1577,8 @@ static int plan_finish(bsgd_plan *p, cudaStream_t st) {
         return fail(BSGD_EINVAL, "CSR is not canonical (code %d: 1=indptr, 2=index range, 4=unsorted/duplicate)", bad);
     }
     rc = (value_dtype == BSGD_F32) ? build_transpose<float>(p, st) : build_transpose<double>(p, st);
+    if (rc != BSGD_OK) return rc;
+    rc = (value_dtype == BSGD_F32) ? build_blocked<float>(p, st) : build_blocked<double>(p, st);
     if (rc != BSGD_OK) return rc;
     {
         // panel-tiled copies (tiled.cuh) are an opt-in experiment: on every
@@ -2423,7 +2505,8 @@ int bsgd_epoch(const bsgd_plan *p, const bsgd_epoch_args *a, void *stream) {
         rc = run_step(p->cols, a, ws, st);
         if (!rc && (fl & BSGD_EP_R_NEXT))
             rc = DISPATCH_V(p, launch_fwd<V>(p, a->x_k, EpiResid{a->y, a->r_next}, ws.rpart, ws.ctl + 2, st));
-    } else if ((fl & BSGD_EP_R_NEXT) && (tiled || p->stacked() || p->gf.ok || p->gt.ok || !getenv("BSGD_MERGE_K1K2"))) {
+    } else if ((fl & BSGD_EP_R_NEXT) &&
+               (tiled || p->stacked() || p->gf.ok || p->gt.ok || blocked_on(p) || !getenv("BSGD_MERGE_K1K2"))) {
         // K1(x_k) then K2(r_k) on the stream.  One merged grid (below, opt-in) reads the
         // same snapshot but measured slower on configs[1] (0.79 vs 0.66 ms per epoch):
         // both halves are gather-bound and the CTA split balances them poorly

@@ -222,6 +222,105 @@ __global__ void __launch_bounds__(kThreads) dual_csr_kernel(Csr<V> A, EA ea, dou
 }
 
 // ---------------------------------------------------------------------------
+// blocked stream (long rows, G = 32): each row padded to whole blocks of 128
+// entries, entry 32 m + l of a block stored at 4 l + m, so lane l fetches its
+// four lane-strided entries l, l + 32, l + 64, l + 96 with one 16-byte index
+// load and one 16-byte value load (float32; two for float64), two blocks in
+// flight.  The per-lane order is the unblocked kernel's (k = beg + l + 32 j),
+// so products are bit-identical to it; padding entries repeat the row's last
+// column with value 0.  The unblocked G = 32 loop stalls on its 4-byte index
+// loads before it can form the gather addresses (profiles/r01_ct_spmv.md).
+// ---------------------------------------------------------------------------
+constexpr int kBlk = 128;
+
+template <typename V>
+struct CsrB {
+    int64_t nrows;
+    const int64_t *ptr;   // [nrows + 1], multiples of kBlk
+    const int32_t *idx;
+    const V *val;
+    const double *vec;
+};
+
+__device__ __forceinline__ void blk_vals(const float *p, double (&v)[4], uint64_t pol) {
+    const float4 a = ld_stream4(p, pol);
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+}
+__device__ __forceinline__ void blk_vals(const double *p, double (&v)[4], uint64_t pol) {
+    const double2 a = ld_stream2(p, pol), b = ld_stream2(p + 2, pol);
+    v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+}
+
+template <typename V, class Epi>
+__global__ void __launch_bounds__(kThreads) csr_blocked_kernel(CsrB<V> A, Epi epi, double *part, int64_t *cnt) {
+    __shared__ double sm[8 * (kThreads / 32)];
+    const int lane = threadIdx.x & 31;
+    const uint64_t pol = policy_evict_first();
+    const double *__restrict__ vec = A.vec;
+    const int64_t nw = (int64_t)gridDim.x * (kThreads / 32);
+    for (int64_t row = (int64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5); row < A.nrows; row += nw) {
+        const int64_t beg = A.ptr[row], end = A.ptr[row + 1];
+        double s = 0.0;
+        int64_t k = beg + 4 * lane;
+        for (; k + kBlk < end; k += 2 * kBlk) {
+            const int4 ca = ld_stream4(A.idx + k, pol), cb = ld_stream4(A.idx + k + kBlk, pol);
+            double va[4], vb[4];
+            blk_vals(A.val + k, va, pol);
+            blk_vals(A.val + k + kBlk, vb, pol);
+            const double xa0 = __ldg(vec + ca.x), xa1 = __ldg(vec + ca.y), xa2 = __ldg(vec + ca.z),
+                         xa3 = __ldg(vec + ca.w), xb0 = __ldg(vec + cb.x), xb1 = __ldg(vec + cb.y),
+                         xb2 = __ldg(vec + cb.z), xb3 = __ldg(vec + cb.w);
+            s = fma(va[0], xa0, s); s = fma(va[1], xa1, s); s = fma(va[2], xa2, s); s = fma(va[3], xa3, s);
+            s = fma(vb[0], xb0, s); s = fma(vb[1], xb1, s); s = fma(vb[2], xb2, s); s = fma(vb[3], xb3, s);
+        }
+        if (k < end) {
+            const int4 ca = ld_stream4(A.idx + k, pol);
+            double va[4];
+            blk_vals(A.val + k, va, pol);
+            const double xa0 = __ldg(vec + ca.x), xa1 = __ldg(vec + ca.y), xa2 = __ldg(vec + ca.z),
+                         xa3 = __ldg(vec + ca.w);
+            s = fma(va[0], xa0, s); s = fma(va[1], xa1, s); s = fma(va[2], xa2, s); s = fma(va[3], xa3, s);
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+        if (lane == 0) epi(row, s);
+    }
+    if constexpr (Epi::K > 0) {
+        double v[Epi::K];
+        epi.flush(v);
+        block_sum<Epi::K>(v, sm);
+        if (threadIdx.x == 0 && part != nullptr)
+            for (int q = 0; q < Epi::K; ++q) part[(size_t)blockIdx.x * Epi::K + q] = v[q];
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0 && cnt != nullptr) cnt[0] = gridDim.x;
+}
+
+// padded row lengths (in blocks) for the blocked copy
+__global__ void blk_len_kernel(int64_t rows, const int64_t *ptr, int64_t *out) {
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x)
+        out[r] = (ptr[r + 1] - ptr[r] + kBlk - 1) / kBlk * kBlk;
+}
+
+// scatter a canonical CSR into the blocked layout (one warp per row)
+template <typename V>
+__global__ void __launch_bounds__(kThreads) blk_fill_kernel(int64_t rows, const int64_t *ptr, const int32_t *idx,
+                                                            const V *val, const int64_t *bptr, int32_t *bidx,
+                                                            V *bval) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = (int64_t)gridDim.x * (kThreads / 32);
+    for (int64_t r = (int64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5); r < rows; r += nw) {
+        const int64_t beg = ptr[r], len = ptr[r + 1] - beg, ob = bptr[r], plen = bptr[r + 1] - ob;
+        const int32_t last = len > 0 ? idx[beg + len - 1] : 0;
+        for (int64_t k = lane; k < plen; k += 32) {
+            const int64_t e = k % kBlk;
+            const int64_t o = ob + (k - e) + (e % 32) * 4 + e / 32;
+            bidx[o] = k < len ? idx[beg + k] : last;
+            bval[o] = k < len ? val[beg + k] : V(0);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // block-restricted products (blockops.py:207-223): rows [r0, r1) of a CSR,
 // entries with column in [c0, c1) (a contiguous run: indices are sorted).
 // out[row - r0] = sum A[row, c] vec[c - c0].  One warp per row.

@@ -288,3 +288,34 @@ def test_gather_tiles_match_csr(B, monkeypatch):
     assert rel(op.matvec(x), oop.matvec(x)) < 1e-12
     with pytest.raises(ValueError):
         op.set_gather_tiles(True, (np.array([0, 17]), np.arange(17)))
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_blocked_stream_bit_identical(B, monkeypatch, dtype):
+    """The blocked copy of A's stream (spmv.cuh csr_blocked_kernel) gives the
+    unblocked G = 32 kernel's products bit for bit (same per-lane order; padding
+    adds exact zeros), including rows shorter than a block and empty rows."""
+    blockops = B[0]
+    from paper_1812_01307_b200 import problems
+    a = problems.parallel_beam_matrix(96, 40, 137, dtype=dtype)   # long rows: G = 32
+    a = a.tolil()
+    a[3, :] = 0          # an empty row
+    a = a.tocsr()
+    a.eliminate_zeros()
+    part = blockops.make_partition(*a.shape, 2, 2)
+    monkeypatch.setenv("BSGD_NO_BLOCKED", "1")
+    plain = blockops.BlockOperator(a, part)
+    monkeypatch.delenv("BSGD_NO_BLOCKED")
+    monkeypatch.setenv("BSGD_BLOCKED", "force")
+    blk = blockops.BlockOperator(a, part)
+    oop = orc.OracleOperator(a, 2, 2)
+    rng = np.random.default_rng(11)
+    for _ in range(3):
+        x = rng.standard_normal(a.shape[1])
+        got = blk.matvec(x, charge=False)
+        assert np.array_equal(got, plain.matvec(x, charge=False))
+        assert rel(got, oop.matvec(x)) < 1e-12
+        y = rng.standard_normal(a.shape[0])
+        r1, s1 = blk.residual_sumsq(x, y)
+        r0, s0 = plain.residual_sumsq(x, y)
+        assert np.array_equal(r1.cpu().numpy(), r0.cpu().numpy())
