@@ -488,6 +488,42 @@ def run_ct_secondary(args, index):
     # value + momentum commit (read c, p, b; write q): 5*dim + 2 fields of 8 bytes
     pbytes = 8 * npx * ((5 * dim + 2) * d.max_inner_iters + 10)
     rows, cols = op.shape
+    products = None
+    if d.depth == 1:
+        # the two products alone on the plan's current kernels, CSR byte model of
+        # SURVEY.md §8(d) (float32 values, int32 indices, int64 row pointers, float64 vectors)
+        from paper_1812_01307_b200 import _native as nat
+        dev = torch.device("cuda", torch.cuda.current_device())
+        xv = torch.rand(cols, dtype=torch.float64, device=dev)
+        rv = torch.randn(rows, dtype=torch.float64, device=dev)
+        yv = torch.randn(rows, dtype=torch.float64, device=dev)
+        ro, go = torch.empty_like(rv), torch.empty_like(xv)
+        sp = nat.stream_ptr(dev)
+
+        def tk(fn, reps=10):
+            for _ in range(2):
+                fn()
+            torch.cuda.synchronize()
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record()
+            for _ in range(reps):
+                fn()
+            a1.record()
+            torch.cuda.synchronize()
+            return a0.elapsed_time(a1) / reps
+
+        t1 = tk(lambda: nat.call("bsgd_residual", op.plan, nat.ptr(xv), nat.ptr(yv), nat.ptr(ro), None, None, sp))
+        t2 = tk(lambda: nat.call("bsgd_grad", op.plan, nat.ptr(rv), nat.ptr(go), sp))
+        nnz = int(op.nnz)
+        b1 = nnz * 8 + (rows + 1) * 8 + cols * 8 + 2 * rows * 8
+        b2 = nnz * 8 + (cols + 1) * 8 + rows * 8 + cols * 8
+        peak, _ = peaks()
+        products = {"k1_forward": {"kernel": "blocked CSR (csr_blocked_kernel)", "ms": round(t1, 4), "bytes": b1,
+                                   "gbs": round(b1 / (t1 * 1e6), 1), "frac": round(b1 / (t1 * 1e6) / peak, 4)},
+                    "k2_transposed": {"kernel": "gather-tiled, blocked stream (gtile_kernel)", "ms": round(t2, 4),
+                                      "bytes": b2, "gbs": round(b2 / (t2 * 1e6), 1),
+                                      "frac": round(b2 / (t2 * 1e6) / peak, 4)},
+                    "peak_gbs": peak, "byte_model": "SURVEY.md 8(d) CSR model: nnz*8 + pointers + vectors"}
     out = {"nnz": int(op.nnz), "epochs_per_s": round(1000.0 / ms, 2), "ms_per_epoch": round(ms, 4),
            "monitor_decrease": False, "mean_fgp_iterations": round(fgp_iters, 2),
            "tv_prox": {"image": "x".join(str(v) for v in shape), "iterations": d.max_inner_iters,
@@ -496,6 +532,8 @@ def run_ct_secondary(args, index):
                                 if dim == 2 else
                                 "fields stream from HBM (134 MB each); latency-bound at 16 warps/SM, "
                                 "profiles/r01_c5.md")}}
+    if products is not None:
+        out["products"] = products
     if d.depth > 1:
         # stacked operator: two products per epoch, each applies every logical nonzero
         # once (a multiply and an add in float64) reading its vector value from L2
