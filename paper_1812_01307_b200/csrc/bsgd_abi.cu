@@ -647,6 +647,7 @@ static int launch_one(const Csr<V> &A, int G, const E &e, double *part, int64_t 
                       cudaStream_t st) {
     const Csr<V> none{0, nullptr, nullptr, nullptr, nullptr};
     if (G == 8) return launch_dual<V, 8, 8, E, EpiNone>(A, e, part, cnt, nnz, none, EpiNone{}, nullptr, nullptr, 0, st);
+    if (G == 4) return launch_dual<V, 4, 8, E, EpiNone>(A, e, part, cnt, nnz, none, EpiNone{}, nullptr, nullptr, 0, st);
     return launch_dual<V, 32, 8, E, EpiNone>(A, e, part, cnt, nnz, none, EpiNone{}, nullptr, nullptr, 0, st);
 }
 
@@ -654,13 +655,22 @@ template <typename V, class EA, class EB>
 static int launch_two(const Csr<V> &A, int GA, const EA &ea, double *partA, int64_t *cntA, int64_t nnzA,
                       const Csr<V> &B, int GB, const EB &eb, double *partB, int64_t *cntB, int64_t nnzB,
                       cudaStream_t st) {
-    if (GA == 8 && GB == 8)
-        return launch_dual<V, 8, 8, EA, EB>(A, ea, partA, cntA, nnzA, B, eb, partB, cntB, nnzB, st);
-    if (GA == 8)
-        return launch_dual<V, 8, 32, EA, EB>(A, ea, partA, cntA, nnzA, B, eb, partB, cntB, nnzB, st);
-    if (GB == 8)
-        return launch_dual<V, 32, 8, EA, EB>(A, ea, partA, cntA, nnzA, B, eb, partB, cntB, nnzB, st);
-    return launch_dual<V, 32, 32, EA, EB>(A, ea, partA, cntA, nnzA, B, eb, partB, cntB, nnzB, st);
+    // lanes per row of each part: 4, 8 or 32 (the plan's choices)
+    auto go = [&](auto ga, auto gb) {
+        return launch_dual<V, decltype(ga)::value, decltype(gb)::value, EA, EB>(A, ea, partA, cntA, nnzA, B, eb,
+                                                                               partB, cntB, nnzB, st);
+    };
+    using G4 = std::integral_constant<int, 4>;
+    using G8 = std::integral_constant<int, 8>;
+    using G32 = std::integral_constant<int, 32>;
+    auto second = [&](auto ga) {
+        if (GB == 4) return go(ga, G4{});
+        if (GB == 8) return go(ga, G8{});
+        return go(ga, G32{});
+    };
+    if (GA == 4) return second(G4{});
+    if (GA == 8) return second(G8{});
+    return second(G32{});
 }
 
 // Keep the tiled copy of a direction only if it beats the CSR kernel on this
@@ -1677,8 +1687,15 @@ static bsgd_plan *plan_new(int device, int64_t rows, int64_t cols, int64_t nnz, 
     p->col_bounds.assign(col_bounds, col_bounds + N + 1);
     p->srows = rows; p->scols = cols; p->snnz = nnz;
     const double mean_r = (double)nnz / rows, mean_c = (double)nnz / cols;
-    p->g_fwd = mean_r < 64.0 ? 8 : 32;
-    p->g_tr = mean_c < 64.0 ? 8 : 32;
+    // lanes per row: short rows take 8-16 entries per lane through 16-byte loads
+    // (configs[1]: 32-nnz rows G = 4, 0.291 -> 0.267 ms; 128-nnz columns G = 8,
+    // 0.289 -> 0.277 ms, tools/gsweep.py), long rows (CT) a full warp
+    auto pick = [](double mean) { return mean < 48.0 ? 4 : (mean < 256.0 ? 8 : 32); };
+    p->g_fwd = pick(mean_r);
+    p->g_tr = pick(mean_c);
+    auto lanes = [](const char *e) { const int v = atoi(e); return (v == 4 || v == 8) ? v : 32; };
+    if (const char *e = getenv("BSGD_G_TR")) p->g_tr = lanes(e);   // experiments
+    if (const char *e = getenv("BSGD_G_FWD")) p->g_fwd = lanes(e);
     return p;
 }
 

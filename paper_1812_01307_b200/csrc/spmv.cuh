@@ -5,8 +5,8 @@
 // Both are the same row-product over a CSR stream with a fused epilogue.
 //
 // Mapping: a warp owns 32/G consecutive rows per pass, G lanes per row
-// (G = 8 for short rows such as the 32-nnz random system, 32 for CT rows of
-// ~100-900 nnz).  Each lane streams a strided slice of its row's (index,
+// (G = 4 for rows under 48 nonzeros such as the 32-nnz random system, 8 under
+// 256, 32 for CT rays of ~400-1800).  Each lane streams a strided slice of its row's (index,
 // value) pairs with L1-bypassing evict-first loads, gathers the vector
 // through the read-only path (the vector stays L2-resident), and accumulates
 // in float64.  The in-row reduction is a fixed shuffle tree, so results are
@@ -117,8 +117,8 @@ __device__ __forceinline__ void csr_rows(const Csr<V> &A, int64_t warp_id, int64
             if constexpr (sizeof(V) == 4 && G <= 8) {
                 // short rows: 16-byte streaming loads over the 4-aligned body of the row:
                 // one L1 request moves 4 (index, value) pairs, leaving the L1 tag stage to
-                // the random gathers (profiles/r01_spmv_baseline.md); measured -9% on the
-                // configs[1] forward product, +4% on 128-nnz rows, hence G <= 8 only
+                // the random gathers (profiles/r01_spmv_baseline.md).  Used with G = 4 / 8
+                // (8-16 entries per lane); with 32 lanes on 128-nnz rows it measured +4%
                 const int64_t b4 = (beg + 3) & ~(int64_t)3;
                 const int64_t e4 = end & ~(int64_t)3;
                 if (b4 < e4) {

@@ -297,7 +297,7 @@ def test_blocked_stream_bit_identical(B, monkeypatch, dtype):
     adds exact zeros), including rows shorter than a block and empty rows."""
     blockops = B[0]
     from paper_1812_01307_b200 import problems
-    a = problems.parallel_beam_matrix(96, 40, 137, dtype=dtype)   # long rows: G = 32
+    a = problems.parallel_beam_matrix(256, 24, 363, dtype=dtype)   # rays of ~290 nonzeros: G = 32
     a = a.tolil()
     a[3, :] = 0          # an empty row
     a = a.tocsr()
