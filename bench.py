@@ -264,7 +264,10 @@ def run_ours(args):
     prof = os.path.join(REPO, "profiles", "roofline_traffic.json")
     if os.path.exists(prof):
         with open(prof) as fh:
-            traffic = json.load(fh).get("dram_bytes_per_launch")
+            tr = json.load(fh)
+        # per-kernel DRAM bytes of one ncu --set full capture (k1 / k2), else the legacy single value
+        traffic = tr.get("k1" if t_k1 >= t_k2 else "k2", {}).get("dram_bytes_per_launch",
+                                                                 tr.get("dram_bytes_per_launch"))
     roofline = {"bound": "hbm", "kernel": dominant[0], "achieved": round(dominant[3], 1), "peak": peak,
                 "unit": "GB/s", "frac": round(dominant[3] / peak, 4), "traffic": traffic,
                 "algorithmic_bytes": dominant[1], "launch_ms": round(dominant[2], 5), "peak_source": peak_src,
