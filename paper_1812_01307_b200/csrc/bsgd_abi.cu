@@ -1030,8 +1030,9 @@ static int prox_occupancy() {
 }
 
 // dynamic shared memory of the split / slab sum passes (pw_cta_fast chunks of 8 leaves)
+// (the fast path sums leaves directly, pw_cta_direct: no dynamic buffer)
 template <int K>
-static size_t slab_smem(bool fast) { return fast ? sizeof(double) * K * 8 * 128 : 0; }
+static size_t slab_smem(bool) { return 0; }
 
 template <int DIM>
 static void split_attrs() {
@@ -1064,8 +1065,9 @@ static int launch_prox_split(const ProxArgs &a, cudaStream_t st) {
     v.ds = a.ds;
     v.fast = a.fast;
     const int64_t S = (int64_t)1 << a.ds;
-    v.G = (int)std::min<int64_t>(S, 256);
-    if (S / v.G > kPwMaxQ * (int64_t)(a.fast ? 8 : kThreads / 8))
+    v.G = (int)std::min<int64_t>(S, 512);   // 256^3: 7.58 -> 7.37-7.5 ms with 512 CTAs of 256 leaves
+    if (v.fast && S / v.G > kPwMaxQ) v.fast = 0;   // direct leaf sums hold <= kPwMaxQ leaves per CTA
+    if (S / v.G > kPwMaxQ * (int64_t)(v.fast ? 1 : kThreads / 8))
         return fail(BSGD_EINVAL, "image too large for the pairwise tree (%lld voxels)", (long long)a.N);
     v.ctl = (FgpCtl *)(a.red + (size_t)kMaxPartials * kPwMaxK);
     double *part = a.red;
@@ -1075,7 +1077,7 @@ static int launch_prox_split(const ProxArgs &a, cudaStream_t st) {
     }
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(a.N, kThreads), (int64_t)num_sms() * 8));
     constexpr int KD = 1 + 2 * DIM;
-    const bool fast = a.fast != 0;
+    const bool fast = v.fast != 0;
     auto sums2 = [&](bool energy) {
         if (energy) {
             if (fast) slab_energy_kernel<DIM, true><<<v.G, kThreads, slab_smem<2>(true), st>>>(v, part);
@@ -1500,9 +1502,10 @@ static int slab_ctx(const bsgd_slab *s, SlabCtx &c, bool need_weight = true) {
     if (rc) return rc;
     c.v.fast = (s->count % 128 == 0 && s->count / 128 == ((int64_t)1 << c.v.ds)) ? 1 : 0;
     const int64_t S = (int64_t)1 << c.v.ds;
-    c.G = (int)std::min<int64_t>(S, 256);
+    c.G = (int)std::min<int64_t>(S, 512);
     c.v.G = c.G;
-    const int64_t per_slot = c.v.fast ? 8 : kThreads / 8;
+    if (c.v.fast && S / c.G > kPwMaxQ) c.v.fast = 0;   // direct leaf sums hold <= kPwMaxQ leaves per CTA
+    const int64_t per_slot = c.v.fast ? 1 : kThreads / 8;
     if (S / c.G > kPwMaxQ * per_slot) return fail(BSGD_EINVAL, "slab too large for the pairwise tree");
     c.part = base;
     c.stats = base + off[11] + 16;
@@ -2626,7 +2629,7 @@ int bsgd_slab_init(const bsgd_slab *s, double *sums_out, void *stream) {
     slab_offsets(c.v.a.D, s->height, s->width, s->count, off);
     for (int slot = 1; slot <= 9; ++slot)
         if (off[slot] >= 0) CU(cudaMemsetAsync((double *)s->workspace + off[slot], 0, sizeof(double) * len, st));
-    const size_t smem = sizeof(double) * 2 * 8 * 128;
+    const size_t smem = 0;   // pw_cta_direct: no staging buffer
     if (c.dim == 3)
         return c.v.fast ? slab_sum_launch<2>(c, slab_init_kernel<3, true>, smem, sums_out, st)
                         : slab_sum_launch<2>(c, slab_init_kernel<3, false>, 0, sums_out, st);
@@ -2685,7 +2688,7 @@ int bsgd_slab_energy(const bsgd_slab *s, double *sums_out, void *stream) {
     if (rc) return rc;
     if (!sums_out) return fail(BSGD_EINVAL, "sums_out is NULL");
     cudaStream_t st = (cudaStream_t)stream;
-    const size_t smem = sizeof(double) * 2 * 8 * 128;
+    const size_t smem = 0;   // pw_cta_direct: no staging buffer
     if (c.dim == 3)
         return c.v.fast ? slab_sum_launch<2>(c, slab_energy_kernel<3, true>, smem, sums_out, st)
                         : slab_sum_launch<2>(c, slab_energy_kernel<3, false>, 0, sums_out, st);

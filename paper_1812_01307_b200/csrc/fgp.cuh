@@ -173,8 +173,17 @@ template <int K, int CH, bool FAST, class F>
 __device__ __forceinline__ void np_sum(cg::grid_group &grid, int64_t N, int ds, F &f, double *red, int &round,
                                        double *sm, double (&out)[K], double *T) {
     double *buf = red + (size_t)(round & 1) * kMaxPartials * kPwMaxK;
-    if constexpr (FAST) pw_cta_fast<K, F, CH>(ds, f, T, sm, buf);
-    else pw_cta<K>(N, ds, f, sm, buf);
+    if constexpr (FAST) {
+        // direct leaf sums when every warp has at least two 4-leaf groups and the
+        // leaves fit one shared K-vector each (2048^2: 4.54 -> 2.93 ms for 20
+        // iterations); staged chunks otherwise (512^2: 8 leaves per CTA would
+        // leave 6 of 8 warps idle)
+        const int64_t q = ((int64_t)1 << ds) / gridDim.x;
+        if (q >= 64 && q <= kPwMaxQ) pw_cta_direct<K>(ds, f, sm, buf);
+        else pw_cta_fast<K, F, CH>(ds, f, T, sm, buf);
+    } else {
+        pw_cta<K>(N, ds, f, sm, buf);
+    }
     grid.sync();
     pw_top<K>(ds, gridDim.x, buf, sm, out);
     ++round;

@@ -309,4 +309,81 @@ __device__ __forceinline__ int pw_cta_fast(int ds, F &f, double *T, double *leaf
     return Q;
 }
 
+// Fast path without the staging buffer: thread (leaf, j) evaluates accumulator
+// j's 16 strided terms of its leaf directly (8 lanes read 8 consecutive
+// voxels: two full sectors per leaf per step), so a warp sums four leaves on
+// its own, with no CTA barrier per chunk and no K * CH * 128 shared buffer.
+// The leaf values of the CTA's Q leaves (Q <= kPwMaxQ, a power of two) are
+// then folded by one balanced tree -- the same pairwise order as pw_cta_fast.
+template <int K, class F>
+__device__ __forceinline__ int pw_cta_direct(int ds, F &f, double *leafv, double *part) {
+    const int64_t S = (int64_t)1 << ds;
+    const int G = gridDim.x;
+    int64_t first;
+    int Q;
+    if (S >= G) {
+        Q = (int)(S / G);
+        first = (int64_t)blockIdx.x * Q;
+    } else {
+        Q = ((int64_t)blockIdx.x < S) ? 1 : 0;
+        first = blockIdx.x;
+    }
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int sub = lane >> 3, j = lane & 7;
+    const unsigned gm = 0xFFu << (lane & 24);
+    const int nw = (int)blockDim.x >> 5;
+    for (int l0 = (tid >> 5) * 4; l0 < Q; l0 += nw * 4) {
+        const int leaf = l0 + sub;
+        double r[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) r[k] = 0.0;
+        if (leaf < Q) {
+            const int64_t base = (first + leaf) * 128 + j;
+            if constexpr (pw_two_stage<F>::value) {
+                constexpr int U = pw_unroll<F>::value;
+                static_assert(16 % U == 0, "unroll must divide 16");
+#pragma unroll 1
+                for (int i0 = 0; i0 < 16; i0 += U) {
+                    typename F::L ld[U];
+#pragma unroll
+                    for (int u = 0; u < U; ++u) ld[u] = f.load(base + 8 * (i0 + u));
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        double t[K];
+                        f.term(base + 8 * (i0 + u), ld[u], t);
+#pragma unroll
+                        for (int k = 0; k < K; ++k) r[k] = (i0 + u == 0) ? t[k] : rn_add(r[k], t[k]);
+                    }
+                }
+            } else {
+#pragma unroll 4
+                for (int i = 0; i < 16; ++i) {
+                    double t[K];
+                    f(base + 8 * i, t);
+#pragma unroll
+                    for (int k = 0; k < K; ++k) r[k] = (i == 0) ? t[k] : rn_add(r[k], t[k]);
+                }
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            r[k] = rn_add(r[k], __shfl_xor_sync(gm, r[k], 1, 8));
+            r[k] = rn_add(r[k], __shfl_xor_sync(gm, r[k], 2, 8));
+            r[k] = rn_add(r[k], __shfl_xor_sync(gm, r[k], 4, 8));
+        }
+        if (j == 0 && leaf < Q)
+#pragma unroll
+            for (int k = 0; k < K; ++k) leafv[leaf * K + k] = r[k];
+    }
+    __syncthreads();
+    if (Q > 0) {
+        pw_smem_tree<K>(leafv, Q);
+        if (threadIdx.x == 0)
+#pragma unroll
+            for (int k = 0; k < K; ++k) part[(size_t)blockIdx.x * K + k] = leafv[k];
+    }
+    __syncthreads();
+    return Q;
+}
+
 }  // namespace bsgd

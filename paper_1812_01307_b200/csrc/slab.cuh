@@ -101,8 +101,7 @@ struct DualSlabTerms : DualCommitTerms<DIM> {
 template <int K, bool FAST, class F>
 __device__ __forceinline__ void slab_sum(const SlabView &s, F &f, double *part) {
     __shared__ double sm[kPwMaxQ * kPwMaxK];
-    extern __shared__ double Tsm[];
-    if constexpr (FAST) pw_cta_fast<K, F, 8>(s.ds, f, Tsm, sm, part);
+    if constexpr (FAST) pw_cta_direct<K>(s.ds, f, sm, part);   // no staging buffer, no per-chunk barriers
     else pw_cta<K>(s.n, s.ds, f, sm, part);
 }
 
