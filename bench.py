@@ -358,15 +358,25 @@ def run_multi(args):
     cfg = SolverConfig(mu=mu, lam=0.0, epochs=10 ** 9, monitor_decrease=False)
     cap = args.steps + args.warmup + 64
     drv = parallel.DistributedBSGD(shard, d.y, cfg, history_capacity=cap)
-    for _ in range(args.warmup):
+    for _ in range(max(1, args.warmup)):
         drv.epoch_step()
+    # two epochs (kernels + NCCL all-reduces) per CUDA graph: no per-epoch host work
+    graphed = drv.capture(2)
+    if graphed:
+        drv.replay()
     torch.cuda.synchronize()
     dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with Clocks(local) as clk:
         e0.record()
-        for _ in range(args.steps):
-            drv.epoch_step()
+        if graphed:
+            for _ in range(args.steps // 2):
+                drv.replay()
+            if args.steps % 2:
+                drv.epoch_step()
+        else:
+            for _ in range(args.steps):
+                drv.epoch_step()
         e1.record()
         torch.cuda.synchronize()
     ms = torch.tensor([e0.elapsed_time(e1)], device=dev)

@@ -245,6 +245,8 @@ class DistributedBSGD:
         self.perm = perm
         self.slab = None
         self.slabs = None
+        self._graph = None
+        self._graph_epochs = 0
         if prox not in ("auto", "slab", "replicated"):
             raise ValueError(f"unknown prox mode {prox!r}")
         dims = shard.prox_dims() if (cfg.lam > 0 and hasattr(shard, "prox_dims")) else None
@@ -273,14 +275,56 @@ class DistributedBSGD:
         if self.dist.is_initialized() and self.dist.get_world_size(self.group) > 1:
             self.dist.all_reduce(tensor, op=self.dist.ReduceOp.SUM, group=self.group)
 
+    def _schedule(self):
+        """Advance the pair-order RNG exactly as the reference does (solvers.py:176-195)."""
+        from .solvers import schedule_pairs
+        sp = self.s.spec.partition
+        schedule_pairs(sp.num_row_blocks, sp.num_col_blocks, 1.0, 1.0, self.rng)
+
     def epoch_step(self, monitor: bool | None = None):
         """One epoch; returns the history row index written."""
-        from .solvers import schedule_pairs
+        self._schedule()
+        return self._epoch(monitor)
+
+    def capture(self, epochs: int = 2, monitor: bool | None = None) -> bool:
+        """Capture ``epochs`` (even: the x / r rings flip every epoch) epochs,
+        collectives included, into one CUDA graph for `replay`.  Needs the
+        collectives warmed up by at least one eager epoch; not available with
+        the slab prox (its FGP decisions are taken on the host).  Returns
+        whether a graph is ready."""
+        if self.slab is not None or epochs < 2 or epochs % 2:
+            return False
+        t = self.s.t
+        saved = (self.xi, self.ri, self.rows_used, self.epoch)
+        g = t.cuda.CUDAGraph()
+        try:
+            side = t.cuda.Stream(device=self.y.device)
+            side.wait_stream(t.cuda.current_stream(self.y.device))
+            with t.cuda.graph(g, stream=side):
+                for _ in range(epochs):
+                    self._epoch(monitor)
+        except Exception:
+            self._graph = None
+            return False
+        finally:
+            self.xi, self.ri, self.rows_used, self.epoch = saved
+        self._graph = g
+        self._graph_epochs = epochs
+        return True
+
+    def replay(self):
+        """Run the captured epochs (same arithmetic as `epoch_step`, one launch)."""
+        for _ in range(self._graph_epochs):
+            self._schedule()
+        self._graph.replay()
+        self.rows_used += self._graph_epochs
+        self.epoch += float(self._graph_epochs)
+
+    def _epoch(self, monitor: bool | None = None):
         cfg = self.cfg
         s = self.s
         if monitor is None:
             monitor = cfg.monitor_decrease or cfg.enforce_decrease
-        schedule_pairs(s.spec.partition.num_row_blocks, s.spec.partition.num_col_blocks, 1.0, 1.0, self.rng)
         xi, ri = self.xi, self.ri
         x_k, x_next = self.x[xi], self.x[1 - xi]
         r_k, r_ahead = self.r[ri], self.r[ri]

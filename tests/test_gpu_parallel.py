@@ -166,3 +166,46 @@ def test_two_stacked_shards_emulated_match_oracle(cuda_ok):
     assert rel(x0, st.x) < 1e-12
     r = np.concatenate([d.r_current.cpu().numpy() for d in drvs])
     assert rel(r, st.r_vec) < 1e-12
+
+
+@pytest.mark.parametrize("with_nccl", [False, True])
+def test_driver_graph_replay_matches_eager(cuda_ok, with_nccl):
+    """DistributedBSGD.capture / replay (two epochs, NCCL all-reduces included, in
+    one CUDA graph) gives the eager epochs' iterates and history bit for bit."""
+    import torch
+    import torch.distributed as dist
+    from paper_1812_01307_b200 import parallel
+    from paper_1812_01307_b200.blockops import make_partition
+    from paper_1812_01307_b200.solvers import SolverConfig
+    z = load_golden("p3_ls")
+    c = golden_cfg(z)
+    a = golden_csr(z)
+    m, n = (int(v) for v in z["mn"])
+    part = make_partition(a.shape[0], a.shape[1], m, n)
+    if with_nccl:
+        dist.init_process_group("nccl", store=dist.HashStore(), rank=0, world_size=1,
+                                device_id=torch.device("cuda", 0))
+    try:
+        runs = []
+        for graphed in (False, True):
+            shard = parallel.CudaShard(a, parallel.ShardSpec(part, 0, 1))
+            cfg = SolverConfig(mu=c["mu"], lam=0.0, epochs=20, monitor_decrease=True)
+            drv = parallel.DistributedBSGD(shard, z["y"], cfg, x_true=z["x_true"], history_capacity=32)
+            drv.epoch_step()
+            if graphed:
+                assert drv.capture(2)
+                for _ in range(3):
+                    drv.replay()
+            else:
+                for _ in range(6):
+                    drv.epoch_step()
+            torch.cuda.synchronize()
+            runs.append((drv.x_current.cpu().numpy(), drv.r_current.cpu().numpy(), drv.history(), drv.epoch,
+                         drv.rng.bit_generator.state["state"]["state"]))
+        (x0, r0, h0, e0, s0), (x1, r1, h1, e1, s1) = runs
+        assert np.array_equal(x0, x1) and np.array_equal(r0, r1)
+        assert h0.shape == h1.shape == (7, h0.shape[1]) and np.array_equal(h0, h1)
+        assert e0 == e1 == 7.0 and s0 == s1
+    finally:
+        if with_nccl:
+            dist.destroy_process_group()
