@@ -84,3 +84,24 @@ def test_tv_value3_and_difference_operators(tv):
     # adjointness <grad u, p> = -<u, div p>
     lhs = sum(float(np.sum(a * b)) for a, b in zip((dz, dv, dh), p))
     assert lhs == pytest.approx(-float(np.sum(vol * div)), rel=1e-12)
+
+
+@pytest.mark.parametrize("shape,w,iters", [((2048, 2048), 0.05, 4), ((128, 128, 128), 0.05, 3),
+                                           ((4, 1024, 512), 0.1, 3)])
+def test_prox_direct_leaf_sums_bit_exact(tv, shape, w, iters):
+    """Sizes whose numpy-order sums take the barrier-free direct leaf path
+    (pairwise.cuh pw_cta_direct): the cooperative kernel at 2048^2 (128 leaves per
+    CTA) and the split prox at >= 2^21 voxels (512 CTAs)."""
+    arr = np.random.default_rng(len(shape) * 7 + iters).random(shape) * 2.0
+    if len(shape) == 2:
+        import torch
+        out, info = tv.tv_prox(torch.tensor(arr, device="cuda"), w, tv.ProxSettings(iters, 1e-12), return_info=True)
+        ref, rep = orc.tv_prox(arr, w, iters, 1e-12)
+        got = out.cpu().numpy()
+    else:
+        out, info = tv.tv_prox(tv.VolumeGrid.from_array(arr), w, tv.ProxSettings(iters, 1e-12), return_info=True)
+        ref, rep = orc.tv_prox3(arr, w, iters, 1e-12)
+        got = out.as_array()
+    assert np.array_equal(got, ref)
+    assert (info.iterations, info.restarts, info.fell_back) == (rep.iterations, rep.restarts, rep.fell_back)
+    assert np.array_equal(np.array(info.dual_objectives), np.array(rep.dual_objectives))
