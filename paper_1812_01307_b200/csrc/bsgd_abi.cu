@@ -207,6 +207,7 @@ struct bsgd_plan {
     // blocked copy of A's stream for long rows (spmv.cuh csr_blocked_kernel)
     struct BlkStore {
         bool ok = false;
+        int gb = 32;            // lanes per row (blocks of 4 gb entries)
         int64_t *ptr = nullptr;
         int32_t *idx = nullptr;
         void *val = nullptr;
@@ -389,6 +390,17 @@ static int build_blocked(bsgd_plan *p, cudaStream_t st) {
         ((double)p->nnz / (double)p->rows < 384.0 && !forced))
         return BSGD_OK;
     bsgd_plan::BlkStore b;
+    // Few lanes per ray, several adjacent rays per warp: the neighbouring bins of
+    // a steep ray read the same sectors in the same gather instruction (one L1
+    // tag lookup instead of one per warp).  K1 at configs[3] (~920 nnz/row):
+    // 32 lanes 4.03 ms, 16: 3.57, 8: 3.18, 4: 3.03; configs[2] (~460):
+    // 0.490 / 0.461 / 0.456 / 0.501 ms.
+    const double mean = (double)p->nnz / (double)p->rows;
+    b.gb = mean >= 768.0 ? 4 : 8;
+    if (const char *g = getenv("BSGD_BLK_G")) {   // experiments
+        const int v = atoi(g);
+        if (v == 4 || v == 8 || v == 16 || v == 32) b.gb = v;
+    }
     void *temp = nullptr;
     size_t temp_bytes = 0;
     int64_t total = 0;
@@ -401,7 +413,7 @@ static int build_blocked(bsgd_plan *p, cudaStream_t st) {
     };
     cudaError_t e = cudaMalloc(&b.ptr, sizeof(int64_t) * (p->rows + 1));
     if (e != cudaSuccess) return bail(e);
-    blk_len_kernel<<<grid_1d(p->rows), kThreads, 0, st>>>(p->rows, p->f_ptr, b.ptr);
+    blk_len_kernel<<<grid_1d(p->rows), kThreads, 0, st>>>(p->rows, p->f_ptr, 4 * b.gb, b.ptr);
     e = cub::DeviceScan::ExclusiveSum(nullptr, temp_bytes, b.ptr, b.ptr, p->rows + 1, st);
     if (e == cudaSuccess) e = cudaMalloc(&temp, temp_bytes);
     if (e == cudaSuccess) e = cudaMemsetAsync(b.ptr + p->rows, 0, sizeof(int64_t), st);
@@ -415,7 +427,7 @@ static int build_blocked(bsgd_plan *p, cudaStream_t st) {
     if (e == cudaSuccess) e = cudaMalloc(&b.val, sizeof(V) * std::max<int64_t>(total, 1));
     if (e != cudaSuccess) return bail(e);
     blk_fill_kernel<V><<<grid_1d(p->rows, kThreads / 32), kThreads, 0, st>>>(
-        p->rows, p->f_ptr, p->f_idx, (const V *)p->f_val, b.ptr, b.idx, (V *)b.val);
+        p->rows, p->f_ptr, p->f_idx, (const V *)p->f_val, b.ptr, b.idx, (V *)b.val, b.gb);
     e = cudaGetLastError();
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) return bail(e);
@@ -839,10 +851,15 @@ static bool gtiles_on(const bsgd_plan::GTileStore &S) { return S.ok && !getenv("
 template <typename V, class E>
 static int launch_blocked(const bsgd_plan *p, const double *vec, const E &e, double *part, int64_t *cnt,
                           cudaStream_t st) {
-    auto kern = csr_blocked_kernel<V, E>;
-    const int cap = std::min(occupancy(kern) * num_sms(), kMaxPartials);
-    const int grid = ctas_for(p->rows, 32, cap);
-    kern<<<grid, kThreads, 0, st>>>(CsrB<V>{p->rows, p->fb.ptr, p->fb.idx, (const V *)p->fb.val, vec}, e, part, cnt);
+    const CsrB<V> A{p->rows, p->fb.ptr, p->fb.idx, (const V *)p->fb.val, vec};
+    auto go = [&](auto kern, int G) {
+        const int cap = std::min(occupancy(kern) * num_sms(), kMaxPartials);
+        kern<<<ctas_for(p->rows, G, cap), kThreads, 0, st>>>(A, e, part, cnt);
+    };
+    if (p->fb.gb == 16) go(csr_blocked_kernel<V, 16, E>, 16);
+    else if (p->fb.gb == 8) go(csr_blocked_kernel<V, 8, E>, 8);
+    else if (p->fb.gb == 4) go(csr_blocked_kernel<V, 4, E>, 4);
+    else go(csr_blocked_kernel<V, 32, E>, 32);
     LAUNCHED();
     return BSGD_OK;
 }

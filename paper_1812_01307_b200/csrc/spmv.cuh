@@ -222,21 +222,22 @@ __global__ void __launch_bounds__(kThreads) dual_csr_kernel(Csr<V> A, EA ea, dou
 }
 
 // ---------------------------------------------------------------------------
-// blocked stream (long rows, G = 32): each row padded to whole blocks of 128
-// entries, entry 32 m + l of a block stored at 4 l + m, so lane l fetches its
-// four lane-strided entries l, l + 32, l + 64, l + 96 with one 16-byte index
-// load and one 16-byte value load (float32; two for float64), two blocks in
-// flight.  The per-lane order is the unblocked kernel's (k = beg + l + 32 j),
-// so products are bit-identical to it; padding entries repeat the row's last
-// column with value 0.  The unblocked G = 32 loop stalls on its 4-byte index
-// loads before it can form the gather addresses (profiles/r01_ct_spmv.md).
+// blocked stream (long rows): GB lanes per row, each row padded to whole blocks
+// of 4 GB entries, entry GB m + l of a block stored at 4 l + m, so lane l
+// fetches its four lane-strided entries l, l + GB, l + 2 GB, l + 3 GB with one
+// 16-byte index load and one 16-byte value load (float32; two for float64), two
+// blocks in flight; padding entries repeat the row's last column with value 0.
+// The unblocked G = 32 loop stalls on its 4-byte index loads before it can form
+// the gather addresses (profiles/r01_ct_spmv.md).  With GB = 32 the per-lane
+// order is the unblocked kernel's (bit-identical); the plan uses GB = 4 / 8 so
+// that one warp covers 8 / 4 adjacent rays, whose gathers share sectors inside
+// one instruction (tomographic rays of neighbouring bins).
 // ---------------------------------------------------------------------------
-constexpr int kBlk = 128;
-
+// lanes per row of the blocked kernel: GB lanes, blocks of 4 GB entries
 template <typename V>
 struct CsrB {
     int64_t nrows;
-    const int64_t *ptr;   // [nrows + 1], multiples of kBlk
+    const int64_t *ptr;   // [nrows + 1], multiples of the block (4 GB entries)
     const int32_t *idx;
     const V *val;
     const double *vec;
@@ -251,39 +252,46 @@ __device__ __forceinline__ void blk_vals(const double *p, double (&v)[4], uint64
     v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
 }
 
-template <typename V, class Epi>
+template <typename V, int GB, class Epi>
 __global__ void __launch_bounds__(kThreads) csr_blocked_kernel(CsrB<V> A, Epi epi, double *part, int64_t *cnt) {
+    constexpr int BLK = 4 * GB;
+    constexpr int RPW = 32 / GB;
     __shared__ double sm[8 * (kThreads / 32)];
     const int lane = threadIdx.x & 31;
+    const int sub = lane / GB, gl = lane % GB;
     const uint64_t pol = policy_evict_first();
     const double *__restrict__ vec = A.vec;
     const int64_t nw = (int64_t)gridDim.x * (kThreads / 32);
-    for (int64_t row = (int64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5); row < A.nrows; row += nw) {
-        const int64_t beg = A.ptr[row], end = A.ptr[row + 1];
+    for (int64_t base = ((int64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5)) * RPW; base < A.nrows;
+         base += nw * RPW) {
+        const int64_t row = base + sub;
         double s = 0.0;
-        int64_t k = beg + 4 * lane;
-        for (; k + kBlk < end; k += 2 * kBlk) {
-            const int4 ca = ld_stream4(A.idx + k, pol), cb = ld_stream4(A.idx + k + kBlk, pol);
-            double va[4], vb[4];
-            blk_vals(A.val + k, va, pol);
-            blk_vals(A.val + k + kBlk, vb, pol);
-            const double xa0 = __ldg(vec + ca.x), xa1 = __ldg(vec + ca.y), xa2 = __ldg(vec + ca.z),
-                         xa3 = __ldg(vec + ca.w), xb0 = __ldg(vec + cb.x), xb1 = __ldg(vec + cb.y),
-                         xb2 = __ldg(vec + cb.z), xb3 = __ldg(vec + cb.w);
-            s = fma(va[0], xa0, s); s = fma(va[1], xa1, s); s = fma(va[2], xa2, s); s = fma(va[3], xa3, s);
-            s = fma(vb[0], xb0, s); s = fma(vb[1], xb1, s); s = fma(vb[2], xb2, s); s = fma(vb[3], xb3, s);
-        }
-        if (k < end) {
-            const int4 ca = ld_stream4(A.idx + k, pol);
-            double va[4];
-            blk_vals(A.val + k, va, pol);
-            const double xa0 = __ldg(vec + ca.x), xa1 = __ldg(vec + ca.y), xa2 = __ldg(vec + ca.z),
-                         xa3 = __ldg(vec + ca.w);
-            s = fma(va[0], xa0, s); s = fma(va[1], xa1, s); s = fma(va[2], xa2, s); s = fma(va[3], xa3, s);
+        if (row < A.nrows) {
+            const int64_t beg = A.ptr[row], end = A.ptr[row + 1];
+            int64_t k = beg + 4 * gl;
+            for (; k + BLK < end; k += 2 * BLK) {
+                const int4 ca = ld_stream4(A.idx + k, pol), cb = ld_stream4(A.idx + k + BLK, pol);
+                double va[4], vb[4];
+                blk_vals(A.val + k, va, pol);
+                blk_vals(A.val + k + BLK, vb, pol);
+                const double xa0 = __ldg(vec + ca.x), xa1 = __ldg(vec + ca.y), xa2 = __ldg(vec + ca.z),
+                             xa3 = __ldg(vec + ca.w), xb0 = __ldg(vec + cb.x), xb1 = __ldg(vec + cb.y),
+                             xb2 = __ldg(vec + cb.z), xb3 = __ldg(vec + cb.w);
+                s = fma(va[0], xa0, s); s = fma(va[1], xa1, s); s = fma(va[2], xa2, s); s = fma(va[3], xa3, s);
+                s = fma(vb[0], xb0, s); s = fma(vb[1], xb1, s); s = fma(vb[2], xb2, s); s = fma(vb[3], xb3, s);
+            }
+            if (k < end) {
+                const int4 ca = ld_stream4(A.idx + k, pol);
+                double va[4];
+                blk_vals(A.val + k, va, pol);
+                const double xa0 = __ldg(vec + ca.x), xa1 = __ldg(vec + ca.y), xa2 = __ldg(vec + ca.z),
+                             xa3 = __ldg(vec + ca.w);
+                s = fma(va[0], xa0, s); s = fma(va[1], xa1, s); s = fma(va[2], xa2, s); s = fma(va[3], xa3, s);
+            }
         }
 #pragma unroll
-        for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-        if (lane == 0) epi(row, s);
+        for (int off = GB / 2; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+        if (gl == 0 && row < A.nrows) epi(row, s);
     }
     if constexpr (Epi::K > 0) {
         double v[Epi::K];
@@ -295,25 +303,25 @@ __global__ void __launch_bounds__(kThreads) csr_blocked_kernel(CsrB<V> A, Epi ep
     if (blockIdx.x == 0 && threadIdx.x == 0 && cnt != nullptr) cnt[0] = gridDim.x;
 }
 
-// padded row lengths (in blocks) for the blocked copy
-__global__ void blk_len_kernel(int64_t rows, const int64_t *ptr, int64_t *out) {
+// padded row lengths (whole blocks of blk entries) for the blocked copy
+__global__ void blk_len_kernel(int64_t rows, const int64_t *ptr, int blk, int64_t *out) {
     for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x)
-        out[r] = (ptr[r + 1] - ptr[r] + kBlk - 1) / kBlk * kBlk;
+        out[r] = (ptr[r + 1] - ptr[r] + blk - 1) / blk * blk;
 }
 
 // scatter a canonical CSR into the blocked layout (one warp per row)
 template <typename V>
 __global__ void __launch_bounds__(kThreads) blk_fill_kernel(int64_t rows, const int64_t *ptr, const int32_t *idx,
                                                             const V *val, const int64_t *bptr, int32_t *bidx,
-                                                            V *bval) {
+                                                            V *bval, int gb) {
     const int lane = threadIdx.x & 31;
     const int64_t nw = (int64_t)gridDim.x * (kThreads / 32);
     for (int64_t r = (int64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5); r < rows; r += nw) {
         const int64_t beg = ptr[r], len = ptr[r + 1] - beg, ob = bptr[r], plen = bptr[r + 1] - ob;
         const int32_t last = len > 0 ? idx[beg + len - 1] : 0;
         for (int64_t k = lane; k < plen; k += 32) {
-            const int64_t e = k % kBlk;
-            const int64_t o = ob + (k - e) + (e % 32) * 4 + e / 32;
+            const int64_t e = k % (4 * gb);
+            const int64_t o = ob + (k - e) + (e % gb) * 4 + e / gb;
             bidx[o] = k < len ? idx[beg + k] : last;
             bval[o] = k < len ? val[beg + k] : V(0);
         }

@@ -290,11 +290,14 @@ def test_gather_tiles_match_csr(B, monkeypatch):
         op.set_gather_tiles(True, (np.array([0, 17]), np.arange(17)))
 
 
-@pytest.mark.parametrize("dtype", [np.float32, np.float64])
-def test_blocked_stream_bit_identical(B, monkeypatch, dtype):
-    """The blocked copy of A's stream (spmv.cuh csr_blocked_kernel) gives the
-    unblocked G = 32 kernel's products bit for bit (same per-lane order; padding
-    adds exact zeros), including rows shorter than a block and empty rows."""
+@pytest.mark.parametrize("dtype,lanes", [(np.float32, "32"), (np.float64, "32"), (np.float32, None),
+                                         (np.float64, "4"), (np.float32, "16")])
+def test_blocked_stream_bit_identical(B, monkeypatch, dtype, lanes):
+    """The blocked copy of A's stream (spmv.cuh csr_blocked_kernel): with 32 lanes
+    per row it gives the unblocked G = 32 kernel's products bit for bit (same
+    per-lane order; padding adds exact zeros); with fewer lanes (the plan's
+    choice, several rays per warp) it agrees to rounding.  Rows shorter than a
+    block and empty rows included."""
     blockops = B[0]
     from paper_1812_01307_b200 import problems
     a = problems.parallel_beam_matrix(256, 24, 363, dtype=dtype)   # rays of ~290 nonzeros: G = 32
@@ -307,15 +310,21 @@ def test_blocked_stream_bit_identical(B, monkeypatch, dtype):
     plain = blockops.BlockOperator(a, part)
     monkeypatch.delenv("BSGD_NO_BLOCKED")
     monkeypatch.setenv("BSGD_BLOCKED", "force")
+    if lanes is not None:
+        monkeypatch.setenv("BSGD_BLK_G", lanes)
     blk = blockops.BlockOperator(a, part)
+    exact = lanes == "32"
     oop = orc.OracleOperator(a, 2, 2)
     rng = np.random.default_rng(11)
     for _ in range(3):
         x = rng.standard_normal(a.shape[1])
         got = blk.matvec(x, charge=False)
-        assert np.array_equal(got, plain.matvec(x, charge=False))
+        if exact:
+            assert np.array_equal(got, plain.matvec(x, charge=False))
         assert rel(got, oop.matvec(x)) < 1e-12
         y = rng.standard_normal(a.shape[0])
         r1, s1 = blk.residual_sumsq(x, y)
         r0, s0 = plain.residual_sumsq(x, y)
-        assert np.array_equal(r1.cpu().numpy(), r0.cpu().numpy())
+        if exact:
+            assert np.array_equal(r1.cpu().numpy(), r0.cpu().numpy())
+        assert rel(r1.cpu().numpy(), y - oop.matvec(x)) < 1e-12
