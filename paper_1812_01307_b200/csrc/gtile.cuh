@@ -62,6 +62,41 @@ __device__ __forceinline__ void gt_load8(const double *p, double (&v)[8], uint64
     }
 }
 
+// one stream block of a lane: eight packed positions and the raw values
+template <typename V>
+struct GtBlk {
+    int4 l;
+    V v[8];
+};
+
+template <typename V>
+__device__ __forceinline__ void gt_load_blk(const uint16_t *loc, const V *val, int64_t k, GtBlk<V> &b,
+                                            uint64_t pol) {
+    b.l = ld_stream4(reinterpret_cast<const int32_t *>(loc + k), pol);
+    if constexpr (sizeof(V) == 4) {
+        const float4 x = ld_stream4(val + k, pol), y = ld_stream4(val + k + 4, pol);
+        b.v[0] = x.x; b.v[1] = x.y; b.v[2] = x.z; b.v[3] = x.w; b.v[4] = y.x; b.v[5] = y.y; b.v[6] = y.z; b.v[7] = y.w;
+    } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const double2 x = ld_stream2(val + k + 2 * q, pol);
+            b.v[2 * q] = x.x;
+            b.v[2 * q + 1] = x.y;
+        }
+    }
+}
+
+template <typename V>
+__device__ __forceinline__ double gt_use_blk(const GtBlk<V> &b, const double *w, double s) {
+    const uint32_t q[4] = {(uint32_t)b.l.x, (uint32_t)b.l.y, (uint32_t)b.l.z, (uint32_t)b.l.w};
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+        s = fma((double)b.v[2 * m], w[q[m] & 0xFFFFu], s);
+        s = fma((double)b.v[2 * m + 1], w[q[m] >> 16], s);
+    }
+    return s;
+}
+
 // s += v[m] * w[pos[m]] for the eight packed uint16 positions, in order m = 0..7
 __device__ __forceinline__ double gt_fma8(const int4 l, const double (&v)[8], const double *w, double s) {
     const uint32_t q[4] = {(uint32_t)l.x, (uint32_t)l.y, (uint32_t)l.z, (uint32_t)l.w};
@@ -78,7 +113,7 @@ __device__ __forceinline__ double gt_fma8(const int4 l, const double (&v)[8], co
 // still leave room for several CTAs per SM; otherwise one window and the
 // overlap comes from the other resident CTAs).
 template <typename V, bool DB, class Epi>
-__global__ void __launch_bounds__(kThreads) gtile_kernel(GTiles T, const double *__restrict__ vec, Epi epi,
+__global__ void __launch_bounds__(kThreads, 3) gtile_kernel(GTiles T, const double *__restrict__ vec, Epi epi,
                                                          double *part, int64_t *cnt) {
     extern __shared__ double win[];   // [DB ? 2 : 1][max_union]
     __shared__ double sm[8 * (kThreads / 32)];
@@ -92,7 +127,16 @@ __global__ void __launch_bounds__(kThreads) gtile_kernel(GTiles T, const double 
         if (t < T.ntiles) {
             const int64_t u0 = T.uni_ptr[t];
             const int nu = (int)(T.uni_ptr[t + 1] - u0);
-            for (int j = threadIdx.x; j < nu; j += kThreads) gt_cp_async8(w + j, vec + __ldg(T.uni + u0 + j));
+            // four union ids loaded before their copies are issued
+            int j = threadIdx.x;
+            for (; j + 3 * kThreads < nu; j += 4 * kThreads) {
+                int32_t c[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) c[q] = __ldg(T.uni + u0 + j + q * kThreads);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) gt_cp_async8(w + j + q * kThreads, vec + c[q]);
+            }
+            for (; j < nu; j += kThreads) gt_cp_async8(w + j, vec + __ldg(T.uni + u0 + j));
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
@@ -100,36 +144,31 @@ __global__ void __launch_bounds__(kThreads) gtile_kernel(GTiles T, const double 
     if constexpr (DB) gather(blockIdx.x, win);
     for (int64_t t = blockIdx.x; t < T.ntiles; t += gridDim.x) {
         double *w = win + (size_t)b * T.max_union;
-        if constexpr (DB) {
-            gather(t + gridDim.x, win + (size_t)(b ^ 1) * T.max_union);
-            asm volatile("cp.async.wait_group 1;" ::: "memory");
-        } else {
-            gather(t, win);
-            asm volatile("cp.async.wait_group 0;" ::: "memory");
-        }
-        __syncthreads();
+        if constexpr (DB) gather(t + gridDim.x, win + (size_t)(b ^ 1) * T.max_union);
+        else gather(t, win);
+        // the row's first two stream blocks are fetched while the union lands
         const int64_t r0 = T.tile_ptr[t], nr = T.tile_ptr[t + 1] - r0;
-        double s = 0.0;
-        int64_t row = -1;
+        int64_t row = -1, k = 0, end = 0;
+        GtBlk<V> c0, c1, n0, n1;
         if (tr < nr) {
             row = T.tile_rows[r0 + tr];
-            const int64_t beg = T.row_ptr[r0 + tr], end = T.row_ptr[r0 + tr + 1];   // multiples of 128
-            int64_t k = beg + 8 * gl;
-            for (; k + 128 < end; k += 256) {   // two blocks in flight
-                const int4 la = ld_stream4(reinterpret_cast<const int32_t *>(T.loc + k), pol);
-                const int4 lb = ld_stream4(reinterpret_cast<const int32_t *>(T.loc + k + 128), pol);
-                double va[8], vb[8];
-                gt_load8(val + k, va, pol);
-                gt_load8(val + k + 128, vb, pol);
-                s = gt_fma8(la, va, w, s);
-                s = gt_fma8(lb, vb, w, s);
-            }
-            if (k < end) {
-                const int4 la = ld_stream4(reinterpret_cast<const int32_t *>(T.loc + k), pol);
-                double va[8];
-                gt_load8(val + k, va, pol);
-                s = gt_fma8(la, va, w, s);
-            }
+            k = T.row_ptr[r0 + tr] + 8 * gl;
+            end = T.row_ptr[r0 + tr + 1];   // multiples of 128
+            if (k < end) gt_load_blk(T.loc, val, k, c0, pol);
+            if (k + 128 < end) gt_load_blk(T.loc, val, k + 128, c1, pol);
+        }
+        if constexpr (DB) asm volatile("cp.async.wait_group 1;" ::: "memory");
+        else asm volatile("cp.async.wait_group 0;" ::: "memory");
+        __syncthreads();
+        double s = 0.0;
+        // software pipeline: the next two blocks are in flight while two are summed
+        for (; k < end; k += 256) {
+            if (k + 256 < end) gt_load_blk(T.loc, val, k + 256, n0, pol);
+            if (k + 384 < end) gt_load_blk(T.loc, val, k + 384, n1, pol);
+            s = gt_use_blk(c0, w, s);
+            if (k + 128 < end) s = gt_use_blk(c1, w, s);
+            c0 = n0;
+            c1 = n1;
         }
 #pragma unroll
         for (int off = 8; off > 0; off >>= 1) s += __shfl_xor_sync(gmask, s, off, 16);
