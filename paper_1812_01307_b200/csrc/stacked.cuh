@@ -289,6 +289,117 @@ __host__ __device__ constexpr size_t stk_tile_smem() {
     return TileStage<V>::bytes * tile_stages<V>() + 2 * tile_stages<V>() * sizeof(uint64_t);
 }
 
+// Producer warps of the tile-staged kernels: walk the CTA's stream of (tile,
+// slice chunk, segment) stages and fill the ring with TMA bulk copies -- one
+// vector row per distinct column, the stage's entry records (REC, `hdr` = the
+// header slot holding their count, padded to a multiple of `pad`), the header.
+template <typename V, class REC>
+__device__ __forceinline__ void stk_tile_produce(const Stk<V> &A, const StkTiles &T, unsigned char *smraw,
+                                                 uint64_t *full, uint64_t *empty, int pw, int hdr, int pad) {
+    using ST = TileStage<V>;
+    constexpr int ZC = kTileZC;
+    constexpr int kTileStages = tile_stages<V>();
+    const int lane = threadIdx.x & 31;
+    const int32_t D = (int32_t)A.D;
+    const int64_t nchunks = D / ZC;
+    const int64_t items = T.ntiles * nchunks;
+    auto slot = [&](int k) { return smraw + (size_t)k * ST::bytes; };
+    // Segments are issued in batches of four.  A batch's metadata (one
+    // segment per lane, shuffled out) and column ids (segment g's ids sit at
+    // uni[32 g ..], one per lane) have no dependent loads, and the next
+    // batch's are fetched before this batch is issued, so the producer never
+    // waits on its own loads.
+    constexpr int B = 4;
+    int64_t seq = 0;  // stream position of the cursor
+    int64_t it = blockIdx.x, g = 0, g1 = 0;
+    int32_t z0 = 0;
+    auto load_item = [&]() {
+        if (it < items) {
+            const int64_t t = it % T.ntiles;
+            g = T.seg_ptr[t];
+            g1 = T.seg_ptr[t + 1];
+            z0 = (int32_t)(it / T.ntiles) * ZC;
+        }
+    };
+    load_item();
+    struct Batch {
+        int64_t gb[B];
+        int64_t sq[B];
+        int32_t zb[B];
+        int nb;
+        int64_t m_eb;
+        int m_nj, m_ne;
+        int32_t col[B];
+    };
+    auto fetch = [&](Batch &bt) {
+        bt.nb = 0;
+#pragma unroll
+        for (int q = 0; q < B; ++q) {
+            bt.gb[q] = -1;
+            bt.zb[q] = 0;
+            bt.sq[q] = 0;
+            // skip the other producers' positions
+            while (it < items && seq % kTileProducers != pw) {
+                ++seq;
+                if (++g == g1) {
+                    it += gridDim.x;
+                    load_item();
+                }
+            }
+            if (it < items) {
+                bt.gb[q] = g;
+                bt.zb[q] = z0;
+                bt.sq[q] = seq;
+                ++bt.nb;
+                ++seq;
+                if (++g == g1) {
+                    it += gridDim.x;
+                    load_item();
+                }
+            }
+        }
+        int64_t mine = -1;
+#pragma unroll
+        for (int q = 0; q < B; ++q)
+            if (lane == q) mine = bt.gb[q];
+        bt.m_eb = 0; bt.m_nj = 0; bt.m_ne = 0;
+        if (mine >= 0) {
+            bt.m_eb = T.seg_ent[mine];
+            bt.m_nj = T.seg_nj[mine];
+            bt.m_ne = (T.seg_row[mine * 24 + hdr] + pad - 1) & ~(pad - 1);
+        }
+#pragma unroll
+        for (int q = 0; q < B; ++q) bt.col[q] = bt.gb[q] >= 0 ? __ldg(T.uni + bt.gb[q] * kTileSeg + lane) : 0;
+    };
+    Batch cur, nxt;
+    fetch(cur);
+    while (cur.nb > 0) {
+        fetch(nxt);
+#pragma unroll
+        for (int q = 0; q < B; ++q) {
+            if (q >= cur.nb) break;
+            const int64_t eb = __shfl_sync(0xffffffffu, cur.m_eb, q);
+            const int nj = __shfl_sync(0xffffffffu, cur.m_nj, q);
+            const int ne = __shfl_sync(0xffffffffu, cur.m_ne, q);
+            const int k = (int)(cur.sq[q] % kTileStages);
+            const uint32_t round = (uint32_t)(cur.sq[q] / kTileStages);
+            if (round > 0) mbar_wait(&empty[k], (round - 1) & 1);
+            unsigned char *sb = slot(k);
+            const uint32_t bytes = (uint32_t)(nj * ZC * 8 + ne * (int)sizeof(REC) + 48);
+            if (lane == 0) mbar_arrive_expect_tx(&full[k], bytes);
+            __syncwarp();
+            if (lane < nj)
+                bulk_g2s(sb + (size_t)lane * ZC * 8, A.vec + (int64_t)cur.col[q] * D + cur.zb[q], ZC * 8, &full[k]);
+            if (lane == 1 && ne > 0)
+                bulk_g2s(sb + ST::win, reinterpret_cast<const REC *>(T.ent) + eb, ne * sizeof(REC),
+                         &full[k]);
+            if (lane == 3) bulk_g2s(sb + ST::win + ST::ent, T.seg_row + cur.gb[q] * 24, 48, &full[k]);
+            __syncwarp();
+        }
+        cur = nxt;
+    }
+}
+
 template <typename V, bool RESID, bool ALIGNED, class Epi>
 __global__ void __launch_bounds__(kStkTileThreads, 1) stacked_tile_kernel(Stk<V> A, StkTiles T, Epi epi, double *part,
                                                                         int64_t *cnt) {
@@ -296,7 +407,7 @@ __global__ void __launch_bounds__(kStkTileThreads, 1) stacked_tile_kernel(Stk<V>
     constexpr int ZC = kTileZC;
     constexpr int kTileStages = tile_stages<V>();
     extern __shared__ __align__(128) unsigned char smraw[];
-    __shared__ double sm[4 * 18];
+    __shared__ double sm[4 * (kStkTileThreads / 32)];
     uint64_t *full = reinterpret_cast<uint64_t *>(smraw + ST::bytes * kTileStages);
     uint64_t *empty = full + kTileStages;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -315,102 +426,7 @@ __global__ void __launch_bounds__(kStkTileThreads, 1) stacked_tile_kernel(Stk<V>
     __syncthreads();
 
     if (warp >= 16) {
-        // ---------------- producers ----------------
-        const int pw = warp - 16;  // producer pw issues stream positions pw, pw + kTileProducers, ...
-        // Segments are issued in batches of four.  A batch's metadata (one
-        // segment per lane, shuffled out) and column ids (segment g's ids sit at
-        // uni[32 g ..], one per lane) have no dependent loads, and the next
-        // batch's are fetched before this batch is issued, so the producer never
-        // waits on its own loads.
-        constexpr int B = 4;
-        int64_t seq = 0;  // stream position of the cursor
-        int64_t it = blockIdx.x, g = 0, g1 = 0;
-        int32_t z0 = 0;
-        auto load_item = [&]() {
-            if (it < items) {
-                const int64_t t = it % T.ntiles;
-                g = T.seg_ptr[t];
-                g1 = T.seg_ptr[t + 1];
-                z0 = (int32_t)(it / T.ntiles) * ZC;
-            }
-        };
-        load_item();
-        struct Batch {
-            int64_t gb[B];
-            int64_t sq[B];
-            int32_t zb[B];
-            int nb;
-            int64_t m_eb;
-            int m_nj, m_ne;
-            int32_t col[B];
-        };
-        auto fetch = [&](Batch &bt) {
-            bt.nb = 0;
-#pragma unroll
-            for (int q = 0; q < B; ++q) {
-                bt.gb[q] = -1;
-                bt.zb[q] = 0;
-                bt.sq[q] = 0;
-                // skip the other producers' positions
-                while (it < items && seq % kTileProducers != pw) {
-                    ++seq;
-                    if (++g == g1) {
-                        it += gridDim.x;
-                        load_item();
-                    }
-                }
-                if (it < items) {
-                    bt.gb[q] = g;
-                    bt.zb[q] = z0;
-                    bt.sq[q] = seq;
-                    ++bt.nb;
-                    ++seq;
-                    if (++g == g1) {
-                        it += gridDim.x;
-                        load_item();
-                    }
-                }
-            }
-            int64_t mine = -1;
-#pragma unroll
-            for (int q = 0; q < B; ++q)
-                if (lane == q) mine = bt.gb[q];
-            bt.m_eb = 0; bt.m_nj = 0; bt.m_ne = 0;
-            if (mine >= 0) {
-                bt.m_eb = T.seg_ent[mine];
-                bt.m_nj = T.seg_nj[mine];
-                bt.m_ne = (T.seg_row[mine * 24 + 16] + 15) & ~15;
-            }
-#pragma unroll
-            for (int q = 0; q < B; ++q) bt.col[q] = bt.gb[q] >= 0 ? __ldg(T.uni + bt.gb[q] * kTileSeg + lane) : 0;
-        };
-        Batch cur, nxt;
-        fetch(cur);
-        while (cur.nb > 0) {
-            fetch(nxt);
-#pragma unroll
-            for (int q = 0; q < B; ++q) {
-                if (q >= cur.nb) break;
-                const int64_t eb = __shfl_sync(0xffffffffu, cur.m_eb, q);
-                const int nj = __shfl_sync(0xffffffffu, cur.m_nj, q);
-                const int ne = __shfl_sync(0xffffffffu, cur.m_ne, q);
-                const int k = (int)(cur.sq[q] % kTileStages);
-                const uint32_t round = (uint32_t)(cur.sq[q] / kTileStages);
-                if (round > 0) mbar_wait(&empty[k], (round - 1) & 1);
-                unsigned char *sb = slot(k);
-                const uint32_t bytes = (uint32_t)(nj * ZC * 8 + ne * (int)sizeof(TileEnt<V>) + 48);
-                if (lane == 0) mbar_arrive_expect_tx(&full[k], bytes);
-                __syncwarp();
-                if (lane < nj)
-                    bulk_g2s(sb + (size_t)lane * ZC * 8, A.vec + (int64_t)cur.col[q] * D + cur.zb[q], ZC * 8, &full[k]);
-                if (lane == 1 && ne > 0)
-                    bulk_g2s(sb + ST::win, reinterpret_cast<const TileEnt<V> *>(T.ent) + eb, ne * sizeof(TileEnt<V>),
-                             &full[k]);
-                if (lane == 3) bulk_g2s(sb + ST::win + ST::ent, T.seg_row + cur.gb[q] * 24, 48, &full[k]);
-                __syncwarp();
-            }
-            cur = nxt;
-        }
+        stk_tile_produce<V, TileEnt<V>>(A, T, smraw, full, empty, warp - 16, 16, 16);
     } else {
         // ---------------- consumers: tile row = warp, slices z0 + lane + 32 s ----------------
         constexpr int KZ = kTileKZ;
