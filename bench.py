@@ -543,8 +543,8 @@ def run_ct_secondary(args, index):
                        "ms": round(pms, 4), "algorithmic_bytes": pbytes, "gbs": round(pbytes / (pms * 1e6), 1),
                        "note": ("fields are L2-resident at 2D sizes; bound by grid barriers / latency, not HBM"
                                 if dim == 2 else
-                                "fields stream from HBM (134 MB each); latency-bound at 16 warps/SM, "
-                                "profiles/r01_c5.md")}}
+                                "fields stream from HBM (134 MB each); split passes with direct pairwise "
+                                "leaf sums, profiles/r01_c5.md")}}
     if products is not None:
         out["products"] = products
     if d.depth > 1:

@@ -1051,6 +1051,22 @@ static int prox_occupancy() {
 template <int K>
 static size_t slab_smem(bool) { return 0; }
 
+// Grid of the grid-stride stencil passes (candidate, finalize, output): exactly
+// the CTAs that are resident at once, so the whole grid sweeps the volume
+// together and a voxel's neighbour planes are still in L2 when it is reached.
+// With 8 CTAs per SM requested but 5 resident (48 registers), the late CTAs
+// re-swept the volume after the others and re-read their neighbour planes from
+// DRAM (candidate pass: 851 MB read for 537 MB of fields, profiles/r01_c5.md).
+template <int DIM>
+static int stencil_grid(int64_t n) {
+    static int occ = 0;
+    if (occ == 0) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, slab_candidate_kernel<DIM>, kThreads, 0);
+        if (occ < 1) occ = 1;
+    }
+    return (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, kThreads), (int64_t)num_sms() * occ));
+}
+
 template <int DIM>
 static void split_attrs() {
     static bool done = false;
@@ -1092,7 +1108,7 @@ static int launch_prox_split(const ProxArgs &a, cudaStream_t st) {
         CU(cudaMemsetAsync(a.f[k], 0, sizeof(double) * a.N, st));
         CU(cudaMemsetAsync(a.f[DIM + k], 0, sizeof(double) * a.N, st));
     }
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(a.N, kThreads), (int64_t)num_sms() * 8));
+    const int grid = stencil_grid<DIM>(a.N);
     constexpr int KD = 1 + 2 * DIM;
     const bool fast = v.fast != 0;
     auto sums2 = [&](bool energy) {
@@ -1526,7 +1542,7 @@ static int slab_ctx(const bsgd_slab *s, SlabCtx &c, bool need_weight = true) {
     if (S / c.G > kPwMaxQ * per_slot) return fail(BSGD_EINVAL, "slab too large for the pairwise tree");
     c.part = base;
     c.stats = base + off[11] + 16;
-    c.grid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(s->count, kThreads), (int64_t)num_sms() * 8));
+    c.grid = c.dim == 3 ? stencil_grid<3>(s->count) : stencil_grid<2>(s->count);
     return BSGD_OK;
 }
 
