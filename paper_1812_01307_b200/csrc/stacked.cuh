@@ -400,6 +400,16 @@ __device__ __forceinline__ void stk_tile_produce(const Stk<V> &A, const StkTiles
     }
 }
 
+// slice s of a consumer lane sits at 2 lane + tile_zoff(s) in the stage's 128 slices
+__device__ __forceinline__ constexpr int tile_zoff(int s) { return (s & 1) + 64 * (s >> 1); }
+
+// the lane's four slice values of one window column (w = column base + 2 lane)
+__device__ __forceinline__ void tile_x4(const double *w, double (&x)[4]) {
+    const double2 a = *reinterpret_cast<const double2 *>(w);
+    const double2 b = *reinterpret_cast<const double2 *>(w + 64);
+    x[0] = a.x; x[1] = a.y; x[2] = b.x; x[3] = b.y;
+}
+
 template <typename V, bool RESID, bool ALIGNED, class Epi>
 __global__ void __launch_bounds__(kStkTileThreads, 1) stacked_tile_kernel(Stk<V> A, StkTiles T, Epi epi, double *part,
                                                                         int64_t *cnt) {
@@ -428,14 +438,15 @@ __global__ void __launch_bounds__(kStkTileThreads, 1) stacked_tile_kernel(Stk<V>
     if (warp >= 16) {
         stk_tile_produce<V, TileEnt<V>>(A, T, smraw, full, empty, warp - 16, 16, 16);
     } else {
-        // ---------------- consumers: tile row = warp, slices z0 + lane + 32 s ----------------
+        // ------- consumers: tile row = warp, slices z0 + zoff(lane, s) = 2 lane + {0, 1, 64, 65} -------
+        // (two 16-byte shared-memory reads give a lane its four slices, conflict-free)
         constexpr int KZ = kTileKZ;
         constexpr int NH = 1;
         int k = 0;
         uint32_t round = 0;
         for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
             const int64_t t = it % T.ntiles, ch = it / T.ntiles;
-            const int32_t zl = (int32_t)ch * ZC + lane;
+            const int32_t zl = (int32_t)ch * ZC + 2 * lane;
             const int64_t r0 = T.tile_ptr[t], nr = T.tile_ptr[t + 1] - r0;
             const int64_t g0 = T.seg_ptr[t], g1 = T.seg_ptr[t + 1];
             double seg[NH][KZ], acc[NH][KZ];
@@ -450,7 +461,7 @@ __global__ void __launch_bounds__(kStkTileThreads, 1) stacked_tile_kernel(Stk<V>
                 srow[h] = live[h] ? T.tile_rows[r0 + rr] : 0;
 #pragma unroll
                 for (int s = 0; s < KZ; ++s) {
-                    const int32_t z = zl + 32 * s;
+                    const int32_t z = zl + tile_zoff(s);
                     seg[h][s] = 0.0;
                     acc[h][s] = (RESID && live[h]) ? A.y[srow[h] * D + z] : 0.0;
                     jb[h][s] = 0;
@@ -469,7 +480,7 @@ __global__ void __launch_bounds__(kStkTileThreads, 1) stacked_tile_kernel(Stk<V>
             for (int64_t g = g0; g < g1; ++g) {
                 mbar_wait(&full[k], round & 1);
                 const unsigned char *sb = slot(k);
-                const double *w = reinterpret_cast<const double *>(sb) + lane;
+                const double *w = reinterpret_cast<const double *>(sb) + 2 * lane;
                 const TileEnt<V> *ents = reinterpret_cast<const TileEnt<V> *>(sb + ST::win);
                 const uint16_t *ro = reinterpret_cast<const uint16_t *>(sb + ST::win + ST::ent);
 #pragma unroll
@@ -493,7 +504,7 @@ __global__ void __launch_bounds__(kStkTileThreads, 1) stacked_tile_kernel(Stk<V>
                                 while (c >= thr[h][s]) {
                                     fold(h, s);
                                     ++jb[h][s];
-                                    thr[h][s] = (int32_t)((__ldg(A.bounds + jb[h][s] + 1) - (zl + 32 * s) + D - 1) / D);
+                                    thr[h][s] = (int32_t)((__ldg(A.bounds + jb[h][s] + 1) - (zl + tile_zoff(s)) + D - 1) / D);
                                 }
                             }
                             tmin[h] = thr[h][0];
@@ -512,7 +523,8 @@ __global__ void __launch_bounds__(kStkTileThreads, 1) stacked_tile_kernel(Stk<V>
                         const double *w0 = w + l0 * ZC, *w1 = w + l1 * ZC;
                         double x0[KZ], x1[KZ];
 #pragma unroll
-                        for (int s = 0; s < KZ; ++s) { x0[s] = w0[32 * s]; x1[s] = w1[32 * s]; }
+                        tile_x4(w0, x0);
+                        tile_x4(w1, x1);
                         if (c1 < (ALIGNED ? thr[h][0] : tmin[h])) {
 #pragma unroll
                             for (int s = 0; s < KZ; ++s) {
@@ -533,9 +545,10 @@ __global__ void __launch_bounds__(kStkTileThreads, 1) stacked_tile_kernel(Stk<V>
                         const int l = r.cl & 255;
                         cross((int32_t)(r.cl >> 8));
                         const double v = (double)r.val;
-                        const double *wl = w + l * ZC;
+                        double xl[KZ];
+                        tile_x4(w + l * ZC, xl);
 #pragma unroll
-                        for (int s = 0; s < KZ; ++s) seg[h][s] = rn_add(seg[h][s], rn_mul(v, wl[32 * s]));
+                        for (int s = 0; s < KZ; ++s) seg[h][s] = rn_add(seg[h][s], rn_mul(v, xl[s]));
                     }
                 }
                 __syncwarp();
@@ -548,7 +561,7 @@ __global__ void __launch_bounds__(kStkTileThreads, 1) stacked_tile_kernel(Stk<V>
 #pragma unroll
                 for (int s = 0; s < KZ; ++s) {
                     for (; jb[h][s] < A.nb; ++jb[h][s]) fold(h, s);
-                    epi(srow[h] * D + zl + 32 * s, acc[h][s]);
+                    epi(srow[h] * D + zl + tile_zoff(s), acc[h][s]);
                 }
             }
         }
