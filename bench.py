@@ -500,6 +500,9 @@ def run_ct_secondary(args, index):
     # per FGP iteration of the fused schedule: candidate (read q, b; write c), dual
     # value + momentum commit (read c, p, b; write q): 5*dim + 2 fields of 8 bytes
     pbytes = 8 * npx * ((5 * dim + 2) * d.max_inner_iters + 10)
+    if npx >= (1 << 21):
+        # pass-per-kernel prox: the first iteration reads p = q = 0 as literals (2 dim fields fewer)
+        pbytes -= 8 * npx * 2 * dim
     rows, cols = op.shape
     products = None
     if d.depth == 1:

@@ -1104,10 +1104,14 @@ static int launch_prox_split(const ProxArgs &a, cudaStream_t st) {
         return fail(BSGD_EINVAL, "image too large for the pairwise tree (%lld voxels)", (long long)a.N);
     v.ctl = (FgpCtl *)(a.red + (size_t)kMaxPartials * kPwMaxK);
     double *part = a.red;
-    for (int k = 0; k < DIM; ++k) {  // p = q = 0 (tv.py:198-201)
-        CU(cudaMemsetAsync(a.f[k], 0, sizeof(double) * a.N, st));
-        CU(cudaMemsetAsync(a.f[DIM + k], 0, sizeof(double) * a.N, st));
-    }
+    // p = q = 0 (tv.py:198-201): the first iteration's passes read them as literal
+    // zeros (v.zero) and write every voxel of c and q, so nothing is cleared; only
+    // a prox without iterations needs the stored zeros (for the finalize pass)
+    if (a.max_iters < 1)
+        for (int k = 0; k < DIM; ++k) {
+            CU(cudaMemsetAsync(a.f[k], 0, sizeof(double) * a.N, st));
+            CU(cudaMemsetAsync(a.f[DIM + k], 0, sizeof(double) * a.N, st));
+        }
     const int grid = stencil_grid<DIM>(a.N);
     constexpr int KD = 1 + 2 * DIM;
     const bool fast = v.fast != 0;
@@ -1128,6 +1132,7 @@ static int launch_prox_split(const ProxArgs &a, cudaStream_t st) {
     sums2(false);
     split_decide_kernel<DIM, 2><<<1, kThreads, 0, st>>>(v, 0, 0, part);
     for (int it = 0; it < a.max_iters; ++it) {
+        v.zero = it == 0 ? 1 : 0;
         v.when = 1;  // unless converged
         slab_candidate_kernel<DIM><<<grid, kThreads, 0, st>>>(v, 0);
         dual();
@@ -1138,6 +1143,7 @@ static int launch_prox_split(const ProxArgs &a, cudaStream_t st) {
         split_decide_kernel<DIM, KD><<<1, kThreads, 0, st>>>(v, 2, it, part);
     }
     v.when = 0;
+    v.zero = 0;
     slab_finalize_kernel<DIM><<<grid, kThreads, 0, st>>>(v);
     sums2(true);
     split_decide_kernel<DIM, 2><<<1, kThreads, 0, st>>>(v, 3, 0, part);
@@ -1528,6 +1534,7 @@ static int slab_ctx(const bsgd_slab *s, SlabCtx &c, bool need_weight = true) {
     c.v.parity = s->parity;
     c.v.when = 0;
     c.v.ctl = nullptr;
+    c.v.zero = 0;
     c.v.u = at(10);
     c.v.off = s->offset;
     c.v.n = s->count;

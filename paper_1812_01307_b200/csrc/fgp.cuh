@@ -115,6 +115,17 @@ __device__ __forceinline__ double u_at(const ProxArgs &a, const double *const *q
     return rn_add(__ldg(a.b + (z * a.H + s) * a.W + t), rn_mul(a.w, div_at<DIM>(qf, z, s, t, a.D, a.H, a.W)));
 }
 
+// c / max(|c|, 1) (tv.py:211-214)
+template <int DIM>
+__device__ __forceinline__ void project_unit(double (&c)[DIM]) {
+    double m2 = rn_add(rn_mul(c[0], c[0]), rn_mul(c[1], c[1]));
+    if constexpr (DIM == 3) m2 = rn_add(m2, rn_mul(c[2], c[2]));
+    double mag = sqrt(m2);
+    mag = (mag < 1.0) ? 1.0 : mag;  // np.maximum(mag, 1): NaN propagates
+#pragma unroll
+    for (int k = 0; k < DIM; ++k) c[k] = c[k] / mag;
+}
+
 // projected gradient candidate from q at voxel p (tv.py:207-214; 3D: same with three fields)
 template <int DIM>
 __device__ __forceinline__ void candidate(const ProxArgs &a, const double *const *qf, int64_t p, double (&c)[DIM]) {
@@ -127,12 +138,25 @@ __device__ __forceinline__ void candidate(const ProxArgs &a, const double *const
     g[DIM - 1] = (t > 0) ? rn_sub(uc, u_at<DIM>(a, qf, z, s, t - 1)) : 0.0;
 #pragma unroll
     for (int k = 0; k < DIM; ++k) c[k] = rn_add(ldcg(qf[k] + p), rn_mul(a.step, g[k]));
-    double m2 = rn_add(rn_mul(c[0], c[0]), rn_mul(c[1], c[1]));
-    if constexpr (DIM == 3) m2 = rn_add(m2, rn_mul(c[2], c[2]));
-    double mag = sqrt(m2);
-    mag = (mag < 1.0) ? 1.0 : mag;  // np.maximum(mag, 1): NaN propagates
+    project_unit<DIM>(c);
+}
+
+// the same candidate for q = 0 (the first FGP iteration, tv.py:198-201): every
+// operation of `candidate` on literal zeros instead of loads -- div 0 is +0, so
+// u = b + w * (+0) and c = (+0) + step g -- bit-identical without the zeroed fields
+template <int DIM>
+__device__ __forceinline__ void candidate_zero(const ProxArgs &a, int64_t p, double (&c)[DIM]) {
+    int64_t z, s, t;
+    split_index<DIM>(p, a.H, a.W, z, s, t);
+    const double wz = rn_mul(a.w, 0.0);
+    const double uc = rn_add(__ldg(a.b + p), wz);
+    double g[DIM];
+    if constexpr (DIM == 3) g[0] = (z > 0) ? rn_sub(uc, rn_add(__ldg(a.b + p - a.H * a.W), wz)) : 0.0;
+    g[DIM - 2] = (s > 0) ? rn_sub(uc, rn_add(__ldg(a.b + p - a.W), wz)) : 0.0;
+    g[DIM - 1] = (t > 0) ? rn_sub(uc, rn_add(__ldg(a.b + p - 1), wz)) : 0.0;
 #pragma unroll
-    for (int k = 0; k < DIM; ++k) c[k] = c[k] / mag;
+    for (int k = 0; k < DIM; ++k) c[k] = rn_add(0.0, rn_mul(a.step, g[k]));
+    project_unit<DIM>(c);
 }
 
 // isotropic TV term at voxel p of u (tv.py:149-152; 3D: sqrt((dz^2 + dv^2) + dh^2))
@@ -208,6 +232,7 @@ struct DualCommitTerms {
     double *Q[DIM];
     double w, beta;
     int64_t D, H, W;
+    bool pzero = false;   // p = 0 (first FGP iteration): literal zeros instead of loads
     struct L {
         double b, here[DIM], next[DIM], p[DIM];
         unsigned first;  // bit k: coordinate k is 0 (no backward neighbour)
@@ -226,7 +251,7 @@ struct DualCommitTerms {
             const int ax = 3 - DIM + k;  // 2D: rows, columns; 3D: z, rows, columns
             l.here[k] = ldcg(C[k] + p);
             l.next[k] = (coord[ax] + 1 < ext[ax]) ? ldcg(C[k] + p + step[ax]) : 0.0;
-            l.p[k] = ldcg(P[k] + p);
+            l.p[k] = pzero ? 0.0 : ldcg(P[k] + p);
             if (coord[ax] == 0) l.first |= 1u << k;
         }
         return l;

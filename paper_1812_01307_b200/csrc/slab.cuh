@@ -52,6 +52,7 @@ struct SlabView {
     int when;         // split prox: 0 always, 1 unless converged, 2 only on a restart
     double *u;        // finalize output; NULL: the dual buffer not holding p
     FgpCtl *ctl;      // split prox control block, NULL for the host loop
+    int zero;         // split prox, first iteration: p = q = 0 are not stored, read as zeros
 };
 
 __device__ __forceinline__ bool slab_skip(const SlabView &s) {
@@ -149,7 +150,8 @@ __global__ void __launch_bounds__(kThreads) slab_candidate_kernel(SlabView s, in
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < s.n; i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t p = s.off + i;
         double c[DIM];
-        candidate<DIM>(s.a, src, p, c);
+        if (s.zero) candidate_zero<DIM>(s.a, p, c);
+        else candidate<DIM>(s.a, src, p, c);
 #pragma unroll
         for (int k = 0; k < DIM; ++k) r.C[k][p] = c[k];
     }
@@ -170,6 +172,7 @@ __global__ void __launch_bounds__(kThreads, 4) slab_dual_kernel(SlabView s, doub
 #pragma unroll
     for (int k = 0; k < DIM; ++k) { f.P[k] = r.P[k]; f.Q[k] = r.Q[k]; f.C[k] = r.C[k]; }
     f.off = s.off;
+    f.pzero = s.zero != 0;
     slab_sum<1 + 2 * DIM, FAST>(s, f, part);
 }
 

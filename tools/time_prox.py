@@ -18,7 +18,10 @@ def prox_bytes(n_pix, iters, restarts=0, dim=2):
     # per FGP iteration of the fused schedule: candidate reads q (dim fields)
     # + b and writes c (dim); dual value + commit reads c, p (2 dim) + b and writes q (dim):
     # 5 dim + 2 field passes; a restart repeats both (5 dim + 2); setup and finalize ~10
-    return 8 * n_pix * ((5 * dim + 2) * (iters + restarts) + 10)
+    b = 8 * n_pix * ((5 * dim + 2) * (iters + restarts) + 10)
+    if n_pix >= (1 << 21) and iters > 0:
+        b -= 8 * n_pix * 2 * dim   # split prox: p = q = 0 of the first iteration are not read
+    return b
 
 
 def main():
