@@ -236,12 +236,12 @@ __global__ void __launch_bounds__(kThreads, (ALIGNED || Epi::K == 4) ? 4 : 3) st
 // measured at 256^2 x 360 x 363).  Per tile the plan keeps the sorted union of
 // the tile's columns cut into segments of kTileSeg columns, and per segment the
 // tile rows' entries that fall in it (row-major, uint8 position in the segment
-// + value).  Warp-specialised CTA: one producer warp walks the CTA's stream of
-// (tile, slice chunk, segment) stages and fills a tile_stages()-deep ring with
-// TMA bulk copies -- one 256-byte vector row per distinct column (instead of
-// one gather per entry), the column ids, the entries -- completing on a
-// full-barrier per slot; eight consumer warps (two tile rows each, one slice
-// per lane) accumulate from shared memory and release the slot on an
+// + value).  Warp-specialised CTA: four producer warps walk the CTA's stream
+// of (tile, 128-slice chunk, segment) stages and fill a tile_stages()-deep ring
+// with TMA bulk copies -- one 1 KB vector row per distinct column (instead of
+// one gather per entry), the entry records, the row offsets -- completing on a
+// full-barrier per slot; sixteen consumer warps (one tile row each, four
+// slices per lane) accumulate from shared memory and release the slot on an
 // empty-barrier.  Each row still consumes its entries in stored order, so every
 // output keeps the exact block-sequential arithmetic of the direct kernel.
 // ---------------------------------------------------------------------------
