@@ -201,6 +201,9 @@ class CudaShard:
         nat.call("bsgd_rmatvec", self.op.plan, nat.ptr(w), nat.ptr(out), self.stream())
 
 
+SLAB_PROX_MIN_VOXELS = 1 << 22   # prox="auto" decomposes volumes from this size on
+
+
 class DistributedBSGD:
     """Row-slab BSGD-TV driver (alpha = gamma = 1) over a process group.
 
@@ -212,7 +215,8 @@ class DistributedBSGD:
         """``prox``: "replicated" runs the whole prox on every rank (bsgd_step);
         "slab" decomposes it over the ranks (SlabProx; needs an identity layout
         and slabs at least one halo plane thick); "auto" takes "slab" on more
-        than one rank when it applies."""
+        than one rank when it applies and the volume has at least
+        SLAB_PROX_MIN_VOXELS voxels (configs[4]'s 256^3), "replicated" otherwise."""
         import torch.distributed as dist
         self.dist = dist
         self.group = group
@@ -260,7 +264,11 @@ class DistributedBSGD:
                     slabs = prox_slabs(int(np.prod(dims)), comm.world, dims[1] * dims[2] if dims[0] > 1 else dims[2])
                 except ValueError as e:
                     why = str(e)
-            if why is None and (prox == "slab" or comm.world > 1):
+            # "auto" decomposes only large volumes: the slab prox takes its FGP decisions
+            # on the host (a gather and halo exchanges per pass), which costs more than
+            # running a small prox redundantly on every rank (1024^2: ~0.13 ms per epoch)
+            big = int(np.prod(dims)) >= SLAB_PROX_MIN_VOXELS
+            if why is None and (prox == "slab" or (comm.world > 1 and big)):
                 lo, n = slabs[comm.rank]
                 self.slab = SlabProx(shard.slab_backend(lo, n), comm, slabs)
                 self.slabs = slabs

@@ -202,8 +202,10 @@ def _epoch_worker(rank, world, port, outdir, epochs):
     spec = parallel.ShardSpec(part, rank, world)
     shard = _CpuProxShard(a, spec, dims, lam=0.5)
     cfg = SolverConfig(mu=2e-3, lam=0.5, epochs=epochs, monitor_decrease=False, prox=tv.ProxSettings(20, 1e-6))
-    drv = parallel.DistributedBSGD(shard, y, cfg, history_capacity=epochs + 4)
+    drv = parallel.DistributedBSGD(shard, y, cfg, history_capacity=epochs + 4, prox="slab")
     assert drv.slab is not None
+    auto = parallel.DistributedBSGD(shard, y, cfg, history_capacity=4)
+    assert auto.slab is None   # small image: "auto" keeps the prox replicated
     infos = []
     for _ in range(epochs):
         drv.epoch_step(monitor=False)
