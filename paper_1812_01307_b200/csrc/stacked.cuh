@@ -253,7 +253,13 @@ __host__ __device__ constexpr int tile_stages() { return sizeof(V) == 4 ? 6 : 5;
 constexpr int kTileSegEnt = kTileRows * kTileSeg;  // entries per segment, upper bound
 constexpr int kTileKZ = 4;         // slices per lane
 constexpr int kTileZC = 32 * kTileKZ;  // slices per item
+// Producer warps: producer p issues ring positions p, p + P, ...; before reusing a
+// slot it waits for the slot's previous round on the empty barrier by phase
+// parity, which is only unambiguous while no producer can run two rounds ahead
+// of the consumers -- guaranteed for P <= the ring depth.
 constexpr int kTileProducers = 4;
+static_assert(kTileProducers <= tile_stages<double>() && kTileProducers <= tile_stages<float>(),
+              "producers must not outnumber the ring slots");
 constexpr int kStkTileThreads = 32 * (16 + kTileProducers);  // 16 consumer warps (one tile row each) + producers
 
 struct StkTiles {
