@@ -191,6 +191,7 @@ struct bsgd_plan {
         int32_t *tile_rows = nullptr, *seg_nj = nullptr, *uni = nullptr;
         uint16_t *seg_row = nullptr;
         void *ent = nullptr;
+        int kz = 4;             // slices per consumer lane (stacked.cuh tile_seg / tile_zc)
         size_t bytes = 0;
     } sf, stt;
     // gather-tiled copies of A / A^T (gtile.cuh), set by bsgd_plan_gather_tiles
@@ -762,11 +763,11 @@ static int launch_stacked(const Stk<V> &A, int kz, const E &e, double *part, int
     }
 }
 
-template <typename V, bool RESID, bool ALIGNED, class E>
-static int launch_stk_tile(const Stk<V> &A, const bsgd_plan::StkTileStore &S, const E &e, double *part, int64_t *cnt,
-                           cudaStream_t st) {
-    auto kern = stacked_tile_kernel<V, RESID, ALIGNED, E>;
-    const size_t smem = stk_tile_smem<V>();
+template <typename V, int KZ, bool RESID, bool ALIGNED, class E>
+static int launch_stk_tile_kz(const Stk<V> &A, const bsgd_plan::StkTileStore &S, const E &e, double *part,
+                              int64_t *cnt, cudaStream_t st) {
+    auto kern = stacked_tile_kernel<V, KZ, RESID, ALIGNED, E>;
+    const size_t smem = stk_tile_smem<V, KZ>();
     static bool attr_set = false;  // per instantiation
     if (!attr_set) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -775,12 +776,19 @@ static int launch_stk_tile(const Stk<V> &A, const bsgd_plan::StkTileStore &S, co
     StkTiles T{S.ntiles, S.tile_ptr, S.tile_rows, S.seg_ptr, S.seg_nj, S.seg_ent, S.seg_row, S.uni, S.ent};
     int occ = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kStkTileThreads, smem);
-    const int64_t items = S.ntiles * (A.D / kTileZC);
+    const int64_t items = S.ntiles * (A.D / tile_zc<KZ>());
     const int cap = std::min(std::max(occ, 1) * num_sms(), kMaxPartials);
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(items, cap));
     kern<<<grid, kStkTileThreads, smem, st>>>(A, T, e, part, cnt);
     LAUNCHED();
     return BSGD_OK;
+}
+
+template <typename V, bool RESID, bool ALIGNED, class E>
+static int launch_stk_tile(const Stk<V> &A, const bsgd_plan::StkTileStore &S, const E &e, double *part, int64_t *cnt,
+                           cudaStream_t st) {
+    if (S.kz == 8) return launch_stk_tile_kz<V, 8, RESID, ALIGNED, E>(A, S, e, part, cnt, st);
+    return launch_stk_tile_kz<V, 4, RESID, ALIGNED, E>(A, S, e, part, cnt, st);
 }
 
 template <typename V, class E>
@@ -800,7 +808,7 @@ static int launch_stacked_dir(const bsgd_plan *p, bool transposed, const double 
     A.L = p->lanes;
     const int kz = transposed ? p->kz_tr : p->kz_fwd;
     const bsgd_plan::StkTileStore &S = transposed ? p->stt : p->sf;
-    if (S.ok && A.D % kTileZC == 0 && !getenv("BSGD_NO_STK_TILES")) {
+    if (S.ok && A.D % (32 * S.kz) == 0 && !getenv("BSGD_NO_STK_TILES")) {
         if constexpr (std::is_same<E, EpiResid>::value) {
             A.y = e.y;
             return A.sbounds ? launch_stk_tile<V, true, true>(A, S, EpiResidFinal{e.r}, part, cnt, st)
@@ -1230,7 +1238,15 @@ static int build_stk_tiles(bsgd_plan *p, bool tr, int64_t ntiles, const int64_t 
     CU(cudaMemcpyAsync(idx.data(), tr ? p->t_idx : p->f_idx, sizeof(int32_t) * nnz, cudaMemcpyDeviceToHost, st));
     CU(cudaMemcpyAsync(val.data(), tr ? p->t_val : p->f_val, sizeof(V) * nnz, cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));
-    // per tile: sorted distinct columns, cut into segments of kTileSeg; per segment
+    // Eight slices per consumer lane for A's rows (rays) when the depth allows (a
+    // multiple of 256: the entry decode serves twice the slices), with half as
+    // many columns per segment so a stage's window stays 32 KB.  configs[4]: A
+    // 2.86 -> 2.62 ms; A^T (pixel rows) ran 3.21 -> 5.09 ms that way and keeps
+    // four.  BSGD_STK_KZ=4 / 8 forces either for both.
+    int kz = (!tr && p->depth % 256 == 0) ? 8 : 4;
+    if (const char *e = getenv("BSGD_STK_KZ")) kz = atoi(e) == 8 && p->depth % 256 == 0 ? 8 : 4;
+    const int64_t seg = kz == 8 ? tile_seg<8>() : tile_seg<4>();
+    // per tile: sorted distinct columns, cut into segments of seg columns; per segment
     // the tile rows' entries inside it (row-major, position in the segment as uint8)
     struct TileOut {
         std::vector<int32_t> uni;
@@ -1258,12 +1274,12 @@ static int build_stk_tiles(bsgd_plan *p, bool tr, int64_t ntiles, const int64_t 
                 cols.erase(std::unique(cols.begin(), cols.end()), cols.end());
                 o.uni = cols;
                 const int64_t nu = (int64_t)cols.size();
-                const int64_t nseg = std::max<int64_t>(1, (nu + kTileSeg - 1) / kTileSeg);
+                const int64_t nseg = std::max<int64_t>(1, (nu + seg - 1) / seg);
                 const int64_t nrt = tptr[t + 1] - tptr[t];
                 std::vector<int64_t> cur(nrt);
                 for (int64_t i = 0; i < nrt; ++i) cur[i] = ptr[trows[tptr[t] + i]];
                 for (int64_t sg = 0; sg < nseg; ++sg) {
-                    const int64_t j0 = sg * kTileSeg, j1 = std::min<int64_t>(nu, j0 + kTileSeg);
+                    const int64_t j0 = sg * seg, j1 = std::min<int64_t>(nu, j0 + seg);
                     const int32_t cmax = j1 > j0 ? cols[j1 - 1] : -1;
                     std::array<uint16_t, 24> ro{};
                     o.ent.push_back((int64_t)o.loc.size());
@@ -1289,7 +1305,7 @@ static int build_stk_tiles(bsgd_plan *p, bool tr, int64_t ntiles, const int64_t 
         });
     }
     for (auto &th : pool) th.join();
-    // flatten: segment g's column ids at uni[g * kTileSeg ..] (zero padded)
+    // flatten: segment g's column ids at uni[g * seg ..] (zero padded)
     int64_t nseg_all = 0, nent = 0;
     std::vector<int64_t> seg_ptr(ntiles + 1, 0);
     for (int64_t t = 0; t < ntiles; ++t) {
@@ -1298,7 +1314,7 @@ static int build_stk_tiles(bsgd_plan *p, bool tr, int64_t ntiles, const int64_t 
     }
     nseg_all = seg_ptr[ntiles];
     std::vector<int64_t> seg_uni(nseg_all), seg_ent(nseg_all);
-    std::vector<int32_t> seg_nj(nseg_all), uni((size_t)std::max<int64_t>(nseg_all, 1) * kTileSeg, 0);
+    std::vector<int32_t> seg_nj(nseg_all), uni((size_t)std::max<int64_t>(nseg_all, 1) * seg, 0);
     std::vector<uint16_t> seg_row((size_t)nseg_all * 24);
     std::vector<TileEnt<V>> ents(std::max<int64_t>(nent, 16));
     int64_t eo = 0;
@@ -1308,11 +1324,11 @@ static int build_stk_tiles(bsgd_plan *p, bool tr, int64_t ntiles, const int64_t 
         for (size_t sg = 0; sg < o.nj.size(); ++sg) {
             const int64_t g = seg_ptr[t] + (int64_t)sg;
             const int32_t nj = o.nj[sg];
-            seg_uni[g] = g * kTileSeg;
+            seg_uni[g] = g * seg;
             seg_nj[g] = nj;
             seg_ent[g] = eo + o.ent[sg];
             std::copy(o.rows[sg].begin(), o.rows[sg].end(), seg_row.begin() + g * 24);
-            std::copy(o.uni.begin() + src, o.uni.begin() + src + nj, uni.begin() + g * kTileSeg);
+            std::copy(o.uni.begin() + src, o.uni.begin() + src + nj, uni.begin() + g * seg);
             src += nj;
         }
         for (size_t q = 0; q < o.loc.size(); ++q) {
@@ -1348,6 +1364,7 @@ static int build_stk_tiles(bsgd_plan *p, bool tr, int64_t ntiles, const int64_t 
                     cudaGetErrorString(e));
     }
     N.ntiles = ntiles;
+    N.kz = kz;
     N.ok = true;
     S = N;
     p->device_bytes += N.bytes;

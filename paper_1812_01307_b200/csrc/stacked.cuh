@@ -234,7 +234,7 @@ __global__ void __launch_bounds__(kThreads, (ALIGNED || Epi::K == 4) ? 4 : 3) st
 // share most of their columns (4x4 pixel tiles of A2^T: 4.0 entries per
 // distinct ray; 4 angles x 4 bins of A2: 3.45 entries per distinct pixel,
 // measured at 256^2 x 360 x 363).  Per tile the plan keeps the sorted union of
-// the tile's columns cut into segments of kTileSeg columns, and per segment the
+// the tile's columns cut into segments of tile_seg<KZ>() columns, and per segment the
 // tile rows' entries that fall in it (row-major, uint8 position in the segment
 // + value).  Warp-specialised CTA: four producer warps walk the CTA's stream
 // of (tile, 128-slice chunk, segment) stages and fill a tile_stages()-deep ring
@@ -246,20 +246,18 @@ __global__ void __launch_bounds__(kThreads, (ALIGNED || Epi::K == 4) ? 4 : 3) st
 // output keeps the exact block-sequential arithmetic of the direct kernel.
 // ---------------------------------------------------------------------------
 constexpr int kTileRows = 16;      // rows per tile
-constexpr int kTileSeg = 32;       // union columns per segment
-// ring depth (227 KB of shared memory per CTA: 6 stages with float values, 5 with double)
-template <typename V>
-__host__ __device__ constexpr int tile_stages() { return sizeof(V) == 4 ? 6 : 5; }
-constexpr int kTileSegEnt = kTileRows * kTileSeg;  // entries per segment, upper bound
-constexpr int kTileKZ = 4;         // slices per lane
-constexpr int kTileZC = 32 * kTileKZ;  // slices per item
+// KZ slices per consumer lane (4, or 8 when the depth is a multiple of 256):
+// items of 32 KZ slices, segments of tile_seg<KZ>() columns, so a stage's vector
+// window is 32 KB either way and the entry decode is shared by KZ slices
+template <int KZ>
+__host__ __device__ constexpr int tile_seg() { return KZ == 8 ? 16 : 32; }
+template <int KZ>
+__host__ __device__ constexpr int tile_zc() { return 32 * KZ; }
 // Producer warps: producer p issues ring positions p, p + P, ...; before reusing a
 // slot it waits for the slot's previous round on the empty barrier by phase
 // parity, which is only unambiguous while no producer can run two rounds ahead
 // of the consumers -- guaranteed for P <= the ring depth.
 constexpr int kTileProducers = 4;
-static_assert(kTileProducers <= tile_stages<double>() && kTileProducers <= tile_stages<float>(),
-              "producers must not outnumber the ring slots");
 constexpr int kStkTileThreads = 32 * (16 + kTileProducers);  // 16 consumer warps (one tile row each) + producers
 
 struct StkTiles {
@@ -270,7 +268,7 @@ struct StkTiles {
     const int32_t *seg_nj;     // [segments] columns in the segment
     const int64_t *seg_ent;    // [segments] first entry (multiple of 16)
     const uint16_t *seg_row;   // [segments][24] cumulative entry counts per tile row ([16] = total, padded)
-    const int32_t *uni;        // [segments][kTileSeg] distinct stored columns, per tile ascending (padded)
+    const int32_t *uni;        // [segments][tile_seg] distinct stored columns, per tile ascending (padded)
     const void *ent;           // TileEnt<V> records, per segment padded to 16
 };
 
@@ -282,29 +280,35 @@ struct alignas(sizeof(V) == 4 ? 8 : 16) TileEnt {
     uint32_t cl;
 };
 
-template <typename V>
+template <typename V, int KZ>
 struct TileStage {
-    static constexpr size_t win = sizeof(double) * kTileSeg * kTileZC;
-    static constexpr size_t ent = sizeof(TileEnt<V>) * kTileSegEnt;
+    static constexpr size_t win = sizeof(double) * tile_seg<KZ>() * tile_zc<KZ>();
+    static constexpr size_t ent = sizeof(TileEnt<V>) * kTileRows * tile_seg<KZ>();
     static constexpr size_t row = 48;
     static constexpr size_t bytes = win + ent + row;
 };
 
-template <typename V>
+// ring depth: as many stages as fit 227 KB of shared memory per CTA
+template <typename V, int KZ>
+__host__ __device__ constexpr int tile_stages() { return (int)((227 * 1024 - 2048) / TileStage<V, KZ>::bytes); }
+
+template <typename V, int KZ>
 __host__ __device__ constexpr size_t stk_tile_smem() {
-    return TileStage<V>::bytes * tile_stages<V>() + 2 * tile_stages<V>() * sizeof(uint64_t);
+    return TileStage<V, KZ>::bytes * tile_stages<V, KZ>() + 2 * tile_stages<V, KZ>() * sizeof(uint64_t);
 }
+static_assert(kTileProducers <= tile_stages<double, 4>() && kTileProducers <= tile_stages<double, 8>(),
+              "producers must not outnumber the ring slots");
 
 // Producer warps of the tile-staged kernels: walk the CTA's stream of (tile,
 // slice chunk, segment) stages and fill the ring with TMA bulk copies -- one
 // vector row per distinct column, the stage's entry records (REC, `hdr` = the
 // header slot holding their count, padded to a multiple of `pad`), the header.
-template <typename V, class REC>
+template <typename V, class REC, int KZ>
 __device__ __forceinline__ void stk_tile_produce(const Stk<V> &A, const StkTiles &T, unsigned char *smraw,
                                                  uint64_t *full, uint64_t *empty, int pw, int hdr, int pad) {
-    using ST = TileStage<V>;
-    constexpr int ZC = kTileZC;
-    constexpr int kTileStages = tile_stages<V>();
+    using ST = TileStage<V, KZ>;
+    constexpr int ZC = tile_zc<KZ>();
+    constexpr int kTileStages = tile_stages<V, KZ>();
     const int lane = threadIdx.x & 31;
     const int32_t D = (int32_t)A.D;
     const int64_t nchunks = D / ZC;
@@ -375,7 +379,8 @@ __device__ __forceinline__ void stk_tile_produce(const Stk<V> &A, const StkTiles
             bt.m_ne = (T.seg_row[mine * 24 + hdr] + pad - 1) & ~(pad - 1);
         }
 #pragma unroll
-        for (int q = 0; q < B; ++q) bt.col[q] = bt.gb[q] >= 0 ? __ldg(T.uni + bt.gb[q] * kTileSeg + lane) : 0;
+        for (int q = 0; q < B; ++q)
+            bt.col[q] = (bt.gb[q] >= 0 && lane < tile_seg<KZ>()) ? __ldg(T.uni + bt.gb[q] * tile_seg<KZ>() + lane) : 0;
     };
     Batch cur, nxt;
     fetch(cur);
@@ -409,19 +414,23 @@ __device__ __forceinline__ void stk_tile_produce(const Stk<V> &A, const StkTiles
 // slice s of a consumer lane sits at 2 lane + tile_zoff(s) in the stage's 128 slices
 __device__ __forceinline__ constexpr int tile_zoff(int s) { return (s & 1) + 64 * (s >> 1); }
 
-// the lane's four slice values of one window column (w = column base + 2 lane)
-__device__ __forceinline__ void tile_x4(const double *w, double (&x)[4]) {
-    const double2 a = *reinterpret_cast<const double2 *>(w);
-    const double2 b = *reinterpret_cast<const double2 *>(w + 64);
-    x[0] = a.x; x[1] = a.y; x[2] = b.x; x[3] = b.y;
+// the lane's KZ slice values of one window column (w = column base + 2 lane)
+template <int KZ>
+__device__ __forceinline__ void tile_xk(const double *w, double (&x)[KZ]) {
+#pragma unroll
+    for (int m = 0; m < KZ / 2; ++m) {
+        const double2 a = *reinterpret_cast<const double2 *>(w + 64 * m);
+        x[2 * m] = a.x;
+        x[2 * m + 1] = a.y;
+    }
 }
 
-template <typename V, bool RESID, bool ALIGNED, class Epi>
+template <typename V, int KZ, bool RESID, bool ALIGNED, class Epi>
 __global__ void __launch_bounds__(kStkTileThreads, 1) stacked_tile_kernel(Stk<V> A, StkTiles T, Epi epi, double *part,
                                                                         int64_t *cnt) {
-    using ST = TileStage<V>;
-    constexpr int ZC = kTileZC;
-    constexpr int kTileStages = tile_stages<V>();
+    using ST = TileStage<V, KZ>;
+    constexpr int ZC = tile_zc<KZ>();
+    constexpr int kTileStages = tile_stages<V, KZ>();
     extern __shared__ __align__(128) unsigned char smraw[];
     __shared__ double sm[4 * (kStkTileThreads / 32)];
     uint64_t *full = reinterpret_cast<uint64_t *>(smraw + ST::bytes * kTileStages);
@@ -442,11 +451,10 @@ __global__ void __launch_bounds__(kStkTileThreads, 1) stacked_tile_kernel(Stk<V>
     __syncthreads();
 
     if (warp >= 16) {
-        stk_tile_produce<V, TileEnt<V>>(A, T, smraw, full, empty, warp - 16, 16, 16);
+        stk_tile_produce<V, TileEnt<V>, KZ>(A, T, smraw, full, empty, warp - 16, 16, 16);
     } else {
-        // ------- consumers: tile row = warp, slices z0 + zoff(lane, s) = 2 lane + {0, 1, 64, 65} -------
-        // (two 16-byte shared-memory reads give a lane its four slices, conflict-free)
-        constexpr int KZ = kTileKZ;
+        // ------- consumers: tile row = warp, slices z0 + zoff(lane, s) = 2 lane + (s & 1) + 64 (s >> 1) -------
+        // (KZ / 2 16-byte shared-memory reads give a lane its slices, conflict-free)
         constexpr int NH = 1;
         int k = 0;
         uint32_t round = 0;
@@ -478,9 +486,10 @@ __global__ void __launch_bounds__(kStkTileThreads, 1) stacked_tile_kernel(Stk<V>
 #pragma unroll
                 for (int s = 1; s < KZ; ++s) tmin[h] = thr[h][s] < tmin[h] ? thr[h][s] : tmin[h];
             }
+            // ALIGNED: every slice crosses the same blocks at the same column, jb[h][0] serves all
             auto fold = [&](int h, int s) {
                 if constexpr (RESID) acc[h][s] = rn_sub(acc[h][s], seg[h][s]);
-                else acc[h][s] = (jb[h][s] == 0) ? seg[h][s] : rn_add(acc[h][s], seg[h][s]);
+                else acc[h][s] = (jb[h][ALIGNED ? 0 : s] == 0) ? seg[h][s] : rn_add(acc[h][s], seg[h][s]);
                 seg[h][s] = 0.0;
             };
             for (int64_t g = g0; g < g1; ++g) {
@@ -499,7 +508,8 @@ __global__ void __launch_bounds__(kStkTileThreads, 1) stacked_tile_kernel(Stk<V>
                         if constexpr (ALIGNED) {
                             while (c >= thr[h][0]) {
 #pragma unroll
-                                for (int s = 0; s < KZ; ++s) { fold(h, s); ++jb[h][s]; }
+                                for (int s = 0; s < KZ; ++s) fold(h, s);
+                                ++jb[h][0];
                                 thr[h][0] = (int32_t)__ldg(A.sbounds + jb[h][0] + 1);
                             }
                             tmin[h] = thr[h][0];
@@ -528,9 +538,8 @@ __global__ void __launch_bounds__(kStkTileThreads, 1) stacked_tile_kernel(Stk<V>
                         const double v0 = (double)r0.val, v1 = (double)r1.val;
                         const double *w0 = w + l0 * ZC, *w1 = w + l1 * ZC;
                         double x0[KZ], x1[KZ];
-#pragma unroll
-                        tile_x4(w0, x0);
-                        tile_x4(w1, x1);
+                        tile_xk<KZ>(w0, x0);
+                        tile_xk<KZ>(w1, x1);
                         if (c1 < (ALIGNED ? thr[h][0] : tmin[h])) {
 #pragma unroll
                             for (int s = 0; s < KZ; ++s) {
@@ -552,7 +561,7 @@ __global__ void __launch_bounds__(kStkTileThreads, 1) stacked_tile_kernel(Stk<V>
                         cross((int32_t)(r.cl >> 8));
                         const double v = (double)r.val;
                         double xl[KZ];
-                        tile_x4(w + l * ZC, xl);
+                        tile_xk<KZ>(w + l * ZC, xl);
 #pragma unroll
                         for (int s = 0; s < KZ; ++s) seg[h][s] = rn_add(seg[h][s], rn_mul(v, xl[s]));
                     }
@@ -566,7 +575,15 @@ __global__ void __launch_bounds__(kStkTileThreads, 1) stacked_tile_kernel(Stk<V>
                 if (!live[h]) continue;
 #pragma unroll
                 for (int s = 0; s < KZ; ++s) {
-                    for (; jb[h][s] < A.nb; ++jb[h][s]) fold(h, s);
+                    if constexpr (ALIGNED) {
+                        for (int j = jb[h][0]; j < A.nb; ++j) {   // fold's jb test reads jb[h][0]
+                            if constexpr (RESID) acc[h][s] = rn_sub(acc[h][s], seg[h][s]);
+                            else acc[h][s] = (j == 0) ? seg[h][s] : rn_add(acc[h][s], seg[h][s]);
+                            seg[h][s] = 0.0;
+                        }
+                    } else {
+                        for (; jb[h][s] < A.nb; ++jb[h][s]) fold(h, s);
+                    }
                     epi(srow[h] * D + zl + tile_zoff(s), acc[h][s]);
                 }
             }
