@@ -286,16 +286,20 @@ def run_ours(args):
         solvers.bsgd_tv_iteration(st2, op, d.y, cfg)
         hx, hr = st2.x, st2.r_vec
     torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    for _ in range(e2e_steps):
-        st2.x, st2.r_vec = hx, hr
-        solvers.bsgd_tv_iteration(st2, op, d.y, cfg)
-        hx, hr = st2.x, st2.r_vec
-    torch.cuda.synchronize()
-    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    batches = []
+    for _ in range(3):   # median of three batches: the host side makes single batches noisy
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            st2.x, st2.r_vec = hx, hr
+            solvers.bsgd_tv_iteration(st2, op, d.y, cfg)
+            hx, hr = st2.x, st2.r_vec
+        torch.cuda.synchronize()
+        batches.append((time.perf_counter() - t0) / e2e_steps)
+    e2e_s = sorted(batches)[1]
     e2e = {"value": round(1.0 / e2e_s, 2), "unit": "epochs/s", "h2d_bytes_per_step": (rows + cols) * 8,
            "d2h_bytes_per_step": (rows + cols) * 8,
-           "how": "bsgd_tv_iteration with numpy x, r_vec set before and read after every epoch"}
+           "how": "bsgd_tv_iteration with numpy x, r_vec set before and read after every epoch "
+                  "(median of three batches)"}
     log(f"[bench] e2e host-state: {e2e_s * 1e3:.3f} ms/epoch")
 
     # ---- CPU baseline (oracle port) on a bounded sample ----
