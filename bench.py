@@ -548,6 +548,7 @@ def run_ct_secondary(args, index):
            "monitor_decrease": False, "mean_fgp_iterations": round(fgp_iters, 2),
            "tv_prox": {"image": "x".join(str(v) for v in shape), "iterations": d.max_inner_iters,
                        "ms": round(pms, 4), "algorithmic_bytes": pbytes, "gbs": round(pbytes / (pms * 1e6), 1),
+                       "frac": round(pbytes / (pms * 1e6) / peaks()[0], 4),
                        "note": ("fields are L2-resident at 2D sizes; bound by grid barriers / latency, not HBM"
                                 if dim == 2 else
                                 "fields stream from HBM (134 MB each); split passes with direct pairwise "
