@@ -106,10 +106,17 @@ class CudaShard:
 
     @classmethod
     def stacked(cls, slice_matrix, depth: int, spec: ShardSpec, device=None, lam: float = 0.0,
-                layout=None) -> "CudaShard":
-        """Shard of a slice-stacked operator A2 (x) I_depth: the rank's stored rows of A2."""
+                layout=None, image_shape=None, rays=None) -> "CudaShard":
+        """Shard of a slice-stacked operator A2 (x) I_depth: the rank's stored rows of A2.
+
+        ``image_shape`` = (height, width) of A2's columns and ``rays`` =
+        (num_angles, num_bins) of its angle-major rows switch on the tile-staged
+        products for the shard (`BlockOperator.set_stacked_tiles`): 4 x 4 pixel
+        tiles for A2^T, and 4 angles x 4 bins for the rank's rays when they are
+        whole angles (else runs of 16 consecutive rays).  Results are unchanged
+        bit for bit."""
         from scipy import sparse
-        from .blockops import BlockPartition
+        from .blockops import BlockPartition, grid_tiles
         if spec.granularity != depth:
             raise ValueError("a stacked shard needs ShardSpec(..., granularity=depth)")
         a2 = sparse.csr_array(slice_matrix)
@@ -117,6 +124,20 @@ class CudaShard:
         part = BlockPartition(spec.local_row_bounds, spec.partition.col_bounds)
         self = cls.__new__(cls)
         op = BlockOperator.stacked(sparse.csr_array(a2[s0:s1, :]), depth, part, device=device)
+        if image_shape is not None:
+            h, w = (int(v) for v in image_shape)
+            if h * w != a2.shape[1]:
+                raise ValueError("image_shape does not match the slice matrix's columns")
+            op.set_stacked_tiles(True, grid_tiles(h, w))
+        if rays is not None:
+            na, nb = (int(v) for v in rays)
+            if na * nb != a2.shape[0]:
+                raise ValueError("rays does not match the slice matrix's rows")
+            nloc = s1 - s0
+            if s0 % nb == 0 and s1 % nb == 0:
+                op.set_stacked_tiles(False, grid_tiles(nloc // nb, nb))
+            else:
+                op.set_stacked_tiles(False, grid_tiles(1, nloc, 1, 16))
         self._finish(spec, op, a2.shape[1] * depth, lam, layout)
         return self
 
