@@ -210,15 +210,17 @@ struct bsgd_plan {
         bool ok = false;
         int gb = 32;            // lanes per row (blocks of 4 gb entries)
         int64_t *ptr = nullptr;
-        int32_t *idx = nullptr;
+        int32_t *idx = nullptr;     // NULL when the compressed indices are used
         void *val = nullptr;
+        int32_t *base = nullptr;    // compressed indices (spmv.cuh blk_cols)
+        uint16_t *del = nullptr;
         size_t bytes = 0;
     } fb;
     bool stacked() const { return depth > 1; }
 };
 
 static void blk_free(bsgd_plan::BlkStore &b) {
-    cudaFree(b.ptr); cudaFree(b.idx); cudaFree(b.val);
+    cudaFree(b.ptr); cudaFree(b.idx); cudaFree(b.val); cudaFree(b.base); cudaFree(b.del);
     b = bsgd_plan::BlkStore();
 }
 
@@ -433,6 +435,34 @@ static int build_blocked(bsgd_plan *p, cudaStream_t st) {
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) return bail(e);
     b.bytes = sizeof(int64_t) * (p->rows + 1) + (sizeof(int32_t) + sizeof(V)) * (size_t)total;
+    // 16-bit column increments within a lane's four entries when they fit (CT rays:
+    // a few image rows apart): 7 instead of 8 stream bytes per float32 entry
+    if (!getenv("BSGD_NO_BLK_COMPRESS")) {
+        int32_t *bb = nullptr;
+        uint16_t *dd = nullptr;
+        int *bad = nullptr;
+        cudaError_t e2 = cudaMalloc(&bb, sizeof(int32_t) * std::max<int64_t>(total / 4, 1));
+        if (e2 == cudaSuccess) e2 = cudaMalloc(&dd, sizeof(uint16_t) * std::max<int64_t>(total, 1));
+        if (e2 == cudaSuccess) e2 = cudaMalloc(&bad, sizeof(int));
+        int hbad = 1;
+        if (e2 == cudaSuccess) e2 = cudaMemsetAsync(bad, 0, sizeof(int), st);
+        if (e2 == cudaSuccess) {
+            blk_compress_kernel<<<grid_1d(std::max<int64_t>(total / 4, 1)), kThreads, 0, st>>>(total / 4, b.idx, bb, dd,
+                                                                                               bad);
+            e2 = cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, st);
+        }
+        if (e2 == cudaSuccess) e2 = cudaStreamSynchronize(st);
+        cudaFree(bad);
+        if (e2 == cudaSuccess && hbad == 0) {   // both kept until tune_blocked times them
+            b.base = bb;
+            b.del = dd;
+            b.bytes += (1 + sizeof(uint16_t)) * (size_t)total;
+        } else {
+            cudaGetLastError();
+            cudaFree(bb);
+            cudaFree(dd);
+        }
+    }
     b.ok = true;
     p->fb = b;
     p->device_bytes += b.bytes;
@@ -859,16 +889,74 @@ static bool gtiles_on(const bsgd_plan::GTileStore &S) { return S.ok && !getenv("
 template <typename V, class E>
 static int launch_blocked(const bsgd_plan *p, const double *vec, const E &e, double *part, int64_t *cnt,
                           cudaStream_t st) {
-    const CsrB<V> A{p->rows, p->fb.ptr, p->fb.idx, (const V *)p->fb.val, vec};
+    CsrB<V> A{p->rows, p->fb.ptr, p->fb.idx, (const V *)p->fb.val, vec};
+    A.base = p->fb.base;
+    A.del = p->fb.del;
     auto go = [&](auto kern, int G) {
         const int cap = std::min(occupancy(kern) * num_sms(), kMaxPartials);
         kern<<<ctas_for(p->rows, G, cap), kThreads, 0, st>>>(A, e, part, cnt);
     };
-    if (p->fb.gb == 16) go(csr_blocked_kernel<V, 16, E>, 16);
-    else if (p->fb.gb == 8) go(csr_blocked_kernel<V, 8, E>, 8);
-    else if (p->fb.gb == 4) go(csr_blocked_kernel<V, 4, E>, 4);
-    else go(csr_blocked_kernel<V, 32, E>, 32);
+    const bool cmp = p->fb.base != nullptr;
+    if (p->fb.gb == 16) cmp ? go(csr_blocked_kernel<V, 16, E, true>, 16) : go(csr_blocked_kernel<V, 16, E>, 16);
+    else if (p->fb.gb == 8) cmp ? go(csr_blocked_kernel<V, 8, E, true>, 8) : go(csr_blocked_kernel<V, 8, E>, 8);
+    else if (p->fb.gb == 4) cmp ? go(csr_blocked_kernel<V, 4, E, true>, 4) : go(csr_blocked_kernel<V, 4, E>, 4);
+    else cmp ? go(csr_blocked_kernel<V, 32, E, true>, 32) : go(csr_blocked_kernel<V, 32, E>, 32);
     LAUNCHED();
+    return BSGD_OK;
+}
+
+// Keep the compressed or the plain indices of the blocked copy, whichever times
+// faster on this matrix (configs[2]: 0.457 -> 0.415 ms compressed; configs[3],
+// 4 lanes per ray: 3.04 ms plain vs 3.20 compressed).
+template <typename V>
+static int tune_blocked(bsgd_plan *p, cudaStream_t st) {
+    bsgd_plan::BlkStore &b = p->fb;
+    if (!b.ok || b.base == nullptr || b.idx == nullptr) return BSGD_OK;
+    double *vin = nullptr, *vout = nullptr;
+    bool keep_cmp = false;
+    if (cudaMalloc(&vin, sizeof(double) * p->cols) == cudaSuccess &&
+        cudaMalloc(&vout, sizeof(double) * p->rows) == cudaSuccess) {
+        cudaMemsetAsync(vin, 0, sizeof(double) * p->cols, st);
+        cudaEvent_t e0, e1;
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        float t[2] = {0.f, 0.f};
+        int32_t *base = b.base;
+        uint16_t *del = b.del;
+        for (int variant = 0; variant < 2; ++variant) {
+            b.base = variant ? base : nullptr;
+            b.del = variant ? del : nullptr;
+            for (int rep = 0; rep < 4; ++rep) {
+                if (rep == 1) cudaEventRecord(e0, st);
+                launch_blocked<V>(p, vin, EpiStore{vout, 1.0}, nullptr, nullptr, st);
+            }
+            cudaEventRecord(e1, st);
+            cudaEventSynchronize(e1);
+            cudaEventElapsedTime(&t[variant], e0, e1);
+        }
+        b.base = base;
+        b.del = del;
+        keep_cmp = t[1] < 0.98f * t[0];
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+    }
+    cudaGetLastError();
+    cudaFree(vin);
+    cudaFree(vout);
+    if (keep_cmp) {
+        cudaFree(b.idx);
+        b.idx = nullptr;
+    } else {
+        cudaFree(b.base);
+        cudaFree(b.del);
+        b.base = nullptr;
+        b.del = nullptr;
+    }
+    const int64_t n = [&]() { int64_t v = 0; cudaMemcpy(&v, b.ptr + p->rows, sizeof(int64_t), cudaMemcpyDeviceToHost); return v; }();
+    p->device_bytes -= b.bytes;
+    b.bytes = sizeof(int64_t) * (p->rows + 1) + (keep_cmp ? (1 + sizeof(uint16_t)) : sizeof(int32_t)) * (size_t)n +
+              sizeof(V) * (size_t)n;
+    p->device_bytes += b.bytes;
     return BSGD_OK;
 }
 
@@ -1649,6 +1737,8 @@ static int plan_finish(bsgd_plan *p, cudaStream_t st) {
     rc = (value_dtype == BSGD_F32) ? build_transpose<float>(p, st) : build_transpose<double>(p, st);
     if (rc != BSGD_OK) return rc;
     rc = (value_dtype == BSGD_F32) ? build_blocked<float>(p, st) : build_blocked<double>(p, st);
+    if (rc != BSGD_OK) return rc;
+    rc = (value_dtype == BSGD_F32) ? tune_blocked<float>(p, st) : tune_blocked<double>(p, st);
     if (rc != BSGD_OK) return rc;
     {
         // panel-tiled copies (tiled.cuh) are an opt-in experiment: on every

@@ -241,7 +241,33 @@ struct CsrB {
     const int32_t *idx;
     const V *val;
     const double *vec;
+    // compressed indices (CMP): a lane's four columns as base[k / 4] plus three
+    // 16-bit increments del[k + 1 .. k + 3] (del[k] unused): 3 bytes per entry
+    const int32_t *base = nullptr;
+    const uint16_t *del = nullptr;
 };
+
+__device__ __forceinline__ uint2 ld_stream_u2(const void *p, uint64_t pol) {
+    uint2 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u32 {%0,%1}, [%2], %3;"
+                 : "=r"(v.x), "=r"(v.y) : "l"(p), "l"(pol));
+    return v;
+}
+
+// the lane's four columns of the block at entry k
+template <bool CMP, typename V>
+__device__ __forceinline__ int4 blk_cols(const CsrB<V> &A, int64_t k, uint64_t pol) {
+    if constexpr (CMP) {
+        const int32_t c0 = ld_stream(A.base + (k >> 2), pol);
+        const uint2 d = ld_stream_u2(A.del + k, pol);
+        const int32_t c1 = c0 + (int32_t)(d.x >> 16);
+        const int32_t c2 = c1 + (int32_t)(d.y & 0xFFFFu);
+        const int32_t c3 = c2 + (int32_t)(d.y >> 16);
+        return make_int4(c0, c1, c2, c3);
+    } else {
+        return ld_stream4(A.idx + k, pol);
+    }
+}
 
 __device__ __forceinline__ void blk_vals(const float *p, double (&v)[4], uint64_t pol) {
     const float4 a = ld_stream4(p, pol);
@@ -252,7 +278,7 @@ __device__ __forceinline__ void blk_vals(const double *p, double (&v)[4], uint64
     v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
 }
 
-template <typename V, int GB, class Epi>
+template <typename V, int GB, class Epi, bool CMP = false>
 __global__ void __launch_bounds__(kThreads) csr_blocked_kernel(CsrB<V> A, Epi epi, double *part, int64_t *cnt) {
     constexpr int BLK = 4 * GB;
     constexpr int RPW = 32 / GB;
@@ -270,7 +296,7 @@ __global__ void __launch_bounds__(kThreads) csr_blocked_kernel(CsrB<V> A, Epi ep
             const int64_t beg = A.ptr[row], end = A.ptr[row + 1];
             int64_t k = beg + 4 * gl;
             for (; k + BLK < end; k += 2 * BLK) {
-                const int4 ca = ld_stream4(A.idx + k, pol), cb = ld_stream4(A.idx + k + BLK, pol);
+                const int4 ca = blk_cols<CMP>(A, k, pol), cb = blk_cols<CMP>(A, k + BLK, pol);
                 double va[4], vb[4];
                 blk_vals(A.val + k, va, pol);
                 blk_vals(A.val + k + BLK, vb, pol);
@@ -281,7 +307,7 @@ __global__ void __launch_bounds__(kThreads) csr_blocked_kernel(CsrB<V> A, Epi ep
                 s = fma(vb[0], xb0, s); s = fma(vb[1], xb1, s); s = fma(vb[2], xb2, s); s = fma(vb[3], xb3, s);
             }
             if (k < end) {
-                const int4 ca = ld_stream4(A.idx + k, pol);
+                const int4 ca = blk_cols<CMP>(A, k, pol);
                 double va[4];
                 blk_vals(A.val + k, va, pol);
                 const double xa0 = __ldg(vec + ca.x), xa1 = __ldg(vec + ca.y), xa2 = __ldg(vec + ca.z),
@@ -301,6 +327,22 @@ __global__ void __launch_bounds__(kThreads) csr_blocked_kernel(CsrB<V> A, Epi ep
             for (int q = 0; q < Epi::K; ++q) part[(size_t)blockIdx.x * Epi::K + q] = v[q];
     }
     if (blockIdx.x == 0 && threadIdx.x == 0 && cnt != nullptr) cnt[0] = gridDim.x;
+}
+
+// compress the blocked indices: per lane-block q (entries 4q .. 4q + 3, one lane's
+// ascending columns) base[q] = first column, del[4q + m] = column m - column m-1;
+// *bad != 0 when an increment does not fit 16 bits
+__global__ void blk_compress_kernel(int64_t nq, const int32_t *idx, int32_t *base, uint16_t *del, int *bad) {
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nq; q += (int64_t)gridDim.x * blockDim.x) {
+        const int4 c = reinterpret_cast<const int4 *>(idx)[q];
+        const int64_t d1 = (int64_t)c.y - c.x, d2 = (int64_t)c.z - c.y, d3 = (int64_t)c.w - c.z;
+        if (d1 < 0 || d2 < 0 || d3 < 0 || d1 > 65535 || d2 > 65535 || d3 > 65535) atomicExch(bad, 1);
+        base[q] = c.x;
+        del[4 * q] = 0;
+        del[4 * q + 1] = (uint16_t)d1;
+        del[4 * q + 2] = (uint16_t)d2;
+        del[4 * q + 3] = (uint16_t)d3;
+    }
 }
 
 // padded row lengths (whole blocks of blk entries) for the blocked copy
