@@ -1,33 +1,42 @@
 #!/usr/bin/env python
-"""BSGD-TV epoch throughput on B200 (BASELINE.json metric, configs[1] workload).
+"""BSGD-TV epoch throughput on B200 (BASELINE.json metric; headline workload configs[3]).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-A step is one BSGD-TV epoch (Algorithm 1, `bsgd_tv_iteration`, alpha = gamma
-= 1, monitor off) over the configs[1] system: A 2,000,000 x 500,000 with 32
-distinct uniform columns per row, float32 values N(0,1)/sqrt(32), M = N = 8
-blocks, lambda = 0, mu = 0.9 / (2 u_max) from 50 power iterations.  Inputs are
-seeded synthetic data of exactly that shape.  A (0.5 GB) and A^T (0.5 GB)
-exceed the 126 MB L2, so every epoch streams from HBM without an explicit
-flush.
+A step is one BSGD-TV epoch (Algorithm 1, `bsgd_tv_iteration`,
+`solvers.py:259-341`, alpha = gamma = 1, monitor off) of configs[3]: 2-D
+parallel-beam CT, 1024 x 1024 image, 1440 angles x 1449 bins, Siddon float32
+CSR (1.92e9 nonzeros, int32 indices), M = N = 8 blocks, lambda = 0.01, TV prox
+by dual FGP with at most 20 iterations (tol 1e-5), mu = 0.9 / (2 u_max) read
+from tests/golden/config_mu.json (computed once, identical in both arms).  The
+largest configuration that fits one GPU and the one BASELINE.json scales over
+1/2/4/8 GPUs.  Inputs are seeded synthetic data of exactly that definition
+(problems.py); A and A^T (15.4 GB each) exceed the 126 MB L2, so every epoch
+streams from HBM with no explicit flush.
 
 Arms:
   ours       value: K epochs with the state resident in HBM (CUDA-graph replay),
              device time from CUDA events, max over ranks.
-             e2e: K epochs through the drop-in `bsgd_tv_iteration` with HOST
-             numpy state (x, r uploaded before and downloaded after every epoch).
-             roofline: the dominant SpMV kernel timed alone with CUDA events.
-             cpu_baseline: the CPU oracle port (C + OpenMP, all host threads) on
-             a bounded sample of epochs of the same workload.
-  reference  the CPU oracle port alone (rank 0), printed as the reference arm.
-Multi-GPU (torchrun, N > 1): row-slab ownership, see paper_1812_01307_b200/parallel.py.
+             phases / roofline: K eager epochs with CUDA events recorded between
+             the epoch's kernels on the launching stream (bsgd_plan_timing): the
+             in-epoch K1 / K2 / prox times, the dominant kernel's achieved GB/s.
+             e2e: K epochs through the drop-in `bsgd_tv_iteration` with HOST numpy
+             state (x, r uploaded before and downloaded after every epoch).
+             cpu_baseline: the CPU oracle port (C + OpenMP, all host threads) on a
+             bounded sample of epochs of the same configs[3] system.
+             secondary: configs[1], [2], [4] (device-resident epochs/s, products).
+  reference  the reference package itself (baseline/_ref, `bsgdtv`, unmodified)
+             through its own bsgd_tv_iteration with a ThreadPoolExecutor over all
+             host cores, on the same A, y, mu; falls back to the oracle port when
+             baseline/_ref is absent.  Rank 0 only.
+Multi-GPU (torchrun, N > 1): configs[3] row slabs generated on each rank's GPU,
+see paper_1812_01307_b200/parallel.py.
 """
 
 from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
 import statistics
 import subprocess
@@ -41,9 +50,21 @@ REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
 
 METRIC = "BSGD-TV epochs/s + achieved HBM GB/s (SpMV, TV-prox) at 1/2/4/8 B200"
-WORKLOAD = ("configs[1]: pure BSGD least squares (lambda=0), A 2,000,000 x 500,000, 32 nnz/row, "
-            "float32 values, M=N=8, mu=0.9/(2 u_max)")
-ROWS, COLS, NNZ_ROW, BLOCKS = 2_000_000, 500_000, 32, 8
+HEADLINE = 3
+MU_TABLE = os.path.join(REPO, "tests", "golden", "config_mu.json")
+REF_DIR = os.path.join(REPO, "baseline", "_ref")
+
+WORKLOADS = {
+    1: "configs[1]: pure BSGD least squares (lambda=0), A 2,000,000 x 500,000, 32 nnz/row, float32 values, "
+       "M=N=8, monitor off",
+    2: "configs[2]: 2D parallel-beam CT 512x512, 720 angles x 727 bins, Siddon float32 CSR, lambda=0.01, "
+       "FGP<=20 (tol 1e-5), M=N=8, monitor off",
+    3: "configs[3]: 2D parallel-beam CT 1024x1024, 1440 angles x 1449 bins, Siddon float32 CSR (int32 indices), "
+       "lambda=0.01, FGP<=20 (tol 1e-5), M=N=8, monitor off",
+    4: "configs[4]: 3D slice-stacked parallel-beam CT 256^3, 360 angles x 256 rows x 363 bins, block-diagonal "
+       "A = A2 (x) I_256 (only the 2-D slice matrix A2 is stored), isotropic 3D TV FGP<=10, lambda=0.01, "
+       "M=N=16, monitor off",
+}
 
 
 def log(*a):
@@ -59,51 +80,49 @@ def peaks():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def config_dict(extra=None):
-    d = {"workload": WORKLOAD, "rows": ROWS, "cols": COLS, "nnz_per_row": NNZ_ROW, "nnz": ROWS * NNZ_ROW,
-         "blocks": f"{BLOCKS}x{BLOCKS}", "lam": 0.0, "monitor_decrease": False,
+def mu_for(index):
+    """(mu, u_max) recorded once for configs[index] (tools/make_mu.py)."""
+    with open(MU_TABLE) as fh:
+        e = json.load(fh)[f"configs[{index}]"]
+    return float(e["mu"]), float(e["u_max"])
+
+
+def config_dict(index, nnz, mu, u_max):
+    """The workload definition: identical in both arms (execution details live outside)."""
+    d = {"workload": WORKLOADS[index], "nnz": int(nnz), "mu": mu, "u_max": u_max,
+         "mu_source": "tests/golden/config_mu.json (50 power iterations, computed once, shared by both arms)",
+         "monitor_decrease": False, "alpha": 1.0, "gamma": 1.0,
          "matrix_dtype": "f32 values, int32 indices, int64 row pointers", "vector_dtype": "f64",
-         "l2": "no flush needed: A and A^T (1.0 GB) exceed the 126 MB L2 every epoch",
-         "seeds": {"matrix": 2, "x_true": 0, "solver": 0, "power_iteration": 0}}
-    if extra:
-        d.update(extra)
-    return d
-
-
-def make_problem():
-    from paper_1812_01307_b200 import problems
-    t0 = time.time()
-    d = problems.config(1)
-    log(f"[bench] generated configs[1] in {time.time() - t0:.1f}s: {d.matrix.shape}, nnz={d.matrix.nnz}")
+         "seeds": {"phantom": 0, "noise": 1, "solver": 0} if index != 1 else
+                  {"matrix": 2, "x_true": 0, "solver": 0}}
+    if index == 3:
+        d.update({"image": "1024x1024", "rays": 1440 * 1449, "blocks": "8x8", "lam": 0.01, "fgp_max_iters": 20,
+                  "fgp_tol": 1e-5, "l2": "no flush needed: A and A^T (15.4 GB each) exceed the 126 MB L2 every epoch"})
     return d
 
 
 # --- CPU (oracle port) ---------------------------------------------------------
 
-def cpu_epochs(d, steps, warmup, mu=None, budget_s=None):
+def oracle_epochs(csr, y, blocks, mu, lam, max_inner, tol, hw, warmup, steps, budget_s):
     """Time oracle epochs (C restatement + numpy, all host threads). Returns (epochs/s, info)."""
     from oracle import oracle as orc
     threads = orc.default_threads()
-    oop = orc.OracleOperator(d.matrix, BLOCKS, BLOCKS, threads=threads)
-    if mu is None:
-        t0 = time.time()
-        u, _, _ = orc.largest_eigenvalue(oop, max_iters=50)
-        mu = 0.9 / (2.0 * u)
-        log(f"[bench] oracle power iteration: u_max={u:.6f} in {time.time() - t0:.1f}s")
-    prm = orc.Params(mu=mu, lam=0.0, epochs=10 ** 9, monitor_decrease=False)
-    st = orc.init_state(oop, d.y, prm)
+    oop = orc.OracleOperator(csr, blocks, blocks, threads=threads)
+    prm = orc.Params(mu=mu, lam=lam, epochs=10 ** 9, max_inner_iters=max_inner, tol=tol, monitor_decrease=False)
+    st = orc.init_state(oop, y, prm)
+    perm = np.arange(csr.shape[1]) if lam > 0 else None
     for _ in range(warmup):
-        orc.epoch(st, oop, d.y, prm)
+        orc.epoch(st, oop, y, prm, perm, hw)
     times = []
     t_start = time.perf_counter()
-    for k in range(steps):
+    for _ in range(steps):
         t0 = time.perf_counter()
-        orc.epoch(st, oop, d.y, prm)
+        orc.epoch(st, oop, y, prm, perm, hw)
         times.append(time.perf_counter() - t0)
-        if budget_s is not None and time.perf_counter() - t_start > budget_s:
+        if time.perf_counter() - t_start > budget_s:
             break
     total = sum(times)
-    return len(times) / total, {"cores": threads, "epochs_timed": len(times), "seconds": total, "mu": mu}
+    return len(times) / total, {"cores": threads, "epochs_timed": len(times), "seconds": round(total, 3)}
 
 
 # --- clocks ------------------------------------------------------------------------
@@ -173,198 +192,308 @@ def dist_info():
     return world, rank, local
 
 
-def bytes_model():
-    """Algorithmic bytes per launch of the two SpMV kernels (DESIGN.md §Byte model)."""
-    nnz = ROWS * NNZ_ROW
-    k1 = nnz * (4 + 4) + (ROWS + 1) * 8 + COLS * 8 + 2 * ROWS * 8          # A, rowptr, x once, y in, r out
-    # K2 is timed as bsgd_grad (g = 2 A^T r): A^T, ptr, r once, g out; inside the epoch the
-    # step epilogue also reads x_k and writes x_next (+2 * COLS * 8)
-    k2 = nnz * (4 + 4) + (COLS + 1) * 8 + ROWS * 8 + COLS * 8
+def csr_bytes(nnz, rows, cols):
+    """SURVEY.md §8(d) byte model of the two products inside an epoch (float32
+    values + int32 indices, int64 row pointers, float64 vectors):
+    K1 (lookahead, EpiResid): A stream, pointers, x once, y in, r out;
+    K2 (EpiStep with the prox on): A^T stream, pointers, r once, x_k in, g and
+    the prox input image b = x_k + mu g out."""
+    k1 = nnz * 8 + (rows + 1) * 8 + cols * 8 + 2 * rows * 8
+    k2 = nnz * 8 + (cols + 1) * 8 + rows * 8 + 3 * cols * 8
     return k1, k2
+
+
+def prox_bytes(npx, dim, iters):
+    """Fused-schedule prox bytes: per FGP iteration the candidate
+    (read q, b; write c) and the dual value + momentum commit (read c, p, b;
+    write q): (5 dim + 2) fields of 8 bytes, plus ~10 fields of setup/finalize."""
+    return 8 * npx * ((5 * dim + 2) * iters + 10)
+
+
+def time_events(fn, reps):
+    import torch
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(reps):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps
 
 
 def run_ours(args):
     import torch
-    from paper_1812_01307_b200 import _native as nat
-    from paper_1812_01307_b200 import blockops, solvers, spectral
+    from paper_1812_01307_b200 import problems, solvers, tv
 
     world, rank, local = dist_info()
     if world > 1:
         return run_multi(args)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    d = make_problem()
     t0 = time.time()
-    op = blockops.BlockOperator(d.matrix, blockops.make_partition(ROWS, COLS, BLOCKS, BLOCKS))
+    d = problems.config_device(HEADLINE)
+    op = d.op
     torch.cuda.synchronize()
-    log(f"[bench] plan (upload + device transpose) {time.time() - t0:.2f}s")
-    pw = spectral.largest_eigenvalue(op, max_iters=50)
-    mu = 0.9 / (2.0 * pw.value)
-    log(f"[bench] GPU power iteration u_max={pw.value:.6f} converged={pw.converged}")
-    cfg = solvers.SolverConfig(mu=mu, lam=0.0, epochs=10 ** 9, monitor_decrease=False)
+    rows, cols = op.shape
+    nnz = int(op.nnz)
+    log(f"[bench] configs[3] on device in {time.time() - t0:.1f}s: {op.shape}, nnz={nnz}, "
+        f"kernels {op.kernel_info()}")
+    mu, u_max = mu_for(HEADLINE)
+    lay = d.layout()
+    cfg = solvers.SolverConfig(mu=mu, lam=d.lam, epochs=10 ** 9, prox=tv.ProxSettings(d.max_inner_iters, 1e-5),
+                               monitor_decrease=False)
+    steps = max(2, args.steps // 2 * 2)
 
     # ---- value: resident state, graph replay ----
     st = solvers.init_bsgd_state(op, d.y, cfg)
-    st._ensure_history(args.steps + args.warmup + 16)
-    for _ in range(max(1, args.warmup)):
-        solvers.bsgd_tv_iteration(st, op, d.y, cfg)
-    runner = solvers._GraphRunner(st, cfg, None, st._y, 2)
+    st._ensure_history(4 * steps + args.warmup + 16)
+    for _ in range(args.warmup):
+        solvers.bsgd_tv_iteration(st, op, d.y, cfg, layout=lay)
+    runner = solvers._GraphRunner(st, cfg, lay, st._y, 2)
     assert runner.capture(False), "CUDA graph capture failed"
-    pairs_needed = args.steps // 2
     runner.replay()  # warm the graph itself
     torch.cuda.synchronize()
+    row0 = st._rows_used + 2
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with Clocks(local) as clk:
         torch.cuda.synchronize()
         start.record()
-        for _ in range(pairs_needed):
+        for _ in range(steps // 2):
             runner.replay()
-        if args.steps % 2:
-            solvers.bsgd_tv_iteration(st, op, st._y, cfg)
         stop.record()
         torch.cuda.synchronize()
-    ms = start.elapsed_time(stop)
-    ms_per_step = ms / args.steps
+    st._rows_used += 2 + steps
+    ms_per_step = start.elapsed_time(stop) / steps
     value = 1000.0 / ms_per_step
     clocks = clk.summary()
-    log(f"[bench] resident: {ms_per_step:.4f} ms/epoch -> {value:.1f} epochs/s")
+    hist = st._hist[row0:row0 + steps].cpu().numpy()
+    fgp_iters = float(np.mean(hist[:, 5]))
+    log(f"[bench] resident: {ms_per_step:.4f} ms/epoch -> {value:.2f} epochs/s (mean FGP iterations {fgp_iters:.2f})")
 
-    # ---- roofline: the two SpMV kernels timed alone on the same inputs ----
-    rows, cols = op.shape
-    x = st.x_device.clone()
-    r = st.r_device.clone()
-    y = st._y
-    rout = torch.empty_like(r)
-    g = torch.empty_like(x)
-    scratch = torch.empty(nat.SCRATCH_BYTES // 8, dtype=torch.float64, device=dev)
-    s_dev = torch.empty(1, dtype=torch.float64, device=dev)
-    reps = 20
-
-    def time_kernel(fn):
-        for _ in range(3):
-            fn()
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(reps):
-            fn()
-        e1.record()
-        torch.cuda.synchronize()
-        return e0.elapsed_time(e1) / reps
-
-    sp = nat.stream_ptr(dev)
-    t_k1 = time_kernel(lambda: nat.call("bsgd_residual", op.plan, nat.ptr(x), nat.ptr(y), nat.ptr(rout), None, None, sp))
-    t_k2 = time_kernel(lambda: nat.call("bsgd_grad", op.plan, nat.ptr(r), nat.ptr(g), sp))
-    b1, b2 = bytes_model()
+    # ---- phases: the same epochs eagerly, CUDA events between the kernels ----
+    op.set_phase_timing(True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(steps):
+        solvers.bsgd_tv_iteration(st, op, st._y, cfg, layout=lay)
+    e1.record()
+    torch.cuda.synchronize()
+    eager_ms = e0.elapsed_time(e1) / steps
+    ph, n_ep = op.phase_timing()
+    op.set_phase_timing(False)
+    ph = {k: v / max(n_ep, 1) for k, v in ph.items()}
+    b1, b2 = csr_bytes(nnz, rows, cols)
     peak, peak_src = peaks()
-    k1_gbs, k2_gbs = b1 / (t_k1 * 1e6), b2 / (t_k2 * 1e6)
-    dominant = ("K1 forward CSR SpMV + residual epilogue", b1, t_k1, k1_gbs) if t_k1 >= t_k2 else \
-               ("K2 transposed CSR SpMV + step epilogue", b2, t_k2, k2_gbs)
+    kernels = {"k1_forward_lookahead": {"kernel": f"{op.kernel_info()['forward']} CSR, EpiResid (r = y - A x)",
+                                        "ms": round(ph["k1_lookahead"], 4), "bytes": b1,
+                                        "gbs": round(b1 / (ph["k1_lookahead"] * 1e6), 1)},
+               "k2_transposed_step": {"kernel": f"{op.kernel_info()['transposed']}, EpiStep (g = 2 A^T r, b = x + mu g)",
+                                      "ms": round(ph["k2_step"], 4), "bytes": b2,
+                                      "gbs": round(b2 / (ph["k2_step"] * 1e6), 1)},
+               "k3_tv_prox": {"kernel": "fgp_kernel<2> (cooperative, FGP decisions on device)",
+                              "ms": round(ph["prox"], 4), "mean_fgp_iterations": round(fgp_iters, 2)},
+               "tail": {"ms": round(ph["tail"], 4)}}
+    for k in kernels.values():
+        if "gbs" in k:
+            k["frac"] = round(k["gbs"] / peak, 4)
+    dom_key = "k1_forward_lookahead" if ph["k1_lookahead"] >= ph["k2_step"] else "k2_transposed_step"
+    dom = kernels[dom_key]
+    phase_sum = sum(ph.values())
     traffic = None
     prof = os.path.join(REPO, "profiles", "roofline_traffic.json")
     if os.path.exists(prof):
         with open(prof) as fh:
-            tr = json.load(fh)
-        # per-kernel DRAM bytes of one ncu --set full capture (k1 / k2), else the legacy single value
-        traffic = tr.get("k1" if t_k1 >= t_k2 else "k2", {}).get("dram_bytes_per_launch",
-                                                                 tr.get("dram_bytes_per_launch"))
-    roofline = {"bound": "hbm", "kernel": dominant[0], "achieved": round(dominant[3], 1), "peak": peak,
-                "unit": "GB/s", "frac": round(dominant[3] / peak, 4), "traffic": traffic,
-                "algorithmic_bytes": dominant[1], "launch_ms": round(dominant[2], 5), "peak_source": peak_src,
-                "kernels": {"k1_forward": {"ms": round(t_k1, 5), "bytes": b1, "gbs": round(k1_gbs, 1)},
-                            "k2_transposed": {"ms": round(t_k2, 5), "bytes": b2, "gbs": round(k2_gbs, 1)}},
-                "epoch_gbs": round((b1 + b2) / (ms_per_step * 1e6), 1)}
-    log(f"[bench] K1 {t_k1:.4f} ms {k1_gbs:.0f} GB/s | K2 {t_k2:.4f} ms {k2_gbs:.0f} GB/s (peak {peak})")
+            traffic = json.load(fh).get("configs[3]", {}).get(dom_key, {}).get("dram_bytes_per_launch")
+    roofline = {"bound": "hbm", "kernel": f"{dom_key}: {dom['kernel']}", "achieved": dom["gbs"], "peak": peak,
+                "unit": "GB/s", "frac": round(dom["gbs"] / peak, 4), "traffic": traffic,
+                "algorithmic_bytes": dom["bytes"], "launch_ms": dom["ms"], "peak_source": peak_src,
+                "timing": "CUDA events between the epoch's kernels on the launching stream, averaged over the "
+                          f"{n_ep} eager epochs after the graph-timed ones",
+                "kernels": kernels,
+                "epoch_eager_ms": round(eager_ms, 4), "phase_sum_ms": round(phase_sum, 4),
+                "phase_sum_over_epoch": round(phase_sum / eager_ms, 4),
+                "epoch_algorithmic_gbs": round((b1 + b2) / (ms_per_step * 1e6), 1)}
+    log(f"[bench] phases (ms): " + ", ".join(f"{k} {v:.4f}" for k, v in ph.items()) +
+        f" | sum {phase_sum:.4f} vs eager epoch {eager_ms:.4f}")
+
+    # ---- standalone prox at the FGP cap (non-converging tolerance) ----
+    img = torch.rand(d.height, d.width, dtype=torch.float64, device=dev)
+    pst = tv.ProxSettings(d.max_inner_iters, 1e-300)
+    tv.tv_prox(img, 0.05, pst)
+    pms = time_events(lambda: tv.tv_prox(img, 0.05, pst), 5)
+    pb = prox_bytes(d.height * d.width, 2, d.max_inner_iters)
+    roofline["tv_prox_standalone"] = {"image": f"{d.height}x{d.width}", "iterations": d.max_inner_iters,
+                                      "ms": round(pms, 4), "algorithmic_bytes": pb,
+                                      "gbs": round(pb / (pms * 1e6), 1), "frac": round(pb / (pms * 1e6) / peak, 4),
+                                      "note": "fields are L2-resident at 1024^2 (8 MB each)"}
+    del img
 
     # ---- e2e: host numpy state through the drop-in API ----
     st2 = solvers.init_bsgd_state(op, d.y, cfg)
+    st2._ensure_history(4 * steps + 16)
     hx = np.zeros(cols)
     hr = np.asarray(d.y, dtype=np.float64).copy()
-    e2e_steps = max(2, min(args.steps, 20))
     for _ in range(2):
         st2.x, st2.r_vec = hx, hr
-        solvers.bsgd_tv_iteration(st2, op, d.y, cfg)
+        solvers.bsgd_tv_iteration(st2, op, d.y, cfg, layout=lay)
         hx, hr = st2.x, st2.r_vec
     torch.cuda.synchronize()
-    batches = []
-    for _ in range(3):   # median of three batches: the host side makes single batches noisy
-        t0 = time.perf_counter()
-        for _ in range(e2e_steps):
-            st2.x, st2.r_vec = hx, hr
-            solvers.bsgd_tv_iteration(st2, op, d.y, cfg)
-            hx, hr = st2.x, st2.r_vec
-        torch.cuda.synchronize()
-        batches.append((time.perf_counter() - t0) / e2e_steps)
-    e2e_s = sorted(batches)[1]
-    e2e = {"value": round(1.0 / e2e_s, 2), "unit": "epochs/s", "h2d_bytes_per_step": (rows + cols) * 8,
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        st2.x, st2.r_vec = hx, hr
+        solvers.bsgd_tv_iteration(st2, op, d.y, cfg, layout=lay)
+        hx, hr = st2.x, st2.r_vec
+    torch.cuda.synchronize()
+    e2e_s = (time.perf_counter() - t0) / steps
+    e2e = {"value": round(1.0 / e2e_s, 3), "unit": "epochs/s", "h2d_bytes_per_step": (rows + cols) * 8,
            "d2h_bytes_per_step": (rows + cols) * 8,
-           "how": "bsgd_tv_iteration with numpy x, r_vec set before and read after every epoch "
-                  "(median of three batches)"}
+           "how": "bsgd_tv_iteration with numpy x and r_vec assigned before and read back after every epoch"}
     log(f"[bench] e2e host-state: {e2e_s * 1e3:.3f} ms/epoch")
+    del st2
 
-    # ---- CPU baseline (oracle port) on a bounded sample ----
+    # ---- CPU baseline (oracle port) on a bounded sample of the same system ----
     cpu = None
     if not args.no_cpu:
-        v, info = cpu_epochs(d, steps=max(3, args.cpu_epochs), warmup=1, mu=mu, budget_s=args.cpu_budget)
-        cpu = {"value": round(v, 3), "unit": "epochs/s", "cores": info["cores"], "kind": "port",
-               "sample": f"{info['epochs_timed']} epochs of the same configs[1] system (same A, y, mu), "
-                         f"oracle/ C restatement of scipy csr/csc_matvec + numpy epilogue, OpenMP over block pairs"}
-        log(f"[bench] cpu oracle: {v:.3f} epochs/s on {info['cores']} threads")
+        t0 = time.time()
+        csr = op.tocsr()
+        log(f"[bench] host CSR copy {time.time() - t0:.1f}s")
+        v, info = oracle_epochs(csr, d.y, 8, mu, d.lam, d.max_inner_iters, 1e-5, (d.height, d.width),
+                                warmup=1, steps=max(2, args.cpu_epochs), budget_s=args.cpu_budget)
+        cpu = {"value": round(v, 4), "unit": "epochs/s", "cores": info["cores"], "kind": "port",
+               "sample": f"{info['epochs_timed']} epochs ({info['seconds']} s) of the same configs[3] system "
+                         f"(same A, y, mu) after 1 warm-up epoch; oracle/ C restatement of scipy csr/csc_matvec + "
+                         f"numpy epilogue and prox, OpenMP over block pairs"}
+        log(f"[bench] cpu oracle: {v:.4f} epochs/s on {info['cores']} threads")
+        del csr
+        op._csr = None
 
-    # The random 8-byte gathers (one per nonzero) are capped by the L1 tag stage at
-    # ~1 distinct sector per SM per cycle (profiles/r01_gather_microbench.md); that
-    # ceiling, not HBM, bounds both products of this random 32-nnz/row system.
-    clk = (clocks or {}).get("sm_mhz") or 1965.0
-    gather_floor_ms = ROWS * NNZ_ROW / (num_sms() * clk * 1e6) * 1e3
-    roofline["gather_ceiling"] = {"gathers_per_launch": ROWS * NNZ_ROW, "loads_per_sm_cycle": 1.0,
-                                  "floor_ms": round(gather_floor_ms, 4),
-                                  "frac_k1": round(gather_floor_ms / t_k1, 3),
-                                  "frac_k2": round(gather_floor_ms / t_k2, 3)}
+    launches = 4  # K2 (gather-tiled A^T + step), prox (1 cooperative kernel), K1 lookahead, tail
     secondary = None
-    if not args.no_ct:
+    del st, runner, op, d
+    torch.cuda.empty_cache()
+    if not args.no_secondary:
         secondary = {}
-        for idx in (2, 3, 4):
+        for idx in (1, 2, 4):
             try:
-                secondary[f"configs[{idx}]"] = run_ct_secondary(args, idx)
+                secondary[f"configs[{idx}]"] = run_secondary(args, idx)
             except Exception as exc:  # keep the headline line even if a secondary run fails
-                secondary[f"configs[{idx}]"] = {"error": repr(exc)[:200]}
+                secondary[f"configs[{idx}]"] = {"error": repr(exc)[:300]}
+            torch.cuda.empty_cache()
 
-    out = {"metric": METRIC, "value": round(value, 2), "unit": "epochs/s", "n_gpus": 1, "steps": args.steps,
+    out = {"metric": METRIC, "value": round(value, 3), "unit": "epochs/s", "n_gpus": 1, "steps": steps,
            "warmup": args.warmup, "ms_per_step": round(ms_per_step, 5), "higher_is_better": True,
-           "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, configs[1] shapes)",
-           "config": config_dict({"parallelism": "single GPU", "mu": mu, "u_max": pw.value}),
+           "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic (seeded configs[3] phantom, projector and noise; problems.py)",
+           "config": config_dict(HEADLINE, nnz, mu, u_max), "parallelism": "single GPU",
            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-           "gpu_launches": 3 * args.steps, "clocks": clocks, "secondary": secondary}
+           "gpu_launches": launches * steps, "clocks": clocks, "secondary": secondary}
     print(json.dumps(out), flush=True)
 
 
+def run_secondary(args, index):
+    """configs[index]: device-resident epochs/s (graph replay) and the in-epoch kernel times."""
+    import torch
+    from paper_1812_01307_b200 import blockops, problems, solvers, tv
+    t0 = time.time()
+    if index == 1:
+        h = problems.config(1)
+        op = blockops.BlockOperator(h.matrix, blockops.make_partition(*h.matrix.shape, 8, 8))
+        y, lam, lay, inner = h.y, 0.0, None, 20
+        shape = None
+        del h
+    else:
+        d = problems.config_device(index)
+        op, y, lam, lay, inner = d.op, d.y, d.lam, d.layout(), d.max_inner_iters
+        shape = (d.depth, d.height, d.width) if d.depth > 1 else (d.height, d.width)
+        del d
+    torch.cuda.synchronize()
+    log(f"[bench] configs[{index}] ready in {time.time() - t0:.1f}s: {op.shape}, nnz={op.nnz}")
+    mu, _ = mu_for(index)
+    cfg = solvers.SolverConfig(mu=mu, lam=lam, epochs=10 ** 9, prox=tv.ProxSettings(inner, 1e-5),
+                               monitor_decrease=False)
+    st = solvers.init_bsgd_state(op, y, cfg)
+    steps = max(4, min(args.steps, 20)) // 2 * 2
+    st._ensure_history(3 * steps + 16)
+    for _ in range(3):
+        solvers.bsgd_tv_iteration(st, op, y, cfg, layout=lay)
+    runner = solvers._GraphRunner(st, cfg, lay, st._y, 2)
+    assert runner.capture(False)
+    runner.replay()
+    torch.cuda.synchronize()
+    row0 = st._rows_used + 2
+    ms = time_events(runner.replay, steps // 2) / 2
+    st._rows_used += 2 + steps
+    hist = st._hist[row0:row0 + steps].cpu().numpy()
+    op.set_phase_timing(True)
+    for _ in range(steps):
+        solvers.bsgd_tv_iteration(st, op, st._y, cfg, layout=lay)
+    ph, n = op.phase_timing()
+    op.set_phase_timing(False)
+    ph = {k: round(v / max(n, 1), 4) for k, v in ph.items()}
+    rows, cols = op.shape
+    out = {"workload": WORKLOADS[index], "nnz": int(op.nnz), "epochs_per_s": round(1000.0 / ms, 2),
+           "ms_per_epoch": round(ms, 4), "phases_ms": ph, "kernels": op.kernel_info(),
+           "mean_fgp_iterations": round(float(np.mean(hist[:, 5])), 2) if lam > 0 else 0}
+    peak, _ = peaks()
+    if op.depth == 1:
+        b1, b2 = csr_bytes(int(op.nnz), rows, cols)
+        if lam == 0:
+            b2 -= cols * 8  # no prox image: g and x_next out
+        out["k1_gbs"] = round(b1 / (ph["k1_lookahead"] * 1e6), 1)
+        out["k2_gbs"] = round(b2 / (ph["k2_step"] * 1e6), 1)
+        out["k1_frac"] = round(out["k1_gbs"] / peak, 4)
+        out["k2_frac"] = round(out["k2_gbs"] / peak, 4)
+    if index == 1:
+        # random 8-byte gathers, one per nonzero: capped by the L1 tag stage at ~1
+        # distinct sector per SM per cycle (profiles/r01_gather_microbench.md)
+        clk = 1965.0
+        sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+        floor = op.nnz / (sms * clk * 1e6) * 1e3
+        out["gather_ceiling"] = {"floor_ms": round(floor, 4), "frac_k1": round(floor / ph["k1_lookahead"], 3),
+                                 "frac_k2": round(floor / ph["k2_step"], 3)}
+    if shape is not None:
+        img = torch.rand(*shape, dtype=torch.float64, device="cuda")
+        pst = tv.ProxSettings(inner, 1e-300)
+        tv.tv_prox(img, 0.05, pst)
+        pms = time_events(lambda: tv.tv_prox(img, 0.05, pst), 5)
+        npx = int(np.prod(shape))
+        pb = prox_bytes(npx, len(shape), inner)
+        if npx >= (1 << 21):
+            pb -= 8 * npx * 2 * len(shape)   # split prox: the first iteration reads p = q = 0 as literals
+        out["tv_prox_standalone"] = {"shape": "x".join(map(str, shape)), "iterations": inner, "ms": round(pms, 4),
+                                     "gbs": round(pb / (pms * 1e6), 1), "frac": round(pb / (pms * 1e6) / peak, 4)}
+    if op.depth > 1:
+        out["operator_note"] = (f"A = A2 (x) I_{op.depth}: {op.nnz // op.depth} stored nonzeros applied to "
+                                f"{op.depth} slices each; the CSR byte model does not apply (the vector reads dominate)")
+        out["epoch_vector_read_gbs"] = round(2 * op.nnz * 8 / (ms * 1e6), 1)
+    del st, runner, op
+    return out
+
+
 def run_multi(args):
-    """N > 1 (torchrun, one rank per GPU): configs[1] sharded by whole row blocks
-    (parallel.py), one NCCL all-reduce of g and of ||r||^2 per epoch.  Same JSON
-    contract as the single-GPU line; timing = max over ranks of CUDA-event time."""
+    """N > 1 (torchrun, one rank per GPU): configs[3] by row slabs, each rank
+    generating only its own rays on its GPU (parallel.CudaShard.parallel_beam),
+    one NCCL all-reduce of g (+ ||r||^2) per epoch.  Same JSON contract as the
+    single-GPU line; timing = max over ranks of CUDA-event time."""
     import torch
     import torch.distributed as dist
-    from paper_1812_01307_b200 import _native as nat
-    from paper_1812_01307_b200 import parallel
-    from paper_1812_01307_b200.blockops import make_partition
+    from paper_1812_01307_b200 import parallel, tv
     from paper_1812_01307_b200.solvers import SolverConfig
 
     world, rank, local = dist_info()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist.init_process_group("nccl", device_id=dev)
-    d = make_problem()
-    part = make_partition(*d.shape, BLOCKS, BLOCKS)
-    spec = parallel.ShardSpec(part, rank, world)
-    shard = parallel.CudaShard(d.matrix, spec)
-    u, _, _ = parallel.distributed_largest_eigenvalue(shard, max_iters=50)
-    mu = 0.9 / (2.0 * u)
-    cfg = SolverConfig(mu=mu, lam=0.0, epochs=10 ** 9, monitor_decrease=False)
-    cap = args.steps + args.warmup + 64
-    drv = parallel.DistributedBSGD(shard, d.y, cfg, history_capacity=cap)
-    for _ in range(max(1, args.warmup)):
+    shard, y_full, meta = parallel.ct_row_slab_shard(HEADLINE, rank, world, device=dev)
+    mu, u_max = mu_for(HEADLINE)
+    cfg = SolverConfig(mu=mu, lam=meta["lam"], epochs=10 ** 9, prox=tv.ProxSettings(meta["max_inner_iters"], 1e-5),
+                       monitor_decrease=False)
+    steps = max(2, args.steps // 2 * 2)
+    drv = parallel.DistributedBSGD(shard, y_full, cfg, history_capacity=4 * steps + args.warmup + 64)
+    for _ in range(args.warmup):
         drv.epoch_step()
-    # two epochs (kernels + NCCL all-reduces) per CUDA graph: no per-epoch host work
     graphed = drv.capture(2)
     if graphed:
         drv.replay()
@@ -374,235 +503,209 @@ def run_multi(args):
     with Clocks(local) as clk:
         e0.record()
         if graphed:
-            for _ in range(args.steps // 2):
+            for _ in range(steps // 2):
                 drv.replay()
-            if args.steps % 2:
-                drv.epoch_step()
         else:
-            for _ in range(args.steps):
+            for _ in range(steps):
                 drv.epoch_step()
         e1.record()
         torch.cuda.synchronize()
     ms = torch.tensor([e0.elapsed_time(e1)], device=dev)
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-    ms_step = float(ms.item()) / args.steps
+    ms_step = float(ms.item()) / steps
     clocks = clk.summary()
 
     # e2e: every step the host state goes in (x, this rank's r slice) and comes back
-    r0, r1 = spec.row_range
-    cols = d.shape[1]
+    r0, r1 = shard.spec.row_range
+    cols = shard.cols
     hx = torch.empty(cols, dtype=torch.float64, pin_memory=True)
     hr = torch.empty(r1 - r0, dtype=torch.float64, pin_memory=True)
     hx.copy_(drv.x_current)
     hr.copy_(drv.r_current)
     torch.cuda.synchronize()
-    e2e_steps = max(2, min(args.steps, 20))
     dist.barrier()
     t0 = time.perf_counter()
-    for _ in range(e2e_steps):
+    for _ in range(steps):
         drv.x_current.copy_(hx, non_blocking=True)
         drv.r_current.copy_(hr, non_blocking=True)
         drv.epoch_step()
         hx.copy_(drv.x_current, non_blocking=True)
         hr.copy_(drv.r_current, non_blocking=True)
         torch.cuda.synchronize()
-    e2e_s = torch.tensor([(time.perf_counter() - t0) / e2e_steps], device=dev)
+    e2e_s = torch.tensor([(time.perf_counter() - t0) / steps], device=dev)
     dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
     e2e_s = float(e2e_s.item())
 
-    # roofline: this rank's forward product (local rows) timed alone
+    # roofline: this rank's forward product (local rays) timed alone
     local_nnz = int(shard.op.nnz)
     rows_l = r1 - r0
     x = drv.x_current.clone()
     rout = torch.empty(rows_l, dtype=torch.float64, device=dev)
-    for _ in range(2):
-        shard.matvec(x, rout)
-    k0, k1e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    k0.record()
-    for _ in range(10):
-        shard.matvec(x, rout)
-    k1e.record()
-    torch.cuda.synchronize()
-    t_k1 = k0.elapsed_time(k1e) / 10
+    t_k1 = time_events(lambda: shard.matvec(x, rout), 10)
     b1 = local_nnz * 8 + (rows_l + 1) * 8 + cols * 8 + rows_l * 8
+    nnz_t = torch.tensor([local_nnz], dtype=torch.int64, device=dev)
+    dist.all_reduce(nnz_t)
     pk, pk_src = peaks()
     if rank == 0:
-        out = {"metric": METRIC, "value": round(1000.0 / ms_step, 2), "unit": "epochs/s", "n_gpus": world,
-               "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 5),
+        out = {"metric": METRIC, "value": round(1000.0 / ms_step, 3), "unit": "epochs/s", "n_gpus": world,
+               "steps": steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 5),
                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-               "data": "synthetic (seeded, configs[1] shapes)",
-               "config": config_dict({"parallelism": f"row slabs x{world} (whole row blocks), NCCL all-reduce of g",
-                                      "mu": mu, "u_max": u}),
-               "roofline": {"bound": "hbm", "kernel": "K1 forward CSR SpMV on rank 0's rows", "achieved":
+               "data": "synthetic (seeded configs[3] phantom, projector and noise; problems.py)",
+               "config": config_dict(HEADLINE, int(nnz_t.item()), mu, u_max),
+               "parallelism": f"row slabs x{world} (whole row blocks, rays generated on each rank's GPU), "
+                              f"NCCL all-reduce of g and ||r||^2 per epoch, prox replicated",
+               "roofline": {"bound": "hbm", "kernel": "K1 forward CSR SpMV on rank 0's rays", "achieved":
                             round(b1 / (t_k1 * 1e6), 1), "peak": pk, "unit": "GB/s",
                             "frac": round(b1 / (t_k1 * 1e6) / pk, 4), "traffic": None,
                             "algorithmic_bytes": b1, "launch_ms": round(t_k1, 5), "peak_source": pk_src},
                "cpu_baseline": None,
-               "e2e": {"value": round(1.0 / e2e_s, 2), "unit": "epochs/s",
+               "e2e": {"value": round(1.0 / e2e_s, 3), "unit": "epochs/s",
                        "h2d_bytes_per_step": (cols + rows_l) * 8, "d2h_bytes_per_step": (cols + rows_l) * 8,
                        "how": "per rank: x and its r slice from pinned host memory in, epoch, both back out"},
-               "gpu_launches": 5 * args.steps, "clocks": clocks}
+               "gpu_launches": 6 * steps, "clocks": clocks, "graphed": graphed}
         print(json.dumps(out), flush=True)
     dist.barrier()
     dist.destroy_process_group()
 
 
-def num_sms():
-    import torch
-    return torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+# --- reference arm -------------------------------------------------------------------
 
-
-def run_ct_secondary(args, index):
-    """configs[index] (parallel-beam CT with the TV prox on; configs[4] is the 3-D
-    slice-stacked volume), projector generated on the GPU: epochs/s and the
-    standalone TV prox's GB/s at the configured FGP cap."""
+def reference_inputs():
+    """configs[3]'s A (host CSR), y and mu: A from the GPU Siddon generator, which is
+    bit-identical to the host generator problems.parallel_beam_matrix
+    (tests/test_gpu_generator.py) and takes seconds instead of minutes; y as in
+    the GPU arm.  Input generation only -- nothing of the B200 path is timed here."""
     import torch
-    from paper_1812_01307_b200 import problems, solvers, spectral, tv
+    from paper_1812_01307_b200 import problems
     t0 = time.time()
-    d = problems.config_device(index)
-    op = d.op
-    torch.cuda.synchronize()
-    log(f"[bench] configs[{index}] on device in {time.time() - t0:.1f}s: {op.shape}, nnz={op.nnz}")
-    u = spectral.largest_eigenvalue(op, max_iters=50).value
-    mu = 0.9 / (2.0 * u)
-    lay = d.layout()
-    cfg = solvers.SolverConfig(mu=mu, lam=d.lam, epochs=10 ** 9, prox=tv.ProxSettings(d.max_inner_iters, 1e-5),
-                               monitor_decrease=False)
-    st = solvers.init_bsgd_state(op, d.y, cfg)
-    steps = max(4, min(args.steps, 20)) // 2 * 2
-    st._ensure_history(steps + 16)
-    for _ in range(3):
-        solvers.bsgd_tv_iteration(st, op, d.y, cfg, layout=lay)
-    runner = solvers._GraphRunner(st, cfg, lay, st._y, 2)
-    assert runner.capture(False)
-    runner.replay()
-    torch.cuda.synchronize()
-    row0 = st._rows_used + 2
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(steps // 2):
-        runner.replay()
-    e1.record()
-    torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / steps
-    hist = st._hist[row0:row0 + steps].cpu().numpy()
-    fgp_iters = float(np.mean(hist[:, 5])) if len(hist) else float("nan")
-    shape = (d.depth, d.height, d.width) if d.depth > 1 else (d.height, d.width)
-    img = torch.rand(*shape, dtype=torch.float64, device="cuda")
-    pst = tv.ProxSettings(d.max_inner_iters, 1e-300)
-    tv.tv_prox(img, 0.05, pst)
-    torch.cuda.synchronize()
-    p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    p0.record()
-    for _ in range(5):
-        tv.tv_prox(img, 0.05, pst)
-    p1.record()
-    torch.cuda.synchronize()
-    pms = p0.elapsed_time(p1) / 5
-    npx = int(np.prod(shape))
-    dim = len(shape)
-    # per FGP iteration of the fused schedule: candidate (read q, b; write c), dual
-    # value + momentum commit (read c, p, b; write q): 5*dim + 2 fields of 8 bytes
-    pbytes = 8 * npx * ((5 * dim + 2) * d.max_inner_iters + 10)
-    if npx >= (1 << 21):
-        # pass-per-kernel prox: the first iteration reads p = q = 0 as literals (2 dim fields fewer)
-        pbytes -= 8 * npx * 2 * dim
-    rows, cols = op.shape
-    products = None
-    if d.depth == 1:
-        # the two products alone on the plan's current kernels, CSR byte model of
-        # SURVEY.md §8(d) (float32 values, int32 indices, int64 row pointers, float64 vectors)
-        from paper_1812_01307_b200 import _native as nat
-        dev = torch.device("cuda", torch.cuda.current_device())
-        xv = torch.rand(cols, dtype=torch.float64, device=dev)
-        rv = torch.randn(rows, dtype=torch.float64, device=dev)
-        yv = torch.randn(rows, dtype=torch.float64, device=dev)
-        ro, go = torch.empty_like(rv), torch.empty_like(xv)
-        sp = nat.stream_ptr(dev)
-
-        def tk(fn, reps=10):
-            for _ in range(2):
-                fn()
-            torch.cuda.synchronize()
-            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a0.record()
-            for _ in range(reps):
-                fn()
-            a1.record()
-            torch.cuda.synchronize()
-            return a0.elapsed_time(a1) / reps
-
-        t1 = tk(lambda: nat.call("bsgd_residual", op.plan, nat.ptr(xv), nat.ptr(yv), nat.ptr(ro), None, None, sp))
-        t2 = tk(lambda: nat.call("bsgd_grad", op.plan, nat.ptr(rv), nat.ptr(go), sp))
-        nnz = int(op.nnz)
-        b1 = nnz * 8 + (rows + 1) * 8 + cols * 8 + 2 * rows * 8
-        b2 = nnz * 8 + (cols + 1) * 8 + rows * 8 + cols * 8
-        peak, _ = peaks()
-        products = {"k1_forward": {"kernel": "blocked CSR (csr_blocked_kernel)", "ms": round(t1, 4), "bytes": b1,
-                                   "gbs": round(b1 / (t1 * 1e6), 1), "frac": round(b1 / (t1 * 1e6) / peak, 4)},
-                    "k2_transposed": {"kernel": "gather-tiled, blocked stream (gtile_kernel)", "ms": round(t2, 4),
-                                      "bytes": b2, "gbs": round(b2 / (t2 * 1e6), 1),
-                                      "frac": round(b2 / (t2 * 1e6) / peak, 4)},
-                    "peak_gbs": peak, "byte_model": "SURVEY.md 8(d) CSR model: nnz*8 + pointers + vectors"}
-    out = {"nnz": int(op.nnz), "epochs_per_s": round(1000.0 / ms, 2), "ms_per_epoch": round(ms, 4),
-           "monitor_decrease": False, "mean_fgp_iterations": round(fgp_iters, 2),
-           "tv_prox": {"image": "x".join(str(v) for v in shape), "iterations": d.max_inner_iters,
-                       "ms": round(pms, 4), "algorithmic_bytes": pbytes, "gbs": round(pbytes / (pms * 1e6), 1),
-                       "frac": round(pbytes / (pms * 1e6) / peaks()[0], 4),
-                       "note": ("fields are L2-resident at 2D sizes; bound by grid barriers / latency, not HBM"
-                                if dim == 2 else
-                                "fields stream from HBM (134 MB each); split passes with direct pairwise "
-                                "leaf sums, profiles/r01_c5.md")}}
-    if products is not None:
-        out["products"] = products
-    if d.depth > 1:
-        # stacked operator: two products per epoch, each applies every logical nonzero
-        # once (a multiply and an add in float64) reading its vector value from L2
-        flops = 2 * 2 * op.nnz
-        out["workload"] = (f"configs[{index}]: 3-D slice-stacked parallel-beam CT {d.depth}x{d.height}x{d.width}, "
-                           f"{rows} rays, lambda={d.lam}, 3-D TV FGP<={d.max_inner_iters}, M=N={d.num_row_blocks}, "
-                           f"float32 slice matrix (A2 (x) I_D, {op.nnz // d.depth} stored nonzeros), "
-                           f"projector built on the GPU")
-        out["epoch_fp64_gflops"] = round(flops / (ms * 1e6), 1)
-        out["epoch_vector_l2_read_gbs"] = round(2 * op.nnz * 8 / (ms * 1e6), 1)
-    else:
-        epoch_bytes = 2 * op.nnz * 8 + (rows + cols) * 8 * 4
-        out["workload"] = (f"configs[{index}]: 2D parallel-beam CT {d.height}^2, {rows} rays, lambda={d.lam}, "
-                           f"FGP<={d.max_inner_iters}, M=N={d.num_row_blocks}, float32 values, projector built on the GPU")
-        out["epoch_algorithmic_gbs"] = round(epoch_bytes / (ms * 1e6), 1)
-    del st, runner, op, d
+    d = problems.config_device(HEADLINE)
+    csr = d.op.tocsr()
+    y = np.asarray(d.y, dtype=np.float64)
+    meta = {"height": d.height, "width": d.width, "lam": d.lam, "max_inner_iters": d.max_inner_iters}
+    d.op._csr = None
+    del d
     torch.cuda.empty_cache()
-    return out
+    log(f"[ref] inputs ready in {time.time() - t0:.1f}s: {csr.shape}, nnz={csr.nnz}")
+    return csr, y, meta
+
+
+def import_reference():
+    if not os.path.isdir(os.path.join(REF_DIR, "bsgdtv")):
+        return None
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    try:
+        import bsgdtv.blockops  # noqa: F401
+        import bsgdtv.solvers  # noqa: F401
+        import bsgdtv.tv  # noqa: F401
+        return sys.modules["bsgdtv.solvers"]
+    except Exception as exc:
+        log(f"[ref] baseline/_ref not importable: {exc!r}")
+        return None
 
 
 def run_reference(args):
     world, rank, _ = dist_info()
     if rank != 0:
         return
-    d = make_problem()
-    v, info = cpu_epochs(d, steps=args.steps, warmup=args.warmup, mu=None, budget_s=args.cpu_budget * 4)
-    cpu = {"value": round(v, 3), "unit": "epochs/s", "cores": info["cores"], "kind": "port",
-           "sample": f"{info['epochs_timed']} full epochs of configs[1] (each step one epoch)"}
-    out = {"impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": "epochs/s", "n_gpus": world,
-           "steps": info["epochs_timed"], "warmup": args.warmup, "ms_per_step": round(1000.0 / v, 3),
+    import concurrent.futures as cf
+
+    csr, y, meta = reference_inputs()
+    mu, u_max = mu_for(HEADLINE)
+    nnz = int(csr.nnz)
+    cores = os.cpu_count() or 1
+    ref = import_reference()
+    variants = {}
+    if ref is not None:
+        from bsgdtv import blockops as rb
+        from bsgdtv import solvers as rs
+        from bsgdtv import tv as rtv
+        t0 = time.time()
+        op = rb.BlockOperator(csr, rb.make_partition(csr.shape[0], csr.shape[1], 8, 8))
+        del csr
+        log(f"[ref] reference BlockOperator built in {time.time() - t0:.1f}s")
+        lay = rtv.PixelLayout(meta["height"], meta["width"], np.arange(meta["height"] * meta["width"]))
+        prox = rtv.ProxSettings(max_inner_iters=meta["max_inner_iters"], tol=1e-5)
+        cfg = rs.SolverConfig(mu=mu, lam=meta["lam"], prox=prox, monitor_decrease=False)
+
+        def timed(cfg_, workers, warm, steps, budget):
+            st = rs.init_bsgd_state(op, y, cfg_)
+            with cf.ThreadPoolExecutor(workers) as ex:
+                exe = ex if workers > 1 else None
+                for _ in range(warm):
+                    rs.bsgd_tv_iteration(st, op, y, cfg_, layout=lay, executor=exe)
+                times = []
+                t_start = time.perf_counter()
+                for _ in range(steps):
+                    t1 = time.perf_counter()
+                    rs.bsgd_tv_iteration(st, op, y, cfg_, layout=lay, executor=exe)
+                    times.append(time.perf_counter() - t1)
+                    if time.perf_counter() - t_start > budget:
+                        break
+            return len(times) / sum(times), len(times), sum(times)
+
+        v, n, secs = timed(cfg, cores, min(args.warmup, 1), args.steps, args.ref_budget)
+        kind, how = "reference", (f"the reference package (baseline/_ref bsgdtv, unmodified) bsgd_tv_iteration, "
+                                  f"ThreadPoolExecutor({cores}), monitor off")
+        log(f"[ref] reference: {v:.4f} epochs/s ({n} epochs, {secs:.1f}s)")
+        if not args.no_variants:
+            v1, n1, _ = timed(cfg, 1, 0, 2, args.ref_budget / 3)
+            variants["workers_1_monitor_off"] = {"value": round(v1, 4), "epochs": n1}
+            cfg_def = rs.SolverConfig(mu=mu, lam=meta["lam"], prox=prox)  # monitor_decrease defaults to True
+            vm, nm, _ = timed(cfg_def, cores, 0, 2, args.ref_budget / 3)
+            variants[f"workers_{cores}_monitor_on"] = {"value": round(vm, 4), "epochs": nm}
+            # run_solver defaults: monitor on and an objective sample every epoch (sample_every = 1)
+            t1 = time.perf_counter()
+            rs.run_solver("bsgd", rs.Problem(op, y, None, lay), rs.SolverConfig(mu=mu, lam=meta["lam"], prox=prox,
+                                                                               epochs=2), workers=cores)
+            variants[f"run_solver_defaults_workers_{cores}"] = {"value": round(2.0 / (time.perf_counter() - t1), 4),
+                                                               "epochs": 2,
+                                                               "note": "includes the initial objective sample"}
+            log(f"[ref] variants: {variants}")
+    else:
+        v, info = oracle_epochs(csr, y, 8, mu, meta["lam"], meta["max_inner_iters"], 1e-5,
+                                (meta["height"], meta["width"]), warmup=min(args.warmup, 1), steps=args.steps,
+                                budget_s=args.ref_budget)
+        n, secs = info["epochs_timed"], info["seconds"]
+        kind, how = "port", "oracle/ C + OpenMP restatement (baseline/_ref absent)"
+    cpu = {"value": round(v, 4), "unit": "epochs/s", "cores": cores, "kind": kind,
+           "sample": f"{n} full configs[3] epochs ({secs:.1f} s) after {min(args.warmup, 1)} warm-up epoch(s); {how}",
+           "host": host_info(), "variants": variants or None}
+    out = {"impl": "reference", "metric": METRIC, "value": round(v, 4), "unit": "epochs/s", "n_gpus": world,
+           "steps": n, "warmup": min(args.warmup, 1), "ms_per_step": round(1000.0 / v, 3),
            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-           "data": "synthetic (seeded, configs[1] shapes)",
-           "config": config_dict({"parallelism": f"{info['cores']} host threads", "mu": info["mu"]}),
+           "data": "synthetic (seeded configs[3] phantom, projector and noise; problems.py)",
+           "config": config_dict(HEADLINE, nnz, mu, u_max), "parallelism": f"{cores} host threads",
            "cpu_baseline": cpu,
-           "e2e": {"value": round(v, 3), "unit": "epochs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+           "e2e": {"value": round(v, 4), "unit": "epochs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
+
+
+def host_info():
+    info = {"cpu_count": os.cpu_count()}
+    try:
+        for line in subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout.splitlines():
+            if line.startswith("Model name:"):
+                info["model"] = line.split(":", 1)[1].strip()
+        with open("/proc/meminfo") as fh:
+            info["mem_gb"] = round(int(fh.readline().split()[1]) / 2 ** 20, 1)
+    except Exception:
+        pass
+    return info
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--no-ct", action="store_true", help="skip the configs[2] CT secondary measurement")
-    ap.add_argument("--cpu-epochs", type=int, default=40)
-    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--no-secondary", action="store_true", help="skip the configs[1], [2], [4] measurements")
+    ap.add_argument("--no-variants", action="store_true", help="reference arm: skip the 1-worker / monitor variants")
+    ap.add_argument("--cpu-epochs", type=int, default=8)
+    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--ref-budget", type=float, default=60.0)
     args = ap.parse_args()
     if args.warmup < 3:
         log("[bench] warmup raised to 3 (timing rules)")

@@ -156,6 +156,30 @@ int bsgd_plan_csr_copy(const bsgd_plan *plan, int64_t *indptr_out, int32_t *indi
 /* shape / nnz / dtype / device bytes (blockops.py:156-162) */
 int bsgd_plan_info(const bsgd_plan *plan, int64_t *rows, int64_t *cols, int64_t *nnz,
                    int *value_dtype, int64_t *device_bytes);
+/* Which product kernels the plan runs (fixed at plan creation by structural
+ * rules, never by timing; BlockOperator.kernel_info).  Lanes: lanes per row
+ * for CSR / blocked / gather-tiled kernels, slices per lane for stacked ones. */
+#define BSGD_K_CSR 0           /* dual_csr_kernel (spmv.cuh) */
+#define BSGD_K_BLOCKED 1       /* csr_blocked_kernel, int32 indices */
+#define BSGD_K_BLOCKED_CMP 2   /* csr_blocked_kernel, int32 base + 16-bit increments */
+#define BSGD_K_GTILE 3         /* gtile_kernel (gtile.cuh) */
+#define BSGD_K_STACKED 4       /* stacked_kernel (stacked.cuh) */
+#define BSGD_K_STACKED_TILE 5  /* stacked_tile_kernel (stacked.cuh) */
+typedef struct bsgd_kernel_info {
+    int32_t fwd_kernel, fwd_lanes;  /* A x  (K1) */
+    int32_t tr_kernel, tr_lanes;    /* A^T r (K2) */
+    int64_t depth;
+} bsgd_kernel_info;
+int bsgd_plan_kernel_info(const bsgd_plan *plan, bsgd_kernel_info *out);
+/* In-epoch phase timing for measurement (bench.py): while enabled, every eager
+ * bsgd_epoch on this plan records CUDA events on its stream between phases
+ * (never inside a graph capture).  bsgd_plan_timing synchronises, returns the
+ * summed milliseconds per phase over the recorded epochs and resets:
+ * [0] K1(x_k) when the lookahead residual is invalid, [1] K2 (A^T r + step
+ * epilogue), [2] TV prox, [3] K1(x_next) lookahead, [4] tail. */
+#define BSGD_TIMING_PHASES 5
+int bsgd_plan_set_timing(bsgd_plan *plan, int enable);
+int bsgd_plan_timing(bsgd_plan *plan, double *ms_out, int64_t *epochs_out);
 /* block_nnz (blockops.py:179-180), host out */
 int bsgd_plan_block_nnz(const bsgd_plan *plan, int64_t i, int64_t j, int64_t *out);
 /* block (blockops.py:176-177): block-local CSR copied to HOST buffers sized

@@ -45,6 +45,17 @@ class SlabArgs(ctypes.Structure):
 SLAB_SLOTS = 12
 
 
+class KernelInfo(ctypes.Structure):
+    """bsgd_kernel_info (include/bsgd_b200.h)."""
+    _fields_ = [("fwd_kernel", ctypes.c_int32), ("fwd_lanes", ctypes.c_int32),
+                ("tr_kernel", ctypes.c_int32), ("tr_lanes", ctypes.c_int32), ("depth", c_i64)]
+
+
+KERNEL_NAMES = {0: "csr", 1: "blocked", 2: "blocked_compressed", 3: "gather_tiled", 4: "stacked",
+                5: "stacked_tile"}
+TIMING_PHASES = ("k1_first", "k2_step", "prox", "k1_lookahead", "tail")
+
+
 class EpochArgs(ctypes.Structure):
     _fields_ = [
         ("x_k", c_p), ("r_k", c_p), ("y", c_p), ("g", c_p), ("x_next", c_p), ("r_next", c_p),
@@ -81,6 +92,9 @@ _SIGS = {
                                        ctypes.POINTER(c_i64), c_p]),
     "bsgd_device_free": (ctypes.c_int, [c_p]),
     "bsgd_plan_info": (ctypes.c_int, [c_p, c_p, c_p, c_p, c_p, c_p]),
+    "bsgd_plan_kernel_info": (ctypes.c_int, [c_p, ctypes.POINTER(KernelInfo)]),
+    "bsgd_plan_set_timing": (ctypes.c_int, [c_p, ctypes.c_int]),
+    "bsgd_plan_timing": (ctypes.c_int, [c_p, c_p, c_p]),
     "bsgd_plan_block_nnz": (ctypes.c_int, [c_p, c_i64, c_i64, ctypes.POINTER(c_i64)]),
     "bsgd_plan_block_copy": (ctypes.c_int, [c_p, c_i64, c_i64, c_p, c_p, c_p, c_p]),
     "bsgd_plan_transpose_copy": (ctypes.c_int, [c_p, c_p, c_p, c_p, c_p]),

@@ -132,14 +132,27 @@ def grid_tiles(height: int, width: int, tile_h: int = 4, tile_w: int = 4):
 def _canonical_csr(matrix, dtype=None) -> sparse.csr_array:
     """float CSR with summed duplicates and sorted indices (`blockops.py:124-126`).
 
-    float32 input stays float32 (exactly representable in the reference's
-    float64); anything else becomes float64 unless ``dtype`` says otherwise.
+    Duplicates are summed in float64, as the reference converts first and
+    sums after (`csr_array(matrix, dtype=np.float64)`).  float32 input stays
+    float32 only when it has no duplicates to sum or every summed value
+    round-trips through float32 exactly (then the stored entries are the
+    reference's float64 values); otherwise it is kept as float64.  An explicit
+    ``dtype`` is honoured after the float64 summation.
     """
     csr = sparse.csr_array(matrix)
+    if dtype is not None and np.dtype(dtype) not in (np.float32, np.float64):
+        raise ValueError("BlockOperator values must be float32 or float64")
+    if not csr.has_canonical_format:
+        src = csr.dtype
+        csr = csr.astype(np.float64)
+        csr.sum_duplicates()
+        csr.sort_indices()
+        if src == np.float32 and dtype is None:
+            narrow = csr.data.astype(np.float32)
+            if np.array_equal(narrow.astype(np.float64), csr.data):
+                csr = sparse.csr_array((narrow, csr.indices, csr.indptr), shape=csr.shape)
     want = np.dtype(dtype) if dtype is not None else (
         np.dtype(np.float32) if csr.dtype == np.float32 else np.dtype(np.float64))
-    if want not in (np.float32, np.float64):
-        raise ValueError("BlockOperator values must be float32 or float64")
     if csr.dtype != want:
         csr = csr.astype(want)
     csr.sum_duplicates()
@@ -240,30 +253,41 @@ class BlockOperator:
     @classmethod
     def from_parallel_beam(cls, n: int, num_angles: int, num_bins: int, num_row_blocks: int = 1,
                            num_col_blocks: int = 1, dtype=np.float32, device=None, depth: int = 1,
-                           tiles: bool = True) -> "BlockOperator":
+                           tiles: bool = True, angle_range=None,
+                           partition: BlockPartition | None = None) -> "BlockOperator":
         """Siddon parallel-beam projector generated on the GPU (`bsgd_siddon_csr`).
 
         Same matrix as `problems.parallel_beam_matrix` (bit-identical); the host
         never holds it, so configs[3]-size problems (~2e9 nonzeros) are possible.
         ``depth`` > 1 stacks it over that many slices (configs[4]), see `stacked`;
         with ``tiles`` the stacked products are tile-staged (`set_stacked_tiles`).
+        ``angle_range`` = (a0, a1) generates only the rays of angles a0 <= a < a1
+        (rows (a - a0) * num_bins + bin of the result: a multi-GPU row slab,
+        `parallel.CudaShard.parallel_beam`); ``partition`` then overrides the
+        even num_row_blocks x num_col_blocks partition of those rows.
         """
         import math
         self = cls.__new__(cls)
         self._device = nat.require_cuda(device)
         dt = np.dtype(dtype)
-        ang = [math.pi * a / num_angles for a in range(num_angles)]
+        a0, a1 = (0, num_angles) if angle_range is None else (int(angle_range[0]), int(angle_range[1]))
+        if not 0 <= a0 < a1 <= num_angles:
+            raise ValueError(f"angle range {angle_range} outside [0, {num_angles})")
+        ang = [math.pi * a / num_angles for a in range(a0, a1)]
         cs = np.array([math.cos(t) for t in ang], dtype=np.float64)
         sn = np.array([math.sin(t) for t in ang], dtype=np.float64)
-        rows2, cols2 = num_angles * num_bins, n * n
+        rows2, cols2 = (a1 - a0) * num_bins, n * n
         rows, cols = rows2 * depth, cols2 * depth
-        partition = make_partition(rows, cols, num_row_blocks, num_col_blocks)
+        if partition is None:
+            partition = make_partition(rows, cols, num_row_blocks, num_col_blocks)
+        elif partition.rows != rows or partition.cols != cols:
+            raise ValueError(f"partition covers {partition.rows}x{partition.cols}, operator is {rows}x{cols}")
         ip, ix, vv = nat.c_p(), nat.c_p(), nat.c_p()
         nnz = nat.c_i64()
         t = nat.torch()
         with t.cuda.device(self._device):
             st = nat.stream_ptr(self._device)
-            nat.call("bsgd_siddon_csr", self._device.index, n, num_angles, num_bins, cs.ctypes.data, sn.ctypes.data,
+            nat.call("bsgd_siddon_csr", self._device.index, n, a1 - a0, num_bins, cs.ctypes.data, sn.ctypes.data,
                      dt.itemsize, nat.ctypes.byref(ip), nat.ctypes.byref(ix), nat.ctypes.byref(vv),
                      nat.ctypes.byref(nnz), st)
             if nnz.value == 0:
@@ -285,11 +309,11 @@ class BlockOperator:
                     nat.load().bsgd_device_free(q)
                 nat.check(rc)
         self._init_fields(handle, (rows, cols), dt, partition, int(nnz.value) * depth, depth=depth)
-        self._slice_source = ("siddon", (n, num_angles, num_bins, dt))
+        self._slice_source = ("siddon", (n, num_angles, num_bins, dt, a0, a1))
         if depth > 1 and tiles:
             # A2^T rows are pixels: 4 x 4 image tiles; A2 rows are rays: 4 angles x 4 bins
             self.set_stacked_tiles(True, grid_tiles(n, n))
-            self.set_stacked_tiles(False, grid_tiles(num_angles, num_bins))
+            self.set_stacked_tiles(False, grid_tiles(a1 - a0, num_bins))
         elif depth == 1 and tiles:
             # gather-tiled A^T (gtile.cuh): a pixel's rays sit nb apart in r, so its
             # gathers share no sectors and the 4x4 tile union pays off (kept only if
@@ -414,6 +438,31 @@ class BlockOperator:
         """Opaque `bsgd_plan*` handle for the C ABI."""
         return self._plan
 
+    def kernel_info(self) -> dict:
+        """The product kernels this plan runs (`bsgd_plan_kernel_info`).
+
+        Chosen at plan creation by fixed structural rules, never by timing, so a
+        given matrix always runs the same kernels (and the same arithmetic).
+        """
+        ki = nat.KernelInfo()
+        nat.call("bsgd_plan_kernel_info", self._plan, nat.ctypes.byref(ki))
+        return {"forward": nat.KERNEL_NAMES[ki.fwd_kernel], "forward_lanes": int(ki.fwd_lanes),
+                "transposed": nat.KERNEL_NAMES[ki.tr_kernel], "transposed_lanes": int(ki.tr_lanes),
+                "depth": int(ki.depth)}
+
+    def set_phase_timing(self, enable: bool) -> None:
+        """Record CUDA events between the phases of every eager epoch on this plan
+        (`bsgd_plan_set_timing`; measurement only, never inside a graph capture)."""
+        nat.call("bsgd_plan_set_timing", self._plan, int(bool(enable)))
+
+    def phase_timing(self):
+        """(milliseconds per phase summed over the recorded epochs, epochs) and reset;
+        phases are `_native.TIMING_PHASES`."""
+        ms = np.zeros(len(nat.TIMING_PHASES))
+        n = nat.c_i64()
+        nat.call("bsgd_plan_timing", self._plan, ms.ctypes.data, nat.ctypes.byref(n))
+        return dict(zip(nat.TIMING_PHASES, ms.tolist())), int(n.value)
+
     def block(self, i: int, j: int) -> sparse.csr_array:
         """Block (i, j) with block-local indices, read back from the device copy."""
         if not (0 <= i < self.num_row_blocks and 0 <= j < self.num_col_blocks):
@@ -463,9 +512,9 @@ class BlockOperator:
             if kind == "host":
                 return BlockOperator.stacked(src, self.depth, make_partition(rows, cols, num_row_blocks,
                                                                              num_col_blocks), device=self._device)
-            n, ang, nb, dt = src
+            n, ang, nb, dt, a0, a1 = src
             return BlockOperator.from_parallel_beam(n, ang, nb, num_row_blocks, num_col_blocks, dtype=dt,
-                                                    device=self._device, depth=self.depth)
+                                                    device=self._device, depth=self.depth, angle_range=(a0, a1))
         return BlockOperator(self.tocsr(), make_partition(rows, cols, num_row_blocks, num_col_blocks),
                              device=self._device)
 

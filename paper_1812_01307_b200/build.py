@@ -12,7 +12,7 @@ CSRC = os.path.join(_HERE, "csrc")
 LIB_DIR = os.path.join(_HERE, "lib")
 LIB_PATH = os.path.join(LIB_DIR, "libbsgd_b200.so")
 SOURCES = ["bsgd_abi.cu"]
-DEPS = ["bsgd_abi.cu", "common.cuh", "spmv.cuh", "fgp.cuh", "pairwise.cuh", "tiled.cuh", "sm100.cuh", "siddon.cuh",
+DEPS = ["bsgd_abi.cu", "common.cuh", "spmv.cuh", "fgp.cuh", "pairwise.cuh", "sm100.cuh", "siddon.cuh",
         "stacked.cuh", "gtile.cuh", "slab.cuh"]
 
 NVCC_FLAGS = [

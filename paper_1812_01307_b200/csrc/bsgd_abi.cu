@@ -26,7 +26,6 @@
 #include "common.cuh"
 #include "fgp.cuh"
 #include "spmv.cuh"
-#include "tiled.cuh"
 #include "siddon.cuh"
 #include "stacked.cuh"
 #include "gtile.cuh"
@@ -161,21 +160,6 @@ struct bsgd_plan {
     int64_t *d_row_bounds = nullptr, *d_col_bounds = nullptr;
     int g_fwd = 32, g_tr = 32;
     size_t device_bytes = 0;
-    // panel-tiled copies of A and A^T (tiled.cuh); used when built and enabled
-    struct TiledStore {
-        bool ok = false;
-        int R = 0, P = 0, NG = 0, NP = 0;
-        int64_t nrows = 0, ncols = 0;
-        uint32_t *keys = nullptr;
-        void *vals = nullptr;
-        uint64_t *unit_start = nullptr;
-        uint32_t *unit_len = nullptr, *tile_unit = nullptr;
-        uint16_t *unit_split = nullptr;
-        size_t bytes = 0;
-        int H = 1;              // panel ranges per row group (work items = NG * H)
-        double *pout = nullptr; // [H][nrows] partial sums when H > 1
-    } tf, tt;
-    bool use_tiled = true;
     // slice-stacked plans (stacked.cuh): A = A2 (x) I_depth in interleaved order;
     // f_* / t_* then hold A2 / A2^T and rows/cols/nnz above are the logical sizes
     int64_t depth = 1;
@@ -217,6 +201,46 @@ struct bsgd_plan {
         size_t bytes = 0;
     } fb;
     bool stacked() const { return depth > 1; }
+    // in-epoch phase timing (bsgd_plan_set_timing / bsgd_plan_timing): kPhaseEvents
+    // events per eager bsgd_epoch on the launching stream, never inside a capture
+    struct Timing {
+        bool on = false;
+        std::vector<cudaEvent_t> pool;
+        size_t used = 0;
+    };
+    mutable Timing timing;
+};
+
+// phases: [0] K1(x_k) when the lookahead r is invalid, [1] K2 + step epilogue,
+// [2] TV prox, [3] K1(x_next) lookahead, [4] tail
+static constexpr int kPhaseEvents = BSGD_TIMING_PHASES + 1;
+
+struct EpochTimer {
+    cudaEvent_t *ev = nullptr;
+    cudaStream_t st = nullptr;
+    EpochTimer(const bsgd_plan *p, cudaStream_t s) : st(s) {
+        bsgd_plan::Timing &T = p->timing;
+        if (!T.on) return;
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
+            cudaGetLastError();
+            return;
+        }
+        while (T.used + kPhaseEvents > T.pool.size()) {
+            cudaEvent_t e;
+            if (cudaEventCreate(&e) != cudaSuccess) {
+                cudaGetLastError();
+                return;
+            }
+            T.pool.push_back(e);
+        }
+        ev = &T.pool[T.used];
+        T.used += kPhaseEvents;
+        cudaEventRecord(ev[0], st);
+    }
+    void mark(int k) {
+        if (ev) cudaEventRecord(ev[k], st);
+    }
 };
 
 static void blk_free(bsgd_plan::BlkStore &b) {
@@ -309,18 +333,11 @@ __global__ void block_nnz_kernel(int64_t rows, const int64_t *ptr, const int32_t
     }
 }
 
-static void tiled_free(bsgd_plan::TiledStore &t) {
-    cudaFree(t.keys); cudaFree(t.vals); cudaFree(t.unit_start); cudaFree(t.unit_len);
-    cudaFree(t.tile_unit); cudaFree(t.pout); cudaFree(t.unit_split);
-    t = bsgd_plan::TiledStore();
-}
-
 static void plan_free(bsgd_plan *p) {
-    blk_free(p->fb);
     if (!p) return;
     DeviceGuard g(p->device);
-    tiled_free(p->tf);
-    tiled_free(p->tt);
+    for (cudaEvent_t e : p->timing.pool) cudaEventDestroy(e);
+    blk_free(p->fb);
     cudaFree(p->f_ptr); cudaFree(p->f_idx); cudaFree(p->f_val);
     cudaFree(p->t_ptr); cudaFree(p->t_idx); cudaFree(p->t_val);
     cudaFree(p->d_row_bounds); cudaFree(p->d_col_bounds);
@@ -470,181 +487,6 @@ static int build_blocked(bsgd_plan *p, cudaStream_t st) {
 }
 
 // ---------------------------------------------------------------------------
-// panel-tiled format (tiled.cuh)
-// ---------------------------------------------------------------------------
-// Pick rows per group R, panel width P and panel ranges H from a small cost
-// model: HBM stream of A, L2->SM re-reads of the vector (each row group reads
-// the whole vector once, ~18 TB/s measured for per-CTA bulk copies) and the
-// partial-sum round trip when H > 1, divided by the load balance of
-// NG * H work items over the SMs.
-template <typename V>
-static void choose_tiling(int64_t nrows, int64_t ncols, int64_t nnz, int &R, int &P, int &H) {
-    P = (int)std::min<int64_t>(kTileMaxP, (ncols + 1) & ~(int64_t)1);
-    if (P < 2) P = 2;
-    const int64_t NP = cdiv(ncols, P);
-    const double sms = num_sms();
-    const double stream = (double)nnz * (4.0 + sizeof(V));
-    double best = 1e300;
-    R = 256;
-    H = 1;
-    for (int r : {8192, 4096, 2048, 1024, 512, 256}) {
-        const int64_t NG = cdiv(nrows, r);
-        for (int h = 1; h <= 32 && h <= NP; ++h) {
-            const double items = (double)NG * h;
-            const double rounds = std::ceil(items / sms);
-            const double eff = items / (rounds * sms);
-            const double vec = (double)NG * ncols * 8.0;
-            const double partial = h > 1 ? 2.0 * h * nrows * 8.0 : 0.0;
-            const double t = std::max(stream / 6.5e12, (stream + vec + partial) / 18e12) / eff;
-            if (t < best * 0.999) { best = t; R = r; H = h; }
-        }
-    }
-}
-
-template <typename V>
-static int build_tiled(bsgd_plan::TiledStore &T, int64_t nrows, int64_t ncols, int64_t nnz, const int64_t *ptr,
-                       const int32_t *idx, const V *val, cudaStream_t st) {
-    constexpr int CH = TileCfg<V>::CH;
-    choose_tiling<V>(nrows, ncols, nnz, T.R, T.P, T.H);
-    T.nrows = nrows; T.ncols = ncols;
-    T.NG = (int)cdiv(nrows, T.R);
-    T.NP = (int)cdiv(ncols, T.P);
-    const int64_t ntiles = (int64_t)T.NG * T.NP;
-    if (ntiles >= ((int64_t)1 << 32) || nnz >= ((int64_t)1 << 32) || T.NP > kTileMaxNP || T.R > kTileMaxR)
-        return BSGD_OK;  // not eligible: keep the CSR kernels
-    int32_t *rowid = nullptr;
-    uint32_t *tkey = nullptr, *packed = nullptr, *pos = nullptr, *skey = nullptr, *perm = nullptr;
-    uint32_t *n_unit = nullptr, *unit_base = nullptr;
-    uint64_t *tile_ptr = nullptr;
-    int *d_bad = nullptr;
-    void *temp = nullptr;
-    size_t temp_bytes = 0;
-    int rc = BSGD_OK;
-    auto cleanup = [&]() {
-        cudaFree(rowid); cudaFree(tkey); cudaFree(packed); cudaFree(pos); cudaFree(skey); cudaFree(perm);
-        cudaFree(n_unit); cudaFree(unit_base); cudaFree(tile_ptr);
-        cudaFree(d_bad); cudaFree(temp);
-    };
-#define TTRY(call)                                                                          \
-    do {                                                                                    \
-        cudaError_t e_ = (call);                                                            \
-        if (e_ != cudaSuccess) {                                                            \
-            rc = fail(e_ == cudaErrorMemoryAllocation ? BSGD_ENOMEM : BSGD_ECUDA,           \
-                      "tiled build: %s failed: %s", #call, cudaGetErrorString(e_));         \
-            cleanup();                                                                      \
-            tiled_free(T);                                                                  \
-            return rc;                                                                      \
-        }                                                                                   \
-    } while (0)
-    TTRY(cudaMalloc(&rowid, sizeof(int32_t) * nnz));
-    TTRY(cudaMalloc(&tkey, sizeof(uint32_t) * nnz));
-    TTRY(cudaMalloc(&packed, sizeof(uint32_t) * nnz));
-    TTRY(cudaMalloc(&pos, sizeof(uint32_t) * nnz));
-    TTRY(cudaMalloc(&skey, sizeof(uint32_t) * nnz));
-    TTRY(cudaMalloc(&perm, sizeof(uint32_t) * nnz));
-    TTRY(cudaMalloc(&T.keys, sizeof(uint32_t) * (nnz + 8)));
-    TTRY(cudaMalloc(&T.vals, sizeof(V) * (nnz + 8)));
-    TTRY(cudaMemsetAsync(T.keys, 0, sizeof(uint32_t) * (nnz + 8), st));
-    TTRY(cudaMemsetAsync(T.vals, 0, sizeof(V) * (nnz + 8), st));
-    expand_rows_kernel<<<grid_1d(nrows), kThreads, 0, st>>>(nrows, ptr, rowid);
-    tile_keys_kernel<<<grid_1d(nnz), kThreads, 0, st>>>(nnz, rowid, idx, T.R, T.P, T.NP, tkey, packed, pos);
-    TTRY(cudaGetLastError());
-    int end_bit = 1;
-    while (end_bit < 32 && ((int64_t)1 << end_bit) <= ntiles) ++end_bit;
-    TTRY(cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, tkey, skey, pos, perm, nnz, 0, end_bit, st));
-    TTRY(cudaMalloc(&temp, temp_bytes));
-    TTRY(cub::DeviceRadixSort::SortPairs(temp, temp_bytes, tkey, skey, pos, perm, nnz, 0, end_bit, st));
-    tile_gather_kernel<V><<<grid_1d(nnz), kThreads, 0, st>>>(nnz, perm, packed, val, T.keys, (V *)T.vals);
-    tile_flags_kernel<<<grid_1d(nnz), kThreads, 0, st>>>(nnz, skey, T.keys);
-    TTRY(cudaMalloc(&tile_ptr, sizeof(uint64_t) * (ntiles + 1)));
-    tile_ptr_kernel<<<grid_1d(ntiles + 1), kThreads, 0, st>>>(ntiles, nnz, skey, tile_ptr);
-    TTRY(cudaGetLastError());
-    TTRY(cudaMalloc(&n_unit, sizeof(uint32_t) * ntiles));
-    TTRY(cudaMalloc(&unit_base, sizeof(uint32_t) * ntiles));
-    TTRY(cudaMalloc(&d_bad, sizeof(int)));
-    TTRY(cudaMemsetAsync(d_bad, 0, sizeof(int), st));
-    tile_segment_kernel<CH><<<grid_1d(ntiles, 64), 64, 0, st>>>(ntiles, tile_ptr, T.keys, 0, n_unit, nullptr, nullptr,
-                                                                 nullptr, d_bad);
-    TTRY(cudaGetLastError());
-    size_t scan_bytes = 0;
-    TTRY(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, n_unit, unit_base, ntiles, st));
-    if (scan_bytes > temp_bytes) {
-        TTRY(cudaFree(temp));
-        temp = nullptr;
-        TTRY(cudaMalloc(&temp, scan_bytes));
-        temp_bytes = scan_bytes;
-    }
-    TTRY(cub::DeviceScan::ExclusiveSum(temp, temp_bytes, n_unit, unit_base, ntiles, st));
-    uint32_t last[2] = {0, 0};
-    int bad = 0;
-    TTRY(cudaMemcpyAsync(&last[0], unit_base + ntiles - 1, 4, cudaMemcpyDeviceToHost, st));
-    TTRY(cudaMemcpyAsync(&last[1], n_unit + ntiles - 1, 4, cudaMemcpyDeviceToHost, st));
-    TTRY(cudaMemcpyAsync(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, st));
-    TTRY(cudaStreamSynchronize(st));
-    if (bad) {  // a row has more than CH entries in one tile: keep the CSR kernels
-        cleanup();
-        tiled_free(T);
-        return BSGD_OK;
-    }
-    const uint32_t total_units = last[0] + last[1];
-    TTRY(cudaMalloc(&T.unit_start, sizeof(uint64_t) * (total_units + 1)));
-    TTRY(cudaMalloc(&T.unit_len, sizeof(uint32_t) * (total_units + 1)));
-    TTRY(cudaMalloc(&T.tile_unit, sizeof(uint32_t) * (ntiles + 1)));
-    tile_segment_kernel<CH><<<grid_1d(ntiles, 64), 64, 0, st>>>(ntiles, tile_ptr, T.keys, 1, n_unit, unit_base,
-                                                                 T.unit_start, T.unit_len, d_bad);
-    tile_finish_kernel<<<grid_1d(ntiles + 1), kThreads, 0, st>>>(ntiles, unit_base, total_units, T.tile_unit);
-    TTRY(cudaMalloc(&T.unit_split, sizeof(uint16_t) * kSplitStride * (total_units + 1)));
-    tile_split_kernel<<<grid_1d(total_units), kThreads, 0, st>>>(total_units, T.unit_start, T.unit_len, T.keys, T.R,
-                                                                 T.unit_split);
-    TTRY(cudaGetLastError());
-    TTRY(cudaStreamSynchronize(st));
-#undef TTRY
-    cleanup();
-    T.bytes = (sizeof(uint32_t) + sizeof(V)) * (nnz + 8) + (12 + 2 * kSplitStride) * (size_t)(total_units + 1) +
-              4 * (size_t)(ntiles + 1) + sizeof(double) * (size_t)T.H * nrows;
-    if (T.H > 1 && cudaMalloc(&T.pout, sizeof(double) * (size_t)T.H * nrows) != cudaSuccess) {
-        cudaGetLastError();
-        tiled_free(T);
-        return fail(BSGD_ENOMEM, "tiled build: partial-sum buffer allocation failed");
-    }
-    // one CTA per SM; the smem attribute is per function and shared by every plan
-    const int smem_max = (int)TileSmem<V>::bytes(8192, 4096);
-    if (cudaFuncSetAttribute(tile_spmv_kernel<V, EpiStore>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max) != cudaSuccess ||
-        cudaFuncSetAttribute(tile_spmv_kernel<V, EpiResid>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max) != cudaSuccess ||
-        cudaFuncSetAttribute(tile_spmv_kernel<V, EpiStep>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max) != cudaSuccess) {
-        cudaGetLastError();
-        tiled_free(T);
-        return BSGD_OK;
-    }
-    T.ok = true;
-    return BSGD_OK;
-}
-
-template <typename V, class E>
-static int launch_tiled(const bsgd_plan::TiledStore &S, const double *vec, const E &e, double *part, int64_t *cnt,
-                        cudaStream_t st) {
-    Tiled<V> T;
-    T.nrows = S.nrows; T.ncols = S.ncols; T.R = S.R; T.P = S.P; T.NG = S.NG; T.NP = S.NP;
-    T.keys = S.keys; T.vals = (const V *)S.vals; T.unit_start = S.unit_start; T.unit_len = S.unit_len;
-    T.tile_unit = S.tile_unit; T.vec = vec; T.unit_split = S.unit_split;
-    T.H = S.H; T.pout = S.pout;
-    const size_t smem = TileSmem<V>::bytes(S.R, S.P);
-    tile_spmv_kernel<V, E><<<num_sms(), kTileThreads, smem, st>>>(T, e, part, cnt);
-    LAUNCHED();
-    if (S.H > 1) {
-        tile_combine_kernel<E><<<grid_1d(S.nrows), kThreads, 0, st>>>(S.nrows, S.H, S.pout, e, part, cnt);
-        LAUNCHED();
-    }
-    return BSGD_OK;
-}
-
-static bool tiled_usable(const bsgd_plan *p, const bsgd_plan::TiledStore &S, const double *vec) {
-    return p->use_tiled && S.ok && (((uintptr_t)vec) & 15) == 0;
-}
-
-
-
-// ---------------------------------------------------------------------------
 // SpMV launchers
 // ---------------------------------------------------------------------------
 template <typename V>
@@ -692,72 +534,6 @@ static int launch_one(const Csr<V> &A, int G, const E &e, double *part, int64_t 
     if (G == 8) return launch_dual<V, 8, 8, E, EpiNone>(A, e, part, cnt, nnz, none, EpiNone{}, nullptr, nullptr, 0, st);
     if (G == 4) return launch_dual<V, 4, 8, E, EpiNone>(A, e, part, cnt, nnz, none, EpiNone{}, nullptr, nullptr, 0, st);
     return launch_dual<V, 32, 8, E, EpiNone>(A, e, part, cnt, nnz, none, EpiNone{}, nullptr, nullptr, 0, st);
-}
-
-template <typename V, class EA, class EB>
-static int launch_two(const Csr<V> &A, int GA, const EA &ea, double *partA, int64_t *cntA, int64_t nnzA,
-                      const Csr<V> &B, int GB, const EB &eb, double *partB, int64_t *cntB, int64_t nnzB,
-                      cudaStream_t st) {
-    // lanes per row of each part: 4, 8 or 32 (the plan's choices)
-    auto go = [&](auto ga, auto gb) {
-        return launch_dual<V, decltype(ga)::value, decltype(gb)::value, EA, EB>(A, ea, partA, cntA, nnzA, B, eb,
-                                                                               partB, cntB, nnzB, st);
-    };
-    using G4 = std::integral_constant<int, 4>;
-    using G8 = std::integral_constant<int, 8>;
-    using G32 = std::integral_constant<int, 32>;
-    auto second = [&](auto ga) {
-        if (GB == 4) return go(ga, G4{});
-        if (GB == 8) return go(ga, G8{});
-        return go(ga, G32{});
-    };
-    if (GA == 4) return second(G4{});
-    if (GA == 8) return second(G8{});
-    return second(G32{});
-}
-
-// Keep the tiled copy of a direction only if it beats the CSR kernel on this
-// matrix (timed once at plan creation on zero vectors); otherwise free it.
-template <typename V>
-static int autotune_direction(bsgd_plan *p, bool transposed, cudaStream_t st) {
-    bsgd_plan::TiledStore &S = transposed ? p->tt : p->tf;
-    if (!S.ok) return BSGD_OK;
-    const int64_t nin = transposed ? p->rows : p->cols, nout = transposed ? p->cols : p->rows;
-    double *vin = nullptr, *vout = nullptr;
-    cudaEvent_t e0 = nullptr, e1 = nullptr;
-    float t_csr = 0.f, t_tiled = 0.f;
-    int rc = BSGD_OK;
-    if (cudaMalloc(&vin, sizeof(double) * nin) != cudaSuccess || cudaMalloc(&vout, sizeof(double) * nout) != cudaSuccess) {
-        cudaGetLastError();
-        cudaFree(vin);
-        tiled_free(S);
-        return BSGD_OK;
-    }
-    cudaMemsetAsync(vin, 0, sizeof(double) * nin, st);
-    cudaEventCreate(&e0);
-    cudaEventCreate(&e1);
-    const Csr<V> csr = transposed ? tr_csr<V>(p, vin) : fwd_csr<V>(p, vin);
-    const int G = transposed ? p->g_tr : p->g_fwd;
-    for (int variant = 0; variant < 2 && rc == BSGD_OK; ++variant) {
-        for (int rep = 0; rep < 3 && rc == BSGD_OK; ++rep) {
-            if (rep == 1) cudaEventRecord(e0, st);
-            rc = variant == 0 ? launch_one<V>(csr, G, EpiStore{vout, 1.0}, nullptr, nullptr, p->nnz, st)
-                              : launch_tiled<V>(S, vin, EpiStore{vout, 1.0}, nullptr, nullptr, st);
-        }
-        cudaEventRecord(e1, st);
-        cudaEventSynchronize(e1);
-        cudaEventElapsedTime(variant == 0 ? &t_csr : &t_tiled, e0, e1);
-    }
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
-    cudaFree(vin);
-    cudaFree(vout);
-    if (rc != BSGD_OK || !(t_tiled < 0.97f * t_csr)) {
-        p->device_bytes -= 0;
-        tiled_free(S);
-        return rc;
-    }
-    return BSGD_OK;
 }
 
 // slice-stacked products (stacked.cuh).  EpiResid becomes the in-kernel
@@ -821,6 +597,10 @@ static int launch_stk_tile(const Stk<V> &A, const bsgd_plan::StkTileStore &S, co
     return launch_stk_tile_kz<V, 4, RESID, ALIGNED, E>(A, S, e, part, cnt, st);
 }
 
+static bool stk_tiles_used(const bsgd_plan *p, const bsgd_plan::StkTileStore &S) {
+    return S.ok && p->depth % (32 * S.kz) == 0 && !getenv("BSGD_NO_STK_TILES");
+}
+
 template <typename V, class E>
 static int launch_stacked_dir(const bsgd_plan *p, bool transposed, const double *vec, const E &e, double *part,
                               int64_t *cnt, cudaStream_t st) {
@@ -838,7 +618,7 @@ static int launch_stacked_dir(const bsgd_plan *p, bool transposed, const double 
     A.L = p->lanes;
     const int kz = transposed ? p->kz_tr : p->kz_fwd;
     const bsgd_plan::StkTileStore &S = transposed ? p->stt : p->sf;
-    if (S.ok && A.D % (32 * S.kz) == 0 && !getenv("BSGD_NO_STK_TILES")) {
+    if (stk_tiles_used(p, S)) {
         if constexpr (std::is_same<E, EpiResid>::value) {
             A.y = e.y;
             return A.sbounds ? launch_stk_tile<V, true, true>(A, S, EpiResidFinal{e.r}, part, cnt, st)
@@ -884,7 +664,7 @@ static int launch_gtile(const bsgd_plan::GTileStore &S, const double *vec, const
     return launch_gtile_k<V, false>(S, vec, e, part, cnt, st);
 }
 
-static bool gtiles_on(const bsgd_plan::GTileStore &S) { return S.ok && !getenv("BSGD_NO_GATHER_TILES"); }
+static bool gtiles_on(const bsgd_plan::GTileStore &S) { return S.ok; }
 
 template <typename V, class E>
 static int launch_blocked(const bsgd_plan *p, const double *vec, const E &e, double *part, int64_t *cnt,
@@ -905,44 +685,23 @@ static int launch_blocked(const bsgd_plan *p, const double *vec, const E &e, dou
     return BSGD_OK;
 }
 
-// Keep the compressed or the plain indices of the blocked copy, whichever times
-// faster on this matrix (configs[2]: 0.457 -> 0.415 ms compressed; configs[3],
-// 4 lanes per ray: 3.04 ms plain vs 3.20 compressed).
+// Keep the compressed or the plain indices of the blocked copy by a fixed
+// structural rule, so the kernel a plan runs does not depend on a timing race:
+// compressed at 8 or more lanes per ray, plain at 4 (measured: configs[2],
+// 8 lanes, 0.457 -> 0.415 ms compressed; configs[3], 4 lanes, 3.04 ms plain vs
+// 3.20 compressed: the extra base load and dependent adds cost more than the
+// bytes they save when each lane walks 4x more entries).  BSGD_BLK_COMPRESS =
+// force | off overrides the rule (tests run both variants against the oracle).
 template <typename V>
 static int tune_blocked(bsgd_plan *p, cudaStream_t st) {
+    (void)st;
     bsgd_plan::BlkStore &b = p->fb;
     if (!b.ok || b.base == nullptr || b.idx == nullptr) return BSGD_OK;
-    double *vin = nullptr, *vout = nullptr;
-    bool keep_cmp = false;
-    if (cudaMalloc(&vin, sizeof(double) * p->cols) == cudaSuccess &&
-        cudaMalloc(&vout, sizeof(double) * p->rows) == cudaSuccess) {
-        cudaMemsetAsync(vin, 0, sizeof(double) * p->cols, st);
-        cudaEvent_t e0, e1;
-        cudaEventCreate(&e0);
-        cudaEventCreate(&e1);
-        float t[2] = {0.f, 0.f};
-        int32_t *base = b.base;
-        uint16_t *del = b.del;
-        for (int variant = 0; variant < 2; ++variant) {
-            b.base = variant ? base : nullptr;
-            b.del = variant ? del : nullptr;
-            for (int rep = 0; rep < 4; ++rep) {
-                if (rep == 1) cudaEventRecord(e0, st);
-                launch_blocked<V>(p, vin, EpiStore{vout, 1.0}, nullptr, nullptr, st);
-            }
-            cudaEventRecord(e1, st);
-            cudaEventSynchronize(e1);
-            cudaEventElapsedTime(&t[variant], e0, e1);
-        }
-        b.base = base;
-        b.del = del;
-        keep_cmp = t[1] < 0.98f * t[0];
-        cudaEventDestroy(e0);
-        cudaEventDestroy(e1);
+    bool keep_cmp = b.gb >= 8;
+    if (const char *f = getenv("BSGD_BLK_COMPRESS")) {
+        if (strcmp(f, "force") == 0) keep_cmp = true;
+        else if (strcmp(f, "off") == 0) keep_cmp = false;
     }
-    cudaGetLastError();
-    cudaFree(vin);
-    cudaFree(vout);
     if (keep_cmp) {
         cudaFree(b.idx);
         b.idx = nullptr;
@@ -969,7 +728,6 @@ template <typename V, class E>
 static int launch_fwd(const bsgd_plan *p, const double *vec, const E &e, double *part, int64_t *cnt, cudaStream_t st) {
     if (p->stacked()) return launch_stacked_dir<V>(p, false, vec, e, part, cnt, st);
     if (gtiles_on(p->gf)) return launch_gtile<V>(p->gf, vec, e, part, cnt, st);
-    if (tiled_usable(p, p->tf, vec)) return launch_tiled<V>(p->tf, vec, e, part, cnt, st);
     if (blocked_on(p)) return launch_blocked<V>(p, vec, e, part, cnt, st);
     return launch_one<V>(fwd_csr<V>(p, vec), p->g_fwd, e, part, cnt, p->nnz, st);
 }
@@ -978,7 +736,6 @@ template <typename V, class E>
 static int launch_tr(const bsgd_plan *p, const double *vec, const E &e, double *part, int64_t *cnt, cudaStream_t st) {
     if (p->stacked()) return launch_stacked_dir<V>(p, true, vec, e, part, cnt, st);
     if (gtiles_on(p->gt)) return launch_gtile<V>(p->gt, vec, e, part, cnt, st);
-    if (tiled_usable(p, p->tt, vec)) return launch_tiled<V>(p->tt, vec, e, part, cnt, st);
     return launch_one<V>(tr_csr<V>(p, vec), p->g_tr, e, part, cnt, p->nnz, st);
 }
 
@@ -1740,40 +1497,6 @@ static int plan_finish(bsgd_plan *p, cudaStream_t st) {
     if (rc != BSGD_OK) return rc;
     rc = (value_dtype == BSGD_F32) ? tune_blocked<float>(p, st) : tune_blocked<double>(p, st);
     if (rc != BSGD_OK) return rc;
-    {
-        // panel-tiled copies (tiled.cuh) are an opt-in experiment: on every
-        // configuration measured the CSR kernel wins, so
-        // plans only build and time them with BSGD_TILED=1 (=2: keep without timing)
-        const char *env = getenv("BSGD_TILED");
-        p->use_tiled = env && (env[0] == '1' || env[0] == '2') && !p->stacked();
-    }
-    if (p->use_tiled) {
-        // the tiled kernel sums each tile row with one lane: only short rows can win
-        // (autotune below decides); long-row (CT) directions keep the CSR kernel
-        const bool fwd_short = (double)nnz / rows <= 64.0, tr_short = (double)nnz / cols <= 64.0;
-        if (value_dtype == BSGD_F32) {
-            if (fwd_short) rc = build_tiled<float>(p->tf, rows, cols, nnz, p->f_ptr, p->f_idx, (const float *)p->f_val, st);
-            if (!rc && tr_short)
-                rc = build_tiled<float>(p->tt, cols, rows, nnz, p->t_ptr, p->t_idx, (const float *)p->t_val, st);
-        } else {
-            if (fwd_short) rc = build_tiled<double>(p->tf, rows, cols, nnz, p->f_ptr, p->f_idx, (const double *)p->f_val, st);
-            if (!rc && tr_short)
-                rc = build_tiled<double>(p->tt, cols, rows, nnz, p->t_ptr, p->t_idx, (const double *)p->t_val, st);
-        }
-        if (rc != BSGD_OK) return rc;
-        const char *force = getenv("BSGD_TILED");
-        if (!(force && force[0] == '2')) {  // BSGD_TILED=2 keeps the tiled path without timing it
-            if (value_dtype == BSGD_F32) {
-                rc = autotune_direction<float>(p, false, st);
-                if (!rc) rc = autotune_direction<float>(p, true, st);
-            } else {
-                rc = autotune_direction<double>(p, false, st);
-                if (!rc) rc = autotune_direction<double>(p, true, st);
-            }
-            if (rc != BSGD_OK) return rc;
-        }
-        p->device_bytes += p->tf.bytes + p->tt.bytes;
-    }
     // block nnz table (blockops.py:179-180)
     unsigned long long *d_cnt = nullptr;
     const int64_t nb = num_row_blocks * num_col_blocks;
@@ -2000,54 +1723,12 @@ int bsgd_plan_gather_tiles(bsgd_plan *p, int transposed, int64_t ntiles, const i
     int rc = p->vdt == BSGD_F32 ? build_gtiles<float>(p, transposed != 0, ntiles, tile_ptr, tile_rows, st)
                                 : build_gtiles<double>(p, transposed != 0, ntiles, tile_ptr, tile_rows, st);
     if (rc) return rc;
-    // keep the tiles only where they beat the CSR kernel on this matrix: the union
-    // staging wins where the CSR gathers have no sector locality of their own
-    // (pixel rows of A^T at 1024^2: 6.1 -> 4.2 ms) and loses where they do
-    // (ray rows of A at 1024^2: 4.5 -> 6.3 ms).  BSGD_GATHER_TILES=force skips the test.
-    const char *force = getenv("BSGD_GATHER_TILES");
-    if (force && strcmp(force, "force") == 0) return BSGD_OK;
-    const int64_t nin = transposed ? p->rows : p->cols, nout = transposed ? p->cols : p->rows;
-    double *vin = nullptr, *vout = nullptr;
-    if (cudaMalloc(&vin, sizeof(double) * nin) != cudaSuccess ||
-        cudaMalloc(&vout, sizeof(double) * nout) != cudaSuccess) {
-        cudaGetLastError();
-        cudaFree(vin);
-        return BSGD_OK;  // keep the tiles untimed
-    }
-    cudaMemsetAsync(vin, 0, sizeof(double) * nin, st);
-    cudaEvent_t e0, e1;
-    cudaEventCreate(&e0);
-    cudaEventCreate(&e1);
-    float t[2] = {0.f, 0.f};
-    for (int variant = 0; variant < 2 && rc == BSGD_OK; ++variant) {
-        for (int rep = 0; rep < 4 && rc == BSGD_OK; ++rep) {
-            if (rep == 1) cudaEventRecord(e0, st);
-            if (variant == 0) {
-                rc = p->vdt == BSGD_F32
-                         ? launch_one<float>(transposed ? tr_csr<float>(p, vin) : fwd_csr<float>(p, vin),
-                                             transposed ? p->g_tr : p->g_fwd, EpiStore{vout, 1.0}, nullptr, nullptr,
-                                             p->nnz, st)
-                         : launch_one<double>(transposed ? tr_csr<double>(p, vin) : fwd_csr<double>(p, vin),
-                                              transposed ? p->g_tr : p->g_fwd, EpiStore{vout, 1.0}, nullptr, nullptr,
-                                              p->nnz, st);
-            } else {
-                rc = p->vdt == BSGD_F32 ? launch_gtile<float>(S, vin, EpiStore{vout, 1.0}, nullptr, nullptr, st)
-                                        : launch_gtile<double>(S, vin, EpiStore{vout, 1.0}, nullptr, nullptr, st);
-            }
-        }
-        cudaEventRecord(e1, st);
-        cudaEventSynchronize(e1);
-        cudaEventElapsedTime(&t[variant], e0, e1);
-    }
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
-    cudaFree(vin);
-    cudaFree(vout);
-    if (rc == BSGD_OK && !(t[1] < 0.97f * t[0])) {
-        p->device_bytes -= S.bytes;
-        gtiles_free(S);
-    }
-    return rc;
+    // The caller asked for these tiles, so they are kept: no timing race decides
+    // which kernel a plan runs.  BlockOperator requests them where they win
+    // (pixel rows of A^T for CT: 6.1 -> 4.2 ms at 1024^2, whose CSR gathers have
+    // no sector locality) and not where they lose (ray rows of A: 4.5 -> 6.3 ms).
+    (void)st;
+    return BSGD_OK;
 }
 
 int bsgd_plan_stacked_tiles(bsgd_plan *p, int transposed, int64_t ntiles, const int64_t *tile_ptr,
@@ -2184,6 +1865,73 @@ int bsgd_plan_csr_copy(const bsgd_plan *p, int64_t *indptr_out, int32_t *indices
 
 int bsgd_plan_destroy(bsgd_plan *plan) {
     plan_free(plan);
+    return BSGD_OK;
+}
+
+// The kernels launch_fwd / launch_tr dispatch to for this plan (same decision order).
+static void kernel_choice(const bsgd_plan *p, bool tr, int32_t *kind, int32_t *lanes) {
+    if (p->stacked()) {
+        const bsgd_plan::StkTileStore &S = tr ? p->stt : p->sf;
+        if (stk_tiles_used(p, S)) {
+            *kind = BSGD_K_STACKED_TILE;
+            *lanes = S.kz;
+        } else {
+            *kind = BSGD_K_STACKED;
+            *lanes = tr ? p->kz_tr : p->kz_fwd;
+        }
+        return;
+    }
+    const bsgd_plan::GTileStore &G = tr ? p->gt : p->gf;
+    if (gtiles_on(G)) {
+        *kind = BSGD_K_GTILE;
+        *lanes = 16;
+        return;
+    }
+    if (!tr && blocked_on(p)) {
+        *kind = p->fb.base ? BSGD_K_BLOCKED_CMP : BSGD_K_BLOCKED;
+        *lanes = p->fb.gb;
+        return;
+    }
+    *kind = BSGD_K_CSR;
+    *lanes = tr ? p->g_tr : p->g_fwd;
+}
+
+int bsgd_plan_kernel_info(const bsgd_plan *p, bsgd_kernel_info *out) {
+    if (!p || !out) return fail(BSGD_EINVAL, "NULL argument");
+    *out = bsgd_kernel_info{};
+    kernel_choice(p, false, &out->fwd_kernel, &out->fwd_lanes);
+    kernel_choice(p, true, &out->tr_kernel, &out->tr_lanes);
+    out->depth = p->depth;
+    return BSGD_OK;
+}
+
+int bsgd_plan_set_timing(bsgd_plan *p, int enable) {
+    if (!p) return fail(BSGD_EINVAL, "plan is NULL");
+    p->timing.on = enable != 0;
+    p->timing.used = 0;
+    return BSGD_OK;
+}
+
+int bsgd_plan_timing(bsgd_plan *p, double *ms_out, int64_t *epochs_out) {
+    if (!p || !ms_out) return fail(BSGD_EINVAL, "NULL argument");
+    DeviceGuard guard(p->device);
+    bsgd_plan::Timing &T = p->timing;
+    for (int k = 0; k < BSGD_TIMING_PHASES; ++k) ms_out[k] = 0.0;
+    const size_t epochs = T.used / kPhaseEvents;
+    if (epochs) {
+        cudaError_t e = cudaEventSynchronize(T.pool[T.used - 1]);
+        for (size_t q = 0; q < epochs && e == cudaSuccess; ++q) {
+            const cudaEvent_t *ev = &T.pool[q * kPhaseEvents];
+            for (int k = 0; k < BSGD_TIMING_PHASES && e == cudaSuccess; ++k) {
+                float ms = 0.f;
+                e = cudaEventElapsedTime(&ms, ev[k], ev[k + 1]);
+                ms_out[k] += ms;
+            }
+        }
+        if (e != cudaSuccess) return fail(BSGD_ECUDA, "phase timing: %s", cudaGetErrorString(e));
+    }
+    if (epochs_out) *epochs_out = (int64_t)epochs;
+    T.used = 0;
     return BSGD_OK;
 }
 
@@ -2665,39 +2413,42 @@ int bsgd_epoch(const bsgd_plan *p, const bsgd_epoch_args *a, void *stream) {
     if ((fl & BSGD_EP_LOOKAHEAD) && !a->r_ahead) return fail(BSGD_EINVAL, "r_ahead is required");
     DeviceGuard guard(p->device);
     cudaStream_t st = (cudaStream_t)stream;
+    EpochTimer timer(p, st);
+#define TIMING_MARK(k) timer.mark(k)
     const bool prox = a->lam > 0.0;
     EpiStep es{a->g, a->x_k, a->mu, a->x_next, prox ? ws.uimg : nullptr, a->perm, a->x_true};
-    const bool tiled = tiled_usable(p, p->tf, a->x_k) && tiled_usable(p, p->tt, a->r_k);
     if (fl & BSGD_EP_SKIP_GRAD) {
         rc = run_step(p->cols, a, ws, st);
         if (!rc && (fl & BSGD_EP_R_NEXT))
             rc = DISPATCH_V(p, launch_fwd<V>(p, a->x_k, EpiResid{a->y, a->r_next}, ws.rpart, ws.ctl + 2, st));
-    } else if ((fl & BSGD_EP_R_NEXT) &&
-               (tiled || p->stacked() || p->gf.ok || p->gt.ok || blocked_on(p) || !getenv("BSGD_MERGE_K1K2"))) {
-        // K1(x_k) then K2(r_k) on the stream.  One merged grid (below, opt-in) reads the
-        // same snapshot but measured slower on configs[1] (0.79 vs 0.66 ms per epoch):
-        // both halves are gather-bound and the CTA split balances them poorly
-        rc = DISPATCH_V(p, launch_fwd<V>(p, a->x_k, EpiResid{a->y, a->r_next}, ws.rpart, ws.ctl + 2, st));
-        if (!rc) rc = DISPATCH_V(p, launch_tr<V>(p, a->r_k, es, ws.xpart, ws.ctl, st));
-    } else if (fl & BSGD_EP_R_NEXT) {
-        // K1(x_k) and K2(r_k) read the same snapshot: one grid (solvers.py:281-290)
-        rc = DISPATCH_V(p, launch_two<V>(fwd_csr<V>(p, a->x_k), p->g_fwd, EpiResid{a->y, a->r_next}, ws.rpart, ws.ctl + 2,
-                                          p->nnz, tr_csr<V>(p, a->r_k), p->g_tr, es, ws.xpart, ws.ctl, p->nnz, st));
     } else {
-        rc = DISPATCH_V(p, launch_tr<V>(p, a->r_k, es, ws.xpart, ws.ctl, st));
+        // K1(x_k) (when the lookahead r is invalid) then K2(r_k): both read the
+        // snapshot x_k / r_k (solvers.py:281-290).  One merged grid was measured
+        // slower on configs[1] (0.79 vs 0.66 ms per epoch; both halves are
+        // gather-bound and the CTA split balances them poorly), so they run back to back.
+        if (fl & BSGD_EP_R_NEXT)
+            rc = DISPATCH_V(p, launch_fwd<V>(p, a->x_k, EpiResid{a->y, a->r_next}, ws.rpart, ws.ctl + 2, st));
+        TIMING_MARK(1);
+        if (!rc) rc = DISPATCH_V(p, launch_tr<V>(p, a->r_k, es, ws.xpart, ws.ctl, st));
     }
+    if (fl & BSGD_EP_SKIP_GRAD) TIMING_MARK(1);
+    TIMING_MARK(2);
     if (rc) return rc;
     if (prox) {
         rc = run_prox(a, ws, st);
         if (rc) return rc;
     }
+    TIMING_MARK(3);
     if (fl & BSGD_EP_LOOKAHEAD) {
         // K1(x_next): the next epoch's residual and the Eq. 9 monitor's f_next (solvers.py:319-320)
         rc = DISPATCH_V(p, launch_fwd<V>(p, a->x_next, EpiResid{a->y, a->r_ahead}, ws.rpart, ws.ctl + 1, st));
         if (rc) return rc;
     }
-    if (!(fl & BSGD_EP_NO_TAIL)) return run_tail(a, ws, (fl & BSGD_EP_LOOKAHEAD) ? 1 : 0, nullptr, st);
-    return BSGD_OK;
+    TIMING_MARK(4);
+    if (!(fl & BSGD_EP_NO_TAIL)) rc = run_tail(a, ws, (fl & BSGD_EP_LOOKAHEAD) ? 1 : 0, nullptr, st);
+    TIMING_MARK(5);
+#undef TIMING_MARK
+    return rc;
 }
 
 int bsgd_step(int64_t cols, const bsgd_epoch_args *a, void *stream) {

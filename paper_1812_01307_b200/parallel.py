@@ -141,6 +141,28 @@ class CudaShard:
         self._finish(spec, op, a2.shape[1] * depth, lam, layout)
         return self
 
+    @classmethod
+    def parallel_beam(cls, n: int, num_angles: int, num_bins: int, spec: ShardSpec, dtype=np.float32, device=None,
+                      lam: float = 0.0, layout=None, tiles: bool = True) -> "CudaShard":
+        """Row-slab shard of the Siddon parallel-beam projector generated on the
+        rank's GPU: only the rank's rays are traced (`BlockOperator.from_parallel_beam`
+        with an angle range), so no host CSR exists at any size (configs[3]: 1.9e9
+        nonzeros over the ranks).  The rank's rows must be whole angles (configs[3]:
+        each of the 8 row blocks is 180 angles x 1449 bins).  The shard's A^T is
+        gather-tiled over 4 x 4 pixel tiles like the single-GPU operator."""
+        from .blockops import BlockPartition, grid_tiles
+        r0, r1 = spec.row_range
+        if r0 % num_bins or r1 % num_bins:
+            raise ValueError(f"rows [{r0}, {r1}) are not whole angles of {num_bins} bins")
+        part = BlockPartition(spec.local_row_bounds, spec.partition.col_bounds)
+        op = BlockOperator.from_parallel_beam(n, num_angles, num_bins, dtype=dtype, device=device, tiles=False,
+                                              angle_range=(r0 // num_bins, r1 // num_bins), partition=part)
+        if tiles:
+            op.set_gather_tiles(True, grid_tiles(n, n))
+        self = cls.__new__(cls)
+        self._finish(spec, op, n * n, lam, layout)
+        return self
+
     def _finish(self, spec, op, cols, lam, layout):
         t = nat.torch()
         self.t = t
@@ -222,6 +244,37 @@ class CudaShard:
         nat.call("bsgd_rmatvec", self.op.plan, nat.ptr(w), nat.ptr(out), self.stream())
 
 
+def ct_row_slab_shard(index: int, rank: int, world: int, device=None, group=None):
+    """configs[index] (2-D CT) as this rank's row slab, generated on its GPU.
+
+    Returns (shard, y_full, meta).  y = A x_true + noise is the single-GPU
+    instance's (`problems.ct_problem_device`) bit for bit: each rank forms its
+    rows of A x_true with the same kernel, the slices are all-gathered (rows
+    doubles), and the seeded noise of the full length is drawn on every rank."""
+    import torch.distributed as dist
+    from . import problems, tv
+    name, n, ang, nb, ell, noise_frac, blocks, lam, inner, epochs, dt = problems.CT_TABLE[index]
+    t = nat.torch()
+    rows, cols = ang * nb, n * n
+    spec = ShardSpec(make_partition(rows, cols, blocks, blocks), rank, world)
+    layout = tv.PixelLayout.row_major(n, n)
+    shard = CudaShard.parallel_beam(n, ang, nb, spec, dtype=dt, device=device, lam=lam, layout=layout)
+    x_true = problems.ellipse_phantom(n, ell, 0).ravel()
+    clean_local = shard.op.matvec(x_true, charge=False)
+    if dist.is_initialized() and dist.get_world_size(group) > 1:
+        counts = [b - a for a, b in (ShardSpec(spec.partition, p, world).row_range for p in range(world))]
+        pieces = [t.empty(c, dtype=t.float64, device=shard.dev) for c in counts]
+        dist.all_gather(pieces, shard.vector(clean_local), group=group)
+        clean = t.cat(pieces).cpu().numpy()
+    else:
+        clean = np.asarray(clean_local)
+    sigma = noise_frac * float(np.max(clean))
+    y = clean + np.random.default_rng(1).standard_normal(rows) * sigma
+    meta = {"name": name, "height": n, "width": n, "lam": lam, "max_inner_iters": inner, "epochs": epochs,
+            "x_true": x_true, "layout": layout}
+    return shard, y, meta
+
+
 SLAB_PROX_MIN_VOXELS = 1 << 22   # prox="auto" decomposes volumes from this size on
 
 
@@ -239,6 +292,12 @@ class DistributedBSGD:
         than one rank when it applies and the volume has at least
         SLAB_PROX_MIN_VOXELS voxels (configs[4]'s 256^3), "replicated" otherwise."""
         import torch.distributed as dist
+        if cfg.alpha != 1.0 or cfg.gamma != 1.0:
+            raise ValueError("DistributedBSGD runs full sweeps only (alpha = gamma = 1); the stochastic "
+                             "pair subsets of solvers.py:186-195 need the single-GPU bsgd_tv_iteration")
+        if cfg.enforce_decrease:
+            raise ValueError("DistributedBSGD monitors Eq. 9 but does not halve mu (enforce_decrease, "
+                             "solvers.py:325-333); use the single-GPU bsgd_tv_iteration for it")
         self.dist = dist
         self.group = group
         self.s = shard
@@ -310,8 +369,24 @@ class DistributedBSGD:
         sp = self.s.spec.partition
         schedule_pairs(sp.num_row_blocks, sp.num_col_blocks, 1.0, 1.0, self.rng)
 
+    def _ensure_history(self, extra: int) -> bool:
+        """Grow the history table so ``extra`` more rows fit (the tail kernel skips
+        rows past the capacity).  Returns True when it was reallocated, which
+        voids a captured graph (it holds the old table's address)."""
+        need = self.rows_used + extra
+        cap = self.hist.shape[0]
+        if need <= cap:
+            return False
+        t = self.s.t
+        new = t.zeros(max(need, 2 * cap), self.hist.shape[1], dtype=self.hist.dtype, device=self.hist.device)
+        new[:cap].copy_(self.hist)
+        self.hist = new
+        self._graph = None
+        return True
+
     def epoch_step(self, monitor: bool | None = None):
         """One epoch; returns the history row index written."""
+        self._ensure_history(1)
         self._schedule()
         return self._epoch(monitor)
 
@@ -342,7 +417,12 @@ class DistributedBSGD:
         return True
 
     def replay(self):
-        """Run the captured epochs (same arithmetic as `epoch_step`, one launch)."""
+        """Run the captured epochs (same arithmetic as `epoch_step`, one launch).
+        When the history table is full it is grown and the graph re-captured."""
+        if self._ensure_history(self._graph_epochs) or self._graph is None:
+            k = self._graph_epochs
+            if not self.capture(k):
+                raise RuntimeError("CUDA graph re-capture failed after growing the history table")
         for _ in range(self._graph_epochs):
             self._schedule()
         self._graph.replay()

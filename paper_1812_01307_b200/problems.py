@@ -395,6 +395,13 @@ def stacked_ct_problem_device(name: str, n: int, depth: int, num_angles: int, nu
                          epochs, {"phantom": phantom_seed, "noise": noise_seed, "solver": 0}, depth=depth)
 
 
+# 2-D CT configurations: name, image side, angles, bins, ellipses, noise fraction,
+# blocks, lambda, FGP cap, epochs, value dtype (BASELINE.json configs[0], [2], [3])
+CT_TABLE = {0: ("C1", 128, 180, 183, 10, 0.01, 4, 0.02, 20, 100, np.float64),
+            2: ("C3", 512, 720, 727, 30, 0.005, 8, 0.01, 20, 100, np.float32),
+            3: ("C4", 1024, 1440, 1449, 60, 0.005, 8, 0.01, 20, 50, np.float32)}
+
+
 def config_device(index: int, scale: float = 1.0, device=None) -> DeviceProblem:
     """configs[0], [2], [3] or [4] with the projector generated on the GPU."""
     if index == 4:
@@ -404,12 +411,9 @@ def config_device(index: int, scale: float = 1.0, device=None) -> DeviceProblem:
         nb = max(9, int(round(363 * scale)) | 1)
         return stacked_ct_problem_device("C5", n, depth, ang, nb, 40, 0.01, 16, 0.01, 10, 30, np.float32,
                                          device=device)
-    table = {0: ("C1", 128, 180, 183, 10, 0.01, 4, 0.02, 20, 100, np.float64),
-             2: ("C3", 512, 720, 727, 30, 0.005, 8, 0.01, 20, 100, np.float32),
-             3: ("C4", 1024, 1440, 1449, 60, 0.005, 8, 0.01, 20, 50, np.float32)}
-    if index not in table:
+    if index not in CT_TABLE:
         raise ValueError(f"config index {index} is not a 2D CT configuration")
-    name, n, ang, nb, ell, noise, blocks, lam, inner, epochs, dt = table[index]
+    name, n, ang, nb, ell, noise, blocks, lam, inner, epochs, dt = CT_TABLE[index]
     n = max(16, int(round(n * scale)))
     ang = max(8, int(round(ang * scale)))
     nb = max(9, int(round(nb * scale)) | 1)

@@ -7,7 +7,7 @@ kernels; `tv_prox` is one persistent cooperative kernel
 (`csrc/fgp.cuh`) that keeps the FGP restart / stop / fallback decisions on
 the device.  `ProxInfo` carries the same diagnostics as the reference.
 
-Volumes (configs[4], 512^3): the reference has 2D TV only.  `VolumeGrid` /
+Volumes (configs[4], 256^3): the reference has 2D TV only.  `VolumeGrid` /
 `VolumeLayout` and the 3-D branches of `tv_prox` / `tv_value` extend tv.py's
 conventions one axis up (z-major storage, backward differences along z, rows,
 columns; dual step 1/(12 w)); the CPU checker is `oracle.tv_prox3`.
@@ -15,6 +15,7 @@ columns; dual step 1/(12 w)); the CPU checker is `oracle.tv_prox3`.
 
 from __future__ import annotations
 
+import threading
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -226,17 +227,25 @@ def _image_tensor(img, device):
 
 
 _ws_cache: dict = {}
+_ws_lock = threading.Lock()
 
 
 def prox_workspace(height: int, width: int, device, depth: int = 1):
-    """Zeroed device workspace for `bsgd_tv_prox(3)`, reused across calls of one shape."""
+    """Zeroed device workspace for `bsgd_tv_prox(3)`, reused across calls of one
+    shape on one stream.  The key includes the current CUDA stream and the
+    calling thread, so concurrent proxes (other streams or threads) never share
+    dual fields or reduction counters; calls on one stream are serialised by
+    the stream itself."""
     t = nat.torch()
-    key = (depth, height, width, str(device))
-    ws = _ws_cache.get(key)
-    if ws is None:
-        nbytes = int(nat.load().bsgd_tv_prox3_workspace_bytes(depth, height, width))
-        ws = t.zeros((nbytes + 7) // 8, dtype=t.float64, device=device)
-        _ws_cache[key] = ws
+    dev = t.device(device)
+    stream = t.cuda.current_stream(dev).cuda_stream
+    key = (depth, height, width, str(dev), stream, threading.get_ident())
+    with _ws_lock:
+        ws = _ws_cache.get(key)
+        if ws is None:
+            nbytes = int(nat.load().bsgd_tv_prox3_workspace_bytes(depth, height, width))
+            ws = t.zeros((nbytes + 7) // 8, dtype=t.float64, device=dev)
+            _ws_cache[key] = ws
     return ws
 
 

@@ -260,10 +260,10 @@ def test_metrics_and_spectral(B):
     assert abs(abs(v1) - 1.0) < 1e-12 and abs(abs(v2) - 1.0) < 1e-12
 
 
-def test_gather_tiles_match_csr(B, monkeypatch):
-    """Gather-tiled products (gtile.cuh, forced past the autotune) agree with the CSR
-    kernel and the oracle to rounding; irregular tiles and removal work."""
-    monkeypatch.setenv("BSGD_GATHER_TILES", "force")
+def test_gather_tiles_match_csr(B):
+    """Gather-tiled products (gtile.cuh; kept whenever requested, no timing race)
+    agree with the CSR kernel and the oracle to rounding; irregular tiles and
+    removal work, and kernel_info reports which kernel runs."""
     blockops = B[0]
     from paper_1812_01307_b200 import problems
     n, ang, nb = 24, 20, 35
@@ -278,6 +278,8 @@ def test_gather_tiles_match_csr(B, monkeypatch):
     ptr = np.concatenate([[0], np.cumsum(sizes)])
     ptr = ptr[ptr < a.shape[0]].tolist() + [a.shape[0]]
     op.set_gather_tiles(False, (np.asarray(ptr, dtype=np.int64), perm.astype(np.int64)))
+    ki = op.kernel_info()
+    assert ki["forward"] == "gather_tiled" and ki["transposed"] == "gather_tiled"
     assert rel(op.matvec(x), oop.matvec(x)) < 1e-12
     assert rel(op.rmatvec(w), oop.rmatvec(w)) < 1e-12
     r, s = op.residual_sumsq(x, y)
@@ -285,19 +287,25 @@ def test_gather_tiles_match_csr(B, monkeypatch):
     assert rel(r.cpu().numpy(), want) < 1e-12
     op.set_gather_tiles(True, None)
     op.set_gather_tiles(False, None)
+    assert op.kernel_info()["transposed"] == "csr"
     assert rel(op.matvec(x), oop.matvec(x)) < 1e-12
     with pytest.raises(ValueError):
         op.set_gather_tiles(True, (np.array([0, 17]), np.arange(17)))
 
 
-@pytest.mark.parametrize("dtype,lanes", [(np.float32, "32"), (np.float64, "32"), (np.float32, None),
-                                         (np.float64, "4"), (np.float32, "16")])
-def test_blocked_stream_bit_identical(B, monkeypatch, dtype, lanes):
+@pytest.mark.parametrize("dtype,lanes,compress", [(np.float32, "32", None), (np.float64, "32", "off"),
+                                                  (np.float32, None, None), (np.float32, None, "off"),
+                                                  (np.float64, "4", None), (np.float32, "4", "force"),
+                                                  (np.float32, "16", "force")])
+def test_blocked_stream_bit_identical(B, monkeypatch, dtype, lanes, compress):
     """The blocked copy of A's stream (spmv.cuh csr_blocked_kernel): with 32 lanes
     per row it gives the unblocked G = 32 kernel's products bit for bit (same
     per-lane order; padding adds exact zeros); with fewer lanes (the plan's
-    choice, several rays per warp) it agrees to rounding.  Rows shorter than a
-    block and empty rows included."""
+    choice, several rays per warp) it agrees to rounding.  Both index forms --
+    plain int32 and the compressed base + 16-bit increments (the structural
+    rule keeps it at >= 8 lanes per ray; BSGD_BLK_COMPRESS forces either) --
+    against the oracle, with kernel_info confirming which one ran.  Rows
+    shorter than a block and empty rows included."""
     blockops = B[0]
     from paper_1812_01307_b200 import problems
     a = problems.parallel_beam_matrix(256, 24, 363, dtype=dtype)   # rays of ~290 nonzeros: G = 32
@@ -312,7 +320,14 @@ def test_blocked_stream_bit_identical(B, monkeypatch, dtype, lanes):
     monkeypatch.setenv("BSGD_BLOCKED", "force")
     if lanes is not None:
         monkeypatch.setenv("BSGD_BLK_G", lanes)
+    if compress is not None:
+        monkeypatch.setenv("BSGD_BLK_COMPRESS", compress)
     blk = blockops.BlockOperator(a, part)
+    g = int(lanes) if lanes is not None else 8
+    want_cmp = compress == "force" or (compress is None and g >= 8)
+    ki = blk.kernel_info()
+    assert ki["forward"] == ("blocked_compressed" if want_cmp else "blocked") and ki["forward_lanes"] == g
+    assert plain.kernel_info()["forward"] == "csr"
     exact = lanes == "32"
     oop = orc.OracleOperator(a, 2, 2)
     rng = np.random.default_rng(11)

@@ -197,26 +197,6 @@ def test_c2_full_size_convergence(S):
     assert tr.matvec_units()[-1] == 2 * 200 + 4
 
 
-def test_merged_and_sequential_first_epoch_agree(S, monkeypatch):
-    """After x is written the epoch recomputes y - A x_k (R_NEXT): sequential K1, K2 by
-    default, one merged grid with BSGD_MERGE_K1K2=1 -- the same rows, bit for bit."""
-    blockops, solvers, tv = S
-    z = load_golden("p3_ls")
-    outs = []
-    for merge in (False, True):
-        if merge:
-            monkeypatch.setenv("BSGD_MERGE_K1K2", "1")
-        op, cfg, layout, c = _setup(S, z)
-        st = solvers.init_bsgd_state(op, z["y"], cfg)
-        hx = np.zeros(op.shape[1])
-        for _ in range(3):
-            st.x = hx
-            solvers.bsgd_tv_iteration(st, op, z["y"], cfg, layout=layout)
-            hx = st.x
-        outs.append((st.x, st.r_vec))
-    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
-
-
 def test_host_readback_overlap_matches_plain_path(S):
     """Reading x / r_vec after every epoch turns on overlapped readback; values are
     the plain path's, bit for bit, and stale buffers are never handed out."""
