@@ -11,14 +11,14 @@ REPO = os.path.dirname(_HERE)
 CSRC = os.path.join(_HERE, "csrc")
 LIB_DIR = os.path.join(_HERE, "lib")
 LIB_PATH = os.path.join(LIB_DIR, "libbsgd_b200.so")
-SOURCES = ["bsgd_abi.cu"]
-DEPS = ["bsgd_abi.cu", "common.cuh", "spmv.cuh", "fgp.cuh", "pairwise.cuh", "sm100.cuh", "siddon.cuh",
-        "stacked.cuh", "gtile.cuh", "slab.cuh"]
+SOURCES = ["bsgd_abi.cu", "fgp2.cu"]
+DEPS = ["bsgd_abi.cu", "fgp2.cu", "fgp2.h", "prox_args.cuh", "common.cuh", "spmv.cuh", "fgp.cuh", "pairwise.cuh",
+        "sm100.cuh", "siddon.cuh", "stacked.cuh", "gtile.cuh", "slab.cuh"]
 
-NVCC_FLAGS = [
-    "-gencode", "arch=compute_100a,code=sm_100a",
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVCC_FLAGS = ARCH + [
     "-lineinfo", "-O3", "-std=c++17",
-    "-Xcompiler", "-fPIC", "-shared",
+    "-Xcompiler", "-fPIC",
     "-Xptxas", "-v",
 ]
 
@@ -37,19 +37,36 @@ def _stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile every translation unit (in parallel) and link libbsgd_b200.so."""
     if not force and not _stale():
         return LIB_PATH
     os.makedirs(LIB_DIR, exist_ok=True)
+    objs, procs = [], []
+    for src in SOURCES:
+        obj = os.path.join(LIB_DIR, os.path.splitext(src)[0] + ".o")
+        objs.append(obj)
+        procs.append(subprocess.Popen([_nvcc(), *NVCC_FLAGS, "-c", "-o", obj, os.path.join(CSRC, src)],
+                                      stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True))
+    logs, failed = [], False
+    for src, pr in zip(SOURCES, procs):
+        out, err = pr.communicate()
+        logs.append(f"== {src}\n{out}{err}")
+        if pr.returncode != 0:
+            sys.stderr.write(out + err)
+            failed = True
+    if failed:
+        raise RuntimeError("nvcc failed building libbsgd_b200.so")
     tmp = LIB_PATH + ".tmp"
-    cmd = [_nvcc(), *NVCC_FLAGS, "-o", tmp, *[os.path.join(CSRC, s) for s in SOURCES]]
-    res = subprocess.run(cmd, capture_output=True, text=True)
+    res = subprocess.run([_nvcc(), *ARCH, "-shared", "-o", tmp, *objs], capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
-        raise RuntimeError("nvcc failed building libbsgd_b200.so")
+        raise RuntimeError("nvcc failed linking libbsgd_b200.so")
     if verbose:
-        sys.stderr.write(res.stderr)
+        sys.stderr.write("".join(logs))
     with open(os.path.join(LIB_DIR, "ptxas.log"), "w") as fh:
-        fh.write(res.stderr)
+        fh.write("".join(logs))
+    for obj in objs:
+        os.unlink(obj)
     os.replace(tmp, LIB_PATH)
     return LIB_PATH
 

@@ -25,6 +25,7 @@
 #include "../../include/bsgd_b200.h"
 #include "common.cuh"
 #include "fgp.cuh"
+#include "fgp2.h"
 #include "spmv.cuh"
 #include "siddon.cuh"
 #include "stacked.cuh"
@@ -406,8 +407,8 @@ template <typename V>
 static int build_blocked(bsgd_plan *p, cudaStream_t st) {
     const char *force = getenv("BSGD_BLOCKED");
     const bool forced = force && strcmp(force, "force") == 0;
-    if (p->stacked() || p->rows == 0 || p->g_fwd != 32 || getenv("BSGD_NO_BLOCKED") ||
-        ((double)p->nnz / (double)p->rows < 384.0 && !forced))
+    if (p->stacked() || p->rows == 0 || getenv("BSGD_NO_BLOCKED") ||
+        ((p->g_fwd != 32 || (double)p->nnz / (double)p->rows < 384.0) && !forced))
         return BSGD_OK;
     bsgd_plan::BlkStore b;
     // Few lanes per ray, several adjacent rays per warp: the neighbouring bins of
@@ -1043,6 +1044,15 @@ static int launch_prox(ProxArgs &a, cudaStream_t st) {
     if (a.D <= 1) {
         a.D = 1;
         if (split) return launch_prox_split<2>(a, st);
+        // power-of-two images up to 1024 wide: the row-walk kernel (one grid barrier per
+        // FGP iteration, fgp2.cu); BSGD_PROX_KERNEL=coop selects fgp_kernel (tests compare them)
+        const char *pk = getenv("BSGD_PROX_KERNEL");
+        if (!(pk && strcmp(pk, "coop") == 0) && fgp2_rows_supported(a)) {
+            cudaError_t e = fgp2_rows_launch(a, num_sms(), st);
+            if (e == cudaSuccess) return BSGD_OK;
+            if (e != cudaErrorCooperativeLaunchTooLarge) return fail(BSGD_ECUDA, "fgp2_rows_kernel: %s", cudaGetErrorString(e));
+            cudaGetLastError();
+        }
         return a.fast ? launch_prox_dim<2, true>(a, st) : launch_prox_dim<2, false>(a, st);
     }
     if (split) return launch_prox_split<3>(a, st);

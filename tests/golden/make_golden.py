@@ -31,6 +31,9 @@ from bsgdtv import blockops, metrics, sim, solvers, spectral, tv  # noqa: E402
 
 from paper_1812_01307_b200 import problems  # noqa: E402
 
+sys.path.insert(0, os.path.join(REPO, "tests"))
+from golden_inputs import prox_rows_inputs  # noqa: E402
+
 
 def save(name, **arrays):
     path = os.path.join(HERE, name + ".npz")
@@ -136,6 +139,21 @@ def gen_prox():
     save("prox", **out)
 
 
+def gen_prox_rows():
+    out = {}
+    for k, (name, img, w, mi, tol) in enumerate(prox_rows_inputs()):
+        grid = tv.ImageGrid.from_matrix(img)
+        res, info = tv.tv_prox(grid, w, tv.ProxSettings(mi, tol), return_info=True)
+        out[f"out{k}"] = res.as_matrix()
+        out[f"info{k}"] = np.array([info.iterations, int(info.converged), info.restarts, int(info.fell_back)],
+                                   dtype=np.int64)
+        out[f"dual{k}"] = np.array(info.dual_objectives)
+        out[f"tv{k}"] = np.array([tv.tv_value(grid), tv.tv_value(res)])
+        print(name, img.shape, "iterations", info.iterations, "restarts", info.restarts)
+    out["count"] = np.array(len(out) // 4)
+    save("prox_rows", **out)
+
+
 # --- solver runs ----------------------------------------------------------------
 
 def solver_case(name, a, y, x_true, layout, m, n, cfg, sample_every=1, epochs_state=3,
@@ -234,6 +252,7 @@ def gen_solvers():
 
 
 if __name__ == "__main__":
-    gen_partitions()
-    gen_prox()
-    gen_solvers()
+    which = sys.argv[1:] or ["partitions", "prox", "prox_rows", "solvers"]
+    for name in which:
+        {"partitions": gen_partitions, "prox": gen_prox, "prox_rows": gen_prox_rows,
+         "solvers": gen_solvers}[name]()

@@ -198,6 +198,43 @@ def test_tv_prox_vs_reference_golden(B):
         assert tv.tv_value(tv.ImageGrid.from_matrix(z[f"in{k}"])) == float(z[f"tv{k}"][0])
 
 
+def test_tv_prox_rows_kernel_vs_reference_golden(B):
+    """Power-of-two images >= 128 wide run the row-walk kernel (csrc/fgp2.cu): output,
+    ProxInfo and dual objectives bit-exact with the reference (restarts included)."""
+    from golden_inputs import prox_rows_inputs
+    tv = B[1]
+    z = load_golden("prox_rows")
+    for k, (name, img, w, mi, tol) in enumerate(prox_rows_inputs()):
+        out, info = tv.tv_prox(tv.ImageGrid.from_matrix(img), w, tv.ProxSettings(mi, tol), return_info=True)
+        assert np.array_equal(out.as_matrix(), z[f"out{k}"]), name
+        assert [info.iterations, int(info.converged), info.restarts, int(info.fell_back)] == list(z[f"info{k}"]), name
+        assert np.array_equal(np.array(info.dual_objectives), z[f"dual{k}"]), name
+        assert tv.tv_value(out) == float(z[f"tv{k}"][1])
+
+
+@pytest.mark.parametrize("shape,w,tol", [((1024, 1024), 0.01, 1e-300), ((1024, 1024), 2.0, 1e-300),
+                                         ((512, 512), 0.05, 1e-12), ((128, 1024), 0.3, 1e-300),
+                                         ((2048, 256), 0.02, 1e-9), ((256, 512), 1e-4, 1e-5)])
+def test_tv_prox_rows_kernel_matches_cooperative_kernel(B, monkeypatch, shape, w, tol):
+    """The row-walk kernel and the cooperative fgp_kernel<2> (BSGD_PROX_KERNEL=coop)
+    give the same bits: output, ProxInfo, dual objectives, in standalone mode."""
+    import torch
+    tv = B[1]
+    g = torch.Generator(device="cuda").manual_seed(sum(shape))
+    img = torch.rand(*shape, dtype=torch.float64, device="cuda", generator=g) * 3.0
+    img[shape[0] // 3:, : shape[1] // 2] += 1.0
+    st = tv.ProxSettings(20, tol)
+    outs = []
+    for kernel in ("rows", "coop"):
+        if kernel == "coop":
+            monkeypatch.setenv("BSGD_PROX_KERNEL", "coop")
+        out, info = tv.tv_prox(img, w, st, return_info=True)
+        outs.append((out.cpu().numpy(), (info.iterations, info.converged, info.restarts, info.fell_back),
+                     list(info.dual_objectives)))
+    assert np.array_equal(outs[0][0], outs[1][0])
+    assert outs[0][1] == outs[1][1] and outs[0][2] == outs[1][2]
+
+
 @pytest.mark.parametrize("shape,w", [((64, 64), 1e-3), ((64, 64), 0.05), ((37, 101), 0.2), ((200, 3), 1.0),
                                      ((256, 256), 0.01), ((1024, 1024), 0.01), ((1000, 999), 0.02)])
 def test_tv_prox_vs_oracle_random(B, shape, w):
@@ -308,12 +345,13 @@ def test_blocked_stream_bit_identical(B, monkeypatch, dtype, lanes, compress):
     shorter than a block and empty rows included."""
     blockops = B[0]
     from paper_1812_01307_b200 import problems
-    a = problems.parallel_beam_matrix(256, 24, 363, dtype=dtype)   # rays of ~290 nonzeros: G = 32
+    a = problems.parallel_beam_matrix(256, 24, 363, dtype=dtype)   # rays of up to ~360 nonzeros
     a = a.tolil()
     a[3, :] = 0          # an empty row
     a = a.tocsr()
     a.eliminate_zeros()
     part = blockops.make_partition(*a.shape, 2, 2)
+    monkeypatch.setenv("BSGD_G_FWD", "32")     # the unblocked reference kernel: a warp per row
     monkeypatch.setenv("BSGD_NO_BLOCKED", "1")
     plain = blockops.BlockOperator(a, part)
     monkeypatch.delenv("BSGD_NO_BLOCKED")
@@ -327,7 +365,7 @@ def test_blocked_stream_bit_identical(B, monkeypatch, dtype, lanes, compress):
     want_cmp = compress == "force" or (compress is None and g >= 8)
     ki = blk.kernel_info()
     assert ki["forward"] == ("blocked_compressed" if want_cmp else "blocked") and ki["forward_lanes"] == g
-    assert plain.kernel_info()["forward"] == "csr"
+    assert plain.kernel_info()["forward"] == "csr" and plain.kernel_info()["forward_lanes"] == 32
     exact = lanes == "32"
     oop = orc.OracleOperator(a, 2, 2)
     rng = np.random.default_rng(11)

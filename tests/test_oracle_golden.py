@@ -42,6 +42,18 @@ def test_prox_bit_exact():
         assert orc.tv_value(out) == z[f"tv{k}"][1]
 
 
+def test_prox_rows_bit_exact():
+    """Power-of-two images >= 128 wide (the row-walk CUDA kernel's shapes), against
+    the reference's own outputs, ProxInfo and dual objectives."""
+    from golden_inputs import prox_rows_inputs
+    z = load_golden("prox_rows")
+    for k, (name, img, w, mi, tol) in enumerate(prox_rows_inputs()):
+        out, rep = orc.tv_prox(img, w, mi, tol)
+        assert np.array_equal(out, z[f"out{k}"]), name
+        assert [rep.iterations, int(rep.converged), rep.restarts, int(rep.fell_back)] == list(z[f"info{k}"]), name
+        assert np.array_equal(np.array(rep.dual_objectives), z[f"dual{k}"]), name
+
+
 def test_tv_hand_values_and_adjointness():
     z = load_golden("prox")
     # SPEC.md:131 quotes 2+sqrt(2) for ((0,1),(1,1)); the reference itself returns 2
