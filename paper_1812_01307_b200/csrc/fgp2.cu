@@ -71,12 +71,18 @@ __device__ __forceinline__ double div4(double down, double here_v, double right,
     return rn_sub(rn_add(rn_sub(down, here_v), right), here_h);
 }
 
-// c / max(|c|, 1) (tv.py:211-214)
+// c / max(|c|, 1) (tv.py:211-214).  Inside the unit ball (m2 < 1) sqrt(m2) <= 1,
+// so the divisor is exactly 1.0 and c / 1.0 == c bit for bit: the sqrt and the
+// two IEEE divisions run only where the projection is active (NaN takes the
+// division path, as np.maximum propagates it).
 __device__ __forceinline__ void proj2(double &cv, double &ch) {
-    double mag = sqrt(rn_add(rn_mul(cv, cv), rn_mul(ch, ch)));
-    mag = (mag < 1.0) ? 1.0 : mag;  // np.maximum(mag, 1): NaN propagates
-    cv = cv / mag;
-    ch = ch / mag;
+    const double m2 = rn_add(rn_mul(cv, cv), rn_mul(ch, ch));
+    if (!(m2 < 1.0)) {
+        double mag = sqrt(m2);
+        mag = (mag < 1.0) ? 1.0 : mag;
+        cv = cv / mag;
+        ch = ch / mag;
+    }
 }
 
 struct F2 {
@@ -111,28 +117,81 @@ __device__ __forceinline__ void f2_reduce_row(const F2 &f, const double *stage, 
     }
 }
 
-// CTA leaf values -> part[blockIdx.x], grid barrier, totals in numpy order
+// Balanced pairwise tree over count (a power of two) values v[i * K] in index
+// order, by one warp: lane l folds its count/32 consecutive values with a
+// balanced local tree, then xor butterflies combine lanes (2l, 2l+1), ...;
+// the additions are commutative, so every lane ends with the bits of the
+// (2i, 2i+1)-paired tree that pw_smem_tree computes.  count < 32: lanes
+// >= count carry duplicates that never reach lanes < count.
+// balanced tree over P consecutive values (P a power of two), fully unrolled
+template <int P, class L>
+__device__ __forceinline__ double fold_run(const L &ld, int base) {
+    double loc[P];
+#pragma unroll
+    for (int i = 0; i < P; ++i) loc[i] = ld(base + i);
+#pragma unroll
+    for (int wdt = P; wdt > 1; wdt >>= 1)
+#pragma unroll
+        for (int i = 0; i < wdt / 2; ++i) loc[i] = rn_add(loc[2 * i], loc[2 * i + 1]);
+    return loc[0];
+}
+
+template <int K, bool GLOBAL>
+__device__ __forceinline__ double warp_pw_tree(const double *v, int count, int lane) {
+    auto ld = [&](int i) { return GLOBAL ? __ldcg(v + (size_t)i * K) : v[(size_t)i * K]; };
+    double acc;
+    int levels = count;
+    if (count >= 32) {
+        const int per = count >> 5, base = lane * per;
+        switch (per) {
+            case 1: acc = fold_run<1>(ld, base); break;
+            case 2: acc = fold_run<2>(ld, base); break;
+            case 4: acc = fold_run<4>(ld, base); break;
+            case 8: acc = fold_run<8>(ld, base); break;
+            default: acc = fold_run<16>(ld, base); break;   // count <= 512 (checked at launch)
+        }
+        levels = 32;
+    } else {
+        acc = ld(lane < count ? lane : 0);
+    }
+    for (int off = 1; off < levels; off <<= 1) acc = rn_add(acc, __shfl_xor_sync(0xffffffffu, acc, off));
+    return acc;
+}
+
+// CTA leaf values -> part[blockIdx.x] (warp k folds sum k), grid barrier, and the
+// G CTA results combined the same way; every thread gets the numpy-order totals.
 template <int K>
 __device__ __forceinline__ void f2_finish_sum(cg::grid_group &grid, const F2 &f, double *red, int &round,
                                               int ds, double (&out)[K]) {
     double *buf = red + (size_t)(round & 1) * kMaxPartials * kPwMaxK;
+    (void)ds;
     __syncthreads();
-    pw_smem_tree<K>(f.leafv, f.R * (f.W >> 7));
-    if (threadIdx.x == 0)
-#pragma unroll
-        for (int k = 0; k < K; ++k) buf[(size_t)blockIdx.x * K + k] = f.leafv[k];
+    const int Q = f.R * (f.W >> 7);
+    for (int k = f.warp; k < K; k += f.nw) {
+        const double v = warp_pw_tree<K, false>(f.leafv + k, Q, f.lane);
+        if (f.lane == 0) buf[(size_t)blockIdx.x * K + k] = v;
+    }
     grid.sync();
-    pw_top<K>(ds, gridDim.x, buf, f.stage, out);
+    for (int k = f.warp; k < K; k += f.nw) {
+        const double v = warp_pw_tree<K, true>(buf + k, (int)gridDim.x, f.lane);
+        if (f.lane == 0) f.stage[k] = v;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < K; ++k) out[k] = f.stage[k];
+    __syncthreads();
     ++round;
 }
 
 // One fused candidate + dual-value + commit pass (see the header).  src: the
-// point the candidate steps from (q, or p on a restart); qzero / pzero: the
-// field is identically zero (first iteration; read as literal zeros).
-__device__ __forceinline__ void f2_pass(const F2 &f, const double *Sv, const double *Sh, bool szero,
-                                        const double *Pv, const double *Ph, bool pzero, double beta, double *Cv,
-                                        double *Ch, double *Qv, double *Qh) {
+// point the candidate steps from (q, or p on a restart); szero / pzero: the
+// field is identically zero (first iteration; read as literal zeros).  Every
+// global load of a step is issued before its arithmetic.
+__device__ __forceinline__ void f2_pass(const F2 &f, double *fb, int fs, int iS, bool szero, int iP, bool pzero,
+                                        double beta, int iC, int iQ) {
     const int W = f.W, H = f.H, t0 = f.t0, lane = f.lane, warp = f.warp;
+    const double *Sv = fb + iS * fs, *Sh = Sv + fs, *Pv = fb + iP * fs, *Ph = Pv + fs;
+    double *Cv = fb + iC * fs, *Ch = Cv + fs, *Qv = fb + iQ * fs, *Qh = Qv + fs;
     const bool has_left = t0 > 0, has_right = t0 + 2 < W;
     Col2 qvH{0.0, 0.0}, qvC{0.0, 0.0}, qhC{0.0, 0.0};
     Col2 um{0.0, 0.0}, uc{0.0, 0.0};
@@ -141,22 +200,36 @@ __device__ __forceinline__ void f2_pass(const F2 &f, const double *Sv, const dou
     const int kstart = f.r0 == 0 ? 1 : 0;
     {
         const int s_first = f.r0 == 0 ? 0 : f.r0 - 1;
-        if (!szero) qvH = ld2(Sv + (size_t)s_first * W + t0);
+        if (!szero) qvH = ld2(Sv + s_first * W + t0);
     }
     for (int k = kstart; k <= f.R + 2; ++k) {
         const int su = f.r0 - 1 + k, sc = su - 1, sb = su - 2;
-        // ---- U: u(su) ----
-        Col2 un{0.0, 0.0}, qvN{0.0, 0.0}, qhU{0.0, 0.0}, bU{0.0, 0.0};
         const bool u_on = su <= f.r1 && su < H;
+        const bool c_on = sc >= f.r0 && sc <= f.r1 && sc < H;
+        const bool b_on = sb >= f.r0 && sb < f.r1;
+        const int ou = su * W + t0, ob = sb * W + t0;
+        // ---- loads of the step ----
+        Col2 qvN{0.0, 0.0}, qhU{0.0, 0.0}, bU{0.0, 0.0}, pv{0.0, 0.0}, ph{0.0, 0.0};
+        double qhR = 0.0;
         if (u_on) {
-            const size_t o = (size_t)su * W + t0;
             if (!szero) {
-                if (su + 1 < H) qvN = ld2(Sv + o + W);
-                qhU = ld2(Sh + o);
+                if (su + 1 < H) qvN = ld2(Sv + ou + W);
+                qhU = ld2(Sh + ou);
+                if (lane == 31 && has_right) qhR = Sh[ou + 2];
             }
-            bU = ldg2(f.b + o);
-            double qhR = __shfl_down_sync(0xffffffffu, qhU.x, 1);
-            if (lane == 31) qhR = (has_right && !szero) ? Sh[o + 2] : 0.0;
+            bU = ldg2(f.b + ou);
+        }
+        if (b_on && !pzero) {
+            pv = ld2(Pv + ob);
+            ph = ld2(Ph + ob);
+        }
+        // the previous row's leaf sums, while this step's loads are in flight
+        if (sb - 1 >= f.r0 && sb - 1 < f.r1) f2_reduce_row<kF2K>(f, f.stage + ((sb - 1) & 1) * kF2K * W, sb - 1 - f.r0);
+        // ---- U: u(su) ----
+        Col2 un{0.0, 0.0};
+        if (u_on) {
+            const double sh = __shfl_down_sync(0xffffffffu, qhU.x, 1);
+            if (lane != 31) qhR = sh;
             const double hv0 = su > 0 ? qvH.x : 0.0, hv1 = su > 0 ? qvH.y : 0.0;
             un.x = rn_add(bU.x, rn_mul(f.w, div4(qvN.x, hv0, qhU.y, has_left ? qhU.x : 0.0)));
             un.y = rn_add(bU.y, rn_mul(f.w, div4(qvN.y, hv1, has_right ? qhR : 0.0, qhU.y)));
@@ -164,7 +237,6 @@ __device__ __forceinline__ void f2_pass(const F2 &f, const double *Sv, const dou
         }
         // ---- C: c(sc) ----
         Col2 cnv{0.0, 0.0}, cnh{0.0, 0.0};
-        const bool c_on = sc >= f.r0 && sc <= f.r1 && sc < H;
         if (c_on) {
             double uleft = __shfl_up_sync(0xffffffffu, uc.y, 1);
             if (lane == 0) uleft = warp > 0 ? f.uxch[(sc & 1) * f.nw + warp - 1] : 0.0;
@@ -181,14 +253,7 @@ __device__ __forceinline__ void f2_pass(const F2 &f, const double *Sv, const dou
             if (lane == 0) f.cxch[(sc & 1) * f.nw + warp] = cnh.x;
         }
         // ---- B: terms, commit and c of row sb ----
-        const bool b_on = sb >= f.r0 && sb < f.r1;
         if (b_on) {
-            const size_t o = (size_t)sb * W + t0;
-            Col2 pv{0.0, 0.0}, ph{0.0, 0.0};
-            if (!pzero) {
-                pv = ld2(Pv + o);
-                ph = ld2(Ph + o);
-            }
             double right1 = __shfl_down_sync(0xffffffffu, cph.x, 1);
             if (lane == 31) right1 = warp + 1 < f.nw ? f.cxch[(sb & 1) * f.nw + warp + 1] : 0.0;
             const bool down = sb + 1 < H;
@@ -197,11 +262,11 @@ __device__ __forceinline__ void f2_pass(const F2 &f, const double *Sv, const dou
             const double res0 = rn_add(bB.x, rn_mul(f.w, d0)), res1 = rn_add(bB.y, rn_mul(f.w, d1));
             const double sv0 = rn_sub(cpv.x, pv.x), sv1 = rn_sub(cpv.y, pv.y);
             const double sh0 = rn_sub(cph.x, ph.x), sh1 = rn_sub(cph.y, ph.y);
-            st2(Qv + o, rn_add(cpv.x, rn_mul(beta, sv0)), rn_add(cpv.y, rn_mul(beta, sv1)));
-            st2(Qh + o, rn_add(cph.x, rn_mul(beta, sh0)), rn_add(cph.y, rn_mul(beta, sh1)));
-            st2(Cv + o, cpv.x, cpv.y);
-            st2(Ch + o, cph.x, cph.y);
-            double *stg = f.stage + (size_t)(sb & 1) * kF2K * W + t0;
+            st2(Qv + ob, rn_add(cpv.x, rn_mul(beta, sv0)), rn_add(cpv.y, rn_mul(beta, sv1)));
+            st2(Qh + ob, rn_add(cph.x, rn_mul(beta, sh0)), rn_add(cph.y, rn_mul(beta, sh1)));
+            st2(Cv + ob, cpv.x, cpv.y);
+            st2(Ch + ob, cph.x, cph.y);
+            double *stg = f.stage + (sb & 1) * kF2K * W + t0;
             st2(stg, rn_mul(res0, res0), rn_mul(res1, res1));
             st2(stg + W, rn_mul(sv0, sv0), rn_mul(sv1, sv1));
             st2(stg + 2 * W, rn_mul(sh0, sh0), rn_mul(sh1, sh1));
@@ -209,7 +274,6 @@ __device__ __forceinline__ void f2_pass(const F2 &f, const double *Sv, const dou
             st2(stg + 4 * W, rn_mul(cph.x, cph.x), rn_mul(cph.y, cph.y));
         }
         __syncthreads();
-        if (b_on) f2_reduce_row<kF2K>(f, f.stage + (size_t)(sb & 1) * kF2K * W, sb - f.r0);
         // ---- roll ----
         um = uc;
         uc = un;
@@ -221,6 +285,8 @@ __device__ __forceinline__ void f2_pass(const F2 &f, const double *Sv, const dou
         bB = bC;
         bC = bU;
     }
+    // the last row's leaf sums (its terms were staged before the final barrier)
+    f2_reduce_row<kF2K>(f, f.stage + ((f.r1 - 1) & 1) * kF2K * W, f.R - 1);
 }
 
 // out(s, t) = b + w div p (tv.py:250)
@@ -287,8 +353,11 @@ __global__ void __launch_bounds__(kF2MaxThreads, 1) fgp2_rows_kernel(ProxArgs a)
     const double tv_b = v2[1];
     if (blockIdx.x == 0 && threadIdx.x == 0 && a.dual != nullptr) a.dual[0] = phi_prev;
 
-    double *P[2] = {a.f[0], a.f[1]}, *Q[2] = {a.f[2], a.f[3]}, *C[2] = {a.f[4], a.f[5]},
-           *Qn[2] = {a.f[6], a.f[7]};
+    // fields f[k] = fb + k * fs: p, q, c, q' at 0 / 2 / 4 / 6 (parity 0); every accepted
+    // iteration swaps p <-> c and q <-> q' (parity flip)
+    double *fb = a.f[0];
+    const int fs = (int)(a.f[1] - a.f[0]);
+    int par = 0;
     bool zero = true;   // p = q = 0 before the first iteration (tv.py:198-201)
     double t_mom = 1.0;
     int iters = 0, restarts = 0, converged = 0;
@@ -296,7 +365,8 @@ __global__ void __launch_bounds__(kF2MaxThreads, 1) fgp2_rows_kernel(ProxArgs a)
         double t_next = 0.5 * (1.0 + sqrt(rn_add(1.0, rn_mul(rn_mul(4.0, t_mom), t_mom))));
         double beta = (t_mom - 1.0) / t_next;
         double vc[kF2K];
-        f2_pass(f, Q[0], Q[1], zero, P[0], P[1], zero, beta, C[0], C[1], Qn[0], Qn[1]);
+        const int iP = par ? 4 : 0, iC = par ? 0 : 4, iQ = par ? 6 : 2, iQn = par ? 2 : 6;
+        f2_pass(f, fb, fs, iQ, zero, iP, zero, beta, iC, iQn);
         f2_finish_sum<kF2K>(grid, f, a.red, round, a.ds, vc);
         double phi = vc[0];
         if (phi > phi_prev) {  // restart from the last accepted point (tv.py:217-231)
@@ -304,14 +374,11 @@ __global__ void __launch_bounds__(kF2MaxThreads, 1) fgp2_rows_kernel(ProxArgs a)
             t_mom = 1.0;
             t_next = 0.5 * (1.0 + sqrt(rn_add(1.0, rn_mul(rn_mul(4.0, t_mom), t_mom))));
             beta = (t_mom - 1.0) / t_next;
-            f2_pass(f, P[0], P[1], zero, P[0], P[1], zero, beta, C[0], C[1], Qn[0], Qn[1]);
+            f2_pass(f, fb, fs, iP, zero, iP, zero, beta, iC, iQn);
             f2_finish_sum<kF2K>(grid, f, a.red, round, a.ds, vc);
             phi = vc[0];
         }
-        for (int k = 0; k < 2; ++k) {
-            double *t = P[k]; P[k] = C[k]; C[k] = t;    // p <- c
-            t = Q[k]; Q[k] = Qn[k]; Qn[k] = t;          // q <- q'
-        }
+        par ^= 1;       // p <- c, q <- q'
         zero = false;
         phi_prev = (phi_prev < phi) ? phi_prev : phi;  // Python min(phi, phi_prev)
         t_mom = t_next;
@@ -327,10 +394,10 @@ __global__ void __launch_bounds__(kF2MaxThreads, 1) fgp2_rows_kernel(ProxArgs a)
 
     // --- finalize: out = b + w div p (tv.py:250) into scratch, the primal energies
     //     ||out - b||^2 and TV(out) (tv.py:166-169) in numpy order
-    double *tmp = C[0];
+    double *tmp = fb + (par ? 0 : 4) * fs;   // c's first field: scratch once p is final
     double e2[2];
     {
-        const double *Pv = P[0], *Ph = P[1];
+        const double *Pv = fb + (par ? 4 : 0) * fs, *Ph = Pv + fs;
         Col2 oprev{0.0, 0.0};
         if (f.r0 > 0) {
             oprev.x = f2_out_at(f, Pv, Ph, f.r0 - 1, t0);
@@ -418,11 +485,13 @@ int f2_grid(int64_t H) { return (int)(H < kF2MaxCtas ? H : kF2MaxCtas); }
 bool fgp2_rows_supported(const ProxArgs &a) {
     auto pow2 = [](int64_t v) { return v > 0 && (v & (v - 1)) == 0; };
     if (a.D > 1 || !pow2(a.W) || !pow2(a.H) || a.W < 128 || a.W > 2 * kF2MaxThreads) return false;
-    if (a.H / f2_grid(a.H) > 128) return false;   // the CTA's leaf tree: Q / 2 <= threads
+    if ((a.H / f2_grid(a.H)) * (a.W / 128) > 512) return false;   // leaves per CTA (warp_pw_tree)
     if ((reinterpret_cast<uintptr_t>(a.b) & 15) || (a.out_img && (reinterpret_cast<uintptr_t>(a.out_img) & 15)))
         return false;
+    const int64_t fs = a.f[1] - a.f[0];
+    if (fs < a.N || (fs & 1) || (reinterpret_cast<uintptr_t>(a.f[0]) & 15) || a.N + 8 * fs > INT32_MAX) return false;
     for (int k = 0; k < 8; ++k)
-        if (reinterpret_cast<uintptr_t>(a.f[k]) & 15) return false;
+        if (a.f[k] != a.f[0] + k * fs) return false;   // one workspace, fixed field stride
     return true;
 }
 
