@@ -292,7 +292,7 @@ def run_ours(args):
                "k2_transposed_step": {"kernel": f"{op.kernel_info()['transposed']}, EpiStep (g = 2 A^T r, b = x + mu g)",
                                       "ms": round(ph["k2_step"], 4), "bytes": b2,
                                       "gbs": round(b2 / (ph["k2_step"] * 1e6), 1)},
-               "k3_tv_prox": {"kernel": "fgp_kernel<2> (cooperative, FGP decisions on device)",
+               "k3_tv_prox": {"kernel": "fgp2_rows_kernel (row walk, one grid barrier per FGP iteration)",
                               "ms": round(ph["prox"], 4), "mean_fgp_iterations": round(fgp_iters, 2)},
                "tail": {"ms": round(ph["tail"], 4)}}
     for k in kernels.values():
@@ -353,23 +353,36 @@ def run_ours(args):
     log(f"[bench] e2e host-state: {e2e_s * 1e3:.3f} ms/epoch")
     del st2
 
-    # ---- CPU baseline (oracle port) on a bounded sample of the same system ----
+    # ---- CPU baseline on a bounded sample of the same system: the reference package
+    #      itself (baseline/_ref) when installed, and the oracle port beside it ----
     cpu = None
     if not args.no_cpu:
         t0 = time.time()
         csr = op.tocsr()
+        op._csr = None
         log(f"[bench] host CSR copy {time.time() - t0:.1f}s")
         v, info = oracle_epochs(csr, d.y, 8, mu, d.lam, d.max_inner_iters, 1e-5, (d.height, d.width),
                                 warmup=1, steps=max(2, args.cpu_epochs), budget_s=args.cpu_budget)
-        cpu = {"value": round(v, 4), "unit": "epochs/s", "cores": info["cores"], "kind": "port",
-               "sample": f"{info['epochs_timed']} epochs ({info['seconds']} s) of the same configs[3] system "
-                         f"(same A, y, mu) after 1 warm-up epoch; oracle/ C restatement of scipy csr/csc_matvec + "
-                         f"numpy epilogue and prox, OpenMP over block pairs"}
-        log(f"[bench] cpu oracle: {v:.4f} epochs/s on {info['cores']} threads")
+        port = {"value": round(v, 4), "unit": "epochs/s", "cores": info["cores"], "kind": "port",
+                "sample": f"{info['epochs_timed']} epochs ({info['seconds']} s) of the same configs[3] system "
+                          f"(same A, y, mu) after 1 warm-up epoch; oracle/ C restatement of scipy csr/csc_matvec "
+                          f"+ numpy epilogue and prox, OpenMP over block pairs"}
+        log(f"[bench] cpu oracle port: {v:.4f} epochs/s on {info['cores']} threads")
+        ref = None if args.no_ref_baseline else reference_epochs(csr, d.y, mu, {
+            "height": d.height, "width": d.width, "lam": d.lam, "max_inner_iters": d.max_inner_iters},
+            workers=os.cpu_count() or 1, warmup=1, steps=max(2, args.cpu_epochs), budget=args.cpu_budget)
         del csr
-        op._csr = None
+        if ref is not None:
+            cpu = {"value": round(ref["value"], 4), "unit": "epochs/s", "cores": ref["workers"], "kind": "reference",
+                   "sample": f"{ref['epochs']} epochs ({ref['seconds']:.1f} s) of the same configs[3] system "
+                             f"(same A, y, mu) after 1 warm-up epoch through the reference package's own "
+                             f"bsgd_tv_iteration (baseline/_ref), ThreadPoolExecutor({ref['workers']}), monitor off",
+                   "host": host_info(), "port": port}
+            log(f"[bench] cpu reference: {ref['value']:.4f} epochs/s on {ref['workers']} threads")
+        else:
+            cpu = port
 
-    launches = 4  # K2 (gather-tiled A^T + step), prox (1 cooperative kernel), K1 lookahead, tail
+    launches = 4  # K2 (gather-tiled A^T + step), prox (1 cooperative row-walk kernel), K1 lookahead, tail
     secondary = None
     del st, runner, op, d
     torch.cuda.empty_cache()
@@ -604,63 +617,71 @@ def import_reference():
         return None
 
 
+def reference_epochs(csr, y, mu, meta, workers, warmup, steps, budget, op=None):
+    """Time the reference package's bsgd_tv_iteration (baseline/_ref, unmodified) on
+    the given system; None when baseline/_ref is not importable."""
+    import concurrent.futures as cf
+    if import_reference() is None:
+        return None
+    from bsgdtv import blockops as rb
+    from bsgdtv import solvers as rs
+    from bsgdtv import tv as rtv
+    t0 = time.time()
+    if op is None:
+        op = rb.BlockOperator(csr, rb.make_partition(csr.shape[0], csr.shape[1], 8, 8))
+    build_s = time.time() - t0
+    lay = rtv.PixelLayout(meta["height"], meta["width"], np.arange(meta["height"] * meta["width"]))
+    prox = rtv.ProxSettings(max_inner_iters=meta["max_inner_iters"], tol=1e-5)
+    cfg = rs.SolverConfig(mu=mu, lam=meta["lam"], prox=prox, monitor_decrease=False)
+    st = rs.init_bsgd_state(op, y, cfg)
+    with cf.ThreadPoolExecutor(workers) as ex:
+        exe = ex if workers > 1 else None
+        for _ in range(warmup):
+            rs.bsgd_tv_iteration(st, op, y, cfg, layout=lay, executor=exe)
+        times = []
+        t_start = time.perf_counter()
+        for _ in range(steps):
+            t1 = time.perf_counter()
+            rs.bsgd_tv_iteration(st, op, y, cfg, layout=lay, executor=exe)
+            times.append(time.perf_counter() - t1)
+            if time.perf_counter() - t_start > budget:
+                break
+    return {"value": len(times) / sum(times), "epochs": len(times), "seconds": sum(times), "workers": workers,
+            "build_s": build_s, "op": op}
+
+
 def run_reference(args):
     world, rank, _ = dist_info()
     if rank != 0:
         return
-    import concurrent.futures as cf
-
     csr, y, meta = reference_inputs()
     mu, u_max = mu_for(HEADLINE)
     nnz = int(csr.nnz)
     cores = os.cpu_count() or 1
-    ref = import_reference()
     variants = {}
-    if ref is not None:
-        from bsgdtv import blockops as rb
-        from bsgdtv import solvers as rs
-        from bsgdtv import tv as rtv
-        t0 = time.time()
-        op = rb.BlockOperator(csr, rb.make_partition(csr.shape[0], csr.shape[1], 8, 8))
+    res = reference_epochs(csr, y, mu, meta, workers=cores, warmup=min(args.warmup, 1), steps=args.steps,
+                           budget=args.ref_budget)
+    if res is not None:
         del csr
-        log(f"[ref] reference BlockOperator built in {time.time() - t0:.1f}s")
-        lay = rtv.PixelLayout(meta["height"], meta["width"], np.arange(meta["height"] * meta["width"]))
-        prox = rtv.ProxSettings(max_inner_iters=meta["max_inner_iters"], tol=1e-5)
-        cfg = rs.SolverConfig(mu=mu, lam=meta["lam"], prox=prox, monitor_decrease=False)
-
-        def timed(cfg_, workers, warm, steps, budget):
-            st = rs.init_bsgd_state(op, y, cfg_)
-            with cf.ThreadPoolExecutor(workers) as ex:
-                exe = ex if workers > 1 else None
-                for _ in range(warm):
-                    rs.bsgd_tv_iteration(st, op, y, cfg_, layout=lay, executor=exe)
-                times = []
-                t_start = time.perf_counter()
-                for _ in range(steps):
-                    t1 = time.perf_counter()
-                    rs.bsgd_tv_iteration(st, op, y, cfg_, layout=lay, executor=exe)
-                    times.append(time.perf_counter() - t1)
-                    if time.perf_counter() - t_start > budget:
-                        break
-            return len(times) / sum(times), len(times), sum(times)
-
-        v, n, secs = timed(cfg, cores, min(args.warmup, 1), args.steps, args.ref_budget)
+        v, n, secs = res["value"], res["epochs"], res["seconds"]
         kind, how = "reference", (f"the reference package (baseline/_ref bsgdtv, unmodified) bsgd_tv_iteration, "
                                   f"ThreadPoolExecutor({cores}), monitor off")
-        log(f"[ref] reference: {v:.4f} epochs/s ({n} epochs, {secs:.1f}s)")
+        log(f"[ref] reference: {v:.4f} epochs/s ({n} epochs, {secs:.1f}s; operator built in {res['build_s']:.1f}s)")
         if not args.no_variants:
-            v1, n1, _ = timed(cfg, 1, 0, 2, args.ref_budget / 3)
-            variants["workers_1_monitor_off"] = {"value": round(v1, 4), "epochs": n1}
-            cfg_def = rs.SolverConfig(mu=mu, lam=meta["lam"], prox=prox)  # monitor_decrease defaults to True
-            vm, nm, _ = timed(cfg_def, cores, 0, 2, args.ref_budget / 3)
-            variants[f"workers_{cores}_monitor_on"] = {"value": round(vm, 4), "epochs": nm}
+            from bsgdtv import solvers as rs
+            from bsgdtv import tv as rtv
+            op = res["op"]
+            r1 = reference_epochs(None, y, mu, meta, workers=1, warmup=0, steps=2, budget=args.ref_budget / 3, op=op)
+            variants["workers_1_monitor_off"] = {"value": round(r1["value"], 4), "epochs": r1["epochs"]}
+            lay = rtv.PixelLayout(meta["height"], meta["width"], np.arange(meta["height"] * meta["width"]))
+            prox = rtv.ProxSettings(max_inner_iters=meta["max_inner_iters"], tol=1e-5)
             # run_solver defaults: monitor on and an objective sample every epoch (sample_every = 1)
             t1 = time.perf_counter()
-            rs.run_solver("bsgd", rs.Problem(op, y, None, lay), rs.SolverConfig(mu=mu, lam=meta["lam"], prox=prox,
-                                                                               epochs=2), workers=cores)
-            variants[f"run_solver_defaults_workers_{cores}"] = {"value": round(2.0 / (time.perf_counter() - t1), 4),
-                                                               "epochs": 2,
-                                                               "note": "includes the initial objective sample"}
+            rs.run_solver("bsgd", rs.Problem(op, y, None, lay),
+                          rs.SolverConfig(mu=mu, lam=meta["lam"], prox=prox, epochs=2), workers=cores)
+            variants[f"run_solver_defaults_workers_{cores}"] = {
+                "value": round(2.0 / (time.perf_counter() - t1), 4), "epochs": 2,
+                "note": "monitor on, sample_every=1; includes the initial objective sample"}
             log(f"[ref] variants: {variants}")
     else:
         v, info = oracle_epochs(csr, y, 8, mu, meta["lam"], meta["max_inner_iters"], 1e-5,
@@ -703,6 +724,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-secondary", action="store_true", help="skip the configs[1], [2], [4] measurements")
     ap.add_argument("--no-variants", action="store_true", help="reference arm: skip the 1-worker / monitor variants")
+    ap.add_argument("--no-ref-baseline", action="store_true", help="cpu_baseline: the oracle port only")
     ap.add_argument("--cpu-epochs", type=int, default=8)
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--ref-budget", type=float, default=60.0)
