@@ -754,7 +754,7 @@ struct Ws {
     double *rpart;   // [kMaxPartials]
     double *red;     // [2 * kMaxPartials * kPwMaxK]
     double *uimg;    // [cols]
-    double *fields;  // [9 * n]: p, q, c for up to three axes
+    double *fields;  // [10 * n]: p, q, c for up to three axes, the split prox's u field
 };
 
 static size_t a256(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -777,7 +777,7 @@ static size_t ws_layout(void *base, int64_t cols, int64_t hw, Ws *ws) {
     char *red = take(sizeof(double) * 2 * kMaxPartials * kPwMaxK);
     (void)take(sizeof(double) * 96);  // keep uimg off the fields' alignment (see field_stride)
     char *uimg = take(sizeof(double) * (size_t)std::max<int64_t>(cols, 1));
-    char *fields = take(sizeof(double) * 9 * (size_t)(hw > 0 ? field_stride(hw) : 0));
+    char *fields = take(sizeof(double) * kProxFields * (size_t)(hw > 0 ? field_stride(hw) : 0));
     if (ws) {
         ws->ctl = (int64_t *)ctl; ws->scal = (double *)scal; ws->xpart = (double *)xpart;
         ws->rpart = (double *)rpart; ws->red = (double *)red; ws->uimg = (double *)uimg;
@@ -942,6 +942,12 @@ static void prox_warm() {
 // Split prox (slab.cuh): one kernel per FGP pass with the decisions on the
 // device, for volumes whose fields do not stay in L2.  A fixed launch sequence
 // (passes that do not apply return at once), so it is graph-capturable.
+// BSGD_PROX_CANDIDATE=fused: the one-pass 3-D candidate (experiments / tests)
+static int getenv_candidate_fused() {
+    const char *e = getenv("BSGD_PROX_CANDIDATE");
+    return (e && strcmp(e, "fused") == 0) ? 1 : 0;
+}
+
 template <int DIM>
 static int launch_prox_split(const ProxArgs &a, cudaStream_t st) {
     split_attrs<DIM>();
@@ -985,14 +991,26 @@ static int launch_prox_split(const ProxArgs &a, cudaStream_t st) {
     v.when = 0;
     sums2(false);
     split_decide_kernel<DIM, 2><<<1, kThreads, 0, st>>>(v, 0, 0, part);
+    // candidate as two passes through the u field (f[kProxFields - 1]) for volumes:
+    // 256^3 candidate 0.55-0.65 ms fused (issue-bound) -> u + c passes
+    const bool two_pass = DIM == 3 && getenv_candidate_fused() == 0;
+    double *ufield = a.f[kProxFields - 1];
+    auto candidate = [&](int from_p) {
+        if (two_pass) {
+            slab_u_kernel<DIM><<<grid, kThreads, 0, st>>>(v, from_p, ufield);
+            slab_cand_u_kernel<DIM><<<grid, kThreads, 0, st>>>(v, from_p, ufield);
+        } else {
+            slab_candidate_kernel<DIM><<<grid, kThreads, 0, st>>>(v, from_p);
+        }
+    };
     for (int it = 0; it < a.max_iters; ++it) {
         v.zero = it == 0 ? 1 : 0;
         v.when = 1;  // unless converged
-        slab_candidate_kernel<DIM><<<grid, kThreads, 0, st>>>(v, 0);
+        candidate(0);
         dual();
         split_decide_kernel<DIM, KD><<<1, kThreads, 0, st>>>(v, 1, it, part);
         v.when = 2;  // only on a restart
-        slab_candidate_kernel<DIM><<<grid, kThreads, 0, st>>>(v, 1);
+        candidate(1);
         dual();
         split_decide_kernel<DIM, KD><<<1, kThreads, 0, st>>>(v, 2, it, part);
     }
@@ -1060,7 +1078,7 @@ static int launch_prox(ProxArgs &a, cudaStream_t st) {
 }
 
 static void prox_fields(ProxArgs &a, const Ws &ws, int64_t n) {
-    for (int k = 0; k < 9; ++k) a.f[k] = ws.fields + (size_t)k * field_stride(n);
+    for (int k = 0; k < kProxFields; ++k) a.f[k] = ws.fields + (size_t)k * field_stride(n);
     a.red = ws.red;
 }
 

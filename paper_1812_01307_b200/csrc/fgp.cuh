@@ -94,14 +94,19 @@ __device__ __forceinline__ double u_at(const ProxArgs &a, const double *const *q
 }
 
 // c / max(|c|, 1) (tv.py:211-214)
+// Inside the unit ball (m2 < 1) sqrt(m2) <= 1, so the divisor is exactly 1.0 and
+// c / 1.0 == c bit for bit: the sqrt and the divisions run only where the
+// projection is active (NaN takes the division path, as np.maximum propagates it).
 template <int DIM>
 __device__ __forceinline__ void project_unit(double (&c)[DIM]) {
     double m2 = rn_add(rn_mul(c[0], c[0]), rn_mul(c[1], c[1]));
     if constexpr (DIM == 3) m2 = rn_add(m2, rn_mul(c[2], c[2]));
-    double mag = sqrt(m2);
-    mag = (mag < 1.0) ? 1.0 : mag;  // np.maximum(mag, 1): NaN propagates
+    if (!(m2 < 1.0)) {
+        double mag = sqrt(m2);
+        mag = (mag < 1.0) ? 1.0 : mag;  // np.maximum(mag, 1): NaN propagates
 #pragma unroll
-    for (int k = 0; k < DIM; ++k) c[k] = c[k] / mag;
+        for (int k = 0; k < DIM; ++k) c[k] = c[k] / mag;
+    }
 }
 
 // projected gradient candidate from q at voxel p (tv.py:207-214; 3D: same with three fields)

@@ -6,10 +6,12 @@
 
 namespace bsgd {
 
+constexpr int kProxFields = 10;   // workspace fields of the prox (fgp.cuh, fgp2.cu, slab.cuh)
+
 struct ProxArgs {
     int64_t D, H, W, N;    // D = 1 for images; 3D volumes are z-major (z, row, column)
     const double *b;       // input image (row-major)
-    double *f[9];          // p[DIM], q[DIM], c[DIM] (workspace); 2D: pv, ph, qv, qh, cv, ch
+    double *f[kProxFields]; // p[DIM], q[DIM], c[DIM], u (workspace); 2D: pv, ph, qv, qh, cv, ch (+ q' for fgp2)
     double *red;           // [2][kMaxPartials * kPwMaxK] reduction partials
     double w, step, tol;
     int32_t max_iters;

@@ -157,6 +157,58 @@ __global__ void __launch_bounds__(kThreads) slab_candidate_kernel(SlabView s, in
     }
 }
 
+// The candidate as two passes over a stored u field (split prox of one GPU,
+// where u's neighbours are not rewritten by another rank): u = b + w div src once
+// per voxel, then c = proj(src + step grad u) from u and its three backward
+// neighbours.  The fused candidate evaluates u four times per voxel (~590
+// instructions, issue-bound); the same operations in the same order, so c is
+// bit-identical to slab_candidate_kernel's.
+template <int DIM>
+__global__ void __launch_bounds__(kThreads) slab_u_kernel(SlabView s, int from_p, double *u) {
+    if (slab_skip(s)) return;
+    const SlabRoles<DIM> r = slab_roles<DIM>(s);
+    const double *src[DIM];
+#pragma unroll
+    for (int k = 0; k < DIM; ++k) src[k] = from_p ? r.P[k] : r.Q[k];
+    const double wz = rn_mul(s.a.w, 0.0);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < s.n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t p = s.off + i;
+        if (s.zero) {
+            u[p] = rn_add(__ldg(s.a.b + p), wz);
+        } else {
+            int64_t z, y, t;
+            split_index<DIM>(p, s.a.H, s.a.W, z, y, t);
+            u[p] = u_at<DIM>(s.a, src, z, y, t);
+        }
+    }
+}
+
+template <int DIM>
+__global__ void __launch_bounds__(kThreads) slab_cand_u_kernel(SlabView s, int from_p, const double *u) {
+    if (slab_skip(s)) return;
+    const SlabRoles<DIM> r = slab_roles<DIM>(s);
+    const double *src[DIM];
+#pragma unroll
+    for (int k = 0; k < DIM; ++k) src[k] = from_p ? r.P[k] : r.Q[k];
+    const int64_t H = s.a.H, W = s.a.W;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < s.n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t p = s.off + i;
+        int64_t z, y, t;
+        split_index<DIM>(p, H, W, z, y, t);
+        const double uc = u[p];
+        double g[DIM];
+        if constexpr (DIM == 3) g[0] = (z > 0) ? rn_sub(uc, u[p - H * W]) : 0.0;
+        g[DIM - 2] = (y > 0) ? rn_sub(uc, u[p - W]) : 0.0;
+        g[DIM - 1] = (t > 0) ? rn_sub(uc, u[p - 1]) : 0.0;
+        double c[DIM];
+#pragma unroll
+        for (int k = 0; k < DIM; ++k) c[k] = rn_add(s.zero ? 0.0 : src[k][p], rn_mul(s.a.step, g[k]));
+        project_unit<DIM>(c);
+#pragma unroll
+        for (int k = 0; k < DIM; ++k) r.C[k][p] = c[k];
+    }
+}
+
 // dual value of c and the speculative momentum commit q = c + beta (c - p)
 // (tv.py:215-216, 233-245): 1 + 2 DIM sums.  beta from the control block when set.
 // 4 CTAs per SM (60 registers, no spills): the 512 CTAs of a 256^3 pass are

@@ -228,7 +228,7 @@ def test_world1_driver_slab_prox_matches_replicated(cuda_ok):
 
 
 SPLIT_CASES = [((1, 64, 48), 0.3, 30, 1e-6), ((1, 128, 128), 2.0, 20, 1e-12), ((16, 12, 10), 0.4, 20, 1e-6),
-               ((32, 32, 32), 0.05, 40, 1e-12), ((8, 8, 8), 1.0, 40, 1e-12)]
+               ((32, 32, 32), 0.05, 40, 1e-12), ((8, 8, 8), 1.0, 40, 1e-12), ((64, 128, 128), 0.05, 10, 1e-300)]
 
 
 @pytest.mark.parametrize("dims,w,iters,tol", SPLIT_CASES)
