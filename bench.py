@@ -227,7 +227,7 @@ def run_ours(args):
     from paper_1812_01307_b200 import problems, solvers, tv
 
     world, rank, local = dist_info()
-    if world > 1:
+    if world > 1 or args.force_dist:
         return run_multi(args)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -745,6 +745,8 @@ def main():
     ap.add_argument("--no-secondary", action="store_true", help="skip the configs[1], [2], [4] measurements")
     ap.add_argument("--no-variants", action="store_true", help="reference arm: skip the 1-worker / monitor variants")
     ap.add_argument("--no-ref-baseline", action="store_true", help="cpu_baseline: the oracle port only")
+    ap.add_argument("--force-dist", action="store_true",
+                    help="run the multi-GPU (row-slab, NCCL) arm even at world size 1 (under torchrun)")
     ap.add_argument("--cpu-epochs", type=int, default=8)
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--ref-budget", type=float, default=60.0)

@@ -193,6 +193,8 @@ def require_cuda(device=None):
     if not t.cuda.is_available():
         raise RuntimeError("paper_1812_01307_b200 needs a CUDA device (B200); none is visible")
     load()
+    if isinstance(device, t.device):
+        return t.device("cuda", device.index if device.index is not None else t.cuda.current_device())
     return t.device("cuda", t.cuda.current_device() if device is None else device)
 
 

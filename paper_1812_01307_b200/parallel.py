@@ -178,6 +178,11 @@ class CudaShard:
         self.ws = t.zeros((nbytes + 7) // 8, dtype=t.float64, device=self.dev)
         self.hw = hw
 
+    @property
+    def shape(self):
+        """Global (rows, cols) of the sharded operator (`Problem` validation)."""
+        return (self.spec.partition.rows, self.cols)
+
     # tensors
     def zeros(self, n):
         return self.t.zeros(n, dtype=self.t.float64, device=self.dev)
@@ -307,7 +312,12 @@ class DistributedBSGD:
         self.y = shard.vector(y_full[r0:r1])
         self.x = [shard.zeros(shard.cols), shard.zeros(shard.cols)]
         self.r = [self.y.clone(), self.y.clone()]   # r_0 = y and its lookahead y - A 0
-        self.g = shard.zeros(shard.cols)
+        # g and, in its last slot, this rank's ||r||^2 of the previous epoch: one
+        # all-reduce per epoch carries both (the previous epoch's tail runs after it)
+        self._gbuf = shard.zeros(shard.cols + 1)
+        self.g = self._gbuf[:shard.cols]
+        self._fslot = self._gbuf[shard.cols:]
+        self._pending = None        # args of the epoch whose tail waits for the next all-reduce
         self.xi = 0
         self.ri = 0
         self.mu = cfg.mu
@@ -396,7 +406,7 @@ class DistributedBSGD:
         collectives warmed up by at least one eager epoch; not available with
         the slab prox (its FGP decisions are taken on the host).  Returns
         whether a graph is ready."""
-        if self.slab is not None or epochs < 2 or epochs % 2:
+        if self.slab is not None or epochs < 2 or epochs % 2 or not getattr(self.y, "is_cuda", False):
             return False
         t = self.s.t
         saved = (self.xi, self.ri, self.rows_used, self.epoch)
@@ -414,12 +424,18 @@ class DistributedBSGD:
             self.xi, self.ri, self.rows_used, self.epoch = saved
         self._graph = g
         self._graph_epochs = epochs
+        self._graph_parity = saved[:2]
         return True
 
     def replay(self):
         """Run the captured epochs (same arithmetic as `epoch_step`, one launch).
         When the history table is full it is grown and the graph re-captured."""
-        if self._ensure_history(self._graph_epochs) or self._graph is None:
+        if self.slab is None and self._pending is None:
+            raise RuntimeError("the graph starts with the previous epoch's tail, which flush() / history() "
+                               "already ran: take one eager epoch_step() before replaying")
+        # the graph holds the x / r ring buffers of the parity it was captured at
+        stale = self._graph is not None and (self.xi, self.ri) != self._graph_parity
+        if self._ensure_history(self._graph_epochs) or self._graph is None or stale:
             k = self._graph_epochs
             if not self.capture(k):
                 raise RuntimeError("CUDA graph re-capture failed after growing the history table")
@@ -442,14 +458,22 @@ class DistributedBSGD:
                       self.x_true, flags)
         s.grad(r_k, self.g)                       # local 2 A_p^T r_p
         if self.slab is None:
-            self._allreduce(self.g)               # g = sum_p
+            # one collective per epoch: [g | ||r_prev||^2] summed over the ranks, then
+            # the previous epoch's tail (Eq. 9 test, f_curr, history row) -- it reads
+            # only the statistics of its own step, which this epoch's step overwrites next
+            self._allreduce(self._gbuf)
+            if self._pending is not None:
+                s.tail(self._pending, self._fslot)
             s.step(args)                          # x_next = prox(x_k + mu g), stats
+            s.forward(x_next, self.y, r_ahead, args)  # r_{k+2}[I_p] into the consumed r_k slot
+            s.forward_sumsq(args, self._fslot)    # this rank's ||r||^2, reduced with the next g
+            self._pending = args
         else:
             self._slab_step(args, x_k, x_next)
-        s.forward(x_next, self.y, r_ahead, args)  # r_{k+2}[I_p] into the consumed r_k slot
-        s.forward_sumsq(args, self.fnext)
-        self._allreduce(self.fnext)               # f_next = sum_p ||r_p||^2
-        s.tail(args, self.fnext)
+            s.forward(x_next, self.y, r_ahead, args)
+            s.forward_sumsq(args, self.fnext)
+            self._allreduce(self.fnext)           # f_next = sum_p ||r_p||^2
+            s.tail(args, self.fnext)
         row = self.rows_used
         self.rows_used += 1
         self.xi, self.ri = 1 - xi, 1 - ri
@@ -477,8 +501,131 @@ class DistributedBSGD:
     def r_current(self):
         return self.r[self.ri]
 
+    def flush(self):
+        """Run the tail still waiting for the next epoch's all-reduce (history rows,
+        f_curr and the Eq. 9 flag of the last epoch become current)."""
+        if self._pending is not None:
+            self._allreduce(self._fslot)
+            self.s.tail(self._pending, self._fslot)
+            self._pending = None
+
     def history(self):
+        self.flush()
         return self.hist[: self.rows_used].cpu().numpy()
+
+
+def run_solver_distributed(problem, cfg, sample_every: int = 1, group=None, *, use_graphs: bool = True,
+                           chunk_epochs: int = 64, prox: str = "auto"):
+    """`run_solver('bsgd', ...)` (`solvers.py:445-533`) over a process group: every
+    rank passes a `Problem` whose ``op`` is its shard (`CudaShard`) and whose y,
+    x_true and layout are the full ones.  Samples (epoch, relative error,
+    objective, matvec units), decrease flags and the `DivergenceError` follow
+    the single-GPU `solvers.run_solver` exactly; the units are charged against
+    the global nonzero count.  alpha = gamma = 1 and no enforce_decrease (see
+    `DistributedBSGD`)."""
+    import torch.distributed as dist
+
+    from .solvers import ConvergenceTrace, DivergenceError, TraceSample
+    if sample_every < 1:
+        raise ValueError("sample_every must be >= 1")
+    shard = problem.op
+    lam = cfg.lam
+    if lam > 0 and problem.layout is None:
+        raise ValueError("problem layout required when lam > 0")
+    if lam > 0 and shard.layout is None:
+        raise ValueError("the shard was built without the pixel layout the prox needs")
+    epochs = int(math.ceil(cfg.epochs - 1e-9))
+    xt_norm = None
+    if problem.x_true is not None:
+        xt = problem.x_true
+        xt_host = xt.detach().cpu().numpy() if hasattr(xt, "detach") else np.asarray(xt, dtype=np.float64)
+        xt_norm = float(np.linalg.norm(xt_host))
+        if xt_norm == 0.0:
+            raise ValueError("reference vector is zero; relative error undefined")
+    drv = DistributedBSGD(shard, problem.y, cfg, x_true=problem.x_true, group=group,
+                          history_capacity=epochs + 8, prox=prox)
+    nnz = shard.zeros(1)
+    nnz.fill_(float(shard.op.nnz))
+    drv._allreduce(nnz)
+    nnz_total = int(round(float(nnz.item())))
+    monitor = cfg.monitor_decrease or cfg.enforce_decrease
+    trace = ConvergenceTrace()
+    applied = 0                                   # nonzeros charged since the start (integer, as the reference)
+
+    def units():
+        return applied / nnz_total
+
+    trace.append(TraceSample(0.0, 1.0 if xt_norm is not None else float("nan"), float(drv.f_curr.item()), units()))
+    applied += nnz_total                          # the sample's objective evaluation is charged
+    pending = []                                  # (history row, epoch, sampled, units at the sample)
+    next_sample = float(sample_every)
+    done = 0
+
+    def book(ep):
+        nonlocal applied, next_sample
+        applied += 2 * nnz_total                  # one A^T and one A product per full sweep
+        sampled = ep >= next_sample - 1e-9
+        u = None
+        if sampled:
+            u = units()
+            applied += nnz_total
+            next_sample = (math.floor(ep / sample_every + 1e-9) + 1) * sample_every
+        pending.append((int(round(ep)) - 1, ep, sampled, u))   # history row of epoch ep (rows from 0)
+
+    def drain():
+        hist = drv.history()
+        for row, ep, sampled, u in pending:
+            h = hist[row]
+            norm = math.sqrt(h[nat.H_XX]) if h[nat.H_XX] >= 0 else float("nan")
+            if monitor:
+                trace.decrease_flags.append(bool(h[nat.H_HOLDS] > 0.5))
+            if not math.isfinite(norm) or norm > cfg.divergence_limit:
+                trace.final_x = None
+                pending.clear()
+                return DivergenceError(f"iterate norm {norm:.3e} left the admissible region at epoch {ep:.6g}",
+                                       trace)
+            if sampled:
+                rel = math.sqrt(max(h[nat.H_XE], 0.0)) / xt_norm if xt_norm is not None else float("nan")
+                obj = float(h[nat.H_FNEXT])
+                if lam > 0:
+                    obj += 2.0 * lam * float(h[nat.H_TV])
+                trace.append(TraceSample(ep, rel, obj, u))
+        pending.clear()
+        return None
+
+    graphed = False
+    while done < epochs:
+        if use_graphs and drv.slab is None and done >= 1 and epochs - done >= 2:
+            if not graphed:
+                graphed = drv.capture(2)
+                if not graphed:
+                    use_graphs = False
+                    continue
+            if drv._pending is None:              # flushed by the last drain: two eager epochs first
+                for _ in range(2):                # (an even count keeps the captured ring parity)
+                    drv.epoch_step()
+                    done += 1
+                    book(float(done))
+                continue
+            drv.replay()
+            for _ in range(2):
+                done += 1
+                book(float(done))
+        else:
+            drv.epoch_step()
+            done += 1
+            book(float(done))
+        if len(pending) >= chunk_epochs or done >= epochs:
+            err = drain()
+            if err is not None:
+                raise err
+    err = drain()
+    if err is not None:
+        raise err
+    trace.final_x = drv.x_current.cpu().numpy().copy()
+    if dist.is_initialized():
+        dist.barrier(group=group)
+    return trace
 
 
 def distributed_largest_eigenvalue(shard, max_iters=50, tol=1e-10, seed=0, group=None):

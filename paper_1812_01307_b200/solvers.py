@@ -715,13 +715,20 @@ class _GraphRunner:
 
 
 def run_solver(kind: str, problem: Problem, cfg: SolverConfig, sample_every: int = 1, workers: int = 1,
-               *, use_graphs: bool = True, chunk_epochs: int = 64) -> ConvergenceTrace:
+               *, use_graphs: bool = True, chunk_epochs: int = 64, group=None) -> ConvergenceTrace:
     """Drive the solver to the epoch budget, sampling the trace (`solvers.py:445-533`).
 
     Samples, decrease flags, divergence checks and matvec units follow the
     reference exactly; per-epoch quantities are produced on the device and
     read back once per chunk of ``chunk_epochs`` epochs (no per-epoch host
-    synchronisation).  ``workers`` is validated and otherwise unused.
+    synchronisation).  ``workers`` is validated and otherwise unused (the
+    products already use the whole GPU).
+
+    Multi-GPU (one process per GPU): pass ``group`` (a torch.distributed process
+    group, or "default" for the world group) and a `Problem` whose ``op`` is this
+    rank's `parallel.CudaShard`; the run is `parallel.run_solver_distributed`
+    (row slabs, one NCCL all-reduce per epoch) and returns the same trace on
+    every rank.  A plain BlockOperator with a group of more than one rank raises.
     """
     if kind not in SOLVER_KINDS:
         raise ValueError(f"unknown solver kind {kind!r}; expected one of {SOLVER_KINDS}")
@@ -732,6 +739,16 @@ def run_solver(kind: str, problem: Problem, cfg: SolverConfig, sample_every: int
     if kind != "bsgd":
         raise NotImplementedError(
             f"solver kind {kind!r} is a reference baseline outside this drop-in's scope (SURVEY.md §2 #13)")
+    if group is not None:
+        from . import parallel
+        grp = None if group == "default" else group
+        if isinstance(problem.op, BlockOperator):
+            import torch.distributed as dist
+            if dist.is_initialized() and dist.get_world_size(grp) > 1:
+                raise ValueError("multi-GPU run_solver needs this rank's shard (parallel.CudaShard) as problem.op")
+        else:
+            return parallel.run_solver_distributed(problem, cfg, sample_every, grp, use_graphs=use_graphs,
+                                                   chunk_epochs=chunk_epochs)
     op = problem.op
     lam = cfg.lam
     if lam > 0 and problem.layout is None:

@@ -13,6 +13,7 @@ import pytest
 
 from conftest import golden_cfg, golden_csr, load_golden
 from oracle import oracle as orc
+from paper_1812_01307_b200.blockops import make_partition
 
 pytestmark = pytest.mark.gpu
 
@@ -234,3 +235,69 @@ def test_stacked_shards_with_tiles_match_plain(cuda_ok, world):
         b = tiled.op.matvec(x, charge=False)
         assert np.array_equal(a, b)
         assert np.array_equal(plain.op.rmatvec(w, charge=False), tiled.op.rmatvec(w, charge=False))
+
+
+def test_run_solver_group_world1_nccl_matches_single_gpu(cuda_ok):
+    """run_solver(..., group=...) with a CudaShard over a world-1 NCCL group (graph
+    replay with the all-reduce inside, lagged tail) gives the single-GPU
+    run_solver's trace: samples, exact units, flags; x bit for bit."""
+    import torch
+    import torch.distributed as dist
+    from paper_1812_01307_b200 import blockops, parallel, solvers
+    z = load_golden("p3_ls")
+    c = golden_cfg(z)
+    a = golden_csr(z)
+    m, n = (int(v) for v in z["mn"])
+    part = make_partition(a.shape[0], a.shape[1], m, n)
+    cfg = solvers.SolverConfig(mu=c["mu"], lam=0.0, epochs=23)
+    single = solvers.run_solver("bsgd", solvers.Problem(blockops.BlockOperator(a, part), z["y"], z["x_true"]), cfg,
+                                sample_every=4)
+    dist.init_process_group("nccl", store=dist.HashStore(), rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        shard = parallel.CudaShard(a, parallel.ShardSpec(part, 0, 1))
+        tr = solvers.run_solver("bsgd", solvers.Problem(shard, z["y"], z["x_true"]), cfg, sample_every=4,
+                                group="default", chunk_epochs=8)
+    finally:
+        dist.destroy_process_group()
+    got, want = np.array([tuple(s) for s in tr.samples]), np.array([tuple(s) for s in single.samples])
+    assert np.array_equal(got[:, 0], want[:, 0]) and np.array_equal(got[:, 3], want[:, 3])
+    assert np.allclose(got[:, 1:3], want[:, 1:3], rtol=1e-12)
+    assert list(tr.decrease_flags) == list(single.decrease_flags)
+    assert np.array_equal(tr.final_x, single.final_x)
+
+
+def test_ct_row_slab_shard_world1_matches_single_operator(cuda_ok):
+    """The device-generated row-slab shard of configs[2] at world size 1 is the
+    single-GPU operator: same kernels, products and y bit for bit."""
+    from paper_1812_01307_b200 import parallel, problems
+    shard, y, meta = parallel.ct_row_slab_shard(2, 0, 1)
+    d = problems.config_device(2)
+    assert shard.op.kernel_info() == d.op.kernel_info()
+    assert np.array_equal(y, d.y)
+    rng = np.random.default_rng(2)
+    x = rng.random(d.op.shape[1])
+    w = rng.standard_normal(d.op.shape[0])
+    assert np.array_equal(shard.op.matvec(x, charge=False), d.op.matvec(x, charge=False))
+    assert np.array_equal(shard.op.rmatvec(w, charge=False), d.op.rmatvec(w, charge=False))
+
+
+def test_ct_row_slab_shards_cover_the_operator(cuda_ok):
+    """configs[2] split over 4 emulated ranks (whole angles each): the shards'
+    rows stack to the full operator's products bit for bit, and the local
+    transposed products sum to A^T w."""
+    from paper_1812_01307_b200 import parallel, problems
+    d = problems.config_device(2)
+    name, n, ang, nb, ell, noise, blocks, lam, inner, epochs, dt = problems.CT_TABLE[2]
+    part = make_partition(ang * nb, n * n, blocks, blocks)
+    rng = np.random.default_rng(3)
+    x = rng.random(n * n)
+    w = rng.standard_normal(ang * nb)
+    full = d.op.matvec(x, charge=False)
+    acc = np.zeros(n * n)
+    for p in range(4):
+        spec = parallel.ShardSpec(part, p, 4)
+        sh = parallel.CudaShard.parallel_beam(n, ang, nb, spec, dtype=dt)
+        r0, r1 = spec.row_range
+        assert np.array_equal(sh.op.matvec(x, charge=False), full[r0:r1])
+        acc += sh.op.rmatvec(w[r0:r1], charge=False)
+    assert rel(acc, d.op.rmatvec(w, charge=False)) < 1e-12

@@ -35,6 +35,11 @@ class CpuShard:
         self.cols = full.shape[1]
         self.rows = r1 - r0
         self.layout = None
+        self.op = types.SimpleNamespace(nnz=int(self.a.nnz))
+
+    @property
+    def shape(self):
+        return (self.spec.partition.rows, self.cols)
 
     def zeros(self, n):
         return torch.zeros(n, dtype=torch.float64)
@@ -226,3 +231,62 @@ def test_world2_gloo_matches_single_process_oracle(tmp_path):
     hist = r0["hist"]
     assert [bool(h > 0.5) for h in hist[:, H.HOLDS]] == flags
     assert np.allclose(hist[:, H.FNEXT], fnext, rtol=1e-12)
+
+
+def _solver_worker(rank, world, port, outdir, epochs, mu_scale, sample_every):
+    import sys
+    sys.path.insert(0, REPO)
+    sys.path.insert(0, os.path.join(REPO, "tests"))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1812_01307_b200 import parallel, solvers
+    from paper_1812_01307_b200.blockops import make_partition
+    z = load_golden("p3_ls")
+    c = golden_cfg(z)
+    a = golden_csr(z)
+    m, n = (int(v) for v in z["mn"])
+    spec = parallel.ShardSpec(make_partition(a.shape[0], a.shape[1], m, n), rank, world)
+    shard = CpuShard(a, spec)
+    cfg = solvers.SolverConfig(mu=c["mu"] * mu_scale, lam=0.0, epochs=epochs)
+    out = {}
+    try:
+        tr = solvers.run_solver("bsgd", solvers.Problem(shard, z["y"], z["x_true"]), cfg, sample_every=sample_every,
+                                group="default")
+        out["x"] = tr.final_x
+    except solvers.DivergenceError as e:
+        tr = e.trace
+        out["diverged"] = np.array(str(e))
+    out["samples"] = np.array([tuple(s) for s in tr.samples])
+    out["flags"] = np.array(tr.decrease_flags)
+    np.savez(os.path.join(outdir, f"run{rank}.npz"), **out)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("epochs,mu_scale,sample_every", [(13, 1.0, 3), (400, 1.3 * 0.5 / 0.9, 25)])
+def test_world2_gloo_run_solver_matches_oracle(tmp_path, epochs, mu_scale, sample_every):
+    """run_solver(..., group=...) over two ranks (one all-reduce per epoch, lagged
+    tail): the trace -- epochs, relative errors, objectives, exact matvec units,
+    decrease flags -- and the final x match the oracle's run_bsgd; with a step
+    beyond the Theorem-1 bound both raise DivergenceError at the same epoch."""
+    from oracle import oracle as orc
+    port = _free_port()
+    mp.spawn(_solver_worker, args=(2, port, str(tmp_path), epochs, mu_scale, sample_every), nprocs=2, join=True)
+    r0, r1 = np.load(tmp_path / "run0.npz"), np.load(tmp_path / "run1.npz")
+    z = load_golden("p3_ls")
+    c = golden_cfg(z)
+    op = orc.OracleOperator(golden_csr(z), *(int(v) for v in z["mn"]))
+    prm = orc.Params(mu=c["mu"] * mu_scale, lam=0.0, epochs=epochs)
+    ref = orc.run_bsgd(op, z["y"], prm, x_true=z["x_true"], sample_every=sample_every)
+    want = np.array(ref.samples)
+    for r in (r0, r1):
+        got = r["samples"]
+        assert got.shape == want.shape
+        assert np.array_equal(got[:, 0], want[:, 0]) and np.array_equal(got[:, 3], want[:, 3])
+        assert np.allclose(got[:, 1:3], want[:, 1:3], rtol=1e-10)
+        assert list(r["flags"]) == list(ref.decrease_flags)
+        assert ("diverged" in r) == ref.diverged
+        if ref.diverged:
+            assert str(r["diverged"]).split(" at ")[1] == ref.message.split(" at ")[1]
+        else:
+            assert np.linalg.norm(r["x"] - ref.final_x) / np.linalg.norm(ref.final_x) < 1e-12
