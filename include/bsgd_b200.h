@@ -299,8 +299,10 @@ typedef struct bsgd_slab {
     int64_t depth, height, width; /* global volume; depth 1 for an image */
     int64_t offset, count;        /* own voxels, C order */
     double weight;                /* prox weight w > 0 (mu * lam) */
-    int32_t parity;               /* dual buffer (0 / 1) holding p; the other holds c */
-    int32_t reserved;
+    int32_t parity;               /* dual buffer (0 / 1) holding p; the other holds c (host decisions) */
+    int32_t flags;                /* 0: host decisions.  BSGD_SLAB_DEVICE | (when << 1): decisions in the
+                                     workspace's control block (bsgd_slab_decide); `when` = 0 always,
+                                     BSGD_SLAB_MAIN / BSGD_SLAB_RESTART for the FGP passes */
     void *workspace;              /* bsgd_slab_workspace_bytes, device */
     size_t workspace_bytes;
 } bsgd_slab;
@@ -330,6 +332,26 @@ int bsgd_slab_energy(const bsgd_slab *s, double *sums_out, void *stream);
  * |x - x*|^2, (x - x_k).g, |x - x_k|^2 over them (x_true may be NULL) */
 int bsgd_slab_output(const bsgd_slab *s, int32_t fell_back, double *x_next, const double *x_k, const double *g,
                      const double *x_true, double *stats_out, void *stream);
+/* --- device-decided slab prox (graph-capturable, no host round trip) ------
+ * With flags = BSGD_SLAB_DEVICE the FGP state (parity, beta, restart, done,
+ * iterations, fallback) lives in the slab workspace; passes read it and return
+ * at once when they do not apply, so the host issues a FIXED sequence per prox
+ * (max_inner_iters blocks of candidate / dual / decide, then the restart
+ * variants), collectives included.  The per-rank sums of a stage
+ * (init: 2, dual: 1 + 2*DIM, energy: 2) are all-gathered rank-major into
+ * `gathered` (device) and combined in numpy's recursion order by `program`
+ * (host postfix: op >= 0 pushes rank op's sums, -1 adds the top two;
+ * parallel.slab_program).  stage: 0 init, 1 main dual, 2 restart dual, 3 energy. */
+#define BSGD_SLAB_DEVICE 1
+#define BSGD_SLAB_MAIN 1
+#define BSGD_SLAB_RESTART 2
+int bsgd_slab_decide(const bsgd_slab *s, int32_t stage, int32_t iteration, const double *gathered, int32_t world,
+                     const int32_t *program, int32_t nprogram, double tol, void *stream);
+/* bsgd_epoch_set_step with the prox scalars taken from the control block */
+int bsgd_slab_set_step(const bsgd_slab *s, int64_t cols, const bsgd_epoch_args *args, const double *stats_dev,
+                       void *stream);
+/* host copy of the control block's ProxInfo (iterations, converged, restarts, fell_back) and TV; synchronises */
+int bsgd_slab_info(const bsgd_slab *s, int32_t *info_out, double *tv_out, void *stream);
 /* hand a distributed step's results to bsgd_epoch_tail: the all-reduced
  * statistics (device, 4 doubles) and the prox scalars */
 int bsgd_epoch_set_step(int64_t cols, const bsgd_epoch_args *args, const double *stats_dev, double tv,

@@ -37,12 +37,13 @@ class SlabArgs(ctypes.Structure):
     """bsgd_slab (include/bsgd_b200.h)."""
     _fields_ = [
         ("depth", c_i64), ("height", c_i64), ("width", c_i64), ("offset", c_i64), ("count", c_i64),
-        ("weight", ctypes.c_double), ("parity", ctypes.c_int32), ("reserved", ctypes.c_int32),
+        ("weight", ctypes.c_double), ("parity", ctypes.c_int32), ("flags", ctypes.c_int32),
         ("workspace", c_p), ("workspace_bytes", ctypes.c_size_t),
     ]
 
 
 SLAB_SLOTS = 12
+SLAB_DEVICE, SLAB_MAIN, SLAB_RESTART = 1, 1, 2
 
 
 class KernelInfo(ctypes.Structure):
@@ -124,6 +125,10 @@ _SIGS = {
     "bsgd_slab_finalize": (ctypes.c_int, [ctypes.POINTER(SlabArgs), c_p]),
     "bsgd_slab_energy": (ctypes.c_int, [ctypes.POINTER(SlabArgs), c_p, c_p]),
     "bsgd_slab_output": (ctypes.c_int, [ctypes.POINTER(SlabArgs), ctypes.c_int32, c_p, c_p, c_p, c_p, c_p, c_p]),
+    "bsgd_slab_decide": (ctypes.c_int, [ctypes.POINTER(SlabArgs), ctypes.c_int32, ctypes.c_int32, c_p,
+                                        ctypes.c_int32, c_p, ctypes.c_int32, ctypes.c_double, c_p]),
+    "bsgd_slab_set_step": (ctypes.c_int, [ctypes.POINTER(SlabArgs), c_i64, ctypes.POINTER(EpochArgs), c_p, c_p]),
+    "bsgd_slab_info": (ctypes.c_int, [ctypes.POINTER(SlabArgs), c_p, c_p, c_p]),
     "bsgd_epoch_set_step": (ctypes.c_int, [c_i64, ctypes.POINTER(EpochArgs), c_p, ctypes.c_double, ctypes.c_int32,
                                            ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, c_p]),
     "bsgd_discrete_gradient3": (ctypes.c_int, [c_i64, c_i64, c_i64, c_p, c_p, c_p, c_p, c_p]),

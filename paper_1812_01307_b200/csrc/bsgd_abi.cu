@@ -1359,6 +1359,8 @@ static int build_gtiles(bsgd_plan *p, bool tr, int64_t ntiles, const int64_t *tp
 // slab-decomposed prox (multi-GPU): workspace layout and launch helpers
 // ---------------------------------------------------------------------------
 constexpr int kSlabPartials = 8192;   // doubles: G <= 512 CTAs x K <= 7 sums, or G x 4 stats
+constexpr int kSlabCtlOffset = 32;     // FgpCtl of the device-decided slab prox, after the sums (16) and stats
+static_assert(sizeof(FgpCtl) <= 96 * sizeof(double), "control block must fit the slot's padding");
 
 static int64_t slab_halo(int64_t depth, int64_t height, int64_t width) {
     return depth > 1 ? height * width : width;
@@ -1425,6 +1427,10 @@ static int slab_ctx(const bsgd_slab *s, SlabCtx &c, bool need_weight = true) {
     c.v.when = 0;
     c.v.ctl = nullptr;
     c.v.zero = 0;
+    if (s->flags & BSGD_SLAB_DEVICE) {   // decisions in the workspace's control block
+        c.v.ctl = (FgpCtl *)(base + off[11] + kSlabCtlOffset);
+        c.v.when = (s->flags >> 1) & 3;
+    }
     c.v.u = at(10);
     c.v.off = s->offset;
     c.v.n = s->count;
@@ -2644,6 +2650,79 @@ __global__ void set_step_kernel(int64_t *ctl, double *xpart, double *scal, const
         ctl[0] = 1;
         scal[0] = tv; scal[1] = iters; scal[2] = restarts; scal[3] = conv; scal[4] = fell;
     }
+}
+
+__global__ void set_step_ctl_kernel(int64_t *ctl, double *xpart, double *scal, const double *stats, const FgpCtl *c) {
+    if (threadIdx.x == 0) {
+        for (int k = 0; k < 4; ++k) xpart[k] = stats[k];
+        ctl[0] = 1;
+        scal[0] = c->fell ? c->tv_b : c->tv_out;
+        scal[1] = c->iters; scal[2] = c->restarts; scal[3] = c->done; scal[4] = c->fell;
+    }
+}
+
+int bsgd_slab_decide(const bsgd_slab *s, int32_t stage, int32_t iteration, const double *gathered, int32_t world,
+                     const int32_t *program, int32_t nprogram, double tol, void *stream) {
+    SlabCtx c;
+    int rc = slab_ctx(s, c, stage == 0 || stage == 3 ? true : true);
+    if (rc) return rc;
+    if (!(s->flags & BSGD_SLAB_DEVICE)) return fail(BSGD_EINVAL, "bsgd_slab_decide needs BSGD_SLAB_DEVICE");
+    if (!gathered || !program) return fail(BSGD_EINVAL, "gathered and program are required");
+    if (world < 1 || world > kSlabRanks || nprogram < 1 || nprogram > kSlabProgram)
+        return fail(BSGD_EINVAL, "slab program: %d ranks, %d ops (at most %d ranks)", world, nprogram, kSlabRanks);
+    if (stage < 0 || stage > 3) return fail(BSGD_EINVAL, "stage must be 0..3");
+    SlabProgram prog = {};
+    prog.n = nprogram;
+    int depth = 0;
+    for (int i = 0; i < nprogram; ++i) {
+        if (program[i] >= world || program[i] < -1) return fail(BSGD_EINVAL, "bad slab program op %d", program[i]);
+        prog.op[i] = (int8_t)program[i];
+        depth += program[i] >= 0 ? 1 : -1;
+        if (depth < 1 || depth > kSlabRanks) return fail(BSGD_EINVAL, "slab program is not a valid postfix sum");
+    }
+    if (depth != 1) return fail(BSGD_EINVAL, "slab program leaves %d values", depth);
+    c.v.a.tol = tol;
+    cudaStream_t st = (cudaStream_t)stream;
+    const bool sum2 = stage == 0 || stage == 3;
+    if (c.dim == 3) {
+        if (sum2) slab_decide_kernel<3, 2><<<1, 32, 0, st>>>(c.v, stage, iteration, gathered, prog);
+        else slab_decide_kernel<3, 7><<<1, 32, 0, st>>>(c.v, stage, iteration, gathered, prog);
+    } else {
+        if (sum2) slab_decide_kernel<2, 2><<<1, 32, 0, st>>>(c.v, stage, iteration, gathered, prog);
+        else slab_decide_kernel<2, 5><<<1, 32, 0, st>>>(c.v, stage, iteration, gathered, prog);
+    }
+    LAUNCHED();
+    return BSGD_OK;
+}
+
+int bsgd_slab_set_step(const bsgd_slab *s, int64_t cols, const bsgd_epoch_args *a, const double *stats_dev,
+                       void *stream) {
+    SlabCtx c;
+    int rc = slab_ctx(s, c, false);
+    if (rc) return rc;
+    if (!(s->flags & BSGD_SLAB_DEVICE)) return fail(BSGD_EINVAL, "bsgd_slab_set_step needs BSGD_SLAB_DEVICE");
+    Ws ws;
+    rc = check_epoch_args(cols, a, &ws);
+    if (rc) return rc;
+    if (!stats_dev) return fail(BSGD_EINVAL, "stats_dev is NULL");
+    set_step_ctl_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(ws.ctl, ws.xpart, ws.scal, stats_dev, c.v.ctl);
+    LAUNCHED();
+    return BSGD_OK;
+}
+
+int bsgd_slab_info(const bsgd_slab *s, int32_t *info_out, double *tv_out, void *stream) {
+    SlabCtx c;
+    int rc = slab_ctx(s, c, false);
+    if (rc) return rc;
+    if (!(s->flags & BSGD_SLAB_DEVICE)) return fail(BSGD_EINVAL, "bsgd_slab_info needs BSGD_SLAB_DEVICE");
+    if (!info_out) return fail(BSGD_EINVAL, "info_out is NULL");
+    FgpCtl h;
+    cudaStream_t st = (cudaStream_t)stream;
+    CU(cudaMemcpyAsync(&h, c.v.ctl, sizeof(FgpCtl), cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    info_out[0] = h.iters; info_out[1] = h.done; info_out[2] = h.restarts; info_out[3] = h.fell;
+    if (tv_out) *tv_out = h.fell ? h.tv_b : h.tv_out;
+    return BSGD_OK;
 }
 
 int bsgd_epoch_set_step(int64_t cols, const bsgd_epoch_args *a, const double *stats_dev, double tv,

@@ -36,7 +36,7 @@ namespace bsgd {
 
 // device-side FGP state of the split prox (fgp_kernel's registers)
 struct FgpCtl {
-    double phi_prev, tv_b, t_mom, t_next, beta;
+    double phi_prev, tv_b, t_mom, t_next, beta, tv_out;
     int32_t iters, restarts, done, parity, restart, fell;
 };
 
@@ -262,6 +262,7 @@ __global__ void __launch_bounds__(kThreads) slab_output_kernel(SlabView s, int f
                                                                const double *g, const double *xtrue, double *part) {
     __shared__ double sm[4 * (kThreads / 32)];
     const SlabRoles<DIM> r = slab_roles<DIM>(s);
+    if (s.ctl != nullptr) fell = s.ctl->fell;   // device decisions
     double st[4] = {0.0, 0.0, 0.0, 0.0};
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < s.n; i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t p = s.off + i;
@@ -294,20 +295,14 @@ __device__ __forceinline__ void fgp_next_beta(FgpCtl &c) {
 
 // stage 0: after the setup sums; 1: after the candidate's dual pass; 2: after
 // the restart's dual pass; 3: after the energy sums (fallback decision, outputs).
-// The same scalar code as fgp_kernel.
-template <int DIM, int K>
-__global__ void __launch_bounds__(kThreads) split_decide_kernel(SlabView s, int stage, int it, const double *part) {
-    if (slab_skip(s)) return;
-    __shared__ double sm[kPwMaxQ * kPwMaxK];
-    double v[K];
-    pw_top<K>(s.ds, s.G, part, sm, v);
-    if (threadIdx.x != 0) return;
-    FgpCtl &c = *s.ctl;
-    const ProxArgs &a = s.a;
+// The same scalar code as fgp_kernel; v = the stage's global numpy-order sums.
+template <int DIM>
+__device__ __forceinline__ void fgp_decide(FgpCtl &c, const ProxArgs &a, int stage, int it, const double *v) {
     if (stage == 0) {
         c.phi_prev = v[0];
         c.tv_b = v[1];
         c.t_mom = 1.0;
+        c.tv_out = 0.0;
         c.iters = c.restarts = c.done = c.parity = c.restart = c.fell = 0;
         fgp_next_beta(c);
         if (a.dual != nullptr) a.dual[0] = c.phi_prev;
@@ -318,6 +313,7 @@ __global__ void __launch_bounds__(kThreads) split_decide_kernel(SlabView s, int 
         const double obj_out = rn_add(v[0], rn_mul(two_w, v[1]));
         const double obj_b = rn_add(0.0, rn_mul(two_w, c.tv_b));
         c.fell = obj_out > obj_b ? 1 : 0;
+        c.tv_out = v[1];
         if (a.scal != nullptr) {
             a.scal[0] = c.fell ? c.tv_b : v[1];
             a.scal[1] = c.iters; a.scal[2] = c.restarts; a.scal[3] = c.done; a.scal[4] = c.fell;
@@ -347,6 +343,49 @@ __global__ void __launch_bounds__(kThreads) split_decide_kernel(SlabView s, int 
     const double floor_scale = (1e-30 > scale) ? 1e-30 : scale;
     if (change <= a.tol * floor_scale) c.done = 1;
     else fgp_next_beta(c);
+}
+
+template <int DIM, int K>
+__global__ void __launch_bounds__(kThreads) split_decide_kernel(SlabView s, int stage, int it, const double *part) {
+    if (slab_skip(s)) return;
+    __shared__ double sm[kPwMaxQ * kPwMaxK];
+    double v[K];
+    pw_top<K>(s.ds, s.G, part, sm, v);
+    if (threadIdx.x != 0) return;
+    fgp_decide<DIM>(*s.ctl, s.a, stage, it, v);
+}
+
+// Multi-GPU slab prox with the decisions on the device (graph-capturable): the
+// ranks' slab sums, all-gathered rank-major into `gathered` (world x K), are
+// combined in numpy's recursion order by a postfix program computed once on the
+// host from the slab nodes (parallel.slab_program: op >= 0 pushes rank op's
+// sums, -1 adds the top two), then the same decision code runs on every rank.
+constexpr int kSlabRanks = 16;
+constexpr int kSlabProgram = 2 * kSlabRanks;
+struct SlabProgram {
+    int32_t n;
+    int8_t op[kSlabProgram];
+};
+
+template <int DIM, int K>
+__global__ void __launch_bounds__(32) slab_decide_kernel(SlabView s, int stage, int it, const double *gathered,
+                                                         SlabProgram prog) {
+    if (slab_skip(s) || threadIdx.x != 0) return;
+    double stk[kSlabRanks][K];
+    int sp = 0;
+    for (int i = 0; i < prog.n; ++i) {
+        const int o = prog.op[i];
+        if (o >= 0) {
+#pragma unroll
+            for (int k = 0; k < K; ++k) stk[sp][k] = gathered[o * K + k];
+            ++sp;
+        } else {
+            --sp;
+#pragma unroll
+            for (int k = 0; k < K; ++k) stk[sp - 1][k] = rn_add(stk[sp - 1][k], stk[sp][k]);
+        }
+    }
+    fgp_decide<DIM>(*s.ctl, s.a, stage, it, stk[0]);
 }
 
 // outputs of the split prox: the image (standalone) or x_next in vector order

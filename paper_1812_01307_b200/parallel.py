@@ -290,12 +290,17 @@ class DistributedBSGD:
     same layout as the single-GPU path (`BSGD_H_*`), replicated on every rank.
     """
 
-    def __init__(self, shard, y_full, cfg, x_true=None, group=None, history_capacity=1024, prox: str = "auto"):
+    def __init__(self, shard, y_full, cfg, x_true=None, group=None, history_capacity=1024, prox: str = "auto",
+                 device_decisions: bool = True):
         """``prox``: "replicated" runs the whole prox on every rank (bsgd_step);
         "slab" decomposes it over the ranks (SlabProx; needs an identity layout
         and slabs at least one halo plane thick); "auto" takes "slab" on more
         than one rank when it applies and the volume has at least
-        SLAB_PROX_MIN_VOXELS voxels (configs[4]'s 256^3), "replicated" otherwise."""
+        SLAB_PROX_MIN_VOXELS voxels (configs[4]'s 256^3), "replicated" otherwise.
+        ``device_decisions``: the slab prox takes its FGP decisions on the device
+        (`SlabProx.run_device`, a fixed sequence with no host round trip, so the
+        epoch can be captured in a CUDA graph) when the backend supports it;
+        False keeps the host loop (`SlabProx.run`, only the iterations taken)."""
         import torch.distributed as dist
         if cfg.alpha != 1.0 or cfg.gamma != 1.0:
             raise ValueError("DistributedBSGD runs full sweeps only (alpha = gamma = 1); the stochastic "
@@ -339,6 +344,7 @@ class DistributedBSGD:
         self.perm = perm
         self.slab = None
         self.slabs = None
+        self.slab_device = False
         self._graph = None
         self._graph_epochs = 0
         if prox not in ("auto", "slab", "replicated"):
@@ -363,6 +369,8 @@ class DistributedBSGD:
                 self.slab = SlabProx(shard.slab_backend(lo, n), comm, slabs)
                 self.slabs = slabs
                 self.comm = comm
+                # device decisions (graph-capturable) when the backend supports them
+                self.slab_device = device_decisions and hasattr(self.slab.be, "decide")
             elif prox == "slab":
                 raise ValueError(why or "slab prox unavailable")
         elif prox == "slab":
@@ -403,10 +411,11 @@ class DistributedBSGD:
     def capture(self, epochs: int = 2, monitor: bool | None = None) -> bool:
         """Capture ``epochs`` (even: the x / r rings flip every epoch) epochs,
         collectives included, into one CUDA graph for `replay`.  Needs the
-        collectives warmed up by at least one eager epoch; not available with
-        the slab prox (its FGP decisions are taken on the host).  Returns
+        collectives warmed up by at least one eager epoch; with the slab prox
+        only when its FGP decisions are on the device (``device_decisions``).  Returns
         whether a graph is ready."""
-        if self.slab is not None or epochs < 2 or epochs % 2 or not getattr(self.y, "is_cuda", False):
+        if (self.slab is not None and not self.slab_device) or epochs < 2 or epochs % 2 or \
+                not getattr(self.y, "is_cuda", False):
             return False
         t = self.s.t
         saved = (self.xi, self.ri, self.rows_used, self.epoch)
@@ -486,6 +495,14 @@ class DistributedBSGD:
         comm, slabs, be = self.comm, self.slabs, self.slab.be
         comm.reduce_scatter(self.g, slabs)        # this rank's share of g = sum_p g_p
         be.step(x_k, self.g, self.mu)             # b = x_k + mu g on the slab
+        if self.slab_device:                      # decisions on the device: no host round trip
+            self.slab.run_device(self.mu * cfg.lam, cfg.prox.max_inner_iters, cfg.prox.tol)
+            stats = be.output(False, x_next, x_k, self.g, self.x_true)
+            comm.allreduce(stats)
+            be.set_step_device(self.s, args, stats)
+            comm.allgather_slabs(x_next, slabs)
+            self.prox_info = None
+            return
         info = self.slab.run(self.mu * cfg.lam, cfg.prox.max_inner_iters, cfg.prox.tol)
         stats = be.output(info["fell_back"], x_next, x_k, self.g, self.x_true)
         comm.allreduce(stats)
@@ -732,6 +749,29 @@ def pw_combine(nvox: int, slabs, values):
     return rec(0, nvox)
 
 
+def slab_program(nvox: int, slabs):
+    """The postfix program of `pw_combine` for `bsgd_slab_decide`: op >= 0 pushes
+    rank op's sums, -1 adds the top two (left + right), walking numpy's
+    recursion from the root exactly as pw_combine does."""
+    index = {tuple(s): i for i, s in enumerate(slabs)}
+    prog = []
+
+    def rec(lo, n):
+        i = index.get((lo, n))
+        if i is not None:
+            prog.append(i)
+            return
+        if n <= 128:
+            raise ValueError("slab boundary inside a pairwise leaf")
+        n2 = _pw_split(n)
+        rec(lo, n2)
+        rec(lo + n2, n - n2)
+        prog.append(-1)
+
+    rec(0, nvox)
+    return prog
+
+
 class TorchComm:
     """Halo / gather / reduce exchanges of the slab prox over torch.distributed
     (NCCL in production, gloo in the CPU tests)."""
@@ -780,6 +820,19 @@ class TorchComm:
         out = [self.torch.empty_like(t) for _ in range(self.world)]
         self.dist.all_gather(out, t.contiguous(), group=self.group)
         return np.stack([o.cpu().numpy() for o in out])
+
+    def gather_flat(self, t):
+        """All ranks' copies of a small tensor, rank-major in one tensor on t's
+        device (no host round trip: graph-capturable with NCCL)."""
+        if self.world == 1:
+            return t.contiguous()
+        if self.nccl:
+            out = self.torch.empty(self.world * t.numel(), dtype=t.dtype, device=t.device)
+            self.dist.all_gather_into_tensor(out, t.contiguous(), group=self.group)
+            return out
+        parts = [self.torch.empty_like(t) for _ in range(self.world)]
+        self.dist.all_gather(parts, t.contiguous(), group=self.group)
+        return self.torch.cat(parts)
 
     def allreduce(self, t):
         if self.world > 1:
@@ -834,9 +887,11 @@ class CudaSlab:
         self._stats = self.ws[offs[11] + 16:offs[11] + 20]
         self.args = nat.SlabArgs(depth, height, width, offset, count, 0.0, 0, 0, nat.ptr(self.ws), self.ws.numel() * 8)
         self.parity = 0
+        self.device = False   # True: FGP decisions in the workspace's control block (bsgd_slab_decide)
 
-    def _a(self):
+    def _a(self, when: int = 0):
         self.args.parity = self.parity
+        self.args.flags = (nat.SLAB_DEVICE | (when << 1)) if self.device else 0
         return ctypes.byref(self.args)
 
     def _st(self):
@@ -853,6 +908,8 @@ class CudaSlab:
             return [self._buf[10]]
         if name == "q":
             return [self._buf[7 + k] for k in range(d)]
+        if name in ("d0", "d1"):   # a dual buffer by index (device decisions: parity unknown to the host)
+            return [self._buf[1 + 3 * int(name[1]) + k] for k in range(d)]
         grp = self.parity if name == "p" else 1 - self.parity
         return [self._buf[1 + 3 * grp + k] for k in range(d)]
 
@@ -867,12 +924,27 @@ class CudaSlab:
         nat.call("bsgd_slab_init", self._a(), nat.ptr(self._sums), self._st())
         return self._sums[:2]
 
-    def candidate(self, from_p: bool):
-        nat.call("bsgd_slab_candidate", self._a(), 1 if from_p else 0, self._st())
+    def candidate(self, from_p: bool, when: int = 0):
+        nat.call("bsgd_slab_candidate", self._a(when), 1 if from_p else 0, self._st())
 
-    def dual(self, beta: float):
-        nat.call("bsgd_slab_dual", self._a(), float(beta), nat.ptr(self._sums), self._st())
+    def dual(self, beta: float, when: int = 0):
+        nat.call("bsgd_slab_dual", self._a(when), float(beta), nat.ptr(self._sums), self._st())
         return self._sums[:1 + 2 * self.dim]
+
+    def decide(self, stage: int, it: int, gathered, program, world: int, tol: float):
+        when = stage if stage in (1, 2) else 0
+        prog = (ctypes.c_int32 * len(program))(*program)
+        nat.call("bsgd_slab_decide", self._a(when), stage, it, nat.ptr(gathered), world, prog, len(program),
+                 float(tol), self._st())
+
+    def set_step_device(self, shard, args, stats):
+        nat.call("bsgd_slab_set_step", self._a(), shard.cols, ctypes.byref(args), nat.ptr(stats), self._st())
+
+    def info(self):
+        out = (ctypes.c_int32 * 4)()
+        tv = ctypes.c_double()
+        nat.call("bsgd_slab_info", self._a(), out, ctypes.byref(tv), self._st())
+        return {"iterations": out[0], "converged": out[1], "restarts": out[2], "fell_back": out[3], "tv": tv.value}
 
     def finalize(self):
         nat.call("bsgd_slab_finalize", self._a(), self._st())
@@ -907,6 +979,38 @@ class SlabProx:
 
     def _halo(self, name, lower=True, upper=True):
         self.comm.halo(self.be.fields(name), self.be.count, self.be.halo, lower, upper)
+
+    def run_device(self, weight: float, max_iters: int, tol: float):
+        """The same prox with every decision on the device (backend.device = True):
+        a FIXED launch / collective sequence -- max_iters blocks of halo, candidate,
+        halo, dual, all-gather, decide, then the restart variants that return at
+        once unless a restart was decided -- with no host synchronisation, so it
+        can be captured in a CUDA graph (`DistributedBSGD.capture`).  Both dual
+        buffers' halos are exchanged (the host does not know which holds c).
+        Bit-identical to `run`; ProxInfo afterwards from ``backend.info()``."""
+        be, comm = self.be, self.comm
+        if not weight > 0:
+            raise ValueError("slab prox needs a positive weight")
+        prog = getattr(self, "_program", None)
+        if prog is None:
+            prog = self._program = slab_program(be.nvox, self.slabs)
+        world = comm.world
+        be.device = True
+        be.set_weight(weight)
+        be.parity = 0
+        self._halo("b")
+        be.decide(0, 0, comm.gather_flat(be.init()), prog, world, tol)
+        for it in range(max_iters):
+            for stage, from_p in ((1, False), (2, True)):
+                if not from_p:
+                    self._halo("q")
+                be.candidate(from_p, when=stage)
+                self._halo("d0")
+                self._halo("d1")
+                be.decide(stage, it, comm.gather_flat(be.dual(0.0, when=stage)), prog, world, tol)
+        be.finalize()
+        self._halo("u", upper=False)
+        be.decide(3, 0, comm.gather_flat(be.energy()), prog, world, tol)
 
     def run(self, weight: float, max_iters: int, tol: float):
         """Prox of the b already stored by ``backend.step``; returns ProxInfo-style fields."""

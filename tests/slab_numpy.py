@@ -166,3 +166,102 @@ class NumpySlab:
         d = xv - x_k.numpy()[o]
         xe = float(np.sum((xv - x_true.numpy()[o]) ** 2)) if x_true is not None else 0.0
         return torch.tensor([float(xv @ xv), xe, float(d @ g.numpy()[o]), float(d @ d)], dtype=torch.float64)
+
+
+class NumpySlabDevice(NumpySlab):
+    """NumpySlab with the device-decision interface of CudaSlab (control block,
+    `when`-predicated passes, `decide`): the Python restatement of
+    slab.cuh's fgp_decide, so the fixed-sequence choreography of
+    parallel.SlabProx.run_device is checked over gloo."""
+
+    def __init__(self, dims, offset, count):
+        super().__init__(dims, offset, count)
+        self.device = False
+        self.ctl = {}
+
+    def fields(self, name):
+        if name in ("d0", "d1"):
+            return list(self._f[int(name[1])])
+        if self.device and name in ("p", "c"):
+            par = self.ctl.get("parity", 0)
+            return list(self._f[par if name == "p" else 1 - par])
+        return super().fields(name)
+
+    def _skip(self, when):
+        if not self.device or when == 0:
+            return False
+        if when == 1:
+            return bool(self.ctl["done"])
+        return bool(self.ctl["done"]) or not self.ctl["restart"]
+
+    def candidate(self, from_p, when=0):
+        if self._skip(when):
+            return
+        super().candidate(from_p)
+
+    def dual(self, beta, when=0):
+        if self._skip(when):
+            return torch.zeros(1 + 2 * self.dim, dtype=torch.float64)
+        return super().dual(self.ctl["beta"] if self.device else beta)
+
+    def output(self, fell, x_next, x_k, g, x_true):
+        return super().output(self.ctl["fell"] if self.device else fell, x_next, x_k, g, x_true)
+
+    @staticmethod
+    def _next_beta(c):
+        import math
+        c["t_next"] = 0.5 * (1.0 + math.sqrt(1.0 + (4.0 * c["t_mom"]) * c["t_mom"]))
+        c["beta"] = (c["t_mom"] - 1.0) / c["t_next"]
+
+    def decide(self, stage, it, gathered, program, world, tol):
+        import math
+        when = stage if stage in (1, 2) else 0
+        if self._skip(when):
+            return
+        k = gathered.numel() // world
+        g = gathered.numpy().reshape(world, k)
+        stk = []
+        for op in program:
+            if op >= 0:
+                stk.append([float(v) for v in g[op]])
+            else:
+                b, a = stk.pop(), stk.pop()
+                stk.append([x + y for x, y in zip(a, b)])
+        v = stk[0]
+        c = self.ctl
+        if stage == 0:
+            c.update(phi_prev=v[0], tv_b=v[1], t_mom=1.0, tv_out=0.0, iters=0, restarts=0, done=0, parity=0,
+                     restart=0, fell=0)
+            self._next_beta(c)
+            return
+        if stage == 3:
+            two_w = 2.0 * self.w
+            c["fell"] = 1 if (v[0] + two_w * v[1]) > (0.0 + two_w * c["tv_b"]) else 0
+            c["tv_out"] = v[1]
+            return
+        phi = v[0]
+        if stage == 1 and phi > c["phi_prev"]:
+            c["restart"] = 1
+            c["restarts"] += 1
+            c["t_mom"] = 1.0
+            self._next_beta(c)
+            return
+        c["restart"] = 0
+        c["parity"] ^= 1
+        c["phi_prev"] = c["phi_prev"] if c["phi_prev"] < phi else phi
+        c["t_mom"] = c["t_next"]
+        c["iters"] = it + 1
+        d = self.dim
+        ch2, sc2 = v[1] + v[2], v[1 + d] + v[2 + d]
+        if d == 3:
+            ch2, sc2 = ch2 + v[3], sc2 + v[6]
+        change, scale = math.sqrt(ch2), math.sqrt(sc2)
+        if change <= tol * (1e-30 if 1e-30 > scale else scale):
+            c["done"] = 1
+        else:
+            self._next_beta(c)
+
+    def info(self):
+        c = self.ctl
+        return {"iterations": c["iters"], "converged": c["done"], "restarts": c["restarts"], "fell_back": c["fell"],
+                "tv": c["tv_b"] if c["fell"] else c["tv_out"]}

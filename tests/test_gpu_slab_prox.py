@@ -55,6 +55,13 @@ class ThreadComm:
         self._sync()
         return rows
 
+    def gather_flat(self, t):
+        self._post("gflat", t.clone())
+        self._sync()
+        out = self.torch.cat([self._get(r, "gflat") for r in range(self.world)])
+        self._sync()
+        return out
+
     def allreduce(self, t):
         self._post("reduce", t.clone())
         self._sync()
@@ -117,8 +124,11 @@ CASES = [  # dims, weight, iters, tol, world; small (general tree) and fast-path
 ]
 
 
+@pytest.mark.parametrize("device", [False, True])
 @pytest.mark.parametrize("dims,w,iters,tol,world", CASES)
-def test_slab_prox_matches_single_gpu_bit_exact(cuda_ok, dims, w, iters, tol, world):
+def test_slab_prox_matches_single_gpu_bit_exact(cuda_ok, dims, w, iters, tol, world, device):
+    """Host-decided (SlabProx.run) and device-decided (run_device: bsgd_slab_decide
+    on all-gathered sums, a fixed launch sequence) slab prox vs the single-GPU prox."""
     import torch
     from paper_1812_01307_b200 import parallel, tv
     dev = torch.device("cuda", 0)
@@ -133,7 +143,11 @@ def test_slab_prox_matches_single_gpu_bit_exact(cuda_ok, dims, w, iters, tol, wo
         lo, n = slabs[r]
         be = parallel.CudaSlab(dims, lo, n, dev)
         be.step(xk, g, 1.0)
-        info = parallel.SlabProx(be, comm, slabs).run(w, iters, tol)
+        if device:
+            parallel.SlabProx(be, comm, slabs).run_device(w, iters, tol)
+            info = be.info()
+        else:
+            info = parallel.SlabProx(be, comm, slabs).run(w, iters, tol)
         xn = torch.zeros(nvox, dtype=torch.float64, device=dev)
         be.output(info["fell_back"], xn, xk, g, None)
         comm.allgather_slabs(xn, slabs)
@@ -294,3 +308,46 @@ def test_split_prox_epochs_match_fused(cuda_ok, monkeypatch):
     for xa, xb in zip(runs[0][0], runs[1][0]):
         assert np.array_equal(xa, xb)
     assert np.array_equal(runs[0][1], runs[1][1]) and runs[0][2] == runs[1][2]
+
+
+def test_distributed_slab_prox_device_capture_world1_nccl(cuda_ok):
+    """DistributedBSGD(prox="slab") with device decisions at world size 1 (NCCL):
+    capture() succeeds (the fixed-sequence prox has no host round trip) and graph
+    replays equal eager epochs, which equal the replicated-prox epochs bit for bit."""
+    import torch
+    import torch.distributed as dist
+    from paper_1812_01307_b200 import parallel, problems, tv
+    from paper_1812_01307_b200.blockops import make_partition
+    from paper_1812_01307_b200.solvers import SolverConfig
+    n = 32
+    a = problems.parallel_beam_matrix(n, 24, 47)
+    rng = np.random.default_rng(9)
+    y = a @ rng.random(n * n)
+    part = make_partition(a.shape[0], a.shape[1], 4, 4)
+    cfg = SolverConfig(mu=5e-4, lam=2.0, epochs=10, monitor_decrease=True, prox=tv.ProxSettings(10, 1e-6))
+    lay = tv.PixelLayout.row_major(n, n)
+    dist.init_process_group("nccl", store=dist.HashStore(), rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        runs = []
+        for mode in ("replicated", "eager", "graph"):
+            shard = parallel.CudaShard(a, parallel.ShardSpec(part, 0, 1), lam=cfg.lam, layout=lay)
+            drv = parallel.DistributedBSGD(shard, y, cfg, history_capacity=16,
+                                           prox="replicated" if mode == "replicated" else "slab")
+            assert (drv.slab is not None) == (mode != "replicated")
+            drv.epoch_step()
+            if mode == "graph":
+                assert drv.slab_device and drv.capture(2)
+                for _ in range(3):
+                    drv.replay()
+            else:
+                for _ in range(6):
+                    drv.epoch_step()
+            torch.cuda.synchronize()
+            runs.append((drv.x_current.cpu().numpy(), drv.r_current.cpu().numpy(), drv.history()))
+    finally:
+        dist.destroy_process_group()
+    (x0, r0, h0), (x1, r1, h1), (x2, r2, h2) = runs
+    assert np.array_equal(x0, x1) and np.array_equal(x1, x2)
+    assert np.array_equal(r1, r2) and np.array_equal(h1, h2)
+    assert np.array_equal(h0[:, 4:9], h1[:, 4:9])   # TV and prox iterations / restarts / converged / fell back
+    assert h1[:, 5].max() > 1

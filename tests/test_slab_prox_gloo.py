@@ -64,7 +64,7 @@ def test_prox_slabs_are_pairwise_nodes():
             assert got[0] == np.sum(a) and got[1] == np.sum(a ** 2), (n, world)
 
 
-def _prox_worker(rank, world, port, outdir):
+def _prox_worker(rank, world, port, outdir, device=False):
     import sys
     sys.path.insert(0, REPO)
     sys.path.insert(0, os.path.join(REPO, "tests"))
@@ -72,7 +72,7 @@ def _prox_worker(rank, world, port, outdir):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     import torch
     from paper_1812_01307_b200 import parallel
-    from slab_numpy import NumpySlab
+    from slab_numpy import NumpySlab, NumpySlabDevice
     comm = parallel.TorchComm()
     out = {}
     for ci, (dims, w, iters, tol, seed) in enumerate(CASES):
@@ -80,12 +80,16 @@ def _prox_worker(rank, world, port, outdir):
         halo = dims[1] * dims[2] if dims[0] > 1 else dims[2]
         slabs = parallel.prox_slabs(nvox, world, halo)
         lo, n = slabs[rank]
-        be = NumpySlab(dims, lo, n)
+        be = NumpySlabDevice(dims, lo, n) if device else NumpySlab(dims, lo, n)
         vol = _volume(dims, seed).ravel()
         xk = torch.from_numpy(vol.copy())
         g = torch.zeros(nvox, dtype=torch.float64)
         be.step(xk, g, 1.0)            # b = vol on the slab
-        info = parallel.SlabProx(be, comm, slabs).run(w, iters, tol)
+        if device:                     # fixed sequence, decisions in the backend's control block
+            parallel.SlabProx(be, comm, slabs).run_device(w, iters, tol)
+            info = be.info()
+        else:
+            info = parallel.SlabProx(be, comm, slabs).run(w, iters, tol)
         xn = torch.zeros(nvox, dtype=torch.float64)
         be.output(info["fell_back"], xn, xk, g, None)
         comm.allgather_slabs(xn, slabs)
@@ -97,10 +101,12 @@ def _prox_worker(rank, world, port, outdir):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_slab_prox_gloo_matches_oracle_bit_exact(tmp_path, world):
+@pytest.mark.parametrize("world,device", [(2, False), (3, False), (2, True), (3, True)])
+def test_slab_prox_gloo_matches_oracle_bit_exact(tmp_path, world, device):
+    """Host-decided (SlabProx.run) and device-decided (run_device: fixed sequence,
+    sums all-gathered and combined by the postfix program) slab prox over gloo."""
     from oracle import oracle as orc
-    mp.spawn(_prox_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    mp.spawn(_prox_worker, args=(world, _free_port(), str(tmp_path), device), nprocs=world, join=True)
     res = [np.load(tmp_path / f"rank{r}.npz") for r in range(world)]
     restarts = 0
     for ci, (dims, w, iters, tol, seed) in enumerate(CASES):
@@ -123,8 +129,9 @@ def test_slab_prox_gloo_matches_oracle_bit_exact(tmp_path, world):
 class _CpuProxShard:
     """CPU stand-in for CudaShard with the slab prox (lam > 0, identity layout)."""
 
-    def __init__(self, matrix, spec, dims, lam):
+    def __init__(self, matrix, spec, dims, lam, device=False):
         import types
+        self.device = device
         from scipy import sparse
         import torch
         from paper_1812_01307_b200 import tv
@@ -142,7 +149,11 @@ class _CpuProxShard:
         return self.dims
 
     def slab_backend(self, offset, count):
-        from slab_numpy import NumpySlab
+        from slab_numpy import NumpySlab, NumpySlabDevice
+        if self.device:
+            be = NumpySlabDevice(self.dims, offset, count)
+            be.set_step_device = lambda shard, a, stats: setattr(a, "stats", tuple(float(v) for v in stats))
+            return be
         return NumpySlab(self.dims, offset, count)
 
     def zeros(self, n):
@@ -188,7 +199,7 @@ def _ct_case():
     return a, y, x_true, (1, n, n)
 
 
-def _epoch_worker(rank, world, port, outdir, epochs):
+def _epoch_worker(rank, world, port, outdir, epochs, device=False):
     import sys
     sys.path.insert(0, REPO)
     sys.path.insert(0, os.path.join(REPO, "tests"))
@@ -200,26 +211,28 @@ def _epoch_worker(rank, world, port, outdir, epochs):
     a, y, x_true, dims = _ct_case()
     part = make_partition(a.shape[0], a.shape[1], 4, 4)
     spec = parallel.ShardSpec(part, rank, world)
-    shard = _CpuProxShard(a, spec, dims, lam=0.5)
+    shard = _CpuProxShard(a, spec, dims, lam=0.5, device=device)
     cfg = SolverConfig(mu=2e-3, lam=0.5, epochs=epochs, monitor_decrease=False, prox=tv.ProxSettings(20, 1e-6))
     drv = parallel.DistributedBSGD(shard, y, cfg, history_capacity=epochs + 4, prox="slab")
-    assert drv.slab is not None
+    assert drv.slab is not None and drv.slab_device == device
     auto = parallel.DistributedBSGD(shard, y, cfg, history_capacity=4)
     assert auto.slab is None   # small image: "auto" keeps the prox replicated
     infos = []
     for _ in range(epochs):
         drv.epoch_step(monitor=False)
-        infos.append([drv.prox_info[k] for k in ("iterations", "converged", "restarts", "fell_back")])
+        info = drv.slab.be.info() if device else drv.prox_info
+        infos.append([info[k] for k in ("iterations", "converged", "restarts", "fell_back")])
     np.savez(os.path.join(outdir, f"rank{rank}.npz"), x=drv.x_current.numpy(), r=drv.r_current.numpy(),
              info=np.array(infos))
     dist.barrier()
     dist.destroy_process_group()
 
 
-def test_world2_gloo_epochs_with_slab_prox_match_oracle(tmp_path):
+@pytest.mark.parametrize("device", [False, True])
+def test_world2_gloo_epochs_with_slab_prox_match_oracle(tmp_path, device):
     from oracle import oracle as orc
     epochs = 5
-    mp.spawn(_epoch_worker, args=(2, _free_port(), str(tmp_path), epochs), nprocs=2, join=True)
+    mp.spawn(_epoch_worker, args=(2, _free_port(), str(tmp_path), epochs, device), nprocs=2, join=True)
     r0, r1 = (np.load(tmp_path / f"rank{r}.npz") for r in range(2))
     assert np.array_equal(r0["x"], r1["x"]) and np.array_equal(r0["info"], r1["info"])
     a, y, x_true, dims = _ct_case()
