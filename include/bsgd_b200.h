@@ -345,6 +345,12 @@ int bsgd_slab_output(const bsgd_slab *s, int32_t fell_back, double *x_next, cons
 #define BSGD_SLAB_DEVICE 1
 #define BSGD_SLAB_MAIN 1
 #define BSGD_SLAB_RESTART 2
+/* flags bit: the x_k / g / x_next / x_true of bsgd_slab_step and bsgd_slab_output
+ * are this rank's LOCAL vectors for its slices of a slice-stacked operator, in
+ * the interleaved order pixel * (count / (H W)) + (slice - offset / (H W)) --
+ * slice ownership of configs[4] (A = A2 (x) I_D is block diagonal in the slices,
+ * so the products need no exchange); the slab must be whole slices */
+#define BSGD_SLAB_INTERLEAVED 8
 int bsgd_slab_decide(const bsgd_slab *s, int32_t stage, int32_t iteration, const double *gathered, int32_t world,
                      const int32_t *program, int32_t nprogram, double tol, void *stream);
 /* bsgd_epoch_set_step with the prox scalars taken from the control block */

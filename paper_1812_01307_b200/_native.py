@@ -43,7 +43,7 @@ class SlabArgs(ctypes.Structure):
 
 
 SLAB_SLOTS = 12
-SLAB_DEVICE, SLAB_MAIN, SLAB_RESTART = 1, 1, 2
+SLAB_DEVICE, SLAB_MAIN, SLAB_RESTART, SLAB_INTERLEAVED = 1, 1, 2, 8
 
 
 class KernelInfo(ctypes.Structure):

@@ -1431,6 +1431,15 @@ static int slab_ctx(const bsgd_slab *s, SlabCtx &c, bool need_weight = true) {
         c.v.ctl = (FgpCtl *)(base + off[11] + kSlabCtlOffset);
         c.v.when = (s->flags >> 1) & 3;
     }
+    c.v.ilv = 0;
+    c.v.ilv_z0 = 0;
+    if (s->flags & BSGD_SLAB_INTERLEAVED) {   // solver vectors: this rank's slices, interleaved
+        const int64_t hw = s->height * s->width;
+        if (D <= 1 || s->offset % hw || s->count % hw)
+            return fail(BSGD_EINVAL, "BSGD_SLAB_INTERLEAVED needs a volume slab of whole slices");
+        c.v.ilv = s->count / hw;
+        c.v.ilv_z0 = s->offset / hw;
+    }
     c.v.u = at(10);
     c.v.off = s->offset;
     c.v.n = s->count;

@@ -53,7 +53,18 @@ struct SlabView {
     double *u;        // finalize output; NULL: the dual buffer not holding p
     FgpCtl *ctl;      // split prox control block, NULL for the host loop
     int zero;         // split prox, first iteration: p = q = 0 are not stored, read as zeros
+    // solver vectors of step / output: 0 = full-length in volume order (vec[p]);
+    // > 0 = the rank's own slices in the interleaved order of A2 (x) I_{ilv}
+    // (vec[(p mod H W) * ilv + p / (H W) - z0], slice ownership of configs[4])
+    int64_t ilv, ilv_z0;
 };
+
+__device__ __forceinline__ int64_t slab_vec_index(const SlabView &s, int64_t p) {
+    if (s.ilv == 0) return p;
+    const int64_t hw = s.a.H * s.a.W;
+    const int64_t z = p / hw;
+    return (p - z * hw) * s.ilv + (z - s.ilv_z0);
+}
 
 __device__ __forceinline__ bool slab_skip(const SlabView &s) {
     if (s.ctl == nullptr || s.when == 0) return false;
@@ -121,7 +132,8 @@ __global__ void __launch_bounds__(kThreads) slab_step_kernel(SlabView s, const d
     double *b = const_cast<double *>(s.a.b);
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < s.n; i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t p = s.off + i;
-        b[p] = rn_add(xk[p], rn_mul(mu, g[p]));
+        const int64_t k = slab_vec_index(s, p);
+        b[p] = rn_add(xk[k], rn_mul(mu, g[k]));
     }
 }
 
@@ -266,12 +278,13 @@ __global__ void __launch_bounds__(kThreads) slab_output_kernel(SlabView s, int f
     double st[4] = {0.0, 0.0, 0.0, 0.0};
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < s.n; i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t p = s.off + i;
+        const int64_t k = slab_vec_index(s, p);
         const double xv = fell ? __ldg(s.a.b + p) : __ldg(r.u + p);
-        xn[p] = xv;
-        const double d = rn_sub(xv, xk[p]);
+        xn[k] = xv;
+        const double d = rn_sub(xv, xk[k]);
         st[0] += xv * xv;
-        if (xtrue != nullptr) { const double e = xv - xtrue[p]; st[1] += e * e; }
-        st[2] += d * g[p];
+        if (xtrue != nullptr) { const double e = xv - xtrue[k]; st[1] += e * e; }
+        st[2] += d * g[k];
         st[3] += d * d;
     }
     block_sum<4>(st, sm);

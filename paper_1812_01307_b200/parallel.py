@@ -249,6 +249,99 @@ class CudaShard:
         nat.call("bsgd_rmatvec", self.op.plan, nat.ptr(w), nat.ptr(out), self.stream())
 
 
+def slice_ranges(depth: int, height: int, width: int, world: int):
+    """Slices [z0, z1) of each rank for slice ownership: the slab prox's pairwise
+    nodes of the slice-major (depth, height, width) volume, which must be whole
+    slices (power-of-two volumes and rank counts: equal slice ranges)."""
+    hw = height * width
+    out = []
+    for lo, n in prox_slabs(depth * hw, world, hw):
+        if lo % hw or n % hw:
+            raise ValueError("the pairwise slabs do not fall on whole slices")
+        out.append((lo // hw, (lo + n) // hw))
+    return out
+
+
+class CudaSliceShard(CudaShard):
+    """configs[4] by SLICES: A = A2 (x) I_D is block diagonal in the slices, so rank p
+    owning slices [z0, z1) holds the stacked operator A2 (x) I_{z1-z0} of its own
+    slices and its x, g, r are local -- the products need no exchange at all.
+    The only collectives of an epoch are the slab prox's one-plane halos and
+    scalar sums (the rank's slices are its prox slab of the slice-major volume,
+    `slice_ranges`) and two small all-reduces (step statistics, ||r||^2).
+
+    Local vectors use the interleaved order of the local operator (pixel *
+    (z1 - z0) + slice - z0; rays likewise); `local_rows` / `local_cols` cut them
+    from the global interleaved vectors.  The block partition is num_blocks x
+    num_blocks over the local operator, so products agree with the global
+    operator's to rounding (the forward products exactly)."""
+
+    owns_slices = True
+
+    def __init__(self, n: int, num_angles: int, num_bins: int, depth: int, rank: int, world: int,
+                 num_blocks: int = 16, dtype=np.float32, device=None, lam: float = 0.0):
+        import types
+
+        from . import tv
+        if not lam > 0:
+            raise ValueError("slice ownership runs the slab-decomposed prox: lam must be positive")
+        z0, z1 = slice_ranges(depth, n, n, world)[rank]
+        dloc = z1 - z0
+        op = BlockOperator.from_parallel_beam(n, num_angles, num_bins, num_blocks, num_blocks, dtype=dtype,
+                                              device=device, depth=dloc)
+        self.z0, self.z1, self.depth, self.n = z0, z1, depth, n
+        self.rays2, self.pix2 = num_angles * num_bins, n * n
+        hw = n * n
+        self.slab_range = (z0 * hw, dloc * hw)
+        rows_l, cols_l = op.shape
+        # the global partition (the pair-order RNG advances over its M x N blocks,
+        # solvers.py:176-195), with this rank's local rows
+        part = make_partition(self.rays2 * depth, hw * depth, num_blocks, num_blocks)
+        spec = types.SimpleNamespace(row_range=(0, rows_l), partition=part, rank=rank, world=world)
+        self._finish(spec, op, cols_l, lam, tv.VolumeLayout.z_major(dloc, n, n))
+        self._global_shape = (self.rays2 * depth, hw * depth)
+
+    @property
+    def shape(self):
+        return self._global_shape
+
+    def _cut(self, v, m):
+        arr = v.detach().cpu().numpy() if hasattr(v, "detach") else np.asarray(v, dtype=np.float64)
+        return self.vector(np.ascontiguousarray(arr.reshape(m, self.depth)[:, self.z0:self.z1]).ravel())
+
+    def local_rows(self, y_full):
+        return self._cut(y_full, self.rays2)
+
+    def local_cols(self, x_full):
+        return self._cut(x_full, self.pix2)
+
+    def prox_dims(self):
+        if not self.hw[0]:
+            return None
+        return (self.depth, self.n, self.n)      # the global slice-major volume
+
+    def slab_backend(self, offset, count):
+        if (offset, count) != self.slab_range:
+            raise ValueError("slab does not match this rank's slices")
+        be = CudaSlab(self.prox_dims(), offset, count, self.dev)
+        be.interleaved = True
+        return be
+
+    def assemble_cols(self, x_local, group=None):
+        """The global interleaved vector from every rank's local one (all-gather)."""
+        import torch.distributed as dist
+        t = self.t
+        xl = x_local.reshape(self.pix2, self.z1 - self.z0)
+        if dist.is_initialized() and dist.get_world_size(group) > 1:
+            world = dist.get_world_size(group)
+            ranges = slice_ranges(self.depth, self.n, self.n, world)
+            parts = [t.empty(self.pix2 * (b - a), dtype=t.float64, device=x_local.device) for a, b in ranges]
+            dist.all_gather(parts, x_local.contiguous(), group=group)
+            cols = [p.reshape(self.pix2, b - a) for p, (a, b) in zip(parts, ranges)]
+            return t.cat(cols, dim=1).reshape(-1)
+        return xl.reshape(-1)
+
+
 def ct_row_slab_shard(index: int, rank: int, world: int, device=None, group=None):
     """configs[index] (2-D CT) as this rank's row slab, generated on its GPU.
 
@@ -277,6 +370,43 @@ def ct_row_slab_shard(index: int, rank: int, world: int, device=None, group=None
     y = clean + np.random.default_rng(1).standard_normal(rows) * sigma
     meta = {"name": name, "height": n, "width": n, "lam": lam, "max_inner_iters": inner, "epochs": epochs,
             "x_true": x_true, "layout": layout}
+    return shard, y, meta
+
+
+def ct_slice_shard(rank: int, world: int, device=None, group=None, scale: float = 1.0):
+    """configs[4] (3-D slice-stacked CT) as this rank's slices, generated on its GPU.
+
+    Returns (shard, y_full, meta); y_full is the global interleaved measurement
+    vector of `problems.config_device(4)` bit for bit: each rank forms its
+    slices' rows of A x_true with the same kernels (the forward products of a
+    slice shard are the global operator's rows exactly), the pieces are
+    all-gathered and interleaved, and the seeded noise of the full length is
+    drawn on every rank."""
+    import torch.distributed as dist
+    from . import problems
+    t = nat.torch()
+    n = max(16, int(round(256 * scale)))
+    depth = max(2, int(round(256 * scale)))
+    ang = max(8, int(round(360 * scale)))
+    nb = max(9, int(round(363 * scale)) | 1)
+    lam, inner, blocks, noise_frac = 0.01, 10, 16, 0.01
+    shard = CudaSliceShard(n, ang, nb, depth, rank, world, num_blocks=blocks, device=device, lam=lam)
+    vol = problems.ellipsoid_phantom(n, depth, 40, 0)
+    x_true = np.ascontiguousarray(vol.reshape(depth, n * n).T).ravel()
+    clean_l = shard.op.matvec(shard.local_cols(x_true), charge=False)
+    rays = ang * nb
+    if dist.is_initialized() and dist.get_world_size(group) > 1:
+        ranges = slice_ranges(depth, n, n, world)
+        parts = [t.empty(rays * (b - a), dtype=t.float64, device=shard.dev) for a, b in ranges]
+        dist.all_gather(parts, shard.vector(clean_l), group=group)
+        clean = t.cat([p.reshape(rays, b - a) for p, (a, b) in zip(parts, ranges)], dim=1).reshape(-1).cpu().numpy()
+    else:
+        clean = clean_l.cpu().numpy() if hasattr(clean_l, "cpu") else np.asarray(clean_l)
+    sigma = noise_frac * float(np.max(clean))
+    y = clean + np.random.default_rng(1).standard_normal(clean.shape[0]) * sigma
+    from . import tv
+    meta = {"n": n, "depth": depth, "lam": lam, "max_inner_iters": inner, "x_true": x_true,
+            "layout": tv.VolumeLayout(depth, n, n, problems.interleaved_perm(n * n, depth))}
     return shard, y, meta
 
 
@@ -314,7 +444,10 @@ class DistributedBSGD:
         self.cfg = cfg
         r0, r1 = shard.spec.row_range
         y_full = np.asarray(y_full, dtype=np.float64) if not hasattr(y_full, "cpu") else y_full
-        self.y = shard.vector(y_full[r0:r1])
+        self.slices = getattr(shard, "owns_slices", False)   # configs[4] by slices: x, g, r all local
+        if self.slices and (cfg.lam <= 0 or prox == "replicated"):
+            raise ValueError("slice ownership needs lam > 0 and the slab prox (its g and x are local)")
+        self.y = shard.local_rows(y_full) if self.slices else shard.vector(y_full[r0:r1])
         self.x = [shard.zeros(shard.cols), shard.zeros(shard.cols)]
         self.r = [self.y.clone(), self.y.clone()]   # r_0 = y and its lookahead y - A 0
         # g and, in its last slot, this rank's ||r||^2 of the previous epoch: one
@@ -328,7 +461,10 @@ class DistributedBSGD:
         self.mu = cfg.mu
         self.epoch = 0.0
         self.rng = np.random.default_rng(cfg.seed)
-        self.x_true = shard.vector(x_true) if x_true is not None else None
+        if x_true is not None:
+            self.x_true = shard.local_cols(x_true) if self.slices else shard.vector(x_true)
+        else:
+            self.x_true = None
         self.f_curr = shard.zeros(1)
         part = shard.zeros(1)
         shard.dot(self.y, self.y, part)
@@ -364,7 +500,11 @@ class DistributedBSGD:
             # on the host (a gather and halo exchanges per pass), which costs more than
             # running a small prox redundantly on every rank (1024^2: ~0.13 ms per epoch)
             big = int(np.prod(dims)) >= SLAB_PROX_MIN_VOXELS
-            if why is None and (prox == "slab" or (comm.world > 1 and big)):
+            if self.slices and why is None and slabs[comm.rank] != shard.slab_range:
+                why = "the slice shard's slices are not this rank's prox slab"
+            if self.slices and why is not None:
+                raise ValueError(why)
+            if why is None and (prox == "slab" or self.slices or (comm.world > 1 and big)):
                 lo, n = slabs[comm.rank]
                 self.slab = SlabProx(shard.slab_backend(lo, n), comm, slabs)
                 self.slabs = slabs
@@ -493,21 +633,24 @@ class DistributedBSGD:
         """x_next = prox(x_k + mu g) with the prox decomposed over the ranks."""
         cfg = self.cfg
         comm, slabs, be = self.comm, self.slabs, self.slab.be
-        comm.reduce_scatter(self.g, slabs)        # this rank's share of g = sum_p g_p
+        if not self.slices:                       # slice ownership: g is already this rank's, complete
+            comm.reduce_scatter(self.g, slabs)    # this rank's share of g = sum_p g_p
         be.step(x_k, self.g, self.mu)             # b = x_k + mu g on the slab
         if self.slab_device:                      # decisions on the device: no host round trip
             self.slab.run_device(self.mu * cfg.lam, cfg.prox.max_inner_iters, cfg.prox.tol)
             stats = be.output(False, x_next, x_k, self.g, self.x_true)
             comm.allreduce(stats)
             be.set_step_device(self.s, args, stats)
-            comm.allgather_slabs(x_next, slabs)
+            if not self.slices:                   # the next forward product reads all of x
+                comm.allgather_slabs(x_next, slabs)
             self.prox_info = None
             return
         info = self.slab.run(self.mu * cfg.lam, cfg.prox.max_inner_iters, cfg.prox.tol)
         stats = be.output(info["fell_back"], x_next, x_k, self.g, self.x_true)
         comm.allreduce(stats)
         self.s.set_step(args, stats, info)
-        comm.allgather_slabs(x_next, slabs)       # the next forward product reads all of x
+        if not self.slices:
+            comm.allgather_slabs(x_next, slabs)   # the next forward product reads all of x
         self.prox_info = info
 
     @property
@@ -612,7 +755,7 @@ def run_solver_distributed(problem, cfg, sample_every: int = 1, group=None, *, u
 
     graphed = False
     while done < epochs:
-        if use_graphs and drv.slab is None and done >= 1 and epochs - done >= 2:
+        if use_graphs and (drv.slab is None or drv.slab_device) and done >= 1 and epochs - done >= 2:
             if not graphed:
                 graphed = drv.capture(2)
                 if not graphed:
@@ -639,7 +782,10 @@ def run_solver_distributed(problem, cfg, sample_every: int = 1, group=None, *, u
     err = drain()
     if err is not None:
         raise err
-    trace.final_x = drv.x_current.cpu().numpy().copy()
+    xf = drv.x_current
+    if getattr(shard, "owns_slices", False):
+        xf = shard.assemble_cols(xf, group)
+    trace.final_x = xf.cpu().numpy().copy()
     if dist.is_initialized():
         dist.barrier(group=group)
     return trace
@@ -888,10 +1034,14 @@ class CudaSlab:
         self.args = nat.SlabArgs(depth, height, width, offset, count, 0.0, 0, 0, nat.ptr(self.ws), self.ws.numel() * 8)
         self.parity = 0
         self.device = False   # True: FGP decisions in the workspace's control block (bsgd_slab_decide)
+        self.interleaved = False   # True: step / output vectors are this rank's slices, interleaved
 
     def _a(self, when: int = 0):
         self.args.parity = self.parity
-        self.args.flags = (nat.SLAB_DEVICE | (when << 1)) if self.device else 0
+        flags = (nat.SLAB_DEVICE | (when << 1)) if self.device else 0
+        if self.interleaved:
+            flags |= nat.SLAB_INTERLEAVED
+        self.args.flags = flags
         return ctypes.byref(self.args)
 
     def _st(self):

@@ -86,8 +86,17 @@ class NumpySlab:
         return np.arange(self.halo, self.halo + self.count)
 
     # --- passes ---------------------------------------------------------------
+    interleaved = False   # step / output vectors: this rank's slices, interleaved (slice ownership)
+
+    def _vec_index(self):
+        p = np.arange(self.offset, self.offset + self.count)
+        if not self.interleaved:
+            return p
+        hw = self.dims[1] * self.dims[2]
+        return (p % hw) * (self.count // hw) + (p // hw - self.offset // hw)
+
     def step(self, x_k, g, mu):
-        o = slice(self.offset, self.offset + self.count)
+        o = self._vec_index()
         self._b.numpy()[self._own] = x_k.numpy()[o] + mu * g.numpy()[o]
 
     def init(self):
@@ -159,7 +168,7 @@ class NumpySlab:
         return torch.tensor([np.sum(d * d), np.sum(self._tv_terms(u, idx))], dtype=torch.float64)
 
     def output(self, fell, x_next, x_k, g, x_true):
-        o = slice(self.offset, self.offset + self.count)
+        o = self._vec_index()
         src = self._b if fell else self._u
         xv = src.numpy()[self._own].copy()
         x_next.numpy()[o] = xv

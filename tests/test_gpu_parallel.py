@@ -301,3 +301,66 @@ def test_ct_row_slab_shards_cover_the_operator(cuda_ok):
         assert np.array_equal(sh.op.matvec(x, charge=False), full[r0:r1])
         acc += sh.op.rmatvec(w[r0:r1], charge=False)
     assert rel(acc, d.op.rmatvec(w, charge=False)) < 1e-12
+
+
+def test_slice_shard_world1_nccl_matches_single_gpu(cuda_ok):
+    """configs[4]-style slice ownership (CudaSliceShard) at world size 1 over NCCL:
+    run_solver(group=...) with the device-decided slab prox on the slice-major
+    volume equals the single-GPU stacked run with the slice-major layout -- x,
+    samples, exact units, flags -- bit for bit (same operator, same prox input)."""
+    import torch
+    import torch.distributed as dist
+    from paper_1812_01307_b200 import blockops, parallel, problems, solvers, spectral, tv
+    n, ang, nb, depth = 32, 24, 47, 16
+    op = blockops.BlockOperator.from_parallel_beam(n, ang, nb, 16, 16, depth=depth)
+    vol = problems.ellipsoid_phantom(n, depth, 6, 0)
+    x_true = np.ascontiguousarray(vol.reshape(depth, n * n).T).ravel()
+    y = op.matvec(x_true, charge=False)
+    y = y + np.random.default_rng(1).standard_normal(y.shape[0]) * 0.01 * float(np.max(y))
+    mu = 0.9 / (2.0 * spectral.largest_eigenvalue(op, max_iters=50).value)
+    cfg = solvers.SolverConfig(mu=mu, lam=0.05, epochs=9, prox=tv.ProxSettings(10, 1e-6))
+    lay = tv.VolumeLayout(depth, n, n, problems.interleaved_perm(n * n, depth))
+    single = solvers.run_solver("bsgd", solvers.Problem(op, y, x_true, lay), cfg, sample_every=2)
+    dist.init_process_group("nccl", store=dist.HashStore(), rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        shard = parallel.CudaSliceShard(n, ang, nb, depth, 0, 1, lam=cfg.lam)
+        tr = solvers.run_solver("bsgd", solvers.Problem(shard, y, x_true, lay), cfg, sample_every=2, group="default")
+    finally:
+        dist.destroy_process_group()
+    got, want = np.array([tuple(s) for s in tr.samples]), np.array([tuple(s) for s in single.samples])
+    assert np.array_equal(got[:, 0], want[:, 0]) and np.array_equal(got[:, 3], want[:, 3])
+    assert np.allclose(got[:, 1:3], want[:, 1:3], rtol=1e-12)
+    assert list(tr.decrease_flags) == list(single.decrease_flags)
+    assert np.array_equal(tr.final_x, single.final_x)
+
+
+def test_slice_shards_products_match_global_operator(cuda_ok):
+    """Two slice shards (ranks 0 and 1 of 2) of a slice-stacked operator: their
+    local forward products are the global operator's rows of their slices bit for
+    bit; the transposed products agree to rounding (local block partition)."""
+    from paper_1812_01307_b200 import blockops, parallel
+    n, ang, nb, depth = 32, 24, 47, 16
+    op = blockops.BlockOperator.from_parallel_beam(n, ang, nb, 16, 16, depth=depth)
+    rng = np.random.default_rng(5)
+    x = rng.random(op.shape[1])
+    w = rng.standard_normal(op.shape[0])
+    ax = op.matvec(x, charge=False).reshape(ang * nb, depth)
+    atw = op.rmatvec(w, charge=False).reshape(n * n, depth)
+    for r in range(2):
+        sh = parallel.CudaSliceShard(n, ang, nb, depth, r, 2, lam=0.05)
+        z0, z1 = sh.z0, sh.z1
+        assert (z0, z1) == ((0, 8) if r == 0 else (8, 16))
+        xl = sh.local_cols(x).cpu().numpy()
+        assert np.array_equal(sh.op.matvec(xl, charge=False), np.ascontiguousarray(ax[:, z0:z1]).ravel())
+        wl = sh.local_rows(w).cpu().numpy()
+        assert rel(sh.op.rmatvec(wl, charge=False), np.ascontiguousarray(atw[:, z0:z1]).ravel()) < 1e-13
+
+
+def test_ct_slice_shard_world1_matches_config_device(cuda_ok):
+    """configs[4] (scaled to 64^3) generated as a slice shard at world size 1: the
+    measurements equal problems.config_device(4)'s bit for bit."""
+    from paper_1812_01307_b200 import parallel, problems
+    shard, y, meta = parallel.ct_slice_shard(0, 1, scale=0.25)
+    d = problems.config_device(4, scale=0.25)
+    assert shard.shape == d.op.shape and shard.op.nnz == d.op.nnz
+    assert np.array_equal(y, d.y)

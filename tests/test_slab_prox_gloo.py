@@ -152,7 +152,12 @@ class _CpuProxShard:
         from slab_numpy import NumpySlab, NumpySlabDevice
         if self.device:
             be = NumpySlabDevice(self.dims, offset, count)
-            be.set_step_device = lambda shard, a, stats: setattr(a, "stats", tuple(float(v) for v in stats))
+
+            def set_step_device(shard, a, stats):
+                a.stats = tuple(float(v) for v in stats)
+                a.tv = be.info()["tv"]
+
+            be.set_step_device = set_step_device
             return be
         return NumpySlab(self.dims, offset, count)
 
@@ -183,6 +188,9 @@ class _CpuProxShard:
     def tail(self, a, fnext1):
         row = int(a.counter.item())
         a.hist[row, 0] = float(fnext1.item())
+        if a.stats is not None:             # |x|^2, |x - x*|^2 (H_XX, H_XE) and TV (H_TV)
+            a.hist[row, 2], a.hist[row, 3] = a.stats[0], a.stats[1]
+            a.hist[row, 4] = getattr(a, "tv", 0.0)
         a.counter.fill_(row + 1)
 
     def dot(self, a, b, out1):
@@ -249,3 +257,114 @@ def test_world2_gloo_epochs_with_slab_prox_match_oracle(tmp_path, device):
     r_full = np.concatenate([r0["r"], r1["r"]])
     assert np.linalg.norm(r_full - st.r_vec) / np.linalg.norm(st.r_vec) < 1e-7
     assert r0["info"][:, 0].max() > 1     # the prox iterated
+
+
+class _CpuSliceShard(_CpuProxShard):
+    """CPU stand-in for parallel.CudaSliceShard: kron(A2, I_{slices}) of this rank's
+    slices (local interleaved vectors), the slab prox on its slices of the
+    slice-major volume (numpy double with the interleaved step / output map)."""
+
+    owns_slices = True
+
+    def __init__(self, a2, n, depth, rank, world, lam):
+        import types
+        from scipy import sparse
+        import torch
+        from paper_1812_01307_b200 import parallel, tv
+        from paper_1812_01307_b200.blockops import make_partition
+        z0, z1 = parallel.slice_ranges(depth, n, n, world)[rank]
+        self.z0, self.z1, self.depth, self.n = z0, z1, depth, n
+        self.rays2, self.pix2 = a2.shape
+        dl = z1 - z0
+        self.a = sparse.csr_array(sparse.kron(sparse.csr_array(a2).astype(np.float64), sparse.identity(dl),
+                                              format="csr"))
+        self.t = torch
+        self.cols, self.rows = self.pix2 * dl, self.rays2 * dl
+        self.dims = (depth, n, n)
+        self.layout = tv.VolumeLayout.z_major(dl, n, n)
+        self.slab_range = (z0 * n * n, dl * n * n)
+        self.spec = types.SimpleNamespace(row_range=(0, self.rows),
+                                          partition=make_partition(self.rays2 * depth, self.pix2 * depth, 4, 4))
+        self._ns = types.SimpleNamespace
+        self.device = True
+        self.op = types.SimpleNamespace(nnz=int(self.a.nnz))
+
+    @property
+    def shape(self):
+        return (self.rays2 * self.depth, self.pix2 * self.depth)
+
+    def _cut(self, v, m):
+        return self.vector(np.ascontiguousarray(np.asarray(v).reshape(m, self.depth)[:, self.z0:self.z1]).ravel())
+
+    def local_rows(self, y):
+        return self._cut(y, self.rays2)
+
+    def local_cols(self, x):
+        return self._cut(x, self.pix2)
+
+    def slab_backend(self, offset, count):
+        be = super().slab_backend(offset, count)
+        be.interleaved = True
+        return be
+
+    def assemble_cols(self, x_local, group=None):
+        import torch.distributed as dist
+        from paper_1812_01307_b200 import parallel
+        world = dist.get_world_size(group)
+        ranges = parallel.slice_ranges(self.depth, self.n, self.n, world)
+        parts = [self.t.zeros(self.pix2 * (b - a), dtype=self.t.float64) for a, b in ranges]
+        dist.all_gather(parts, x_local.contiguous(), group=group)
+        return self.t.cat([p.reshape(self.pix2, b - a) for p, (a, b) in zip(parts, ranges)], dim=1).reshape(-1)
+
+
+def _slice_case():
+    from paper_1812_01307_b200 import problems
+    n, depth = 8, 8
+    a2 = problems.parallel_beam_matrix(n, 6, 11)
+    vol = problems.ellipsoid_phantom(n, depth, 5, 0)
+    x_true = np.ascontiguousarray(vol.reshape(depth, n * n).T).ravel()
+    from scipy import sparse
+    a = sparse.csr_array(sparse.kron(sparse.csr_array(a2), sparse.identity(depth), format="csr"))
+    a.sort_indices()
+    y = a @ x_true + np.random.default_rng(2).standard_normal(a.shape[0]) * 0.02
+    return a2, a, y, x_true, n, depth
+
+
+def _slice_worker(rank, world, port, outdir, epochs):
+    import sys
+    sys.path.insert(0, REPO)
+    sys.path.insert(0, os.path.join(REPO, "tests"))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1812_01307_b200 import problems, solvers, tv
+    a2, a, y, x_true, n, depth = _slice_case()
+    shard = _CpuSliceShard(a2, n, depth, rank, world, lam=0.3)
+    cfg = solvers.SolverConfig(mu=0.9 / (2.0 * 60.0), lam=0.3, epochs=epochs, monitor_decrease=False,
+                               prox=tv.ProxSettings(15, 1e-7))
+    lay = tv.VolumeLayout(depth, n, n, problems.interleaved_perm(n * n, depth))
+    tr = solvers.run_solver("bsgd", solvers.Problem(shard, y, x_true, lay), cfg, sample_every=2, group="default")
+    np.savez(os.path.join(outdir, f"s{rank}.npz"), x=tr.final_x, samples=np.array([tuple(s) for s in tr.samples]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_world2_gloo_slice_ownership_matches_oracle(tmp_path):
+    """configs[4]-style slice ownership over two ranks: no product exchange, the
+    slab prox on each rank's slices (device-decision choreography), against the
+    oracle on the full kron(A2, I_D) with the slice-major volume view."""
+    from oracle import oracle as orc
+    from paper_1812_01307_b200 import problems
+    epochs = 6
+    mp.spawn(_slice_worker, args=(2, _free_port(), str(tmp_path), epochs), nprocs=2, join=True)
+    r0, r1 = (np.load(tmp_path / f"s{r}.npz") for r in range(2))
+    assert np.array_equal(r0["x"], r1["x"])
+    a2, a, y, x_true, n, depth = _slice_case()
+    op = orc.OracleOperator(a, 4, 4)
+    prm = orc.Params(mu=0.9 / (2.0 * 60.0), lam=0.3, epochs=epochs, max_inner_iters=15, tol=1e-7,
+                     monitor_decrease=False)
+    ref = orc.run_bsgd(op, y, prm, x_true=x_true, perm=problems.interleaved_perm(n * n, depth), hw=(depth, n, n),
+                       sample_every=2)
+    assert np.linalg.norm(r0["x"] - ref.final_x) / np.linalg.norm(ref.final_x) < 1e-10
+    want = np.array(ref.samples)
+    assert np.array_equal(r0["samples"][:, 0], want[:, 0]) and np.array_equal(r0["samples"][:, 3], want[:, 3])
+    assert np.allclose(r0["samples"][:, 1:3], want[:, 1:3], rtol=1e-10)
