@@ -963,6 +963,9 @@ static int launch_prox_split(const ProxArgs &a, cudaStream_t st) {
     if (S / v.G > kPwMaxQ * (int64_t)(v.fast ? 1 : kThreads / 8))
         return fail(BSGD_EINVAL, "image too large for the pairwise tree (%lld voxels)", (long long)a.N);
     v.ctl = (FgpCtl *)(a.red + (size_t)kMaxPartials * kPwMaxK);
+    // the control block shares the reduction buffer with the other prox kernels:
+    // clear it (the folded decisions count arriving CTAs in it)
+    CU(cudaMemsetAsync(v.ctl, 0, sizeof(FgpCtl), st));
     double *part = a.red;
     // p = q = 0 (tv.py:198-201): the first iteration's passes read them as literal
     // zeros (v.zero) and write every voxel of c and q, so nothing is cleared; only
@@ -984,41 +987,58 @@ static int launch_prox_split(const ProxArgs &a, cudaStream_t st) {
             else slab_init_kernel<DIM, false><<<v.G, kThreads, 0, st>>>(v, part);
         }
     };
-    auto dual = [&]() {
-        if (fast) slab_dual_kernel<DIM, true><<<v.G, kThreads, slab_smem<KD>(true), st>>>(v, 0.0, part);
-        else slab_dual_kernel<DIM, false><<<v.G, kThreads, 0, st>>>(v, 0.0, part);
-    };
-    v.when = 0;
-    sums2(false);
-    split_decide_kernel<DIM, 2><<<1, kThreads, 0, st>>>(v, 0, 0, part);
-    // candidate as two passes through the u field (f[kProxFields - 1]) for volumes:
-    // 256^3 candidate 0.55-0.65 ms fused (issue-bound) -> u + c passes
+    // volumes: the candidate reads a stored u field (f[kProxFields - 1]) instead of
+    // evaluating u = b + w div src four times per voxel (256^3: 0.55-0.65 ms fused,
+    // issue-bound), and the dual pass writes the next iteration's u' from q' in
+    // the same sweep, so an iteration is two passes (u is recomputed only for
+    // the first candidate and after a restart, from p)
     const bool two_pass = DIM == 3 && getenv_candidate_fused() == 0;
     double *ufield = a.f[kProxFields - 1];
-    auto candidate = [&](int from_p) {
+    auto dual = [&]() {
         if (two_pass) {
-            slab_u_kernel<DIM><<<grid, kThreads, 0, st>>>(v, from_p, ufield);
-            slab_cand_u_kernel<DIM><<<grid, kThreads, 0, st>>>(v, from_p, ufield);
+            if (fast) slab_dual_u_kernel<DIM, true><<<v.G, kThreads, slab_smem<KD>(true), st>>>(v, part, ufield);
+            else slab_dual_u_kernel<DIM, false><<<v.G, kThreads, 0, st>>>(v, part, ufield);
         } else {
+            if (fast) slab_dual_kernel<DIM, true><<<v.G, kThreads, slab_smem<KD>(true), st>>>(v, 0.0, part);
+            else slab_dual_kernel<DIM, false><<<v.G, kThreads, 0, st>>>(v, 0.0, part);
+        }
+    };
+    // every sum pass takes its own decision in its last CTA (slab_fold_decide):
+    // per FGP iteration 2 launches on the main path and 2 (returning at once
+    // unless a restart was decided) on the restart path
+    v.when = 0;
+    v.fold_stage = 0;
+    v.fold_it = 0;
+    sums2(false);
+    auto candidate = [&](int from_p, bool need_u) {
+        if (two_pass && !from_p) {
+            if (need_u) slab_u_kernel<DIM><<<grid, kThreads, 0, st>>>(v, from_p, ufield);
+            slab_cand_u_kernel<DIM><<<grid, kThreads, 0, st>>>(v, from_p, ufield);
+        } else {   // restarts (rare) take the one-pass candidate from p
             slab_candidate_kernel<DIM><<<grid, kThreads, 0, st>>>(v, from_p);
         }
     };
     for (int it = 0; it < a.max_iters; ++it) {
         v.zero = it == 0 ? 1 : 0;
+        v.fold_it = it;
         v.when = 1;  // unless converged
-        candidate(0);
+        v.fold_stage = -1;
+        candidate(0, it == 0);   // later iterations: u' of the last accepted dual pass
+        v.fold_stage = 1;
         dual();
-        split_decide_kernel<DIM, KD><<<1, kThreads, 0, st>>>(v, 1, it, part);
         v.when = 2;  // only on a restart
-        candidate(1);
+        v.fold_stage = -1;
+        candidate(1, true);
+        v.fold_stage = 2;
         dual();
-        split_decide_kernel<DIM, KD><<<1, kThreads, 0, st>>>(v, 2, it, part);
     }
     v.when = 0;
     v.zero = 0;
+    v.fold_stage = -1;
     slab_finalize_kernel<DIM><<<grid, kThreads, 0, st>>>(v);
+    v.fold_stage = 3;
     sums2(true);
-    split_decide_kernel<DIM, 2><<<1, kThreads, 0, st>>>(v, 3, 0, part);
+    v.fold_stage = -1;
     split_output_kernel<DIM><<<grid, kThreads, 0, st>>>(v);
     LAUNCHED();
     return BSGD_OK;
@@ -1433,6 +1453,7 @@ static int slab_ctx(const bsgd_slab *s, SlabCtx &c, bool need_weight = true) {
     }
     c.v.ilv = 0;
     c.v.ilv_z0 = 0;
+    c.v.fold_stage = -1;
     if (s->flags & BSGD_SLAB_INTERLEAVED) {   // solver vectors: this rank's slices, interleaved
         const int64_t hw = s->height * s->width;
         if (D <= 1 || s->offset % hw || s->count % hw)

@@ -386,4 +386,63 @@ __device__ __forceinline__ int pw_cta_direct(int ds, F &f, double *leafv, double
     return Q;
 }
 
+// Balanced pairwise tree over count (a power of two) values v[i * K] in index
+// order, by one warp: lane l folds its count/32 consecutive values with a
+// balanced local tree, then xor butterflies combine lanes (2l, 2l+1), ...;
+// the additions are commutative, so every lane ends with the bits of the
+// (2i, 2i+1)-paired tree that pw_smem_tree computes.  count < 32: lanes
+// >= count carry duplicates that never reach lanes < count.
+// balanced tree over P consecutive values (P a power of two), fully unrolled
+template <int P, class L>
+__device__ __forceinline__ double fold_run(const L &ld, int base) {
+    double loc[P];
+#pragma unroll
+    for (int i = 0; i < P; ++i) loc[i] = ld(base + i);
+#pragma unroll
+    for (int wdt = P; wdt > 1; wdt >>= 1)
+#pragma unroll
+        for (int i = 0; i < wdt / 2; ++i) loc[i] = rn_add(loc[2 * i], loc[2 * i + 1]);
+    return loc[0];
+}
+
+template <int K, bool GLOBAL>
+__device__ __forceinline__ double warp_pw_tree(const double *v, int count, int lane) {
+    auto ld = [&](int i) { return GLOBAL ? __ldcg(v + (size_t)i * K) : v[(size_t)i * K]; };
+    double acc;
+    int levels = count;
+    if (count >= 32) {
+        const int per = count >> 5, base = lane * per;
+        switch (per) {
+            case 1: acc = fold_run<1>(ld, base); break;
+            case 2: acc = fold_run<2>(ld, base); break;
+            case 4: acc = fold_run<4>(ld, base); break;
+            case 8: acc = fold_run<8>(ld, base); break;
+            default: acc = fold_run<16>(ld, base); break;   // count <= 512 (checked at launch)
+        }
+        levels = 32;
+    } else {
+        acc = ld(lane < count ? lane : 0);
+    }
+    for (int off = 1; off < levels; off <<= 1) acc = rn_add(acc, __shfl_xor_sync(0xffffffffu, acc, off));
+    return acc;
+}
+
+// pw_top by warps: warp k < K folds sum k of the G CTA partials (G a power of two,
+// <= 512) with warp_pw_tree -- the same balanced tree as pw_top's, no CTA-wide
+// barriers per level.  Every thread receives the totals.  `sm` holds K doubles.
+template <int K>
+__device__ __forceinline__ void pw_top_warps(int ds, int G, const double *part, double *sm, double (&out)[K]) {
+    const int64_t S = (int64_t)1 << ds;
+    const int cnt = (int)(S < (int64_t)G ? S : (int64_t)G);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = (int)blockDim.x >> 5;
+    for (int k = warp; k < K; k += nw) {
+        const double v = warp_pw_tree<K, true>(part + k, cnt, lane);
+        if (lane == 0) sm[k] = v;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < K; ++k) out[k] = sm[k];
+    __syncthreads();
+}
+
 }  // namespace bsgd

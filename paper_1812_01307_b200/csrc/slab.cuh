@@ -38,6 +38,7 @@ namespace bsgd {
 struct FgpCtl {
     double phi_prev, tv_b, t_mom, t_next, beta, tv_out;
     int32_t iters, restarts, done, parity, restart, fell;
+    uint32_t arrive;   // CTAs of the current sum pass that finished (folded decide)
 };
 
 struct SlabView {
@@ -57,6 +58,9 @@ struct SlabView {
     // > 0 = the rank's own slices in the interleaved order of A2 (x) I_{ilv}
     // (vec[(p mod H W) * ilv + p / (H W) - z0], slice ownership of configs[4])
     int64_t ilv, ilv_z0;
+    // split prox: the sum pass's last CTA to finish runs the decision of stage
+    // fold_stage (iteration fold_it) itself -- no separate decide launch; -1: off
+    int fold_stage, fold_it;
 };
 
 __device__ __forceinline__ int64_t slab_vec_index(const SlabView &s, int64_t p) {
@@ -95,6 +99,86 @@ __device__ __forceinline__ SlabRoles<DIM> slab_roles(const SlabView &s) {
     return r;
 }
 
+__device__ __forceinline__ void fgp_next_beta(FgpCtl &c) {
+    c.t_next = 0.5 * (1.0 + sqrt(rn_add(1.0, rn_mul(rn_mul(4.0, c.t_mom), c.t_mom))));
+    c.beta = (c.t_mom - 1.0) / c.t_next;
+}
+
+// stage 0: after the setup sums; 1: after the candidate's dual pass; 2: after
+// the restart's dual pass; 3: after the energy sums (fallback decision, outputs).
+// The same scalar code as fgp_kernel; v = the stage's global numpy-order sums.
+template <int DIM>
+__device__ __forceinline__ void fgp_decide(FgpCtl &c, const ProxArgs &a, int stage, int it, const double *v) {
+    if (stage == 0) {
+        c.phi_prev = v[0];
+        c.tv_b = v[1];
+        c.t_mom = 1.0;
+        c.tv_out = 0.0;
+        c.iters = c.restarts = c.done = c.parity = c.restart = c.fell = 0;
+        fgp_next_beta(c);
+        if (a.dual != nullptr) a.dual[0] = c.phi_prev;
+        return;
+    }
+    if (stage == 3) {
+        const double two_w = 2.0 * a.w;
+        const double obj_out = rn_add(v[0], rn_mul(two_w, v[1]));
+        const double obj_b = rn_add(0.0, rn_mul(two_w, c.tv_b));
+        c.fell = obj_out > obj_b ? 1 : 0;
+        c.tv_out = v[1];
+        if (a.scal != nullptr) {
+            a.scal[0] = c.fell ? c.tv_b : v[1];
+            a.scal[1] = c.iters; a.scal[2] = c.restarts; a.scal[3] = c.done; a.scal[4] = c.fell;
+        }
+        if (a.info != nullptr) {
+            a.info[0] = c.iters; a.info[1] = c.done; a.info[2] = c.restarts; a.info[3] = c.fell;
+        }
+        return;
+    }
+    const double phi = v[0];
+    if (stage == 1 && phi > c.phi_prev) {  // restart from the last accepted point (tv.py:217-231)
+        c.restart = 1;
+        ++c.restarts;
+        c.t_mom = 1.0;
+        fgp_next_beta(c);
+        return;
+    }
+    c.restart = 0;
+    c.parity ^= 1;  // p <- c
+    c.phi_prev = (c.phi_prev < phi) ? c.phi_prev : phi;
+    c.t_mom = c.t_next;
+    c.iters = it + 1;
+    if (a.dual != nullptr) a.dual[it + 1] = c.phi_prev;
+    double ch2 = rn_add(v[1], v[2]), sc2 = rn_add(v[1 + DIM], v[2 + DIM]);
+    if constexpr (DIM == 3) { ch2 = rn_add(ch2, v[3]); sc2 = rn_add(sc2, v[6]); }
+    const double change = sqrt(ch2), scale = sqrt(sc2);
+    const double floor_scale = (1e-30 > scale) ? 1e-30 : scale;
+    if (change <= a.tol * floor_scale) c.done = 1;
+    else fgp_next_beta(c);
+}
+
+// The last CTA of a sum pass (all CTAs' partials visible after their fences)
+// folds the CTA partials in pw_top's order and takes the stage's decision.
+template <int DIM, int K>
+__device__ __forceinline__ void slab_fold_decide(const SlabView &s, const double *part) {
+    if (s.fold_stage < 0) return;
+    __shared__ int last;
+    __shared__ double sm[kPwMaxK];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        last = atomicAdd(&s.ctl->arrive, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    double v[K];
+    pw_top_warps<K>(s.ds, s.G, part, sm, v);
+    if (threadIdx.x == 0) {
+        fgp_decide<DIM>(*s.ctl, s.a, s.fold_stage, s.fold_it, v);
+        s.ctl->arrive = 0;
+    }
+}
+
 // DualCommitTerms over the slab: local index i -> voxel off + i
 template <int DIM>
 struct DualSlabTerms : DualCommitTerms<DIM> {
@@ -108,6 +192,52 @@ struct DualSlabTerms : DualCommitTerms<DIM> {
     __device__ __forceinline__ void operator()(int64_t i, double (&t)[1 + 2 * DIM]) const {
         Base::term(off + i, Base::load(off + i), t);
     }
+};
+
+// The dual pass of the single-GPU split prox also writes u' = b + w div q' for the
+// NEXT iteration's candidate (slab_cand_u_kernel), so no separate u pass runs
+// between them: q' at the three forward neighbours is recomputed here from c
+// (already loaded for div c) and p there (three extra loads, L1 / L2 hits) with
+// the very operations the neighbours' own threads commit -- the same bits.
+template <int DIM>
+struct DualSlabTermsU : DualSlabTerms<DIM> {
+    using Base = DualCommitTerms<DIM>;
+    double *U;
+    struct L {
+        typename Base::L l;
+        double pn[DIM];
+    };
+    __device__ __forceinline__ L load(int64_t i) const {
+        L x;
+        const int64_t p = this->off + i;
+        x.l = Base::load(p);
+        int64_t z, s, t;
+        split_index<DIM>(p, this->H, this->W, z, s, t);
+        const int64_t coord[3] = {z, s, t};
+        const int64_t ext[3] = {this->D, this->H, this->W};
+        const int64_t step[3] = {this->H * this->W, this->W, 1};
+#pragma unroll
+        for (int k = 0; k < DIM; ++k) {
+            const int ax = 3 - DIM + k;
+            x.pn[k] = (this->pzero || coord[ax] + 1 >= ext[ax]) ? 0.0 : ldcg(this->P[k] + p + step[ax]);
+        }
+        return x;
+    }
+    __device__ __forceinline__ void term(int64_t i, const L &x, double (&t)[1 + 2 * DIM]) const {
+        const int64_t p = this->off + i;
+        Base::term(p, x.l, t);
+        // div q' in div_at's order; q'_k = c_k + beta (c_k - p_k) here and at the forward neighbour
+        double d = 0.0;
+#pragma unroll
+        for (int k = 0; k < DIM; ++k) {
+            const double qh = rn_add(x.l.here[k], rn_mul(this->beta, rn_sub(x.l.here[k], x.l.p[k])));
+            const double back = (x.l.first >> k) & 1u ? 0.0 : qh;
+            const double qn = rn_add(x.l.next[k], rn_mul(this->beta, rn_sub(x.l.next[k], x.pn[k])));
+            d = (k == 0) ? rn_sub(qn, back) : rn_sub(rn_add(d, qn), back);
+        }
+        U[p] = rn_add(x.l.b, rn_mul(this->w, d));
+    }
+    __device__ __forceinline__ void operator()(int64_t i, double (&t)[1 + 2 * DIM]) const { term(i, load(i), t); }
 };
 
 template <int K, bool FAST, class F>
@@ -149,6 +279,7 @@ __global__ void __launch_bounds__(kThreads) slab_init_kernel(SlabView s, double 
         t[1] = tv_term<DIM>(b, p, H, W, false);
     };
     slab_sum<2, FAST>(s, f, part);
+    slab_fold_decide<DIM, 2>(s, part);
 }
 
 // c = proj(src + step grad(b + w div src)) on the own voxels (tv.py:207-214)
@@ -226,6 +357,23 @@ __global__ void __launch_bounds__(kThreads) slab_cand_u_kernel(SlabView s, int f
 // 4 CTAs per SM (60 registers, no spills): the 512 CTAs of a 256^3 pass are
 // resident at once (256^3 prox 6.73 -> 6.23-6.29 ms against 2 per SM)
 template <int DIM, bool FAST>
+__global__ void __launch_bounds__(kThreads, 4) slab_dual_u_kernel(SlabView s, double *part, double *u) {
+    if (slab_skip(s)) return;
+    const SlabRoles<DIM> r = slab_roles<DIM>(s);
+    DualSlabTermsU<DIM> f;
+    f.b = s.a.b; f.w = s.a.w;
+    f.beta = s.ctl->beta;
+    f.D = s.a.D; f.H = s.a.H; f.W = s.a.W;
+#pragma unroll
+    for (int k = 0; k < DIM; ++k) { f.P[k] = r.P[k]; f.Q[k] = r.Q[k]; f.C[k] = r.C[k]; }
+    f.off = s.off;
+    f.pzero = s.zero != 0;
+    f.U = u;
+    slab_sum<1 + 2 * DIM, FAST>(s, f, part);
+    slab_fold_decide<DIM, 1 + 2 * DIM>(s, part);
+}
+
+template <int DIM, bool FAST>
 __global__ void __launch_bounds__(kThreads, 4) slab_dual_kernel(SlabView s, double beta, double *part) {
     if (slab_skip(s)) return;
     const SlabRoles<DIM> r = slab_roles<DIM>(s);
@@ -238,6 +386,7 @@ __global__ void __launch_bounds__(kThreads, 4) slab_dual_kernel(SlabView s, doub
     f.off = s.off;
     f.pzero = s.zero != 0;
     slab_sum<1 + 2 * DIM, FAST>(s, f, part);
+    slab_fold_decide<DIM, 1 + 2 * DIM>(s, part);
 }
 
 // u = b + w div p (tv.py:250)
@@ -265,6 +414,7 @@ __global__ void __launch_bounds__(kThreads) slab_energy_kernel(SlabView s, doubl
         t[1] = tv_term<DIM>(u, p, H, W, false);
     };
     slab_sum<2, FAST>(s, f, part);
+    slab_fold_decide<DIM, 2>(s, part);
 }
 
 // x_next on the own voxels (identity fallback when fell) and the epoch
@@ -301,69 +451,12 @@ __global__ void slab_sum4_kernel(const double *part, int n, double *out) {
 
 // ---- split prox: device-side decisions ----
 
-__device__ __forceinline__ void fgp_next_beta(FgpCtl &c) {
-    c.t_next = 0.5 * (1.0 + sqrt(rn_add(1.0, rn_mul(rn_mul(4.0, c.t_mom), c.t_mom))));
-    c.beta = (c.t_mom - 1.0) / c.t_next;
-}
-
-// stage 0: after the setup sums; 1: after the candidate's dual pass; 2: after
-// the restart's dual pass; 3: after the energy sums (fallback decision, outputs).
-// The same scalar code as fgp_kernel; v = the stage's global numpy-order sums.
-template <int DIM>
-__device__ __forceinline__ void fgp_decide(FgpCtl &c, const ProxArgs &a, int stage, int it, const double *v) {
-    if (stage == 0) {
-        c.phi_prev = v[0];
-        c.tv_b = v[1];
-        c.t_mom = 1.0;
-        c.tv_out = 0.0;
-        c.iters = c.restarts = c.done = c.parity = c.restart = c.fell = 0;
-        fgp_next_beta(c);
-        if (a.dual != nullptr) a.dual[0] = c.phi_prev;
-        return;
-    }
-    if (stage == 3) {
-        const double two_w = 2.0 * a.w;
-        const double obj_out = rn_add(v[0], rn_mul(two_w, v[1]));
-        const double obj_b = rn_add(0.0, rn_mul(two_w, c.tv_b));
-        c.fell = obj_out > obj_b ? 1 : 0;
-        c.tv_out = v[1];
-        if (a.scal != nullptr) {
-            a.scal[0] = c.fell ? c.tv_b : v[1];
-            a.scal[1] = c.iters; a.scal[2] = c.restarts; a.scal[3] = c.done; a.scal[4] = c.fell;
-        }
-        if (a.info != nullptr) {
-            a.info[0] = c.iters; a.info[1] = c.done; a.info[2] = c.restarts; a.info[3] = c.fell;
-        }
-        return;
-    }
-    const double phi = v[0];
-    if (stage == 1 && phi > c.phi_prev) {  // restart from the last accepted point (tv.py:217-231)
-        c.restart = 1;
-        ++c.restarts;
-        c.t_mom = 1.0;
-        fgp_next_beta(c);
-        return;
-    }
-    c.restart = 0;
-    c.parity ^= 1;  // p <- c
-    c.phi_prev = (c.phi_prev < phi) ? c.phi_prev : phi;
-    c.t_mom = c.t_next;
-    c.iters = it + 1;
-    if (a.dual != nullptr) a.dual[it + 1] = c.phi_prev;
-    double ch2 = rn_add(v[1], v[2]), sc2 = rn_add(v[1 + DIM], v[2 + DIM]);
-    if constexpr (DIM == 3) { ch2 = rn_add(ch2, v[3]); sc2 = rn_add(sc2, v[6]); }
-    const double change = sqrt(ch2), scale = sqrt(sc2);
-    const double floor_scale = (1e-30 > scale) ? 1e-30 : scale;
-    if (change <= a.tol * floor_scale) c.done = 1;
-    else fgp_next_beta(c);
-}
-
 template <int DIM, int K>
 __global__ void __launch_bounds__(kThreads) split_decide_kernel(SlabView s, int stage, int it, const double *part) {
     if (slab_skip(s)) return;
-    __shared__ double sm[kPwMaxQ * kPwMaxK];
+    __shared__ double sm[kPwMaxK];
     double v[K];
-    pw_top<K>(s.ds, s.G, part, sm, v);
+    pw_top_warps<K>(s.ds, s.G, part, sm, v);
     if (threadIdx.x != 0) return;
     fgp_decide<DIM>(*s.ctl, s.a, stage, it, v);
 }
