@@ -990,8 +990,8 @@ static int launch_prox_split(const ProxArgs &a, cudaStream_t st) {
     // volumes: the candidate reads a stored u field (f[kProxFields - 1]) instead of
     // evaluating u = b + w div src four times per voxel (256^3: 0.55-0.65 ms fused,
     // issue-bound), and the dual pass writes the next iteration's u' from q' in
-    // the same sweep, so an iteration is two passes (u is recomputed only for
-    // the first candidate and after a restart, from p)
+    // the same sweep, so an iteration is two passes (the first candidate reads b;
+    // a restart takes the one-pass candidate from p)
     const bool two_pass = DIM == 3 && getenv_candidate_fused() == 0;
     double *ufield = a.f[kProxFields - 1];
     auto dual = [&]() {
@@ -1010,10 +1010,9 @@ static int launch_prox_split(const ProxArgs &a, cudaStream_t st) {
     v.fold_stage = 0;
     v.fold_it = 0;
     sums2(false);
-    auto candidate = [&](int from_p, bool need_u) {
+    auto candidate = [&](int from_p) {
         if (two_pass && !from_p) {
-            if (need_u) slab_u_kernel<DIM><<<grid, kThreads, 0, st>>>(v, from_p, ufield);
-            slab_cand_u_kernel<DIM><<<grid, kThreads, 0, st>>>(v, from_p, ufield);
+            slab_cand_u_kernel<DIM><<<grid, kThreads, 0, st>>>(v, 0, ufield);
         } else {   // restarts (rare) take the one-pass candidate from p
             slab_candidate_kernel<DIM><<<grid, kThreads, 0, st>>>(v, from_p);
         }
@@ -1023,12 +1022,12 @@ static int launch_prox_split(const ProxArgs &a, cudaStream_t st) {
         v.fold_it = it;
         v.when = 1;  // unless converged
         v.fold_stage = -1;
-        candidate(0, it == 0);   // later iterations: u' of the last accepted dual pass
+        candidate(0);            // u' of the last accepted dual pass (b itself at it = 0)
         v.fold_stage = 1;
         dual();
         v.when = 2;  // only on a restart
         v.fold_stage = -1;
-        candidate(1, true);
+        candidate(1);
         v.fold_stage = 2;
         dual();
     }

@@ -300,32 +300,12 @@ __global__ void __launch_bounds__(kThreads) slab_candidate_kernel(SlabView s, in
     }
 }
 
-// The candidate as two passes over a stored u field (split prox of one GPU,
-// where u's neighbours are not rewritten by another rank): u = b + w div src once
-// per voxel, then c = proj(src + step grad u) from u and its three backward
-// neighbours.  The fused candidate evaluates u four times per voxel (~590
-// instructions, issue-bound); the same operations in the same order, so c is
-// bit-identical to slab_candidate_kernel's.
-template <int DIM>
-__global__ void __launch_bounds__(kThreads) slab_u_kernel(SlabView s, int from_p, double *u) {
-    if (slab_skip(s)) return;
-    const SlabRoles<DIM> r = slab_roles<DIM>(s);
-    const double *src[DIM];
-#pragma unroll
-    for (int k = 0; k < DIM; ++k) src[k] = from_p ? r.P[k] : r.Q[k];
-    const double wz = rn_mul(s.a.w, 0.0);
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < s.n; i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t p = s.off + i;
-        if (s.zero) {
-            u[p] = rn_add(__ldg(s.a.b + p), wz);
-        } else {
-            int64_t z, y, t;
-            split_index<DIM>(p, s.a.H, s.a.W, z, y, t);
-            u[p] = u_at<DIM>(s.a, src, z, y, t);
-        }
-    }
-}
-
+// The candidate from a stored u field (split prox of one GPU, where u's
+// neighbours are not rewritten by another rank; u = b + w div q is written by
+// the previous dual pass, slab_dual_u_kernel): c = proj(q + step grad u) from u
+// and its three backward neighbours.  The fused candidate evaluates u four times
+// per voxel (~590 instructions, issue-bound); the same operations in the same
+// order, so c is bit-identical to slab_candidate_kernel's.
 template <int DIM>
 __global__ void __launch_bounds__(kThreads) slab_cand_u_kernel(SlabView s, int from_p, const double *u) {
     if (slab_skip(s)) return;
@@ -334,6 +314,10 @@ __global__ void __launch_bounds__(kThreads) slab_cand_u_kernel(SlabView s, int f
 #pragma unroll
     for (int k = 0; k < DIM; ++k) src[k] = from_p ? r.P[k] : r.Q[k];
     const int64_t H = s.a.H, W = s.a.W;
+    // first iteration (q = 0): u = b + w * 0 equals b except that -0 becomes +0,
+    // and every gradient built from it gives the same c (0 + step * (+-0) = +0),
+    // so the candidate reads b and no u pass runs
+    if (s.zero) u = s.a.b;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < s.n; i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t p = s.off + i;
         int64_t z, y, t;
