@@ -413,3 +413,31 @@ def test_ct_full_size_products_consistent(B, index):
             r0, r1 = op.partition.row_range(i)
             acc += op.block_matvec_transpose(i, j, w[r0:r1])
         assert rel(atw[c0:c1], acc) < 1e-12
+
+
+def test_prox_workspace_per_stream_and_thread(B):
+    """Concurrent proxes never share a workspace: the cache key holds the current
+    stream and thread; the same stream reuses its workspace."""
+    import threading
+    import torch
+    tv = B[1]
+    dev = torch.device("cuda", 0)
+    w0 = tv.prox_workspace(64, 64, dev)
+    assert tv.prox_workspace(64, 64, dev) is w0
+    s1 = torch.cuda.Stream(device=dev)
+    with torch.cuda.stream(s1):
+        w1 = tv.prox_workspace(64, 64, dev)
+    assert w1 is not w0
+    other = []
+    th = threading.Thread(target=lambda: other.append(tv.prox_workspace(64, 64, dev)))
+    th.start()
+    th.join()
+    assert other[0] is not w0
+    # two proxes of the same image on two streams give the same bits
+    img = torch.rand(64, 64, dtype=torch.float64, device=dev)
+    outs = []
+    for st in (torch.cuda.current_stream(dev), s1):
+        with torch.cuda.stream(st):
+            outs.append(tv.tv_prox(img, 0.1, tv.ProxSettings(20, 1e-9)).clone())
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0], outs[1])

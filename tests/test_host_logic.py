@@ -150,3 +150,60 @@ def test_parallel_beam_chord_lengths():
                 lo, hi = max(lo, min(t1, t2)), min(hi, max(t1, t2))
             chord = max(0.0, hi - lo)
             assert abs(sums[ang * 23 + b] - chord) < 1e-9
+
+
+def test_canonical_csr_sums_float32_duplicates_in_float64():
+    """BlockOperator's canonical form (blockops.py:124-126): duplicates are summed in
+    float64 as the reference does; float32 input stays float32 only when every
+    summed value round-trips exactly, and an explicit dtype is honoured."""
+    from scipy import sparse
+    from paper_1812_01307_b200.blockops import _canonical_csr
+    # 0.1f + 0.2f is not exactly representable in float32
+    a = sparse.csr_array((np.array([0.1, 0.2, 3.0], dtype=np.float32), np.array([1, 1, 0]), np.array([0, 2, 3])),
+                         shape=(2, 2))
+    ref = sparse.csr_array(a.copy(), dtype=np.float64)   # (sum_duplicates mutates shared index arrays)
+    ref.sum_duplicates()
+    ref.sort_indices()
+    c = _canonical_csr(a)
+    assert c.dtype == np.float64 and np.array_equal(c.toarray(), ref.toarray())
+    # exact sums keep float32
+    b = sparse.csr_array((np.array([0.5, 0.25, 3.0], dtype=np.float32), np.array([1, 1, 0]), np.array([0, 2, 3])),
+                         shape=(2, 2))
+    cb = _canonical_csr(b)
+    assert cb.dtype == np.float32 and cb.toarray()[0, 1] == 0.75
+    # canonical float32 input is kept as is; explicit dtype wins
+    d = sparse.random(30, 20, density=0.3, format="csr", dtype=np.float32, random_state=1)
+    assert _canonical_csr(d).dtype == np.float32
+    assert _canonical_csr(d, np.float64).dtype == np.float64
+    with pytest.raises(ValueError):
+        _canonical_csr(d, np.int32)
+
+
+def test_distributed_driver_rejects_unsupported_modes():
+    """DistributedBSGD raises on alpha / gamma < 1 and enforce_decrease instead of
+    silently running a different algorithm (solvers.py:186-195, 325-333)."""
+    import types
+    from paper_1812_01307_b200 import parallel
+    from paper_1812_01307_b200.solvers import SolverConfig
+    shard = types.SimpleNamespace()
+    for kw in ({"alpha": 0.5}, {"gamma": 0.5}, {"enforce_decrease": True}):
+        with pytest.raises(ValueError):
+            parallel.DistributedBSGD(shard, np.zeros(4), SolverConfig(mu=0.1, **kw))
+
+
+def test_slab_program_is_pw_combine():
+    """The postfix program bsgd_slab_decide runs reproduces pw_combine bit for bit."""
+    from paper_1812_01307_b200 import parallel
+    rng = np.random.default_rng(0)
+    for nvox, world, halo in ((1 << 20, 8, 4096), (1 << 16, 3, 256), (5000, 2, 50), (1 << 18, 5, 512)):
+        slabs = parallel.prox_slabs(nvox, world, halo)
+        vals = rng.standard_normal((world, 3)) * 10 ** rng.uniform(-8, 8, (world, 3))
+        want = parallel.pw_combine(nvox, slabs, vals)
+        stack = []
+        for op in parallel.slab_program(nvox, slabs):
+            if op >= 0:
+                stack.append(list(vals[op]))
+            else:
+                b, a = stack.pop(), stack.pop()
+                stack.append([x + y for x, y in zip(a, b)])
+        assert len(stack) == 1 and stack[0] == want
