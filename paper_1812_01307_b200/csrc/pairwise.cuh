@@ -417,7 +417,20 @@ __device__ __forceinline__ double warp_pw_tree(const double *v, int count, int l
             case 2: acc = fold_run<2>(ld, base); break;
             case 4: acc = fold_run<4>(ld, base); break;
             case 8: acc = fold_run<8>(ld, base); break;
-            default: acc = fold_run<16>(ld, base); break;   // count <= 512 (checked at launch)
+            case 16: acc = fold_run<16>(ld, base); break;
+            default: {   // 32 .. 128 per lane (count <= 4096): a balanced tree over runs of 16
+                const int nc = per >> 4;
+                double c[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) c[j] = j < nc ? fold_run<16>(ld, base + 16 * j) : 0.0;
+#pragma unroll
+                for (int wdt = 8; wdt > 1; wdt >>= 1)
+                    if (wdt <= nc)
+#pragma unroll
+                        for (int i = 0; i < wdt / 2; ++i) c[i] = rn_add(c[2 * i], c[2 * i + 1]);
+                acc = c[0];
+                break;
+            }
         }
         levels = 32;
     } else {
