@@ -2499,7 +2499,13 @@ int bsgd_epoch(const bsgd_plan *p, const bsgd_epoch_args *a, void *stream) {
         if (fl & BSGD_EP_R_NEXT)
             rc = DISPATCH_V(p, launch_fwd<V>(p, a->x_k, EpiResid{a->y, a->r_next}, ws.rpart, ws.ctl + 2, st));
         TIMING_MARK(1);
-        if (!rc) rc = DISPATCH_V(p, launch_tr<V>(p, a->r_k, es, ws.xpart, ws.ctl, st));
+        if (!rc) {
+            if (prox)   // the prox's output pass writes the step statistics
+                rc = DISPATCH_V(p, launch_tr<V>(p, a->r_k, EpiStepImg{a->g, a->x_k, a->mu, ws.uimg, a->perm}, nullptr,
+                                                nullptr, st));
+            else
+                rc = DISPATCH_V(p, launch_tr<V>(p, a->r_k, es, ws.xpart, ws.ctl, st));
+        }
     }
     if (fl & BSGD_EP_SKIP_GRAD) TIMING_MARK(1);
     TIMING_MARK(2);

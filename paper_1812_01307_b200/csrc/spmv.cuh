@@ -80,6 +80,26 @@ struct EpiStep {
     }
 };
 
+// The step with the TV prox on (lam > 0): g = 2 s and the prox input b = x_k + mu g
+// scattered to image order; no statistics (the prox's output pass computes them
+// from x_next), so no accumulators and no partials -- the K2 kernels keep fewer
+// live registers (gtile_kernel<float, *, EpiStep> spilled 60-64 B at its
+// 80-register cap).
+struct EpiStepImg {
+    double *g;
+    const double *xk;
+    double mu;
+    double *uimg;
+    const int64_t *perm;   // NULL = identity
+    static constexpr int K = 0;
+    __device__ __forceinline__ void operator()(int64_t col, double s) {
+        const double gg = 2.0 * s;
+        g[col] = gg;
+        uimg[perm != nullptr ? perm[col] : col] = rn_add(xk[col], rn_mul(mu, gg));
+    }
+    __device__ __forceinline__ void flush(double *) {}
+};
+
 struct EpiNone {
     static constexpr int K = 0;
     __device__ __forceinline__ void operator()(int64_t, double) {}
