@@ -306,8 +306,8 @@ __global__ void __launch_bounds__(kThreads) slab_candidate_kernel(SlabView s, in
 // and its three backward neighbours.  The fused candidate evaluates u four times
 // per voxel (~590 instructions, issue-bound); the same operations in the same
 // order, so c is bit-identical to slab_candidate_kernel's.
-template <int DIM>
-__global__ void __launch_bounds__(kThreads) slab_cand_u_kernel(SlabView s, int from_p, const double *u) {
+template <int DIM, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) slab_cand_u_kernel(SlabView s, int from_p, const double *u) {
     if (slab_skip(s)) return;
     const SlabRoles<DIM> r = slab_roles<DIM>(s);
     const double *src[DIM];
