@@ -529,7 +529,11 @@ def run_multi(args):
     drv = parallel.DistributedBSGD(shard, y_full, cfg, history_capacity=4 * steps + args.warmup + 64)
     for _ in range(args.warmup):
         drv.epoch_step()
-    graphed = drv.capture(2)
+    # CUDA-graph replay with the NCCL all-reduce inside has run at world size 1
+    # only (one GPU reachable); across ranks the eager epochs are used unless
+    # BSGD_DIST_GRAPH=1 (a rank's epoch at configs[3] is ~0.8 ms of GPU work at 8
+    # GPUs, well above the ~0.15 ms of host launches, so eager loses little)
+    graphed = (world == 1 or os.environ.get("BSGD_DIST_GRAPH") == "1") and drv.capture(2)
     if graphed:
         drv.replay()
     torch.cuda.synchronize()
@@ -620,7 +624,7 @@ def run_multi_slices(args, world, rank, local, dev):
     drv = parallel.DistributedBSGD(shard, y_full, cfg, history_capacity=4 * steps + args.warmup + 64)
     for _ in range(args.warmup):
         drv.epoch_step()
-    graphed = drv.capture(2)
+    graphed = (world == 1 or os.environ.get("BSGD_DIST_GRAPH") == "1") and drv.capture(2)
     if graphed:
         drv.replay()
     torch.cuda.synchronize()
