@@ -268,16 +268,59 @@ __global__ void __launch_bounds__(kThreads) slab_step_kernel(SlabView s, const d
 }
 
 // np.sum(b * b) and TV(b) over the own voxels (tv.py:203; tv.py:166-169 at p = 0)
+// (|v - ref|^2 or |v|^2, TV(v)) per voxel as a two-stage functor (pairwise.cuh):
+// the loads of kUnroll voxels (v and its three backward neighbours) are issued
+// before any arithmetic -- the setup / fallback-energy sums were latency-bound
+// at 1.7-2.5 TB/s as plain lambdas.  Same operations as tv_term, same bits.
+template <int DIM>
+struct TvSumTerms {
+    static constexpr bool kTwoStage = true;
+    static constexpr int kUnroll = 4;
+    const double *v, *ref;   // ref NULL: t0 = v^2 (tv.py:203), else (v - ref)^2 (tv.py:166-169)
+    int64_t off, H, W;
+    struct L {
+        double c, up, left, below;   // v at p, p - W, p - 1, p - H W (0 where absent)
+        double r;
+        unsigned has;                // bit 0: row > 0, bit 1: column > 0, bit 2: plane > 0
+    };
+    __device__ __forceinline__ L load(int64_t i) const {
+        L l;
+        const int64_t p = off + i;
+        int64_t z, s, t;
+        split_index<DIM>(p, H, W, z, s, t);
+        l.has = (s > 0 ? 1u : 0u) | (t > 0 ? 2u : 0u) | (z > 0 ? 4u : 0u);
+        l.c = __ldg(v + p);
+        l.up = s > 0 ? __ldg(v + p - W) : 0.0;
+        l.left = t > 0 ? __ldg(v + p - 1) : 0.0;
+        l.below = (DIM == 3 && z > 0) ? __ldg(v + p - H * W) : 0.0;
+        l.r = ref != nullptr ? __ldg(ref + p) : 0.0;
+        return l;
+    }
+    __device__ __forceinline__ void term(int64_t, const L &l, double (&t)[2]) const {
+        if (ref != nullptr) {
+            const double d = rn_sub(l.c, l.r);
+            t[0] = rn_mul(d, d);
+        } else {
+            t[0] = rn_mul(l.c, l.c);
+        }
+        const double dv = (l.has & 1u) ? rn_sub(l.c, l.up) : 0.0;
+        const double dh = (l.has & 2u) ? rn_sub(l.c, l.left) : 0.0;
+        if constexpr (DIM == 2) {
+            t[1] = sqrt(rn_add(rn_mul(dv, dv), rn_mul(dh, dh)));
+        } else {
+            const double dz = (l.has & 4u) ? rn_sub(l.c, l.below) : 0.0;
+            t[1] = sqrt(rn_add(rn_add(rn_mul(dz, dz), rn_mul(dv, dv)), rn_mul(dh, dh)));
+        }
+    }
+    __device__ __forceinline__ void operator()(int64_t i, double (&t)[2]) const { term(i, load(i), t); }
+};
+
 template <int DIM, bool FAST>
 __global__ void __launch_bounds__(kThreads) slab_init_kernel(SlabView s, double *part) {
-    const double *b = s.a.b;
-    const int64_t H = s.a.H, W = s.a.W, off = s.off;
-    auto f = [&](int64_t i, double (&t)[2]) {
-        const int64_t p = off + i;
-        const double bb = __ldg(b + p);
-        t[0] = rn_mul(bb, bb);
-        t[1] = tv_term<DIM>(b, p, H, W, false);
-    };
+    TvSumTerms<DIM> f;
+    f.v = s.a.b;
+    f.ref = nullptr;
+    f.off = s.off; f.H = s.a.H; f.W = s.a.W;
     slab_sum<2, FAST>(s, f, part);
     slab_fold_decide<DIM, 2>(s, part);
 }
@@ -389,14 +432,10 @@ __global__ void __launch_bounds__(kThreads) slab_finalize_kernel(SlabView s) {
 template <int DIM, bool FAST>
 __global__ void __launch_bounds__(kThreads) slab_energy_kernel(SlabView s, double *part) {
     const SlabRoles<DIM> r = slab_roles<DIM>(s);
-    const double *b = s.a.b, *u = r.u;
-    const int64_t H = s.a.H, W = s.a.W, off = s.off;
-    auto f = [&](int64_t i, double (&t)[2]) {
-        const int64_t p = off + i;
-        const double d = rn_sub(__ldg(u + p), __ldg(b + p));
-        t[0] = rn_mul(d, d);
-        t[1] = tv_term<DIM>(u, p, H, W, false);
-    };
+    TvSumTerms<DIM> f;
+    f.v = r.u;
+    f.ref = s.a.b;
+    f.off = s.off; f.H = s.a.H; f.W = s.a.W;
     slab_sum<2, FAST>(s, f, part);
     slab_fold_decide<DIM, 2>(s, part);
 }
