@@ -516,9 +516,15 @@ def run_multi(args):
     from paper_1812_01307_b200.solvers import SolverConfig
 
     world, rank, local = dist_info()
+    # one rank per GPU; the modulo only matters for the functional gloo check of
+    # the N > 1 code path with every rank on one GPU (--dist-backend gloo)
+    local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    dist.init_process_group("nccl", device_id=dev)
+    if args.dist_backend == "nccl":
+        dist.init_process_group("nccl", device_id=dev)
+    else:
+        dist.init_process_group(args.dist_backend)
     if args.multi_config == 4:
         return run_multi_slices(args, world, rank, local, dev)
     shard, y_full, meta = parallel.ct_row_slab_shard(HEADLINE, rank, world, device=dev)
@@ -807,6 +813,9 @@ def main():
                     help="multi-GPU arm: configs[3] row slabs (default) or configs[4] slice ownership")
     ap.add_argument("--force-dist", action="store_true",
                     help="run the multi-GPU (row-slab, NCCL) arm even at world size 1 (under torchrun)")
+    ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
+                    help="N > 1: gloo only to exercise the multi-rank path with all ranks on one GPU "
+                         "(a functional check, not a measurement)")
     ap.add_argument("--cpu-epochs", type=int, default=8)
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--ref-budget", type=float, default=60.0)

@@ -557,6 +557,9 @@ class DistributedBSGD:
         if (self.slab is not None and not self.slab_device) or epochs < 2 or epochs % 2 or \
                 not getattr(self.y, "is_cuda", False):
             return False
+        d = self.dist
+        if d.is_initialized() and d.get_world_size(self.group) > 1 and d.get_backend(self.group) != "nccl":
+            return False   # gloo stages device tensors through the host: not capturable
         t = self.s.t
         saved = (self.xi, self.ri, self.rows_used, self.epoch)
         g = t.cuda.CUDAGraph()
@@ -943,21 +946,37 @@ class TorchComm:
         if self.world == 1:
             return
         d = self.dist
-        ops = []
+        # gloo moves host memory only: device buffers are staged through the host
+        # there (the functional multi-rank checks); NCCL sends device memory directly
+        staged = not self.nccl and any(b.is_cuda for b in bufs)
+        ops, back = [], []
+
+        def send(t, peer):
+            ops.append(d.P2POp(d.isend, t.cpu() if staged else t, peer, self.group))
+
+        def recv(t, peer):
+            if staged:
+                tmp = self.torch.empty(t.shape, dtype=t.dtype)
+                back.append((t, tmp))
+                t = tmp
+            ops.append(d.P2POp(d.irecv, t, peer, self.group))
+
         for b in bufs:
             if lower:
                 if self.rank + 1 < self.world:
-                    ops.append(d.P2POp(d.isend, b[n:n + h], self._peer(self.rank + 1), self.group))
+                    send(b[n:n + h], self._peer(self.rank + 1))
                 if self.rank > 0:
-                    ops.append(d.P2POp(d.irecv, b[0:h], self._peer(self.rank - 1), self.group))
+                    recv(b[0:h], self._peer(self.rank - 1))
             if upper:
                 if self.rank > 0:
-                    ops.append(d.P2POp(d.isend, b[h:2 * h], self._peer(self.rank - 1), self.group))
+                    send(b[h:2 * h], self._peer(self.rank - 1))
                 if self.rank + 1 < self.world:
-                    ops.append(d.P2POp(d.irecv, b[n + h:n + 2 * h], self._peer(self.rank + 1), self.group))
+                    recv(b[n + h:n + 2 * h], self._peer(self.rank + 1))
         if ops:
             for req in d.batch_isend_irecv(ops):
                 req.wait()
+        for t, tmp in back:
+            t.copy_(tmp)
 
     def gather(self, t):
         """All ranks' copies of a small tensor, as a host array [world, len]."""
