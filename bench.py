@@ -382,7 +382,9 @@ def run_ours(args):
         else:
             cpu = port
 
-    launches = 4  # K2 (gather-tiled A^T + step), prox (1 cooperative row-walk kernel), K1 lookahead, tail
+    # K2 (gather-tiled A^T + step), prox (1 cooperative row-walk kernel), the x permute
+    # into K1's tiled gather order, K1 lookahead, tail
+    launches = 5 if op.kernel_info()["forward_order"] != "native" else 4
     secondary = None
     del st, runner, op, d
     torch.cuda.empty_cache()

@@ -165,10 +165,15 @@ int bsgd_plan_info(const bsgd_plan *plan, int64_t *rows, int64_t *cols, int64_t 
 #define BSGD_K_GTILE 3         /* gtile_kernel (gtile.cuh) */
 #define BSGD_K_STACKED 4       /* stacked_kernel (stacked.cuh) */
 #define BSGD_K_STACKED_TILE 5  /* stacked_tile_kernel (stacked.cuh) */
+#define BSGD_ORDER_NATIVE 0     /* K1 gathers in A's column order */
+#define BSGD_ORDER_TILE4 1      /* blocked K1 on an n x n image: 4 x 4 pixel tiles */
+#define BSGD_ORDER_MORTON 2     /* (experiment, BSGD_BLK_ORDER=morton) Z order */
 typedef struct bsgd_kernel_info {
     int32_t fwd_kernel, fwd_lanes;  /* A x  (K1) */
     int32_t tr_kernel, tr_lanes;    /* A^T r (K2) */
     int64_t depth;
+    int32_t fwd_order;              /* BSGD_ORDER_*: pixel order of K1's gathers */
+    int32_t reserved;
 } bsgd_kernel_info;
 int bsgd_plan_kernel_info(const bsgd_plan *plan, bsgd_kernel_info *out);
 /* In-epoch phase timing for measurement (bench.py): while enabled, every eager

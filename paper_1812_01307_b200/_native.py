@@ -49,11 +49,13 @@ SLAB_DEVICE, SLAB_MAIN, SLAB_RESTART, SLAB_INTERLEAVED = 1, 1, 2, 8
 class KernelInfo(ctypes.Structure):
     """bsgd_kernel_info (include/bsgd_b200.h)."""
     _fields_ = [("fwd_kernel", ctypes.c_int32), ("fwd_lanes", ctypes.c_int32),
-                ("tr_kernel", ctypes.c_int32), ("tr_lanes", ctypes.c_int32), ("depth", c_i64)]
+                ("tr_kernel", ctypes.c_int32), ("tr_lanes", ctypes.c_int32), ("depth", c_i64),
+                ("fwd_order", ctypes.c_int32), ("reserved", ctypes.c_int32)]
 
 
 KERNEL_NAMES = {0: "csr", 1: "blocked", 2: "blocked_compressed", 3: "gather_tiled", 4: "stacked",
                 5: "stacked_tile"}
+GATHER_ORDERS = {0: "native", 1: "tile4", 2: "morton"}
 TIMING_PHASES = ("k1_first", "k2_step", "prox", "k1_lookahead", "tail")
 
 

@@ -448,7 +448,7 @@ class BlockOperator:
         nat.call("bsgd_plan_kernel_info", self._plan, nat.ctypes.byref(ki))
         return {"forward": nat.KERNEL_NAMES[ki.fwd_kernel], "forward_lanes": int(ki.fwd_lanes),
                 "transposed": nat.KERNEL_NAMES[ki.tr_kernel], "transposed_lanes": int(ki.tr_lanes),
-                "depth": int(ki.depth)}
+                "depth": int(ki.depth), "forward_order": nat.GATHER_ORDERS[ki.fwd_order]}
 
     def set_phase_timing(self, enable: bool) -> None:
         """Record CUDA events between the phases of every eager epoch on this plan

@@ -280,9 +280,9 @@ __device__ __forceinline__ int4 blk_cols(const CsrB<V> &A, int64_t k, uint64_t p
     if constexpr (CMP) {
         const int32_t c0 = ld_stream(A.base + (k >> 2), pol);
         const uint2 d = ld_stream_u2(A.del + k, pol);
-        const int32_t c1 = c0 + (int32_t)(d.x >> 16);
-        const int32_t c2 = c1 + (int32_t)(d.y & 0xFFFFu);
-        const int32_t c3 = c2 + (int32_t)(d.y >> 16);
+        const int32_t c1 = c0 + (int32_t)(int16_t)(d.x >> 16);
+        const int32_t c2 = c1 + (int32_t)(int16_t)(d.y & 0xFFFFu);
+        const int32_t c3 = c2 + (int32_t)(int16_t)(d.y >> 16);
         return make_int4(c0, c1, c2, c3);
     } else {
         return ld_stream4(A.idx + k, pol);
@@ -350,19 +350,45 @@ __global__ void __launch_bounds__(kThreads) csr_blocked_kernel(CsrB<V> A, Epi ep
 }
 
 // compress the blocked indices: per lane-block q (entries 4q .. 4q + 3, one lane's
-// ascending columns) base[q] = first column, del[4q + m] = column m - column m-1;
-// *bad != 0 when an increment does not fit 16 bits
+// columns) base[q] = first column, del[4q + m] = column m - column m-1 as a signed
+// 16-bit step (columns ascend in A's own order, not in a renumbered pixel order);
+// *bad != 0 when a step does not fit
 __global__ void blk_compress_kernel(int64_t nq, const int32_t *idx, int32_t *base, uint16_t *del, int *bad) {
     for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nq; q += (int64_t)gridDim.x * blockDim.x) {
         const int4 c = reinterpret_cast<const int4 *>(idx)[q];
         const int64_t d1 = (int64_t)c.y - c.x, d2 = (int64_t)c.z - c.y, d3 = (int64_t)c.w - c.z;
-        if (d1 < 0 || d2 < 0 || d3 < 0 || d1 > 65535 || d2 > 65535 || d3 > 65535) atomicExch(bad, 1);
+        if (d1 < -32768 || d2 < -32768 || d3 < -32768 || d1 > 32767 || d2 > 32767 || d3 > 32767)
+            atomicExch(bad, 1);
         base[q] = c.x;
         del[4 * q] = 0;
         del[4 * q + 1] = (uint16_t)d1;
         del[4 * q + 2] = (uint16_t)d2;
         del[4 * q + 3] = (uint16_t)d3;
     }
+}
+
+// Pixel order of the blocked stream's gathers (img x img image, column c = row-major
+// pixel): order 1 = 4 x 4 tiles (one 128-byte line each), 2 = Morton (Z) order
+__device__ __forceinline__ uint32_t spread_bits16(uint32_t v) {
+    v &= 0xffffu;
+    v = (v | (v << 8)) & 0x00ff00ffu;
+    v = (v | (v << 4)) & 0x0f0f0f0fu;
+    v = (v | (v << 2)) & 0x33333333u;
+    v = (v | (v << 1)) & 0x55555555u;
+    return v;
+}
+__device__ __forceinline__ int32_t blk_order_map(int32_t c, int n, int order) {
+    const int y = c / n, x = c - y * n;
+    if (order == 1) return ((y >> 2) * (n >> 2) + (x >> 2)) * 16 + ((y & 3) << 2) + (x & 3);
+    return (int32_t)((spread_bits16((uint32_t)y) << 1) | spread_bits16((uint32_t)x));
+}
+__global__ void blk_renumber_kernel(int64_t total, int32_t *idx, int n, int order) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x)
+        idx[i] = blk_order_map(idx[i], n, order);
+}
+__global__ void blk_permute_kernel(int64_t cols, const double *x, double *xt, int n, int order) {
+    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < cols; c += (int64_t)gridDim.x * blockDim.x)
+        xt[blk_order_map((int32_t)c, n, order)] = x[c];
 }
 
 // padded row lengths (whole blocks of blk entries) for the blocked copy

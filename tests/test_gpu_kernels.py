@@ -365,6 +365,7 @@ def test_blocked_stream_bit_identical(B, monkeypatch, dtype, lanes, compress):
     want_cmp = compress == "force" or (compress is None and g >= 8)
     ki = blk.kernel_info()
     assert ki["forward"] == ("blocked_compressed" if want_cmp else "blocked") and ki["forward_lanes"] == g
+    assert ki["forward_order"] == "tile4"      # 256 x 256 image: gathers in 4 x 4 pixel tiles
     assert plain.kernel_info()["forward"] == "csr" and plain.kernel_info()["forward_lanes"] == 32
     exact = lanes == "32"
     oop = orc.OracleOperator(a, 2, 2)
@@ -381,6 +382,39 @@ def test_blocked_stream_bit_identical(B, monkeypatch, dtype, lanes, compress):
         if exact:
             assert np.array_equal(r1.cpu().numpy(), r0.cpu().numpy())
         assert rel(r1.cpu().numpy(), y - oop.matvec(x)) < 1e-12
+
+
+@pytest.mark.parametrize("lanes,compress", [(None, None), ("4", None), ("4", "force"), ("16", "off")])
+def test_blocked_gather_order_bit_identical(B, monkeypatch, lanes, compress):
+    """K1's tiled gather order (4 x 4 pixel tiles of a square image, the vector
+    permuted the same way before the launch) keeps every entry at its position in
+    the stream: products and residuals equal A's native column order bit for bit,
+    with plain and compressed (signed 16-bit step) indices."""
+    blockops = B[0]
+    from paper_1812_01307_b200 import problems
+    a = problems.parallel_beam_matrix(128, 30, 181, dtype=np.float32)
+    part = blockops.make_partition(*a.shape, 2, 3)
+    monkeypatch.setenv("BSGD_BLOCKED", "force")
+    if lanes is not None:
+        monkeypatch.setenv("BSGD_BLK_G", lanes)
+    if compress is not None:
+        monkeypatch.setenv("BSGD_BLK_COMPRESS", compress)
+    tiled = blockops.BlockOperator(a, part)
+    monkeypatch.setenv("BSGD_BLK_ORDER", "native")
+    native = blockops.BlockOperator(a, part)
+    kt, kn = tiled.kernel_info(), native.kernel_info()
+    assert kt["forward_order"] == "tile4" and kn["forward_order"] == "native"
+    assert kt["forward"] == kn["forward"] and kt["forward_lanes"] == kn["forward_lanes"]
+    oop = orc.OracleOperator(a, 2, 3)
+    rng = np.random.default_rng(4)
+    for _ in range(3):
+        x, y = rng.standard_normal(a.shape[1]), rng.standard_normal(a.shape[0])
+        got = tiled.matvec(x, charge=False)
+        assert np.array_equal(got, native.matvec(x, charge=False))
+        assert rel(got, oop.matvec(x)) < 1e-12
+        r1, s1 = tiled.residual_sumsq(x, y)
+        r0, s0 = native.residual_sumsq(x, y)
+        assert np.array_equal(r1.cpu().numpy(), r0.cpu().numpy()) and float(s1) == float(s0)
 
 
 @pytest.mark.parametrize("index", [2, 3])
