@@ -230,3 +230,78 @@ def test_oracle_3d_epoch_runs():
     prm = orc.Params(mu=0.9 / (2 * eig), lam=0.01, epochs=3, max_inner_iters=5)
     res = orc.run_bsgd(op, y, prm, x_true=x_true, perm=perm, hw=(d, 8, 8))
     assert len(res.samples) == 4 and res.samples[-1][1] < res.samples[0][1]
+
+
+def _tv3_independent(t):
+    """Isotropic 3-D TV written from np.diff (shares no code with the oracle)."""
+    g2 = np.zeros(t.shape)
+    g2[1:, :, :] += np.diff(t, axis=0) ** 2
+    g2[:, 1:, :] += np.diff(t, axis=1) ** 2
+    g2[:, :, 1:] += np.diff(t, axis=2) ** 2
+    return float(np.sqrt(g2).sum())
+
+
+def test_oracle_3d_prox_reduces_to_reference_pinned_2d_prox():
+    """A volume constant along z has a z-constant minimiser whose slices solve the 2-D
+    problem, so tv_prox3 must reproduce the 2-D tv_prox (pinned bit-exact to the reference,
+    tv.py:172-255) on every slice: ties the unpinned 3-D restatement to the pinned 2-D one."""
+    rng = np.random.default_rng(21)
+    img = rng.random((12, 15))
+    img[3:8, 4:11] += 1.0
+    vol = np.repeat(img[None], 5, axis=0)
+    for w in (0.02, 0.3):
+        ref2, rep2 = orc.tv_prox(img, w, 4000, 1e-12)
+        out3, rep3 = orc.tv_prox3(vol, w, 4000, 1e-12)
+        assert not rep2.fell_back and not rep3.fell_back
+        assert np.abs(out3 - out3[:1]).max() < 1e-8          # z-constant
+        assert np.abs(out3[2] - ref2).max() < 1e-7
+
+
+def test_oracle_3d_prox_is_the_minimiser():
+    """Optimality against an independent statement of the 3-D problem: the prox output's
+    energy ||t - b||^2 + 2 w TV3(t) (TV from np.diff, not the oracle's operators) is not
+    improved by an independent Chambolle-Pock solve nor by random perturbations."""
+    rng = np.random.default_rng(22)
+    b = rng.random((7, 9, 8))
+    b[2:5, 3:7, 1:6] += 0.8
+    w = 0.15
+    out, rep = orc.tv_prox3(b, w, 3000, 1e-12)
+    assert not rep.fell_back
+
+    def energy(t):
+        return float(((t - b) ** 2).sum()) + 2.0 * w * _tv3_independent(t)
+
+    # Chambolle-Pock on min_t 0.5 ||t - b||^2 + w ||D t||_{2,1}, D from np.diff
+    def grad(t):
+        g = np.zeros((3,) + t.shape)
+        g[0, 1:] = np.diff(t, axis=0)
+        g[1, :, 1:] = np.diff(t, axis=1)
+        g[2, :, :, 1:] = np.diff(t, axis=2)
+        return g
+
+    def grad_t(g):                    # adjoint of grad
+        t = np.zeros(g.shape[1:])
+        t[1:] += g[0, 1:]
+        t[:-1] -= g[0, 1:]
+        t[:, 1:] += g[1, :, 1:]
+        t[:, :-1] -= g[1, :, 1:]
+        t[:, :, 1:] += g[2, :, :, 1:]
+        t[:, :, :-1] -= g[2, :, :, 1:]
+        return t
+
+    t = b.copy()
+    tb = t.copy()
+    dual = np.zeros((3,) + b.shape)
+    sigma = tau = 1.0 / np.sqrt(12.0)
+    for _ in range(6000):
+        dual = dual + sigma * grad(tb)
+        dual /= np.maximum(1.0, np.sqrt((dual ** 2).sum(axis=0)) / w)
+        t_new = (t - tau * grad_t(dual) + tau * b) / (1.0 + tau)
+        tb = 2.0 * t_new - t
+        t = t_new
+    assert np.linalg.norm(out - t) / np.linalg.norm(t) < 2e-5   # plain CP converges at O(1/k)
+    e0 = energy(out)
+    assert e0 <= energy(t) + 1e-9
+    for _ in range(20):
+        d = rng.standard_normal(b.shape)
+        assert e0 <= energy(out + 1e-4 * d) and e0 <= energy(out - 1e-4 * d)
