@@ -197,8 +197,8 @@ struct bsgd_plan {
         int64_t *ptr = nullptr;
         int32_t *idx = nullptr;     // NULL when the compressed indices are used
         void *val = nullptr;
-        int32_t *base = nullptr;    // compressed indices (spmv.cuh blk_cols)
-        uint16_t *del = nullptr;
+        int2 *half = nullptr;       // compressed indices (spmv.cuh blk_cols)
+        uint16_t *off = nullptr;
         size_t bytes = 0;
         // column order of the stream (spmv.cuh blk_order_map): 0 = A's own,
         // else the image's pixels renumbered (img x img) and K1 gathers from xt,
@@ -251,7 +251,7 @@ struct EpochTimer {
 };
 
 static void blk_free(bsgd_plan::BlkStore &b) {
-    cudaFree(b.ptr); cudaFree(b.idx); cudaFree(b.val); cudaFree(b.base); cudaFree(b.del); cudaFree(b.xt);
+    cudaFree(b.ptr); cudaFree(b.idx); cudaFree(b.val); cudaFree(b.half); cudaFree(b.off); cudaFree(b.xt);
     b = bsgd_plan::BlkStore();
 }
 
@@ -417,13 +417,25 @@ static int build_blocked(bsgd_plan *p, cudaStream_t st) {
         ((p->g_fwd != 32 || (double)p->nnz / (double)p->rows < 384.0) && !forced))
         return BSGD_OK;
     bsgd_plan::BlkStore b;
-    // Few lanes per ray, several adjacent rays per warp: the neighbouring bins of
-    // a steep ray read the same sectors in the same gather instruction (one L1
-    // tag lookup instead of one per warp).  K1 at configs[3] (~920 nnz/row):
-    // 32 lanes 4.03 ms, 16: 3.57, 8: 3.18, 4: 3.03; configs[2] (~460):
-    // 0.490 / 0.461 / 0.456 / 0.501 ms.
+    // Gather order: a square column space (n x n, n % 4 == 0: a CT image) is read
+    // in 4 x 4 pixel tiles, one 128-byte line each, so a ray's consecutive pixels and
+    // the neighbouring rays of a warp share lines; the stream's entries keep their
+    // positions (same sums, bit for bit) and K1 gathers from the vector permuted into
+    // that order (blk_order_map).  BSGD_BLK_ORDER = native | morton overrides (experiments).
+    int order = 1, img = (int)llround(sqrt((double)p->cols));
+    if (const char *o = getenv("BSGD_BLK_ORDER"))
+        order = strcmp(o, "tile4") == 0 ? 1 : strcmp(o, "morton") == 0 ? 2 : 0;
+    if ((int64_t)img * img != p->cols || (order == 1 ? img % 4 != 0 : (img & (img - 1)) != 0)) order = 0;
+    // Lanes per ray.  In A's own column order, few lanes per ray and several adjacent
+    // rays per warp: the neighbouring bins of a steep ray read the same sectors in the
+    // same gather instruction (K1 at configs[3], ~920 nnz/row, round 1: 32 lanes 4.03 ms,
+    // 16: 3.57, 8: 3.18, 4: 3.03; configs[2], ~460: 0.490 / 0.461 / 0.456 / 0.501).
+    // In tile order a ray's own consecutive pixels share lines, the kernel is no longer
+    // bound by L1 tag lookups (ncu: L1tex 96% -> 68%) and 16 lanes with the compressed
+    // indices stream best (configs[3]: 4 lanes plain 3.01 ms, 8 compressed 2.69, 16
+    // compressed 2.55, 32 compressed 2.99; configs[2]: 8 -> 16 lanes 0.386 -> 0.332).
     const double mean = (double)p->nnz / (double)p->rows;
-    b.gb = mean >= 768.0 ? 4 : 8;
+    b.gb = order ? 16 : mean >= 768.0 ? 4 : 8;
     if (const char *g = getenv("BSGD_BLK_G")) {   // experiments
         const int v = atoi(g);
         if (v == 4 || v == 8 || v == 16 || v == 32) b.gb = v;
@@ -459,55 +471,44 @@ static int build_blocked(bsgd_plan *p, cudaStream_t st) {
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) return bail(e);
     b.bytes = sizeof(int64_t) * (p->rows + 1) + (sizeof(int32_t) + sizeof(V)) * (size_t)total;
-    // Gather order: a square column space (n x n, n % 4 == 0: a CT image) is read
-    // in 4 x 4 pixel tiles, one 128-byte line each, so the neighbouring rays of a
-    // warp share lines; the stream's entries keep their positions (same sums, bit
-    // for bit) and K1 gathers from the vector permuted into that order (blk_order_map).
-    // configs[3] K1 3.08 -> 2.90 ms, configs[2] 0.418 -> 0.382 ms (with the signed
-    // 16-bit steps).  BSGD_BLK_ORDER = native | morton overrides (experiments).
-    {
-        const char *o = getenv("BSGD_BLK_ORDER");
-        const int order = !o ? 1 : strcmp(o, "tile4") == 0 ? 1 : strcmp(o, "morton") == 0 ? 2 : 0;
-        int n = (int)llround(sqrt((double)p->cols));
-        const bool square = (int64_t)n * n == p->cols;
-        if (order && square && (order == 1 ? n % 4 == 0 : (n & (n - 1)) == 0)) {
-            e = cudaMalloc(&b.xt, sizeof(double) * p->cols);
-            if (e != cudaSuccess) return bail(e);
-            blk_renumber_kernel<<<grid_1d(total), kThreads, 0, st>>>(total, b.idx, n, order);
-            e = cudaGetLastError();
-            if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-            if (e != cudaSuccess) return bail(e);
-            b.order = order;
-            b.img = n;
-            b.bytes += sizeof(double) * p->cols;
-        }
+    if (order) {
+        e = cudaMalloc(&b.xt, sizeof(double) * p->cols);
+        if (e != cudaSuccess) return bail(e);
+        blk_renumber_kernel<<<grid_1d(total), kThreads, 0, st>>>(total, b.idx, img, order);
+        e = cudaGetLastError();
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) return bail(e);
+        b.order = order;
+        b.img = img;
+        b.bytes += sizeof(double) * p->cols;
     }
-    // 16-bit column increments within a lane's four entries when they fit (CT rays:
-    // a few image rows apart): 7 instead of 8 stream bytes per float32 entry
-    if (!getenv("BSGD_NO_BLK_COMPRESS")) {
-        int32_t *bb = nullptr;
-        uint16_t *dd = nullptr;
+    // 16-bit column offsets from two bases per block when they fit (CT rays: the 2 gb
+    // consecutive pixels of half a block lie a few image rows apart): 6 + 8 / (4 gb)
+    // instead of 8 stream bytes per float32 entry
+    if (!getenv("BSGD_NO_BLK_COMPRESS") && total > 0) {
+        int2 *hh = nullptr;
+        uint16_t *oo = nullptr;
         int *bad = nullptr;
-        cudaError_t e2 = cudaMalloc(&bb, sizeof(int32_t) * std::max<int64_t>(total / 4, 1));
-        if (e2 == cudaSuccess) e2 = cudaMalloc(&dd, sizeof(uint16_t) * std::max<int64_t>(total, 1));
+        const int64_t nblocks = total / (4 * b.gb);
+        cudaError_t e2 = cudaMalloc(&hh, sizeof(int2) * nblocks);
+        if (e2 == cudaSuccess) e2 = cudaMalloc(&oo, sizeof(uint16_t) * total);
         if (e2 == cudaSuccess) e2 = cudaMalloc(&bad, sizeof(int));
         int hbad = 1;
         if (e2 == cudaSuccess) e2 = cudaMemsetAsync(bad, 0, sizeof(int), st);
         if (e2 == cudaSuccess) {
-            blk_compress_kernel<<<grid_1d(std::max<int64_t>(total / 4, 1)), kThreads, 0, st>>>(total / 4, b.idx, bb, dd,
-                                                                                               bad);
+            blk_compress_kernel<<<grid_1d(nblocks), kThreads, 0, st>>>(nblocks, b.gb, b.idx, hh, oo, bad);
             e2 = cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, st);
         }
         if (e2 == cudaSuccess) e2 = cudaStreamSynchronize(st);
         cudaFree(bad);
-        if (e2 == cudaSuccess && hbad == 0) {   // both kept until tune_blocked times them
-            b.base = bb;
-            b.del = dd;
-            b.bytes += (1 + sizeof(uint16_t)) * (size_t)total;
+        if (e2 == cudaSuccess && hbad == 0) {   // both forms kept until tune_blocked picks one
+            b.half = hh;
+            b.off = oo;
+            b.bytes += sizeof(uint16_t) * (size_t)total + sizeof(int2) * (size_t)nblocks;
         } else {
             cudaGetLastError();
-            cudaFree(bb);
-            cudaFree(dd);
+            cudaFree(hh);
+            cudaFree(oo);
         }
     }
     b.ok = true;
@@ -704,13 +705,13 @@ static int launch_blocked(const bsgd_plan *p, const double *vec, const E &e, dou
         vec = p->fb.xt;
     }
     CsrB<V> A{p->rows, p->fb.ptr, p->fb.idx, (const V *)p->fb.val, vec};
-    A.base = p->fb.base;
-    A.del = p->fb.del;
+    A.half = p->fb.half;
+    A.off = p->fb.off;
     auto go = [&](auto kern, int G) {
         const int cap = std::min(occupancy(kern) * num_sms(), kMaxPartials);
         kern<<<ctas_for(p->rows, G, cap), kThreads, 0, st>>>(A, e, part, cnt);
     };
-    const bool cmp = p->fb.base != nullptr;
+    const bool cmp = p->fb.half != nullptr;
     if (p->fb.gb == 16) cmp ? go(csr_blocked_kernel<V, 16, E, true>, 16) : go(csr_blocked_kernel<V, 16, E>, 16);
     else if (p->fb.gb == 8) cmp ? go(csr_blocked_kernel<V, 8, E, true>, 8) : go(csr_blocked_kernel<V, 8, E>, 8);
     else if (p->fb.gb == 4) cmp ? go(csr_blocked_kernel<V, 4, E, true>, 4) : go(csr_blocked_kernel<V, 4, E>, 4);
@@ -721,16 +722,16 @@ static int launch_blocked(const bsgd_plan *p, const double *vec, const E &e, dou
 
 // Keep the compressed or the plain indices of the blocked copy by a fixed
 // structural rule, so the kernel a plan runs does not depend on a timing race:
-// compressed at 8 or more lanes per ray, plain at 4 (measured: configs[2],
-// 8 lanes, 0.457 -> 0.415 ms compressed; configs[3], 4 lanes, 3.04 ms plain vs
-// 3.20 compressed: the extra base load and dependent adds cost more than the
-// bytes they save when each lane walks 4x more entries).  BSGD_BLK_COMPRESS =
+// compressed at 8 or more lanes per ray, plain at 4 (measured with A's own column
+// order: configs[2], 8 lanes, 0.457 -> 0.415 ms compressed; configs[3], 4 lanes,
+// 3.01 ms plain vs 3.07 compressed: the extra loads cost more than the bytes they
+// save when the kernel is bound by L1 tag lookups).  BSGD_BLK_COMPRESS =
 // force | off overrides the rule (tests run both variants against the oracle).
 template <typename V>
 static int tune_blocked(bsgd_plan *p, cudaStream_t st) {
     (void)st;
     bsgd_plan::BlkStore &b = p->fb;
-    if (!b.ok || b.base == nullptr || b.idx == nullptr) return BSGD_OK;
+    if (!b.ok || b.half == nullptr || b.idx == nullptr) return BSGD_OK;
     bool keep_cmp = b.gb >= 8;
     if (const char *f = getenv("BSGD_BLK_COMPRESS")) {
         if (strcmp(f, "force") == 0) keep_cmp = true;
@@ -740,15 +741,16 @@ static int tune_blocked(bsgd_plan *p, cudaStream_t st) {
         cudaFree(b.idx);
         b.idx = nullptr;
     } else {
-        cudaFree(b.base);
-        cudaFree(b.del);
-        b.base = nullptr;
-        b.del = nullptr;
+        cudaFree(b.half);
+        cudaFree(b.off);
+        b.half = nullptr;
+        b.off = nullptr;
     }
     const int64_t n = [&]() { int64_t v = 0; cudaMemcpy(&v, b.ptr + p->rows, sizeof(int64_t), cudaMemcpyDeviceToHost); return v; }();
     p->device_bytes -= b.bytes;
-    b.bytes = sizeof(int64_t) * (p->rows + 1) + (keep_cmp ? (1 + sizeof(uint16_t)) : sizeof(int32_t)) * (size_t)n +
-              sizeof(V) * (size_t)n;
+    b.bytes = sizeof(int64_t) * (p->rows + 1) +
+              (keep_cmp ? sizeof(uint16_t) * (size_t)n + sizeof(int2) * (size_t)(n / (4 * b.gb)) : sizeof(int32_t) * (size_t)n) +
+              sizeof(V) * (size_t)n + (b.xt ? sizeof(double) * (size_t)p->cols : 0);
     p->device_bytes += b.bytes;
     return BSGD_OK;
 }
@@ -2007,7 +2009,7 @@ static void kernel_choice(const bsgd_plan *p, bool tr, int32_t *kind, int32_t *l
         return;
     }
     if (!tr && blocked_on(p)) {
-        *kind = p->fb.base ? BSGD_K_BLOCKED_CMP : BSGD_K_BLOCKED;
+        *kind = p->fb.half ? BSGD_K_BLOCKED_CMP : BSGD_K_BLOCKED;
         *lanes = p->fb.gb;
         return;
     }

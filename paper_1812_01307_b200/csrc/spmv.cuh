@@ -261,10 +261,12 @@ struct CsrB {
     const int32_t *idx;
     const V *val;
     const double *vec;
-    // compressed indices (CMP): a lane's four columns as base[k / 4] plus three
-    // 16-bit increments del[k + 1 .. k + 3] (del[k] unused): 3 bytes per entry
-    const int32_t *base = nullptr;
-    const uint16_t *del = nullptr;
+    // compressed indices (CMP): 16-bit offsets from two bases per block, half[b] = (least
+    // column of the block's first 2 GB entries, of its last 2 GB): a lane's entries
+    // l, l + GB come from the first half and l + 2 GB, l + 3 GB from the second, so
+    // column = base + offset with no dependent chain; 2 + 8 / (4 GB) bytes per entry
+    const int2 *half = nullptr;
+    const uint16_t *off = nullptr;
 };
 
 __device__ __forceinline__ uint2 ld_stream_u2(const void *p, uint64_t pol) {
@@ -274,16 +276,21 @@ __device__ __forceinline__ uint2 ld_stream_u2(const void *p, uint64_t pol) {
     return v;
 }
 
-// the lane's four columns of the block at entry k
-template <bool CMP, typename V>
+__device__ __forceinline__ int2 ld_stream_i2(const int2 *p, uint64_t pol) {
+    int2 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.s32 {%0,%1}, [%2], %3;"
+                 : "=r"(v.x), "=r"(v.y) : "l"(p), "l"(pol));
+    return v;
+}
+
+// the lane's four columns of the block at entry k (k = block start + 4 lane)
+template <bool CMP, int GB, typename V>
 __device__ __forceinline__ int4 blk_cols(const CsrB<V> &A, int64_t k, uint64_t pol) {
     if constexpr (CMP) {
-        const int32_t c0 = ld_stream(A.base + (k >> 2), pol);
-        const uint2 d = ld_stream_u2(A.del + k, pol);
-        const int32_t c1 = c0 + (int32_t)(int16_t)(d.x >> 16);
-        const int32_t c2 = c1 + (int32_t)(int16_t)(d.y & 0xFFFFu);
-        const int32_t c3 = c2 + (int32_t)(int16_t)(d.y >> 16);
-        return make_int4(c0, c1, c2, c3);
+        const int2 h = ld_stream_i2(A.half + k / (4 * GB), pol);
+        const uint2 d = ld_stream_u2(A.off + k, pol);
+        return make_int4(h.x + (int32_t)(d.x & 0xFFFFu), h.x + (int32_t)(d.x >> 16), h.y + (int32_t)(d.y & 0xFFFFu),
+                         h.y + (int32_t)(d.y >> 16));
     } else {
         return ld_stream4(A.idx + k, pol);
     }
@@ -316,7 +323,7 @@ __global__ void __launch_bounds__(kThreads) csr_blocked_kernel(CsrB<V> A, Epi ep
             const int64_t beg = A.ptr[row], end = A.ptr[row + 1];
             int64_t k = beg + 4 * gl;
             for (; k + BLK < end; k += 2 * BLK) {
-                const int4 ca = blk_cols<CMP>(A, k, pol), cb = blk_cols<CMP>(A, k + BLK, pol);
+                const int4 ca = blk_cols<CMP, GB>(A, k, pol), cb = blk_cols<CMP, GB>(A, k + BLK, pol);
                 double va[4], vb[4];
                 blk_vals(A.val + k, va, pol);
                 blk_vals(A.val + k + BLK, vb, pol);
@@ -327,7 +334,7 @@ __global__ void __launch_bounds__(kThreads) csr_blocked_kernel(CsrB<V> A, Epi ep
                 s = fma(vb[0], xb0, s); s = fma(vb[1], xb1, s); s = fma(vb[2], xb2, s); s = fma(vb[3], xb3, s);
             }
             if (k < end) {
-                const int4 ca = blk_cols<CMP>(A, k, pol);
+                const int4 ca = blk_cols<CMP, GB>(A, k, pol);
                 double va[4];
                 blk_vals(A.val + k, va, pol);
                 const double xa0 = __ldg(vec + ca.x), xa1 = __ldg(vec + ca.y), xa2 = __ldg(vec + ca.z),
@@ -349,21 +356,31 @@ __global__ void __launch_bounds__(kThreads) csr_blocked_kernel(CsrB<V> A, Epi ep
     if (blockIdx.x == 0 && threadIdx.x == 0 && cnt != nullptr) cnt[0] = gridDim.x;
 }
 
-// compress the blocked indices: per lane-block q (entries 4q .. 4q + 3, one lane's
-// columns) base[q] = first column, del[4q + m] = column m - column m-1 as a signed
-// 16-bit step (columns ascend in A's own order, not in a renumbered pixel order);
-// *bad != 0 when a step does not fit
-__global__ void blk_compress_kernel(int64_t nq, const int32_t *idx, int32_t *base, uint16_t *del, int *bad) {
-    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nq; q += (int64_t)gridDim.x * blockDim.x) {
-        const int4 c = reinterpret_cast<const int4 *>(idx)[q];
-        const int64_t d1 = (int64_t)c.y - c.x, d2 = (int64_t)c.z - c.y, d3 = (int64_t)c.w - c.z;
-        if (d1 < -32768 || d2 < -32768 || d3 < -32768 || d1 > 32767 || d2 > 32767 || d3 > 32767)
-            atomicExch(bad, 1);
-        base[q] = c.x;
-        del[4 * q] = 0;
-        del[4 * q + 1] = (uint16_t)d1;
-        del[4 * q + 2] = (uint16_t)d2;
-        del[4 * q + 3] = (uint16_t)d3;
+// compress the blocked indices (CsrB::half / off): one thread per block of 4 gb stored
+// entries (stored position 4 l + m holds entry gb m + l, so m < 2 is the first half);
+// *bad != 0 when an offset does not fit 16 bits
+__global__ void blk_compress_kernel(int64_t nblocks, int gb, const int32_t *idx, int2 *half, uint16_t *off, int *bad) {
+    for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nblocks;
+         b += (int64_t)gridDim.x * blockDim.x) {
+        const int4 *c = reinterpret_cast<const int4 *>(idx) + b * gb;
+        int32_t lo0 = INT32_MAX, lo1 = INT32_MAX;
+        for (int l = 0; l < gb; ++l) {
+            const int4 v = c[l];
+            lo0 = min(lo0, min(v.x, v.y));
+            lo1 = min(lo1, min(v.z, v.w));
+        }
+        half[b] = make_int2(lo0, lo1);
+        bool over = false;
+        for (int l = 0; l < gb; ++l) {
+            const int4 v = c[l];
+            const int64_t d0 = (int64_t)v.x - lo0, d1 = (int64_t)v.y - lo0, d2 = (int64_t)v.z - lo1,
+                          d3 = (int64_t)v.w - lo1;
+            over |= d0 > 65535 || d1 > 65535 || d2 > 65535 || d3 > 65535;
+            ushort4 o;
+            o.x = (uint16_t)d0; o.y = (uint16_t)d1; o.z = (uint16_t)d2; o.w = (uint16_t)d3;
+            reinterpret_cast<ushort4 *>(off)[b * gb + l] = o;
+        }
+        if (over) atomicExch(bad, 1);
     }
 }
 

@@ -339,8 +339,8 @@ def test_blocked_stream_bit_identical(B, monkeypatch, dtype, lanes, compress):
     per row it gives the unblocked G = 32 kernel's products bit for bit (same
     per-lane order; padding adds exact zeros); with fewer lanes (the plan's
     choice, several rays per warp) it agrees to rounding.  Both index forms --
-    plain int32 and the compressed base + 16-bit increments (the structural
-    rule keeps it at >= 8 lanes per ray; BSGD_BLK_COMPRESS forces either) --
+    plain int32 and the compressed 16-bit offsets from two bases per block (the
+    structural rule keeps it at >= 8 lanes per ray; BSGD_BLK_COMPRESS forces either) --
     against the oracle, with kernel_info confirming which one ran.  Rows
     shorter than a block and empty rows included."""
     blockops = B[0]
@@ -361,7 +361,7 @@ def test_blocked_stream_bit_identical(B, monkeypatch, dtype, lanes, compress):
     if compress is not None:
         monkeypatch.setenv("BSGD_BLK_COMPRESS", compress)
     blk = blockops.BlockOperator(a, part)
-    g = int(lanes) if lanes is not None else 8
+    g = int(lanes) if lanes is not None else 16    # tile-ordered gathers: 16 lanes per ray
     want_cmp = compress == "force" or (compress is None and g >= 8)
     ki = blk.kernel_info()
     assert ki["forward"] == ("blocked_compressed" if want_cmp else "blocked") and ki["forward_lanes"] == g
@@ -389,7 +389,7 @@ def test_blocked_gather_order_bit_identical(B, monkeypatch, lanes, compress):
     """K1's tiled gather order (4 x 4 pixel tiles of a square image, the vector
     permuted the same way before the launch) keeps every entry at its position in
     the stream: products and residuals equal A's native column order bit for bit,
-    with plain and compressed (signed 16-bit step) indices."""
+    with plain and compressed (16-bit offset) indices."""
     blockops = B[0]
     from paper_1812_01307_b200 import problems
     a = problems.parallel_beam_matrix(128, 30, 181, dtype=np.float32)
@@ -401,6 +401,7 @@ def test_blocked_gather_order_bit_identical(B, monkeypatch, lanes, compress):
         monkeypatch.setenv("BSGD_BLK_COMPRESS", compress)
     tiled = blockops.BlockOperator(a, part)
     monkeypatch.setenv("BSGD_BLK_ORDER", "native")
+    monkeypatch.setenv("BSGD_BLK_G", str(tiled.kernel_info()["forward_lanes"]))   # the order alone differs
     native = blockops.BlockOperator(a, part)
     kt, kn = tiled.kernel_info(), native.kernel_info()
     assert kt["forward_order"] == "tile4" and kn["forward_order"] == "native"
