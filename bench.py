@@ -382,9 +382,10 @@ def run_ours(args):
         else:
             cpu = port
 
-    # K2 (gather-tiled A^T + step), prox (1 cooperative row-walk kernel), the x permute
-    # into K1's tiled gather order, K1 lookahead, tail
-    launches = 5 if op.kernel_info()["forward_order"] != "native" else 4
+    # the r permute into K2's tiled gather order, K2 (blocked A^T + step), prox (1 cooperative
+    # row-walk kernel), the x permute into K1's tiled gather order, K1 lookahead, tail
+    ki = op.kernel_info()
+    launches = 4 + (ki["forward_order"] != "native") + (ki.get("transposed_order", "native") != "native")
     secondary = None
     del st, runner, op, d
     torch.cuda.empty_cache()

@@ -146,6 +146,15 @@ int bsgd_plan_stacked_tiles(bsgd_plan *plan, int transposed, int64_t ntiles, con
  * per-row reduction shape).  ntiles = 0 removes the tiles. */
 int bsgd_plan_gather_tiles(bsgd_plan *plan, int transposed, int64_t ntiles, const int64_t *tile_ptr,
                            const int64_t *tile_rows, void *stream);
+/* Blocked stream for A^T (the copy csr_blocked_kernel runs; A's own is built at plan
+ * creation when its rows are long).  grid_h x grid_w = rows of A is the grid the
+ * gathered vector r lives on (row-major; a sinogram's angles x bins): the stream is
+ * then gathered in 4 x 4 grid tiles (one 128-byte line each) from r permuted into
+ * that order before each launch, with 16-bit offset indices when they fit.  0, 0 =
+ * no grid (A^T's own column order); a negative size removes the copy.  The blocked
+ * copy takes precedence over gather tiles.  Values agree with the CSR kernel to
+ * rounding (lane-strided per-row sums, fixed shuffle tree). */
+int bsgd_plan_blocked_transposed(bsgd_plan *plan, int64_t grid_h, int64_t grid_w, void *stream);
 /* depth (1 for ordinary plans) and the stored CSR's shape / nnz */
 int bsgd_plan_stacked_info(const bsgd_plan *plan, int64_t *depth, int64_t *rows2, int64_t *cols2,
                            int64_t *nnz2);
@@ -161,19 +170,19 @@ int bsgd_plan_info(const bsgd_plan *plan, int64_t *rows, int64_t *cols, int64_t 
  * for CSR / blocked / gather-tiled kernels, slices per lane for stacked ones. */
 #define BSGD_K_CSR 0           /* dual_csr_kernel (spmv.cuh) */
 #define BSGD_K_BLOCKED 1       /* csr_blocked_kernel, int32 indices */
-#define BSGD_K_BLOCKED_CMP 2   /* csr_blocked_kernel, int32 base + 16-bit increments */
+#define BSGD_K_BLOCKED_CMP 2   /* csr_blocked_kernel, 16-bit offsets from two int32 bases per block */
 #define BSGD_K_GTILE 3         /* gtile_kernel (gtile.cuh) */
 #define BSGD_K_STACKED 4       /* stacked_kernel (stacked.cuh) */
 #define BSGD_K_STACKED_TILE 5  /* stacked_tile_kernel (stacked.cuh) */
-#define BSGD_ORDER_NATIVE 0     /* K1 gathers in A's column order */
-#define BSGD_ORDER_TILE4 1      /* blocked K1 on an n x n image: 4 x 4 pixel tiles */
+#define BSGD_ORDER_NATIVE 0     /* gathers in the matrix's own column order */
+#define BSGD_ORDER_TILE4 1      /* blocked stream over a grid (n x n image; sinogram): 4 x 4 tiles */
 #define BSGD_ORDER_MORTON 2     /* (experiment, BSGD_BLK_ORDER=morton) Z order */
 typedef struct bsgd_kernel_info {
     int32_t fwd_kernel, fwd_lanes;  /* A x  (K1) */
     int32_t tr_kernel, tr_lanes;    /* A^T r (K2) */
     int64_t depth;
     int32_t fwd_order;              /* BSGD_ORDER_*: pixel order of K1's gathers */
-    int32_t reserved;
+    int32_t tr_order;               /* BSGD_ORDER_*: order of K2's gathers from r */
 } bsgd_kernel_info;
 int bsgd_plan_kernel_info(const bsgd_plan *plan, bsgd_kernel_info *out);
 /* In-epoch phase timing for measurement (bench.py): while enabled, every eager

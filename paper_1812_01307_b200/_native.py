@@ -50,7 +50,7 @@ class KernelInfo(ctypes.Structure):
     """bsgd_kernel_info (include/bsgd_b200.h)."""
     _fields_ = [("fwd_kernel", ctypes.c_int32), ("fwd_lanes", ctypes.c_int32),
                 ("tr_kernel", ctypes.c_int32), ("tr_lanes", ctypes.c_int32), ("depth", c_i64),
-                ("fwd_order", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+                ("fwd_order", ctypes.c_int32), ("tr_order", ctypes.c_int32)]
 
 
 KERNEL_NAMES = {0: "csr", 1: "blocked", 2: "blocked_compressed", 3: "gather_tiled", 4: "stacked",
@@ -88,6 +88,7 @@ _SIGS = {
     "bsgd_plan_stacked_info": (ctypes.c_int, [c_p, c_p, c_p, c_p, c_p]),
     "bsgd_plan_stacked_tiles": (ctypes.c_int, [c_p, ctypes.c_int, c_i64, c_p, c_p, c_p]),
     "bsgd_plan_gather_tiles": (ctypes.c_int, [c_p, ctypes.c_int, c_i64, c_p, c_p, c_p]),
+    "bsgd_plan_blocked_transposed": (ctypes.c_int, [c_p, c_i64, c_i64, c_p]),
     "bsgd_plan_destroy": (ctypes.c_int, [c_p]),
     "bsgd_plan_csr_copy": (ctypes.c_int, [c_p, c_p, c_p, c_p, c_p]),
     "bsgd_siddon_csr": (ctypes.c_int, [ctypes.c_int, c_i64, c_i64, c_i64, c_p, c_p, ctypes.c_int,

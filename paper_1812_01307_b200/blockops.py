@@ -14,6 +14,7 @@ nonzero count under a lock, divided on read (`blockops.py:150-152,195-203`).
 
 from __future__ import annotations
 
+import os
 import threading
 from dataclasses import dataclass
 
@@ -315,11 +316,15 @@ class BlockOperator:
             self.set_stacked_tiles(True, grid_tiles(n, n))
             self.set_stacked_tiles(False, grid_tiles(a1 - a0, num_bins))
         elif depth == 1 and tiles:
-            # gather-tiled A^T (gtile.cuh): a pixel's rays sit nb apart in r, so its
-            # gathers share no sectors and the 4x4 tile union pays off (kept only if
-            # faster, 1024^2: 6.1 -> 4.2 ms).  A's ray rows already walk adjacent
-            # pixels; tiling them lost inside the epoch at 512^2, so they stay CSR.
-            self.set_gather_tiles(True, grid_tiles(n, n))
+            # Blocked stream for A^T gathered in 4 x 4 sinogram tiles (angles x bins): a
+            # pixel's bins over consecutive angles and the neighbouring pixels of a warp
+            # share 128-byte lines of the permuted r (configs[3] K2: CSR 6.1 ms, gather
+            # tiles over 4 x 4 pixel tiles 2.9 ms, blocked 2.6 ms -- same bits as the
+            # gather tiles).  BSGD_TR_GTILE=1 keeps the gather tiles (experiments).
+            if os.environ.get("BSGD_TR_GTILE"):
+                self.set_gather_tiles(True, grid_tiles(n, n))
+            else:
+                self.set_transposed_blocked((a1 - a0, num_bins))
         return self
 
     def set_gather_tiles(self, transposed: bool, tiles) -> None:
@@ -342,6 +347,21 @@ class BlockOperator:
             rows = np.ascontiguousarray(tiles[1], dtype=np.int64)
             nat.call("bsgd_plan_gather_tiles", self._plan, int(bool(transposed)), ptr.size - 1, ptr.ctypes.data,
                      rows.ctypes.data, nat.stream_ptr(self._device))
+
+    def set_transposed_blocked(self, grid) -> None:
+        """Blocked stream for A^T (`bsgd_plan_blocked_transposed`).
+
+        ``grid`` = (h, w) with h * w = rows of A: the grid r lives on (a sinogram's
+        angles x bins); A^T's gathers then run in 4 x 4 grid tiles.  ``()`` builds
+        the copy in A^T's own column order; None removes it.  Takes precedence
+        over gather tiles.  Values agree with the CSR kernel to rounding.
+        """
+        if self.depth > 1:
+            raise ValueError("stacked operators have no blocked stream")
+        h, w = (-1, -1) if grid is None else (0, 0) if len(grid) == 0 else (int(grid[0]), int(grid[1]))
+        t = nat.torch()
+        with t.cuda.device(self._device):
+            nat.call("bsgd_plan_blocked_transposed", self._plan, h, w, nat.stream_ptr(self._device))
 
     def set_stacked_tiles(self, transposed: bool, tiles) -> None:
         """Tile-staged products for a stacked operator (`bsgd_plan_stacked_tiles`).
@@ -448,7 +468,8 @@ class BlockOperator:
         nat.call("bsgd_plan_kernel_info", self._plan, nat.ctypes.byref(ki))
         return {"forward": nat.KERNEL_NAMES[ki.fwd_kernel], "forward_lanes": int(ki.fwd_lanes),
                 "transposed": nat.KERNEL_NAMES[ki.tr_kernel], "transposed_lanes": int(ki.tr_lanes),
-                "depth": int(ki.depth), "forward_order": nat.GATHER_ORDERS[ki.fwd_order]}
+                "depth": int(ki.depth), "forward_order": nat.GATHER_ORDERS[ki.fwd_order],
+                "transposed_order": nat.GATHER_ORDERS[ki.tr_order]}
 
     def set_phase_timing(self, enable: bool) -> None:
         """Record CUDA events between the phases of every eager epoch on this plan

@@ -30,6 +30,7 @@
 #include "siddon.cuh"
 #include "stacked.cuh"
 #include "gtile.cuh"
+#include "ring.cuh"
 #include "slab.cuh"
 
 using namespace bsgd;
@@ -200,13 +201,18 @@ struct bsgd_plan {
         int2 *half = nullptr;       // compressed indices (spmv.cuh blk_cols)
         uint16_t *off = nullptr;
         size_t bytes = 0;
-        // column order of the stream (spmv.cuh blk_order_map): 0 = A's own,
-        // else the image's pixels renumbered (img x img) and K1 gathers from xt,
-        // the vector permuted the same way before each launch
+        // column order of the stream (spmv.cuh blk_order_map): 0 = the matrix's own,
+        // else the gathered vector's gh x gw grid (image pixels for A, the sinogram's
+        // angles x bins for A^T) renumbered and the product gathers from xt, the
+        // vector permuted the same way before each launch
         int order = 0;
-        int img = 0;
+        int gh = 0, gw = 0;
         double *xt = nullptr;
-    } fb;
+        int64_t nrows = 0, veclen = 0;
+        // TMA-staged record form (ring.cuh): replaces off / val / half when built
+        int64_t *bptr = nullptr;
+        unsigned char *rec = nullptr;
+    } fb, tb;   // of A (built at plan creation for long rows), of A^T (bsgd_plan_blocked_transposed)
     bool stacked() const { return depth > 1; }
     // in-epoch phase timing (bsgd_plan_set_timing / bsgd_plan_timing): kPhaseEvents
     // events per eager bsgd_epoch on the launching stream, never inside a capture
@@ -251,7 +257,7 @@ struct EpochTimer {
 };
 
 static void blk_free(bsgd_plan::BlkStore &b) {
-    cudaFree(b.ptr); cudaFree(b.idx); cudaFree(b.val); cudaFree(b.half); cudaFree(b.off); cudaFree(b.xt);
+    cudaFree(b.ptr); cudaFree(b.idx); cudaFree(b.val); cudaFree(b.half); cudaFree(b.off); cudaFree(b.xt); cudaFree(b.bptr); cudaFree(b.rec);
     b = bsgd_plan::BlkStore();
 }
 
@@ -345,6 +351,7 @@ static void plan_free(bsgd_plan *p) {
     DeviceGuard g(p->device);
     for (cudaEvent_t e : p->timing.pool) cudaEventDestroy(e);
     blk_free(p->fb);
+    blk_free(p->tb);
     cudaFree(p->f_ptr); cudaFree(p->f_idx); cudaFree(p->f_val);
     cudaFree(p->t_ptr); cudaFree(p->t_idx); cudaFree(p->t_val);
     cudaFree(p->d_row_bounds); cudaFree(p->d_col_bounds);
@@ -405,38 +412,43 @@ static int build_transpose(bsgd_plan *p, cudaStream_t st) {
 }
 
 
-// Blocked copy of A's stream (csr_blocked_kernel) for plans whose rows are long
-// (>= 384 nonzeros on average: CT rays; padding to 128-entry blocks then costs
-// <= ~17% more stream bytes).  Skipped quietly when memory is short.
-// BSGD_BLOCKED=force builds it for any plan (tests), BSGD_NO_BLOCKED=1 never.
+// Blocked copy of a stream (csr_blocked_kernel) of A (tr = false) or A^T (tr = true).
+// (gh, gw) is the grid the gathered vector is laid out on (row-major, gh * gw = its
+// length; 0, 0 = unknown): image pixels for A, the sinogram's angles x bins for A^T.
+// Skipped quietly when memory is short.
 template <typename V>
-static int build_blocked(bsgd_plan *p, cudaStream_t st) {
-    const char *force = getenv("BSGD_BLOCKED");
-    const bool forced = force && strcmp(force, "force") == 0;
-    if (p->stacked() || p->rows == 0 || getenv("BSGD_NO_BLOCKED") ||
-        ((p->g_fwd != 32 || (double)p->nnz / (double)p->rows < 384.0) && !forced))
-        return BSGD_OK;
+static int build_blocked_dir(bsgd_plan *p, bool tr, int gh, int gw, cudaStream_t st) {
     bsgd_plan::BlkStore b;
-    // Gather order: a square column space (n x n, n % 4 == 0: a CT image) is read
-    // in 4 x 4 pixel tiles, one 128-byte line each, so a ray's consecutive pixels and
-    // the neighbouring rays of a warp share lines; the stream's entries keep their
-    // positions (same sums, bit for bit) and K1 gathers from the vector permuted into
-    // that order (blk_order_map).  BSGD_BLK_ORDER = native | morton overrides (experiments).
-    int order = 1, img = (int)llround(sqrt((double)p->cols));
+    b.nrows = tr ? p->cols : p->rows;
+    b.veclen = tr ? p->rows : p->cols;
+    const int64_t *sptr = tr ? p->t_ptr : p->f_ptr;
+    const int32_t *sidx = tr ? p->t_idx : p->f_idx;
+    const V *sval = (const V *)(tr ? p->t_val : p->f_val);
+    // Gather order: a gh x gw grid is read in 4 x 4 tiles, one 128-byte line each, so a
+    // row's consecutive entries (a ray's pixels; a pixel's bins over consecutive angles)
+    // and the neighbouring rows of a warp share lines; the stream's entries keep their
+    // positions (same sums, bit for bit) and the product gathers from the vector
+    // permuted into that order (blk_order_map).  BSGD_BLK_ORDER = native | morton
+    // overrides (experiments).
+    int order = 1;
     if (const char *o = getenv("BSGD_BLK_ORDER"))
         order = strcmp(o, "tile4") == 0 ? 1 : strcmp(o, "morton") == 0 ? 2 : 0;
-    if ((int64_t)img * img != p->cols || (order == 1 ? img % 4 != 0 : (img & (img - 1)) != 0)) order = 0;
-    // Lanes per ray.  In A's own column order, few lanes per ray and several adjacent
-    // rays per warp: the neighbouring bins of a steep ray read the same sectors in the
-    // same gather instruction (K1 at configs[3], ~920 nnz/row, round 1: 32 lanes 4.03 ms,
-    // 16: 3.57, 8: 3.18, 4: 3.03; configs[2], ~460: 0.490 / 0.461 / 0.456 / 0.501).
-    // In tile order a ray's own consecutive pixels share lines, the kernel is no longer
+    if (gh <= 0 || gw <= 0 || (int64_t)gh * gw != b.veclen) order = 0;
+    if (order == 2 && (gh != gw || (gw & (gw - 1)) != 0)) order = 0;
+    int64_t xt_len = b.veclen;
+    if (order == 1) xt_len = (int64_t)((gh + 3) / 4) * ((gw + 3) / 4) * 16;
+    if (xt_len > INT32_MAX) order = 0;
+    // Lanes per row.  In the matrix's own column order, few lanes per ray and several
+    // adjacent rays per warp: the neighbouring bins of a steep ray read the same sectors
+    // in the same gather instruction (K1 at configs[3], ~920 nnz/row, round 1: 32 lanes
+    // 4.03 ms, 16: 3.57, 8: 3.18, 4: 3.03; configs[2], ~460: 0.490 / 0.461 / 0.456 / 0.501).
+    // In tile order a row's own consecutive entries share lines, the kernel is no longer
     // bound by L1 tag lookups (ncu: L1tex 96% -> 68%) and 16 lanes with the compressed
-    // indices stream best (configs[3]: 4 lanes plain 3.01 ms, 8 compressed 2.69, 16
-    // compressed 2.55, 32 compressed 2.99; configs[2]: 8 -> 16 lanes 0.386 -> 0.332).
-    const double mean = (double)p->nnz / (double)p->rows;
+    // indices stream best (configs[3]: 4 lanes plain 3.01 ms, 8 compressed 2.56, 16
+    // compressed 2.46, 32 plain 3.07; configs[2]: 8 -> 16 lanes 0.369 -> 0.317).
+    const double mean = (double)p->nnz / (double)std::max<int64_t>(b.nrows, 1);
     b.gb = order ? 16 : mean >= 768.0 ? 4 : 8;
-    if (const char *g = getenv("BSGD_BLK_G")) {   // experiments
+    if (const char *g = getenv(tr ? "BSGD_BLK_G_TR" : "BSGD_BLK_G")) {   // experiments
         const int v = atoi(g);
         if (v == 4 || v == 8 || v == 16 || v == 32) b.gb = v;
     }
@@ -450,14 +462,14 @@ static int build_blocked(bsgd_plan *p, cudaStream_t st) {
         if (e == cudaErrorMemoryAllocation) return BSGD_OK;   // keep the unblocked kernel
         return fail(BSGD_ECUDA, "blocked stream build failed: %s", cudaGetErrorString(e));
     };
-    cudaError_t e = cudaMalloc(&b.ptr, sizeof(int64_t) * (p->rows + 1));
+    cudaError_t e = cudaMalloc(&b.ptr, sizeof(int64_t) * (b.nrows + 1));
     if (e != cudaSuccess) return bail(e);
-    blk_len_kernel<<<grid_1d(p->rows), kThreads, 0, st>>>(p->rows, p->f_ptr, 4 * b.gb, b.ptr);
-    e = cub::DeviceScan::ExclusiveSum(nullptr, temp_bytes, b.ptr, b.ptr, p->rows + 1, st);
+    blk_len_kernel<<<grid_1d(b.nrows), kThreads, 0, st>>>(b.nrows, sptr, 4 * b.gb, b.ptr);
+    e = cub::DeviceScan::ExclusiveSum(nullptr, temp_bytes, b.ptr, b.ptr, b.nrows + 1, st);
     if (e == cudaSuccess) e = cudaMalloc(&temp, temp_bytes);
-    if (e == cudaSuccess) e = cudaMemsetAsync(b.ptr + p->rows, 0, sizeof(int64_t), st);
-    if (e == cudaSuccess) e = cub::DeviceScan::ExclusiveSum(temp, temp_bytes, b.ptr, b.ptr, p->rows + 1, st);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(&total, b.ptr + p->rows, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(b.ptr + b.nrows, 0, sizeof(int64_t), st);
+    if (e == cudaSuccess) e = cub::DeviceScan::ExclusiveSum(temp, temp_bytes, b.ptr, b.ptr, b.nrows + 1, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&total, b.ptr + b.nrows, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) return bail(e);
     cudaFree(temp);
@@ -465,22 +477,24 @@ static int build_blocked(bsgd_plan *p, cudaStream_t st) {
     e = cudaMalloc(&b.idx, sizeof(int32_t) * std::max<int64_t>(total, 1));
     if (e == cudaSuccess) e = cudaMalloc(&b.val, sizeof(V) * std::max<int64_t>(total, 1));
     if (e != cudaSuccess) return bail(e);
-    blk_fill_kernel<V><<<grid_1d(p->rows, kThreads / 32), kThreads, 0, st>>>(
-        p->rows, p->f_ptr, p->f_idx, (const V *)p->f_val, b.ptr, b.idx, (V *)b.val, b.gb);
+    blk_fill_kernel<V><<<grid_1d(b.nrows, kThreads / 32), kThreads, 0, st>>>(b.nrows, sptr, sidx, sval, b.ptr, b.idx,
+                                                                             (V *)b.val, b.gb);
     e = cudaGetLastError();
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) return bail(e);
-    b.bytes = sizeof(int64_t) * (p->rows + 1) + (sizeof(int32_t) + sizeof(V)) * (size_t)total;
+    b.bytes = sizeof(int64_t) * (b.nrows + 1) + (sizeof(int32_t) + sizeof(V)) * (size_t)total;
     if (order) {
-        e = cudaMalloc(&b.xt, sizeof(double) * p->cols);
+        e = cudaMalloc(&b.xt, sizeof(double) * xt_len);
+        if (e == cudaSuccess) e = cudaMemsetAsync(b.xt, 0, sizeof(double) * xt_len, st);
         if (e != cudaSuccess) return bail(e);
-        blk_renumber_kernel<<<grid_1d(total), kThreads, 0, st>>>(total, b.idx, img, order);
+        blk_renumber_kernel<<<grid_1d(total), kThreads, 0, st>>>(total, b.idx, gw, order);
         e = cudaGetLastError();
         if (e == cudaSuccess) e = cudaStreamSynchronize(st);
         if (e != cudaSuccess) return bail(e);
         b.order = order;
-        b.img = img;
-        b.bytes += sizeof(double) * p->cols;
+        b.gh = gh;
+        b.gw = gw;
+        b.bytes += sizeof(double) * xt_len;
     }
     // 16-bit column offsets from two bases per block when they fit (CT rays: the 2 gb
     // consecutive pixels of half a block lie a few image rows apart): 6 + 8 / (4 gb)
@@ -512,9 +526,28 @@ static int build_blocked(bsgd_plan *p, cudaStream_t st) {
         }
     }
     b.ok = true;
-    p->fb = b;
+    bsgd_plan::BlkStore &dst = tr ? p->tb : p->fb;
+    p->device_bytes -= dst.bytes;
+    blk_free(dst);
+    dst = b;
     p->device_bytes += b.bytes;
     return BSGD_OK;
+}
+
+// The forward copy is built at plan creation for plans whose rows are long (>= 384
+// nonzeros on average: CT rays; padding to whole blocks then costs a few percent more
+// stream bytes); a square column space is taken for an image (n x n, gathered in tile
+// order).  BSGD_BLOCKED=force builds it for any plan (tests), BSGD_NO_BLOCKED=1 never.
+template <typename V>
+static int build_blocked(bsgd_plan *p, cudaStream_t st) {
+    const char *force = getenv("BSGD_BLOCKED");
+    const bool forced = force && strcmp(force, "force") == 0;
+    if (p->stacked() || p->rows == 0 || getenv("BSGD_NO_BLOCKED") ||
+        ((p->g_fwd != 32 || (double)p->nnz / (double)p->rows < 384.0) && !forced))
+        return BSGD_OK;
+    int img = (int)llround(sqrt((double)p->cols));
+    if ((int64_t)img * img != p->cols || img % 4 != 0) img = 0;
+    return build_blocked_dir<V>(p, false, img, img, st);
 }
 
 // ---------------------------------------------------------------------------
@@ -697,24 +730,50 @@ static int launch_gtile(const bsgd_plan::GTileStore &S, const double *vec, const
 
 static bool gtiles_on(const bsgd_plan::GTileStore &S) { return S.ok; }
 
-template <typename V, class E>
-static int launch_blocked(const bsgd_plan *p, const double *vec, const E &e, double *part, int64_t *cnt,
-                          cudaStream_t st) {
-    if (p->fb.order) {
-        blk_permute_kernel<<<grid_1d(p->cols), kThreads, 0, st>>>(p->cols, vec, p->fb.xt, p->fb.img, p->fb.order);
-        vec = p->fb.xt;
+template <typename V, int S, class E>
+static void launch_ring(const bsgd_plan::BlkStore &B, const double *vec, const E &e, double *part, int64_t *cnt,
+                        cudaStream_t st) {
+    auto kern = csr_ring_kernel<V, S, E>;
+    const size_t smem = ring_smem_bytes<V, S>();
+    static bool attr_set = false;   // per instantiation
+    static int occ = 1;
+    if (!attr_set) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, smem);
+        if (occ < 1) occ = 1;
+        attr_set = true;
     }
-    CsrB<V> A{p->rows, p->fb.ptr, p->fb.idx, (const V *)p->fb.val, vec};
-    A.half = p->fb.half;
-    A.off = p->fb.off;
+    const int cap = std::min(occ * num_sms(), kMaxPartials);
+    CsrR<V> A{B.nrows, B.bptr, B.rec, vec};
+    kern<<<ctas_for(B.nrows, kRingLanes, cap), kThreads, smem, st>>>(A, e, part, cnt);
+}
+
+template <typename V, class E>
+static int launch_blocked(const bsgd_plan::BlkStore &B, const double *vec, const E &e, double *part, int64_t *cnt,
+                          cudaStream_t st) {
+    if (B.order) {
+        blk_permute_kernel<<<grid_1d(B.veclen), kThreads, 0, st>>>(B.veclen, vec, B.xt, B.gw, B.order);
+        vec = B.xt;
+    }
+    if (B.rec) {
+        static const int depth = getenv("BSGD_BLK_RING") ? atoi(getenv("BSGD_BLK_RING")) : 8;   // experiments
+        if (depth == 4) launch_ring<V, 4>(B, vec, e, part, cnt, st);
+        else if (depth == 16 && sizeof(V) == 4) launch_ring<V, sizeof(V) == 4 ? 16 : 8>(B, vec, e, part, cnt, st);
+        else launch_ring<V, 8>(B, vec, e, part, cnt, st);
+        LAUNCHED();
+        return BSGD_OK;
+    }
+    CsrB<V> A{B.nrows, B.ptr, B.idx, (const V *)B.val, vec};
+    A.half = B.half;
+    A.off = B.off;
     auto go = [&](auto kern, int G) {
         const int cap = std::min(occupancy(kern) * num_sms(), kMaxPartials);
-        kern<<<ctas_for(p->rows, G, cap), kThreads, 0, st>>>(A, e, part, cnt);
+        kern<<<ctas_for(B.nrows, G, cap), kThreads, 0, st>>>(A, e, part, cnt);
     };
-    const bool cmp = p->fb.half != nullptr;
-    if (p->fb.gb == 16) cmp ? go(csr_blocked_kernel<V, 16, E, true>, 16) : go(csr_blocked_kernel<V, 16, E>, 16);
-    else if (p->fb.gb == 8) cmp ? go(csr_blocked_kernel<V, 8, E, true>, 8) : go(csr_blocked_kernel<V, 8, E>, 8);
-    else if (p->fb.gb == 4) cmp ? go(csr_blocked_kernel<V, 4, E, true>, 4) : go(csr_blocked_kernel<V, 4, E>, 4);
+    const bool cmp = B.half != nullptr;
+    if (B.gb == 16) cmp ? go(csr_blocked_kernel<V, 16, E, true>, 16) : go(csr_blocked_kernel<V, 16, E>, 16);
+    else if (B.gb == 8) cmp ? go(csr_blocked_kernel<V, 8, E, true>, 8) : go(csr_blocked_kernel<V, 8, E>, 8);
+    else if (B.gb == 4) cmp ? go(csr_blocked_kernel<V, 4, E, true>, 4) : go(csr_blocked_kernel<V, 4, E>, 4);
     else cmp ? go(csr_blocked_kernel<V, 32, E, true>, 32) : go(csr_blocked_kernel<V, 32, E>, 32);
     LAUNCHED();
     return BSGD_OK;
@@ -728,9 +787,7 @@ static int launch_blocked(const bsgd_plan *p, const double *vec, const E &e, dou
 // save when the kernel is bound by L1 tag lookups).  BSGD_BLK_COMPRESS =
 // force | off overrides the rule (tests run both variants against the oracle).
 template <typename V>
-static int tune_blocked(bsgd_plan *p, cudaStream_t st) {
-    (void)st;
-    bsgd_plan::BlkStore &b = p->fb;
+static int tune_blocked(bsgd_plan *p, bsgd_plan::BlkStore &b) {
     if (!b.ok || b.half == nullptr || b.idx == nullptr) return BSGD_OK;
     bool keep_cmp = b.gb >= 8;
     if (const char *f = getenv("BSGD_BLK_COMPRESS")) {
@@ -746,12 +803,36 @@ static int tune_blocked(bsgd_plan *p, cudaStream_t st) {
         b.half = nullptr;
         b.off = nullptr;
     }
-    const int64_t n = [&]() { int64_t v = 0; cudaMemcpy(&v, b.ptr + p->rows, sizeof(int64_t), cudaMemcpyDeviceToHost); return v; }();
+    const int64_t n = [&]() { int64_t v = 0; cudaMemcpy(&v, b.ptr + b.nrows, sizeof(int64_t), cudaMemcpyDeviceToHost); return v; }();
     p->device_bytes -= b.bytes;
-    b.bytes = sizeof(int64_t) * (p->rows + 1) +
+    const size_t xt_len = b.order == 1 ? (size_t)((b.gh + 3) / 4) * ((b.gw + 3) / 4) * 16 : (size_t)b.veclen;
+    b.bytes = sizeof(int64_t) * (b.nrows + 1) +
               (keep_cmp ? sizeof(uint16_t) * (size_t)n + sizeof(int2) * (size_t)(n / (4 * b.gb)) : sizeof(int32_t) * (size_t)n) +
-              sizeof(V) * (size_t)n + (b.xt ? sizeof(double) * (size_t)p->cols : 0);
+              sizeof(V) * (size_t)n + (b.xt ? sizeof(double) * xt_len : 0);
     p->device_bytes += b.bytes;
+    // record form for the TMA-staged kernel (ring.cuh): 16 lanes, compressed indices
+    if (keep_cmp && b.gb == kRingLanes && n > 0 && getenv("BSGD_BLK_RING")) {
+        const int64_t nblocks = n / kRingBlock;
+        const size_t rec_bytes = (size_t)nblocks * ring_rec_bytes<V>();
+        cudaError_t e = cudaMalloc(&b.bptr, sizeof(int64_t) * (b.nrows + 1));
+        if (e == cudaSuccess) e = cudaMalloc(&b.rec, rec_bytes);
+        if (e == cudaSuccess) {
+            ring_bptr_kernel<<<grid_1d(b.nrows + 1), kThreads>>>(b.nrows + 1, b.ptr, b.bptr);
+            ring_pack_kernel<V><<<grid_1d(nblocks * (ring_rec_bytes<V>() / 16)), kThreads>>>(
+                nblocks, b.half, b.off, (const V *)b.val, b.rec);
+            e = cudaGetLastError();
+            if (e == cudaSuccess) e = cudaDeviceSynchronize();
+        }
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            cudaFree(b.bptr);
+            cudaFree(b.rec);
+            b.bptr = nullptr;
+            b.rec = nullptr;
+            if (e != cudaErrorMemoryAllocation)
+                return fail(BSGD_ECUDA, "record stream build failed: %s", cudaGetErrorString(e));
+        }
+    }
     return BSGD_OK;
 }
 
@@ -759,18 +840,20 @@ static bool blocked_on(const bsgd_plan *p) {
     static const bool off = getenv("BSGD_NO_BLOCKED") != nullptr;
     return p->fb.ok && !off;
 }
+static bool blocked_tr_on(const bsgd_plan *p) { return p->tb.ok; }
 
 template <typename V, class E>
 static int launch_fwd(const bsgd_plan *p, const double *vec, const E &e, double *part, int64_t *cnt, cudaStream_t st) {
     if (p->stacked()) return launch_stacked_dir<V>(p, false, vec, e, part, cnt, st);
     if (gtiles_on(p->gf)) return launch_gtile<V>(p->gf, vec, e, part, cnt, st);
-    if (blocked_on(p)) return launch_blocked<V>(p, vec, e, part, cnt, st);
+    if (blocked_on(p)) return launch_blocked<V>(p->fb, vec, e, part, cnt, st);
     return launch_one<V>(fwd_csr<V>(p, vec), p->g_fwd, e, part, cnt, p->nnz, st);
 }
 
 template <typename V, class E>
 static int launch_tr(const bsgd_plan *p, const double *vec, const E &e, double *part, int64_t *cnt, cudaStream_t st) {
     if (p->stacked()) return launch_stacked_dir<V>(p, true, vec, e, part, cnt, st);
+    if (blocked_tr_on(p)) return launch_blocked<V>(p->tb, vec, e, part, cnt, st);
     if (gtiles_on(p->gt)) return launch_gtile<V>(p->gt, vec, e, part, cnt, st);
     return launch_one<V>(tr_csr<V>(p, vec), p->g_tr, e, part, cnt, p->nnz, st);
 }
@@ -1616,7 +1699,7 @@ static int plan_finish(bsgd_plan *p, cudaStream_t st) {
     if (rc != BSGD_OK) return rc;
     rc = (value_dtype == BSGD_F32) ? build_blocked<float>(p, st) : build_blocked<double>(p, st);
     if (rc != BSGD_OK) return rc;
-    rc = (value_dtype == BSGD_F32) ? tune_blocked<float>(p, st) : tune_blocked<double>(p, st);
+    rc = (value_dtype == BSGD_F32) ? tune_blocked<float>(p, p->fb) : tune_blocked<double>(p, p->fb);
     if (rc != BSGD_OK) return rc;
     // block nnz table (blockops.py:179-180)
     unsigned long long *d_cnt = nullptr;
@@ -1852,6 +1935,26 @@ int bsgd_plan_gather_tiles(bsgd_plan *p, int transposed, int64_t ntiles, const i
     return BSGD_OK;
 }
 
+int bsgd_plan_blocked_transposed(bsgd_plan *p, int64_t grid_h, int64_t grid_w, void *stream) {
+    if (!p) return fail(BSGD_EINVAL, "plan is NULL");
+    if (p->stacked()) return fail(BSGD_EINVAL, "stacked plans have no blocked stream");
+    DeviceGuard guard(p->device);
+    if (grid_h < 0 || grid_w < 0) {   // remove
+        p->device_bytes -= p->tb.bytes;
+        blk_free(p->tb);
+        return BSGD_OK;
+    }
+    if ((grid_h || grid_w) && grid_h * grid_w != p->rows)
+        return fail(BSGD_EINVAL, "grid %lld x %lld does not match the %lld rows of A", (long long)grid_h,
+                    (long long)grid_w, (long long)p->rows);
+    if (p->cols == 0 || p->nnz == 0) return BSGD_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    int rc = p->vdt == BSGD_F32 ? build_blocked_dir<float>(p, true, (int)grid_h, (int)grid_w, st)
+                                : build_blocked_dir<double>(p, true, (int)grid_h, (int)grid_w, st);
+    if (rc) return rc;
+    return p->vdt == BSGD_F32 ? tune_blocked<float>(p, p->tb) : tune_blocked<double>(p, p->tb);
+}
+
 int bsgd_plan_stacked_tiles(bsgd_plan *p, int transposed, int64_t ntiles, const int64_t *tile_ptr,
                             const int64_t *tile_rows, void *stream) {
     if (!p) return fail(BSGD_EINVAL, "plan is NULL");
@@ -2002,6 +2105,11 @@ static void kernel_choice(const bsgd_plan *p, bool tr, int32_t *kind, int32_t *l
         }
         return;
     }
+    if (tr && blocked_tr_on(p)) {
+        *kind = p->tb.half ? BSGD_K_BLOCKED_CMP : BSGD_K_BLOCKED;
+        *lanes = p->tb.gb;
+        return;
+    }
     const bsgd_plan::GTileStore &G = tr ? p->gt : p->gf;
     if (gtiles_on(G)) {
         *kind = BSGD_K_GTILE;
@@ -2024,6 +2132,7 @@ int bsgd_plan_kernel_info(const bsgd_plan *p, bsgd_kernel_info *out) {
     kernel_choice(p, true, &out->tr_kernel, &out->tr_lanes);
     out->depth = p->depth;
     out->fwd_order = (!p->stacked() && blocked_on(p) && !gtiles_on(p->gf)) ? p->fb.order : 0;
+    out->tr_order = (!p->stacked() && blocked_tr_on(p)) ? p->tb.order : 0;
     return BSGD_OK;
 }
 

@@ -384,8 +384,9 @@ __global__ void blk_compress_kernel(int64_t nblocks, int gb, const int32_t *idx,
     }
 }
 
-// Pixel order of the blocked stream's gathers (img x img image, column c = row-major
-// pixel): order 1 = 4 x 4 tiles (one 128-byte line each), 2 = Morton (Z) order
+// Order of the blocked stream's gathers over the vector's grid (rows of n columns,
+// element c row-major): order 1 = 4 x 4 tiles (one 128-byte line each; a ragged last
+// tile column / row is padded), 2 = Morton (Z) order (square power-of-two grids)
 __device__ __forceinline__ uint32_t spread_bits16(uint32_t v) {
     v &= 0xffffu;
     v = (v | (v << 8)) & 0x00ff00ffu;
@@ -396,7 +397,7 @@ __device__ __forceinline__ uint32_t spread_bits16(uint32_t v) {
 }
 __device__ __forceinline__ int32_t blk_order_map(int32_t c, int n, int order) {
     const int y = c / n, x = c - y * n;
-    if (order == 1) return ((y >> 2) * (n >> 2) + (x >> 2)) * 16 + ((y & 3) << 2) + (x & 3);
+    if (order == 1) return ((y >> 2) * ((n + 3) >> 2) + (x >> 2)) * 16 + ((y & 3) << 2) + (x & 3);
     return (int32_t)((spread_bits16((uint32_t)y) << 1) | spread_bits16((uint32_t)x));
 }
 __global__ void blk_renumber_kernel(int64_t total, int32_t *idx, int n, int order) {

@@ -149,7 +149,7 @@ class CudaShard:
         with an angle range), so no host CSR exists at any size (configs[3]: 1.9e9
         nonzeros over the ranks).  The rank's rows must be whole angles (configs[3]:
         each of the 8 row blocks is 180 angles x 1449 bins).  The shard's A^T is
-        gather-tiled over 4 x 4 pixel tiles like the single-GPU operator."""
+        a blocked stream gathered in 4 x 4 sinogram tiles like the single-GPU operator's."""
         from .blockops import BlockPartition, grid_tiles
         r0, r1 = spec.row_range
         if r0 % num_bins or r1 % num_bins:
@@ -158,7 +158,7 @@ class CudaShard:
         op = BlockOperator.from_parallel_beam(n, num_angles, num_bins, dtype=dtype, device=device, tiles=False,
                                               angle_range=(r0 // num_bins, r1 // num_bins), partition=part)
         if tiles:
-            op.set_gather_tiles(True, grid_tiles(n, n))
+            op.set_transposed_blocked(((r1 - r0) // num_bins, num_bins))
         self = cls.__new__(cls)
         self._finish(spec, op, n * n, lam, layout)
         return self
