@@ -30,7 +30,6 @@
 #include "siddon.cuh"
 #include "stacked.cuh"
 #include "gtile.cuh"
-#include "ring.cuh"
 #include "slab.cuh"
 
 using namespace bsgd;
@@ -209,9 +208,6 @@ struct bsgd_plan {
         int gh = 0, gw = 0;
         double *xt = nullptr;
         int64_t nrows = 0, veclen = 0;
-        // TMA-staged record form (ring.cuh): replaces off / val / half when built
-        int64_t *bptr = nullptr;
-        unsigned char *rec = nullptr;
     } fb, tb;   // of A (built at plan creation for long rows), of A^T (bsgd_plan_blocked_transposed)
     bool stacked() const { return depth > 1; }
     // in-epoch phase timing (bsgd_plan_set_timing / bsgd_plan_timing): kPhaseEvents
@@ -257,7 +253,7 @@ struct EpochTimer {
 };
 
 static void blk_free(bsgd_plan::BlkStore &b) {
-    cudaFree(b.ptr); cudaFree(b.idx); cudaFree(b.val); cudaFree(b.half); cudaFree(b.off); cudaFree(b.xt); cudaFree(b.bptr); cudaFree(b.rec);
+    cudaFree(b.ptr); cudaFree(b.idx); cudaFree(b.val); cudaFree(b.half); cudaFree(b.off); cudaFree(b.xt);
     b = bsgd_plan::BlkStore();
 }
 
@@ -730,38 +726,12 @@ static int launch_gtile(const bsgd_plan::GTileStore &S, const double *vec, const
 
 static bool gtiles_on(const bsgd_plan::GTileStore &S) { return S.ok; }
 
-template <typename V, int S, class E>
-static void launch_ring(const bsgd_plan::BlkStore &B, const double *vec, const E &e, double *part, int64_t *cnt,
-                        cudaStream_t st) {
-    auto kern = csr_ring_kernel<V, S, E>;
-    const size_t smem = ring_smem_bytes<V, S>();
-    static bool attr_set = false;   // per instantiation
-    static int occ = 1;
-    if (!attr_set) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, smem);
-        if (occ < 1) occ = 1;
-        attr_set = true;
-    }
-    const int cap = std::min(occ * num_sms(), kMaxPartials);
-    CsrR<V> A{B.nrows, B.bptr, B.rec, vec};
-    kern<<<ctas_for(B.nrows, kRingLanes, cap), kThreads, smem, st>>>(A, e, part, cnt);
-}
-
 template <typename V, class E>
 static int launch_blocked(const bsgd_plan::BlkStore &B, const double *vec, const E &e, double *part, int64_t *cnt,
                           cudaStream_t st) {
     if (B.order) {
         blk_permute_kernel<<<grid_1d(B.veclen), kThreads, 0, st>>>(B.veclen, vec, B.xt, B.gw, B.order);
         vec = B.xt;
-    }
-    if (B.rec) {
-        static const int depth = getenv("BSGD_BLK_RING") ? atoi(getenv("BSGD_BLK_RING")) : 8;   // experiments
-        if (depth == 4) launch_ring<V, 4>(B, vec, e, part, cnt, st);
-        else if (depth == 16 && sizeof(V) == 4) launch_ring<V, sizeof(V) == 4 ? 16 : 8>(B, vec, e, part, cnt, st);
-        else launch_ring<V, 8>(B, vec, e, part, cnt, st);
-        LAUNCHED();
-        return BSGD_OK;
     }
     CsrB<V> A{B.nrows, B.ptr, B.idx, (const V *)B.val, vec};
     A.half = B.half;
@@ -810,29 +780,6 @@ static int tune_blocked(bsgd_plan *p, bsgd_plan::BlkStore &b) {
               (keep_cmp ? sizeof(uint16_t) * (size_t)n + sizeof(int2) * (size_t)(n / (4 * b.gb)) : sizeof(int32_t) * (size_t)n) +
               sizeof(V) * (size_t)n + (b.xt ? sizeof(double) * xt_len : 0);
     p->device_bytes += b.bytes;
-    // record form for the TMA-staged kernel (ring.cuh): 16 lanes, compressed indices
-    if (keep_cmp && b.gb == kRingLanes && n > 0 && getenv("BSGD_BLK_RING")) {
-        const int64_t nblocks = n / kRingBlock;
-        const size_t rec_bytes = (size_t)nblocks * ring_rec_bytes<V>();
-        cudaError_t e = cudaMalloc(&b.bptr, sizeof(int64_t) * (b.nrows + 1));
-        if (e == cudaSuccess) e = cudaMalloc(&b.rec, rec_bytes);
-        if (e == cudaSuccess) {
-            ring_bptr_kernel<<<grid_1d(b.nrows + 1), kThreads>>>(b.nrows + 1, b.ptr, b.bptr);
-            ring_pack_kernel<V><<<grid_1d(nblocks * (ring_rec_bytes<V>() / 16)), kThreads>>>(
-                nblocks, b.half, b.off, (const V *)b.val, b.rec);
-            e = cudaGetLastError();
-            if (e == cudaSuccess) e = cudaDeviceSynchronize();
-        }
-        if (e != cudaSuccess) {
-            cudaGetLastError();
-            cudaFree(b.bptr);
-            cudaFree(b.rec);
-            b.bptr = nullptr;
-            b.rec = nullptr;
-            if (e != cudaErrorMemoryAllocation)
-                return fail(BSGD_ECUDA, "record stream build failed: %s", cudaGetErrorString(e));
-        }
-    }
     return BSGD_OK;
 }
 

@@ -418,46 +418,6 @@ def test_blocked_gather_order_bit_identical(B, monkeypatch, lanes, compress):
         assert np.array_equal(r1.cpu().numpy(), r0.cpu().numpy()) and float(s1) == float(s0)
 
 
-@pytest.mark.parametrize("dtype,depth", [(np.float32, "8"), (np.float32, "4"), (np.float64, "8")])
-def test_ring_kernel_bit_identical(B, monkeypatch, dtype, depth):
-    """The TMA-staged record form of the blocked stream (ring.cuh: 16 lanes per row,
-    one 64-entry record per bulk copy into a per-half-warp shared-memory ring) sums
-    like csr_blocked_kernel: A x, y - A x and A^T r equal the register-staged kernel
-    bit for bit, rows shorter than a record, empty rows and odd record counts included."""
-    blockops = B[0]
-    from paper_1812_01307_b200 import problems
-    n, ang, nb = 128, 30, 181
-    a = problems.parallel_beam_matrix(n, ang, nb, dtype=dtype).tolil()
-    a[5, :] = 0
-    a[nb + 7, :] = 0
-    a = a.tocsr()
-    a.eliminate_zeros()
-    part = blockops.make_partition(*a.shape, 2, 3)
-    monkeypatch.setenv("BSGD_BLOCKED", "force")
-    ref = blockops.BlockOperator(a, part)
-    ref.set_transposed_blocked((ang, nb))
-    monkeypatch.setenv("BSGD_BLK_RING", depth)
-    ring = blockops.BlockOperator(a, part)
-    ring.set_transposed_blocked((ang, nb))
-    for op in (ref, ring):
-        ki = op.kernel_info()
-        assert ki["forward"] == "blocked_compressed" and ki["forward_lanes"] == 16
-        assert ki["transposed"] == "blocked_compressed" and ki["transposed_lanes"] == 16
-    oop = orc.OracleOperator(a, 2, 3)
-    rng = np.random.default_rng(21)
-    for _ in range(3):
-        x, y = rng.standard_normal(a.shape[1]), rng.standard_normal(a.shape[0])
-        got = ring.matvec(x, charge=False)
-        assert np.array_equal(got, ref.matvec(x, charge=False))
-        assert rel(got, oop.matvec(x)) < 1e-12
-        r1, s1 = ring.residual_sumsq(x, y)
-        r0, s0 = ref.residual_sumsq(x, y)
-        assert np.array_equal(r1.cpu().numpy(), r0.cpu().numpy()) and float(s1) == float(s0)
-        gt = ring.rmatvec(y, charge=False)
-        assert np.array_equal(gt, ref.rmatvec(y, charge=False))
-        assert rel(gt, oop.rmatvec(y)) < 1e-12
-
-
 @pytest.mark.parametrize("grid", ["sinogram", "none"])
 def test_transposed_blocked_stream(B, monkeypatch, grid):
     """The blocked stream of A^T (bsgd_plan_blocked_transposed): 16 lanes per pixel
