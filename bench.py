@@ -519,6 +519,10 @@ def run_multi(args):
     from paper_1812_01307_b200.solvers import SolverConfig
 
     world, rank, local = dist_info()
+    if "RANK" not in os.environ:   # --force-dist outside torchrun: a world of one
+        os.environ.update({"RANK": "0", "WORLD_SIZE": "1", "LOCAL_RANK": "0"})
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29517")
     # one rank per GPU; the modulo only matters for the functional gloo check of
     # the N > 1 code path with every rank on one GPU (--dist-backend gloo)
     local = local % torch.cuda.device_count()
