@@ -418,6 +418,10 @@ class DistributedBSGD:
 
     ``shard`` is a backend (CudaShard in production).  History rows use the
     same layout as the single-GPU path (`BSGD_H_*`), replicated on every rank.
+    ``cfg.enforce_decrease`` (solvers.py:325-333) is honoured with the replicated
+    prox: an epoch then reduces its f_next at once, every rank reads the Eq. 9
+    flag and, while it fails, halves mu and repeats the step and the forward
+    product (`_epoch_enforce`; one host read per attempt, no graph capture).
     """
 
     def __init__(self, shard, y_full, cfg, x_true=None, group=None, history_capacity=1024, prox: str = "auto",
@@ -435,9 +439,6 @@ class DistributedBSGD:
         if cfg.alpha != 1.0 or cfg.gamma != 1.0:
             raise ValueError("DistributedBSGD runs full sweeps only (alpha = gamma = 1); the stochastic "
                              "pair subsets of solvers.py:186-195 need the single-GPU bsgd_tv_iteration")
-        if cfg.enforce_decrease:
-            raise ValueError("DistributedBSGD monitors Eq. 9 but does not halve mu (enforce_decrease, "
-                             "solvers.py:325-333); use the single-GPU bsgd_tv_iteration for it")
         self.dist = dist
         self.group = group
         self.s = shard
@@ -516,6 +517,9 @@ class DistributedBSGD:
         elif prox == "slab":
             raise ValueError("slab prox needs lam > 0 and a layout")
         self.prox_info = None
+        if cfg.enforce_decrease and self.slab is not None:
+            raise ValueError("enforce_decrease (solvers.py:325-333) needs the replicated prox: the slab prox "
+                             "does not repeat a step with a halved mu")
 
     def _allreduce(self, tensor):
         if self.dist.is_initialized() and self.dist.get_world_size(self.group) > 1:
@@ -555,7 +559,7 @@ class DistributedBSGD:
         only when its FGP decisions are on the device (``device_decisions``).  Returns
         whether a graph is ready."""
         if (self.slab is not None and not self.slab_device) or epochs < 2 or epochs % 2 or \
-                not getattr(self.y, "is_cuda", False):
+                not getattr(self.y, "is_cuda", False) or self.cfg.enforce_decrease:
             return False
         d = self.dist
         if d.is_initialized() and d.get_world_size(self.group) > 1 and d.get_backend(self.group) != "nccl":
@@ -602,6 +606,8 @@ class DistributedBSGD:
         s = self.s
         if monitor is None:
             monitor = cfg.monitor_decrease or cfg.enforce_decrease
+        if cfg.enforce_decrease:
+            return self._epoch_enforce()
         xi, ri = self.xi, self.ri
         x_k, x_next = self.x[xi], self.x[1 - xi]
         r_k, r_ahead = self.r[ri], self.r[ri]
@@ -627,6 +633,45 @@ class DistributedBSGD:
             self._allreduce(self.fnext)           # f_next = sum_p ||r_p||^2
             s.tail(args, self.fnext)
         row = self.rows_used
+        self.rows_used += 1
+        self.xi, self.ri = 1 - xi, 1 - ri
+        self.epoch += 1.0
+        return row
+
+    def _epoch_enforce(self):
+        """One epoch with the enforced two-point decrease (solvers.py:316-334): the
+        gradient is reduced once; the step, the prox and the forward product of
+        x_next are repeated with mu halved until Eq. 9 holds or max_halvings is
+        reached.  f_next is reduced in the epoch itself (no lagged tail) and every
+        rank reads the same flag from its replicated history row, so the ranks take
+        the same number of attempts.  mu stays halved for the following epochs."""
+        cfg, s = self.cfg, self.s
+        xi, ri = self.xi, self.ri
+        x_k, x_next = self.x[xi], self.x[1 - xi]
+        r_k, r_ahead = self.r[ri], self.r[ri]
+        flags = nat.EP_LOOKAHEAD | nat.EP_MONITOR
+        s.grad(r_k, self.g)
+        self._fslot.zero_()
+        self._allreduce(self._gbuf)
+        f_before = self.f_curr.clone()
+        row = self.rows_used
+        mu, halvings = self.mu, 0
+        while True:
+            args = s.args(x_k, self.g, x_next, mu, cfg, self.f_curr, self.hist, self.counter, self.perm,
+                          self.x_true, flags)
+            s.step(args)
+            s.forward(x_next, self.y, r_ahead, args)
+            s.forward_sumsq(args, self.fnext)
+            self._allreduce(self.fnext)
+            s.tail(args, self.fnext)
+            holds = float(self.hist[row, nat.H_HOLDS].item()) > 0.5
+            if holds or halvings >= cfg.max_halvings:
+                break
+            mu *= 0.5
+            halvings += 1
+            self.f_curr.copy_(f_before)
+            self.counter.fill_(row)
+        self.mu = mu
         self.rows_used += 1
         self.xi, self.ri = 1 - xi, 1 - ri
         self.epoch += 1.0
@@ -684,8 +729,8 @@ def run_solver_distributed(problem, cfg, sample_every: int = 1, group=None, *, u
     x_true and layout are the full ones.  Samples (epoch, relative error,
     objective, matvec units), decrease flags and the `DivergenceError` follow
     the single-GPU `solvers.run_solver` exactly; the units are charged against
-    the global nonzero count.  alpha = gamma = 1 and no enforce_decrease (see
-    `DistributedBSGD`)."""
+    the global nonzero count.  alpha = gamma = 1 only; enforce_decrease runs
+    eagerly with the replicated prox (see `DistributedBSGD`)."""
     import torch.distributed as dist
 
     from .solvers import ConvergenceTrace, DivergenceError, TraceSample
@@ -757,6 +802,8 @@ def run_solver_distributed(problem, cfg, sample_every: int = 1, group=None, *, u
         return None
 
     graphed = False
+    if cfg.enforce_decrease:
+        use_graphs = False                        # the halving loop reads a flag per attempt
     while done < epochs:
         if use_graphs and (drv.slab is None or drv.slab_device) and done >= 1 and epochs - done >= 2:
             if not graphed:

@@ -266,6 +266,35 @@ def test_run_solver_group_world1_nccl_matches_single_gpu(cuda_ok):
     assert np.array_equal(tr.final_x, single.final_x)
 
 
+@pytest.mark.parametrize("case,mu_scale", [("p3_ls", 6.0), ("p1_ct", 4.0)])
+def test_run_solver_group_enforce_decrease_matches_single_gpu(cuda_ok, case, mu_scale):
+    """enforce_decrease (solvers.py:325-333) through the distributed driver at world
+    size 1 (no process group: the all-reduces are no-ops): a step beyond the bound is
+    halved exactly as the single-GPU bsgd_tv_iteration halves it -- same flags, same
+    samples, x bit for bit -- with lam = 0 and with the TV prox (replicated)."""
+    from paper_1812_01307_b200 import blockops, parallel, solvers, tv
+    z = load_golden(case)
+    c = golden_cfg(z)
+    a = golden_csr(z)
+    m, n = (int(v) for v in z["mn"])
+    part = make_partition(a.shape[0], a.shape[1], m, n)
+    lam = float(c["lam"])
+    layout = tv.PixelLayout(*(int(v) for v in z["hw"]), z["perm"]) if "perm" in z else None
+    cfg = solvers.SolverConfig(mu=c["mu"] * mu_scale, lam=lam, epochs=12, enforce_decrease=True,
+                               prox=tv.ProxSettings(c["max_inner_iters"], c["tol"]))
+    single = solvers.run_solver("bsgd", solvers.Problem(blockops.BlockOperator(a, part), z["y"], z["x_true"], layout),
+                                cfg, sample_every=3)
+    shard = parallel.CudaShard(a, parallel.ShardSpec(part, 0, 1), lam=lam, layout=layout)
+    tr = solvers.run_solver("bsgd", solvers.Problem(shard, z["y"], z["x_true"], layout), cfg, sample_every=3,
+                            group="default")
+    assert not all(single.decrease_flags)      # some first attempts failed Eq. 9 and were halved
+    got, want = np.array([tuple(s) for s in tr.samples]), np.array([tuple(s) for s in single.samples])
+    assert np.array_equal(got[:, 0], want[:, 0]) and np.array_equal(got[:, 3], want[:, 3])
+    assert np.allclose(got[:, 1:3], want[:, 1:3], rtol=1e-12)
+    assert list(tr.decrease_flags) == list(single.decrease_flags)
+    assert np.array_equal(tr.final_x, single.final_x)
+
+
 def test_ct_row_slab_shard_world1_matches_single_operator(cuda_ok):
     """The device-generated row-slab shard of configs[2] at world size 1 is the
     single-GPU operator: same kernels, products and y bit for bit."""

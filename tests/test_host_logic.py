@@ -180,13 +180,14 @@ def test_canonical_csr_sums_float32_duplicates_in_float64():
 
 
 def test_distributed_driver_rejects_unsupported_modes():
-    """DistributedBSGD raises on alpha / gamma < 1 and enforce_decrease instead of
-    silently running a different algorithm (solvers.py:186-195, 325-333)."""
+    """DistributedBSGD raises on alpha / gamma < 1 instead of silently running a
+    different algorithm (solvers.py:186-195); enforce_decrease is supported with the
+    replicated prox (tests/test_parallel_gloo.py)."""
     import types
     from paper_1812_01307_b200 import parallel
     from paper_1812_01307_b200.solvers import SolverConfig
     shard = types.SimpleNamespace()
-    for kw in ({"alpha": 0.5}, {"gamma": 0.5}, {"enforce_decrease": True}):
+    for kw in ({"alpha": 0.5}, {"gamma": 0.5}):
         with pytest.raises(ValueError):
             parallel.DistributedBSGD(shard, np.zeros(4), SolverConfig(mu=0.1, **kw))
 

@@ -233,7 +233,7 @@ def test_world2_gloo_matches_single_process_oracle(tmp_path):
     assert np.allclose(hist[:, H.FNEXT], fnext, rtol=1e-12)
 
 
-def _solver_worker(rank, world, port, outdir, epochs, mu_scale, sample_every):
+def _solver_worker(rank, world, port, outdir, epochs, mu_scale, sample_every, enforce=False):
     import sys
     sys.path.insert(0, REPO)
     sys.path.insert(0, os.path.join(REPO, "tests"))
@@ -247,7 +247,7 @@ def _solver_worker(rank, world, port, outdir, epochs, mu_scale, sample_every):
     m, n = (int(v) for v in z["mn"])
     spec = parallel.ShardSpec(make_partition(a.shape[0], a.shape[1], m, n), rank, world)
     shard = CpuShard(a, spec)
-    cfg = solvers.SolverConfig(mu=c["mu"] * mu_scale, lam=0.0, epochs=epochs)
+    cfg = solvers.SolverConfig(mu=c["mu"] * mu_scale, lam=0.0, epochs=epochs, enforce_decrease=enforce)
     out = {}
     try:
         tr = solvers.run_solver("bsgd", solvers.Problem(shard, z["y"], z["x_true"]), cfg, sample_every=sample_every,
@@ -263,20 +263,24 @@ def _solver_worker(rank, world, port, outdir, epochs, mu_scale, sample_every):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("epochs,mu_scale,sample_every", [(13, 1.0, 3), (400, 1.3 * 0.5 / 0.9, 25)])
-def test_world2_gloo_run_solver_matches_oracle(tmp_path, epochs, mu_scale, sample_every):
+@pytest.mark.parametrize("epochs,mu_scale,sample_every,enforce",
+                         [(13, 1.0, 3, False), (400, 1.3 * 0.5 / 0.9, 25, False), (30, 6.0, 4, True)])
+def test_world2_gloo_run_solver_matches_oracle(tmp_path, epochs, mu_scale, sample_every, enforce):
     """run_solver(..., group=...) over two ranks (one all-reduce per epoch, lagged
     tail): the trace -- epochs, relative errors, objectives, exact matvec units,
     decrease flags -- and the final x match the oracle's run_bsgd; with a step
-    beyond the Theorem-1 bound both raise DivergenceError at the same epoch."""
+    beyond the Theorem-1 bound both raise DivergenceError at the same epoch; with
+    enforce_decrease (solvers.py:325-333) the same step is halved on both ranks
+    exactly as the oracle halves it."""
     from oracle import oracle as orc
     port = _free_port()
-    mp.spawn(_solver_worker, args=(2, port, str(tmp_path), epochs, mu_scale, sample_every), nprocs=2, join=True)
+    mp.spawn(_solver_worker, args=(2, port, str(tmp_path), epochs, mu_scale, sample_every, enforce), nprocs=2,
+             join=True)
     r0, r1 = np.load(tmp_path / "run0.npz"), np.load(tmp_path / "run1.npz")
     z = load_golden("p3_ls")
     c = golden_cfg(z)
     op = orc.OracleOperator(golden_csr(z), *(int(v) for v in z["mn"]))
-    prm = orc.Params(mu=c["mu"] * mu_scale, lam=0.0, epochs=epochs)
+    prm = orc.Params(mu=c["mu"] * mu_scale, lam=0.0, epochs=epochs, enforce_decrease=enforce)
     ref = orc.run_bsgd(op, z["y"], prm, x_true=z["x_true"], sample_every=sample_every)
     want = np.array(ref.samples)
     for r in (r0, r1):
