@@ -224,7 +224,8 @@ int bsgd_assemble_residual(int64_t rows, int64_t num_col_blocks, const double *y
 /* --- stochastic pair path (solvers.py:274-303 with alpha/gamma < 1) ---- */
 /* z_cache[j, I_i] = A_ij x_k[J_j] for the selected pairs; g[J_j] = 2 sum_i A_ij^T r_k[I_i]
  * over selected i (zero for unselected column blocks); r_next = y - sum_j z_cache[j].
- * row_sel / col_sel: host arrays of selected block indices. */
+ * row_sel / col_sel: host arrays of selected block indices.  n_rows_sel may be 0 (a
+ * row-slab shard owning none of the selected row blocks): g = 0, r_next from the cache. */
 int bsgd_pair_products(const bsgd_plan *plan, int64_t n_rows_sel, const int64_t *row_sel,
                        int64_t n_cols_sel, const int64_t *col_sel, const double *x_k,
                        const double *r_k, const double *y, double *z_cache, double *g,

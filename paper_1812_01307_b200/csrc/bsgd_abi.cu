@@ -2304,7 +2304,9 @@ int bsgd_pair_products(const bsgd_plan *p, int64_t n_rows_sel, const int64_t *ro
                        double *z_cache, double *g, double *r_next, void *stream) {
     if (!p || !x_k || !r_k || !y || !z_cache || !g || !r_next) return fail(BSGD_EINVAL, "NULL argument");
     if (p->M > 256 || p->N > 256) return fail(BSGD_EINVAL, "pair path supports at most 256 blocks per side");
-    if (n_rows_sel < 1 || n_cols_sel < 1 || !row_sel || !col_sel)
+    // a row-slab shard may own none of the selected row blocks (n_rows_sel = 0): its g is
+    // zero and its residual is rebuilt from the unchanged cache
+    if (n_rows_sel < 0 || n_cols_sel < 1 || (n_rows_sel > 0 && !row_sel) || !col_sel)
         return fail(BSGD_EINVAL, "alpha/gamma select no blocks");
     BlockMask rs{{0, 0, 0, 0}}, cs{{0, 0, 0, 0}};
     for (int64_t k = 0; k < n_rows_sel; ++k) {

@@ -212,6 +212,20 @@ class CudaShard:
     def grad(self, r_local, g_out):
         nat.call("bsgd_grad", self.op.plan, nat.ptr(r_local), nat.ptr(g_out), self.stream())
 
+    def pair_products(self, local_rows, cols_sel, x_k, r_k, y_local, z, g_out, r_next):
+        """The selected pairs' products on this rank's row blocks (`bsgd_pair_products`,
+        solvers.py:274-303): z cache commit, g = 2 sum_i A_ij^T r_i over the local
+        selected row blocks, r_next = y - sum_j z[j].  ``local_rows`` may be empty."""
+        rs = np.asarray(local_rows, dtype=np.int64)
+        cs = np.asarray(cols_sel, dtype=np.int64)
+        nat.call("bsgd_pair_products", self.op.plan, rs.size, rs.ctypes.data if rs.size else None, cs.size,
+                 cs.ctypes.data, nat.ptr(x_k), nat.ptr(r_k), nat.ptr(y_local), nat.ptr(z), nat.ptr(g_out),
+                 nat.ptr(r_next), self.stream())
+
+    def block_nnz_table(self):
+        """nnz of this rank's (local row block, column block) blocks, (local blocks, N)."""
+        return np.asarray(self.op._block_nnz, dtype=np.float64)
+
     def step(self, args):
         nat.call("bsgd_step", self.cols, ctypes.byref(args), self.stream())
 
@@ -414,7 +428,7 @@ SLAB_PROX_MIN_VOXELS = 1 << 22   # prox="auto" decomposes volumes from this size
 
 
 class DistributedBSGD:
-    """Row-slab BSGD-TV driver (alpha = gamma = 1) over a process group.
+    """Row-slab BSGD-TV driver over a process group.
 
     ``shard`` is a backend (CudaShard in production).  History rows use the
     same layout as the single-GPU path (`BSGD_H_*`), replicated on every rank.
@@ -422,6 +436,8 @@ class DistributedBSGD:
     prox: an epoch then reduces its f_next at once, every rank reads the Eq. 9
     flag and, while it fails, halves mu and repeats the step and the forward
     product (`_epoch_enforce`; one host read per attempt, no graph capture).
+    alpha, gamma < 1 (solvers.py:186-195) run `_epoch_stochastic`: each rank commits
+    the selected pairs of its own row blocks to its z cache; eager, replicated prox.
     """
 
     def __init__(self, shard, y_full, cfg, x_true=None, group=None, history_capacity=1024, prox: str = "auto",
@@ -436,9 +452,10 @@ class DistributedBSGD:
         epoch can be captured in a CUDA graph) when the backend supports it;
         False keeps the host loop (`SlabProx.run`, only the iterations taken)."""
         import torch.distributed as dist
-        if cfg.alpha != 1.0 or cfg.gamma != 1.0:
-            raise ValueError("DistributedBSGD runs full sweeps only (alpha = gamma = 1); the stochastic "
-                             "pair subsets of solvers.py:186-195 need the single-GPU bsgd_tv_iteration")
+        self.stochastic = cfg.alpha != 1.0 or cfg.gamma != 1.0
+        if self.stochastic and (getattr(shard, "owns_slices", False) or not hasattr(shard, "pair_products")):
+            raise ValueError("the stochastic pair subsets (alpha, gamma < 1; solvers.py:186-195) run on row-slab "
+                             "shards only")
         self.dist = dist
         self.group = group
         self.s = shard
@@ -520,16 +537,34 @@ class DistributedBSGD:
         if cfg.enforce_decrease and self.slab is not None:
             raise ValueError("enforce_decrease (solvers.py:325-333) needs the replicated prox: the slab prox "
                              "does not repeat a step with a halved mu")
+        if self.stochastic:
+            if self.slab is not None:
+                raise ValueError("the stochastic pair subsets (alpha, gamma < 1) need the replicated prox")
+            sp = shard.spec.partition
+            # z cache of this rank's rows (solvers.py:228: zeros) and a scratch residual
+            # for the monitor's / the samples' fidelity product
+            self.z = shard.zeros(sp.num_col_blocks * shard.rows)
+            self.r_fid = shard.zeros(shard.rows)
+            # global block nnz (matvec units of the selected pairs, blockops.py:195-203)
+            table = shard.t.zeros(sp.num_row_blocks, sp.num_col_blocks, dtype=shard.t.float64, device=self.y.device)
+            b0, b1 = shard.spec.block_range
+            table[b0:b1] += shard.t.as_tensor(shard.block_nnz_table(), dtype=shard.t.float64).to(self.y.device)
+            self._allreduce(table)
+            self.block_nnz = table.cpu().numpy().round().astype(np.int64)
+        self.last_pairs = None
 
     def _allreduce(self, tensor):
         if self.dist.is_initialized() and self.dist.get_world_size(self.group) > 1:
             self.dist.all_reduce(tensor, op=self.dist.ReduceOp.SUM, group=self.group)
 
     def _schedule(self):
-        """Advance the pair-order RNG exactly as the reference does (solvers.py:176-195)."""
+        """Draw the epoch's pairs exactly as the reference does (solvers.py:176-195); with
+        alpha = gamma = 1 only the RNG advance matters."""
         from .solvers import schedule_pairs
         sp = self.s.spec.partition
-        schedule_pairs(sp.num_row_blocks, sp.num_col_blocks, 1.0, 1.0, self.rng)
+        self.last_pairs = schedule_pairs(sp.num_row_blocks, sp.num_col_blocks, self.cfg.alpha, self.cfg.gamma,
+                                         self.rng)
+        return self.last_pairs
 
     def _ensure_history(self, extra: int) -> bool:
         """Grow the history table so ``extra`` more rows fit (the tail kernel skips
@@ -549,7 +584,9 @@ class DistributedBSGD:
     def epoch_step(self, monitor: bool | None = None):
         """One epoch; returns the history row index written."""
         self._ensure_history(1)
-        self._schedule()
+        pairs = self._schedule()
+        if self.stochastic:
+            return self._epoch_stochastic(pairs, monitor)
         return self._epoch(monitor)
 
     def capture(self, epochs: int = 2, monitor: bool | None = None) -> bool:
@@ -559,7 +596,7 @@ class DistributedBSGD:
         only when its FGP decisions are on the device (``device_decisions``).  Returns
         whether a graph is ready."""
         if (self.slab is not None and not self.slab_device) or epochs < 2 or epochs % 2 or \
-                not getattr(self.y, "is_cuda", False) or self.cfg.enforce_decrease:
+                not getattr(self.y, "is_cuda", False) or self.cfg.enforce_decrease or self.stochastic:
             return False
         d = self.dist
         if d.is_initialized() and d.get_world_size(self.group) > 1 and d.get_backend(self.group) != "nccl":
@@ -636,6 +673,55 @@ class DistributedBSGD:
         self.rows_used += 1
         self.xi, self.ri = 1 - xi, 1 - ri
         self.epoch += 1.0
+        return row
+
+    def _epoch_stochastic(self, pairs, monitor: bool | None = None):
+        """One iteration over a pair subset (alpha, gamma < 1; solvers.py:274-334): this
+        rank commits the selected pairs of its own row blocks to its z cache, rebuilds
+        its residual rows from the cache and contributes g = 2 sum_i A_ij^T r_i over
+        them; one all-reduce gives g, the step and the prox run replicated, and the
+        fidelity of x_next (the monitor's uncharged product, also the samples'
+        objective) is reduced in the same epoch.  With enforce_decrease the step is
+        repeated with mu halved like `_epoch_enforce`."""
+        cfg, s = self.cfg, self.s
+        if monitor is None:
+            monitor = cfg.monitor_decrease or cfg.enforce_decrease
+        sp = s.spec.partition
+        b0, b1 = s.spec.block_range
+        rows_sel = sorted({i for i, _ in pairs})
+        cols_sel = sorted({j for _, j in pairs})
+        xi, ri = self.xi, self.ri
+        x_k, x_next = self.x[xi], self.x[1 - xi]
+        r_k, r_next = self.r[ri], self.r[1 - ri]
+        s.pair_products([i - b0 for i in rows_sel if b0 <= i < b1], cols_sel, x_k, r_k, self.y, self.z, self.g,
+                        r_next)
+        self._fslot.zero_()
+        self._allreduce(self._gbuf)
+        flags = nat.EP_MONITOR if monitor else 0
+        f_before = self.f_curr.clone() if cfg.enforce_decrease else None
+        row = self.rows_used
+        mu, halvings = self.mu, 0
+        while True:
+            args = s.args(x_k, self.g, x_next, mu, cfg, self.f_curr, self.hist, self.counter, self.perm,
+                          self.x_true, flags)
+            s.step(args)
+            s.forward(x_next, self.y, self.r_fid, args)
+            s.forward_sumsq(args, self.fnext)
+            self._allreduce(self.fnext)
+            s.tail(args, self.fnext)
+            if not cfg.enforce_decrease:
+                break
+            holds = float(self.hist[row, nat.H_HOLDS].item()) > 0.5
+            if holds or halvings >= cfg.max_halvings:
+                break
+            mu *= 0.5
+            halvings += 1
+            self.f_curr.copy_(f_before)
+            self.counter.fill_(row)
+        self.mu = mu
+        self.rows_used += 1
+        self.xi, self.ri = 1 - xi, 1 - ri
+        self.epoch += len(pairs) / (sp.num_row_blocks * sp.num_col_blocks)
         return row
 
     def _epoch_enforce(self):
@@ -729,8 +815,8 @@ def run_solver_distributed(problem, cfg, sample_every: int = 1, group=None, *, u
     x_true and layout are the full ones.  Samples (epoch, relative error,
     objective, matvec units), decrease flags and the `DivergenceError` follow
     the single-GPU `solvers.run_solver` exactly; the units are charged against
-    the global nonzero count.  alpha = gamma = 1 only; enforce_decrease runs
-    eagerly with the replicated prox (see `DistributedBSGD`)."""
+    the global nonzero count.  alpha, gamma < 1 and enforce_decrease run eagerly
+    with the replicated prox (see `DistributedBSGD`)."""
     import torch.distributed as dist
 
     from .solvers import ConvergenceTrace, DivergenceError, TraceSample
@@ -769,16 +855,18 @@ def run_solver_distributed(problem, cfg, sample_every: int = 1, group=None, *, u
     next_sample = float(sample_every)
     done = 0
 
-    def book(ep):
+    def book(ep, row=None, charged=None):
         nonlocal applied, next_sample
-        applied += 2 * nnz_total                  # one A^T and one A product per full sweep
+        # one A^T and one A product per full sweep; the selected blocks' for a pair subset
+        applied += 2 * nnz_total if charged is None else charged
         sampled = ep >= next_sample - 1e-9
         u = None
         if sampled:
             u = units()
             applied += nnz_total
             next_sample = (math.floor(ep / sample_every + 1e-9) + 1) * sample_every
-        pending.append((int(round(ep)) - 1, ep, sampled, u))   # history row of epoch ep (rows from 0)
+        # history row: epoch ep of a full-sweep run wrote row ep - 1 (rows from 0)
+        pending.append((int(round(ep)) - 1 if row is None else row, ep, sampled, u))
 
     def drain():
         hist = drv.history()
@@ -804,6 +892,15 @@ def run_solver_distributed(problem, cfg, sample_every: int = 1, group=None, *, u
     graphed = False
     if cfg.enforce_decrease:
         use_graphs = False                        # the halving loop reads a flag per attempt
+    while drv.stochastic and drv.epoch < cfg.epochs - 1e-9:
+        row = drv.epoch_step()                    # a pair subset: a fraction of an epoch, eager
+        book(drv.epoch, row, 2 * int(sum(drv.block_nnz[i, j] for i, j in drv.last_pairs)))
+        if len(pending) >= chunk_epochs:
+            err = drain()
+            if err is not None:
+                raise err
+    if drv.stochastic:
+        done = epochs
     while done < epochs:
         if use_graphs and (drv.slab is None or drv.slab_device) and done >= 1 and epochs - done >= 2:
             if not graphed:

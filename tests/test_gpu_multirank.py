@@ -57,7 +57,7 @@ def _ct_slab_case():
 
 # --- row slabs, lam = 0: run_solver(group=...) against the oracle ----------------------
 
-def _ls_worker(rank, world, port, outdir, epochs, sample_every):
+def _ls_worker(rank, world, port, outdir, epochs, sample_every, mu_scale=1.0, frac=1.0, enforce=False):
     dist = _init(rank, world, port)
     from paper_1812_01307_b200 import parallel, solvers
     from paper_1812_01307_b200.blockops import make_partition
@@ -66,7 +66,8 @@ def _ls_worker(rank, world, port, outdir, epochs, sample_every):
     a = golden_csr(z)
     m, n = (int(v) for v in z["mn"])
     shard = parallel.CudaShard(a, parallel.ShardSpec(make_partition(a.shape[0], a.shape[1], m, n), rank, world))
-    cfg = solvers.SolverConfig(mu=c["mu"], lam=0.0, epochs=epochs)
+    cfg = solvers.SolverConfig(mu=c["mu"] * mu_scale, lam=0.0, epochs=epochs, alpha=frac, gamma=frac,
+                               enforce_decrease=enforce)
     tr = solvers.run_solver("bsgd", solvers.Problem(shard, z["y"], z["x_true"]), cfg, sample_every=sample_every,
                             group="default", chunk_epochs=8)
     u, _, _ = parallel.distributed_largest_eigenvalue(shard, max_iters=50)
@@ -76,15 +77,20 @@ def _ls_worker(rank, world, port, outdir, epochs, sample_every):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_row_slabs_run_solver_matches_oracle(cuda_ok, tmp_path, world):
+@pytest.mark.parametrize("world,mu_scale,frac,enforce",
+                         [(2, 1.0, 1.0, False), (3, 1.0, 1.0, False), (2, 1.0, 0.5, False), (3, 3.0, 0.5, True),
+                          (2, 6.0, 1.0, True)])
+def test_row_slabs_run_solver_matches_oracle(cuda_ok, tmp_path, world, mu_scale, frac, enforce):
+    """Real CUDA ranks over gloo through run_solver(group=...): full sweeps, the
+    stochastic pair subsets (alpha = gamma = 0.5: per-rank z caches) and
+    enforce_decrease (mu halved on every rank) against the oracle's run_bsgd."""
     from oracle import oracle as orc
     epochs, every = 13, 3
-    _spawn(_ls_worker, world, str(tmp_path), epochs, every)
+    _spawn(_ls_worker, world, str(tmp_path), epochs, every, mu_scale, frac, enforce)
     z = load_golden("p3_ls")
     c = golden_cfg(z)
     op = orc.OracleOperator(golden_csr(z), *(int(v) for v in z["mn"]))
-    prm = orc.Params(mu=c["mu"], lam=0.0, epochs=epochs)
+    prm = orc.Params(mu=c["mu"] * mu_scale, lam=0.0, epochs=epochs, alpha=frac, gamma=frac, enforce_decrease=enforce)
     ref = orc.run_bsgd(op, z["y"], prm, x_true=z["x_true"], sample_every=every)
     want = np.array(ref.samples)
     u_ref = float(load_golden("p3_eig")["value"])

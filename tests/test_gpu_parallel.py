@@ -266,6 +266,37 @@ def test_run_solver_group_world1_nccl_matches_single_gpu(cuda_ok):
     assert np.array_equal(tr.final_x, single.final_x)
 
 
+@pytest.mark.parametrize("case,enforce", [("p1_stoch", False), ("p1_stoch", True)])
+def test_run_solver_group_pair_subsets_match_single_gpu(cuda_ok, case, enforce):
+    """The stochastic pair subsets (alpha = gamma = 0.5, solvers.py:186-195) through the
+    distributed driver at world size 1 with the TV prox: the reference's own golden
+    configuration, equal to the single-GPU run_solver -- fractional epochs, exact
+    units, flags, samples; x bit for bit -- also with enforce_decrease on a step
+    four times too large."""
+    from paper_1812_01307_b200 import blockops, parallel, solvers, tv
+    z = load_golden(case)
+    c = golden_cfg(z)
+    a = golden_csr(z)
+    m, n = (int(v) for v in z["mn"])
+    part = make_partition(a.shape[0], a.shape[1], m, n)
+    layout = tv.PixelLayout(*(int(v) for v in z["hw"]), z["perm"]) if "perm" in z else None
+    assert c["alpha"] < 1 and c["gamma"] < 1
+    cfg = solvers.SolverConfig(mu=c["mu"] * (4.0 if enforce else 1.0), lam=c["lam"], epochs=6, alpha=c["alpha"],
+                               gamma=c["gamma"], enforce_decrease=enforce, seed=c["seed"],
+                               prox=tv.ProxSettings(c["max_inner_iters"], c["tol"]))
+    single = solvers.run_solver("bsgd", solvers.Problem(blockops.BlockOperator(a, part), z["y"], z["x_true"], layout),
+                                cfg, sample_every=1)
+    shard = parallel.CudaShard(a, parallel.ShardSpec(part, 0, 1), lam=c["lam"], layout=layout)
+    tr = solvers.run_solver("bsgd", solvers.Problem(shard, z["y"], z["x_true"], layout), cfg, sample_every=1,
+                            group="default")
+    got, want = np.array([tuple(s) for s in tr.samples]), np.array([tuple(s) for s in single.samples])
+    assert got.shape == want.shape and len(got) > 6
+    assert np.array_equal(got[:, 0], want[:, 0]) and np.array_equal(got[:, 3], want[:, 3])
+    assert np.allclose(got[:, 1:3], want[:, 1:3], rtol=1e-12)
+    assert list(tr.decrease_flags) == list(single.decrease_flags)
+    assert np.array_equal(tr.final_x, single.final_x)
+
+
 @pytest.mark.parametrize("case,mu_scale", [("p3_ls", 6.0), ("p1_ct", 4.0)])
 def test_run_solver_group_enforce_decrease_matches_single_gpu(cuda_ok, case, mu_scale):
     """enforce_decrease (solvers.py:325-333) through the distributed driver at world

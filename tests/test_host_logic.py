@@ -180,16 +180,17 @@ def test_canonical_csr_sums_float32_duplicates_in_float64():
 
 
 def test_distributed_driver_rejects_unsupported_modes():
-    """DistributedBSGD raises on alpha / gamma < 1 instead of silently running a
-    different algorithm (solvers.py:186-195); enforce_decrease is supported with the
-    replicated prox (tests/test_parallel_gloo.py)."""
+    """DistributedBSGD raises instead of silently running a different algorithm: the
+    stochastic pair subsets (alpha / gamma < 1, solvers.py:186-195) need a row-slab
+    shard with pair products (they and enforce_decrease are supported there,
+    tests/test_parallel_gloo.py), not a slice shard or an unknown backend."""
     import types
     from paper_1812_01307_b200 import parallel
     from paper_1812_01307_b200.solvers import SolverConfig
-    shard = types.SimpleNamespace()
-    for kw in ({"alpha": 0.5}, {"gamma": 0.5}):
-        with pytest.raises(ValueError):
-            parallel.DistributedBSGD(shard, np.zeros(4), SolverConfig(mu=0.1, **kw))
+    for shard in (types.SimpleNamespace(), types.SimpleNamespace(owns_slices=True, pair_products=None)):
+        for kw in ({"alpha": 0.5}, {"gamma": 0.5}):
+            with pytest.raises(ValueError):
+                parallel.DistributedBSGD(shard, np.zeros(4), SolverConfig(mu=0.1, **kw))
 
 
 def test_slab_program_is_pw_combine():

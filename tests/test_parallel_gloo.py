@@ -54,6 +54,29 @@ class CpuShard:
     def grad(self, r_local, g_out):
         g_out.copy_(torch.from_numpy(2.0 * (self.a.T @ r_local.numpy())))
 
+    def pair_products(self, local_rows, cols_sel, x_k, r_k, y_local, z, g_out, r_next):
+        ncb = self.spec.partition.num_col_blocks
+        zc = z.numpy().reshape(ncb, self.rows)
+        x, r = x_k.numpy(), r_k.numpy()
+        g = np.zeros(self.cols)
+        for i in local_rows:
+            r0, r1 = self.spec.local_row_bounds[i]
+            for j in cols_sel:
+                c0, c1 = self.spec.partition.col_bounds[j]
+                blk = self.a[r0:r1, c0:c1]
+                zc[j, r0:r1] = blk @ x[c0:c1]
+                g[c0:c1] += blk.T @ r[r0:r1]
+        g_out.copy_(torch.from_numpy(2.0 * g))
+        rn = y_local.numpy().copy()
+        for j in range(ncb):
+            rn -= zc[j]
+        r_next.copy_(torch.from_numpy(rn))
+
+    def block_nnz_table(self):
+        ncb = self.spec.partition.num_col_blocks
+        return np.array([[self.a[r0:r1, self.spec.partition.col_bounds[j][0]:self.spec.partition.col_bounds[j][1]].nnz
+                          for j in range(ncb)] for r0, r1 in self.spec.local_row_bounds], dtype=np.float64)
+
     def step(self, a):
         xk, g = a.x_k.numpy(), a.g.numpy()
         xn = xk + a.mu * g
@@ -233,7 +256,7 @@ def test_world2_gloo_matches_single_process_oracle(tmp_path):
     assert np.allclose(hist[:, H.FNEXT], fnext, rtol=1e-12)
 
 
-def _solver_worker(rank, world, port, outdir, epochs, mu_scale, sample_every, enforce=False):
+def _solver_worker(rank, world, port, outdir, epochs, mu_scale, sample_every, enforce=False, frac=1.0):
     import sys
     sys.path.insert(0, REPO)
     sys.path.insert(0, os.path.join(REPO, "tests"))
@@ -247,7 +270,8 @@ def _solver_worker(rank, world, port, outdir, epochs, mu_scale, sample_every, en
     m, n = (int(v) for v in z["mn"])
     spec = parallel.ShardSpec(make_partition(a.shape[0], a.shape[1], m, n), rank, world)
     shard = CpuShard(a, spec)
-    cfg = solvers.SolverConfig(mu=c["mu"] * mu_scale, lam=0.0, epochs=epochs, enforce_decrease=enforce)
+    cfg = solvers.SolverConfig(mu=c["mu"] * mu_scale, lam=0.0, epochs=epochs, enforce_decrease=enforce, alpha=frac,
+                               gamma=frac)
     out = {}
     try:
         tr = solvers.run_solver("bsgd", solvers.Problem(shard, z["y"], z["x_true"]), cfg, sample_every=sample_every,
@@ -263,24 +287,27 @@ def _solver_worker(rank, world, port, outdir, epochs, mu_scale, sample_every, en
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("epochs,mu_scale,sample_every,enforce",
-                         [(13, 1.0, 3, False), (400, 1.3 * 0.5 / 0.9, 25, False), (30, 6.0, 4, True)])
-def test_world2_gloo_run_solver_matches_oracle(tmp_path, epochs, mu_scale, sample_every, enforce):
+@pytest.mark.parametrize("epochs,mu_scale,sample_every,enforce,frac",
+                         [(13, 1.0, 3, False, 1.0), (400, 1.3 * 0.5 / 0.9, 25, False, 1.0), (30, 6.0, 4, True, 1.0),
+                          (9, 1.0, 2, False, 0.5), (6, 3.0, 1, True, 0.5)])
+def test_world2_gloo_run_solver_matches_oracle(tmp_path, epochs, mu_scale, sample_every, enforce, frac):
     """run_solver(..., group=...) over two ranks (one all-reduce per epoch, lagged
     tail): the trace -- epochs, relative errors, objectives, exact matvec units,
     decrease flags -- and the final x match the oracle's run_bsgd; with a step
     beyond the Theorem-1 bound both raise DivergenceError at the same epoch; with
     enforce_decrease (solvers.py:325-333) the same step is halved on both ranks
-    exactly as the oracle halves it."""
+    exactly as the oracle halves it; with alpha = gamma = 0.5 (solvers.py:186-195) each
+    rank commits the selected pairs of its own row blocks to its z cache and the
+    fractional epochs, units and samples follow the oracle's."""
     from oracle import oracle as orc
     port = _free_port()
-    mp.spawn(_solver_worker, args=(2, port, str(tmp_path), epochs, mu_scale, sample_every, enforce), nprocs=2,
+    mp.spawn(_solver_worker, args=(2, port, str(tmp_path), epochs, mu_scale, sample_every, enforce, frac), nprocs=2,
              join=True)
     r0, r1 = np.load(tmp_path / "run0.npz"), np.load(tmp_path / "run1.npz")
     z = load_golden("p3_ls")
     c = golden_cfg(z)
     op = orc.OracleOperator(golden_csr(z), *(int(v) for v in z["mn"]))
-    prm = orc.Params(mu=c["mu"] * mu_scale, lam=0.0, epochs=epochs, enforce_decrease=enforce)
+    prm = orc.Params(mu=c["mu"] * mu_scale, lam=0.0, epochs=epochs, enforce_decrease=enforce, alpha=frac, gamma=frac)
     ref = orc.run_bsgd(op, z["y"], prm, x_true=z["x_true"], sample_every=sample_every)
     want = np.array(ref.samples)
     for r in (r0, r1):
