@@ -321,8 +321,9 @@ def run_ours(args):
     # ---- standalone prox at the FGP cap (non-converging tolerance) ----
     img = torch.rand(d.height, d.width, dtype=torch.float64, device=dev)
     pst = tv.ProxSettings(d.max_inner_iters, 1e-300)
-    tv.tv_prox(img, 0.05, pst)
-    pms = time_events(lambda: tv.tv_prox(img, 0.05, pst), 5)
+    for _ in range(5):   # a sub-millisecond kernel: warm the clocks before the timed repetitions
+        tv.tv_prox(img, 0.05, pst)
+    pms = time_events(lambda: tv.tv_prox(img, 0.05, pst), 20)
     pb = prox_bytes(d.height * d.width, 2, d.max_inner_iters)
     roofline["tv_prox_standalone"] = {"image": f"{d.height}x{d.width}", "iterations": d.max_inner_iters,
                                       "ms": round(pms, 4), "algorithmic_bytes": pb,
@@ -472,8 +473,9 @@ def run_secondary(args, index):
     if shape is not None:
         img = torch.rand(*shape, dtype=torch.float64, device="cuda")
         pst = tv.ProxSettings(inner, 1e-300)
-        tv.tv_prox(img, 0.05, pst)
-        pms = time_events(lambda: tv.tv_prox(img, 0.05, pst), 5)
+        for _ in range(3):
+            tv.tv_prox(img, 0.05, pst)
+        pms = time_events(lambda: tv.tv_prox(img, 0.05, pst), 10)
         npx = int(np.prod(shape))
         pb = prox_bytes(npx, len(shape), inner)
         if npx >= (1 << 21):
