@@ -418,8 +418,8 @@ def test_blocked_gather_order_bit_identical(B, monkeypatch, lanes, compress):
         assert np.array_equal(r1.cpu().numpy(), r0.cpu().numpy()) and float(s1) == float(s0)
 
 
-@pytest.mark.parametrize("grid", ["sinogram", "none"])
-def test_transposed_blocked_stream(B, monkeypatch, grid):
+@pytest.mark.parametrize("grid,dtype", [("sinogram", np.float32), ("none", np.float32), ("sinogram", np.float64)])
+def test_transposed_blocked_stream(B, monkeypatch, grid, dtype):
     """The blocked stream of A^T (bsgd_plan_blocked_transposed): 16 lanes per pixel
     row, gathers from r in 4 x 4 sinogram tiles (ragged last bin tile: 181 bins) with
     16-bit offset indices, or in A^T's own order.  Lane l sums the entries = l mod 16
@@ -429,7 +429,7 @@ def test_transposed_blocked_stream(B, monkeypatch, grid):
     blockops, tv = B[0], B[1]
     from paper_1812_01307_b200 import problems, solvers
     n, ang, nb = 128, 30, 181
-    a = problems.parallel_beam_matrix(n, ang, nb, dtype=np.float32)
+    a = problems.parallel_beam_matrix(n, ang, nb, dtype=dtype)
     part = blockops.make_partition(*a.shape, 2, 3)
     tiled = blockops.BlockOperator(a, part)
     tiled.set_gather_tiles(True, blockops.grid_tiles(n, n))
@@ -461,6 +461,10 @@ def test_transposed_blocked_stream(B, monkeypatch, grid):
     assert np.array_equal(s1.x, s2.x)
     blk.set_transposed_blocked(None)
     assert blk.kernel_info()["transposed"] == "csr"
+    stacked = blockops.BlockOperator.stacked(problems.parallel_beam_matrix(8, 6, 11), 2,
+                                             blockops.make_partition(6 * 11 * 2, 64 * 2, 2, 2))
+    with pytest.raises(ValueError):
+        stacked.set_transposed_blocked((6, 11))
 
 
 @pytest.mark.parametrize("index", [2, 3])
