@@ -470,13 +470,16 @@ def test_transposed_blocked_stream(B, monkeypatch, grid, dtype):
 @pytest.mark.parametrize("index", [2, 3])
 def test_ct_full_size_products_consistent(B, index):
     """configs[2] / configs[3] at full size (2.4e8 / 1.9e9 nonzeros, projector built on
-    the GPU) through the kernels the epoch uses -- blocked forward stream with several
-    rays per warp, gather-tiled transposed product -- against size-independent
+    the GPU) through the kernels the epoch uses -- tile-ordered blocked streams with 16-bit
+    offset indices for A and A^T (asserted via kernel_info) -- against size-independent
     properties: adjointness, and agreement with the block-restricted kernels (a
     different reduction) on sampled row / column blocks."""
     from paper_1812_01307_b200 import problems
     d = problems.config_device(index)
     op = d.op
+    ki = op.kernel_info()
+    assert ki["forward"] == "blocked_compressed" and ki["forward_order"] == "tile4" and ki["forward_lanes"] == 16
+    assert ki["transposed"] == "blocked_compressed" and ki["transposed_order"] == "tile4"
     rows, cols = op.shape
     rng = np.random.default_rng(index)
     x, w = rng.random(cols), rng.standard_normal(rows)
