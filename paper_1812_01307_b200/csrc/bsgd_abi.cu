@@ -443,7 +443,10 @@ static int build_blocked_dir(bsgd_plan *p, bool tr, int gh, int gw, cudaStream_t
     // indices stream best (configs[3]: 4 lanes plain 3.01 ms, 8 compressed 2.56, 16
     // compressed 2.46, 32 plain 3.07; configs[2]: 8 -> 16 lanes 0.369 -> 0.317).
     const double mean = (double)p->nnz / (double)std::max<int64_t>(b.nrows, 1);
-    b.gb = order ? 16 : mean >= 768.0 ? 4 : 8;
+    // A^T in its own order (pixel rows of a CT system whose sinogram grid is unknown):
+    // 8 lanes with compressed indices (configs[3] K2: 4 lanes plain 3.53 ms, 8 compressed
+    // 3.29, 16: 3.83, 32: 5.60; the CSR kernel 6.1)
+    b.gb = order ? 16 : tr ? 8 : mean >= 768.0 ? 4 : 8;
     if (const char *g = getenv(tr ? "BSGD_BLK_G_TR" : "BSGD_BLK_G")) {   // experiments
         const int v = atoi(g);
         if (v == 4 || v == 8 || v == 16 || v == 32) b.gb = v;
@@ -1648,6 +1651,17 @@ static int plan_finish(bsgd_plan *p, cudaStream_t st) {
     if (rc != BSGD_OK) return rc;
     rc = (value_dtype == BSGD_F32) ? tune_blocked<float>(p, p->fb) : tune_blocked<double>(p, p->fb);
     if (rc != BSGD_OK) return rc;
+    // A^T's rows long too (a CT system handed over as a plain CSR: ~1.3 nonzeros per
+    // angle and pixel): a blocked copy of A^T in its own column order, which
+    // bsgd_plan_blocked_transposed replaces by the tile-ordered one when the caller
+    // names the grid of A's rows
+    if (!p->stacked() && cols > 0 && (double)p->nnz / (double)cols >= 384.0 && !getenv("BSGD_NO_BLOCKED")) {
+        rc = (value_dtype == BSGD_F32) ? build_blocked_dir<float>(p, true, 0, 0, st)
+                                       : build_blocked_dir<double>(p, true, 0, 0, st);
+        if (rc != BSGD_OK) return rc;
+        rc = (value_dtype == BSGD_F32) ? tune_blocked<float>(p, p->tb) : tune_blocked<double>(p, p->tb);
+        if (rc != BSGD_OK) return rc;
+    }
     // block nnz table (blockops.py:179-180)
     unsigned long long *d_cnt = nullptr;
     const int64_t nb = num_row_blocks * num_col_blocks;

@@ -467,6 +467,44 @@ def test_transposed_blocked_stream(B, monkeypatch, grid, dtype):
         stacked.set_transposed_blocked((6, 11))
 
 
+def test_plain_csr_ct_system_gets_blocked_streams(B):
+    """A CT system handed over as a plain scipy CSR (the reference's own call,
+    blockops.py:123-152; no grid hints): rays and pixel rows are both long, so the plan
+    builds the blocked stream of A (square image: tile order) and, on its own, a blocked
+    stream of A^T in A^T's column order; products, residual and two TV epochs against
+    the oracle; naming the sinogram grid afterwards switches A^T to the tile order
+    with the same rounding-level agreement."""
+    blockops, tv = B[0], B[1]
+    from paper_1812_01307_b200 import problems, solvers
+    n, ang, nb = 256, 400, 363                 # ~510 nonzeros per pixel row, ~230 per ray
+    a = problems.parallel_beam_matrix(n, ang, nb, dtype=np.float32)
+    assert a.nnz / a.shape[1] >= 384
+    op = blockops.BlockOperator(a, blockops.make_partition(*a.shape, 4, 4))
+    ki = op.kernel_info()
+    assert ki["transposed"] == "blocked_compressed" and ki["transposed_lanes"] == 8
+    assert ki["transposed_order"] == "native"
+    oop = orc.OracleOperator(a, 4, 4)
+    rng = np.random.default_rng(17)
+    x, w = rng.standard_normal(a.shape[1]), rng.standard_normal(a.shape[0])
+    assert rel(op.rmatvec(w, charge=False), oop.rmatvec(w)) < 1e-12
+    assert rel(op.matvec(x, charge=False), oop.matvec(x)) < 1e-12
+    y = rng.standard_normal(a.shape[0])
+    mu = 1e-5
+    cfg = solvers.SolverConfig(mu=mu, lam=0.5, epochs=2, prox=tv.ProxSettings(10, 1e-5))
+    lay = tv.PixelLayout.row_major(n, n)
+    st = solvers.init_bsgd_state(op, y, cfg)
+    prm = orc.Params(mu=mu, lam=0.5, epochs=2, max_inner_iters=10, tol=1e-5)
+    ost = orc.init_state(oop, y, prm)
+    for _ in range(2):
+        solvers.bsgd_tv_iteration(st, op, y, cfg, layout=lay)
+        orc.epoch(ost, oop, y, prm, lay.perm, (n, n))
+    assert rel(st.x, ost.x) < 1e-9 and rel(st.r_vec, ost.r_vec) < 1e-9
+    op.set_transposed_blocked((ang, nb))
+    ki = op.kernel_info()
+    assert ki["transposed_order"] == "tile4" and ki["transposed_lanes"] == 16
+    assert rel(op.rmatvec(w, charge=False), oop.rmatvec(w)) < 1e-12
+
+
 @pytest.mark.parametrize("index", [2, 3])
 def test_ct_full_size_products_consistent(B, index):
     """configs[2] / configs[3] at full size (2.4e8 / 1.9e9 nonzeros, projector built on
