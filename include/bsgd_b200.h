@@ -152,8 +152,9 @@ int bsgd_plan_gather_tiles(bsgd_plan *plan, int transposed, int64_t ntiles, cons
  * gathered vector r lives on (row-major; a sinogram's angles x bins): the stream is
  * then gathered in 4 x 4 grid tiles (one 128-byte line each) from r permuted into
  * that order before each launch, with 16-bit offset indices when they fit.  0, 0 =
- * no grid (A^T's own column order); a negative size removes the copy.  The blocked
- * copy takes precedence over gather tiles.  Values agree with the CSR kernel to
+ * no grid (A^T's own column order); a negative size removes the copy.  Between the
+ * blocked copy and gather tiles of A^T the latest explicit request wins (requesting
+ * gather tiles drops the blocked copy; a blocked copy built later runs instead of them).  Values agree with the CSR kernel to
  * rounding (lane-strided per-row sums, fixed shuffle tree). */
 int bsgd_plan_blocked_transposed(bsgd_plan *plan, int64_t grid_h, int64_t grid_w, void *stream);
 /* depth (1 for ordinary plans) and the stored CSR's shape / nnz */

@@ -353,8 +353,8 @@ class BlockOperator:
 
         ``grid`` = (h, w) with h * w = rows of A: the grid r lives on (a sinogram's
         angles x bins); A^T's gathers then run in 4 x 4 grid tiles.  ``()`` builds
-        the copy in A^T's own column order; None removes it.  Takes precedence
-        over gather tiles.  Values agree with the CSR kernel to rounding.
+        the copy in A^T's own column order; None removes it.  Replaces gather
+        tiles of A^T (and `set_gather_tiles(True, ...)` afterwards replaces it).  Values agree with the CSR kernel to rounding.
         """
         if self.depth > 1:
             raise ValueError("stacked operators have no blocked stream")

@@ -1888,6 +1888,10 @@ int bsgd_plan_gather_tiles(bsgd_plan *p, int transposed, int64_t ntiles, const i
     int rc = p->vdt == BSGD_F32 ? build_gtiles<float>(p, transposed != 0, ntiles, tile_ptr, tile_rows, st)
                                 : build_gtiles<double>(p, transposed != 0, ntiles, tile_ptr, tile_rows, st);
     if (rc) return rc;
+    if (transposed) {   // the latest explicit request wins over a blocked copy of A^T
+        p->device_bytes -= p->tb.bytes;
+        blk_free(p->tb);
+    }
     // The caller asked for these tiles, so they are kept: no timing race decides
     // which kernel a plan runs.  BlockOperator requests them where they win
     // (pixel rows of A^T for CT: 6.1 -> 4.2 ms at 1024^2, whose CSR gathers have

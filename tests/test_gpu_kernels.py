@@ -503,6 +503,9 @@ def test_plain_csr_ct_system_gets_blocked_streams(B):
     ki = op.kernel_info()
     assert ki["transposed_order"] == "tile4" and ki["transposed_lanes"] == 16
     assert rel(op.rmatvec(w, charge=False), oop.rmatvec(w)) < 1e-12
+    op.set_gather_tiles(True, blockops.grid_tiles(n, n))      # the latest explicit request wins
+    assert op.kernel_info()["transposed"] == "gather_tiled"
+    assert rel(op.rmatvec(w, charge=False), oop.rmatvec(w)) < 1e-12
 
 
 @pytest.mark.parametrize("index", [2, 3])
