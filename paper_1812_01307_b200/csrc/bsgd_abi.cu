@@ -730,8 +730,8 @@ static int launch_gtile(const bsgd_plan::GTileStore &S, const double *vec, const
 static bool gtiles_on(const bsgd_plan::GTileStore &S) { return S.ok; }
 
 template <typename V, class E>
-static int launch_blocked(const bsgd_plan::BlkStore &B, const double *vec, const E &e, double *part, int64_t *cnt,
-                          cudaStream_t st) {
+static int launch_blocked(const bsgd_plan::BlkStore &B, bool tr, const double *vec, const E &e, double *part,
+                          int64_t *cnt, cudaStream_t st) {
     if (B.order) {
         blk_permute_kernel<<<grid_1d(B.veclen), kThreads, 0, st>>>(B.veclen, vec, B.xt, B.gw, B.order);
         vec = B.xt;
@@ -744,7 +744,12 @@ static int launch_blocked(const bsgd_plan::BlkStore &B, const double *vec, const
         kern<<<ctas_for(B.nrows, G, cap), kThreads, 0, st>>>(A, e, part, cnt);
     };
     const bool cmp = B.half != nullptr;
-    if (B.gb == 16) cmp ? go(csr_blocked_kernel<V, 16, E, true>, 16) : go(csr_blocked_kernel<V, 16, E>, 16);
+    // 16 lanes, compressed, tile order: A^T's pixel rows (twice as long as the rays, a
+    // higher L1 hit rate) run best at 32 registers / 64 warps per SM, A's rays at 40 / 48
+    // (configs[3]: K2 2.55-2.60 -> 2.47 ms, K1 2.42-2.46 -> 2.53 ms with 64 warps)
+    static const int minb_tr = getenv("BSGD_BLK_MINB_TR") ? atoi(getenv("BSGD_BLK_MINB_TR")) : 8;   // experiments
+    if (tr && B.gb == 16 && cmp && B.order && minb_tr == 8) go(csr_blocked_w64_kernel<V, 16, E, true>, 16);
+    else if (B.gb == 16) cmp ? go(csr_blocked_kernel<V, 16, E, true>, 16) : go(csr_blocked_kernel<V, 16, E>, 16);
     else if (B.gb == 8) cmp ? go(csr_blocked_kernel<V, 8, E, true>, 8) : go(csr_blocked_kernel<V, 8, E>, 8);
     else if (B.gb == 4) cmp ? go(csr_blocked_kernel<V, 4, E, true>, 4) : go(csr_blocked_kernel<V, 4, E>, 4);
     else cmp ? go(csr_blocked_kernel<V, 32, E, true>, 32) : go(csr_blocked_kernel<V, 32, E>, 32);
@@ -796,14 +801,14 @@ template <typename V, class E>
 static int launch_fwd(const bsgd_plan *p, const double *vec, const E &e, double *part, int64_t *cnt, cudaStream_t st) {
     if (p->stacked()) return launch_stacked_dir<V>(p, false, vec, e, part, cnt, st);
     if (gtiles_on(p->gf)) return launch_gtile<V>(p->gf, vec, e, part, cnt, st);
-    if (blocked_on(p)) return launch_blocked<V>(p->fb, vec, e, part, cnt, st);
+    if (blocked_on(p)) return launch_blocked<V>(p->fb, false, vec, e, part, cnt, st);
     return launch_one<V>(fwd_csr<V>(p, vec), p->g_fwd, e, part, cnt, p->nnz, st);
 }
 
 template <typename V, class E>
 static int launch_tr(const bsgd_plan *p, const double *vec, const E &e, double *part, int64_t *cnt, cudaStream_t st) {
     if (p->stacked()) return launch_stacked_dir<V>(p, true, vec, e, part, cnt, st);
-    if (blocked_tr_on(p)) return launch_blocked<V>(p->tb, vec, e, part, cnt, st);
+    if (blocked_tr_on(p)) return launch_blocked<V>(p->tb, true, vec, e, part, cnt, st);
     if (gtiles_on(p->gt)) return launch_gtile<V>(p->gt, vec, e, part, cnt, st);
     return launch_one<V>(tr_csr<V>(p, vec), p->g_tr, e, part, cnt, p->nnz, st);
 }

@@ -305,8 +305,8 @@ __device__ __forceinline__ void blk_vals(const double *p, double (&v)[4], uint64
     v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
 }
 
-template <typename V, int GB, class Epi, bool CMP = false>
-__global__ void __launch_bounds__(kThreads) csr_blocked_kernel(CsrB<V> A, Epi epi, double *part, int64_t *cnt) {
+template <typename V, int GB, class Epi, bool CMP>
+__device__ __forceinline__ void csr_blocked_body(const CsrB<V> &A, Epi &epi, double *part, int64_t *cnt) {
     constexpr int BLK = 4 * GB;
     constexpr int RPW = 32 / GB;
     __shared__ double sm[8 * (kThreads / 32)];
@@ -354,6 +354,20 @@ __global__ void __launch_bounds__(kThreads) csr_blocked_kernel(CsrB<V> A, Epi ep
             for (int q = 0; q < Epi::K; ++q) part[(size_t)blockIdx.x * Epi::K + q] = v[q];
     }
     if (blockIdx.x == 0 && threadIdx.x == 0 && cnt != nullptr) cnt[0] = gridDim.x;
+}
+
+// Two register budgets of the same body: ptxas fits the loop in 40 registers (48 warps
+// per SM) when left alone and in 32 (64 warps) when asked for 8 CTAs per SM, both
+// without spills (any other explicit bound measured slower: 1 -> 64 registers, 6 -> a
+// different 40-register schedule).  Which one wins depends on the product (launch_blocked).
+template <typename V, int GB, class Epi, bool CMP = false>
+__global__ void __launch_bounds__(kThreads) csr_blocked_kernel(CsrB<V> A, Epi epi, double *part, int64_t *cnt) {
+    csr_blocked_body<V, GB, Epi, CMP>(A, epi, part, cnt);
+}
+template <typename V, int GB, class Epi, bool CMP = false>
+__global__ void __launch_bounds__(kThreads, 8) csr_blocked_w64_kernel(CsrB<V> A, Epi epi, double *part,
+                                                                      int64_t *cnt) {
+    csr_blocked_body<V, GB, Epi, CMP>(A, epi, part, cnt);
 }
 
 // compress the blocked indices (CsrB::half / off): one thread per block of 4 gb stored
