@@ -178,6 +178,8 @@ int bsgd_plan_info(const bsgd_plan *plan, int64_t *rows, int64_t *cols, int64_t 
 #define BSGD_K_STACKED_TILE 5  /* stacked_tile_kernel (stacked.cuh) */
 #define BSGD_ORDER_NATIVE 0     /* gathers in the matrix's own column order */
 #define BSGD_ORDER_TILE4 1      /* blocked stream over a grid (n x n image; sinogram): 4 x 4 tiles */
+#define BSGD_ORDER_TILE8X2 4    /* tiles of 8 grid rows x 2 columns (A^T on a sinogram: entries run along the angles) */
+#define BSGD_ORDER_TILE2X8 5    /* tiles of 2 grid rows x 8 columns */
 #define BSGD_ORDER_MORTON 2     /* (experiment, BSGD_BLK_ORDER=morton) Z order */
 typedef struct bsgd_kernel_info {
     int32_t fwd_kernel, fwd_lanes;  /* A x  (K1) */

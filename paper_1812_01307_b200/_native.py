@@ -55,7 +55,7 @@ class KernelInfo(ctypes.Structure):
 
 KERNEL_NAMES = {0: "csr", 1: "blocked", 2: "blocked_compressed", 3: "gather_tiled", 4: "stacked",
                 5: "stacked_tile"}
-GATHER_ORDERS = {0: "native", 1: "tile4", 2: "morton"}
+GATHER_ORDERS = {0: "native", 1: "tile4", 2: "morton", 4: "tile8x2", 5: "tile2x8"}
 TIMING_PHASES = ("k1_first", "k2_step", "prox", "k1_lookahead", "tail")
 
 

@@ -431,8 +431,33 @@ static int build_blocked_dir(bsgd_plan *p, bool tr, int gh, int gw, cudaStream_t
         order = strcmp(o, "tile4") == 0 ? 1 : strcmp(o, "morton") == 0 ? 2 : 0;
     if (gh <= 0 || gw <= 0 || (int64_t)gh * gw != b.veclen) order = 0;
     if (order == 2 && (gh != gw || (gw & (gw - 1)) != 0)) order = 0;
+    // Tile shape (structural, from the matrix alone): the footprint of a gather
+    // instruction -- 16 consecutive entries of a row -- on the grid.  Rays cross the
+    // image in every direction (row and column spans balance: 4 x 4 tiles); a pixel's
+    // entries run along the sinogram's angles with a slowly drifting bin (row spans
+    // twice the column spans: 8 x 2 tiles, configs[3] K2 2.46-2.50 -> 2.24-2.29 ms once the
+    // 64-warp build had made it L1-bound).  BSGD_BLK_TILE = 1 | 4 | 5 forces a shape.
+    if (order == 1) {
+        unsigned long long *acc = nullptr, h[3] = {0, 0, 0};
+        if (cudaMalloc(&acc, sizeof(h)) == cudaSuccess) {
+            cudaMemsetAsync(acc, 0, sizeof(h), st);
+            blk_span_kernel<<<grid_1d(b.nrows, kThreads / 32), kThreads, 0, st>>>(b.nrows, sptr, sidx, gw, acc);
+            cudaMemcpyAsync(h, acc, sizeof(h), cudaMemcpyDeviceToHost, st);
+            cudaStreamSynchronize(st);
+            cudaFree(acc);
+        }
+        cudaGetLastError();
+        if (h[2] > 0 && 2 * h[0] >= 3 * h[1]) order = 4;        // grid-row spans >= 1.5 x column spans
+        else if (h[2] > 0 && 2 * h[1] >= 3 * h[0]) order = 5;
+        if (const char *t = getenv("BSGD_BLK_TILE")) {
+            const int v = atoi(t);
+            if (v == 1 || v == 4 || v == 5) order = v;
+        }
+    }
     int64_t xt_len = b.veclen;
     if (order == 1) xt_len = (int64_t)((gh + 3) / 4) * ((gw + 3) / 4) * 16;
+    if (order == 4) xt_len = (int64_t)((gh + 7) / 8) * ((gw + 1) / 2) * 16;
+    if (order == 5) xt_len = (int64_t)((gh + 1) / 2) * ((gw + 7) / 8) * 16;
     if (xt_len > INT32_MAX) order = 0;
     // Lanes per row.  In the matrix's own column order, few lanes per ray and several
     // adjacent rays per warp: the neighbouring bins of a steep ray read the same sectors
@@ -783,7 +808,10 @@ static int tune_blocked(bsgd_plan *p, bsgd_plan::BlkStore &b) {
     }
     const int64_t n = [&]() { int64_t v = 0; cudaMemcpy(&v, b.ptr + b.nrows, sizeof(int64_t), cudaMemcpyDeviceToHost); return v; }();
     p->device_bytes -= b.bytes;
-    const size_t xt_len = b.order == 1 ? (size_t)((b.gh + 3) / 4) * ((b.gw + 3) / 4) * 16 : (size_t)b.veclen;
+    const size_t xt_len = b.order == 1   ? (size_t)((b.gh + 3) / 4) * ((b.gw + 3) / 4) * 16
+                          : b.order == 4 ? (size_t)((b.gh + 7) / 8) * ((b.gw + 1) / 2) * 16
+                          : b.order == 5 ? (size_t)((b.gh + 1) / 2) * ((b.gw + 7) / 8) * 16
+                                         : (size_t)b.veclen;
     b.bytes = sizeof(int64_t) * (b.nrows + 1) +
               (keep_cmp ? sizeof(uint16_t) * (size_t)n + sizeof(int2) * (size_t)(n / (4 * b.gb)) : sizeof(int32_t) * (size_t)n) +
               sizeof(V) * (size_t)n + (b.xt ? sizeof(double) * xt_len : 0);

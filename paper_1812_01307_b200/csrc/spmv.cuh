@@ -400,7 +400,8 @@ __global__ void blk_compress_kernel(int64_t nblocks, int gb, const int32_t *idx,
 
 // Order of the blocked stream's gathers over the vector's grid (rows of n columns,
 // element c row-major): order 1 = 4 x 4 tiles (one 128-byte line each; a ragged last
-// tile column / row is padded), 2 = Morton (Z) order (square power-of-two grids)
+// tile column / row is padded), 4 = 8 x 2 tiles (8 grid rows x 2 columns), 5 = 2 x 8
+// tiles, 2 = Morton (Z) order (square power-of-two grids)
 __device__ __forceinline__ uint32_t spread_bits16(uint32_t v) {
     v &= 0xffffu;
     v = (v | (v << 8)) & 0x00ff00ffu;
@@ -412,6 +413,8 @@ __device__ __forceinline__ uint32_t spread_bits16(uint32_t v) {
 __device__ __forceinline__ int32_t blk_order_map(int32_t c, int n, int order) {
     const int y = c / n, x = c - y * n;
     if (order == 1) return ((y >> 2) * ((n + 3) >> 2) + (x >> 2)) * 16 + ((y & 3) << 2) + (x & 3);
+    if (order == 4) return ((y >> 3) * ((n + 1) >> 1) + (x >> 1)) * 16 + ((y & 7) << 1) + (x & 1);   // 8 x 2 tiles
+    if (order == 5) return ((y >> 1) * ((n + 7) >> 3) + (x >> 3)) * 16 + ((y & 1) << 3) + (x & 7);   // 2 x 8 tiles
     return (int32_t)((spread_bits16((uint32_t)y) << 1) | spread_bits16((uint32_t)x));
 }
 __global__ void blk_renumber_kernel(int64_t total, int32_t *idx, int n, int order) {
@@ -421,6 +424,40 @@ __global__ void blk_renumber_kernel(int64_t total, int32_t *idx, int n, int orde
 __global__ void blk_permute_kernel(int64_t cols, const double *x, double *xt, int n, int order) {
     for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < cols; c += (int64_t)gridDim.x * blockDim.x)
         xt[blk_order_map((int32_t)c, n, order)] = x[c];
+}
+
+// Footprint of a gather instruction on the grid: over every run of 16 consecutive
+// entries of a row, the spans (max - min + 1) of their grid rows and grid columns,
+// summed into acc[0] / acc[1] (acc[2] counts the runs).  One warp per row.
+__global__ void blk_span_kernel(int64_t nrows, const int64_t *ptr, const int32_t *idx, int gw,
+                                unsigned long long *acc) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    unsigned long long sy = 0, sx = 0, cnt = 0;
+    for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < nrows; r += nw) {
+        const int64_t beg = ptr[r], end = ptr[r + 1];
+        for (int64_t k = beg + 16 * lane; k + 16 <= end; k += 16 * 32) {
+            int y0 = INT32_MAX, y1 = -1, x0 = INT32_MAX, x1 = -1;
+            for (int q = 0; q < 16; ++q) {
+                const int c = idx[k + q];
+                const int y = c / gw, x = c - y * gw;
+                y0 = min(y0, y); y1 = max(y1, y); x0 = min(x0, x); x1 = max(x1, x);
+            }
+            sy += (unsigned long long)(y1 - y0 + 1);
+            sx += (unsigned long long)(x1 - x0 + 1);
+            ++cnt;
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        sy += __shfl_xor_sync(0xffffffffu, sy, o);
+        sx += __shfl_xor_sync(0xffffffffu, sx, o);
+        cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    }
+    if (lane == 0 && cnt) {
+        atomicAdd(acc, sy);
+        atomicAdd(acc + 1, sx);
+        atomicAdd(acc + 2, cnt);
+    }
 }
 
 // padded row lengths (whole blocks of blk entries) for the blocked copy

@@ -418,10 +418,12 @@ def test_blocked_gather_order_bit_identical(B, monkeypatch, lanes, compress):
         assert np.array_equal(r1.cpu().numpy(), r0.cpu().numpy()) and float(s1) == float(s0)
 
 
-@pytest.mark.parametrize("grid,dtype", [("sinogram", np.float32), ("none", np.float32), ("sinogram", np.float64)])
+@pytest.mark.parametrize("grid,dtype", [("sinogram", np.float32), ("none", np.float32), ("sinogram", np.float64),
+                                        ("sinogram4x4", np.float32), ("sinogram8x2", np.float32)])
 def test_transposed_blocked_stream(B, monkeypatch, grid, dtype):
     """The blocked stream of A^T (bsgd_plan_blocked_transposed): 16 lanes per pixel
-    row, gathers from r in 4 x 4 sinogram tiles (ragged last bin tile: 181 bins) with
+    row, gathers from r in sinogram tiles (the shape the plan picks from the gather
+    footprint, and 4 x 4 / 8 x 2 forced; ragged last tiles: 30 angles, 181 bins) with
     16-bit offset indices, or in A^T's own order.  Lane l sums the entries = l mod 16
     in order and the lanes fold in the same shuffle tree as the gather-tiled kernel,
     so the two agree bit for bit; both against the oracle, through rmatvec and the
@@ -436,10 +438,19 @@ def test_transposed_blocked_stream(B, monkeypatch, grid, dtype):
     blk = blockops.BlockOperator(a, part)
     if grid == "none":
         monkeypatch.setenv("BSGD_BLK_G_TR", "16")
-    blk.set_transposed_blocked((ang, nb) if grid == "sinogram" else ())
+    forced = {"sinogram4x4": ("1", "tile4"), "sinogram8x2": ("4", "tile8x2")}.get(grid)
+    if forced:
+        monkeypatch.setenv("BSGD_BLK_TILE", forced[0])
+    blk.set_transposed_blocked(() if grid == "none" else (ang, nb))
+    monkeypatch.delenv("BSGD_BLK_TILE", raising=False)
     ki = blk.kernel_info()
     assert ki["transposed"] == "blocked_compressed" and ki["transposed_lanes"] == 16
-    assert ki["transposed_order"] == ("tile4" if grid == "sinogram" else "native")
+    # the plan picks the tile shape from the gather footprint (here, with only 30 angles,
+    # the bins drift faster than the angles advance); the forced shapes cover the others
+    if forced:
+        assert ki["transposed_order"] == forced[1]
+    else:
+        assert ki["transposed_order"].startswith("tile") if grid == "sinogram" else ki["transposed_order"] == "native"
     assert tiled.kernel_info()["transposed"] == "gather_tiled"
     oop = orc.OracleOperator(a, 2, 3)
     rng = np.random.default_rng(8)
@@ -501,7 +512,7 @@ def test_plain_csr_ct_system_gets_blocked_streams(B):
     assert rel(st.x, ost.x) < 1e-9 and rel(st.r_vec, ost.r_vec) < 1e-9
     op.set_transposed_blocked((ang, nb))
     ki = op.kernel_info()
-    assert ki["transposed_order"] == "tile4" and ki["transposed_lanes"] == 16
+    assert ki["transposed_order"].startswith("tile") and ki["transposed_lanes"] == 16
     assert rel(op.rmatvec(w, charge=False), oop.rmatvec(w)) < 1e-12
     op.set_gather_tiles(True, blockops.grid_tiles(n, n))      # the latest explicit request wins
     assert op.kernel_info()["transposed"] == "gather_tiled"
@@ -520,7 +531,7 @@ def test_ct_full_size_products_consistent(B, index):
     op = d.op
     ki = op.kernel_info()
     assert ki["forward"] == "blocked_compressed" and ki["forward_order"] == "tile4" and ki["forward_lanes"] == 16
-    assert ki["transposed"] == "blocked_compressed" and ki["transposed_order"] == "tile4"
+    assert ki["transposed"] == "blocked_compressed" and ki["transposed_order"] == "tile8x2"
     rows, cols = op.shape
     rng = np.random.default_rng(index)
     x, w = rng.random(cols), rng.standard_normal(rows)
