@@ -302,10 +302,13 @@ def run_ours(args):
     ph = {k: v / max(n_ep, 1) for k, v in ph.items()}
     b1, b2 = csr_bytes(nnz, rows, cols)
     peak, peak_src = peaks()
-    kernels = {"k1_forward_lookahead": {"kernel": f"{op.kernel_info()['forward']} CSR, EpiResid (r = y - A x)",
+    kinfo = op.kernel_info()
+    kernels = {"k1_forward_lookahead": {"kernel": f"{kinfo['forward']} CSR ({kinfo['forward_lanes']} lanes per ray, gather order "
+                                                  f"{kinfo['forward_order']}), EpiResid (r = y - A x)",
                                         "ms": round(ph["k1_lookahead"], 4), "bytes": b1,
                                         "gbs": round(b1 / (ph["k1_lookahead"] * 1e6), 1)},
-               "k2_transposed_step": {"kernel": f"{op.kernel_info()['transposed']}, EpiStep (g = 2 A^T r, b = x + mu g)",
+               "k2_transposed_step": {"kernel": f"{kinfo['transposed']} A^T ({kinfo['transposed_lanes']} lanes per pixel, gather order "
+                                                f"{kinfo.get('transposed_order', 'native')}), EpiStep (g = 2 A^T r, b = x + mu g)",
                                       "ms": round(ph["k2_step"], 4), "bytes": b2,
                                       "gbs": round(b2 / (ph["k2_step"] * 1e6), 1)},
                "k3_tv_prox": {"kernel": "fgp2_rows_kernel (row walk, one grid barrier per FGP iteration)",
