@@ -150,7 +150,8 @@ int bsgd_plan_gather_tiles(bsgd_plan *plan, int transposed, int64_t ntiles, cons
  * creation when its rows are long, and so is A^T's, in A^T's own column order, when
  * A has >= 384 nonzeros per column).  grid_h x grid_w = rows of A is the grid the
  * gathered vector r lives on (row-major; a sinogram's angles x bins): the stream is
- * then gathered in 4 x 4 grid tiles (one 128-byte line each) from r permuted into
+ * then gathered in 16-element grid tiles (one 128-byte line each; 4 x 4, 8 x 2 or 2 x 8,
+ * chosen from the footprint of 16 consecutive entries on the grid) from r permuted into
  * that order before each launch, with 16-bit offset indices when they fit.  0, 0 =
  * no grid (A^T's own column order); a negative size removes the copy.  Between the
  * blocked copy and gather tiles of A^T the latest explicit request wins (requesting

@@ -316,7 +316,7 @@ class BlockOperator:
             self.set_stacked_tiles(True, grid_tiles(n, n))
             self.set_stacked_tiles(False, grid_tiles(a1 - a0, num_bins))
         elif depth == 1 and tiles:
-            # Blocked stream for A^T gathered in 4 x 4 sinogram tiles (angles x bins): a
+            # Blocked stream for A^T gathered in sinogram tiles (8 angles x 2 bins): a
             # pixel's bins over consecutive angles and the neighbouring pixels of a warp
             # share 128-byte lines of the permuted r (configs[3] K2: CSR 6.1 ms, gather
             # tiles over 4 x 4 pixel tiles 2.9 ms, blocked 2.6 ms -- same bits as the
@@ -352,7 +352,7 @@ class BlockOperator:
         """Blocked stream for A^T (`bsgd_plan_blocked_transposed`).
 
         ``grid`` = (h, w) with h * w = rows of A: the grid r lives on (a sinogram's
-        angles x bins); A^T's gathers then run in 4 x 4 grid tiles.  ``()`` builds
+        angles x bins); A^T's gathers then run in 16-element grid tiles (shape picked by the plan).  ``()`` builds
         the copy in A^T's own column order; None removes it.  Replaces gather
         tiles of A^T (and `set_gather_tiles(True, ...)` afterwards replaces it).  Values agree with the CSR kernel to rounding.
         """

@@ -149,7 +149,7 @@ class CudaShard:
         with an angle range), so no host CSR exists at any size (configs[3]: 1.9e9
         nonzeros over the ranks).  The rank's rows must be whole angles (configs[3]:
         each of the 8 row blocks is 180 angles x 1449 bins).  The shard's A^T is
-        a blocked stream gathered in 4 x 4 sinogram tiles like the single-GPU operator's."""
+        a blocked stream gathered in sinogram tiles like the single-GPU operator's."""
         from .blockops import BlockPartition, grid_tiles
         r0, r1 = spec.row_range
         if r0 % num_bins or r1 % num_bins:
