@@ -147,8 +147,9 @@ int bsgd_plan_stacked_tiles(bsgd_plan *plan, int transposed, int64_t ntiles, con
 int bsgd_plan_gather_tiles(bsgd_plan *plan, int transposed, int64_t ntiles, const int64_t *tile_ptr,
                            const int64_t *tile_rows, void *stream);
 /* Blocked stream for A^T (the copy csr_blocked_kernel runs; A's own is built at plan
- * creation when its rows are long, and so is A^T's, in A^T's own column order, when
- * A has >= 384 nonzeros per column).  grid_h x grid_w = rows of A is the grid the
+ * creation when its rows are long, and so is A^T's when A has >= 384 nonzeros per
+ * column: on the row grid the plan infers from A^T's index gaps, else in A^T's own
+ * column order).  grid_h x grid_w = rows of A is the grid the
  * gathered vector r lives on (row-major; a sinogram's angles x bins): the stream is
  * then gathered in 16-element grid tiles (one 128-byte line each; 4 x 4, 8 x 2 or 2 x 8,
  * chosen from the footprint of 16 consecutive entries on the grid) from r permuted into

@@ -558,6 +558,51 @@ static int build_blocked_dir(bsgd_plan *p, bool tr, int gh, int gw, cudaStream_t
     return BSGD_OK;
 }
 
+// Grid of A's row space, inferred from A^T alone (a plain CSR carries no geometry): the
+// gaps between consecutive entries of A^T's rows peak at the grid width w (a pixel meets
+// adjacent bins of one angle, then the next angle ~w rays further), and w divides the
+// number of rows.  Only the ORDER of the gathers depends on the answer -- the stream's
+// entries keep their positions and the sums their bits -- so a wrong guess can cost time,
+// never correctness.  Returns false when no width within 4 of the peak divides the rows
+// or the peak holds less than 80% of the gaps.  BSGD_NO_GRID_INFER=1 disables it.
+static bool infer_row_grid(const bsgd_plan *p, cudaStream_t st, int *gh, int *gw) {
+    if (getenv("BSGD_NO_GRID_INFER") || p->cols < 1 || p->rows < 64) return false;
+    const int nbins = (int)std::min<int64_t>(p->rows, 1 << 20);
+    unsigned int *d_hist = nullptr;
+    if (cudaMalloc(&d_hist, sizeof(unsigned int) * nbins) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    std::vector<unsigned int> hist(nbins);
+    const int64_t stride = std::max<int64_t>(1, p->cols / 16384);   // ~16K sampled rows of A^T
+    cudaMemsetAsync(d_hist, 0, sizeof(unsigned int) * nbins, st);
+    blk_gap_hist_kernel<<<grid_1d(cdiv(p->cols, stride), kThreads / 32), kThreads, 0, st>>>(p->cols, stride, p->t_ptr,
+                                                                                          p->t_idx, nbins, d_hist);
+    cudaMemcpyAsync(hist.data(), d_hist, sizeof(unsigned int) * nbins, cudaMemcpyDeviceToHost, st);
+    const cudaError_t e = cudaStreamSynchronize(st);
+    cudaFree(d_hist);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    int64_t total = 0, peak = 0;
+    for (int d = 2; d < nbins; ++d) {
+        total += hist[d];
+        if (hist[d] > hist[peak]) peak = d;
+    }
+    if (peak < 8 || total == 0) return false;
+    int64_t best = 0;
+    for (int64_t c = std::max<int64_t>(8, peak - 4); c <= std::min<int64_t>(nbins - 1, peak + 4); ++c)
+        if (p->rows % c == 0 && (best == 0 || std::llabs(c - peak) < std::llabs(best - peak))) best = c;
+    if (best == 0 || p->rows / best > INT32_MAX) return false;
+    int64_t near = 0;
+    for (int64_t d = std::max<int64_t>(2, best - 4); d <= std::min<int64_t>(nbins - 1, best + 4); ++d) near += hist[d];
+    if (5 * near < 4 * total) return false;
+    *gw = (int)best;
+    *gh = (int)(p->rows / best);
+    return true;
+}
+
 // The forward copy is built at plan creation for plans whose rows are long (>= 384
 // nonzeros on average: CT rays; padding to whole blocks then costs a few percent more
 // stream bytes); a square column space is taken for an image (n x n, gathered in tile
@@ -1685,12 +1730,14 @@ static int plan_finish(bsgd_plan *p, cudaStream_t st) {
     rc = (value_dtype == BSGD_F32) ? tune_blocked<float>(p, p->fb) : tune_blocked<double>(p, p->fb);
     if (rc != BSGD_OK) return rc;
     // A^T's rows long too (a CT system handed over as a plain CSR: ~1.3 nonzeros per
-    // angle and pixel): a blocked copy of A^T in its own column order, which
-    // bsgd_plan_blocked_transposed replaces by the tile-ordered one when the caller
-    // names the grid of A's rows
+    // angle and pixel): a blocked copy of A^T, gathered in tiles of the row grid when
+    // infer_row_grid finds one (a sinogram), else in A^T's own column order;
+    // bsgd_plan_blocked_transposed replaces it when the caller names the grid
     if (!p->stacked() && cols > 0 && (double)p->nnz / (double)cols >= 384.0 && !getenv("BSGD_NO_BLOCKED")) {
-        rc = (value_dtype == BSGD_F32) ? build_blocked_dir<float>(p, true, 0, 0, st)
-                                       : build_blocked_dir<double>(p, true, 0, 0, st);
+        int gh = 0, gw = 0;
+        if (!infer_row_grid(p, st, &gh, &gw)) gh = gw = 0;
+        rc = (value_dtype == BSGD_F32) ? build_blocked_dir<float>(p, true, gh, gw, st)
+                                       : build_blocked_dir<double>(p, true, gh, gw, st);
         if (rc != BSGD_OK) return rc;
         rc = (value_dtype == BSGD_F32) ? tune_blocked<float>(p, p->tb) : tune_blocked<double>(p, p->tb);
         if (rc != BSGD_OK) return rc;

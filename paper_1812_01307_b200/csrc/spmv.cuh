@@ -460,6 +460,24 @@ __global__ void blk_span_kernel(int64_t nrows, const int64_t *ptr, const int32_t
     }
 }
 
+// Histogram of the gaps between consecutive column indices (1 < gap < nbins) over every
+// `stride`-th row: a matrix whose gathered vector lives on a row-major grid of width w
+// (A^T of a CT system: bins of one angle adjacent, the next angle ~w further) shows a
+// sharp peak at ~w.  One warp per sampled row.
+__global__ void blk_gap_hist_kernel(int64_t nrows, int64_t stride, const int64_t *ptr, const int32_t *idx,
+                                    int nbins, unsigned int *hist) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t r = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * stride; r < nrows;
+         r += nw * stride) {
+        const int64_t beg = ptr[r], end = ptr[r + 1];
+        for (int64_t k = beg + lane; k + 1 < end; k += 32) {
+            const int64_t d = (int64_t)idx[k + 1] - idx[k];
+            if (d > 1 && d < nbins) atomicAdd(hist + d, 1u);
+        }
+    }
+}
+
 // padded row lengths (whole blocks of blk entries) for the blocked copy
 __global__ void blk_len_kernel(int64_t rows, const int64_t *ptr, int blk, int64_t *out) {
     for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x)

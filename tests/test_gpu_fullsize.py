@@ -96,13 +96,13 @@ def test_ct_full_size_stated_epochs(cuda_ok, index, epochs, monitor):
     assert tr.objectives()[-1] < tr.objectives()[0]
     if index == 2:
         # the reference's own call -- BlockOperator(A_csr, partition) on the plain host CSR, no
-        # grid hints: K1 finds the square image by itself, A^T gets a blocked stream in its own
-        # column order; the same run against the same oracle trace
+        # grid hints: K1 finds the square image by itself and the plan infers the sinogram grid
+        # of A^T's gathers from the matrix; the same run against the same oracle trace
         from paper_1812_01307_b200 import blockops
         op2 = blockops.BlockOperator(csr, blockops.make_partition(*csr.shape, 8, 8))
         ki = op2.kernel_info()
         assert ki["forward"] == "blocked_compressed" and ki["forward_order"] == "tile4"
-        assert ki["transposed"] == "blocked_compressed" and ki["transposed_order"] == "native"
+        assert ki["transposed"] == "blocked_compressed" and ki["transposed_order"] == "tile8x2"
         tr2 = solvers.run_solver("bsgd", solvers.Problem(op2, d.y, d.x_true, lay), cfg, sample_every=10)
         _compare(tr2, ref)
         assert list(tr2.decrease_flags) == list(ref.decrease_flags)

@@ -478,22 +478,29 @@ def test_transposed_blocked_stream(B, monkeypatch, grid, dtype):
         stacked.set_transposed_blocked((6, 11))
 
 
-def test_plain_csr_ct_system_gets_blocked_streams(B):
+@pytest.mark.parametrize("infer", [True, False])
+def test_plain_csr_ct_system_gets_blocked_streams(B, monkeypatch, infer):
     """A CT system handed over as a plain scipy CSR (the reference's own call,
     blockops.py:123-152; no grid hints): rays and pixel rows are both long, so the plan
     builds the blocked stream of A (square image: tile order) and, on its own, a blocked
-    stream of A^T in A^T's column order; products, residual and two TV epochs against
-    the oracle; naming the sinogram grid afterwards switches A^T to the tile order
-    with the same rounding-level agreement."""
+    stream of A^T -- gathered in tiles of the sinogram grid it infers from the gaps
+    between A^T's consecutive entries (angles x bins = 400 x 363 here), or, with the
+    inference off, in A^T's own column order; products, residual and two TV epochs
+    against the oracle; naming the grid afterwards gives the tile order either way."""
     blockops, tv = B[0], B[1]
     from paper_1812_01307_b200 import problems, solvers
     n, ang, nb = 256, 400, 363                 # ~510 nonzeros per pixel row, ~230 per ray
     a = problems.parallel_beam_matrix(n, ang, nb, dtype=np.float32)
     assert a.nnz / a.shape[1] >= 384
+    if not infer:
+        monkeypatch.setenv("BSGD_NO_GRID_INFER", "1")
     op = blockops.BlockOperator(a, blockops.make_partition(*a.shape, 4, 4))
     ki = op.kernel_info()
-    assert ki["transposed"] == "blocked_compressed" and ki["transposed_lanes"] == 8
-    assert ki["transposed_order"] == "native"
+    assert ki["transposed"] == "blocked_compressed"
+    if infer:
+        assert ki["transposed_lanes"] == 16 and ki["transposed_order"].startswith("tile")
+    else:
+        assert ki["transposed_lanes"] == 8 and ki["transposed_order"] == "native"
     oop = orc.OracleOperator(a, 4, 4)
     rng = np.random.default_rng(17)
     x, w = rng.standard_normal(a.shape[1]), rng.standard_normal(a.shape[0])
