@@ -558,26 +558,31 @@ static int build_blocked_dir(bsgd_plan *p, bool tr, int gh, int gw, cudaStream_t
     return BSGD_OK;
 }
 
-// Grid of A's row space, inferred from A^T alone (a plain CSR carries no geometry): the
-// gaps between consecutive entries of A^T's rows peak at the grid width w (a pixel meets
-// adjacent bins of one angle, then the next angle ~w rays further), and w divides the
-// number of rows.  Only the ORDER of the gathers depends on the answer -- the stream's
+// Grid of a gathered vector, inferred from the matrix alone (a plain CSR carries no
+// geometry): the gaps between consecutive entries of a row peak at the grid width w (a
+// pixel meets adjacent bins of one angle, then the next angle ~w rays further; a ray meets
+// adjacent pixels of one image row, then the next row ~w pixels further), and w divides
+// the vector's length.  Only the ORDER of the gathers depends on the answer -- the stream's
 // entries keep their positions and the sums their bits -- so a wrong guess can cost time,
 // never correctness.  Returns false when no width within 4 of the peak divides the rows
 // or the peak holds less than 80% of the gaps.  BSGD_NO_GRID_INFER=1 disables it.
-static bool infer_row_grid(const bsgd_plan *p, cudaStream_t st, int *gh, int *gw) {
-    if (getenv("BSGD_NO_GRID_INFER") || p->cols < 1 || p->rows < 64) return false;
-    const int nbins = (int)std::min<int64_t>(p->rows, 1 << 20);
+static bool infer_grid(const bsgd_plan *p, bool tr, cudaStream_t st, int *gh, int *gw) {
+    // tr: A^T's rows gather from A's row space; else A's rows gather from its column space
+    const int64_t srows = tr ? p->cols : p->rows, veclen = tr ? p->rows : p->cols;
+    const int64_t *sptr = tr ? p->t_ptr : p->f_ptr;
+    const int32_t *sidx = tr ? p->t_idx : p->f_idx;
+    if (getenv("BSGD_NO_GRID_INFER") || srows < 1 || veclen < 64) return false;
+    const int nbins = (int)std::min<int64_t>(veclen, 1 << 20);
     unsigned int *d_hist = nullptr;
     if (cudaMalloc(&d_hist, sizeof(unsigned int) * nbins) != cudaSuccess) {
         cudaGetLastError();
         return false;
     }
     std::vector<unsigned int> hist(nbins);
-    const int64_t stride = std::max<int64_t>(1, p->cols / 16384);   // ~16K sampled rows of A^T
+    const int64_t stride = std::max<int64_t>(1, srows / 16384);   // ~16K sampled rows
     cudaMemsetAsync(d_hist, 0, sizeof(unsigned int) * nbins, st);
-    blk_gap_hist_kernel<<<grid_1d(cdiv(p->cols, stride), kThreads / 32), kThreads, 0, st>>>(p->cols, stride, p->t_ptr,
-                                                                                          p->t_idx, nbins, d_hist);
+    blk_gap_hist_kernel<<<grid_1d(cdiv(srows, stride), kThreads / 32), kThreads, 0, st>>>(srows, stride, sptr, sidx,
+                                                                                        nbins, d_hist);
     cudaMemcpyAsync(hist.data(), d_hist, sizeof(unsigned int) * nbins, cudaMemcpyDeviceToHost, st);
     const cudaError_t e = cudaStreamSynchronize(st);
     cudaFree(d_hist);
@@ -593,13 +598,13 @@ static bool infer_row_grid(const bsgd_plan *p, cudaStream_t st, int *gh, int *gw
     if (peak < 8 || total == 0) return false;
     int64_t best = 0;
     for (int64_t c = std::max<int64_t>(8, peak - 4); c <= std::min<int64_t>(nbins - 1, peak + 4); ++c)
-        if (p->rows % c == 0 && (best == 0 || std::llabs(c - peak) < std::llabs(best - peak))) best = c;
-    if (best == 0 || p->rows / best > INT32_MAX) return false;
+        if (veclen % c == 0 && (best == 0 || std::llabs(c - peak) < std::llabs(best - peak))) best = c;
+    if (best == 0 || veclen / best > INT32_MAX) return false;
     int64_t near = 0;
     for (int64_t d = std::max<int64_t>(2, best - 4); d <= std::min<int64_t>(nbins - 1, best + 4); ++d) near += hist[d];
     if (5 * near < 4 * total) return false;
     *gw = (int)best;
-    *gh = (int)(p->rows / best);
+    *gh = (int)(veclen / best);
     return true;
 }
 
@@ -616,7 +621,9 @@ static int build_blocked(bsgd_plan *p, cudaStream_t st) {
         return BSGD_OK;
     int img = (int)llround(sqrt((double)p->cols));
     if ((int64_t)img * img != p->cols || img % 4 != 0) img = 0;
-    return build_blocked_dir<V>(p, false, img, img, st);
+    int gh = img, gw = img;
+    if (!img && !infer_grid(p, false, st, &gh, &gw)) gh = gw = 0;   // a non-square image: width from the rays' index gaps
+    return build_blocked_dir<V>(p, false, gh, gw, st);
 }
 
 // ---------------------------------------------------------------------------
@@ -1731,11 +1738,11 @@ static int plan_finish(bsgd_plan *p, cudaStream_t st) {
     if (rc != BSGD_OK) return rc;
     // A^T's rows long too (a CT system handed over as a plain CSR: ~1.3 nonzeros per
     // angle and pixel): a blocked copy of A^T, gathered in tiles of the row grid when
-    // infer_row_grid finds one (a sinogram), else in A^T's own column order;
+    // infer_grid finds one (a sinogram), else in A^T's own column order;
     // bsgd_plan_blocked_transposed replaces it when the caller names the grid
     if (!p->stacked() && cols > 0 && (double)p->nnz / (double)cols >= 384.0 && !getenv("BSGD_NO_BLOCKED")) {
         int gh = 0, gw = 0;
-        if (!infer_row_grid(p, st, &gh, &gw)) gh = gw = 0;
+        if (!infer_grid(p, true, st, &gh, &gw)) gh = gw = 0;
         rc = (value_dtype == BSGD_F32) ? build_blocked_dir<float>(p, true, gh, gw, st)
                                        : build_blocked_dir<double>(p, true, gh, gw, st);
         if (rc != BSGD_OK) return rc;

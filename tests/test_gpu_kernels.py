@@ -526,6 +526,34 @@ def test_plain_csr_ct_system_gets_blocked_streams(B, monkeypatch, infer):
     assert rel(op.rmatvec(w, charge=False), oop.rmatvec(w)) < 1e-12
 
 
+def test_forward_grid_inferred_for_non_square_image(B, monkeypatch):
+    """A 128 x 256 image (not a square column space): the plan reads the image width off
+    the rays' index gaps and gathers K1 in tile order; the products equal those of the
+    plan without the inference (A's own column order) bit for bit -- only the order of
+    the gathers differs -- and the oracle to rounding."""
+    blockops = B[0]
+    from paper_1812_01307_b200 import problems
+    full = problems.parallel_beam_matrix(256, 60, 363, dtype=np.float32)
+    a = sparse.csr_array(full[:, : 128 * 256])
+    a.sort_indices()
+    part = blockops.make_partition(*a.shape, 3, 2)
+    monkeypatch.setenv("BSGD_BLOCKED", "force")
+    monkeypatch.setenv("BSGD_BLK_G", "16")
+    tiled = blockops.BlockOperator(a, part)
+    monkeypatch.setenv("BSGD_NO_GRID_INFER", "1")
+    native = blockops.BlockOperator(a, part)
+    kt, kn = tiled.kernel_info(), native.kernel_info()
+    assert kt["forward_order"].startswith("tile") and kn["forward_order"] == "native"
+    assert kt["forward"] == kn["forward"] and kt["forward_lanes"] == kn["forward_lanes"] == 16
+    oop = orc.OracleOperator(a, 3, 2)
+    rng = np.random.default_rng(31)
+    for _ in range(2):
+        x = rng.standard_normal(a.shape[1])
+        got = tiled.matvec(x, charge=False)
+        assert np.array_equal(got, native.matvec(x, charge=False))
+        assert rel(got, oop.matvec(x)) < 1e-12
+
+
 @pytest.mark.parametrize("index", [2, 3])
 def test_ct_full_size_products_consistent(B, index):
     """configs[2] / configs[3] at full size (2.4e8 / 1.9e9 nonzeros, projector built on
